@@ -1,0 +1,235 @@
+/* sgtr.h — C-ABI of the B200-native 3DGS²-TR training iteration.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * `splat::step_3dgs2tr` (/root/reference/proj/src/optimizer.cpp:189-220) and
+ * the seams its tests and checks call.  Every entry point names the
+ * reference interface it replaces.  Plain pointers and sizes only; host
+ * memory is caller-owned and copied, device memory is owned by the context.
+ *
+ * Layouts are the reference's:
+ *   scene x  : double[14*K] group-major [mu 3K | s 3K | q 4K | alpha K | c 3K]
+ *              (scene.hpp:37-52)
+ *   images   : double[H*W*3] row-major, channel-interleaved (image.hpp:10-27)
+ *   residual : double[6*H*W], L1 block then D-SSIM block, index c*H*W+y*W+x
+ *              (residuals.hpp:17-22)
+ *
+ * Status codes mirror the reference's exception classes:
+ *   SGTR_OK, SGTR_INVALID_ARGUMENT (std::invalid_argument, CLI exit 1),
+ *   SGTR_NUMERIC (splat::NumericError, errors.hpp:11-14, CLI exit 2),
+ *   SGTR_RUNTIME (CUDA/NCCL failure).  sgtr_last_error() returns the message
+ *   (same wording and locator as the reference's exception text).
+ *
+ * One host thread per context (not re-entrant), like the reference's single
+ * control thread.
+ */
+#ifndef SGTR_H
+#define SGTR_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SGTR_OK = 0, SGTR_INVALID_ARGUMENT = 1, SGTR_NUMERIC = 2, SGTR_RUNTIME = 3 };
+
+typedef struct sgtr_ctx sgtr_ctx;
+
+/* splat::Camera (scene.hpp:70-81) minus the GT image */
+typedef struct sgtr_camera {
+    int32_t id, width, height, pad;
+    double fx, fy, cx, cy;
+    double q_wc[4]; /* unit (x, y, z, w), x_cam = R(q_wc) x_world + t_wc */
+    double t_wc[3];
+} sgtr_camera;
+
+/* splat::RenderOptions (render.hpp:12-22); `workers` has no GPU meaning */
+typedef struct sgtr_render_options {
+    double z_near, lowpass, alpha_clamp, alpha_skip, t_stop, cutoff_sigma;
+    double background[3];
+} sgtr_render_options;
+
+/* splat::ResidualOptions (residuals.hpp:13-16) */
+typedef struct sgtr_residual_options {
+    double lambda, floor;
+} sgtr_residual_options;
+
+/* splat::OptimizerOptions (optimizer.hpp:37-53) for the 3DGS²-TR kind, with
+ * TrustRegionSchedule, RadiusCaps (trust_region.hpp:66-89) and ParamBounds
+ * (scene.hpp:29-35) flattened */
+typedef struct sgtr_optimizer_options {
+    double theta1, theta2;
+    int32_t hess_interval, hutch_samples, batch_size, hutch_batch_size;
+    double gamma_d;
+    double eps_start, eps_end;
+    int32_t total_steps, record_applied_step;
+    double cap_mean, cap_scale, cap_rotation, cap_opacity, cap_color;
+    double s_min, alpha_min, alpha_max, c_min, c_max;
+    sgtr_residual_options residual;
+    sgtr_render_options render;
+} sgtr_optimizer_options;
+
+/* splat::StepDiagnostics (optimizer.hpp:74-83); applied_step is fetched with
+ * sgtr_get_applied_step when record_applied_step was set */
+typedef struct sgtr_step_diagnostics {
+    double batch_loss, gnorm, step_pre, step_post, clip_frac, eps,
+        max_step_over_radius;
+    int32_t refreshed, n_local_views;
+} sgtr_step_diagnostics;
+
+/* ------------------------------------------------------------ context */
+const char* sgtr_last_error(void);
+int sgtr_create(int device, sgtr_ctx** out);
+int sgtr_destroy(sgtr_ctx* ctx);
+/* cudaStream_t the context launches on (for event timing by the caller) */
+int sgtr_get_stream(sgtr_ctx* ctx, void** stream);
+int sgtr_synchronize(sgtr_ctx* ctx);
+/* number of kernels this context has launched so far */
+int64_t sgtr_launch_count(const sgtr_ctx* ctx);
+
+/* ------------------------------------------------------------ scene */
+/* Scene::unpack / pack (scene.cpp:13-39) */
+int sgtr_set_scene(sgtr_ctx* ctx, const double* x, int64_t n_splats);
+int sgtr_get_scene(sgtr_ctx* ctx, double* x);
+int64_t sgtr_scene_size(const sgtr_ctx* ctx);
+
+/* ------------------------------------------------------------ views */
+/* the training views passed to step_3dgs2tr (optimizer.hpp:129-131);
+ * gts[i] is the Camera::gt image (H*W*3 doubles), or gts == NULL to keep
+ * the views without targets (render-only use).  All views share one size,
+ * as the reference's m = 6*P*M assumes (optimizer.cpp:44). */
+int sgtr_set_views(sgtr_ctx* ctx, const sgtr_camera* cams, int32_t n,
+                   const double* const* gts);
+/* replaces view i's target by the quantize8 of the current scene's render
+ * (dataset.cpp:63, with the render on the GPU) */
+int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro,
+                        int32_t quantize);
+int sgtr_get_target(sgtr_ctx* ctx, int32_t view, double* gt);
+
+/* ------------------------------------------------------------ optimizer state */
+/* OptimizerState(dim, seed) (optimizer.hpp:58-72): g_hat = d_hat = 0, t = 0,
+ * Rng(seed) */
+int sgtr_state_reset(sgtr_ctx* ctx, uint64_t seed);
+int sgtr_state_set(sgtr_ctx* ctx, const double* g_hat, const double* d_hat,
+                   int64_t t);
+int sgtr_state_get(sgtr_ctx* ctx, double* g_hat, double* d_hat, int64_t* t);
+/* n raw mt19937_64 outputs from the state's Rng (rng.hpp:24) */
+int sgtr_rng_raw(sgtr_ctx* ctx, int64_t n, uint64_t* out);
+
+/* a standalone reference Rng (rng.hpp:15-72: std::mt19937_64); the variate
+ * mappings (uniform, normal, rademacher, below) are applied by the caller */
+typedef struct sgtr_rng sgtr_rng;
+int sgtr_rng_new(uint64_t seed, sgtr_rng** out);
+int sgtr_rng_draw(sgtr_rng* rng, int64_t n, uint64_t* out);
+int sgtr_rng_free(sgtr_rng* rng);
+
+/* ------------------------------------------------------------ Algorithm 1 */
+/* step_3dgs2tr (optimizer.cpp:189-220): S1, S2 and probes drawn from the
+ * state's Rng in the reference order */
+int sgtr_step_3dgs2tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                      sgtr_step_diagnostics* diag);
+/* teacher-forced variant: the step's draws supplied explicitly; probe_bits
+ * holds nu probes of ceil(14K/32) words each, bit k of probe s set <=> z_k =
+ * +1 (rng.hpp:46); s2/probe_bits are read on refresh steps only */
+int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                               const int32_t* s1, int32_t n1, const int32_t* s2,
+                               int32_t n2, const uint32_t* probe_bits,
+                               int32_t nu, sgtr_step_diagnostics* diag);
+int sgtr_get_applied_step(sgtr_ctx* ctx, double* out);
+
+/* ------------------------------------------------------------ seams */
+/* rasterize (render.hpp:73-74) */
+int sgtr_rasterize(sgtr_ctx* ctx, const sgtr_camera* cam,
+                   const sgtr_render_options* ro, double* color,
+                   double* t_final);
+/* rasterize_jvp (render.hpp:78-79); v has 14K entries */
+int sgtr_rasterize_jvp(sgtr_ctx* ctx, const sgtr_camera* cam,
+                       const sgtr_render_options* ro, const double* v,
+                       double* tangent);
+/* rasterize_vjp (render.hpp:83-84); grad has 14K entries */
+int sgtr_rasterize_vjp(sgtr_ctx* ctx, const sgtr_camera* cam,
+                       const sgtr_render_options* ro, const double* adjoint,
+                       double* grad);
+/* ssim_map / ssim_jvp / ssim_vjp (ssim.hpp:11-20) */
+int sgtr_ssim_map(sgtr_ctx* ctx, const double* a, const double* b, int32_t w,
+                  int32_t h, double* out);
+int sgtr_ssim_jvp(sgtr_ctx* ctx, const double* a, const double* da,
+                  const double* b, int32_t w, int32_t h, double* s,
+                  double* ds);
+int sgtr_ssim_vjp(sgtr_ctx* ctx, const double* a, const double* b,
+                  const double* upstream, int32_t w, int32_t h, double* grad);
+/* residual_vector / residual_jvp / residual_vjp (residuals.hpp:23-33) */
+int sgtr_residual_vector(sgtr_ctx* ctx, const double* rendered,
+                         const double* gt, int32_t w, int32_t h,
+                         const sgtr_residual_options* o, double* r);
+int sgtr_residual_jvp(sgtr_ctx* ctx, const double* rendered,
+                      const double* tangent, const double* gt, int32_t w,
+                      int32_t h, const sgtr_residual_options* o, double* dr);
+int sgtr_residual_vjp(sgtr_ctx* ctx, const double* rendered, const double* gt,
+                      int32_t w, int32_t h, const double* u,
+                      const sgtr_residual_options* o, double* adj);
+/* view_jacobian_apply / applyT (optimizer.hpp:87-94) on context view i */
+int sgtr_view_jacobian_apply(sgtr_ctx* ctx, int32_t view, const double* v,
+                             const sgtr_residual_options* rs,
+                             const sgtr_render_options* ro, double* out);
+int sgtr_view_jacobian_applyT(sgtr_ctx* ctx, int32_t view, const double* u,
+                              const sgtr_residual_options* rs,
+                              const sgtr_render_options* ro, double* grad);
+/* stochastic_gradient (optimizer.hpp:99-104) over context views */
+int sgtr_stochastic_gradient(sgtr_ctx* ctx, const int32_t* batch, int32_t n,
+                             const sgtr_residual_options* rs,
+                             const sgtr_render_options* ro, double* g,
+                             double* batch_loss);
+/* hutchinson_diag (optimizer.hpp:106-117); probes are nu dense vectors of
+ * 14K entries, each entry +1 or -1 */
+int sgtr_hutchinson_diag(sgtr_ctx* ctx, const int32_t* batch, int32_t n,
+                         int32_t nu, const double* probes,
+                         const sgtr_residual_options* rs,
+                         const sgtr_render_options* ro, double* d);
+/* shd_radii (trust_region.hpp:81-83) */
+int sgtr_shd_radii(sgtr_ctx* ctx, double eps, const double caps[5],
+                   double* eta);
+/* eps_at (trust_region.hpp:87-89) */
+int sgtr_eps_at(double eps_start, double eps_end, int32_t total, int32_t t,
+                double* out);
+
+/* ------------------------------------------------------------ parity dumps */
+/* projected fragment fields per splat, 12 doubles each:
+ * culled, depth, px, py, bx0, bx1, by0, by1, i00, i01, i11, 0
+ * (render.cpp:51-69) */
+int sgtr_project(sgtr_ctx* ctx, const sgtr_camera* cam,
+                 const sgtr_render_options* ro, double* out);
+/* GPU tile binning of one view (16x16 tiles): depth order of visible
+ * splats, per-tile [start, end) and per-tile splat lists.  Call with
+ * lists == NULL first to get the sizes. */
+int sgtr_dump_binning(sgtr_ctx* ctx, const sgtr_camera* cam,
+                      const sgtr_render_options* ro, int32_t* n_visible,
+                      int32_t* order, int64_t* n_dup, int64_t* tile_start,
+                      int64_t* tile_end, int32_t* lists);
+
+/* ------------------------------------------------------------ data */
+/* make_synthetic (dataset.cpp:25-67) with two declared extensions for the
+ * large configurations: width != height (fx = fy = focal_factor*height),
+ * and splat-size scaling (scale range, init_scale and sigma_init multiplied
+ * by size_scale).  With size_scale = 1 and width = height the scenes and
+ * cameras equal the reference's.  Writes gt_x[14*gt_splats],
+ * init_x[14*init_splats] and cams[views]. */
+typedef struct sgtr_synth_config {
+    int32_t gt_splats, init_splats, views, width, height, pad;
+    uint64_t seed;
+    double sigma_init, init_scale, init_opacity, camera_radius, camera_height,
+        focal_factor, size_scale;
+} sgtr_synth_config;
+int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x,
+                        double* init_x, sgtr_camera* cams);
+
+/* ------------------------------------------------------------ multi-GPU */
+/* one process per GPU; views of each step are split round-robin over
+ * ranks and g | z.w | loss are summed with one ncclAllReduce per step */
+int sgtr_nccl_unique_id(uint8_t out[128]);
+int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks,
+                   int32_t rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1416 @@
+// api.cu — context, host orchestration of Algorithm 1, and the C-ABI.
+//
+// The host side mirrors the reference's control flow (optimizer.cpp:36-220)
+// and its RNG consumption order exactly; all arithmetic over splats, pixels
+// and parameters runs in the kernels of project.cu, binning.cu, raster.cu,
+// ssim.cu and update.cu.  There is no CPU fallback: without a CUDA device
+// every entry point fails with SGTR_RUNTIME.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "launch.h"
+
+namespace sgtr {
+namespace {
+
+thread_local std::string g_last_error;
+
+Error invalid(const std::string& m) { return Error(SGTR_INVALID_ARGUMENT, m); }
+Error numeric(const std::string& m) { return Error(SGTR_NUMERIC, m); }
+
+const char* const kGroupNames[5] = {"position", "scale", "rotation", "opacity", "color"};
+int group_of(long long K, long long k) {  // scene.cpp:41-47
+    if (k < 3 * K) return 0;
+    if (k < 6 * K) return 1;
+    if (k < 10 * K) return 2;
+    if (k < 11 * K) return 3;
+    return 4;
+}
+
+// ------------------------------------------------------------------ buffers
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    Buf() = default;
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+    ~Buf() {
+        if (p) cudaFree(p);
+    }
+    void* ensure(size_t need) {
+        if (need <= bytes && p) return p;
+        if (p) SGTR_CUDA(cudaFree(p));
+        p = nullptr;
+        size_t nb = std::max(need, bytes + bytes / 4);
+        nb = std::max<size_t>(nb, 256);
+        SGTR_CUDA(cudaMalloc(&p, nb));
+        bytes = nb;
+        return p;
+    }
+    template <typename T>
+    T* as(size_t n) {
+        return static_cast<T*>(ensure(n * sizeof(T)));
+    }
+    template <typename T>
+    T* get() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// device status block (pinned host mirror in Ctx::hstat)
+struct DevStatus {
+    ViewStatus vs;
+    int bad_index;
+    int degenerate;
+    double tr[5];
+    double scalar;
+};
+
+// RNG with the reference's variate mappings (rng.hpp:15-72)
+struct Rng {
+    std::mt19937_64 gen;
+    bool have_spare = false;
+    double spare = 0.0;
+    explicit Rng(uint64_t s = 1) : gen(s) {}
+    double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    double log_uniform(double lo, double hi) {
+        return std::exp(uniform(std::log(lo), std::log(hi)));
+    }
+    double normal() {
+        if (have_spare) {
+            have_spare = false;
+            return spare;
+        }
+        double u1 = uniform();
+        while (u1 <= 0.0) u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        spare = r * std::sin(2.0 * M_PI * u2);
+        have_spare = true;
+        return r * std::cos(2.0 * M_PI * u2);
+    }
+    std::vector<int> sample(int n, int k) {
+        std::vector<int> idx(n);
+        for (int i = 0; i < n; ++i) idx[i] = i;
+        const int m = std::min(k, n);
+        for (int i = 0; i < m; ++i) {
+            const int j = i + static_cast<int>(gen() % static_cast<uint64_t>(n - i));
+            std::swap(idx[i], idx[j]);
+        }
+        idx.resize(m);
+        return idx;
+    }
+};
+
+struct View {
+    sgtr_camera cam;
+    DevCam dc;
+};
+
+DevCam make_devcam(const sgtr_camera& c) {
+    DevCam d;
+    d.W = c.width;
+    d.H = c.height;
+    d.fx = c.fx;
+    d.fy = c.fy;
+    d.cx = c.cx;
+    d.cy = c.cy;
+    if (!quat_rot(c.q_wc, d.w)) throw invalid("quat_to_rotation: degenerate quaternion");
+    for (int i = 0; i < 3; ++i) d.t[i] = c.t_wc[i];
+    return d;
+}
+
+// NCCL, loaded on demand so single-GPU use needs no NCCL at all
+struct Nccl {
+    void* lib = nullptr;
+    int (*get_unique_id)(void*) = nullptr;
+    int (*comm_init_rank)(void**, int, const char*, int) = nullptr;
+    int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    const char* (*get_error)(int) = nullptr;
+    void load() {
+        if (lib) return;
+        lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) throw Error(SGTR_RUNTIME, std::string("dlopen libnccl.so.2: ") + dlerror());
+        get_unique_id = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
+        all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+            lib, "ncclAllReduce");
+        get_error = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+        if (!get_unique_id || !all_reduce)
+            throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks the required symbols");
+    }
+    void check(int rc, const char* what) {
+        if (rc != 0)
+            throw Error(SGTR_RUNTIME,
+                        std::string(what) + ": " + (get_error ? get_error(rc) : "nccl error"));
+    }
+};
+Nccl g_nccl;
+
+// ncclCommInitRank takes ncclUniqueId (128 bytes) by value
+struct UniqueId {
+    char internal[128];
+};
+typedef int (*CommInitRankFn)(void**, int, UniqueId, int);
+
+}  // namespace
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    long long launches = 0;
+    int K = 0;
+    Buf x, x_alt, ghat, dhat, fused, applied, vecbuf;
+    bool have_applied = false;
+    std::vector<View> views;
+    Buf gt;  // planar targets, one (3, H, W) block per view
+    bool has_gt = false;
+    long long t = 0;
+    Rng rng{1};
+    // per-view workspace
+    Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
+    Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
+    Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
+    DevStatus* dstat = nullptr;
+    DevStatus* hstat = nullptr;  // pinned
+    double* htail = nullptr;     // pinned staging for the fused tail
+    size_t htail_n = 0;
+    int nranks = 1, rank = 0;
+    void* comm = nullptr;
+
+    ~Ctx() {
+        if (dstat) cudaFree(dstat);
+        if (hstat) cudaFreeHost(hstat);
+        if (htail) cudaFreeHost(htail);
+        if (st) cudaStreamDestroy(st);
+    }
+    long long dim() const { return 14LL * K; }
+    double* X() const { return x.get<double>(); }
+};
+
+namespace {
+
+struct ViewRender {
+    int W, H;
+    int n_visible;
+    long long n_dup;
+    TileLists tl;
+    int err_kind;  // 0 none, 1 non-finite parameter, 2 degenerate quaternion
+    int err_index;
+};
+
+void bind(Ctx& c) { SGTR_CUDA(cudaSetDevice(c.device)); }
+
+double* img_ptr(Ctx& c, Buf& b, int P) { return b.as<double>(3LL * P); }
+
+// K1..K7 for one camera on the context's scene
+ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_errors) {
+    ViewRender vr{};
+    vr.W = dc.W;
+    vr.H = dc.H;
+    const int K = c.K;
+    const int tiles_x = ceil_div(dc.W, kTile), tiles_y = ceil_div(dc.H, kTile);
+    const int n_tiles = tiles_x * tiles_y;
+    BinBuffers b;
+    b.keys = c.keys.as<unsigned long long>(K + 1);
+    b.keys_alt = c.keys_alt.as<unsigned long long>(K + 1);
+    b.ids = c.ids.as<int>(K + 1);
+    b.ids_alt = c.ids_alt.as<int>(K + 1);
+    b.rect = c.rect.as<int4>(K + 1);
+    b.tcount = c.tcount.as<int>(K + 1);
+    b.off_r = c.off_r.as<long long>(K + 1);
+    b.tile_start = c.tile_start.as<int>(n_tiles);
+    b.tile_end = c.tile_end.as<int>(n_tiles);
+    size_t tb = std::max(depth_sort_temp_bytes(K), scan_temp_bytes(K));
+    b.temp = c.temp.ensure(tb);
+    b.temp_bytes = c.temp.bytes;
+    double* rec = c.rec.as<double>((size_t)kRec * (K + 1));
+
+    ViewStatus init{INT_MAX, INT_MAX, 0, 0, 0};
+    c.hstat->vs = init;
+    SGTR_CUDA(cudaMemcpyAsync(&c.dstat->vs, &c.hstat->vs, sizeof(ViewStatus),
+                              cudaMemcpyHostToDevice, c.st));
+    launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, &c.dstat->vs);
+    depth_sort_and_scan(c.st, b, K);
+    c.launches += 1 + 9 + 3;  // project, onesweep sort (histogram + 8 passes), counts + scan
+    SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs.n_dup, b.off_r + K, sizeof(long long),
+                              cudaMemcpyDeviceToHost, c.st));
+    SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs, &c.dstat->vs, offsetof(ViewStatus, n_dup),
+                              cudaMemcpyDeviceToHost, c.st));
+    SGTR_CUDA(cudaStreamSynchronize(c.st));
+    const ViewStatus vs = c.hstat->vs;
+    if (vs.nonfinite_splat != INT_MAX) {
+        vr.err_kind = 1;
+        vr.err_index = vs.nonfinite_splat;
+    } else if (vs.degenerate_splat != INT_MAX) {
+        vr.err_kind = 2;
+        vr.err_index = vs.degenerate_splat;
+    }
+    if (vr.err_kind && throw_errors) {
+        if (vr.err_kind == 1)
+            throw numeric("rasterize: non-finite parameter in splat " + std::to_string(vr.err_index));
+        throw invalid("quat_to_rotation: degenerate quaternion");
+    }
+    if (vr.err_kind) return vr;
+    vr.n_visible = vs.n_visible;
+    vr.n_dup = vs.n_dup;
+    if (vr.n_dup > INT_MAX) throw Error(SGTR_RUNTIME, "binning: more than 2^31 tile duplicates");
+    const long long nd = std::max(vr.n_dup, 1LL);
+    b.tkeys = c.tkeys.as<unsigned int>(nd);
+    b.tkeys_alt = c.tkeys_alt.as<unsigned int>(nd);
+    b.dval = c.dval.as<int>(nd);
+    b.dval_alt = c.dval_alt.as<int>(nd);
+    b.dup_id = c.dup_id.as<int>(nd);
+    b.temp = c.temp.ensure(std::max(tb, tile_sort_temp_bytes(vr.n_dup, n_tiles)));
+    b.temp_bytes = c.temp.bytes;
+    emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
+    c.launches += vr.n_dup ? 5 : 0;  // emit, tile sort (histogram + 2 passes), ranges
+    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt, b.dup_id};
+    const int P = dc.W * dc.H;
+    launch_raster_fwd(c.st, vr.tl, rec, dc.W, dc.H, ro, img_ptr(c, c.img, P),
+                      c.tfin.as<double>(P), c.last.as<int>(P));
+    c.launches += 1;
+    return vr;
+}
+
+// K10 + K11 for an image-space adjoint already in c.adj
+void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender& vr, int mode,
+                   const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
+    const long long nd = std::max(vr.n_dup, 1LL);
+    double* slots = c.slots.as<double>((size_t)kAdj * nd);
+    launch_raster_vjp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro, c.adj.get<double>(),
+                      c.tfin.get<double>(), c.last.get<int>(), slots);
+    launch_chain(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+                 c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits, acc, flag);
+    c.launches += 2;
+}
+
+struct SsimOut {
+    double* adjl1;
+};
+
+// K8/K13 + K9: residual chain adjoint of the rendered image into c.adj
+void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const double* tangent,
+                      const double* u, double lambda, double floor_, double* loss_out) {
+    const int P = W * H;
+    SsimArgs a{};
+    a.mode = mode;
+    a.W = W;
+    a.H = H;
+    a.a = c.img.get<double>();
+    a.da = tangent;
+    a.b = gt;
+    a.u = u;
+    a.lambda = lambda;
+    a.floor = floor_;
+    a.adjl1 = mode == SSIM_VJP ? nullptr : img_ptr(c, c.adjl1, P);
+    a.P = img_ptr(c, c.Pf, P);
+    a.Q = img_ptr(c, c.Qf, P);
+    a.R = img_ptr(c, c.Rf, P);
+    const int nb = ssim_num_blocks(W, H);
+    a.loss_partials = c.partials.as<double>(std::max(nb, 5 * tr_num_blocks(c.K) + 8));
+    launch_ssim(c.st, a);
+    c.launches += 1;
+    if (mode == GRAD && loss_out) {
+        launch_sum_partials(c.st, a.loss_partials, nb, loss_out);
+        c.launches += 1;
+    }
+    launch_ssim_gather(c.st, W, H, c.img.get<double>(), gt, a.adjl1, a.P, a.Q, a.R,
+                       img_ptr(c, c.adj, P));
+    c.launches += 1;
+}
+
+void check_views(Ctx& c, bool need_gt) {
+    if (c.views.empty()) throw invalid("no views set");
+    if (need_gt && !c.has_gt) throw invalid("views have no target images");
+}
+
+const double* view_gt(Ctx& c, int v) {
+    const long long P = (long long)c.views[0].dc.W * c.views[0].dc.H;
+    return c.gt.get<double>() + 3 * P * v;
+}
+
+void check_ssim_size(int w, int h) {
+    if (w < 6 || h < 6) throw invalid("ssim: image smaller than the window");
+}
+
+// upload an interleaved host image into a planar device buffer
+double* upload_planar(Ctx& c, Buf& dst, const double* host, int P) {
+    double* tmp = c.vecbuf.as<double>(3LL * P);
+    SGTR_CUDA(cudaMemcpyAsync(tmp, host, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, c.st));
+    double* out = img_ptr(c, dst, P);
+    launch_to_planar(c.st, tmp, P, out);
+    c.launches += 1;
+    return out;
+}
+
+void download_interleaved(Ctx& c, const double* planar, int P, double* host) {
+    double* tmp = c.vecbuf.as<double>(3LL * P);
+    launch_to_interleaved(c.st, planar, P, tmp);
+    c.launches += 1;
+    SGTR_CUDA(cudaMemcpyAsync(host, tmp, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, c.st));
+    SGTR_CUDA(cudaStreamSynchronize(c.st));
+}
+
+void ensure_tail(Ctx& c, size_t n) {
+    if (c.htail_n >= n) return;
+    if (c.htail) cudaFreeHost(c.htail);
+    SGTR_CUDA(cudaMallocHost(&c.htail, sizeof(double) * n));
+    c.htail_n = n;
+}
+
+void allreduce(Ctx& c, double* buf, size_t n) {
+    if (c.nranks <= 1 || n == 0) return;
+    g_nccl.check(g_nccl.all_reduce(buf, buf, n, /*ncclFloat64*/ 8, /*ncclSum*/ 0, c.comm, c.st),
+                 "ncclAllReduce");
+}
+
+// ------------------------------------------------------------------ Algorithm 1
+// One step with its draws given.  `rng_ckpt` (if any) is the state to restore
+// when the step fails inside the gradient phase, where the reference throws
+// before drawing S2 and the probes.
+void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& s1,
+               const std::vector<int>& s2, const std::vector<uint32_t>& zbits, int nu,
+               bool refresh, const Rng* rng_ckpt, sgtr_step_diagnostics* diag) {
+    const int M = (int)c.views.size();
+    const int W = c.views[0].dc.W, H = c.views[0].dc.H, P = W * H;
+    const long long dim = c.dim();
+    const long long m = 6LL * P * M;
+    const RenderP ro = render_params(o.render);
+    const int n1 = (int)s1.size(), n2 = refresh ? (int)s2.size() : 0;
+    // fused buffer, summed by one allreduce per step:
+    //   [g_acc (dim) | loss[n1] | gflag[n1] | hflag | err_kind[n1+n2] |
+    //    err_index[n1+n2] | w_acc (dim, refresh steps only)]
+    const size_t tail_n = 2 * n1 + 1 + 2 * (n1 + n2);
+    const size_t tail_off = dim;
+    double* fused = c.fused.as<double>(2 * dim + tail_n);
+    double* g_acc = fused;
+    double* tail = fused + tail_off;
+    double* w_acc = tail + tail_n;
+    double* loss = tail;
+    double* gflag = tail + n1;
+    double* hflag = tail + 2 * n1;
+    double* errk = tail + 2 * n1 + 1;
+    double* erri = errk + (n1 + n2);
+    const size_t fused_n = dim + tail_n + (refresh ? dim : 0);
+    SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
+    ensure_tail(c, tail_n);
+    std::vector<double> herr(2 * (n1 + n2), 0.0);
+    bool local_error = false;
+    // gradient phase: stochastic_gradient (optimizer.cpp:36-65), views of S1
+    // split round-robin over ranks
+    for (int p = c.rank; p < n1 && !local_error; p += c.nranks) {
+        const View& v = c.views[s1[p]];
+        const ViewRender vr = render_view(c, v.dc, ro, false);
+        if (vr.err_kind) {
+            herr[p] = vr.err_kind;
+            herr[(n1 + n2) + p] = vr.err_index;
+            local_error = true;
+            break;
+        }
+        residual_adjoint(c, GRAD, W, H, view_gt(c, s1[p]), nullptr, nullptr, o.residual.lambda,
+                         o.residual.floor, loss + p);
+        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, g_acc, gflag + p);
+    }
+    // Hutchinson phase (optimizer.cpp:75-104), views of S2 split over ranks
+    if (refresh && !local_error) {
+        const long long words = (dim + 31) / 32;
+        uint32_t* dz = c.zbits.as<uint32_t>(std::max<long long>(words * nu, 1));
+        SGTR_CUDA(cudaMemcpyAsync(dz, zbits.data(), sizeof(uint32_t) * words * nu,
+                                  cudaMemcpyHostToDevice, c.st));
+        for (int s = 0; s < nu && !local_error; ++s) {
+            const uint32_t* zb = dz + words * s;
+            for (int q = c.rank; q < n2; q += c.nranks) {
+                const View& v = c.views[s2[q]];
+                const ViewRender vr = render_view(c, v.dc, ro, false);
+                if (vr.err_kind) {
+                    herr[n1 + q] = vr.err_kind;
+                    herr[(n1 + n2) + n1 + q] = vr.err_index;
+                    local_error = true;
+                    break;
+                }
+                double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
+                launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
+                launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, ro,
+                                  img_ptr(c, c.tan, P));
+                c.launches += 2;
+                residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(), nullptr,
+                                 o.residual.lambda, o.residual.floor, nullptr);
+                backward_view(c, v.dc, ro, vr, 1, nullptr, zb, w_acc, hflag);
+            }
+        }
+    }
+    if (local_error)
+        SGTR_CUDA(cudaMemcpyAsync(errk, herr.data(), sizeof(double) * herr.size(),
+                                  cudaMemcpyHostToDevice, c.st));
+    allreduce(c, fused, fused_n);
+    SGTR_CUDA(cudaMemcpyAsync(c.htail, tail, sizeof(double) * tail_n, cudaMemcpyDeviceToHost,
+                              c.st));
+    SGTR_CUDA(cudaStreamSynchronize(c.st));
+    const double* ht = c.htail;
+    const double* hk = ht + 2 * n1 + 1;
+    const double* hi = hk + (n1 + n2);
+    // gradient-phase failures: nothing but t and the S1 draw has happened
+    for (int p = 0; p < n1; ++p) {
+        if (hk[p] != 0.0 || ht[n1 + p] != 0.0) {
+            if (rng_ckpt) c.rng = *rng_ckpt;
+            if (hk[p] == 1.0)
+                throw numeric("rasterize: non-finite parameter in splat " +
+                              std::to_string((long long)hi[p]));
+            if (hk[p] == 2.0) throw invalid("quat_to_rotation: degenerate quaternion");
+            throw numeric("stochastic_gradient: non-finite gradient from view " +
+                          std::to_string(c.views[s1[p]].cam.id));
+        }
+    }
+    double loss_sum = 0.0;
+    for (int p = 0; p < n1; ++p) loss_sum += ht[p];
+    diag->batch_loss = loss_sum * static_cast<double>(M) / (2.0 * static_cast<double>(m) * n1);
+    int hutch_err = 0;
+    long long hutch_idx = 0;
+    bool hutch_fail = false;
+    if (refresh) {
+        for (int q = 0; q < n2 && !hutch_err; ++q)
+            if (hk[n1 + q] != 0.0) {
+                hutch_err = (int)hk[n1 + q];
+                hutch_idx = (long long)hi[n1 + q];
+            }
+        hutch_fail = hutch_err != 0 || ht[2 * n1] != 0.0;
+    }
+    // K14
+    if (!(o.eps_start >= o.eps_end) || !(o.eps_end > 0.0)) throw invalid("eps_at: bad schedule");
+    double eps;
+    sgtr_eps_at(o.eps_start, o.eps_end, o.total_steps, (int)c.t, &eps);
+    TrArgs a{};
+    a.K = c.K;
+    a.x = c.X();
+    a.x_out = c.x_alt.as<double>(std::max<long long>(dim, 1));
+    a.g_acc = g_acc;
+    a.gscale = static_cast<double>(M) / (static_cast<double>(m) * n1);
+    a.g_hat = c.ghat.get<double>();
+    a.d_hat = c.dhat.get<double>();
+    a.w_acc = w_acc;
+    a.dscale = refresh ? static_cast<double>(M) / (static_cast<double>(m) * n2 * nu) : 0.0;
+    a.refresh = refresh && !hutch_fail;
+    a.ghat_only = hutch_fail;
+    a.theta1 = o.theta1;
+    a.theta2 = o.theta2;
+    a.gamma_d = o.gamma_d;
+    a.eps = eps;
+    const double caps[5] = {o.cap_mean, o.cap_scale, o.cap_rotation, o.cap_opacity, o.cap_color};
+    const double bounds[5] = {o.s_min, o.alpha_min, o.alpha_max, o.c_min, o.c_max};
+    std::copy(caps, caps + 5, a.caps);
+    std::copy(bounds, bounds + 5, a.bounds);
+    c.have_applied = o.record_applied_step != 0;
+    a.applied = c.have_applied ? c.applied.as<double>(std::max<long long>(dim, 1)) : nullptr;
+    const int nb = tr_num_blocks(c.K);
+    a.partials = c.partials.as<double>(std::max(5 * nb + 8, ssim_num_blocks(W, H)));
+    c.hstat->bad_index = INT_MAX;
+    c.hstat->degenerate = 0;
+    SGTR_CUDA(cudaMemcpyAsync(&c.dstat->bad_index, &c.hstat->bad_index, 2 * sizeof(int),
+                              cudaMemcpyHostToDevice, c.st));
+    a.bad_index = &c.dstat->bad_index;
+    a.degenerate_flag = &c.dstat->degenerate;
+    launch_tr_update(c.st, a);
+    launch_tr_finalize(c.st, a.partials, nb, c.dstat->tr);
+    c.launches += 2;
+    SGTR_CUDA(cudaMemcpyAsync(&c.hstat->bad_index, &c.dstat->bad_index,
+                              offsetof(DevStatus, scalar) - offsetof(DevStatus, bad_index),
+                              cudaMemcpyDeviceToHost, c.st));
+    SGTR_CUDA(cudaStreamSynchronize(c.st));
+    diag->gnorm = std::sqrt(c.hstat->tr[0]);
+    diag->refreshed = refresh ? 1 : 0;
+    diag->n_local_views = 0;
+    for (int p = c.rank; p < n1; p += c.nranks) ++diag->n_local_views;
+    if (hutch_fail) {
+        if (hutch_err == 1)
+            throw numeric("rasterize: non-finite parameter in splat " + std::to_string(hutch_idx));
+        if (hutch_err == 2) throw invalid("quat_to_rotation: degenerate quaternion");
+        throw numeric("hutchinson_diag: non-finite sample");
+    }
+    diag->step_pre = std::sqrt(c.hstat->tr[1]);
+    if (c.hstat->degenerate) throw invalid("quat_to_rotation: degenerate quaternion");
+    if (c.hstat->bad_index != INT_MAX)
+        throw numeric(std::string("non-finite update in group ") +
+                      kGroupNames[group_of(c.K, c.hstat->bad_index)]);
+    diag->eps = eps;
+    diag->clip_frac = dim ? c.hstat->tr[3] / static_cast<double>(dim) : 0.0;
+    diag->step_post = std::sqrt(c.hstat->tr[2]);
+    diag->max_step_over_radius = c.hstat->tr[4];
+    std::swap(c.x.p, c.x_alt.p);
+    std::swap(c.x.bytes, c.x_alt.bytes);
+}
+
+void validate_opts(const sgtr_optimizer_options& o) {
+    if (o.hutch_samples < 1) throw invalid("hutchinson_diag: nu must be >= 1");
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return SGTR_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("out of host memory: ") + e.what();
+        return SGTR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SGTR_RUNTIME;
+    }
+}
+
+Ctx& ctx_ref(sgtr_ctx* c) {
+    if (!c) throw invalid("null context");
+    return *reinterpret_cast<Ctx*>(c);
+}
+
+void need_scene(Ctx& c) {
+    if (!c.x.p && c.K > 0) throw invalid("scene not set");
+}
+
+}  // namespace
+}  // namespace sgtr
+
+using namespace sgtr;
+
+extern "C" {
+
+const char* sgtr_last_error(void) { return g_last_error.c_str(); }
+
+int sgtr_create(int device, sgtr_ctx** out) {
+    return guarded([&] {
+        int n = 0;
+        SGTR_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw invalid("sgtr_create: no such CUDA device");
+        Ctx* c = new Ctx();
+        c->device = device;
+        try {
+            bind(*c);
+            SGTR_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+            SGTR_CUDA(cudaMalloc(&c->dstat, sizeof(DevStatus)));
+            SGTR_CUDA(cudaMallocHost(&c->hstat, sizeof(DevStatus)));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = reinterpret_cast<sgtr_ctx*>(c);
+    });
+}
+
+int sgtr_destroy(sgtr_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        Ctx* c = reinterpret_cast<Ctx*>(ctx);
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->st);
+        delete c;
+    });
+}
+
+int sgtr_get_stream(sgtr_ctx* ctx, void** stream) {
+    return guarded([&] { *stream = (void*)ctx_ref(ctx).st; });
+}
+
+int sgtr_synchronize(sgtr_ctx* ctx) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int64_t sgtr_launch_count(const sgtr_ctx* ctx) {
+    return ctx ? reinterpret_cast<const Ctx*>(ctx)->launches : 0;
+}
+
+int sgtr_set_scene(sgtr_ctx* ctx, const double* x, int64_t n_splats) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (n_splats < 0 || n_splats > (1LL << 28)) throw invalid("sgtr_set_scene: bad splat count");
+        const long long dim = 14LL * n_splats;
+        const bool resized = n_splats != c.K;
+        c.K = (int)n_splats;
+        double* d = c.x.as<double>(std::max<long long>(dim, 1));
+        if (dim)
+            SGTR_CUDA(cudaMemcpyAsync(d, x, sizeof(double) * dim, cudaMemcpyHostToDevice, c.st));
+        if (resized) {
+            // OptimizerState(dim, seed) lives with the scene dimension
+            c.ghat.as<double>(std::max<long long>(dim, 1));
+            c.dhat.as<double>(std::max<long long>(dim, 1));
+            SGTR_CUDA(cudaMemsetAsync(c.ghat.p, 0, sizeof(double) * std::max<long long>(dim, 1), c.st));
+            SGTR_CUDA(cudaMemsetAsync(c.dhat.p, 0, sizeof(double) * std::max<long long>(dim, 1), c.st));
+        }
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_get_scene(sgtr_ctx* ctx, double* x) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (c.dim())
+            SGTR_CUDA(cudaMemcpyAsync(x, c.X(), sizeof(double) * c.dim(), cudaMemcpyDeviceToHost,
+                                      c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int64_t sgtr_scene_size(const sgtr_ctx* ctx) {
+    return ctx ? reinterpret_cast<const Ctx*>(ctx)->K : 0;
+}
+
+int sgtr_set_views(sgtr_ctx* ctx, const sgtr_camera* cams, int32_t n, const double* const* gts) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (n < 0) throw invalid("sgtr_set_views: negative count");
+        std::vector<View> vs;
+        for (int i = 0; i < n; ++i) {
+            if (cams[i].width <= 0 || cams[i].height <= 0)
+                throw invalid("sgtr_set_views: empty image");
+            if (cams[i].width != cams[0].width || cams[i].height != cams[0].height)
+                throw invalid("sgtr_set_views: all views must share one image size");
+            vs.push_back({cams[i], make_devcam(cams[i])});
+        }
+        c.views = vs;
+        c.has_gt = false;
+        if (gts && n > 0) {
+            const int P = cams[0].width * cams[0].height;
+            double* g = c.gt.as<double>(3LL * P * n);
+            for (int i = 0; i < n; ++i) {
+                double* tmp = c.vecbuf.as<double>(3LL * P);
+                SGTR_CUDA(cudaMemcpyAsync(tmp, gts[i], sizeof(double) * 3 * P,
+                                          cudaMemcpyHostToDevice, c.st));
+                launch_to_planar(c.st, tmp, P, g + 3LL * P * i);
+            }
+            c.has_gt = true;
+        }
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro, int32_t quantize) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        check_views(c, false);
+        const int P = c.views[0].dc.W * c.views[0].dc.H;
+        double* g = c.gt.as<double>(3LL * P * c.views.size());
+        const RenderP rp = render_params(*ro);
+        for (size_t i = 0; i < c.views.size(); ++i) {
+            render_view(c, c.views[i].dc, rp, true);
+            SGTR_CUDA(cudaMemcpyAsync(g + 3LL * P * i, c.img.get<double>(), sizeof(double) * 3 * P,
+                                      cudaMemcpyDeviceToDevice, c.st));
+            if (quantize) launch_quantize8(c.st, g + 3LL * P * i, 3LL * P);
+        }
+        c.has_gt = true;
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_get_target(sgtr_ctx* ctx, int32_t view, double* gt) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        check_views(c, true);
+        if (view < 0 || view >= (int)c.views.size()) throw invalid("sgtr_get_target: bad view");
+        const int P = c.views[0].dc.W * c.views[0].dc.H;
+        download_interleaved(c, view_gt(c, view), P, gt);
+    });
+}
+
+int sgtr_state_reset(sgtr_ctx* ctx, uint64_t seed) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const long long n = std::max<long long>(c.dim(), 1);
+        SGTR_CUDA(cudaMemsetAsync(c.ghat.as<double>(n), 0, sizeof(double) * n, c.st));
+        SGTR_CUDA(cudaMemsetAsync(c.dhat.as<double>(n), 0, sizeof(double) * n, c.st));
+        c.t = 0;
+        c.rng = Rng(seed);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_state_set(sgtr_ctx* ctx, const double* g_hat, const double* d_hat, int64_t t) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const long long n = c.dim();
+        if (g_hat && n)
+            SGTR_CUDA(cudaMemcpyAsync(c.ghat.as<double>(n), g_hat, sizeof(double) * n,
+                                      cudaMemcpyHostToDevice, c.st));
+        if (d_hat && n)
+            SGTR_CUDA(cudaMemcpyAsync(c.dhat.as<double>(n), d_hat, sizeof(double) * n,
+                                      cudaMemcpyHostToDevice, c.st));
+        c.t = t;
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_state_get(sgtr_ctx* ctx, double* g_hat, double* d_hat, int64_t* t) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const long long n = c.dim();
+        if (g_hat && n)
+            SGTR_CUDA(cudaMemcpyAsync(g_hat, c.ghat.get<double>(), sizeof(double) * n,
+                                      cudaMemcpyDeviceToHost, c.st));
+        if (d_hat && n)
+            SGTR_CUDA(cudaMemcpyAsync(d_hat, c.dhat.get<double>(), sizeof(double) * n,
+                                      cudaMemcpyDeviceToHost, c.st));
+        if (t) *t = c.t;
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_rng_raw(sgtr_ctx* ctx, int64_t n, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        for (int64_t i = 0; i < n; ++i) out[i] = c.rng.gen();
+    });
+}
+
+int sgtr_rng_new(uint64_t seed, sgtr_rng** out) {
+    return guarded([&] { *out = reinterpret_cast<sgtr_rng*>(new std::mt19937_64(seed)); });
+}
+
+int sgtr_rng_draw(sgtr_rng* rng, int64_t n, uint64_t* out) {
+    return guarded([&] {
+        if (!rng) throw invalid("null rng");
+        auto& g = *reinterpret_cast<std::mt19937_64*>(rng);
+        for (int64_t i = 0; i < n; ++i) out[i] = g();
+    });
+}
+
+int sgtr_rng_free(sgtr_rng* rng) {
+    return guarded([&] { delete reinterpret_cast<std::mt19937_64*>(rng); });
+}
+
+int sgtr_step_3dgs2tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                      sgtr_step_diagnostics* diag) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        validate_opts(*opt);
+        *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
+        c.t += 1;
+        const int M = (int)c.views.size();
+        if (opt->batch_size < 1) throw invalid("stochastic_gradient: empty batch");
+        const std::vector<int> s1 = c.rng.sample(M, opt->batch_size);
+        const Rng ckpt = c.rng;
+        const bool refresh = opt->hess_interval <= 1 || c.t % opt->hess_interval == 1;
+        std::vector<int> s2;
+        std::vector<uint32_t> bits;
+        if (refresh) {
+            if (opt->hutch_batch_size < 1) throw invalid("hutchinson_diag: empty batch");
+            s2 = c.rng.sample(M, opt->hutch_batch_size);
+            const long long dim = c.dim(), words = (dim + 31) / 32;
+            bits.assign(words * opt->hutch_samples, 0u);
+            for (int s = 0; s < opt->hutch_samples; ++s) {
+                uint32_t* w = bits.data() + words * s;
+                for (long long k = 0; k < dim; ++k)
+                    if (c.rng.gen() & 1u) w[k >> 5] |= 1u << (k & 31);
+            }
+        }
+        step_core(c, *opt, s1, s2, bits, opt->hutch_samples, refresh, &ckpt, diag);
+    });
+}
+
+int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                               const int32_t* s1, int32_t n1, const int32_t* s2, int32_t n2,
+                               const uint32_t* probe_bits, int32_t nu,
+                               sgtr_step_diagnostics* diag) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
+        c.t += 1;
+        const int M = (int)c.views.size();
+        if (n1 < 1) throw invalid("stochastic_gradient: empty batch");
+        std::vector<int> v1(s1, s1 + n1), v2;
+        for (int v : v1)
+            if (v < 0 || v >= M) throw invalid("stochastic_gradient: view index out of range");
+        const bool refresh = opt->hess_interval <= 1 || c.t % opt->hess_interval == 1;
+        std::vector<uint32_t> bits;
+        if (refresh) {
+            if (nu < 1) throw invalid("hutchinson_diag: nu must be >= 1");
+            if (n2 < 1) throw invalid("hutchinson_diag: empty batch");
+            v2.assign(s2, s2 + n2);
+            for (int v : v2)
+                if (v < 0 || v >= M) throw invalid("hutchinson_diag: view index out of range");
+            const long long words = (c.dim() + 31) / 32;
+            bits.assign(probe_bits, probe_bits + words * nu);
+        }
+        step_core(c, *opt, v1, v2, bits, nu, refresh, nullptr, diag);
+    });
+}
+
+int sgtr_get_applied_step(sgtr_ctx* ctx, double* out) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (!c.have_applied) throw invalid("no applied step recorded");
+        SGTR_CUDA(cudaMemcpyAsync(out, c.applied.get<double>(), sizeof(double) * c.dim(),
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+// ------------------------------------------------------------------ seams
+int sgtr_rasterize(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                   double* color, double* t_final) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        render_view(c, dc, render_params(*ro), true);
+        const int P = dc.W * dc.H;
+        if (t_final)
+            SGTR_CUDA(cudaMemcpyAsync(t_final, c.tfin.get<double>(), sizeof(double) * P,
+                                      cudaMemcpyDeviceToHost, c.st));
+        download_interleaved(c, c.img.get<double>(), P, color);
+    });
+}
+
+int sgtr_rasterize_jvp(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                       const double* v, double* tangent) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        const RenderP rp = render_params(*ro);
+        const ViewRender vr = render_view(c, dc, rp, true);
+        const int P = dc.W * dc.H;
+        double* dv = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
+        SGTR_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * c.dim(), cudaMemcpyHostToDevice, c.st));
+        double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
+        launch_project_jvp(c.st, c.X(), c.K, dc, rp, dv, nullptr, trec);
+        launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, dc.W, dc.H, rp,
+                          img_ptr(c, c.tan, P));
+        c.launches += 2;
+        download_interleaved(c, c.tan.get<double>(), P, tangent);
+    });
+}
+
+int sgtr_rasterize_vjp(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                       const double* adjoint, double* grad) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        const RenderP rp = render_params(*ro);
+        const ViewRender vr = render_view(c, dc, rp, true);
+        const int P = dc.W * dc.H;
+        upload_planar(c, c.adj, adjoint, P);
+        double* g = c.seam1.as<double>(std::max<long long>(c.dim(), 1));
+        SGTR_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * std::max<long long>(c.dim(), 1), c.st));
+        double* flag = c.seam2.as<double>(1);
+        backward_view(c, dc, rp, vr, 0, nullptr, nullptr, g, flag);
+        SGTR_CUDA(cudaMemcpyAsync(grad, g, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+namespace {
+
+// shared body of the SSIM / residual seams on host images
+void ssim_seam(Ctx& c, int mode, const double* a, const double* da, const double* b,
+               const double* u, int w, int h, double lambda, double floor_, double* out0,
+               double* out1, double* adj_out) {
+    bind(c);
+    check_ssim_size(w, h);
+    const int P = w * h;
+    double* A = upload_planar(c, c.img, a, P);
+    double* B = upload_planar(c, c.seam0, b, P);
+    double* DA = da ? upload_planar(c, c.tan, da, P) : nullptr;
+    double* U = nullptr;
+    if (u && mode == RES_VJP) {
+        U = c.seam1.as<double>(6LL * P);
+        SGTR_CUDA(cudaMemcpyAsync(U, u, sizeof(double) * 6 * P, cudaMemcpyHostToDevice, c.st));
+    } else if (u) {
+        U = upload_planar(c, c.seam1, u, P);
+    }
+    if (mode == RES_VJP || mode == SSIM_VJP) {
+        residual_adjoint(c, mode, w, h, B, DA, U, lambda, floor_, nullptr);
+        download_interleaved(c, c.adj.get<double>(), P, adj_out);
+        return;
+    }
+    SsimArgs s{};
+    s.mode = mode;
+    s.W = w;
+    s.H = h;
+    s.a = A;
+    s.da = DA;
+    s.b = B;
+    s.lambda = lambda;
+    s.floor = floor_;
+    const bool resid = mode == RES_VEC || mode == RES_JVP;
+    double* o0 = c.seam2.as<double>((resid ? 6LL : 6LL) * P);
+    double* o1 = o0 + 3LL * P;
+    s.out0 = o0;
+    s.out1 = o1;
+    launch_ssim(c.st, s);
+    c.launches += 1;
+    if (resid) {
+        SGTR_CUDA(cudaMemcpyAsync(out0, o0, sizeof(double) * 6 * P, cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        return;
+    }
+    download_interleaved(c, o0, P, out0);
+    if (out1) download_interleaved(c, o1, P, out1);
+}
+
+}  // namespace
+
+int sgtr_ssim_map(sgtr_ctx* ctx, const double* a, const double* b, int32_t w, int32_t h,
+                  double* out) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), SSIM_MAP, a, nullptr, b, nullptr, w, h, 0.0, 0.0, out, nullptr,
+                  nullptr);
+    });
+}
+
+int sgtr_ssim_jvp(sgtr_ctx* ctx, const double* a, const double* da, const double* b, int32_t w,
+                  int32_t h, double* s, double* ds) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), SSIM_JVP, a, da, b, nullptr, w, h, 0.0, 0.0, s, ds, nullptr);
+    });
+}
+
+int sgtr_ssim_vjp(sgtr_ctx* ctx, const double* a, const double* b, const double* upstream,
+                  int32_t w, int32_t h, double* grad) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), SSIM_VJP, a, nullptr, b, upstream, w, h, 0.0, 0.0, nullptr,
+                  nullptr, grad);
+    });
+}
+
+int sgtr_residual_vector(sgtr_ctx* ctx, const double* rendered, const double* gt, int32_t w,
+                         int32_t h, const sgtr_residual_options* o, double* r) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), RES_VEC, rendered, nullptr, gt, nullptr, w, h, o->lambda,
+                  o->floor, r, nullptr, nullptr);
+    });
+}
+
+int sgtr_residual_jvp(sgtr_ctx* ctx, const double* rendered, const double* tangent,
+                      const double* gt, int32_t w, int32_t h, const sgtr_residual_options* o,
+                      double* dr) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), RES_JVP, rendered, tangent, gt, nullptr, w, h, o->lambda,
+                  o->floor, dr, nullptr, nullptr);
+    });
+}
+
+int sgtr_residual_vjp(sgtr_ctx* ctx, const double* rendered, const double* gt, int32_t w,
+                      int32_t h, const double* u, const sgtr_residual_options* o, double* adj) {
+    return guarded([&] {
+        ssim_seam(ctx_ref(ctx), RES_VJP, rendered, nullptr, gt, u, w, h, o->lambda, o->floor,
+                  nullptr, nullptr, adj);
+    });
+}
+
+int sgtr_view_jacobian_apply(sgtr_ctx* ctx, int32_t view, const double* v,
+                             const sgtr_residual_options* rs, const sgtr_render_options* ro,
+                             double* out) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        if (view < 0 || view >= (int)c.views.size()) throw invalid("view index out of range");
+        const View& vw = c.views[view];
+        const RenderP rp = render_params(*ro);
+        const ViewRender vr = render_view(c, vw.dc, rp, true);
+        const int W = vw.dc.W, H = vw.dc.H, P = W * H;
+        check_ssim_size(W, H);
+        double* dv = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
+        SGTR_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * c.dim(), cudaMemcpyHostToDevice, c.st));
+        double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
+        launch_project_jvp(c.st, c.X(), c.K, vw.dc, rp, dv, nullptr, trec);
+        launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, rp, img_ptr(c, c.tan, P));
+        SsimArgs s{};
+        s.mode = RES_JVP;
+        s.W = W;
+        s.H = H;
+        s.a = c.img.get<double>();
+        s.da = c.tan.get<double>();
+        s.b = view_gt(c, view);
+        s.lambda = rs->lambda;
+        s.floor = rs->floor;
+        s.out0 = c.seam2.as<double>(6LL * P);
+        launch_ssim(c.st, s);
+        c.launches += 3;
+        SGTR_CUDA(cudaMemcpyAsync(out, s.out0, sizeof(double) * 6 * P, cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_view_jacobian_applyT(sgtr_ctx* ctx, int32_t view, const double* u,
+                              const sgtr_residual_options* rs, const sgtr_render_options* ro,
+                              double* grad) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        if (view < 0 || view >= (int)c.views.size()) throw invalid("view index out of range");
+        const View& vw = c.views[view];
+        const RenderP rp = render_params(*ro);
+        const ViewRender vr = render_view(c, vw.dc, rp, true);
+        const int W = vw.dc.W, H = vw.dc.H, P = W * H;
+        check_ssim_size(W, H);
+        double* U = c.seam1.as<double>(6LL * P);
+        SGTR_CUDA(cudaMemcpyAsync(U, u, sizeof(double) * 6 * P, cudaMemcpyHostToDevice, c.st));
+        residual_adjoint(c, RES_VJP, W, H, view_gt(c, view), nullptr, U, rs->lambda, rs->floor,
+                         nullptr);
+        double* g = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
+        SGTR_CUDA(cudaMemsetAsync(g, 0, sizeof(double) * std::max<long long>(c.dim(), 1), c.st));
+        double* flag = c.seam2.as<double>(1);
+        backward_view(c, vw.dc, rp, vr, 0, nullptr, nullptr, g, flag);
+        SGTR_CUDA(cudaMemcpyAsync(grad, g, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_stochastic_gradient(sgtr_ctx* ctx, const int32_t* batch, int32_t n,
+                             const sgtr_residual_options* rs, const sgtr_render_options* ro,
+                             double* g, double* batch_loss) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        if (n < 1) throw invalid("stochastic_gradient: empty batch");
+        const int M = (int)c.views.size();
+        const int W = c.views[0].dc.W, H = c.views[0].dc.H;
+        check_ssim_size(W, H);
+        const long long m = 6LL * W * H * M, dim = std::max<long long>(c.dim(), 1);
+        double* acc = c.seam0.as<double>(dim + 2LL * n);
+        double* loss = acc + dim;
+        double* flags = loss + n;
+        SGTR_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (dim + 2LL * n), c.st));
+        const RenderP rp = render_params(*ro);
+        for (int p = 0; p < n; ++p) {
+            if (batch[p] < 0 || batch[p] >= M)
+                throw invalid("stochastic_gradient: view index out of range");
+            const View& v = c.views[batch[p]];
+            const ViewRender vr = render_view(c, v.dc, rp, true);
+            residual_adjoint(c, GRAD, W, H, view_gt(c, batch[p]), nullptr, nullptr, rs->lambda,
+                             rs->floor, loss + p);
+            backward_view(c, v.dc, rp, vr, 0, nullptr, nullptr, acc, flags + p);
+        }
+        std::vector<double> tail(2 * n);
+        SGTR_CUDA(cudaMemcpyAsync(tail.data(), loss, sizeof(double) * 2 * n,
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        for (int p = 0; p < n; ++p)
+            if (tail[n + p] != 0.0)
+                throw numeric("stochastic_gradient: non-finite gradient from view " +
+                              std::to_string(c.views[batch[p]].cam.id));
+        const double scale = static_cast<double>(M) / (static_cast<double>(m) * n);
+        launch_scale(c.st, acc, c.dim(), scale);
+        c.launches += 1;
+        SGTR_CUDA(cudaMemcpyAsync(g, acc, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        double loss_sum = 0.0;
+        for (int p = 0; p < n; ++p) loss_sum += tail[p];
+        if (batch_loss)
+            *batch_loss = loss_sum * static_cast<double>(M) / (2.0 * static_cast<double>(m) * n);
+    });
+}
+
+int sgtr_hutchinson_diag(sgtr_ctx* ctx, const int32_t* batch, int32_t n, int32_t nu,
+                         const double* probes, const sgtr_residual_options* rs,
+                         const sgtr_render_options* ro, double* d) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        check_views(c, true);
+        if (nu < 1) throw invalid("hutchinson_diag: nu must be >= 1");
+        if (n < 1) throw invalid("hutchinson_diag: empty batch");
+        const int M = (int)c.views.size();
+        const int W = c.views[0].dc.W, H = c.views[0].dc.H, P = W * H;
+        check_ssim_size(W, H);
+        const long long m = 6LL * P * M, dim = std::max<long long>(c.dim(), 1);
+        double* acc = c.seam1.as<double>(dim + 1);
+        double* flag = acc + dim;
+        SGTR_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (dim + 1), c.st));
+        double* z = c.seam0.as<double>(dim);
+        const RenderP rp = render_params(*ro);
+        for (int s = 0; s < nu; ++s) {
+            SGTR_CUDA(cudaMemcpyAsync(z, probes + s * c.dim(), sizeof(double) * c.dim(),
+                                      cudaMemcpyHostToDevice, c.st));
+            for (int q = 0; q < n; ++q) {
+                if (batch[q] < 0 || batch[q] >= M)
+                    throw invalid("hutchinson_diag: view index out of range");
+                const View& v = c.views[batch[q]];
+                const ViewRender vr = render_view(c, v.dc, rp, true);
+                double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
+                launch_project_jvp(c.st, c.X(), c.K, v.dc, rp, z, nullptr, trec);
+                launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, rp,
+                                  img_ptr(c, c.tan, P));
+                c.launches += 2;
+                residual_adjoint(c, HUTCH, W, H, view_gt(c, batch[q]), c.tan.get<double>(),
+                                 nullptr, rs->lambda, rs->floor, nullptr);
+                backward_view(c, v.dc, rp, vr, 1, z, nullptr, acc, flag);
+            }
+            double hf = 0.0;
+            SGTR_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+            SGTR_CUDA(cudaStreamSynchronize(c.st));
+            if (hf != 0.0) throw numeric("hutchinson_diag: non-finite sample");
+        }
+        const double scale = static_cast<double>(M) / (static_cast<double>(m) * n * nu);
+        launch_scale(c.st, acc, c.dim(), scale);
+        c.launches += 1;
+        SGTR_CUDA(cudaMemcpyAsync(d, acc, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_shd_radii(sgtr_ctx* ctx, double eps, const double caps[5], double* eta) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        double* e = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
+        launch_shd_radii(c.st, c.K, c.X(), eps, caps, e);
+        c.launches += 1;
+        SGTR_CUDA(cudaMemcpyAsync(eta, e, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_eps_at(double e0, double e1, int32_t total, int32_t t, double* out) {
+    return guarded([&] {  // trust_region.cpp:261-268
+        if (!(e0 >= e1) || !(e1 > 0.0)) throw invalid("eps_at: bad schedule");
+        if (total <= 0 || t <= 0) {
+            *out = e0;
+        } else if (t >= total) {
+            *out = e1;
+        } else {
+            const double frac = static_cast<double>(t) / total;
+            *out = e0 * std::pow(e1 / e0, frac);
+        }
+    });
+}
+
+int sgtr_project(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                 double* out) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        double* o = c.seam0.as<double>(std::max(12LL * c.K, 1LL));
+        launch_project_dump(c.st, c.X(), c.K, dc, render_params(*ro), o);
+        c.launches += 1;
+        SGTR_CUDA(cudaMemcpyAsync(out, o, sizeof(double) * 12 * c.K, cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_dump_binning(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                      int32_t* n_visible, int32_t* order, int64_t* n_dup, int64_t* tile_start,
+                      int64_t* tile_end, int32_t* lists) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        const ViewRender vr = render_view(c, dc, render_params(*ro), true);
+        *n_visible = vr.n_visible;
+        *n_dup = vr.n_dup;
+        if (!lists) return;
+        const int n_tiles = vr.tl.tiles_x * vr.tl.tiles_y;
+        std::vector<int> ids(vr.n_visible), ts(n_tiles), te(n_tiles), dv(vr.n_dup), did(vr.n_dup);
+        SGTR_CUDA(cudaMemcpyAsync(ids.data(), c.ids_alt.get<int>(), sizeof(int) * vr.n_visible,
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaMemcpyAsync(ts.data(), vr.tl.tile_start, sizeof(int) * n_tiles,
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaMemcpyAsync(te.data(), vr.tl.tile_end, sizeof(int) * n_tiles,
+                                  cudaMemcpyDeviceToHost, c.st));
+        if (vr.n_dup) {
+            SGTR_CUDA(cudaMemcpyAsync(dv.data(), vr.tl.sorted_d, sizeof(int) * vr.n_dup,
+                                      cudaMemcpyDeviceToHost, c.st));
+            SGTR_CUDA(cudaMemcpyAsync(did.data(), vr.tl.dup_id, sizeof(int) * vr.n_dup,
+                                      cudaMemcpyDeviceToHost, c.st));
+        }
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        for (int i = 0; i < vr.n_visible; ++i) order[i] = ids[i];
+        for (int t = 0; t < n_tiles; ++t) {
+            tile_start[t] = ts[t];
+            tile_end[t] = te[t];
+        }
+        for (long long j = 0; j < vr.n_dup; ++j) lists[j] = did[dv[j]];
+    });
+}
+
+// dataset.cpp:25-67 with the declared extensions (W != H, size scaling)
+int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init_x,
+                        sgtr_camera* cams) {
+    return guarded([&] {
+        if (cfg->gt_splats < 1 || cfg->init_splats < 0 || cfg->views < 0 || cfg->width < 1 ||
+            cfg->height < 1)
+            throw invalid("sgtr_make_synthetic: bad configuration");
+        Rng rng(cfg->seed);
+        const long long kg = cfg->gt_splats, ki = cfg->init_splats;
+        const double ss = cfg->size_scale;
+        auto put = [](double* x, long long k, long long i, const double* mu, const double* s,
+                      const double* q, double a, const double* c) {
+            for (int j = 0; j < 3; ++j) {
+                x[3 * i + j] = mu[j];
+                x[3 * k + 3 * i + j] = s[j];
+                x[11 * k + 3 * i + j] = c[j];
+            }
+            for (int j = 0; j < 4; ++j) x[6 * k + 4 * i + j] = q[j];
+            x[10 * k + i] = a;
+        };
+        std::vector<double> gmu(3 * kg);
+        for (long long i = 0; i < kg; ++i) {
+            double mu[3], s[3], q[4], c[3];
+            for (int a = 0; a < 3; ++a) mu[a] = rng.uniform(-0.5, 0.5);
+            for (int a = 0; a < 3; ++a) s[a] = rng.log_uniform(0.02 * ss, 0.2 * ss);
+            for (int a = 0; a < 4; ++a) q[a] = rng.normal();
+            const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            if (n > 1e-9) {
+                for (int a = 0; a < 4; ++a) q[a] = q[a] / n;
+            } else {
+                q[0] = q[1] = q[2] = 0.0;
+                q[3] = 1.0;
+            }
+            const double alpha = rng.uniform(0.3, 0.9);
+            for (int a = 0; a < 3; ++a) c[a] = rng.uniform(0.1, 1.0);
+            put(gt_x, kg, i, mu, s, q, alpha, c);
+            for (int a = 0; a < 3; ++a) gmu[3 * i + a] = mu[a];
+        }
+        for (long long i = 0; i < ki; ++i) {
+            double mu[3];
+            const double* src = gmu.data() + 3 * (i % kg);
+            for (int a = 0; a < 3; ++a) mu[a] = src[a] + cfg->sigma_init * ss * rng.normal();
+            const double s[3] = {cfg->init_scale * ss, cfg->init_scale * ss, cfg->init_scale * ss};
+            const double q[4] = {0, 0, 0, 1};
+            const double c[3] = {0.5, 0.5, 0.5};
+            put(init_x, ki, i, mu, s, q, cfg->init_opacity, c);
+        }
+        const double focal = cfg->focal_factor * cfg->height;
+        for (int v = 0; v < cfg->views; ++v) {
+            const double ang = 2.0 * M_PI * v / cfg->views;
+            const double eye[3] = {cfg->camera_radius * std::cos(ang),
+                                   cfg->camera_radius * std::sin(ang), cfg->camera_height};
+            // look_at_camera (scene.cpp:130-147)
+            double z[3] = {-eye[0], -eye[1], -eye[2]};
+            auto normalize = [](double* u) {
+                const double n2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+                if (n2 > 0.0) {
+                    const double s = std::sqrt(n2);
+                    for (int i = 0; i < 3; ++i) u[i] = u[i] / s;
+                }
+            };
+            auto cross = [](const double* a, const double* b, double* o) {
+                o[0] = a[1] * b[2] - a[2] * b[1];
+                o[1] = a[2] * b[0] - a[0] * b[2];
+                o[2] = a[0] * b[1] - a[1] * b[0];
+            };
+            normalize(z);
+            double up[3] = {0, 0, 1};
+            if (std::abs(z[0] * up[0] + z[1] * up[1] + z[2] * up[2]) > 0.999) {
+                up[1] = 1;
+                up[2] = 0;
+            }
+            double xa[3], ya[3];
+            cross(z, up, xa);
+            normalize(xa);
+            cross(z, xa, ya);
+            const double r[9] = {xa[0], xa[1], xa[2], ya[0], ya[1], ya[2], z[0], z[1], z[2]};
+            sgtr_camera cam{};
+            cam.id = v;
+            cam.width = cfg->width;
+            cam.height = cfg->height;
+            cam.fx = focal;
+            cam.fy = focal;
+            cam.cx = cfg->width / 2.0;
+            cam.cy = cfg->height / 2.0;
+            // rotation_to_quat (scene.cpp:94-128)
+            double* q = cam.q_wc;
+            const double tr = r[0] + r[4] + r[8];
+            if (tr > 0.0) {
+                const double s = std::sqrt(tr + 1.0) * 2.0;
+                q[3] = 0.25 * s;
+                q[0] = (r[7] - r[5]) / s;
+                q[1] = (r[2] - r[6]) / s;
+                q[2] = (r[3] - r[1]) / s;
+            } else if (r[0] > r[4] && r[0] > r[8]) {
+                const double s = std::sqrt(1.0 + r[0] - r[4] - r[8]) * 2.0;
+                q[3] = (r[7] - r[5]) / s;
+                q[0] = 0.25 * s;
+                q[1] = (r[1] + r[3]) / s;
+                q[2] = (r[2] + r[6]) / s;
+            } else if (r[4] > r[8]) {
+                const double s = std::sqrt(1.0 + r[4] - r[0] - r[8]) * 2.0;
+                q[3] = (r[2] - r[6]) / s;
+                q[0] = (r[1] + r[3]) / s;
+                q[1] = 0.25 * s;
+                q[2] = (r[5] + r[7]) / s;
+            } else {
+                const double s = std::sqrt(1.0 + r[8] - r[0] - r[4]) * 2.0;
+                q[3] = (r[3] - r[1]) / s;
+                q[0] = (r[2] + r[6]) / s;
+                q[1] = (r[5] + r[7]) / s;
+                q[2] = 0.25 * s;
+            }
+            const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            for (int i = 0; i < 4; ++i) q[i] = q[i] / qn;
+            for (int i = 0; i < 3; ++i)
+                cam.t_wc[i] = -r[3 * i] * eye[0] + -r[3 * i + 1] * eye[1] + -r[3 * i + 2] * eye[2];
+            cams[v] = cam;
+        }
+    });
+}
+
+int sgtr_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        g_nccl.load();
+        g_nccl.check(g_nccl.get_unique_id(out), "ncclGetUniqueId");
+    });
+}
+
+int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw invalid("sgtr_comm_init: bad rank");
+        c.nranks = nranks;
+        c.rank = rank;
+        if (nranks == 1) return;
+        g_nccl.load();
+        auto init = (CommInitRankFn)dlsym(g_nccl.lib, "ncclCommInitRank");
+        if (!init) throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks ncclCommInitRank");
+        UniqueId u;
+        std::memcpy(u.internal, id, 128);
+        g_nccl.check(init(&c.comm, nranks, u, rank), "ncclCommInitRank");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// binning.cu — K2 depth sort, K3 tile-count scan, K4 duplicate emission,
+// K5 stable tile sort, K6 tile ranges.
+//
+// Integer work, bit-exact against the oracle's restated binning: the depth
+// keys are an order-preserving map of the FP64 depths (ties broken by the
+// splat index because the radix sort is stable over index-ordered input,
+// render.cpp:83-87), and duplicates are emitted in depth-rank order so the
+// stable sort on the tile id alone leaves every tile list in (depth, index)
+// order.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace sgtr {
+namespace {
+
+__global__ void k_gather_counts(const int* __restrict__ sorted_ids,
+                                const int* __restrict__ tcount, int K,
+                                long long* __restrict__ cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < K) cnt[r] = tcount[sorted_ids[r]];
+    if (r == K) cnt[r] = 0;
+}
+
+// one warp per splat: lanes stride over the splat's tile rectangle
+__global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids,
+                                              const int* __restrict__ tcount,
+                                              const int4* __restrict__ rect,
+                                              const long long* __restrict__ off_r,
+                                              int n_visible, int tiles_x,
+                                              unsigned int* __restrict__ tkeys,
+                                              int* __restrict__ dval,
+                                              int* __restrict__ dup_id) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_visible) return;
+    const int id = sorted_ids[warp];
+    const int c = tcount[id];
+    if (c == 0) return;
+    const int4 t = rect[id];
+    const int w = t.z - t.x + 1;
+    const long long base = off_r[warp];
+    for (int j = lane; j < c; j += 32) {
+        const int ty = t.y + j / w, tx = t.x + j % w;
+        const long long d = base + j;
+        tkeys[d] = (unsigned int)(ty * tiles_x + tx);
+        dval[d] = (int)d;
+        dup_id[d] = id;
+    }
+}
+
+__global__ void k_ranges(const unsigned int* __restrict__ tkeys, long long n,
+                         int* __restrict__ start, int* __restrict__ end) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned int k = tkeys[i];
+    if (i == 0 || tkeys[i - 1] != k) start[k] = (int)i;
+    if (i == n - 1 || tkeys[i + 1] != k) end[k] = (int)(i + 1);
+}
+
+int bits_for(int n) {
+    int b = 1;
+    while ((1LL << b) < n) ++b;
+    return b;
+}
+
+}  // namespace
+
+size_t depth_sort_temp_bytes(int K) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr,
+                                    K);
+    return bytes;
+}
+
+size_t scan_temp_bytes(int K) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (long long*)nullptr, (long long*)nullptr,
+                                  K + 1);
+    return bytes;
+}
+
+size_t tile_sort_temp_bytes(long long n_dup, int n_tiles) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned int*)nullptr,
+                                    (unsigned int*)nullptr, (int*)nullptr, (int*)nullptr,
+                                    (int)n_dup, 0, bits_for(n_tiles));
+    return bytes;
+}
+
+void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
+    if (K > 0) {
+        size_t bytes = b.temp_bytes;
+        SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.keys, b.keys_alt, b.ids,
+                                                  b.ids_alt, K, 0, 64, st));
+    }
+    // counts in depth-rank order (reuses keys as a long long scratch of K+1)
+    long long* cnt = reinterpret_cast<long long*>(b.keys);
+    k_gather_counts<<<ceil_div(K + 1, 256), 256, 0, st>>>(b.ids_alt, b.tcount, K, cnt);
+    SGTR_CUDA(cudaGetLastError());
+    size_t bytes = b.temp_bytes;
+    SGTR_CUDA(cub::DeviceScan::ExclusiveSum(b.temp, bytes, cnt, b.off_r, K + 1, st));
+}
+
+void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long long n_dup,
+                         int tiles_x, int n_tiles) {
+    SGTR_CUDA(cudaMemsetAsync(b.tile_start, 0, sizeof(int) * n_tiles, st));
+    SGTR_CUDA(cudaMemsetAsync(b.tile_end, 0, sizeof(int) * n_tiles, st));
+    if (n_dup == 0) return;
+    k_emit<<<ceil_div((long long)n_visible * 32, 256), 256, 0, st>>>(
+        b.ids_alt, b.tcount, b.rect, b.off_r, n_visible, tiles_x, b.tkeys, b.dval, b.dup_id);
+    SGTR_CUDA(cudaGetLastError());
+    size_t bytes = b.temp_bytes;
+    SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,
+                                              b.dval_alt, (int)n_dup, 0, bits_for(n_tiles),
+                                              st));
+    k_ranges<<<ceil_div(n_dup, 256), 256, 0, st>>>(b.tkeys_alt, n_dup, b.tile_start,
+                                                   b.tile_end);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+}  // namespace sgtr

@@ -1,0 +1,137 @@
+// launch.h — host-side launchers shared between the translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace sgtr {
+
+// ---------------------------------------------------------------- project.cu
+// K1: per-splat projection -> 128-byte fragment record, order-preserving
+// 64-bit depth key (culled = ~0), tile rectangle and tile count.
+void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                    const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
+                    int4* rect, int* tcount, ViewStatus* status);
+// parity dump: 12 doubles per splat (culled, depth, px, py, bx0..by1, i00..i11, 0)
+void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                         const RenderP& ro, double* out);
+// K12 (projection half): tangent records along a dense direction v (seam) or
+// along probe bits (bit set -> +1)
+void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                        const RenderP& ro, const double* v, const uint32_t* zbits,
+                        double* trec);
+// K11: segmented reduce of the (tile, fragment) adjoint slots of each visible
+// splat, then the chain through projection + invert2x2.  mode 0 adds the
+// gradient into acc; mode 1 adds z (.) contribution (Hutchinson).
+// The probe is dense (zdense) or packed bits (zbits); a non-finite
+// contribution stores 1.0 into *nonfinite_flag.
+void launch_chain(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+                  const RenderP& ro, const int* sorted_ids, int n_visible,
+                  const long long* off_r, const int* tcount, const double* slots,
+                  const double* zdense, const uint32_t* zbits, double* acc,
+                  double* nonfinite_flag);
+
+// ---------------------------------------------------------------- binning.cu
+struct BinBuffers {
+    unsigned long long *keys, *keys_alt;
+    int *ids, *ids_alt;
+    int4* rect;
+    int* tcount;
+    long long* off_r;      // n+1 exclusive offsets in depth-rank order
+    unsigned int *tkeys, *tkeys_alt;
+    int *dval, *dval_alt;  // duplicate index carried through the tile sort
+    int* dup_id;           // duplicate -> splat id
+    int *tile_start, *tile_end;
+    void* temp;
+    size_t temp_bytes;
+};
+size_t depth_sort_temp_bytes(int K);
+size_t scan_temp_bytes(int K);
+size_t tile_sort_temp_bytes(long long n_dup, int n_tiles);
+// K2 (+ the K3 scan): sorts keys, returns sorted ids in b.ids_alt and the
+// exclusive tile-count offsets (total at off_r[K])
+void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K);
+// K4-K6: duplicates, stable tile sort, tile ranges
+void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long long n_dup,
+                         int tiles_x, int n_tiles);
+
+// ---------------------------------------------------------------- raster.cu
+struct TileLists {
+    int tiles_x, tiles_y;
+    const int* tile_start;
+    const int* tile_end;
+    const int* sorted_d;  // tile-sorted duplicate indices
+    const int* dup_id;    // duplicate -> splat id
+};
+// K7: front-to-back blend -> planar image, final T, processed count per pixel
+void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
+                       int H, const RenderP& ro, double* img, double* tfinal, int* last);
+// K10: back-to-front adjoint sweep -> 9 adjoints per (tile, fragment) slot
+void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
+                       int H, const RenderP& ro, const double* adj, const double* tfinal,
+                       const int* last, double* slots);
+// K12 (raster half): tangent image along the tangent records
+void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
+                       const double* trec, int W, int H, const RenderP& ro,
+                       double* tangent);
+
+// ---------------------------------------------------------------- ssim.cu
+enum SsimMode {
+    SSIM_MAP = 0,  // out0 = SSIM
+    SSIM_JVP,      // out0 = SSIM, out1 = dSSIM
+    RES_VEC,       // out0 = residual vector (6P)
+    RES_JVP,       // out0 = residual JVP (6P)
+    GRAD,          // u = f: loss partials, adjL1 and P, Q, R (K8)
+    HUTCH,         // u = J t: adjL1 and P, Q, R (K13)
+    RES_VJP,       // u given (6P, in `u`): adjL1 and P, Q, R
+    SSIM_VJP       // upstream given (3P planar, in `u`): P, Q, R
+};
+struct SsimArgs {
+    int mode, W, H;
+    const double *a, *da, *b, *u;
+    double lambda, floor;
+    double *out0, *out1, *adjl1, *P, *Q, *R, *loss_partials;
+};
+int ssim_num_blocks(int W, int H);
+void launch_ssim(cudaStream_t st, const SsimArgs& a);
+// K9: adj = adjL1 + W^T P + a (.) W^T Q + b (.) W^T R (reflection-aware gather)
+void launch_ssim_gather(cudaStream_t st, int W, int H, const double* a, const double* b,
+                        const double* adjl1, const double* P, const double* Q,
+                        const double* R, double* adj);
+void launch_sum_partials(cudaStream_t st, const double* partials, int n, double* out);
+// layout conversions: interleaved (H,W,3) <-> planar (3,H,W)
+void launch_to_planar(cudaStream_t st, const double* in, int P, double* out);
+void launch_to_interleaved(cudaStream_t st, const double* in, int P, double* out);
+void launch_quantize8(cudaStream_t st, double* img, long long n);
+
+// ---------------------------------------------------------------- update.cu
+struct TrArgs {
+    int K;
+    const double* x;
+    double* x_out;
+    const double* g_acc;  // unscaled sum of per-view gradients
+    double gscale;
+    double* g_hat;
+    double* d_hat;
+    const double* w_acc;  // unscaled sum of z (.) J^T J z (refresh steps)
+    double dscale;
+    int refresh;          // update D-hat from w_acc
+    int ghat_only;        // Hutchinson failed: update g-hat and stop
+    double theta1, theta2, gamma_d, eps;
+    double caps[5];
+    double bounds[5];     // s_min, alpha_min, alpha_max, c_min, c_max
+    double* applied;      // optional clipped step
+    double* partials;     // per block: sum g^2, sum dx^2, sum clipped^2, n_clip, max ratio
+    int* bad_index;       // min index of a non-finite clipped coordinate
+    int* degenerate_flag; // a splat with |q|^2 < 1e-24 reached shd_radii
+};
+int tr_num_blocks(int K);
+void launch_tr_update(cudaStream_t st, const TrArgs& a);
+// 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
+void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5);
+void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
+                      const double caps[5], double* eta);
+void launch_scale(cudaStream_t st, double* v, long long n, double s);
+void launch_fill_int(cudaStream_t st, int* p, long long n, int v);
+
+}  // namespace sgtr

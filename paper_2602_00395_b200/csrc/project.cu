@@ -1,0 +1,269 @@
+// project.cu — K1 projection, K12 tangent projection, K11 adjoint chain.
+// Compiled with --fmad=false: every FP64 expression rounds like the oracle,
+// so depth keys, mu2d and the bounding boxes are bit-identical to it.
+#include "common.cuh"
+#include "geometry.cuh"
+#include "launch.h"
+
+namespace sgtr {
+namespace {
+
+constexpr unsigned long long kCulledKey = ~0ull;
+
+// order-preserving map of an IEEE double onto uint64
+__device__ __forceinline__ unsigned long long depth_key(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+struct Splat {
+    double mu[3], s[3], q[4], c[3], alpha;
+};
+
+__device__ __forceinline__ Splat load_splat(const double* __restrict__ x, int K, int i) {
+    Splat p;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        p.mu[a] = x[3LL * i + a];
+        p.s[a] = x[3LL * K + 3LL * i + a];
+        p.c[a] = x[11LL * K + 3LL * i + a];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) p.q[a] = x[6LL * K + 4LL * i + a];
+    p.alpha = x[10LL * K + i];
+    return p;
+}
+
+__device__ __forceinline__ bool splat_finite(const Splat& p) {
+    bool ok = isfinite(p.alpha);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ok = ok && isfinite(p.mu[a]) && isfinite(p.s[a]) && isfinite(p.c[a]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ok = ok && isfinite(p.q[a]);
+    return ok;
+}
+
+__device__ __forceinline__ Proj<double> project_primal(const Splat& p, const DevCam& cam,
+                                                       const RenderP& ro) {
+    return project<double>(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, cam.cx, cam.cy,
+                           ro.z_near, ro.lowpass);
+}
+
+__global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, int K, DevCam cam,
+                                                 RenderP ro, double* __restrict__ rec,
+                                                 unsigned long long* __restrict__ keys,
+                                                 int* __restrict__ ids, int4* __restrict__ rect,
+                                                 int* __restrict__ tcount, ViewStatus* status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool visible = false;
+    if (i < K) {
+        const Splat p = load_splat(x, K, i);
+        ids[i] = i;
+        if (!splat_finite(p)) atomicMin(&status->nonfinite_splat, i);
+        const Proj<double> pr = project_primal(p, cam, ro);
+        if (!pr.culled && pr.degenerate) atomicMin(&status->degenerate_splat, i);
+        if (pr.culled || pr.degenerate) {
+            keys[i] = kCulledKey;
+            tcount[i] = 0;
+        } else {
+            visible = true;
+            const double px = pr.mx, py = pr.my;
+            const double rx = ro.cutoff * sqrt(pr.c00);
+            const double ry = ro.cutoff * sqrt(pr.c11);
+            double i00, i01, i11;
+            invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
+            double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,   py,       i00, i01,
+                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], pr.depth, 0.0, 0.0};
+            double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
+#pragma unroll
+            for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);
+            keys[i] = depth_key(pr.depth);
+            int x0, x1, y0, y1;
+            pixel_range(r[R_BX0], r[R_BX1], cam.W, x0, x1);
+            pixel_range(r[R_BY0], r[R_BY1], cam.H, y0, y1);
+            if (x0 > x1 || y0 > y1) {
+                tcount[i] = 0;
+            } else {
+                const int4 t = make_int4(x0 / kTile, y0 / kTile, x1 / kTile, y1 / kTile);
+                rect[i] = t;
+                tcount[i] = (t.z - t.x + 1) * (t.w - t.y + 1);
+            }
+        }
+    }
+    // warp-aggregated visible count
+    const unsigned m = __ballot_sync(0xffffffffu, visible);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&status->n_visible, __popc(m));
+}
+
+__global__ void k_project_dump(const double* __restrict__ x, int K, DevCam cam, RenderP ro,
+                               double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const Splat p = load_splat(x, K, i);
+    const Proj<double> pr = project_primal(p, cam, ro);
+    double* o = out + 12LL * i;
+    for (int j = 0; j < 12; ++j) o[j] = 0.0;
+    if (pr.culled || pr.degenerate) {
+        o[0] = 1.0;
+        return;
+    }
+    const double rx = ro.cutoff * sqrt(pr.c00), ry = ro.cutoff * sqrt(pr.c11);
+    double i00, i01, i11;
+    invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
+    o[1] = pr.depth;
+    o[2] = pr.mx;
+    o[3] = pr.my;
+    o[4] = pr.mx - rx;
+    o[5] = pr.mx + rx;
+    o[6] = pr.my - ry;
+    o[7] = pr.my + ry;
+    o[8] = i00;
+    o[9] = i01;
+    o[10] = i11;
+}
+
+__device__ __forceinline__ double probe_at(const double* v, const uint32_t* zbits, long long k) {
+    if (v) return v[k];
+    return ((zbits[k >> 5] >> (k & 31)) & 1u) ? 1.0 : -1.0;
+}
+
+// tangent records along v: build_fragments_dual (render.cpp:91-120)
+__global__ void __launch_bounds__(256) k_project_jvp(const double* __restrict__ x, int K,
+                                                     DevCam cam, RenderP ro,
+                                                     const double* __restrict__ v,
+                                                     const uint32_t* __restrict__ zbits,
+                                                     double* __restrict__ trec) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const Splat p = load_splat(x, K, i);
+    const long long k = K;
+    Dual mu[3], s[3], q[4];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        mu[a] = Dual(p.mu[a], probe_at(v, zbits, 3LL * i + a));
+        s[a] = Dual(p.s[a], probe_at(v, zbits, 3 * k + 3LL * i + a));
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) q[a] = Dual(p.q[a], probe_at(v, zbits, 6 * k + 4LL * i + a));
+    const Proj<Dual> pr = project<Dual>(mu, s, q, cam.w, cam.t, cam.fx, cam.fy, cam.cx, cam.cy,
+                                        ro.z_near, ro.lowpass);
+    if (pr.culled || pr.degenerate) return;  // never referenced by a tile list
+    Dual i00, i01, i11;
+    invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
+    double* o = trec + (long long)kTRec * i;
+    o[T_MX] = pr.mx.d;
+    o[T_MY] = pr.my.d;
+    o[T_I00] = i00.d;
+    o[T_I01] = i01.d;
+    o[T_I11] = i11.d;
+    o[T_ALPHA] = probe_at(v, zbits, 10 * k + i);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) o[T_C0 + a] = probe_at(v, zbits, 11 * k + 3LL * i + a);
+}
+
+// K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
+// the fixed-order sum of its (tile, fragment) slots; the 5x10 Jacobian of
+// (mu2d, inverse covariance) w.r.t. (mu, s, q) is evaluated with the same 10
+// dual seeds the reference uses.
+__global__ void __launch_bounds__(128) k_chain(int mode, const double* __restrict__ x, int K,
+                                               DevCam cam, RenderP ro,
+                                               const int* __restrict__ sorted_ids, int n_visible,
+                                               const long long* __restrict__ off_r,
+                                               const int* __restrict__ tcount,
+                                               const double* __restrict__ slots,
+                                               const double* __restrict__ zdense,
+                                               const uint32_t* __restrict__ zbits,
+                                               double* __restrict__ acc,
+                                               double* nonfinite_flag) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_visible) return;
+    const int id = sorted_ids[r];
+    const int cnt = tcount[id];
+    if (cnt == 0) return;
+    double a[kAdj];
+#pragma unroll
+    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
+    const double* sl = slots + (long long)kAdj * off_r[r];
+    for (int t = 0; t < cnt; ++t) {
+#pragma unroll
+        for (int j = 0; j < kAdj; ++j) a[j] += sl[(long long)kAdj * t + j];
+    }
+    const long long k = K;
+    bool finite = true;
+    auto add = [&](long long idx, double v) {
+        if (mode == 1) v = probe_at(zdense, zbits, idx) * v;
+        finite = finite && isfinite(v);
+        acc[idx] += v;
+    };
+    add(10 * k + id, a[5]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
+    if (any) {
+        const Splat p = load_splat(x, K, id);
+        for (int seed = 0; seed < 10; ++seed) {
+            Dual mu[3], s[3], q[4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                mu[c] = Dual(p.mu[c], seed == c ? 1.0 : 0.0);
+                s[c] = Dual(p.s[c], seed == 3 + c ? 1.0 : 0.0);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) q[c] = Dual(p.q[c], seed == 6 + c ? 1.0 : 0.0);
+            const Proj<Dual> pr = project<Dual>(mu, s, q, cam.w, cam.t, cam.fx, cam.fy, cam.cx,
+                                                cam.cy, ro.z_near, ro.lowpass);
+            if (pr.culled) break;
+            Dual i00, i01, i11;
+            invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
+            const double dot = a[0] * pr.mx.d + a[1] * pr.my.d + a[2] * i00.d +
+                               a[3] * i01.d + a[4] * i11.d;
+            const long long off = seed < 3 ? 3LL * id + seed
+                                           : (seed < 6 ? 3 * k + 3LL * id + (seed - 3)
+                                                       : 6 * k + 4LL * id + (seed - 6));
+            add(off, dot);
+        }
+    }
+    if (!finite) *nonfinite_flag = 1.0;  // idempotent store
+}
+
+}  // namespace
+
+void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                    const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
+                    int4* rect, int* tcount, ViewStatus* status) {
+    if (K == 0) return;
+    k_project<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, rec, keys, ids, rect, tcount,
+                                                 status);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                         const RenderP& ro, double* out) {
+    if (K == 0) return;
+    k_project_dump<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, out);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& cam,
+                        const RenderP& ro, const double* v, const uint32_t* zbits,
+                        double* trec) {
+    if (K == 0) return;
+    k_project_jvp<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, v, zbits, trec);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_chain(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+                  const RenderP& ro, const int* sorted_ids, int n_visible,
+                  const long long* off_r, const int* tcount, const double* slots,
+                  const double* zdense, const uint32_t* zbits, double* acc,
+                  double* nonfinite_flag) {
+    if (n_visible == 0) return;
+    k_chain<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, cam, ro, sorted_ids,
+                                                       n_visible, off_r, tcount, slots, zdense,
+                                                       zbits, acc, nonfinite_flag);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+}  // namespace sgtr

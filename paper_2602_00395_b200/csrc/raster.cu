@@ -1,0 +1,336 @@
+// raster.cu — tile rasteriser: K7 forward blend, K10 reverse-order VJP,
+// K12 forward-mode JVP.
+//
+// One CTA per 16x16 tile, one thread per pixel.  The tile's fragment list
+// (depth order, from binning.cu) is staged through shared memory in batches;
+// each 128-byte fragment record is copied by 8 lanes (one full cache line per
+// record, 4 records per warp instruction), and every pixel then reads the
+// staged record as a warp-wide broadcast.
+//
+// Branch parity: the three kernels evaluate the primal alpha with the same
+// pinned operation sequence (no FMA; identical to the oracle's restatement
+// of render.cpp:132-136), so bbox reject, alpha clamp, alpha skip and the
+// transmittance stop take the same branches in forward, VJP and JVP — the
+// reference's "frozen branches" contract (render.hpp:76-79).
+#include "common.cuh"
+#include "geometry.cuh"
+#include "launch.h"
+
+namespace sgtr {
+namespace {
+
+constexpr int kThreads = kTilePixels;  // 256
+constexpr int kFwdBatch = 256;
+constexpr int kVjpBatch = 64;
+constexpr int kWarps = kThreads / 32;
+
+struct PixelCtx {
+    int px, py;
+    bool inside;
+    double pxc, pyc;
+};
+
+__device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H) {
+    PixelCtx p;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    p.px = tx * kTile + (threadIdx.x & (kTile - 1));
+    p.py = ty * kTile + (threadIdx.x / kTile);
+    p.inside = p.px < W && p.py < H;
+    p.pxc = p.px + 0.5;
+    p.pyc = p.py + 0.5;
+    return p;
+}
+
+// reference: -0.5 * (dx*dx*i00 + dy*dy*i11) - dx*dy*i01  (render.cpp:134-135)
+__device__ __forceinline__ double eval_expo(double dx, double dy, const double* f) {
+    const double a = __dmul_rn(__dmul_rn(dx, dx), f[R_I00]);
+    const double b = __dmul_rn(__dmul_rn(dy, dy), f[R_I11]);
+    const double c = __dmul_rn(__dmul_rn(dx, dy), f[R_I01]);
+    return __dsub_rn(__dmul_rn(-0.5, __dadd_rn(a, b)), c);
+}
+
+__device__ __forceinline__ bool outside_bbox(double pxc, double pyc, const double* f) {
+    return pxc < f[R_BX0] || pxc > f[R_BX1] || pyc < f[R_BY0] || pyc > f[R_BY1];
+}
+
+// cooperative staging: 8 lanes per 128-byte record; entries [b, b+n) of the
+// tile-sorted list go to s_rec[0, n)
+__device__ __forceinline__ void stage_records(const TileLists& tl, const double* __restrict__ rec,
+                                              int b, int n, double* s_rec, int* s_d) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane >> 3, chunk = lane & 7;
+    for (int e = warp * 4 + sub; e < n; e += kWarps * 4) {
+        const int d = tl.sorted_d[b + e];
+        const int id = tl.dup_id[d];
+        const double2 v = reinterpret_cast<const double2*>(rec + (long long)kRec * id)[chunk];
+        reinterpret_cast<double2*>(s_rec + kRec * e)[chunk] = v;
+        if (s_d && chunk == 0) s_d[e] = d;
+    }
+}
+
+__device__ __forceinline__ void stage_tangents(const TileLists& tl, const double* __restrict__ trec,
+                                               int b, int n, double* s_t) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane >> 3, chunk = lane & 7;
+    for (int e = warp * 4 + sub; e < n; e += kWarps * 4) {
+        if (chunk >= kTRec / 2) continue;
+        const int id = tl.dup_id[tl.sorted_d[b + e]];
+        const double2 v = reinterpret_cast<const double2*>(trec + (long long)kTRec * id)[chunk];
+        reinterpret_cast<double2*>(s_t + kTRec * e)[chunk] = v;
+    }
+}
+
+// ------------------------------------------------------------------ K7
+__global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
+                                                         const double* __restrict__ rec, int W,
+                                                         int H, RenderP ro,
+                                                         double* __restrict__ img,
+                                                         double* __restrict__ tfinal,
+                                                         int* __restrict__ last) {
+    __shared__ __align__(16) double s_rec[kFwdBatch * kRec];
+    const int tile = blockIdx.x;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool done = !pc.inside;
+    int processed = end - start;
+    for (int b = start; b < end; b += kFwdBatch) {
+        if (__syncthreads_and(done)) break;
+        const int n = min(kFwdBatch, end - b);
+        stage_records(tl, rec, b, n, s_rec, nullptr);
+        __syncthreads();
+        if (!done) {
+            for (int jj = 0; jj < n; ++jj) {
+                const double* f = s_rec + kRec * jj;
+                if (outside_bbox(pc.pxc, pc.pyc, f)) continue;
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+                if (abar < ro.alpha_skip) continue;
+                const double w = abar * T;
+                c0 += f[R_C0] * w;
+                c1 += f[R_C1] * w;
+                c2 += f[R_C2] * w;
+                T = __dmul_rn(T, __dsub_rn(1.0, abar));
+                if (T < ro.t_stop) {
+                    done = true;
+                    processed = b - start + jj + 1;
+                    break;
+                }
+            }
+        }
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    img[p] = c0 + ro.bg[0] * T;
+    img[P + p] = c1 + ro.bg[1] * T;
+    img[2 * P + p] = c2 + ro.bg[2] * T;
+    tfinal[p] = T;
+    last[p] = processed;
+}
+
+// ------------------------------------------------------------------ K10
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
+                                                         const double* __restrict__ rec, int W,
+                                                         int H, RenderP ro,
+                                                         const double* __restrict__ adj,
+                                                         const double* __restrict__ tfinal,
+                                                         const int* __restrict__ last,
+                                                         double* __restrict__ slots) {
+    __shared__ __align__(16) double s_rec[kVjpBatch * kRec];
+    __shared__ double s_red[kWarps][kVjpBatch][kAdj];
+    __shared__ int s_d[kVjpBatch];
+    __shared__ int s_maxlast[kWarps];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
+    int lastp = 0;
+    if (pc.inside) {
+        u0 = adj[p];
+        u1 = adj[P + p];
+        u2 = adj[2 * P + p];
+        T = tfinal[p];
+        lastp = last[p];
+    }
+    // pixels with an all-zero adjoint are skipped (render.cpp:283)
+    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
+    if (!active) lastp = 0;
+    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;  // "behind"
+    // entries past every pixel's last processed fragment get zero slots
+    int ml = __reduce_max_sync(0xffffffffu, lastp);
+    if (lane == 0) s_maxlast[warp] = ml;
+    __syncthreads();
+    ml = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) ml = max(ml, s_maxlast[w]);
+    const int hi = start + ml;
+    for (int j = hi + threadIdx.x; j < end; j += kThreads) {
+        double* s = slots + (long long)kAdj * tl.sorted_d[j];
+#pragma unroll
+        for (int c = 0; c < kAdj; ++c) s[c] = 0.0;
+    }
+    for (int bend = hi; bend > start; bend -= kVjpBatch) {
+        const int bstart = max(start, bend - kVjpBatch);
+        const int n = bend - bstart;
+        __syncthreads();
+        stage_records(tl, rec, bstart, n, s_rec, s_d);
+        __syncthreads();
+        for (int jj = n - 1; jj >= 0; --jj) {
+            const double* f = s_rec + kRec * jj;
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            if (bstart - start + jj < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                const double gauss = exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], gauss);
+                const bool clamped = abar >= ro.alpha_clamp;
+                if (clamped) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    contrib = true;
+                    const double om = __dsub_rn(1.0, abar);
+                    const double t_in = T / om;
+                    const double at = abar * t_in;
+                    g[6] = u0 * at;
+                    g[7] = u1 * at;
+                    g[8] = u2 * at;
+                    const double dab = u0 * (f[R_C0] * t_in - b0 / om) +
+                                       u1 * (f[R_C1] * t_in - b1 / om) +
+                                       u2 * (f[R_C2] * t_in - b2 / om);
+                    b0 += f[R_C0] * at;
+                    b1 += f[R_C1] * at;
+                    b2 += f[R_C2] * at;
+                    if (!clamped) {
+                        g[5] = gauss * dab;
+                        const double de = abar * dab;
+                        g[2] = de * (-0.5 * dx * dx);
+                        g[3] = de * (-dx * dy);
+                        g[4] = de * (-0.5 * dy * dy);
+                        g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
+                        g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
+                    }
+                    T = t_in;
+                }
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+#pragma unroll
+                for (int c = 0; c < kAdj; ++c) g[c] = warp_sum(g[c]);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int c = 0; c < kAdj; ++c) s_red[warp][jj][c] = g[c];
+            }
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < n * kAdj; idx += kThreads) {
+            const int jj = idx / kAdj, c = idx % kAdj;
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s += s_red[w][jj][c];
+            slots[(long long)kAdj * s_d[jj] + c] = s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K12 (raster)
+__global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
+                                                         const double* __restrict__ rec,
+                                                         const double* __restrict__ trec, int W,
+                                                         int H, RenderP ro,
+                                                         double* __restrict__ tangent) {
+    constexpr int kB = 128;
+    __shared__ __align__(16) double s_rec[kB * kRec];
+    __shared__ __align__(16) double s_t[kB * kTRec];
+    const int tile = blockIdx.x;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0;
+    Dual Td(1.0, 0.0);
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    bool done = !pc.inside;
+    for (int b = start; b < end; b += kB) {
+        if (__syncthreads_and(done)) break;
+        const int n = min(kB, end - b);
+        stage_records(tl, rec, b, n, s_rec, nullptr);
+        stage_tangents(tl, trec, b, n, s_t);
+        __syncthreads();
+        if (!done) {
+            for (int jj = 0; jj < n; ++jj) {
+                const double* f = s_rec + kRec * jj;
+                if (outside_bbox(pc.pxc, pc.pyc, f)) continue;
+                const double* t = s_t + kTRec * jj;
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                const double e = exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], e);
+                // tangent of the same expression (dual.hpp semantics)
+                const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
+                const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
+                    I11(f[R_I11], t[T_I11]);
+                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
+                double dabar = t[T_ALPHA] * e + f[R_ALPHA] * (e * ex.d);
+                if (abar >= ro.alpha_clamp) {
+                    abar = ro.alpha_clamp;
+                    dabar = 0.0;
+                }
+                if (abar < ro.alpha_skip) continue;
+                // w = abar * T ; acc += c * w ; T = T * (1 - abar)
+                const double w = abar * T;
+                const double dw = dabar * T + abar * Td.d;
+                d0 += t[T_C0] * w + f[R_C0] * dw;
+                d1 += t[T_C1] * w + f[R_C1] * dw;
+                d2 += t[T_C2] * w + f[R_C2] * dw;
+                const double om = __dsub_rn(1.0, abar);
+                Td.d = Td.d * om + T * (-dabar);
+                T = __dmul_rn(T, om);
+                if (T < ro.t_stop) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    tangent[p] = d0 + ro.bg[0] * Td.d;
+    tangent[P + p] = d1 + ro.bg[1] * Td.d;
+    tangent[2 * P + p] = d2 + ro.bg[2] * Td.d;
+}
+
+}  // namespace
+
+void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
+                       const RenderP& ro, double* img, double* tfinal, int* last) {
+    const int n = tl.tiles_x * tl.tiles_y;
+    if (n == 0) return;
+    k_raster_fwd<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
+                       const RenderP& ro, const double* adj, const double* tfinal,
+                       const int* last, double* slots) {
+    const int n = tl.tiles_x * tl.tiles_y;
+    if (n == 0) return;
+    k_raster_vjp<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
+                       const double* trec, int W, int H, const RenderP& ro, double* tangent) {
+    const int n = tl.tiles_x * tl.tiles_y;
+    if (n == 0) return;
+    k_raster_jvp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+}  // namespace sgtr

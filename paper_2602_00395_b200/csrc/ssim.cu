@@ -1,0 +1,385 @@
+// ssim.cu — K8 SSIM + residual + residual-VJP fields, K13 (its JVP form),
+// K9 reflection-aware transposed-window gather.
+//
+// The reference evaluates SSIM with a direct 121-tap gather per pixel and
+// its adjoint as a 121-tap scatter (ssim.cpp:60-168), single-threaded.  The
+// window weight is k[dy]*k[dx] and the reflection is per axis, so both are
+// separable: K8 runs a horizontal then a vertical 11-tap pass over a tile
+// staged in shared memory with a 5-pixel reflected halo, and K9 turns the
+// scatter into a gather: with P = u*dS/dmu_a, Q = 2u*dS/dmaa, R = u*dS/dmab
+// at each window centre,
+//     grad[p] = (W^T P)[p] + a[p] (W^T Q)[p] + b[p] (W^T R)[p]
+// where per axis (W^T X)(p) = B0(p) + [1<=p<=5] B0(-p)
+//                              + [n-6<=p<=n-2] B0(2n-2-p)
+// and B0(i) = sum_d k[d] X[i+d] with zero padding (k is symmetric), i.e. the
+// preimages of p under reflect() over [-5, n+4].
+//
+// Images are planar (3, H, W); for a planar image the residual block index
+// c*H*W + y*W + x (residuals.cpp:19-22) is the plane index itself.
+#include <cmath>
+
+#include "common.cuh"
+#include "geometry.cuh"
+#include "launch.h"
+
+namespace sgtr {
+namespace {
+
+constexpr int TX = 32, TY = 8, HALO = 5;
+constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 18
+constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
+
+__constant__ double c_k[11];
+
+__device__ __forceinline__ int reflect(int i, int n) {
+    if (i < 0) return -i;
+    if (i >= n) return 2 * n - 2 - i;
+    return i;
+}
+
+__device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+template <int MODE>
+struct ModeTraits {
+    static constexpr bool kTangent = MODE == SSIM_JVP || MODE == RES_JVP || MODE == HUTCH;
+    static constexpr int kMoments = kTangent ? 8 : 5;
+};
+
+// moments: 0 mu_a, 1 mu_b, 2 maa, 3 mbb, 4 mab, (5 dmu_a, 6 dmaa, 7 dmab)
+template <int MODE>
+__global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
+    using Tr = ModeTraits<MODE>;
+    constexpr int NM = Tr::kMoments;
+    extern __shared__ __align__(16) double smem[];
+    double* s_a = smem;                      // SY x SX
+    double* s_b = s_a + SY * SX;
+    double* s_da = s_b + SY * SX;            // (tangent modes)
+    double* s_h = s_da + (Tr::kTangent ? SY * SX : 0);  // NM x SY x TX
+    const int W = args.W, H = args.H;
+    const long long P = (long long)W * H;
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const double* A = args.a + c * P;
+    const double* B = args.b + c * P;
+    const double* DA = Tr::kTangent ? args.da + c * P : nullptr;
+    for (int i = threadIdx.x; i < SY * SX; i += TX * TY) {
+        const int sy = i / SX, sx = i % SX;
+        const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
+        double va = 0.0, vb = 0.0, vd = 0.0;
+        if (gy <= H - 1 + HALO && gx <= W - 1 + HALO) {
+            const long long q = (long long)reflect(gy, H) * W + reflect(gx, W);
+            va = A[q];
+            vb = B[q];
+            if (Tr::kTangent) vd = DA[q];
+        }
+        s_a[i] = va;
+        s_b[i] = vb;
+        if (Tr::kTangent) s_da[i] = vd;
+    }
+    __syncthreads();
+    // horizontal pass over all SY rows
+    for (int i = threadIdx.x; i < SY * TX; i += TX * TY) {
+        const int sy = i / TX, tx = i % TX;
+        double m[NM];
+#pragma unroll
+        for (int j = 0; j < NM; ++j) m[j] = 0.0;
+#pragma unroll
+        for (int d = 0; d < 11; ++d) {
+            const int si = sy * SX + tx + d;
+            const double w = c_k[d], av = s_a[si], bv = s_b[si];
+            m[0] += w * av;
+            m[1] += w * bv;
+            m[2] += w * av * av;
+            m[3] += w * bv * bv;
+            m[4] += w * av * bv;
+            if (Tr::kTangent) {
+                const double dv = s_da[si];
+                m[5] += w * dv;
+                m[6] += w * 2.0 * av * dv;
+                m[7] += w * bv * dv;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TX + tx] = m[j];
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    const int gx = x0 + tx, gy = y0 + ty;
+    double m[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) m[j] = 0.0;
+#pragma unroll
+    for (int d = 0; d < 11; ++d) {
+        const double w = c_k[d];
+#pragma unroll
+        for (int j = 0; j < NM; ++j) m[j] += w * s_h[(j * SY + ty + d) * TX + tx];
+    }
+    double partial = 0.0;
+    if (gx < W && gy < H) {
+        const long long p = (long long)gy * W + gx;
+        const long long pi = c * P + p;
+        // SSIM with its tangent (ssim.cpp:50-58 with Dual a)
+        const Dual mu_a(m[0], Tr::kTangent ? m[5] : 0.0);
+        const Dual maa(m[2], Tr::kTangent ? m[6] : 0.0);
+        const Dual mab(m[4], Tr::kTangent ? m[7] : 0.0);
+        const double mu_b = m[1], mbb = m[3];
+        const Dual n1 = 2.0 * mu_a * mu_b + kC1;
+        const Dual d1 = mu_a * mu_a + mu_b * mu_b + kC1;
+        const Dual n2 = 2.0 * (mab - mu_a * mu_b) + kC2;
+        const Dual d2 = (maa - mu_a * mu_a) + (mbb - mu_b * mu_b) + kC2;
+        const Dual s = (n1 * n2) / (d1 * d2);
+        const double av = s_a[(ty + HALO) * SX + tx + HALO];
+        const double bv = s_b[(ty + HALO) * SX + tx + HALO];
+        const double diff = av - bv;
+        const double lam = args.lambda, fl = args.floor;
+        const double u1 = (1.0 - lam) * fabs(diff);
+        const double u2 = lam * (1.0 - s.v) / 2.0;
+        if (MODE == SSIM_MAP) {
+            args.out0[pi] = s.v;
+        } else if (MODE == SSIM_JVP) {
+            args.out0[pi] = s.v;
+            args.out1[pi] = s.d;
+        } else if (MODE == RES_VEC) {
+            args.out0[pi] = sqrt(fmax(u1, fl));
+            args.out0[3 * P + pi] = sqrt(fmax(u2, fl));
+        } else if (MODE == RES_JVP) {
+            const double t = s_da[(ty + HALO) * SX + tx + HALO];
+            args.out0[pi] = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
+            args.out0[3 * P + pi] = u2 > fl ? -lam * s.d / (4.0 * sqrt(u2)) : 0.0;
+        } else {
+            // image-space adjoint of the residual chain (residuals.cpp:81-117)
+            double ur1, ur2;  // residual-space upstream for this entry
+            if (MODE == GRAD) {
+                ur1 = sqrt(fmax(u1, fl));
+                ur2 = sqrt(fmax(u2, fl));
+                partial = ur1 * ur1 + ur2 * ur2;
+            } else if (MODE == HUTCH) {
+                const double t = s_da[(ty + HALO) * SX + tx + HALO];
+                ur1 = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
+                ur2 = u2 > fl ? -lam * s.d / (4.0 * sqrt(u2)) : 0.0;
+            } else if (MODE == RES_VJP) {
+                ur1 = args.u[pi];
+                ur2 = args.u[3 * P + pi];
+            } else {  // SSIM_VJP
+                ur1 = 0.0;
+                ur2 = 0.0;
+            }
+            double up;
+            if (MODE == SSIM_VJP) {
+                up = args.u[pi];
+            } else {
+                args.adjl1[pi] = u1 > fl ? ur1 * (1.0 - lam) * sgn(diff) / (2.0 * sqrt(u1)) : 0.0;
+                up = u2 > fl ? ur2 * (-lam / (4.0 * sqrt(u2))) : 0.0;
+            }
+            // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155)
+            const double pp = n1.v / d1.v, qq = n2.v / d2.v;
+            const double ds_dmu = qq * (2.0 * mu_b * d1.v - 2.0 * mu_a.v * n1.v) / (d1.v * d1.v) +
+                                  pp * (2.0 * mu_a.v * n2.v - 2.0 * mu_b * d2.v) / (d2.v * d2.v);
+            const double ds_dmaa = -pp * n2.v / (d2.v * d2.v);
+            const double ds_dmab = pp * 2.0 / d2.v;
+            args.P[pi] = up * ds_dmu;
+            args.Q[pi] = up * ds_dmaa * 2.0;
+            args.R[pi] = up * ds_dmab;
+        }
+    }
+    if (MODE == GRAD) {
+        // deterministic block sum -> one partial per block
+        __shared__ double s_red[TX * TY / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) partial += __shfl_xor_sync(0xffffffffu, partial, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = partial;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < TX * TY / 32; ++w) t += s_red[w];
+            const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            args.loss_partials[blk] = t;
+        }
+    }
+}
+
+// per-axis transposed window: sum over preimages i of p of B0(i)
+template <typename Ld>
+__device__ __forceinline__ double transposed_1d(int p, int n, Ld ld) {
+    auto b0 = [&](int i) {
+        double s = 0.0;
+#pragma unroll
+        for (int d = -HALO; d <= HALO; ++d) {
+            const int q = i + d;
+            if (q >= 0 && q < n) s += c_k[d + HALO] * ld(q);
+        }
+        return s;
+    };
+    double t = b0(p);
+    if (p >= 1 && p <= HALO) t += b0(-p);
+    if (p >= n - 6 && p <= n - 2) t += b0(2 * n - 2 - p);
+    return t;
+}
+
+__global__ void __launch_bounds__(TX* TY) k_gather(int W, int H, const double* __restrict__ a,
+                                                   const double* __restrict__ b,
+                                                   const double* __restrict__ adjl1,
+                                                   const double* __restrict__ Pf,
+                                                   const double* __restrict__ Qf,
+                                                   const double* __restrict__ Rf,
+                                                   double* __restrict__ adj) {
+    __shared__ double s_f[3][SY][SX];
+    __shared__ double s_h[3][SY][TX];
+    const long long P = (long long)W * H;
+    const int c = blockIdx.z;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    for (int i = threadIdx.x; i < SY * SX; i += TX * TY) {
+        const int sy = i / SX, sx = i % SX;
+        const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
+        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+        const long long q = c * P + (long long)gy * W + gx;
+        s_f[0][sy][sx] = in ? Pf[q] : 0.0;
+        s_f[1][sy][sx] = in ? Qf[q] : 0.0;
+        s_f[2][sy][sx] = in ? Rf[q] : 0.0;
+    }
+    __syncthreads();
+    // horizontal transposed pass for every staged row
+    for (int i = threadIdx.x; i < SY * TX; i += TX * TY) {
+        const int sy = i / TX, tx = i % TX;
+        const int gx = x0 + tx;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            s_h[f][sy][tx] = gx < W ? transposed_1d(gx, W, [&](int q) {
+                return s_f[f][sy][q - x0 + HALO];
+            })
+                                    : 0.0;
+        }
+    }
+    __syncthreads();
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    const int gx = x0 + tx, gy = y0 + ty;
+    if (gx >= W || gy >= H) return;
+    double t[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+        t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
+    const long long p = c * P + (long long)gy * W + gx;
+    const double base = adjl1 ? adjl1[p] : 0.0;
+    adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partials, int n, double* out) {
+    __shared__ double s[256];
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) t += partials[i];
+    s[threadIdx.x] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r = 0.0;
+        for (int i = 0; i < 256; ++i) r += s[i];
+        *out = r;
+    }
+}
+
+__global__ void k_to_planar(const double* __restrict__ in, int P, double* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[(long long)c * P + p] = in[3LL * p + c];
+}
+
+__global__ void k_to_interleaved(const double* __restrict__ in, int P, double* __restrict__ out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[3LL * p + c] = in[(long long)c * P + p];
+}
+
+// image.cpp:13-20
+__global__ void k_quantize8(double* img, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = img[i];
+    const double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    img[i] = round(c * 255.0) / 255.0;
+}
+
+bool g_kernel_ready = false;
+
+void init_constants() {
+    if (g_kernel_ready) return;
+    // kernel1d (ssim.cpp:21-34), computed on the host exactly as the oracle
+    double k[11], sum = 0.0;
+    for (int i = 0; i < 11; ++i) {
+        const double d = i - 5;
+        k[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        sum += k[i];
+    }
+    for (double& v : k) v /= sum;
+    SGTR_CUDA(cudaMemcpyToSymbol(c_k, k, sizeof(k)));
+    g_kernel_ready = true;
+}
+
+template <int MODE>
+void run_ssim(cudaStream_t st, const SsimArgs& a) {
+    using Tr = ModeTraits<MODE>;
+    const size_t smem = sizeof(double) * (SY * SX * (Tr::kTangent ? 3 : 2) +
+                                          Tr::kMoments * SY * TX);
+    static bool attr = false;
+    if (!attr) {
+        SGTR_CUDA(cudaFuncSetAttribute(k_ssim<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        attr = true;
+    }
+    dim3 grid(ceil_div(a.W, TX), ceil_div(a.H, TY), 3);
+    k_ssim<MODE><<<grid, TX * TY, smem, st>>>(a);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+int ssim_num_blocks(int W, int H) { return ceil_div(W, TX) * ceil_div(H, TY) * 3; }
+
+void launch_ssim(cudaStream_t st, const SsimArgs& a) {
+    init_constants();
+    switch (a.mode) {
+        case SSIM_MAP: run_ssim<SSIM_MAP>(st, a); break;
+        case SSIM_JVP: run_ssim<SSIM_JVP>(st, a); break;
+        case RES_VEC: run_ssim<RES_VEC>(st, a); break;
+        case RES_JVP: run_ssim<RES_JVP>(st, a); break;
+        case GRAD: run_ssim<GRAD>(st, a); break;
+        case HUTCH: run_ssim<HUTCH>(st, a); break;
+        case RES_VJP: run_ssim<RES_VJP>(st, a); break;
+        case SSIM_VJP: run_ssim<SSIM_VJP>(st, a); break;
+        default: throw Error(SGTR_RUNTIME, "launch_ssim: bad mode");
+    }
+}
+
+void launch_ssim_gather(cudaStream_t st, int W, int H, const double* a, const double* b,
+                        const double* adjl1, const double* P, const double* Q, const double* R,
+                        double* adj) {
+    init_constants();
+    dim3 grid(ceil_div(W, TX), ceil_div(H, TY), 3);
+    k_gather<<<grid, TX * TY, 0, st>>>(W, H, a, b, adjl1, P, Q, R, adj);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_sum_partials(cudaStream_t st, const double* partials, int n, double* out) {
+    k_sum_partials<<<1, 256, 0, st>>>(partials, n, out);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_to_planar(cudaStream_t st, const double* in, int P, double* out) {
+    if (P == 0) return;
+    k_to_planar<<<ceil_div(P, 256), 256, 0, st>>>(in, P, out);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_to_interleaved(cudaStream_t st, const double* in, int P, double* out) {
+    if (P == 0) return;
+    k_to_interleaved<<<ceil_div(P, 256), 256, 0, st>>>(in, P, out);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_quantize8(cudaStream_t st, double* img, long long n) {
+    if (n == 0) return;
+    k_quantize8<<<ceil_div(n, 256), 256, 0, st>>>(img, n);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+}  // namespace sgtr

@@ -1,0 +1,354 @@
+"""GPU parity: libsgtr.so (through the C-ABI) against the CPU oracle.
+
+Tolerances are the north star's (BASELINE.json): sort order and tile lists
+bit-exact; images, JVP tangents, Hessian diagonals 1e-4 relative; accumulated
+gradients 1e-3 relative.  Relative error is max|a-b| / max|b|.
+The projection records are additionally checked bit-for-bit, because the
+binning's exactness rests on them.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2602_00395_b200 import splat
+    return splat
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-30))
+
+
+def cams_of(sp, orc_cams, gts=None):
+    gts = gts or [None] * len(orc_cams)
+    return [sp.Camera.from_c(c, g) for c, g in zip(orc_cams, gts)]
+
+
+def axis_camera(sp, size=16):  # test_render.cpp:20-28
+    return sp.Camera(0, 2.0 * size, 2.0 * size, size / 2.0 - 0.5, size / 2.0 - 0.5, size, size)
+
+
+def centered_scene(sp, prims):  # test_render.cpp:30-38
+    return sp.Scene.from_primitives([[0, 0, 1]] * len(prims), [[0.05] * 3] * len(prims),
+                                    [[0, 0, 0, 1]] * len(prims), [p[0] for p in prims],
+                                    [p[1] for p in prims])
+
+
+# ------------------------------------------------------------------ reference KATs on the GPU
+def test_single_splat_center(sp):  # test_render.cpp:42-54
+    cam = axis_camera(sp)
+    out = sp.rasterize(centered_scene(sp, [(0.8, [1, 0, 0])]), cam)
+    px = py = int(cam.cx)
+    assert out.color[py, px, 0] == pytest.approx(0.8, rel=1e-12)
+    assert out.color[py, px, 1] == 0.0 and out.color[py, px, 2] == 0.0
+    assert out.t_final[py, px] == pytest.approx(0.2, rel=1e-12)
+
+
+def test_coincident_tie_by_index(sp):  # test_render.cpp:56-65
+    cam = axis_camera(sp)
+    out = sp.rasterize(centered_scene(sp, [(0.5, [1, 1, 1]), (0.5, [0, 0, 0])]), cam)
+    assert out.color[int(cam.cy), int(cam.cx), 0] == pytest.approx(0.5, rel=1e-12)
+
+
+def test_empty_scene(sp):  # test_render.cpp:67-79
+    cam = axis_camera(sp, 8)
+    out = sp.rasterize(sp.Scene(np.zeros(0)), cam, sp.RenderOptions(background=(0.25, 0.5, 0.75)))
+    assert np.all(out.color[..., 0] == 0.25) and np.all(out.color[..., 2] == 0.75)
+    assert np.all(out.t_final == 1.0)
+
+
+def test_nonfinite_names_splat(sp):  # test_render.cpp:81-89
+    s = centered_scene(sp, [(0.5, [1, 1, 1])] * 2)
+    s.x[3 * 1 + 2] = np.inf
+    with pytest.raises(sp.NumericError, match="splat 1"):
+        sp.rasterize(s, axis_camera(sp, 8))
+
+
+def test_vjp_zero_and_color(sp):  # test_render.cpp:161-178
+    cam = axis_camera(sp)
+    s = centered_scene(sp, [(0.3, [0.2, 0.9, 0.4])])
+    adj = np.zeros((16, 16, 3))
+    assert np.linalg.norm(sp.rasterize_vjp(s, cam, adj)) == 0.0
+    adj[int(cam.cy), int(cam.cx), 1] = 1.0
+    g = sp.rasterize_vjp(s, cam, adj)
+    assert g[s.color_offset() + 1] == pytest.approx(0.3, rel=1e-12)
+    assert g[s.color_offset()] == 0.0
+
+
+def test_storage_order_bitwise(sp, orc):  # test_render.cpp:91-100
+    x, cams, _ = orc.make_check_scene(10, 16, 1, 42)
+    mu, s, q, a, c = orc.unpack(x)
+    xr = orc.pack(mu[::-1], s[::-1], q[::-1], a[::-1], c[::-1])
+    cam = cams_of(sp, cams)[0]
+    assert np.array_equal(sp.rasterize(sp.Scene(x), cam).color,
+                          sp.rasterize(sp.Scene(xr), cam).color)
+
+
+def test_jvp_zero_and_dead(sp, orc):  # test_render.cpp:114-132
+    x, ocams, _ = orc.make_check_scene(6, 16, 1, 3)
+    cam = cams_of(sp, ocams)[0]
+    assert np.all(sp.rasterize_jvp(sp.Scene(x), cam, np.zeros_like(x)) == 0.0)
+    mu, s, q, a, c = orc.unpack(x)
+    behind = cam.center() - cam.rotation()[2]
+    x2 = orc.pack(np.vstack([mu, behind]), np.vstack([s, s[0]]), np.vstack([q, q[0]]),
+                  np.append(a, a[0]), np.vstack([c, c[0]]))
+    k = x2.size // 14
+    v = np.zeros_like(x2)
+    v[11 * k + 3 * (k - 1)] = 1.0
+    assert np.all(sp.rasterize_jvp(sp.Scene(x2), cam, v) == 0.0)
+
+
+# ------------------------------------------------------------------ bit-exact stages
+@pytest.fixture(scope="module")
+def c1(orc):
+    """BASELINE config 1: 10K splats, 4 views at 128x128 (reference generator)."""
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=10000, init_splats=10000, views=4,
+                                            image_size=128, seed=1))
+    return ds
+
+
+def test_projection_bitexact(sp, orc, c1):
+    ctx = sp.default_context()
+    import ctypes as C
+    from paper_2602_00395_b200 import _lib
+    for x in (c1.gt_x, c1.init_x):
+        ctx.set_scene(x)
+        for oc in c1.cams:
+            cam = sp.Camera.from_c(oc)
+            out = np.empty((x.size // 14, 12))
+            _lib.check(_lib.lib().sgtr_project(ctx.handle, C.byref(cam._c()),
+                                               C.byref(sp.RenderOptions()._c()),
+                                               out.ctypes.data_as(C.c_void_p)))
+            ref = orc.project(x, oc)
+            assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+
+
+def _gpu_binning(sp, x, cam):
+    import ctypes as C
+    from paper_2602_00395_b200 import _lib
+    ctx = sp.default_context()
+    ctx.set_scene(x)
+    nv, nd = C.c_int32(), C.c_int64()
+    L = _lib.lib()
+    ro = sp.RenderOptions()._c()
+    _lib.check(L.sgtr_dump_binning(ctx.handle, C.byref(cam._c()), C.byref(ro), C.byref(nv),
+                                   None, C.byref(nd), None, None, None))
+    nt = ((cam.width + 15) // 16) * ((cam.height + 15) // 16)
+    order = np.empty(nv.value, np.int32)
+    ts, te = np.empty(nt, np.int64), np.empty(nt, np.int64)
+    lists = np.empty(nd.value, np.int32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    _lib.check(L.sgtr_dump_binning(ctx.handle, C.byref(cam._c()), C.byref(ro), C.byref(nv),
+                                   p(order), C.byref(nd), p(ts), p(te), p(lists)))
+    return order, ts, te, lists
+
+
+@pytest.mark.parametrize("which", ["gt", "init"])
+def test_binning_bitexact(sp, orc, c1, which):
+    x = c1.gt_x if which == "gt" else c1.init_x
+    for oc in c1.cams:
+        g = _gpu_binning(sp, x, sp.Camera.from_c(oc))
+        r = orc.binning(x, oc)
+        for a, b in zip(g, r):
+            assert np.array_equal(a, b)
+
+
+def test_binning_edge_cases(sp, orc):
+    # splats straddling the image border, behind the camera, between pixel
+    # centres, and non-square images with partial tiles
+    rng = np.random.default_rng(5)
+    k = 400
+    mu = np.column_stack([rng.uniform(-1.2, 1.2, k), rng.uniform(-1.2, 1.2, k),
+                          rng.uniform(-0.5, 3.0, k)])
+    s = np.exp(rng.uniform(np.log(0.002), np.log(0.3), (k, 3)))
+    q = rng.normal(size=(k, 4))
+    x = orc.pack(mu, s, q, rng.uniform(0.1, 0.9, k), rng.uniform(0, 1, (k, 3)))
+    for w, h in ((37, 23), (16, 16), (100, 7)):
+        oc = orc.camera(width=w, height=h, fx=1.5 * h, fy=1.5 * h, cx=w / 2.0, cy=h / 2.0)
+        g = _gpu_binning(sp, x, sp.Camera.from_c(oc))
+        r = orc.binning(x, oc)
+        for a, b in zip(g, r):
+            assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ renderer parity
+def test_rasterize_parity(sp, orc, c1):
+    for x in (c1.gt_x, c1.init_x):
+        for oc in c1.cams:
+            img, t = orc.rasterize(x, oc)
+            out = sp.rasterize(sp.Scene(x), sp.Camera.from_c(oc))
+            assert rel(out.color, img) < IMG_TOL
+            assert rel(out.t_final, t) < IMG_TOL
+
+
+def test_render_targets_match_oracle_gt(sp, orc, c1):
+    # dataset.cpp:63: quantize8(rasterize(gt)) — GPU render of the targets
+    ctx = sp.Context()
+    ctx.set_scene(c1.gt_x)
+    ctx.set_cameras(c1.cams)
+    ctx.render_targets()
+    for i, g in enumerate(c1.gts):
+        got = ctx.get_target(i, 128, 128)
+        assert np.mean(got != g) < 1e-4  # quantization-boundary flips only
+
+
+def test_jvp_parity_and_adjoint(sp, orc):
+    x, ocams, gts = orc.make_check_scene(8, 16, 2, 1)
+    rng = np.random.default_rng(17)
+    for oc in ocams:
+        cam = sp.Camera.from_c(oc)
+        for _ in range(3):
+            v = rng.normal(size=x.size)
+            u = rng.normal(size=(16, 16, 3))
+            jv = sp.rasterize_jvp(sp.Scene(x), cam, v)
+            assert rel(jv, orc.rasterize_jvp(x, oc, v)) < IMG_TOL
+            vj = sp.rasterize_vjp(sp.Scene(x), cam, u)
+            assert rel(vj, orc.rasterize_vjp(x, oc, u)) < GRAD_TOL
+            lhs, rhs = float(np.sum(u * jv)), float(vj @ v)
+            assert abs(lhs - rhs) <= 1e-9 * (1 + abs(lhs))  # test_render.cpp:180-208
+
+
+def test_jvp_vjp_parity_c1(sp, orc, c1):
+    rng = np.random.default_rng(3)
+    x = c1.init_x
+    oc = c1.cams[1]
+    cam = sp.Camera.from_c(oc)
+    v = rng.normal(size=x.size)
+    u = rng.normal(size=(128, 128, 3))
+    assert rel(sp.rasterize_jvp(sp.Scene(x), cam, v), orc.rasterize_jvp(x, oc, v)) < IMG_TOL
+    assert rel(sp.rasterize_vjp(sp.Scene(x), cam, u), orc.rasterize_vjp(x, oc, u)) < GRAD_TOL
+
+
+# ------------------------------------------------------------------ SSIM / residual parity
+def test_ssim_residual_parity(sp, orc):
+    rng = np.random.default_rng(9)
+    for (w, h) in ((16, 16), (20, 14), (37, 6), (130, 67)):
+        a, b = rng.uniform(size=(h, w, 3)), rng.uniform(size=(h, w, 3))
+        da, up = rng.uniform(-1, 1, (h, w, 3)), rng.uniform(-1, 1, (h, w, 3))
+        assert rel(sp.ssim_map(a, b), orc.ssim_map(a, b)) < 1e-12
+        s, ds = sp.ssim_jvp(a, da, b)
+        so, dso = orc.ssim_jvp(a, da, b)
+        assert rel(s, so) < 1e-12 and rel(ds, dso) < 1e-10
+        assert rel(sp.ssim_vjp(a, b, up), orc.ssim_vjp(a, b, up)) < 1e-10
+        assert rel(sp.residual_vector(a, b), orc.residual_vector(a, b)) < 1e-12
+        assert rel(sp.residual_jvp(a, da, b), orc.residual_jvp(a, da, b)) < 1e-10
+        u = rng.normal(size=6 * w * h)
+        assert rel(sp.residual_vjp(a, b, u), orc.residual_vjp(a, b, u)) < 1e-10
+
+
+def test_ssim_small_image_rejected(sp):
+    with pytest.raises(sp.InvalidArgument, match="smaller than the window"):
+        sp.ssim_map(np.zeros((5, 8, 3)), np.zeros((5, 8, 3)))
+
+
+# ------------------------------------------------------------------ optimizer parity
+def test_stochastic_gradient_parity(sp, orc, c1):
+    views = cams_of(sp, c1.cams, c1.gts)
+    for batch in ([0], [2, 1], [0, 1, 2, 3]):
+        g, loss = sp.stochastic_gradient(sp.Scene(c1.init_x), views, batch)
+        go, losso = orc.stochastic_gradient(c1.init_x, c1.cams, c1.gts, batch)
+        assert rel(g, go) < GRAD_TOL
+        assert loss == pytest.approx(losso, rel=1e-9)
+
+
+def test_gradient_vanishes_at_perfect_fit(sp, orc):  # test_optimizer.cpp:77-87
+    x, ocams, _ = orc.make_check_scene(4, 12, 2, 71)
+    views = [sp.Camera.from_c(c, orc.rasterize(x, c)[0]) for c in ocams]
+    g, _ = sp.stochastic_gradient(sp.Scene(x), views, [0, 1])
+    assert np.linalg.norm(g) <= 1e-6
+
+
+def test_hutchinson_parity(sp, orc, c1):
+    views = cams_of(sp, c1.cams, c1.gts)
+    z = orc.Rng(11).rademacher(2 * c1.init_x.size).reshape(2, -1)
+    d = sp.hutchinson_diag(sp.Scene(c1.init_x), views, [3], 2, lambda s: z[s])
+    do = orc.hutchinson_diag(c1.init_x, c1.cams, c1.gts, [3], z)
+    assert rel(d, do) < IMG_TOL
+
+
+def test_hutchinson_unit_probe(sp, orc):  # test_optimizer.cpp:89-108
+    x, ocams, gts = orc.make_check_scene(4, 12, 2, 73)
+    views = cams_of(sp, ocams, gts)
+    exact = orc.exact_gn_diagonal(x, ocams, gts)
+    for k in (0, 7, x.size - 1):
+        e = np.zeros(x.size)
+        e[k] = 1.0
+        d = sp.hutchinson_diag(sp.Scene(x), views, [0, 1], 1, lambda s: e)
+        assert d[k] == pytest.approx(exact[k], rel=1e-9, abs=1e-300)
+
+
+def test_shd_radii_parity(sp, orc, c1):
+    for x in (c1.gt_x, c1.init_x):
+        for eps in (1e-6, 1e-4):
+            assert rel(sp.shd_radii(sp.Scene(x), eps), orc.shd_radii(x, eps)) < 1e-9
+
+
+# ------------------------------------------------------------------ Algorithm 1
+def _tr_opts(sp, total, **kw):
+    return sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, total), **kw)
+
+
+def test_step_parity_rng_mode(sp, orc):
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=300, init_splats=300, views=6,
+                                            image_size=48, seed=2))
+    views = cams_of(sp, ds.cams, ds.gts)
+    st = sp.OptimizerState(ds.init_x.size, 123)
+    scene = sp.Scene(ds.init_x)
+    ost = orc.State(ds.init_x.size, 123)
+    xo = ds.init_x.copy()
+    opts = _tr_opts(sp, 25, batch_size=2)
+    oopts = orc.TrOptions(total_steps=25, batch_size=2)
+    for t in range(1, 13):
+        dg = sp.step_3dgs2tr(st, scene, views, opts)
+        do = orc.step_3dgs2tr(ost, xo, ds.cams, ds.gts, oopts, want_applied=True)
+        g, d, tt = st.ctx.state_get()
+        go, dd, to = ost.get()
+        assert tt == to == t
+        assert dg.refreshed == (t % 10 == 1)
+        assert rel(g, go) < GRAD_TOL
+        assert rel(d, dd) < IMG_TOL
+        assert rel(scene.x, xo) < 1e-6
+        assert dg.batch_loss == pytest.approx(do["batch_loss"], rel=1e-8)
+        assert dg.eps == do["eps"]
+        assert dg.clip_frac == pytest.approx(do["clip_frac"], abs=2.0 / xo.size)
+        assert dg.max_step_over_radius <= 1.0
+
+
+def test_perfect_fit_fixed_point(sp, orc):  # test_optimizer.cpp:269-282
+    x, ocams, _ = orc.make_check_scene(3, 12, 2, 109)
+    views = [sp.Camera.from_c(c, orc.rasterize(x, c)[0]) for c in ocams]
+    st = sp.OptimizerState(x.size, 13)
+    scene = sp.Scene(x)
+    for _ in range(5):
+        sp.step_3dgs2tr(st, scene, views, _tr_opts(sp, 10))
+    assert np.array_equal(scene.x, x)
+
+
+def test_ema_cold_start(sp, orc):  # test_optimizer.cpp:187-202
+    x, ocams, gts = orc.make_check_scene(4, 12, 3, 97)
+    views = cams_of(sp, ocams, gts)
+    batch = sp.Rng(55).sample_without_replacement(len(views), 1)
+    g1, _ = sp.stochastic_gradient(sp.Scene(x), views, batch)
+    st = sp.OptimizerState(x.size, 55)
+    sp.step_3dgs2tr(st, sp.Scene(x), views, _tr_opts(sp, 10))
+    assert np.linalg.norm(st.g_hat - 0.1 * g1) <= 1e-15 * max(1.0, np.linalg.norm(g1))
+
+
+def test_step_nonfinite_parameter_names_splat(sp, orc):
+    x, ocams, gts = orc.make_check_scene(4, 12, 2, 5)
+    views = cams_of(sp, ocams, gts)
+    x = x.copy()
+    x[10 * 4 + 2] = np.nan  # opacity of splat 2
+    st = sp.OptimizerState(x.size, 1)
+    with pytest.raises(sp.NumericError, match="non-finite parameter in splat 2"):
+        sp.step_3dgs2tr(st, sp.Scene(x), views, _tr_opts(sp, 10))
+    assert st.t == 1  # the reference increments t before the first render
