@@ -222,6 +222,23 @@ typedef struct sgtr_synth_config {
 int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x,
                         double* init_x, sgtr_camera* cams);
 
+/* ------------------------------------------------------------ measurement */
+/* per-kernel-class CUDA-event timing on the context stream (enable resets
+ * the totals); the report is JSON {"class": [launches, total_ms], ...} */
+int sgtr_kernel_timing(sgtr_ctx* ctx, int32_t enable);
+int sgtr_kernel_timing_report(sgtr_ctx* ctx, char* buf, int32_t len);
+/* algorithmic-work counters of one view: (pixel, fragment) pairs reaching
+ * the alpha evaluation and contributing pairs (render.cpp:132-144) */
+int sgtr_blend_stats(sgtr_ctx* ctx, const sgtr_camera* cam,
+                     const sgtr_render_options* ro, int64_t* evaluated,
+                     int64_t* contributing);
+/* visible splats and tile duplicates of one view */
+int sgtr_view_stats(sgtr_ctx* ctx, const sgtr_camera* cam,
+                    const sgtr_render_options* ro, int32_t* n_visible,
+                    int64_t* n_dup);
+/* FP64 FMA-pipe throughput of the device (TFLOP/s), measured */
+int sgtr_fp64_peak(int device, double* tflops);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* one process per GPU; views of each step are split round-robin over
  * ranks and g | z.w | loss are summed with one ncclAllReduce per step */

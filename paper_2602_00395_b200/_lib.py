@@ -119,6 +119,11 @@ _SIGS = {
     "sgtr_dump_binning": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int32), VP,
                                     C.POINTER(C.c_int64), VP, VP, VP]),
     "sgtr_make_synthetic": (C.c_int, [VP, VP, VP, VP]),
+    "sgtr_kernel_timing": (C.c_int, [VP, C.c_int32]),
+    "sgtr_kernel_timing_report": (C.c_int, [VP, C.c_char_p, C.c_int32]),
+    "sgtr_blend_stats": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sgtr_view_stats": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "sgtr_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
     "sgtr_nccl_unique_id": (C.c_int, [VP]),
     "sgtr_comm_init": (C.c_int, [VP, VP, C.c_int32, C.c_int32]),
 }

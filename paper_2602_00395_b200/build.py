@@ -24,7 +24,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                  "-Xptxas", "-warn-spills"]
 NO_FMA = {"project.cu", "update.cu"}
-SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu"]
+SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu", "probe.cu"]
 HEADERS = ["common.cuh", "geometry.cuh", "launch.h"]
 
 

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <string>
@@ -162,12 +163,54 @@ struct UniqueId {
 };
 typedef int (*CommInitRankFn)(void**, int, UniqueId, int);
 
+// Per-kernel-class CUDA-event timing (off unless bench.py asks for it):
+// events bracket each launch on the context stream, durations are harvested
+// after the stream synchronises.
+enum KClass {
+    KC_PROJECT, KC_DEPTH_SORT, KC_TILE_BIN, KC_RASTER_FWD, KC_SSIM, KC_GATHER,
+    KC_RASTER_VJP, KC_CHAIN, KC_PROJECT_JVP, KC_RASTER_JVP, KC_TR_UPDATE, KC_COUNT
+};
+const char* const kClassNames[KC_COUNT] = {
+    "project", "depth_sort_scan", "tile_binning", "raster_fwd", "ssim_residual",
+    "ssim_gather", "raster_vjp", "chain", "project_jvp", "raster_jvp", "tr_update"};
+
+struct KTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<int, size_t>> pending;  // class, index of start event
+    double total_ms[KC_COUNT] = {};
+    long long count[KC_COUNT] = {};
+    ~KTimer() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+    cudaEvent_t next() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            SGTR_CUDA(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void harvest() {
+        for (auto& p : pending) {
+            float ms = 0.f;
+            SGTR_CUDA(cudaEventElapsedTime(&ms, pool[p.second], pool[p.second + 1]));
+            total_ms[p.first] += ms;
+            count[p.first] += 1;
+        }
+        pending.clear();
+        used = 0;
+    }
+};
+
 }  // namespace
 
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
     long long launches = 0;
+    KTimer timer;
     int K = 0;
     Buf x, x_alt, ghat, dhat, fused, applied, vecbuf;
     bool have_applied = false;
@@ -210,6 +253,27 @@ struct ViewRender {
 
 void bind(Ctx& c) { SGTR_CUDA(cudaSetDevice(c.device)); }
 
+struct Timed {
+    Ctx& c;
+    int cls;
+    size_t idx = 0;
+    Timed(Ctx& ctx, int k) : c(ctx), cls(k) {
+        if (!c.timer.on) return;
+        if (c.timer.used % 2) c.timer.used++;  // keep start/stop pairs adjacent
+        idx = c.timer.used;
+        SGTR_CUDA(cudaEventRecord(c.timer.next(), c.st));
+    }
+    ~Timed() {
+        if (!c.timer.on) return;
+        cudaEventRecord(c.timer.next(), c.st);
+        c.timer.pending.push_back({cls, idx});
+    }
+};
+
+void harvest_timing(Ctx& c) {
+    if (c.timer.on) c.timer.harvest();
+}
+
 double* img_ptr(Ctx& c, Buf& b, int P) { return b.as<double>(3LL * P); }
 
 // K1..K7 for one camera on the context's scene
@@ -239,8 +303,15 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     c.hstat->vs = init;
     SGTR_CUDA(cudaMemcpyAsync(&c.dstat->vs, &c.hstat->vs, sizeof(ViewStatus),
                               cudaMemcpyHostToDevice, c.st));
-    launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, &c.dstat->vs);
-    depth_sort_and_scan(c.st, b, K);
+    {
+        Timed t(c, KC_PROJECT);
+        launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount,
+                       &c.dstat->vs);
+    }
+    {
+        Timed t(c, KC_DEPTH_SORT);
+        depth_sort_and_scan(c.st, b, K);
+    }
     c.launches += 1 + 9 + 3;  // project, onesweep sort (histogram + 8 passes), counts + scan
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs.n_dup, b.off_r + K, sizeof(long long),
                               cudaMemcpyDeviceToHost, c.st));
@@ -272,10 +343,14 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.dup_id = c.dup_id.as<int>(nd);
     b.temp = c.temp.ensure(std::max(tb, tile_sort_temp_bytes(vr.n_dup, n_tiles)));
     b.temp_bytes = c.temp.bytes;
-    emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
+    {
+        Timed t(c, KC_TILE_BIN);
+        emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
+    }
     c.launches += vr.n_dup ? 5 : 0;  // emit, tile sort (histogram + 2 passes), ranges
     vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt, b.dup_id};
     const int P = dc.W * dc.H;
+    Timed t(c, KC_RASTER_FWD);
     launch_raster_fwd(c.st, vr.tl, rec, dc.W, dc.H, ro, img_ptr(c, c.img, P),
                       c.tfin.as<double>(P), c.last.as<int>(P));
     c.launches += 1;
@@ -287,8 +362,12 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
     const long long nd = std::max(vr.n_dup, 1LL);
     double* slots = c.slots.as<double>((size_t)kAdj * nd);
-    launch_raster_vjp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro, c.adj.get<double>(),
-                      c.tfin.get<double>(), c.last.get<int>(), slots);
+    {
+        Timed t(c, KC_RASTER_VJP);
+        launch_raster_vjp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
+                          c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(), slots);
+    }
+    Timed t(c, KC_CHAIN);
     launch_chain(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                  c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits, acc, flag);
     c.launches += 2;
@@ -318,12 +397,16 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
     a.R = img_ptr(c, c.Rf, P);
     const int nb = ssim_num_blocks(W, H);
     a.loss_partials = c.partials.as<double>(std::max(nb, 5 * tr_num_blocks(c.K) + 8));
-    launch_ssim(c.st, a);
-    c.launches += 1;
-    if (mode == GRAD && loss_out) {
-        launch_sum_partials(c.st, a.loss_partials, nb, loss_out);
+    {
+        Timed t(c, KC_SSIM);
+        launch_ssim(c.st, a);
         c.launches += 1;
+        if (mode == GRAD && loss_out) {
+            launch_sum_partials(c.st, a.loss_partials, nb, loss_out);
+            c.launches += 1;
+        }
     }
+    Timed t(c, KC_GATHER);
     launch_ssim_gather(c.st, W, H, c.img.get<double>(), gt, a.adjl1, a.P, a.Q, a.R,
                        img_ptr(c, c.adj, P));
     c.launches += 1;
@@ -439,9 +522,15 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                     break;
                 }
                 double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
-                launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
-                launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, ro,
-                                  img_ptr(c, c.tan, P));
+                {
+                    Timed t(c, KC_PROJECT_JVP);
+                    launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
+                }
+                {
+                    Timed t(c, KC_RASTER_JVP);
+                    launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, ro,
+                                      img_ptr(c, c.tan, P));
+                }
                 c.launches += 2;
                 residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(), nullptr,
                                  o.residual.lambda, o.residual.floor, nullptr);
@@ -519,13 +608,17 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                               cudaMemcpyHostToDevice, c.st));
     a.bad_index = &c.dstat->bad_index;
     a.degenerate_flag = &c.dstat->degenerate;
-    launch_tr_update(c.st, a);
-    launch_tr_finalize(c.st, a.partials, nb, c.dstat->tr);
+    {
+        Timed t(c, KC_TR_UPDATE);
+        launch_tr_update(c.st, a);
+        launch_tr_finalize(c.st, a.partials, nb, c.dstat->tr);
+    }
     c.launches += 2;
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->bad_index, &c.dstat->bad_index,
                               offsetof(DevStatus, scalar) - offsetof(DevStatus, bad_index),
                               cudaMemcpyDeviceToHost, c.st));
     SGTR_CUDA(cudaStreamSynchronize(c.st));
+    harvest_timing(c);
     diag->gnorm = std::sqrt(c.hstat->tr[0]);
     diag->refreshed = refresh ? 1 : 0;
     diag->n_local_views = 0;
@@ -1387,6 +1480,77 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
             cams[v] = cam;
         }
     });
+}
+
+int sgtr_kernel_timing(sgtr_ctx* ctx, int32_t enable) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        harvest_timing(c);
+        c.timer.on = enable != 0;
+        for (int k = 0; k < KC_COUNT; ++k) {
+            c.timer.total_ms[k] = 0.0;
+            c.timer.count[k] = 0;
+        }
+    });
+}
+
+int sgtr_kernel_timing_report(sgtr_ctx* ctx, char* buf, int32_t len) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        harvest_timing(c);
+        std::string s = "{";
+        for (int k = 0; k < KC_COUNT; ++k) {
+            char item[128];
+            std::snprintf(item, sizeof(item), "%s\"%s\": [%lld, %.6f]", k ? ", " : "",
+                          kClassNames[k], c.timer.count[k], c.timer.total_ms[k]);
+            s += item;
+        }
+        s += "}";
+        if ((int)s.size() >= len) throw invalid("sgtr_kernel_timing_report: buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+int sgtr_blend_stats(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                     int64_t* evaluated, int64_t* contributing) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const DevCam dc = make_devcam(*cam);
+        const RenderP rp = render_params(*ro);
+        const ViewRender vr = render_view(c, dc, rp, true);
+        unsigned long long* cnt = c.seam2.as<unsigned long long>(2);
+        SGTR_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c.st));
+        const int P = dc.W * dc.H;
+        launch_raster_fwd(c.st, vr.tl, c.rec.get<double>(), dc.W, dc.H, rp, img_ptr(c, c.img, P),
+                          c.tfin.as<double>(P), c.last.as<int>(P), cnt);
+        unsigned long long h[2];
+        SGTR_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        *evaluated = (int64_t)h[0];
+        *contributing = (int64_t)h[1];
+    });
+}
+
+int sgtr_view_stats(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_options* ro,
+                    int32_t* n_visible, int64_t* n_dup) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const ViewRender vr = render_view(c, make_devcam(*cam), render_params(*ro), true);
+        *n_visible = vr.n_visible;
+        *n_dup = vr.n_dup;
+    });
+}
+
+int sgtr_fp64_peak(int device, double* tflops) {
+    return guarded([&] { *tflops = fp64_fma_peak_tflops(device); });
 }
 
 int sgtr_nccl_unique_id(uint8_t out[128]) {

@@ -65,7 +65,8 @@ struct TileLists {
 };
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
-                       int H, const RenderP& ro, double* img, double* tfinal, int* last);
+                       int H, const RenderP& ro, double* img, double* tfinal, int* last,
+                       unsigned long long* counters = nullptr);
 // K10: back-to-front adjoint sweep -> 9 adjoints per (tile, fragment) slot
 void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, const double* adj, const double* tfinal,
@@ -132,6 +133,8 @@ void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, do
 void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
                       const double caps[5], double* eta);
 void launch_scale(cudaStream_t st, double* v, long long n, double s);
+// probe.cu
+double fp64_fma_peak_tflops(int device);
 void launch_fill_int(cudaStream_t st, int* p, long long n, int v);
 
 }  // namespace sgtr

@@ -81,12 +81,17 @@ __device__ __forceinline__ void stage_tangents(const TileLists& tl, const double
 }
 
 // ------------------------------------------------------------------ K7
+// kCount: also count the (pixel, fragment) pairs reaching the alpha
+// evaluation (E) and the contributing ones (C), the algorithmic-work units
+// of SURVEY §8(d); used outside timed regions only.
+template <bool kCount>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                                                          const double* __restrict__ rec, int W,
                                                          int H, RenderP ro,
                                                          double* __restrict__ img,
                                                          double* __restrict__ tfinal,
-                                                         int* __restrict__ last) {
+                                                         int* __restrict__ last,
+                                                         unsigned long long* counters) {
     __shared__ __align__(16) double s_rec[kFwdBatch * kRec];
     const int tile = blockIdx.x;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -94,6 +99,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
     double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
     bool done = !pc.inside;
     int processed = end - start;
+    unsigned long long n_eval = 0, n_contrib = 0;
     for (int b = start; b < end; b += kFwdBatch) {
         if (__syncthreads_and(done)) break;
         const int n = min(kFwdBatch, end - b);
@@ -105,8 +111,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                 if (outside_bbox(pc.pxc, pc.pyc, f)) continue;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                if (kCount) ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar < ro.alpha_skip) continue;
+                if (kCount) ++n_contrib;
                 const double w = abar * T;
                 c0 += f[R_C0] * w;
                 c1 += f[R_C1] * w;
@@ -118,6 +126,16 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                     break;
                 }
             }
+        }
+    }
+    if (kCount) {
+        for (int o = 16; o > 0; o >>= 1) {
+            n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
+            n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(counters, n_eval);
+            atomicAdd(counters + 1, n_contrib);
         }
     }
     if (!pc.inside) return;
@@ -309,10 +327,16 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
 }  // namespace
 
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
-                       const RenderP& ro, double* img, double* tfinal, int* last) {
+                       const RenderP& ro, double* img, double* tfinal, int* last,
+                       unsigned long long* counters) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    k_raster_fwd<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    if (counters)
+        k_raster_fwd<true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
+                                                   counters);
+    else
+        k_raster_fwd<false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
+                                                    nullptr);
     SGTR_CUDA(cudaGetLastError());
 }
 

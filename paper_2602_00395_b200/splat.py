@@ -313,9 +313,13 @@ class Context:
         self.n_views = n
         self._views_key = tuple(id(v) for v in views)
 
-    def set_cameras(self, cams: Sequence[_lib.Camera]) -> None:
+    def set_cameras(self, cams) -> None:
+        """Views without targets; ``cams`` are Camera objects or any struct
+        with the sgtr_camera fields."""
         n = len(cams)
-        arr = (_lib.Camera * max(n, 1))(*cams)
+        arr = (_lib.Camera * max(n, 1))()
+        for i, c in enumerate(cams):
+            arr[i] = c._c() if isinstance(c, Camera) else Camera.from_c(c)._c()
         check(lib().sgtr_set_views(self._h, arr, n, None))
         self.n_views = n
         self._views_key = None
