@@ -1717,10 +1717,13 @@ int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro, int 
     return guarded([&] {
         Rng rng(cfg->seed);
         const int64_t kg = cfg->gt_splats, ki = cfg->init_splats;
+        const double ss = cfg->size_scale > 0.0 ? cfg->size_scale : 1.0;
+        const int W = cfg->width > 0 ? cfg->width : cfg->image_size;
+        const int H = cfg->height > 0 ? cfg->height : cfg->image_size;
         std::vector<Prim> gt(kg);
         for (Prim& p : gt) {
             for (int a = 0; a < 3; ++a) p.mu[a] = rng.uniform(-0.5, 0.5);
-            for (int a = 0; a < 3; ++a) p.s[a] = rng.log_uniform(0.02, 0.2);
+            for (int a = 0; a < 3; ++a) p.s[a] = rng.log_uniform(0.02 * ss, 0.2 * ss);
             double q[4];
             for (int a = 0; a < 4; ++a) q[a] = rng.normal();
             const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
@@ -1735,23 +1738,23 @@ int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro, int 
         for (int64_t i = 0; i < ki; ++i) {
             const Prim& src = gt[i % kg];
             Prim p{};
-            for (int a = 0; a < 3; ++a) p.mu[a] = src.mu[a] + cfg->sigma_init * rng.normal();
-            for (int a = 0; a < 3; ++a) p.s[a] = cfg->init_scale;
+            for (int a = 0; a < 3; ++a) p.mu[a] = src.mu[a] + cfg->sigma_init * ss * rng.normal();
+            for (int a = 0; a < 3; ++a) p.s[a] = cfg->init_scale * ss;
             p.q[0] = p.q[1] = p.q[2] = 0.0;
             p.q[3] = 1.0;
             p.alpha = cfg->init_opacity;
             for (int a = 0; a < 3; ++a) p.c[a] = 0.5;
             set_prim(init_x, ki, i, p);
         }
-        const double focal = cfg->focal_factor * cfg->image_size;
-        const int64_t n = 3LL * cfg->image_size * cfg->image_size;
+        const double focal = cfg->focal_factor * H;
+        const int64_t n = 3LL * W * H;
         std::vector<double> img(n);
         for (int v = 0; v < cfg->views; ++v) {
             const double ang = 2.0 * M_PI * v / cfg->views;
             const double eye[3] = {cfg->camera_radius * std::cos(ang),
                                    cfg->camera_radius * std::sin(ang), cfg->camera_height};
             const double tgt[3] = {0, 0, 0};
-            orc_camera c = look_at(eye, tgt, focal, focal, cfg->image_size, cfg->image_size);
+            orc_camera c = look_at(eye, tgt, focal, focal, W, H);
             c.id = v;
             cams[v] = c;
             if (gts) {

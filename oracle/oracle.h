@@ -197,6 +197,11 @@ typedef struct orc_synth_cfg {
     uint64_t seed;
     double sigma_init, init_scale, init_opacity, camera_radius, camera_height,
         focal_factor;
+    /* declared extensions for the large configurations (0 = reference):
+     * width x height images with fx = fy = focal_factor * height, and the
+     * GT scale range, init_scale and sigma_init multiplied by size_scale */
+    int32_t width, height;
+    double size_scale;
 } orc_synth_cfg;
 /* gt_x[14*gt], init_x[14*init], cams[views], gts[views][H*W*3] */
 int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro,

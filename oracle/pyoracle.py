@@ -77,7 +77,8 @@ class SynthCfg(C.Structure):
                 ("seed", C.c_uint64), ("sigma_init", C.c_double),
                 ("init_scale", C.c_double), ("init_opacity", C.c_double),
                 ("camera_radius", C.c_double), ("camera_height", C.c_double),
-                ("focal_factor", C.c_double)]
+                ("focal_factor", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("size_scale", C.c_double)]
 
 
 def build(force: bool = False) -> str:
@@ -518,6 +519,9 @@ class SynthConfig:  # config.hpp:83-95 defaults
     camera_radius: float = 2.2
     camera_height: float = 0.77
     focal_factor: float = 2.0
+    width: int = 0        # 0: image_size (reference); W x H is a declared extension
+    height: int = 0
+    size_scale: float = 1.0
 
 
 @dataclass
@@ -532,11 +536,12 @@ def make_synthetic(cfg: SynthConfig, ro=None, with_gt=True) -> Dataset:
     ro = ro or RenderOptions()
     c = SynthCfg(cfg.gt_splats, cfg.init_splats, cfg.views, cfg.image_size, cfg.seed,
                  cfg.sigma_init, cfg.init_scale, cfg.init_opacity, cfg.camera_radius,
-                 cfg.camera_height, cfg.focal_factor)
+                 cfg.camera_height, cfg.focal_factor, cfg.width, cfg.height, cfg.size_scale)
     gt_x = np.empty(14 * cfg.gt_splats)
     init_x = np.empty(14 * cfg.init_splats)
     cams = (Camera * cfg.views)()
-    gts = [np.empty((cfg.image_size, cfg.image_size, 3)) for _ in range(cfg.views)]
+    W, H = cfg.width or cfg.image_size, cfg.height or cfg.image_size
+    gts = [np.empty((H, W, 3)) for _ in range(cfg.views)]
     ptrs = (C.c_void_p * cfg.views)(*[g.ctypes.data for g in gts]) if with_gt else None
     _check(lib().orc_make_synthetic(C.byref(c), C.byref(ro.c()), ro.workers, _p(gt_x),
                                     _p(init_x), cams, ptrs))
