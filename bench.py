@@ -124,52 +124,56 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, samples=1,
-                         model=None):
-    """Time the CPU reference path on full-width bands of the view and
-    extrapolate to one full iteration (|S1| gradient views + 1/l refresh
-    view + shd_radii at full K).  Per-call cost is modelled as a + b*rows
-    (projection + sort of all K splats, then Theta(P K) per-pixel scans); a,
-    b come from bands of 1 and 2 rows.  Returns (it/s, details)."""
+def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=None):
+    """Time the CPU reference path (the oracle port) on small central crops of
+    a view and extrapolate to one full iteration: |S1| gradient views + 1/l of
+    a refresh view + shd_radii at full K.  A call's cost is modelled as
+    a + b * pixels (projection + depth sort of all K splats, then the
+    reference's Theta(P K) per-pixel scans, render.cpp:122-151); a and b come
+    from 320 x T and 320 x 3T crops, T = host threads (>= 6 rows for SSIM).  Returns
+    (it/s, model)."""
     from oracle import pyoracle as orc
     k = x_init.size // 14
-    H = cam_full.height
+    W, H = cam_full.width, cam_full.height
 
-    def band(rows, y0=None):
-        y0 = (H - rows) // 2 if y0 is None else y0
+    def crop(rows, cols=320):
+        y0, x0 = (H - rows) // 2, (W - cols) // 2
         c = orc.Camera()
         for f, _ in orc.Camera._fields_:
             setattr(c, f, getattr(cam_full, f))
-        c.height = rows
-        c.cy = cam_full.cy - y0
+        c.height, c.width = rows, cols
+        c.cy, c.cx = cam_full.cy - y0, cam_full.cx - x0
         return c
 
     def gt_of(c):
         img, _ = orc.rasterize(x_gt, c)
         return orc.quantize8(img)
 
-    def t_grad(rows):
-        c = band(rows)
+    def t_grad(c):
         g = gt_of(c)
         t0 = time.perf_counter()
         orc.stochastic_gradient(x_init, [c], [g], [0])
         return time.perf_counter() - t0
 
-    def t_hutch(rows):
-        c = band(rows)
+    def t_hutch(c):
         g = gt_of(c)
         z = orc.Rng(7).rademacher(x_init.size)
         t0 = time.perf_counter()
         orc.hutchinson_diag(x_init, [c], [g], [0], z)
         return time.perf_counter() - t0
 
+    # row counts are multiples of the worker count: the reference splits rows
+    # round-robin over hardware threads (parallel.hpp:21-44)
+    rows = max(6, cpu_cores())
+    c1, c2 = crop(rows), crop(3 * rows)
+    p1, p2 = c1.width * c1.height, c2.width * c2.height
     if model is None:
-        g1, g2 = t_grad(1), t_grad(2)
-        b_g = max(g2 - g1, 1e-9)
-        a_g = max(g1 - b_g, 0.0)
-        h1 = t_hutch(1)
-        frac_fixed = a_g / g1 if g1 > 0 else 0.0
-        a_h, b_h = h1 * frac_fixed, h1 * (1 - frac_fixed)
+        g1, g2 = t_grad(c1), t_grad(c2)
+        b_g = max((g2 - g1) / (p2 - p1), 1e-12)
+        a_g = max(g1 - b_g * p1, 0.0)
+        h1 = t_hutch(c1)
+        fixed = a_g / g1 if g1 > 0 else 0.0
+        a_h, b_h = h1 * fixed, h1 * (1 - fixed) / p1
         sub = min(k, 100_000)
         xs = np.concatenate([x_init[:3 * k].reshape(k, 3)[:sub].ravel(),
                              x_init[3 * k:6 * k].reshape(k, 3)[:sub].ravel(),
@@ -180,16 +184,14 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, sample
         orc.shd_radii(xs, 1e-6)
         t_radii = (time.perf_counter() - t0) * k / sub
         model = dict(a_g=a_g, b_g=b_g, a_h=a_h, b_h=b_h, t_radii=t_radii)
-        sample_rows = 3
     else:
-        # one more 1-row gradient sample refreshes the per-row estimate
-        g1 = t_grad(1)
-        model = dict(model, b_g=max(g1 - model["a_g"], 1e-9))
-        sample_rows = 1
-    t_grad_full = model["a_g"] + H * model["b_g"]
-    t_hutch_full = model["a_h"] + H * model["b_h"]
-    t_iter = batch * t_grad_full + t_hutch_full / refresh_every + model["t_radii"]
-    return 1.0 / t_iter, model, sample_rows
+        # a fresh 320 x T gradient sample re-estimates the per-pixel cost
+        g1 = t_grad(c1)
+        model = dict(model, b_g=max((g1 - model["a_g"]) / p1, 1e-12))
+    P = W * H
+    t_iter = (batch * (model["a_g"] + P * model["b_g"]) +
+              (model["a_h"] + P * model["b_h"]) / refresh_every + model["t_radii"])
+    return 1.0 / t_iter, model
 
 
 def cpu_cores():
@@ -227,23 +229,23 @@ def run_reference(args):
     for f, _ in orc.Camera._fields_:
         setattr(cam, f, getattr(src, f))
     model = None
-    for _ in range(max(args.warmup, 1)):
-        _, model, _ = cpu_reference_sample(init.x, gt.x, cam, b)
-        break  # the first warm-up builds the cost model; more would only repeat it
+    # warm-up: builds the cost model (320 x T and 320 x 3T gradient crops, a
+    # 320 x T refresh crop, shd_radii on a 100K subset; T = host threads)
+    _, model = cpu_reference_sample(init.x, gt.x, cam, b)
     rates = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r, model, _ = cpu_reference_sample(init.x, gt.x, cam, b, model=model)
+        r, model = cpu_reference_sample(init.x, gt.x, cam, b, model=model)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
     cores = cpu_cores()
     sample = (f"CPU reference path (oracle port of render/ssim/residuals/optimizer/"
               f"trust_region, FP64, {cores} threads for the row-parallel raster passes as in "
-              f"parallel.hpp): each step times one 1920x1-row band of a gradient view with all "
-              f"{k} splats; cost model a+b*rows (from 1- and 2-row bands), Hutchinson view and "
-              f"shd_radii measured once; extrapolated to 1080 rows x {b} views + 1/10 refresh "
-              f"view + shd_radii (extrapolated)")
+              f"parallel.hpp): each step times one central 320xT crop (T = threads) of a gradient view with "
+              f"all {k} splats; cost model a+b*pixels from 320xT/320x3T crops, the refresh view "
+              f"and shd_radii (100K subset) measured once in warm-up; extrapolated to "
+              f"{w}x{h} x {b} views + 1/10 refresh view + shd_radii at full K")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -429,13 +431,14 @@ def main():
         src = cams[1]._c()
         for f, _ in orc.Camera._fields_:
             setattr(cam, f, getattr(src, f))
-        rate, model, _ = cpu_reference_sample(init.x, gt.x, cam, b)
+        rate, model = cpu_reference_sample(init.x, gt.x, cam, b)
         cores = cpu_cores()
         cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "port",
-               "sample": (f"oracle port of the reference path, {cores} threads; 1- and 2-row "
-                          f"1920-px bands of one gradient view + a 1-row Hutchinson view with all "
-                          f"{k} splats, shd_radii on a 100K subset; extrapolated to {b} views x "
-                          f"1080 rows + 1/10 refresh view + shd_radii at full K"),
+               "sample": (f"oracle port of the reference path, {cores} threads; central 320xT "
+                          f"and 320x3T crops (T = threads) of one gradient view + a 320xT refresh crop, all "
+                          f"{k} splats, shd_radii on a 100K subset; cost a+b*pixels "
+                          f"extrapolated to {b} views x {w}x{h} + 1/10 refresh view + "
+                          f"shd_radii at full K"),
                "model_s": {kk: float(vv) for kk, vv in model.items()}}
 
     if rank == 0:

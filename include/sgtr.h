@@ -243,6 +243,10 @@ int sgtr_fp64_peak(int device, double* tflops);
 /* one process per GPU; views of each step are split round-robin over
  * ranks and g | z.w | loss are summed with one ncclAllReduce per step */
 int sgtr_nccl_unique_id(uint8_t out[128]);
+/* positions of a step's view batch (S1 or S2) that `rank` renders: the
+ * round-robin split the step uses; host-only, no device needed */
+int sgtr_shard_views(int32_t n, int32_t rank, int32_t nranks, int32_t* positions,
+                     int32_t* count);
 int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks,
                    int32_t rank);
 

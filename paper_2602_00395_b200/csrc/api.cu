@@ -490,7 +490,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     std::vector<double> herr(2 * (n1 + n2), 0.0);
     bool local_error = false;
     // gradient phase: stochastic_gradient (optimizer.cpp:36-65), views of S1
-    // split round-robin over ranks
+    // split round-robin over ranks (sgtr_shard_views)
     for (int p = c.rank; p < n1 && !local_error; p += c.nranks) {
         const View& v = c.views[s1[p]];
         const ViewRender vr = render_view(c, v.dc, ro, false);
@@ -1551,6 +1551,19 @@ int sgtr_view_stats(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_opt
 
 int sgtr_fp64_peak(int device, double* tflops) {
     return guarded([&] { *tflops = fp64_fma_peak_tflops(device); });
+}
+
+int sgtr_shard_views(int32_t n, int32_t rank, int32_t nranks, int32_t* positions,
+                     int32_t* count) {
+    return guarded([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw invalid("sgtr_shard_views: bad rank");
+        int m = 0;
+        for (int p = rank; p < n; p += nranks) {  // the loop step_core runs
+            if (positions) positions[m] = p;
+            ++m;
+        }
+        *count = m;
+    });
 }
 
 int sgtr_nccl_unique_id(uint8_t out[128]) {

@@ -376,6 +376,15 @@ class Context:
         check(lib().sgtr_comm_init(self._h, buf, nranks, rank))
 
 
+def shard_views(n: int, rank: int, nranks: int) -> List[int]:
+    """Positions of an n-view batch that ``rank`` of ``nranks`` renders (the
+    split libsgtr's step uses before its single allreduce)."""
+    out = np.empty(max(n, 1), np.int32)
+    cnt = C.c_int32()
+    check(lib().sgtr_shard_views(n, rank, nranks, _ptr(out), C.byref(cnt)))
+    return out[:cnt.value].tolist()
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     check(lib().sgtr_nccl_unique_id(buf))
