@@ -8,7 +8,12 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -74,6 +79,8 @@ struct DevStatus {
     int degenerate;
     double tr[5];
     double scalar;
+    int queue_count;
+    int pad;
 };
 
 // RNG with the reference's variate mappings (rng.hpp:15-72)
@@ -111,6 +118,112 @@ struct Rng {
         idx.resize(m);
         return idx;
     }
+};
+
+// The draws of one Algorithm-1 step in the reference order
+// (optimizer.cpp:193-211): |S1| sample, then on refresh steps the |S2|
+// sample and nu probes of dim Rademacher draws, coordinate-ascending.
+struct DrawKey {
+    int M = 0;
+    long long dim = 0;
+    int b1 = 0, b2 = 0, nu = 0, l = 0;
+    bool operator==(const DrawKey& o) const {
+        return M == o.M && dim == o.dim && b1 == o.b1 && b2 == o.b2 && nu == o.nu && l == o.l;
+    }
+};
+
+struct StepDraws {
+    long long t = 0;
+    std::vector<int> s1, s2;
+    bool refresh = false;
+    std::vector<uint32_t> bits;
+    Rng after_s1;  // state to restore when the gradient phase fails
+    Rng after;     // state after all of the step's draws
+};
+
+StepDraws draw_step(Rng& rng, long long t, const DrawKey& k, const std::atomic<bool>* stop) {
+    StepDraws d;
+    d.t = t;
+    d.s1 = rng.sample(k.M, k.b1);
+    d.after_s1 = rng;
+    d.refresh = k.l <= 1 || t % k.l == 1;
+    if (d.refresh) {
+        d.s2 = rng.sample(k.M, k.b2);
+        const long long words = (k.dim + 31) / 32;
+        d.bits.assign(words * k.nu, 0u);
+        for (int s = 0; s < k.nu; ++s) {
+            uint32_t* w = d.bits.data() + words * s;
+            for (long long base = 0; base < k.dim; base += 32) {
+                if (stop && (base & ((1 << 20) - 1)) == 0 && stop->load()) return d;
+                const int n = (int)std::min<long long>(32, k.dim - base);
+                uint32_t word = 0;
+                for (int b = 0; b < n; ++b) word |= (uint32_t)(rng.gen() & 1u) << b;
+                w[base >> 5] = word;
+            }
+        }
+    }
+    d.after = rng;
+    return d;
+}
+
+// Runs the RNG ahead of the GPU on a host thread: the whole consumption
+// schedule up to the next refresh step is known from the options, so the
+// probes of the next refresh (dim draws each) are generated while the
+// intervening steps run on the device.
+struct Prefetcher {
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<StepDraws> q;
+    bool done = true;
+    std::atomic<bool> stop{false};
+    DrawKey key;
+
+    void start(const Rng& from, long long t_next, const DrawKey& k) {
+        reset();
+        key = k;
+        done = false;
+        stop = false;
+        th = std::thread([this, from, t_next, k]() {
+            Rng r = from;
+            for (long long t = t_next; t < t_next + 64 && !stop.load(); ++t) {
+                StepDraws d = draw_step(r, t, k, &stop);
+                const bool last = d.refresh;
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    q.push_back(std::move(d));
+                }
+                cv.notify_all();
+                if (last) break;
+            }
+            {
+                std::lock_guard<std::mutex> g(mu);
+                done = true;
+            }
+            cv.notify_all();
+        });
+    }
+    bool take(long long t, const DrawKey& k, StepDraws& out) {
+        if (!th.joinable() || !(k == key)) return false;
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return !q.empty() || done; });
+        if (q.empty() || q.front().t != t) return false;
+        out = std::move(q.front());
+        q.pop_front();
+        return true;
+    }
+    bool exhausted() {
+        std::lock_guard<std::mutex> g(mu);
+        return done && q.empty();
+    }
+    void reset() {
+        stop = true;
+        if (th.joinable()) th.join();
+        q.clear();
+        done = true;
+        stop = false;
+    }
+    ~Prefetcher() { reset(); }
 };
 
 struct View {
@@ -218,11 +331,13 @@ struct Ctx {
     Buf gt;  // planar targets, one (3, H, W) block per view
     bool has_gt = false;
     long long t = 0;
-    Rng rng{1};
+    Rng rng{1};       // committed state: all draws of completed steps
+    Prefetcher prefetch;
     // per-view workspace
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
+    Buf dxbuf, etabuf, queue;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     double* htail = nullptr;     // pinned staging for the fused tail
@@ -231,6 +346,7 @@ struct Ctx {
     void* comm = nullptr;
 
     ~Ctx() {
+        prefetch.reset();
         if (dstat) cudaFree(dstat);
         if (hstat) cudaFreeHost(hstat);
         if (htail) cudaFreeHost(htail);
@@ -396,7 +512,7 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
     a.Q = img_ptr(c, c.Qf, P);
     a.R = img_ptr(c, c.Rf, P);
     const int nb = ssim_num_blocks(W, H);
-    a.loss_partials = c.partials.as<double>(std::max(nb, 5 * tr_num_blocks(c.K) + 8));
+    a.loss_partials = c.partials.as<double>(std::max(nb, 10 * tr_num_blocks(c.K) + 8));
     {
         Timed t(c, KC_SSIM);
         launch_ssim(c.st, a);
@@ -551,7 +667,10 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     // gradient-phase failures: nothing but t and the S1 draw has happened
     for (int p = 0; p < n1; ++p) {
         if (hk[p] != 0.0 || ht[n1 + p] != 0.0) {
-            if (rng_ckpt) c.rng = *rng_ckpt;
+            if (rng_ckpt) {
+                c.prefetch.reset();
+                c.rng = *rng_ckpt;
+            }
             if (hk[p] == 1.0)
                 throw numeric("rasterize: non-finite parameter in splat " +
                               std::to_string((long long)hi[p]));
@@ -601,7 +720,11 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     c.have_applied = o.record_applied_step != 0;
     a.applied = c.have_applied ? c.applied.as<double>(std::max<long long>(dim, 1)) : nullptr;
     const int nb = tr_num_blocks(c.K);
-    a.partials = c.partials.as<double>(std::max(5 * nb + 8, ssim_num_blocks(W, H)));
+    a.partials = c.partials.as<double>(std::max(10 * nb + 8, ssim_num_blocks(W, H)));
+    a.dx_buf = c.dxbuf.as<double>(std::max<long long>(dim, 1));
+    a.eta_buf = c.etabuf.as<double>(std::max<long long>(dim, 1));
+    a.queue = c.queue.as<int>(std::max(4LL * c.K, 1LL));
+    a.queue_count = &c.dstat->queue_count;
     c.hstat->bad_index = INT_MAX;
     c.hstat->degenerate = 0;
     SGTR_CUDA(cudaMemcpyAsync(&c.dstat->bad_index, &c.hstat->bad_index, 2 * sizeof(int),
@@ -831,6 +954,7 @@ int sgtr_state_reset(sgtr_ctx* ctx, uint64_t seed) {
         const long long n = std::max<long long>(c.dim(), 1);
         SGTR_CUDA(cudaMemsetAsync(c.ghat.as<double>(n), 0, sizeof(double) * n, c.st));
         SGTR_CUDA(cudaMemsetAsync(c.dhat.as<double>(n), 0, sizeof(double) * n, c.st));
+        c.prefetch.reset();
         c.t = 0;
         c.rng = Rng(seed);
         SGTR_CUDA(cudaStreamSynchronize(c.st));
@@ -848,6 +972,7 @@ int sgtr_state_set(sgtr_ctx* ctx, const double* g_hat, const double* d_hat, int6
         if (d_hat && n)
             SGTR_CUDA(cudaMemcpyAsync(c.dhat.as<double>(n), d_hat, sizeof(double) * n,
                                       cudaMemcpyHostToDevice, c.st));
+        c.prefetch.reset();
         c.t = t;
         SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
@@ -872,6 +997,7 @@ int sgtr_state_get(sgtr_ctx* ctx, double* g_hat, double* d_hat, int64_t* t) {
 int sgtr_rng_raw(sgtr_ctx* ctx, int64_t n, uint64_t* out) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
+        c.prefetch.reset();
         for (int64_t i = 0; i < n; ++i) out[i] = c.rng.gen();
     });
 }
@@ -901,26 +1027,27 @@ int sgtr_step_3dgs2tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
         check_views(c, true);
         validate_opts(*opt);
         *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
-        c.t += 1;
-        const int M = (int)c.views.size();
         if (opt->batch_size < 1) throw invalid("stochastic_gradient: empty batch");
-        const std::vector<int> s1 = c.rng.sample(M, opt->batch_size);
-        const Rng ckpt = c.rng;
-        const bool refresh = opt->hess_interval <= 1 || c.t % opt->hess_interval == 1;
-        std::vector<int> s2;
-        std::vector<uint32_t> bits;
-        if (refresh) {
-            if (opt->hutch_batch_size < 1) throw invalid("hutchinson_diag: empty batch");
-            s2 = c.rng.sample(M, opt->hutch_batch_size);
-            const long long dim = c.dim(), words = (dim + 31) / 32;
-            bits.assign(words * opt->hutch_samples, 0u);
-            for (int s = 0; s < opt->hutch_samples; ++s) {
-                uint32_t* w = bits.data() + words * s;
-                for (long long k = 0; k < dim; ++k)
-                    if (c.rng.gen() & 1u) w[k >> 5] |= 1u << (k & 31);
-            }
+        if (opt->hutch_batch_size < 1) throw invalid("hutchinson_diag: empty batch");
+        DrawKey key;
+        key.M = (int)c.views.size();
+        key.dim = c.dim();
+        key.b1 = opt->batch_size;
+        key.b2 = opt->hutch_batch_size;
+        key.nu = opt->hutch_samples;
+        key.l = opt->hess_interval;
+        const long long t_new = c.t + 1;
+        StepDraws d;
+        if (!c.prefetch.take(t_new, key, d)) {
+            c.prefetch.reset();
+            Rng r = c.rng;
+            d = draw_step(r, t_new, key, nullptr);
         }
-        step_core(c, *opt, s1, s2, bits, opt->hutch_samples, refresh, &ckpt, diag);
+        c.t = t_new;
+        c.rng = d.after;
+        if (c.prefetch.exhausted()) c.prefetch.start(c.rng, t_new + 1, key);
+        const Rng ckpt = d.after_s1;
+        step_core(c, *opt, d.s1, d.s2, d.bits, opt->hutch_samples, d.refresh, &ckpt, diag);
     });
 }
 
@@ -934,6 +1061,7 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
         need_scene(c);
         check_views(c, true);
         *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
+        c.prefetch.reset();
         c.t += 1;
         const int M = (int)c.views.size();
         if (n1 < 1) throw invalid("stochastic_gradient: empty batch");

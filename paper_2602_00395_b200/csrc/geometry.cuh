@@ -150,6 +150,131 @@ SGTR_HD void invert2x2(const T& c00, const T& c01, const T& c11, T& i00, T& i01,
     i11 = c00 / det;
 }
 
+// Reverse-mode chain of the 5 screen-space adjoints (mu2d, inverse 2d
+// covariance) through invert2x2 and project() to (mu, s, q): the transpose of
+// the 5x10 Jacobian the reference evaluates with 10 dual seeds
+// (render.cpp:297-329), one backward sweep over the same computational graph.
+SGTR_HD void chain_reverse(const double* mu, const double* s, const double* q,
+                           const double* w, const double* t, double fx, double fy,
+                           double lowpass, const double* a, double* gmu, double* gs,
+                           double* gq) {
+    // ---- forward recompute (the graph of project() + invert2x2)
+    double pc[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        pc[i] = w[3 * i] * mu[0] + w[3 * i + 1] * mu[1] + w[3 * i + 2] * mu[2] + t[i];
+    const double iz = 1.0 / pc[2];
+    const double x = q[0], y = q[1], z = q[2], qw = q[3];
+    const double r2 = x * x + y * y + z * z + qw * qw;
+    const double rt[9] = {r2 - 2.0 * (y * y + z * z), 2.0 * (x * y - qw * z),
+                          2.0 * (x * z + qw * y),      2.0 * (x * y + qw * z),
+                          r2 - 2.0 * (z * z + x * x), 2.0 * (y * z - qw * x),
+                          2.0 * (x * z - qw * y),      2.0 * (y * z + qw * x),
+                          r2 - 2.0 * (x * x + y * y)};
+    const double ir2 = 1.0 / r2;
+    double R[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = rt[i] * ir2;
+    const double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+    double sig[9], ws[9], sc[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            sig[3 * i + j] = R[i] * s2[0] * R[j] + R[3 + i] * s2[1] * R[3 + j] +
+                             R[6 + i] * s2[2] * R[6 + j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            ws[3 * i + j] = w[3 * i] * sig[j] + w[3 * i + 1] * sig[3 + j] + w[3 * i + 2] * sig[6 + j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            sc[3 * i + j] = ws[3 * i] * w[3 * j] + ws[3 * i + 1] * w[3 * j + 1] +
+                            ws[3 * i + 2] * w[3 * j + 2];
+    const double j00 = fx * iz, j02 = -fx * pc[0] * iz * iz;
+    const double j11 = fy * iz, j12 = -fy * pc[1] * iz * iz;
+    const double js00 = j00 * sc[0] + j02 * sc[6], js01 = j00 * sc[1] + j02 * sc[7];
+    const double js02 = j00 * sc[2] + j02 * sc[8];
+    const double js11 = j11 * sc[4] + j12 * sc[7], js12 = j11 * sc[5] + j12 * sc[8];
+    const double c00 = js00 * j00 + js02 * j02 + lowpass;
+    const double c01 = js01 * j11 + js02 * j12;
+    const double c11 = js11 * j11 + js12 * j12 + lowpass;
+    const double det = c00 * c11 - c01 * c01;
+    const double idet = 1.0 / det;
+    const double i00 = c11 * idet, i01 = -c01 * idet, i11 = c00 * idet;
+    // ---- invert2x2 backward
+    const double a_det = -(a[2] * i00 + a[3] * i01 + a[4] * i11) * idet;
+    const double a_c00 = a[4] * idet + a_det * c11;
+    const double a_c11 = a[2] * idet + a_det * c00;
+    const double a_c01 = -a[3] * idet - 2.0 * a_det * c01;
+    // ---- J SC J^T backward
+    const double a_js00 = a_c00 * j00, a_js02 = a_c00 * j02 + a_c01 * j12;
+    const double a_js01 = a_c01 * j11, a_js11 = a_c11 * j11, a_js12 = a_c11 * j12;
+    double a_j00 = a_c00 * js00 + a_js00 * sc[0] + a_js01 * sc[1] + a_js02 * sc[2];
+    double a_j02 = a_c00 * js02 + a_js00 * sc[6] + a_js01 * sc[7] + a_js02 * sc[8];
+    double a_j11 = a_c01 * js01 + a_c11 * js11 + a_js11 * sc[4] + a_js12 * sc[5];
+    double a_j12 = a_c01 * js02 + a_c11 * js12 + a_js11 * sc[7] + a_js12 * sc[8];
+    double a_sc[9] = {a_js00 * j00, a_js01 * j00, a_js02 * j00,
+                      0.0,          a_js11 * j11, a_js12 * j11,
+                      a_js00 * j02, a_js01 * j02 + a_js11 * j12, a_js02 * j02 + a_js12 * j12};
+    // ---- SC = (W Sigma) W^T, WS = W Sigma backward
+    double a_ws[9], a_sig[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            a_ws[3 * i + k] = a_sc[3 * i] * w[k] + a_sc[3 * i + 1] * w[3 + k] + a_sc[3 * i + 2] * w[6 + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            a_sig[3 * k + j] = w[k] * a_ws[j] + w[3 + k] * a_ws[3 + j] + w[6 + k] * a_ws[6 + j];
+    // ---- Sigma = R^T diag(s^2) R backward
+    double a_R[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double as2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                acc += (a_sig[3 * i + j] + a_sig[3 * j + i]) * R[3 * k + j];
+                as2 += a_sig[3 * i + j] * R[3 * k + i] * R[3 * k + j];
+            }
+            a_R[3 * k + i] = s2[k] * acc;
+        }
+        gs[k] = 2.0 * s[k] * as2;
+    }
+    // ---- R = R~(q) / |q|^2 backward (dR~/dq_c as trust_region.cpp:95-117)
+    double a_r2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) a_r2 -= a_R[i] * R[i];
+    a_r2 *= ir2;
+    double art[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) art[i] = a_R[i] * ir2;
+    gq[0] = 2.0 * (x * (art[0] - art[4] - art[8]) + y * (art[1] + art[3]) +
+                   z * (art[2] + art[6]) + qw * (art[7] - art[5])) + 2.0 * x * a_r2;
+    gq[1] = 2.0 * (-y * (art[0] - art[4] + art[8]) + x * (art[1] + art[3]) +
+                   qw * (art[2] - art[6]) + z * (art[5] + art[7])) + 2.0 * y * a_r2;
+    gq[2] = 2.0 * (-z * (art[0] + art[4] - art[8]) + qw * (art[3] - art[1]) +
+                   x * (art[2] + art[6]) + y * (art[5] + art[7])) + 2.0 * z * a_r2;
+    gq[3] = 2.0 * (qw * (art[0] + art[4] + art[8]) + z * (art[3] - art[1]) +
+                   y * (art[2] - art[6]) + x * (art[7] - art[5])) + 2.0 * qw * a_r2;
+    // ---- J, mu2d, inverse depth, pc = W mu + t backward
+    double a_pc0 = a[0] * fx * iz - a_j02 * fx * iz * iz;
+    double a_pc1 = a[1] * fy * iz - a_j12 * fy * iz * iz;
+    const double a_iz = a[0] * fx * pc[0] + a[1] * fy * pc[1] + a_j00 * fx + a_j11 * fy -
+                        2.0 * a_j02 * fx * pc[0] * iz - 2.0 * a_j12 * fy * pc[1] * iz;
+    const double a_pc2 = -a_iz * iz * iz;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) gmu[k] = w[k] * a_pc0 + w[3 + k] * a_pc1 + w[6 + k] * a_pc2;
+}
+
 // pixel-centre range [p0, p1] inside the closed interval [lo, hi], clipped
 // to [0, n-1]; p0 > p1 means empty.  Exact: every comparison is between
 // p + 0.5 (exactly representable) and the FP64 bound itself.

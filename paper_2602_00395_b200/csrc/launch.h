@@ -125,10 +125,15 @@ struct TrArgs {
     double* partials;     // per block: sum g^2, sum dx^2, sum clipped^2, n_clip, max ratio
     int* bad_index;       // min index of a non-finite clipped coordinate
     int* degenerate_flag; // a splat with |q|^2 < 1e-24 reached shd_radii
+    double* dx_buf;       // Newton direction (dim)
+    double* eta_buf;      // trust-region radii (dim)
+    int* queue;           // (splat, rotation axis) pairs needing bisection (4K)
+    int* queue_count;
 };
 int tr_num_blocks(int K);
 void launch_tr_update(cudaStream_t st, const TrArgs& a);
 // 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
+// (partials hold 2 * tr_num_blocks(K) rows of 5)
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5);
 void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
                       const double caps[5], double* eta);

@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(256) k_project_jvp(const double* __restrict__ 
 }
 
 // K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
-// the fixed-order sum of its (tile, fragment) slots; the 5x10 Jacobian of
-// (mu2d, inverse covariance) w.r.t. (mu, s, q) is evaluated with the same 10
-// dual seeds the reference uses.
+// the fixed-order sum of its (tile, fragment) slots; the transpose of the 5x10
+// Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
+// reference evaluates with 10 dual seeds, is applied in one reverse sweep.
 __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restrict__ x, int K,
                                                DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
@@ -202,28 +202,16 @@ __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restric
 #pragma unroll
     for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
     if (any) {
+        // J^T a for (mu, s, q) in one reverse sweep (geometry.cuh)
         const Splat p = load_splat(x, K, id);
-        for (int seed = 0; seed < 10; ++seed) {
-            Dual mu[3], s[3], q[4];
+        double gmu[3], gs[3], gq[4];
+        chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                mu[c] = Dual(p.mu[c], seed == c ? 1.0 : 0.0);
-                s[c] = Dual(p.s[c], seed == 3 + c ? 1.0 : 0.0);
-            }
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu[c]);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) q[c] = Dual(p.q[c], seed == 6 + c ? 1.0 : 0.0);
-            const Proj<Dual> pr = project<Dual>(mu, s, q, cam.w, cam.t, cam.fx, cam.fy, cam.cx,
-                                                cam.cy, ro.z_near, ro.lowpass);
-            if (pr.culled) break;
-            Dual i00, i01, i11;
-            invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
-            const double dot = a[0] * pr.mx.d + a[1] * pr.my.d + a[2] * i00.d +
-                               a[3] * i01.d + a[4] * i11.d;
-            const long long off = seed < 3 ? 3LL * id + seed
-                                           : (seed < 6 ? 3 * k + 3LL * id + (seed - 3)
-                                                       : 6 * k + 4LL * id + (seed - 6));
-            add(off, dot);
-        }
+        for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
     }
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }

@@ -1,11 +1,15 @@
 // raster.cu — tile rasteriser: K7 forward blend, K10 reverse-order VJP,
 // K12 forward-mode JVP.
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's fragment list
+// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
+// block so that the per-fragment bounding-box test can first be done once per
+// warp (uniform branch) against the block's span of pixel centres — most
+// (pixel, fragment) pairs of a tile list fail the reference's bbox test
+// (render.cpp:129-131), and whole warps skip them.  The tile's fragment list
 // (depth order, from binning.cu) is staged through shared memory in batches;
 // each 128-byte fragment record is copied by 8 lanes (one full cache line per
-// record, 4 records per warp instruction), and every pixel then reads the
-// staged record as a warp-wide broadcast.
+// record, 4 records per warp instruction), and every pixel reads the staged
+// record as a warp-wide broadcast.
 //
 // Branch parity: the three kernels evaluate the primal alpha with the same
 // pinned operation sequence (no FMA; identical to the oracle's restatement
@@ -22,22 +26,32 @@ namespace {
 constexpr int kThreads = kTilePixels;  // 256
 constexpr int kFwdBatch = 256;
 constexpr int kVjpBatch = 64;
+constexpr int kJvpBatch = 128;
 constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
 
 struct PixelCtx {
     int px, py;
     bool inside;
     double pxc, pyc;
+    double wx0, wx1, wy0, wy1;  // the warp's span of pixel centres
 };
 
+// warp w covers columns (w & 1) * 8 .. +7 and rows (w >> 1) * 4 .. +3
 __device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H) {
     PixelCtx p;
-    const int tx = tile % tiles_x, ty = tile / tiles_x;
-    p.px = tx * kTile + (threadIdx.x & (kTile - 1));
-    p.py = ty * kTile + (threadIdx.x / kTile);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int x0 = (tile % tiles_x) * kTile + (warp & 1) * 8;
+    const int y0 = (tile / tiles_x) * kTile + (warp >> 1) * 4;
+    p.px = x0 + (lane & 7);
+    p.py = y0 + (lane >> 3);
     p.inside = p.px < W && p.py < H;
     p.pxc = p.px + 0.5;
     p.pyc = p.py + 0.5;
+    p.wx0 = x0 + 0.5;
+    p.wx1 = x0 + 7.5;
+    p.wy0 = y0 + 0.5;
+    p.wy1 = y0 + 3.5;
     return p;
 }
 
@@ -51,6 +65,12 @@ __device__ __forceinline__ double eval_expo(double dx, double dy, const double* 
 
 __device__ __forceinline__ bool outside_bbox(double pxc, double pyc, const double* f) {
     return pxc < f[R_BX0] || pxc > f[R_BX1] || pyc < f[R_BY0] || pyc > f[R_BY1];
+}
+
+// true when no pixel centre of the warp's block lies in the fragment's bbox
+// (warp-uniform: every lane evaluates the same broadcast values)
+__device__ __forceinline__ bool warp_misses(const PixelCtx& p, const double* f) {
+    return p.wx1 < f[R_BX0] || p.wx0 > f[R_BX1] || p.wy1 < f[R_BY0] || p.wy0 > f[R_BY1];
 }
 
 // cooperative staging: 8 lanes per 128-byte record; entries [b, b+n) of the
@@ -105,33 +125,35 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
         const int n = min(kFwdBatch, end - b);
         stage_records(tl, rec, b, n, s_rec, nullptr);
         __syncthreads();
-        if (!done) {
-            for (int jj = 0; jj < n; ++jj) {
-                const double* f = s_rec + kRec * jj;
-                if (outside_bbox(pc.pxc, pc.pyc, f)) continue;
+        if (__all_sync(kFull, done)) continue;
+        for (int jj = 0; jj < n; ++jj) {
+            const double* f = s_rec + kRec * jj;
+            if (warp_misses(pc, f)) continue;
+            if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
                 if (kCount) ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar < ro.alpha_skip) continue;
-                if (kCount) ++n_contrib;
-                const double w = abar * T;
-                c0 += f[R_C0] * w;
-                c1 += f[R_C1] * w;
-                c2 += f[R_C2] * w;
-                T = __dmul_rn(T, __dsub_rn(1.0, abar));
-                if (T < ro.t_stop) {
-                    done = true;
-                    processed = b - start + jj + 1;
-                    break;
+                if (abar >= ro.alpha_skip) {
+                    if (kCount) ++n_contrib;
+                    const double w = abar * T;
+                    c0 += f[R_C0] * w;
+                    c1 += f[R_C1] * w;
+                    c2 += f[R_C2] * w;
+                    T = __dmul_rn(T, __dsub_rn(1.0, abar));
+                    if (T < ro.t_stop) {
+                        done = true;
+                        processed = b - start + jj + 1;
+                    }
                 }
             }
+            if (__all_sync(kFull, done)) break;
         }
     }
     if (kCount) {
         for (int o = 16; o > 0; o >>= 1) {
-            n_eval += __shfl_xor_sync(0xffffffffu, n_eval, o);
-            n_contrib += __shfl_xor_sync(0xffffffffu, n_contrib, o);
+            n_eval += __shfl_xor_sync(kFull, n_eval, o);
+            n_contrib += __shfl_xor_sync(kFull, n_contrib, o);
         }
         if ((threadIdx.x & 31) == 0) {
             atomicAdd(counters, n_eval);
@@ -148,10 +170,37 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
 }
 
 // ------------------------------------------------------------------ K10
-__device__ __forceinline__ double warp_sum(double v) {
+// Transposed butterfly: sums g[0..7] over the warp so that lane l with
+// (l & 3) == 0 ends with the total of g[l >> 2] (9 shuffles instead of 40),
+// and g[8] with a plain butterfly (lane 0 keeps it).  Fixed order, so the
+// result is deterministic.
+__device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane, double& v8) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    double h4[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? g[i] : g[4 + i];
+        const double keep = b4 ? g[4 + i] : g[i];
+        h4[i] = keep + __shfl_xor_sync(kFull, send, 16);
+    }
+    double h2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? h4[i] : h4[2 + i];
+        const double keep = b3 ? h4[2 + i] : h4[i];
+        h2[i] = keep + __shfl_xor_sync(kFull, send, 8);
+    }
+    {
+        const double send = b2 ? h2[0] : h2[1];
+        const double keep = b2 ? h2[1] : h2[0];
+        v_lane = keep + __shfl_xor_sync(kFull, send, 4);
+    }
+    v_lane += __shfl_xor_sync(kFull, v_lane, 2);
+    v_lane += __shfl_xor_sync(kFull, v_lane, 1);
+    double s = g[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    v8 = s;
 }
 
 __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
@@ -164,6 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
     __shared__ __align__(16) double s_rec[kVjpBatch * kRec];
     __shared__ double s_red[kWarps][kVjpBatch][kAdj];
     __shared__ int s_d[kVjpBatch];
+    __shared__ unsigned s_mask[kVjpBatch];
     __shared__ int s_maxlast[kWarps];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -184,10 +234,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
     if (!active) lastp = 0;
     double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;  // "behind"
     // entries past every pixel's last processed fragment get zero slots
-    int ml = __reduce_max_sync(0xffffffffu, lastp);
-    if (lane == 0) s_maxlast[warp] = ml;
+    const int wlast = __reduce_max_sync(kFull, lastp);
+    if (lane == 0) s_maxlast[warp] = wlast;
     __syncthreads();
-    ml = 0;
+    int ml = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) ml = max(ml, s_maxlast[w]);
     const int hi = start + ml;
@@ -201,14 +251,18 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
         const int n = bend - bstart;
         __syncthreads();
         stage_records(tl, rec, bstart, n, s_rec, s_d);
+        if (threadIdx.x < n) s_mask[threadIdx.x] = 0u;
         __syncthreads();
         for (int jj = n - 1; jj >= 0; --jj) {
+            const int rel = bstart - start + jj;
+            if (rel >= wlast) continue;
             const double* f = s_rec + kRec * jj;
+            if (warp_misses(pc, f)) continue;
             double g[kAdj];
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
             bool contrib = false;
-            if (bstart - start + jj < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
+            if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 const double gauss = exp(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
@@ -240,21 +294,23 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
                     T = t_in;
                 }
             }
-            if (__any_sync(0xffffffffu, contrib)) {
-#pragma unroll
-                for (int c = 0; c < kAdj; ++c) g[c] = warp_sum(g[c]);
-            }
+            if (!__any_sync(kFull, contrib)) continue;
+            double v, v8;
+            warp_reduce9(g, lane, v, v8);
+            if ((lane & 3) == 0) s_red[warp][jj][lane >> 2] = v;
             if (lane == 0) {
-#pragma unroll
-                for (int c = 0; c < kAdj; ++c) s_red[warp][jj][c] = g[c];
+                s_red[warp][jj][8] = v8;
+                atomicOr(&s_mask[jj], 1u << warp);
             }
         }
         __syncthreads();
         for (int idx = threadIdx.x; idx < n * kAdj; idx += kThreads) {
             const int jj = idx / kAdj, c = idx % kAdj;
+            const unsigned m = s_mask[jj];
             double s = 0.0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) s += s_red[w][jj][c];
+            for (int w = 0; w < kWarps; ++w)
+                if (m & (1u << w)) s += s_red[w][jj][c];
             slots[(long long)kAdj * s_d[jj] + c] = s;
         }
     }
@@ -266,26 +322,25 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
                                                          const double* __restrict__ trec, int W,
                                                          int H, RenderP ro,
                                                          double* __restrict__ tangent) {
-    constexpr int kB = 128;
-    __shared__ __align__(16) double s_rec[kB * kRec];
-    __shared__ __align__(16) double s_t[kB * kTRec];
+    __shared__ __align__(16) double s_rec[kJvpBatch * kRec];
+    __shared__ __align__(16) double s_t[kJvpBatch * kTRec];
     const int tile = blockIdx.x;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0;
-    Dual Td(1.0, 0.0);
+    double T = 1.0, dT = 0.0;
     double d0 = 0.0, d1 = 0.0, d2 = 0.0;
     bool done = !pc.inside;
-    for (int b = start; b < end; b += kB) {
+    for (int b = start; b < end; b += kJvpBatch) {
         if (__syncthreads_and(done)) break;
-        const int n = min(kB, end - b);
+        const int n = min(kJvpBatch, end - b);
         stage_records(tl, rec, b, n, s_rec, nullptr);
         stage_tangents(tl, trec, b, n, s_t);
         __syncthreads();
-        if (!done) {
-            for (int jj = 0; jj < n; ++jj) {
-                const double* f = s_rec + kRec * jj;
-                if (outside_bbox(pc.pxc, pc.pyc, f)) continue;
+        if (__all_sync(kFull, done)) continue;
+        for (int jj = 0; jj < n; ++jj) {
+            const double* f = s_rec + kRec * jj;
+            if (warp_misses(pc, f)) continue;
+            if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double* t = s_t + kTRec * jj;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 const double e = exp(eval_expo(dx, dy, f));
@@ -300,28 +355,27 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
                     abar = ro.alpha_clamp;
                     dabar = 0.0;
                 }
-                if (abar < ro.alpha_skip) continue;
-                // w = abar * T ; acc += c * w ; T = T * (1 - abar)
-                const double w = abar * T;
-                const double dw = dabar * T + abar * Td.d;
-                d0 += t[T_C0] * w + f[R_C0] * dw;
-                d1 += t[T_C1] * w + f[R_C1] * dw;
-                d2 += t[T_C2] * w + f[R_C2] * dw;
-                const double om = __dsub_rn(1.0, abar);
-                Td.d = Td.d * om + T * (-dabar);
-                T = __dmul_rn(T, om);
-                if (T < ro.t_stop) {
-                    done = true;
-                    break;
+                if (abar >= ro.alpha_skip) {
+                    // w = abar * T ; acc += c * w ; T = T * (1 - abar)
+                    const double w = abar * T;
+                    const double dw = dabar * T + abar * dT;
+                    d0 += t[T_C0] * w + f[R_C0] * dw;
+                    d1 += t[T_C1] * w + f[R_C1] * dw;
+                    d2 += t[T_C2] * w + f[R_C2] * dw;
+                    const double om = __dsub_rn(1.0, abar);
+                    dT = dT * om + T * (-dabar);
+                    T = __dmul_rn(T, om);
+                    if (T < ro.t_stop) done = true;
                 }
             }
+            if (__all_sync(kFull, done)) break;
         }
     }
     if (!pc.inside) return;
     const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    tangent[p] = d0 + ro.bg[0] * Td.d;
-    tangent[P + p] = d1 + ro.bg[1] * Td.d;
-    tangent[2 * P + p] = d2 + ro.bg[2] * Td.d;
+    tangent[p] = d0 + ro.bg[0] * dT;
+    tangent[P + p] = d1 + ro.bg[1] * dT;
+    tangent[2 * P + p] = d2 + ro.bg[2] * dT;
 }
 
 }  // namespace

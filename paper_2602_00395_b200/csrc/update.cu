@@ -45,6 +45,23 @@ struct Prim {
     double mu[3], s[3], q[4], alpha, c[3];
 };
 
+__device__ __forceinline__ void set9(double* d, double a0, double a1, double a2, double a3,
+                                     double a4, double a5, double a6, double a7, double a8) {
+    d[0] = a0; d[1] = a1; d[2] = a2; d[3] = a3; d[4] = a4;
+    d[5] = a5; d[6] = a6; d[7] = a7; d[8] = a8;
+}
+
+// dR~/dq_c (trust_region.cpp:95-117)
+__device__ __forceinline__ void quat_drt(double x, double y, double z, double w, int axis,
+                                         double* d) {
+    switch (axis) {
+        case 0: set9(d, 2 * x, 2 * y, 2 * z, 2 * y, -2 * x, -2 * w, 2 * z, 2 * w, -2 * x); break;
+        case 1: set9(d, -2 * y, 2 * x, 2 * w, 2 * x, 2 * y, 2 * z, -2 * w, 2 * z, -2 * y); break;
+        case 2: set9(d, -2 * z, -2 * w, 2 * x, 2 * w, -2 * z, 2 * y, 2 * x, 2 * y, 2 * z); break;
+        default: set9(d, 2 * w, -2 * z, 2 * y, 2 * z, 2 * w, -2 * x, -2 * y, 2 * x, 2 * w); break;
+    }
+}
+
 // trust_region.cpp:54-69 (inverse diagonal by cofactors)
 __device__ void radius_mean(const Prim& p, double eps, double cap, double* out) {
     const double lf = log_factor(eps, p.alpha);
@@ -73,36 +90,18 @@ __device__ void radius_mean(const Prim& p, double eps, double cap, double* out) 
 __device__ double beta_rotation(const Prim& p, int axis) {
     const double x = p.q[0], y = p.q[1], z = p.q[2], w = p.q[3];
     const double r2 = x * x + y * y + z * z + w * w;
-    const double qc = p.q[axis];
+    const double qc = axis == 0 ? x : (axis == 1 ? y : (axis == 2 ? z : w));
     const double rt[9] = {r2 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z),
                           2.0 * (x * z + w * y),      2.0 * (x * y + w * z),
                           r2 - 2.0 * (z * z + x * x), 2.0 * (y * z - w * x),
                           2.0 * (x * z - w * y),      2.0 * (y * z + w * x),
                           r2 - 2.0 * (x * x + y * y)};
     double drt[9];
-    switch (axis) {
-        case 0: {
-            const double t[9] = {2 * x, 2 * y, 2 * z, 2 * y, -2 * x, -2 * w, 2 * z, 2 * w, -2 * x};
-            for (int i = 0; i < 9; ++i) drt[i] = t[i];
-        } break;
-        case 1: {
-            const double t[9] = {-2 * y, 2 * x, 2 * w, 2 * x, 2 * y, 2 * z, -2 * w, 2 * z, -2 * y};
-            for (int i = 0; i < 9; ++i) drt[i] = t[i];
-        } break;
-        case 2: {
-            const double t[9] = {-2 * z, -2 * w, 2 * x, 2 * w, -2 * z, 2 * y, 2 * x, 2 * y, 2 * z};
-            for (int i = 0; i < 9; ++i) drt[i] = t[i];
-        } break;
-        default: {
-            const double t[9] = {2 * w, -2 * z, 2 * y, 2 * z, 2 * w, -2 * x, -2 * y, 2 * x, 2 * w};
-            for (int i = 0; i < 9; ++i) drt[i] = t[i];
-        } break;
-    }
-    const double dg[4][3] = {{2, -2, -2}, {-2, 2, -2}, {-2, -2, 2}, {2, 2, 2}};
+    quat_drt(x, y, z, w, axis, drt);
     double d2rt[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    d2rt[0] = dg[axis][0];
-    d2rt[4] = dg[axis][1];
-    d2rt[8] = dg[axis][2];
+    d2rt[0] = (axis == 0 || axis == 3) ? 2.0 : -2.0;
+    d2rt[4] = (axis == 1 || axis == 3) ? 2.0 : -2.0;
+    d2rt[8] = (axis == 2 || axis == 3) ? 2.0 : -2.0;
     double r[9];
     for (int i = 0; i < 9; ++i) r[i] = rt[i] / r2;
     const double k1 = 2.0 * qc / (r2 * r2);
@@ -126,54 +125,81 @@ __device__ double beta_rotation(const Prim& p, int axis) {
     return 2.0 * frob + 2.0 * tr;
 }
 
-// trust_region.cpp:183-194
-__device__ double rotation_h2(const Prim& p, const double* sigma, double det_s, int axis,
-                              double dq) {
-    double q2[4] = {p.q[0], p.q[1], p.q[2], p.q[3]};
-    q2[axis] += dq;
-    if (q2[0] * q2[0] + q2[1] * q2[1] + q2[2] * q2[2] + q2[3] * q2[3] < 1e-24) return CUDART_INF;
-    double c2[9], mid[9];
-    covariance(p.s, q2, c2);
-    for (int i = 0; i < 9; ++i) mid[i] = 0.5 * (sigma[i] + c2[i]);
-    const double dm = det3(mid);
-    if (!(dm > 0.0)) return CUDART_INF;
-    return p.alpha * (1.0 - det_s / sqrt(dm));
+// Rotation-only squared Hellinger (trust_region.cpp:183-194) as a function of
+// dq along axis c, evaluated from per-axis precomputed terms: R~(q + dq e_c)
+// = R~(q) + dq dR~/dq_c + dq^2 diag(d2R~/dq_c^2)/2 exactly (R~ is quadratic),
+// and R^T S^2 R = R~^T S^2 R~ / |q'|^4.  Same quantity as the reference's
+// covariance() path with one division instead of nine; differences are at the
+// rounding level of the 1 - det_s/sqrt(det) cancellation the reference has too.
+struct RotAxis {
+    double rt[9], drt[9], h[3];
+    double r2, qc, s2[3], sigma[9], det_s, alpha;
+};
+
+__device__ void rot_axis_setup(const Prim& p, const double* sigma, int axis, RotAxis& ra) {
+    const double x = p.q[0], y = p.q[1], z = p.q[2], w = p.q[3];
+    ra.r2 = x * x + y * y + z * z + w * w;
+    ra.qc = axis == 0 ? x : (axis == 1 ? y : (axis == 2 ? z : w));
+    const double rt[9] = {ra.r2 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z),
+                          2.0 * (x * z + w * y),         2.0 * (x * y + w * z),
+                          ra.r2 - 2.0 * (z * z + x * x), 2.0 * (y * z - w * x),
+                          2.0 * (x * z - w * y),         2.0 * (y * z + w * x),
+                          ra.r2 - 2.0 * (x * x + y * y)};
+    for (int i = 0; i < 9; ++i) ra.rt[i] = rt[i];
+    quat_drt(x, y, z, w, axis, ra.drt);
+    // diag(d2R~/dq_c^2) / 2 (trust_region.cpp:119-128)
+    ra.h[0] = (axis == 0 || axis == 3) ? 1.0 : -1.0;
+    ra.h[1] = (axis == 1 || axis == 3) ? 1.0 : -1.0;
+    ra.h[2] = (axis == 2 || axis == 3) ? 1.0 : -1.0;
+    for (int i = 0; i < 3; ++i) ra.s2[i] = p.s[i] * p.s[i];
+    for (int i = 0; i < 9; ++i) ra.sigma[i] = sigma[i];
+    ra.det_s = p.s[0] * p.s[1] * p.s[2];
+    ra.alpha = p.alpha;
 }
 
-// trust_region.cpp:198-234 (Taylor radius, certified, bisected if needed)
-__device__ void radius_rotation(const Prim& p, double eps, double cap, double* out) {
-    const double lf = log_factor(eps, p.alpha);
-    if (lf <= 0.0) {
-        out[0] = out[1] = out[2] = out[3] = cap;
-        return;
+__device__ double rot_h2(const RotAxis& ra, double dq) {
+    const double r2p = ra.r2 + dq * (2.0 * ra.qc + dq);
+    if (r2p < 1e-24) return CUDART_INF;
+    double m[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) m[i] = ra.rt[i] + dq * ra.drt[i];
+    m[0] += dq * dq * ra.h[0];
+    m[4] += dq * dq * ra.h[1];
+    m[8] += dq * dq * ra.h[2];
+    const double inv = 1.0 / (r2p * r2p);
+    double c[6];  // (R~^T S^2 R~)_{00,01,02,11,12,22}
+    const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+        const int i = ij[e][0], j = ij[e][1];
+        c[e] = (m[i] * ra.s2[0] * m[j] + m[3 + i] * ra.s2[1] * m[3 + j] +
+                m[6 + i] * ra.s2[2] * m[6 + j]) * inv;
     }
-    double sigma[9];
-    if (!covariance(p.s, p.q, sigma)) {
-        out[0] = out[1] = out[2] = out[3] = cap;
-        return;
+    const double mid[9] = {0.5 * (ra.sigma[0] + c[0]), 0.5 * (ra.sigma[1] + c[1]),
+                           0.5 * (ra.sigma[2] + c[2]), 0.5 * (ra.sigma[3] + c[1]),
+                           0.5 * (ra.sigma[4] + c[3]), 0.5 * (ra.sigma[5] + c[4]),
+                           0.5 * (ra.sigma[6] + c[2]), 0.5 * (ra.sigma[7] + c[4]),
+                           0.5 * (ra.sigma[8] + c[5])};
+    const double dm = det3(mid);
+    if (!(dm > 0.0)) return CUDART_INF;
+    return ra.alpha * (1.0 - ra.det_s / sqrt(dm));
+}
+
+__device__ __forceinline__ bool rot_within(const RotAxis& ra, double st, double tol) {
+    return rot_h2(ra, st) <= tol && rot_h2(ra, -st) <= tol;
+}
+
+// the reference's 60-step bisection down to the constraint boundary
+__device__ double rot_bisect(const RotAxis& ra, double r, double tol) {
+    double lo = 0.0, hi = r;
+    for (int it = 0; it < 60; ++it) {
+        const double mid = 0.5 * (lo + hi);
+        if (rot_within(ra, mid, tol))
+            lo = mid;
+        else
+            hi = mid;
     }
-    const double det_s = p.s[0] * p.s[1] * p.s[2];
-    const double tol = eps * (1.0 + 1e-9);
-    for (int c = 0; c < 4; ++c) {
-        const double beta = beta_rotation(p, c);
-        double r = beta <= 1e-12 ? cap : cap_radius(sqrt(lf / beta), cap);
-        auto within = [&](double st) {
-            return rotation_h2(p, sigma, det_s, c, st) <= tol &&
-                   rotation_h2(p, sigma, det_s, c, -st) <= tol;
-        };
-        if (!within(r)) {
-            double lo = 0.0, hi = r;
-            for (int it = 0; it < 60; ++it) {
-                const double mid = 0.5 * (lo + hi);
-                if (within(mid))
-                    lo = mid;
-                else
-                    hi = mid;
-            }
-            r = lo > 0.0 ? lo : r * 0x1.0p-60;
-        }
-        out[c] = r;
-    }
+    return lo > 0.0 ? lo : r * 0x1.0p-60;
 }
 
 __device__ void radii(const Prim& p, double eps, const double* caps, double* eta) {
@@ -182,8 +208,23 @@ __device__ void radii(const Prim& p, double eps, const double* caps, double* eta
         eta[3 + c] = cap_radius(sqrt(2.0 * p.s[c] * p.s[c] * eps / p.alpha), caps[1]);
         eta[11 + c] = cap_radius(sqrt(4.0 * p.c[c] * eps / p.alpha), caps[4]);
     }
-    radius_rotation(p, eps, caps[2], eta + 6);
     eta[10] = cap_radius(sqrt(4.0 * p.alpha * eps), caps[3]);
+    // rotation (trust_region.cpp:198-234)
+    const double lf = log_factor(eps, p.alpha);
+    double sigma[9];
+    if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
+        for (int c = 0; c < 4; ++c) eta[6 + c] = caps[2];
+        return;
+    }
+    const double tol = eps * (1.0 + 1e-9);
+    for (int c = 0; c < 4; ++c) {
+        const double beta = beta_rotation(p, c);
+        double r = beta <= 1e-12 ? caps[2] : cap_radius(sqrt(lf / beta), caps[2]);
+        RotAxis ra;
+        rot_axis_setup(p, sigma, c, ra);
+        if (!rot_within(ra, r, tol)) r = rot_bisect(ra, r, tol);
+        eta[6 + c] = r;
+    }
 }
 
 // flat index of local coordinate j (0..13) of splat i in the group-major layout
@@ -207,69 +248,11 @@ __device__ __forceinline__ Prim load_prim(const double* __restrict__ x, long lon
     return p;
 }
 
-__global__ void __launch_bounds__(kThreads) k_tr_update(TrArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const long long K = a.K;
-    double sg = 0.0, sdx = 0.0, scl = 0.0, nclip = 0.0, mr = 0.0;
-    int bad = INT_MAX;
-    if (i < a.K) {
-        const Prim p = load_prim(a.x, K, i);
-        if (!a.ghat_only && p.q[0] * p.q[0] + p.q[1] * p.q[1] + p.q[2] * p.q[2] +
-                                    p.q[3] * p.q[3] < 1e-24)
-            atomicOr(a.degenerate_flag, 1);  // quat_to_rotation throws in shd_radii
-        double dx[14];
-        for (int j = 0; j < 14; ++j) {
-            const long long k = flat_index(K, i, j);
-            const double g = a.g_acc[k] * a.gscale;
-            sg += g * g;
-            const double gh = a.theta1 * a.g_hat[k] + (1.0 - a.theta1) * g;
-            a.g_hat[k] = gh;
-            if (a.ghat_only) continue;
-            double dh = a.d_hat[k];
-            if (a.refresh) {
-                const double d = a.w_acc[k] * a.dscale;
-                dh = a.theta2 * dh + (1.0 - a.theta2) * d;
-                a.d_hat[k] = dh;
-            }
-            // std::max(d, gamma) returns d unless d < gamma (NaN d -> d)
-            dx[j] = -gh / ((dh < a.gamma_d) ? a.gamma_d : dh);
-            sdx += dx[j] * dx[j];
-        }
-        if (!a.ghat_only) {
-            double eta[14];
-            radii(p, a.eps, a.caps, eta);
-            double xo[14];
-            for (int j = 0; j < 14; ++j) {
-                const long long k = flat_index(K, i, j);
-                // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
-                double c = dx[j] < -eta[j] ? -eta[j] : dx[j];
-                c = eta[j] < c ? eta[j] : c;
-                if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
-                if (fabs(dx[j]) > eta[j]) nclip += 1.0;
-                const double ratio = fabs(c) / eta[j];
-                mr = mr < ratio ? ratio : mr;
-                scl += c * c;
-                if (a.applied) a.applied[k] = c;
-                xo[j] = a.x[k] + c;
-            }
-            // Scene::clamp (scene.cpp:49-57)
-            for (int c = 0; c < 3; ++c) {
-                double& s = xo[3 + c];
-                s = s < a.bounds[0] ? a.bounds[0] : s;
-                double& col = xo[11 + c];
-                col = col < a.bounds[3] ? a.bounds[3] : col;
-                col = a.bounds[4] < col ? a.bounds[4] : col;
-            }
-            double& al = xo[10];
-            al = al < a.bounds[1] ? a.bounds[1] : al;
-            al = a.bounds[2] < al ? a.bounds[2] : al;
-            for (int j = 0; j < 14; ++j) a.x_out[flat_index(K, i, j)] = xo[j];
-        }
-    }
-    // deterministic block reduction of the diagnostics
+// deterministic block reduction of up to 5 values (sums, with value 4 a max)
+// and a min index; thread 0 stores them at out[0..4] and folds bad into *bad
+__device__ void block_reduce5(double* v, int bad, double* out, int* bad_out) {
     __shared__ double s_red[5][kThreads / 32];
     __shared__ int s_bad[kThreads / 32];
-    double v[5] = {sg, sdx, scl, nclip, mr};
     for (int o = 16; o > 0; o >>= 1) {
         for (int q = 0; q < 4; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
         const double m = __shfl_xor_sync(0xffffffffu, v[4], o);
@@ -290,9 +273,125 @@ __global__ void __launch_bounds__(kThreads) k_tr_update(TrArgs a) {
             r[4] = r[4] < s_red[4][w] ? s_red[4][w] : r[4];
             b = min(b, s_bad[w]);
         }
-        for (int q = 0; q < 5; ++q) a.partials[5LL * blockIdx.x + q] = r[q];
-        if (b != INT_MAX) atomicMin(a.bad_index, b);
+        for (int q = 0; q < 5; ++q) out[q] = r[q];
+        if (bad_out && b != INT_MAX) atomicMin(bad_out, b);
     }
+}
+
+// K14a: EMAs, Newton direction and all radii; rotation axes whose Taylor
+// radius fails certification are queued for K14b
+__global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long K = a.K;
+    double v[5] = {0, 0, 0, 0, 0};  // sum g^2, sum dx^2
+    if (i < a.K) {
+        const Prim p = load_prim(a.x, K, i);
+        const bool degenerate =
+            p.q[0] * p.q[0] + p.q[1] * p.q[1] + p.q[2] * p.q[2] + p.q[3] * p.q[3] < 1e-24;
+        if (!a.ghat_only && degenerate) atomicOr(a.degenerate_flag, 1);
+        for (int j = 0; j < 14; ++j) {
+            const long long k = flat_index(K, i, j);
+            const double g = a.g_acc[k] * a.gscale;
+            v[0] += g * g;
+            const double gh = a.theta1 * a.g_hat[k] + (1.0 - a.theta1) * g;
+            a.g_hat[k] = gh;
+            if (a.ghat_only) continue;
+            double dh = a.d_hat[k];
+            if (a.refresh) {
+                const double d = a.w_acc[k] * a.dscale;
+                dh = a.theta2 * dh + (1.0 - a.theta2) * d;
+                a.d_hat[k] = dh;
+            }
+            // std::max(d, gamma) returns d unless d < gamma (NaN d -> d)
+            const double dx = -gh / ((dh < a.gamma_d) ? a.gamma_d : dh);
+            v[1] += dx * dx;
+            a.dx_buf[k] = dx;
+        }
+        if (!a.ghat_only && !degenerate) {
+            double eta[14];
+            radius_mean(p, a.eps, a.caps[0], eta);
+            for (int c = 0; c < 3; ++c) {
+                eta[3 + c] = cap_radius(sqrt(2.0 * p.s[c] * p.s[c] * a.eps / p.alpha), a.caps[1]);
+                eta[11 + c] = cap_radius(sqrt(4.0 * p.c[c] * a.eps / p.alpha), a.caps[4]);
+            }
+            eta[10] = cap_radius(sqrt(4.0 * p.alpha * a.eps), a.caps[3]);
+            // rotation (trust_region.cpp:198-234): Taylor radius + certification
+            const double lf = log_factor(a.eps, p.alpha);
+            double sigma[9];
+            if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
+                for (int c = 0; c < 4; ++c) eta[6 + c] = a.caps[2];
+            } else {
+                const double tol = a.eps * (1.0 + 1e-9);
+                for (int c = 0; c < 4; ++c) {
+                    const double beta = beta_rotation(p, c);
+                    const double r =
+                        beta <= 1e-12 ? a.caps[2] : cap_radius(sqrt(lf / beta), a.caps[2]);
+                    eta[6 + c] = r;
+                    RotAxis ra;
+                    rot_axis_setup(p, sigma, c, ra);
+                    if (!rot_within(ra, r, tol)) {
+                        const int slot = atomicAdd(a.queue_count, 1);
+                        a.queue[slot] = 4 * i + c;
+                    }
+                }
+            }
+            for (int j = 0; j < 14; ++j) a.eta_buf[flat_index(K, i, j)] = eta[j];
+        }
+    }
+    block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
+}
+
+// K14b: one thread per queued (splat, rotation axis): the 60-step bisection
+__global__ void __launch_bounds__(kThreads) k_tr_bisect(TrArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= *a.queue_count) return;
+    const int i = a.queue[t] >> 2, c = a.queue[t] & 3;
+    const long long K = a.K;
+    const Prim p = load_prim(a.x, K, i);
+    double sigma[9];
+    covariance(p.s, p.q, sigma);
+    RotAxis ra;
+    rot_axis_setup(p, sigma, c, ra);
+    const long long k = 6 * K + 4LL * i + c;
+    a.eta_buf[k] = rot_bisect(ra, a.eta_buf[k], a.eps * (1.0 + 1e-9));
+}
+
+// K14c: clip, step statistics, apply and clamp (optimizer.cpp:124-142)
+__global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long K = a.K;
+    double v[5] = {0, 0, 0, 0, 0};  // -, -, sum clipped^2, n clipped, max ratio
+    int bad = INT_MAX;
+    if (i < a.K) {
+        double xo[14];
+        for (int j = 0; j < 14; ++j) {
+            const long long k = flat_index(K, i, j);
+            const double dx = a.dx_buf[k], eta = a.eta_buf[k];
+            // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
+            double c = dx < -eta ? -eta : dx;
+            c = eta < c ? eta : c;
+            if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
+            if (fabs(dx) > eta) v[3] += 1.0;
+            const double ratio = fabs(c) / eta;
+            v[4] = v[4] < ratio ? ratio : v[4];
+            v[2] += c * c;
+            if (a.applied) a.applied[k] = c;
+            xo[j] = a.x[k] + c;
+        }
+        // Scene::clamp (scene.cpp:49-57)
+        for (int c = 0; c < 3; ++c) {
+            double& sc = xo[3 + c];
+            sc = sc < a.bounds[0] ? a.bounds[0] : sc;
+            double& col = xo[11 + c];
+            col = col < a.bounds[3] ? a.bounds[3] : col;
+            col = a.bounds[4] < col ? a.bounds[4] : col;
+        }
+        double& al = xo[10];
+        al = al < a.bounds[1] ? a.bounds[1] : al;
+        al = a.bounds[2] < al ? a.bounds[2] : al;
+        for (int j = 0; j < 14; ++j) a.x_out[flat_index(K, i, j)] = xo[j];
+    }
+    block_reduce5(v, bad, a.partials + 5LL * (gridDim.x + blockIdx.x), a.bad_index);
 }
 
 __global__ void k_tr_finalize(const double* __restrict__ partials, int nblocks, double* out) {
@@ -343,12 +442,24 @@ int tr_num_blocks(int K) { return ceil_div(K, kThreads); }
 
 void launch_tr_update(cudaStream_t st, const TrArgs& a) {
     if (a.K == 0) return;
-    k_tr_update<<<tr_num_blocks(a.K), kThreads, 0, st>>>(a);
+    const int nb = tr_num_blocks(a.K);
+    SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
+    k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
+    SGTR_CUDA(cudaGetLastError());
+    if (a.ghat_only) {
+        SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
+        return;
+    }
+    k_tr_bisect<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
+    SGTR_CUDA(cudaGetLastError());
+    k_tr_apply<<<nb, kThreads, 0, st>>>(a);
     SGTR_CUDA(cudaGetLastError());
 }
 
+// partials: [nblocks][5] from K14a (sum g^2, sum dx^2) then [nblocks][5] from
+// K14c (sum clipped^2, n clipped, max ratio)
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5) {
-    k_tr_finalize<<<1, 256, 0, st>>>(partials, nblocks, out5);
+    k_tr_finalize<<<1, 256, 0, st>>>(partials, 2 * nblocks, out5);
     SGTR_CUDA(cudaGetLastError());
 }
 
