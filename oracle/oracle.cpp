@@ -1391,10 +1391,45 @@ int orc_project(const double* x, int64_t k, const orc_camera* cam,
     });
 }
 
-// Restated tile binning.  A visible fragment belongs to tile (tx, ty) iff
-// its closed bbox contains at least one pixel centre (x+0.5, y+0.5) of that
-// tile inside the image — exactly the pixels whose bbox test in blend()
-// passes (render.cpp:129-131).  Lists are in (depth, index) order.
+// Conservative contribution test of the GPU binning (restated from
+// geometry.cuh): can any pixel centre of [x0..x1] x [y0..y1] reach
+// alpha_bar = alpha exp(-q/2) >= alpha_skip?  False only when the minimum of
+// q = d^T Sigma^-1 d over the rectangle is certainly above
+// rho2 = 2 ln(alpha/alpha_skip), i.e. when blend() skips every such pair
+// (render.cpp:132-137).
+static double contrib_rho2(double alpha, double alpha_skip) {
+    if (!(alpha_skip > 0.0)) return INFINITY;
+    if (alpha < alpha_skip) return -1.0;
+    return 2.0 * std::log(alpha / alpha_skip);
+}
+
+static bool ellipse_may_hit(double mx, double my, double i00, double i01, double i11,
+                            double rho2, int x0, int x1, int y0, int y1) {
+    if (!(rho2 < INFINITY)) return true;
+    if (rho2 < 0.0) return false;
+    const double ax = (x0 + 0.5) - mx, bx = (x1 + 0.5) - mx;
+    const double ay = (y0 + 0.5) - my, by = (y1 + 0.5) - my;
+    if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
+    auto q = [&](double dx, double dy) {
+        return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy;
+    };
+    auto clampd = [](double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); };
+    double qmin = q(ax, clampd(-i01 * ax / i11, ay, by));
+    qmin = std::fmin(qmin, q(bx, clampd(-i01 * bx / i11, ay, by)));
+    qmin = std::fmin(qmin, q(clampd(-i01 * ay / i00, ax, bx), ay));
+    qmin = std::fmin(qmin, q(clampd(-i01 * by / i00, ax, bx), by));
+    const double mxd = std::fmax(std::fabs(ax), std::fabs(bx));
+    const double myd = std::fmax(std::fabs(ay), std::fabs(by));
+    const double bound = std::fabs(i00) * mxd * mxd + std::fabs(i11) * myd * myd +
+                         2.0 * std::fabs(i01) * mxd * myd;
+    return qmin <= rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12;
+}
+
+// Restated tile binning of the GPU build.  A visible fragment belongs to tile
+// (tx, ty) iff its closed bbox contains at least one pixel centre
+// (x+0.5, y+0.5) of that tile inside the image — exactly the pixels whose
+// bbox test in blend() passes (render.cpp:129-131) — and ellipse_may_hit
+// admits those centres.  Lists are in (depth, index) order.
 int orc_binning(const double* x, int64_t k, const orc_camera* cam,
                 const orc_render_opts* ro, int32_t tile, int32_t* n_visible,
                 int32_t* order, int64_t* n_dup, int64_t* tile_start,
@@ -1435,9 +1470,13 @@ int orc_binning(const double* x, int64_t k, const orc_camera* cam,
             prange(f.bx0, f.bx1, W, x0, x1);
             prange(f.by0, f.by1, H, y0, y1);
             if (x0 > x1 || y0 > y1) continue;
+            const double rho2 = contrib_rho2(f.alpha, ro->alpha_skip);
             for (int ty = y0 / tile; ty <= y1 / tile; ++ty)
                 for (int tx = x0 / tile; tx <= x1 / tile; ++tx)
-                    per[(size_t)ty * tw + tx].push_back((int32_t)f.splat);
+                    if (ellipse_may_hit(f.mx, f.my, f.i00, f.i01, f.i11, rho2,
+                                        std::max(x0, tx * tile), std::min(x1, tx * tile + tile - 1),
+                                        std::max(y0, ty * tile), std::min(y1, ty * tile + tile - 1)))
+                        per[(size_t)ty * tw + tx].push_back((int32_t)f.splat);
         }
         int64_t total = 0;
         for (size_t t = 0; t < per.size(); ++t) {

@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                  "-Xptxas", "-warn-spills"]
-NO_FMA = {"project.cu", "update.cu"}
+NO_FMA = {"project.cu", "update.cu", "binning.cu"}
 SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu", "probe.cu"]
 HEADERS = ["common.cuh", "geometry.cuh", "launch.h"]
 

@@ -414,6 +414,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.temp = c.temp.ensure(tb);
     b.temp_bytes = c.temp.bytes;
     double* rec = c.rec.as<double>((size_t)kRec * (K + 1));
+    b.rec = rec;
 
     ViewStatus init{INT_MAX, INT_MAX, 0, 0, 0};
     c.hstat->vs = init;

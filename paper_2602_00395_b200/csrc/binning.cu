@@ -10,6 +10,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "geometry.cuh"
 #include "launch.h"
 
 namespace sgtr {
@@ -23,10 +24,13 @@ __global__ void k_gather_counts(const int* __restrict__ sorted_ids,
     if (r == K) cnt[r] = 0;
 }
 
-// one warp per splat: lanes stride over the splat's tile rectangle
+// one warp per splat: lanes stride over the tiles of the splat's bbox pixel
+// range, keep the ones ellipse_may_hit admits (the same test K1 counted) and
+// write them compacted in row-major tile order
 __global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids,
                                               const int* __restrict__ tcount,
                                               const int4* __restrict__ rect,
+                                              const double* __restrict__ rec,
                                               const long long* __restrict__ off_r,
                                               int n_visible, int tiles_x,
                                               unsigned int* __restrict__ tkeys,
@@ -36,17 +40,33 @@ __global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids
     const int lane = threadIdx.x & 31;
     if (warp >= n_visible) return;
     const int id = sorted_ids[warp];
-    const int c = tcount[id];
-    if (c == 0) return;
-    const int4 t = rect[id];
-    const int w = t.z - t.x + 1;
-    const long long base = off_r[warp];
-    for (int j = lane; j < c; j += 32) {
-        const int ty = t.y + j / w, tx = t.x + j % w;
-        const long long d = base + j;
-        tkeys[d] = (unsigned int)(ty * tiles_x + tx);
-        dval[d] = (int)d;
-        dup_id[d] = id;
+    if (tcount[id] == 0) return;
+    const int4 pr = rect[id];  // pixel range x0, y0, x1, y1
+    const double* f = rec + (long long)kRec * id;
+    const double mx = f[R_MX], my = f[R_MY], i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
+    const double rho2 = f[R_RHO2];
+    const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
+    const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
+    long long base = off_r[warp];
+    for (int j0 = 0; j0 < w * h; j0 += 32) {
+        const int j = j0 + lane;
+        bool hit = false;
+        int tx = 0, ty = 0;
+        if (j < w * h) {
+            ty = ty0 + j / w;
+            tx = tx0 + j % w;
+            hit = ellipse_may_hit(mx, my, i00, i01, i11, rho2, max(pr.x, tx * kTile),
+                                  min(pr.z, tx * kTile + kTile - 1), max(pr.y, ty * kTile),
+                                  min(pr.w, ty * kTile + kTile - 1));
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+            const long long d = base + __popc(m & ((1u << lane) - 1u));
+            tkeys[d] = (unsigned int)(ty * tiles_x + tx);
+            dval[d] = (int)d;
+            dup_id[d] = id;
+        }
+        base += __popc(m);
     }
 }
 
@@ -110,7 +130,8 @@ void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long lon
     SGTR_CUDA(cudaMemsetAsync(b.tile_end, 0, sizeof(int) * n_tiles, st));
     if (n_dup == 0) return;
     k_emit<<<ceil_div((long long)n_visible * 32, 256), 256, 0, st>>>(
-        b.ids_alt, b.tcount, b.rect, b.off_r, n_visible, tiles_x, b.tkeys, b.dval, b.dup_id);
+        b.ids_alt, b.tcount, b.rect, b.rec, b.off_r, n_visible, tiles_x, b.tkeys, b.dval,
+        b.dup_id);
     SGTR_CUDA(cudaGetLastError());
     size_t bytes = b.temp_bytes;
     SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,

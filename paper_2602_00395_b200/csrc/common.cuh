@@ -35,7 +35,8 @@ enum RecField {
     R_MX, R_MY,                      // mu2d
     R_I00, R_I01, R_I11,             // inverse 2d covariance
     R_ALPHA, R_C0, R_C1, R_C2,
-    R_DEPTH
+    R_DEPTH,
+    R_RHO2                           // 2 ln(alpha / alpha_skip) (contribution ellipse)
 };
 // tangent record fields
 enum TRecField { T_MX = 0, T_MY, T_I00, T_I01, T_I11, T_ALPHA, T_C0, T_C1, T_C2 };

@@ -275,6 +275,41 @@ SGTR_HD void chain_reverse(const double* mu, const double* s, const double* q,
     for (int k = 0; k < 3; ++k) gmu[k] = w[k] * a_pc0 + w[3 + k] * a_pc1 + w[6 + k] * a_pc2;
 }
 
+// rho2 = 2 ln(alpha / alpha_skip): the fragment can contribute at a pixel
+// only where d^T Sigma^-1 d <= rho2 (alpha_bar = alpha exp(-q/2) >=
+// alpha_skip, render.cpp:132-137).  Negative: it never contributes.
+// Infinite: no culling (alpha_skip <= 0).
+SGTR_HD double contrib_rho2(double alpha, double alpha_skip) {
+    if (!(alpha_skip > 0.0)) return INFINITY;
+    if (alpha < alpha_skip) return -1.0;
+    return 2.0 * log(alpha / alpha_skip);
+}
+
+// Conservative culling of a fragment against the pixel centres
+// [x0+0.5, x1+0.5] x [y0+0.5, y1+0.5]: false only when every centre has
+// q = d^T Sigma^-1 d certainly above rho2 (the minimum of the convex q over
+// the rectangle, with a margin far above the rounding of the reference's own
+// exponent), i.e. when the reference would skip every one of these pairs.
+SGTR_HD bool ellipse_may_hit(double mx, double my, double i00, double i01, double i11,
+                             double rho2, int x0, int x1, int y0, int y1) {
+    if (!(rho2 < INFINITY)) return true;
+    if (rho2 < 0.0) return false;
+    const double ax = (x0 + 0.5) - mx, bx = (x1 + 0.5) - mx;
+    const double ay = (y0 + 0.5) - my, by = (y1 + 0.5) - my;
+    if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
+    auto q = [&](double dx, double dy) {
+        return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy;
+    };
+    auto clampd = [](double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); };
+    double qmin = q(ax, clampd(-i01 * ax / i11, ay, by));
+    qmin = fmin(qmin, q(bx, clampd(-i01 * bx / i11, ay, by)));
+    qmin = fmin(qmin, q(clampd(-i01 * ay / i00, ax, bx), ay));
+    qmin = fmin(qmin, q(clampd(-i01 * by / i00, ax, bx), by));
+    const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
+    const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
+    return qmin <= rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12;
+}
+
 // pixel-centre range [p0, p1] inside the closed interval [lo, hi], clipped
 // to [0, n-1]; p0 > p1 means empty.  Exact: every comparison is between
 // p + 0.5 (exactly representable) and the FP64 bound itself.

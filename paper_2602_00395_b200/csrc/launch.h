@@ -35,7 +35,8 @@ void launch_chain(cudaStream_t st, int mode, const double* x, int K, const DevCa
 struct BinBuffers {
     unsigned long long *keys, *keys_alt;
     int *ids, *ids_alt;
-    int4* rect;
+    int4* rect;            // bbox pixel range (x0, y0, x1, y1) per splat
+    const double* rec;     // fragment records (K1)
     int* tcount;
     long long* off_r;      // n+1 exclusive offsets in depth-rank order
     unsigned int *tkeys, *tkeys_alt;

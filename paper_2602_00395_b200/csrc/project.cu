@@ -72,8 +72,9 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             const double ry = ro.cutoff * sqrt(pr.c11);
             double i00, i01, i11;
             invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
-            double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,   py,       i00, i01,
-                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], pr.depth, 0.0, 0.0};
+            const double rho2 = contrib_rho2(p.alpha, ro.alpha_skip);
+            double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,   py,       i00,  i01,
+                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], pr.depth, rho2, 0.0};
             double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
 #pragma unroll
             for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);
@@ -84,9 +85,17 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             if (x0 > x1 || y0 > y1) {
                 tcount[i] = 0;
             } else {
-                const int4 t = make_int4(x0 / kTile, y0 / kTile, x1 / kTile, y1 / kTile);
-                rect[i] = t;
-                tcount[i] = (t.z - t.x + 1) * (t.w - t.y + 1);
+                // tiles whose pixel centres inside the bbox can reach
+                // alpha_bar >= alpha_skip (geometry.cuh: ellipse_may_hit)
+                rect[i] = make_int4(x0, y0, x1, y1);
+                int n = 0;
+                for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx)
+                        n += ellipse_may_hit(px, py, i00, i01, i11, rho2, max(x0, tx * kTile),
+                                             min(x1, tx * kTile + kTile - 1),
+                                             max(y0, ty * kTile),
+                                             min(y1, ty * kTile + kTile - 1));
+                tcount[i] = n;
             }
         }
     }

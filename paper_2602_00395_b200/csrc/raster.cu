@@ -270,15 +270,17 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
                 if (clamped) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     contrib = true;
-                    const double om = __dsub_rn(1.0, abar);
-                    const double t_in = T / om;
+                    // one reciprocal for T_in = T / (1 - abar) and the three
+                    // behind / (1 - abar) terms (render.cpp:243-245)
+                    const double rom = 1.0 / __dsub_rn(1.0, abar);
+                    const double t_in = T * rom;
                     const double at = abar * t_in;
                     g[6] = u0 * at;
                     g[7] = u1 * at;
                     g[8] = u2 * at;
-                    const double dab = u0 * (f[R_C0] * t_in - b0 / om) +
-                                       u1 * (f[R_C1] * t_in - b1 / om) +
-                                       u2 * (f[R_C2] * t_in - b2 / om);
+                    const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
+                                       u1 * (f[R_C1] * t_in - b1 * rom) +
+                                       u2 * (f[R_C2] * t_in - b2 * rom);
                     b0 += f[R_C0] * at;
                     b1 += f[R_C1] * at;
                     b2 += f[R_C2] * at;
