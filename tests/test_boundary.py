@@ -87,3 +87,19 @@ def test_host_helpers(built):
     s = splat.Scene.from_primitives([[1, 2, 3]], [[4, 5, 6]], [[7, 8, 9, 10]], [11], [[12, 13, 14]])
     assert s.x.tolist() == list(range(1, 15))
     assert (s.scale_offset(), s.quat_offset(), s.opacity_offset(), s.color_offset()) == (3, 6, 10, 11)
+
+
+def test_cpp_caller_of_the_c_abi(built):
+    """A C++ program compiled against include/sgtr.h and linked with
+    libsgtr.so exercises the boundary without Python (host-only part here;
+    the GPU part runs when a device is present)."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(tempfile.mkdtemp(), "cpp_host")
+    libdir = os.path.join(ROOT, "paper_2602_00395_b200")
+    subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cpp_host.cpp"), "-L", libdir, "-lsgtr",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host-only C-ABI ok" in r.stdout
