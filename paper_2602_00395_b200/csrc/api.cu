@@ -1651,7 +1651,8 @@ int sgtr_blend_stats(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_op
         bind(c);
         need_scene(c);
         const DevCam dc = make_devcam(*cam);
-        const RenderP rp = render_params(*ro);
+        RenderP rp = render_params(*ro);
+        rp.cull = 0;  // count the reference's pairs: no contribution culling
         const ViewRender vr = render_view(c, dc, rp, true);
         unsigned long long* cnt = c.seam2.as<unsigned long long>(2);
         SGTR_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c.st));

@@ -35,8 +35,9 @@ enum RecField {
     R_MX, R_MY,                      // mu2d
     R_I00, R_I01, R_I11,             // inverse 2d covariance
     R_ALPHA, R_C0, R_C1, R_C2,
-    R_DEPTH,
-    R_RHO2                           // 2 ln(alpha / alpha_skip) (contribution ellipse)
+    R_K11,                           // i01 / i11 (edge minimiser slope)
+    R_RHO2,                          // 2 ln(alpha / alpha_skip) (contribution ellipse)
+    R_K00                            // i01 / i00
 };
 // tangent record fields
 enum TRecField { T_MX = 0, T_MY, T_I00, T_I01, T_I11, T_ALPHA, T_C0, T_C1, T_C2 };
@@ -53,11 +54,12 @@ struct DevCam {
 struct RenderP {
     double z_near, lowpass, alpha_clamp, alpha_skip, t_stop, cutoff;
     double bg[3];
+    int cull;  // contribution-ellipse culling (off only for the E/C counters)
 };
 
 inline RenderP render_params(const sgtr_render_options& o) {
     return {o.z_near, o.lowpass, o.alpha_clamp, o.alpha_skip, o.t_stop, o.cutoff_sigma,
-            {o.background[0], o.background[1], o.background[2]}};
+            {o.background[0], o.background[1], o.background[2]}, 1};
 }
 
 // per-view device error/status block

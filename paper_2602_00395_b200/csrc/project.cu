@@ -72,9 +72,10 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             const double ry = ro.cutoff * sqrt(pr.c11);
             double i00, i01, i11;
             invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
-            const double rho2 = contrib_rho2(p.alpha, ro.alpha_skip);
+            const double rho2 = ro.cull ? contrib_rho2(p.alpha, ro.alpha_skip) : INFINITY;
             double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,   py,       i00,  i01,
-                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], pr.depth, rho2, 0.0};
+                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], i01 / i11, rho2,
+                              i01 / i00};
             double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
 #pragma unroll
             for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);

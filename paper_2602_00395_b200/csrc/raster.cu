@@ -73,6 +73,31 @@ __device__ __forceinline__ bool warp_misses(const PixelCtx& p, const double* f) 
     return p.wx1 < f[R_BX0] || p.wx0 > f[R_BX1] || p.wy1 < f[R_BY0] || p.wy0 > f[R_BY1];
 }
 
+// Warp-level contribution filter (after warp_misses): false only when no
+// pixel centre of the warp's 8x4 block can reach alpha_bar >= alpha_skip —
+// the minimum of q = d^T Sigma^-1 d over the block is certainly above
+// rho2 (same bound as geometry.cuh:ellipse_may_hit, with the edge-minimiser
+// slopes precomputed in the record).  Warp-uniform.
+__device__ __forceinline__ bool warp_may_hit(const PixelCtx& p, const double* f) {
+    const double rho2 = f[R_RHO2];
+    if (!(rho2 < INFINITY)) return true;
+    if (rho2 < 0.0) return false;
+    const double ax = p.wx0 - f[R_MX], bx = p.wx1 - f[R_MX];
+    const double ay = p.wy0 - f[R_MY], by = p.wy1 - f[R_MY];
+    if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
+    const double i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
+    const double k11 = f[R_K11], k00 = f[R_K00];
+    auto q = [&](double dx, double dy) { return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy; };
+    auto cl = [](double v, double lo, double hi) { return fmin(fmax(v, lo), hi); };
+    double qmin = q(ax, cl(-k11 * ax, ay, by));
+    qmin = fmin(qmin, q(bx, cl(-k11 * bx, ay, by)));
+    qmin = fmin(qmin, q(cl(-k00 * ay, ax, bx), ay));
+    qmin = fmin(qmin, q(cl(-k00 * by, ax, bx), by));
+    const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
+    const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
+    return qmin <= rho2 + 1e-8 * rho2 + 1e-11 * bound + 1e-11;
+}
+
 // cooperative staging: 8 lanes per 128-byte record; entries [b, b+n) of the
 // tile-sorted list go to s_rec[0, n)
 __device__ __forceinline__ void stage_records(const TileLists& tl, const double* __restrict__ rec,
@@ -128,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
         if (__all_sync(kFull, done)) continue;
         for (int jj = 0; jj < n; ++jj) {
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f)) continue;
+            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
@@ -203,7 +228,7 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
     v8 = s;
 }
 
-__global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
+__global__ void __launch_bounds__(kThreads, 3) k_raster_vjp(TileLists tl,
                                                          const double* __restrict__ rec, int W,
                                                          int H, RenderP ro,
                                                          const double* __restrict__ adj,
@@ -257,7 +282,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_vjp(TileLists tl,
             const int rel = bstart - start + jj;
             if (rel >= wlast) continue;
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f)) continue;
+            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
             double g[kAdj];
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
@@ -341,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
         if (__all_sync(kFull, done)) continue;
         for (int jj = 0; jj < n; ++jj) {
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f)) continue;
+            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double* t = s_t + kTRec * jj;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];

@@ -360,3 +360,21 @@ def test_step_nonfinite_parameter_names_splat(sp, orc):
     with pytest.raises(sp.NumericError, match="non-finite parameter in splat 2"):
         sp.step_3dgs2tr(st, sp.Scene(x), views, _tr_opts(sp, 10))
     assert st.t == 1  # the reference increments t before the first render
+
+
+def test_blend_counters_match_oracle(sp, orc, c1):
+    # the algorithmic-work units of the roofline: pairs reaching
+    # the alpha evaluation (E) and contributing pairs (C), counted on the GPU
+    # without contribution culling, must equal the reference count
+    import ctypes as C
+    from paper_2602_00395_b200 import _lib
+    ctx = sp.default_context()
+    for x in (c1.gt_x, c1.init_x):
+        ctx.set_scene(x)
+        for oc in c1.cams[:2]:
+            e, c = C.c_int64(), C.c_int64()
+            _lib.check(_lib.lib().sgtr_blend_stats(ctx.handle, C.byref(sp.Camera.from_c(oc)._c()),
+                                                   C.byref(sp.RenderOptions()._c()),
+                                                   C.byref(e), C.byref(c)))
+            eo, co = orc.blend_stats(x, oc)
+            assert abs(e.value - eo) <= 2 and abs(c.value - co) <= 2
