@@ -16,6 +16,8 @@
 // of render.cpp:132-136), so bbox reject, alpha clamp, alpha skip and the
 // transmittance stop take the same branches in forward, VJP and JVP — the
 // reference's "frozen branches" contract (render.hpp:76-79).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "launch.h"
@@ -129,7 +131,7 @@ __device__ __forceinline__ void stage_tangents(const TileLists& tl, const double
 // kCount: also count the (pixel, fragment) pairs reaching the alpha
 // evaluation (E) and the contributing ones (C), the algorithmic-work units
 // of SURVEY §8(d); used outside timed regions only.
-template <bool kCount>
+template <bool kCount, bool kWarpCull>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                                                          const double* __restrict__ rec, int W,
                                                          int H, RenderP ro,
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
         if (__all_sync(kFull, done)) continue;
         for (int jj = 0; jj < n; ++jj) {
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
+            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
@@ -228,7 +230,8 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
     v8 = s;
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_raster_vjp(TileLists tl,
+template <bool kWarpCull, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists tl,
                                                          const double* __restrict__ rec, int W,
                                                          int H, RenderP ro,
                                                          const double* __restrict__ adj,
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster_vjp(TileLists tl,
             const int rel = bstart - start + jj;
             if (rel >= wlast) continue;
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
+            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
             double g[kAdj];
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_raster_vjp(TileLists tl,
 }
 
 // ------------------------------------------------------------------ K12 (raster)
+template <bool kWarpCull>
 __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
                                                          const double* __restrict__ rec,
                                                          const double* __restrict__ trec, int W,
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
         if (__all_sync(kFull, done)) continue;
         for (int jj = 0; jj < n; ++jj) {
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || !warp_may_hit(pc, f)) continue;
+            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double* t = s_t + kTRec * jj;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
@@ -405,6 +409,15 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
     tangent[2 * P + p] = d2 + ro.bg[2] * dT;
 }
 
+// experiment knobs (read once): SGTR_WARP_CULL=1 enables the warp-level
+// contribution filter, SGTR_VJP_MINBLOCKS in {2, 3} the VJP register budget
+int knob(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
+const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 2);
+
 }  // namespace
 
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
@@ -413,11 +426,14 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
     if (counters)
-        k_raster_fwd<true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
-                                                   counters);
+        k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
+                                                          counters);
+    else if (g_warp_cull)
+        k_raster_fwd<false, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
+                                                          nullptr);
     else
-        k_raster_fwd<false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
-                                                    nullptr);
+        k_raster_fwd<false, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal,
+                                                           last, nullptr);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -426,7 +442,14 @@ void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, 
                        const int* last, double* slots) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    k_raster_vjp<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    if (g_warp_cull && g_vjp_min_blocks == 3)
+        k_raster_vjp<true, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    else if (g_warp_cull)
+        k_raster_vjp<true, 2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    else if (g_vjp_min_blocks == 3)
+        k_raster_vjp<false, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    else
+        k_raster_vjp<false, 2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -434,7 +457,10 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    k_raster_jvp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    if (g_warp_cull)
+        k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    else
+        k_raster_jvp<false><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     SGTR_CUDA(cudaGetLastError());
 }
 
