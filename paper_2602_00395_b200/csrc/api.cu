@@ -337,7 +337,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     double* htail = nullptr;     // pinned staging for the fused tail
@@ -465,7 +465,13 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
         emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
     }
     c.launches += vr.n_dup ? 5 : 0;  // emit, tile sort (histogram + 2 passes), ranges
-    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt, b.dup_id};
+    int* tids = c.tile_ids.as<int>(nd);
+    {
+        Timed t(c, KC_TILE_BIN);
+        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, tids, c.inv.as<int>(nd));
+    }
+    c.launches += vr.n_dup ? 1 : 0;
+    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt, b.dup_id, tids};
     const int P = dc.W * dc.H;
     Timed t(c, KC_RASTER_FWD);
     launch_raster_fwd(c.st, vr.tl, rec, dc.W, dc.H, ro, img_ptr(c, c.img, P),
@@ -478,6 +484,23 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
 void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender& vr, int mode,
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
     const long long nd = std::max(vr.n_dup, 1LL);
+    if (vjp_mode() == 1) {
+        double* part = c.part.as<double>((size_t)8 * kAdj * nd);
+        unsigned char* mask = c.mask.as<unsigned char>((size_t)8 * nd);
+        {
+            Timed t(c, KC_RASTER_VJP);
+            SGTR_CUDA(cudaMemsetAsync(mask, 0, (size_t)8 * nd, c.st));
+            launch_raster_vjp_warp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
+                                   c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(),
+                                   part, mask);
+        }
+        Timed t(c, KC_CHAIN);
+        launch_chain_warp(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+                          c.off_r.get<long long>(), c.tcount.get<int>(), c.inv.get<int>(), part,
+                          mask, zdense, zbits, acc, flag);
+        c.launches += 2;
+        return;
+    }
     double* slots = c.slots.as<double>((size_t)kAdj * nd);
     {
         Timed t(c, KC_RASTER_VJP);

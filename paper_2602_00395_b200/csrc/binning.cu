@@ -79,6 +79,15 @@ __global__ void k_ranges(const unsigned int* __restrict__ tkeys, long long n,
     if (i == n - 1 || tkeys[i + 1] != k) end[k] = (int)(i + 1);
 }
 
+__global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restrict__ dup_id,
+                           long long n, int* __restrict__ tile_ids, int* __restrict__ inv) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int d = sorted_d[j];
+    tile_ids[j] = dup_id[d];
+    inv[d] = (int)j;
+}
+
 int bits_for(int n) {
     int b = 1;
     while ((1LL << b) < n) ++b;
@@ -86,6 +95,13 @@ int bits_for(int n) {
 }
 
 }  // namespace
+
+void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
+                     int* tile_ids, int* inv) {
+    if (n == 0) return;
+    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, tile_ids, inv);
+    SGTR_CUDA(cudaGetLastError());
+}
 
 size_t depth_sort_temp_bytes(int K) {
     size_t bytes = 0;

@@ -63,6 +63,7 @@ struct TileLists {
     const int* tile_end;
     const int* sorted_d;  // tile-sorted duplicate indices
     const int* dup_id;    // duplicate -> splat id
+    const int* tile_ids;  // splat id per tile-sorted position (dup_id[sorted_d[j]])
 };
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
@@ -72,6 +73,22 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
 void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, const double* adj, const double* tfinal,
                        const int* last, double* slots);
+// K10 (barrier-free form): each warp walks its tile's list alone and writes
+// its reduced adjoints to part[(j * 8 + warp) * 9 ...], flagging mask[j * 8 +
+// warp]; mask must be zeroed first.  Used when launch_vjp_mode() == 1.
+int vjp_mode();
+void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
+                            int H, const RenderP& ro, const double* adj, const double* tfinal,
+                            const int* last, double* part, unsigned char* mask);
+// K11 over the per-warp partials of the barrier-free K10
+void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+                       const RenderP& ro, const int* sorted_ids, int n_visible,
+                       const long long* off_r, const int* tcount, const int* inv,
+                       const double* part, const unsigned char* mask, const double* zdense,
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag);
+// tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j
+void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
+                     int* tile_ids, int* inv);
 // K12 (raster half): tangent image along the tangent records
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro,

@@ -226,6 +226,73 @@ __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restric
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
 
+// K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
+// the fixed-order sum of its (tile, fragment) slots; the transpose of the 5x10
+// Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
+// reference evaluates with 10 dual seeds, is applied in one reverse sweep.
+__global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __restrict__ x, int K,
+                                               DevCam cam, RenderP ro,
+                                               const int* __restrict__ sorted_ids, int n_visible,
+                                               const long long* __restrict__ off_r,
+                                               const int* __restrict__ tcount,
+                                               const int* __restrict__ inv,
+                                               const double* __restrict__ part,
+                                               const unsigned char* __restrict__ mask,
+                                               const double* __restrict__ zdense,
+                                               const uint32_t* __restrict__ zbits,
+                                               double* __restrict__ acc,
+                                               double* nonfinite_flag) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_visible) return;
+    const int id = sorted_ids[r];
+    const int cnt = tcount[id];
+    if (cnt == 0) return;
+    double a[kAdj];
+#pragma unroll
+    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
+    // the <= 8 per-warp partials of each duplicate, in warp order
+    const long long off = off_r[r];
+    for (int t = 0; t < cnt; ++t) {
+        const long long jpos = inv[off + t];
+        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * jpos);
+        if (m == 0ull) continue;
+        const double* pp = part + jpos * 8 * kAdj;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            if ((m >> (8 * w)) & 0xffull) {
+#pragma unroll
+                for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+            }
+        }
+    }
+    const long long k = K;
+    bool finite = true;
+    auto add = [&](long long idx, double v) {
+        if (mode == 1) v = probe_at(zdense, zbits, idx) * v;
+        finite = finite && isfinite(v);
+        acc[idx] += v;
+    };
+    add(10 * k + id, a[5]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
+    if (any) {
+        // J^T a for (mu, s, q) in one reverse sweep (geometry.cuh)
+        const Splat p = load_splat(x, K, id);
+        double gmu[3], gs[3], gq[4];
+        chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu[c]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
+    }
+    if (!finite) *nonfinite_flag = 1.0;  // idempotent store
+}
+
 }  // namespace
 
 void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
@@ -249,6 +316,19 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& c
                         double* trec) {
     if (K == 0) return;
     k_project_jvp<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, v, zbits, trec);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+                       const RenderP& ro, const int* sorted_ids, int n_visible,
+                       const long long* off_r, const int* tcount, const int* inv,
+                       const double* part, const unsigned char* mask, const double* zdense,
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag) {
+    if (n_visible == 0) return;
+    k_chain_warp<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, cam, ro, sorted_ids,
+                                                            n_visible, off_r, tcount, inv, part,
+                                                            mask, zdense, zbits, acc,
+                                                            nonfinite_flag);
     SGTR_CUDA(cudaGetLastError());
 }
 

@@ -346,6 +346,96 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
     }
 }
 
+// ------------------------------------------------------------------ K10, barrier-free
+// Every warp walks its tile's list on its own: records are read through L1 as
+// warp-broadcast loads (the 8 warps of a tile hit the same lines), so no
+// shared-memory staging, no CTA barriers and no cross-warp reduction are
+// needed.  A warp reduces each fragment's 9 adjoints over its 32 pixels and
+// stores them in its own partial slot (tile-sorted position j, warp w),
+// flagging mask[j * 8 + w]; K11 sums the flagged partials of each duplicate in
+// warp order (deterministic, no atomics).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    k_raster_vjp_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                      const double* __restrict__ adj, const double* __restrict__ tfinal,
+                      const int* __restrict__ last, double* __restrict__ part,
+                      unsigned char* __restrict__ mask) {
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
+    int lastp = 0;
+    if (pc.inside) {
+        u0 = adj[p];
+        u1 = adj[P + p];
+        u2 = adj[2 * P + p];
+        T = tfinal[p];
+        lastp = last[p];
+    }
+    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
+    if (!active) lastp = 0;
+    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;
+    const int wlast = __reduce_max_sync(kFull, lastp);
+    for (int j = start + wlast - 1; j >= start; --j) {
+        const int id = __ldg(tl.tile_ids + j);
+        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
+        if (pc.wx1 < bx.x || pc.wx0 > bx.y || pc.wy1 < by.x || pc.wy0 > by.y) continue;
+        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
+        const double2 c01 = __ldg(r2 + 5), c2 = __ldg(r2 + 6);
+        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                              c01.x, c01.y, c2.x};
+        const int rel = j - start;
+        double g[kAdj];
+#pragma unroll
+        for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+        bool contrib = false;
+        if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
+            const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+            const double gauss = exp(eval_expo(dx, dy, f));
+            double abar = __dmul_rn(f[R_ALPHA], gauss);
+            const bool clamped = abar >= ro.alpha_clamp;
+            if (clamped) abar = ro.alpha_clamp;
+            if (abar >= ro.alpha_skip) {
+                contrib = true;
+                const double rom = 1.0 / __dsub_rn(1.0, abar);
+                const double t_in = T * rom;
+                const double at = abar * t_in;
+                g[6] = u0 * at;
+                g[7] = u1 * at;
+                g[8] = u2 * at;
+                const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
+                                   u1 * (f[R_C1] * t_in - b1 * rom) +
+                                   u2 * (f[R_C2] * t_in - b2 * rom);
+                b0 += f[R_C0] * at;
+                b1 += f[R_C1] * at;
+                b2 += f[R_C2] * at;
+                if (!clamped) {
+                    g[5] = gauss * dab;
+                    const double de = abar * dab;
+                    g[2] = de * (-0.5 * dx * dx);
+                    g[3] = de * (-dx * dy);
+                    g[4] = de * (-0.5 * dy * dy);
+                    g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
+                    g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
+                }
+                T = t_in;
+            }
+        }
+        if (!__any_sync(kFull, contrib)) continue;
+        double v, v8;
+        warp_reduce9(g, lane, v, v8);
+        double* o = part + ((long long)j * kWarps + warp) * kAdj;
+        if ((lane & 3) == 0) o[lane >> 2] = v;
+        if (lane == 0) {
+            o[8] = v8;
+            mask[(long long)j * kWarps + warp] = 1;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K12 (raster)
 template <bool kWarpCull>
 __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
@@ -416,7 +506,8 @@ int knob(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
-const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 2);
+const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
+const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 
 }  // namespace
 
@@ -450,6 +541,22 @@ void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, 
         k_raster_vjp<false, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
     else
         k_raster_vjp<false, 2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+int vjp_mode() { return g_vjp_mode; }
+
+void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
+                            int H, const RenderP& ro, const double* adj, const double* tfinal,
+                            const int* last, double* part, unsigned char* mask) {
+    const int n = tl.tiles_x * tl.tiles_y;
+    if (n == 0) return;
+    if (g_vjp_min_blocks == 3)
+        k_raster_vjp_warp<3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                     mask);
+    else
+        k_raster_vjp_warp<2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                     mask);
     SGTR_CUDA(cudaGetLastError());
 }
 
