@@ -413,12 +413,16 @@ def main():
         achieved = bytes_per / (avg_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
                     "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None}
-    # HBM roofline of the fused trust-region update for reference
-    tr_cnt, tr_tot = ktimes.get("tr_update", [0, 0.0])
-    tr_bytes = 8 * 14 * k * (6 + 1.0 / 10)  # x, g, g_hat(rw), d_hat(r), x_out; + w on refresh
-    roofline_tr = {"bound": "hbm", "kernel": "tr_update",
+    # HBM roofline of the trust-region update K14 (a + b + c): algorithmic bytes
+    # per step = x, g_acc, g_hat (r+w), D_hat (r) and x_out (6 vectors of 8*dim)
+    # + D_hat write and z.w read on the 1-in-10 refresh steps
+    tr_cnt = ktimes.get("tr_update", [0, 0.0])[0]
+    tr_tot = sum(ktimes.get(n, [0, 0.0])[1] for n in ("tr_update", "tr_bisect", "tr_apply"))
+    tr_bytes = 8 * 14 * k * (6 + 2.0 / 10)
+    roofline_tr = {"bound": "hbm", "kernel": "tr_update+tr_bisect+tr_apply",
                    "achieved": tr_bytes / (tr_tot / max(tr_cnt, 1) * 1e-3) / 1e9 if tr_cnt else None,
-                   "peak": hbm_peak, "unit": "GB/s"}
+                   "peak": hbm_peak, "unit": "GB/s",
+                   "work": "48.8 B per parameter per step (6.2 FP64 vectors)"}
     if roofline_tr["achieved"]:
         roofline_tr["frac"] = roofline_tr["achieved"] / hbm_peak
 

@@ -281,11 +281,13 @@ typedef int (*CommInitRankFn)(void**, int, UniqueId, int);
 // after the stream synchronises.
 enum KClass {
     KC_PROJECT, KC_DEPTH_SORT, KC_TILE_BIN, KC_RASTER_FWD, KC_SSIM, KC_GATHER,
-    KC_RASTER_VJP, KC_CHAIN, KC_PROJECT_JVP, KC_RASTER_JVP, KC_TR_UPDATE, KC_COUNT
+    KC_RASTER_VJP, KC_CHAIN, KC_PROJECT_JVP, KC_RASTER_JVP, KC_TR_UPDATE, KC_TR_BISECT,
+    KC_TR_APPLY, KC_COUNT
 };
 const char* const kClassNames[KC_COUNT] = {
     "project", "depth_sort_scan", "tile_binning", "raster_fwd", "ssim_residual",
-    "ssim_gather", "raster_vjp", "chain", "project_jvp", "raster_jvp", "tr_update"};
+    "ssim_gather", "raster_vjp", "chain", "project_jvp", "raster_jvp", "tr_update",
+    "tr_bisect", "tr_apply"};
 
 struct KTimer {
     bool on = false;
@@ -757,10 +759,18 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     a.degenerate_flag = &c.dstat->degenerate;
     {
         Timed t(c, KC_TR_UPDATE);
-        launch_tr_update(c.st, a);
+        launch_tr_update(c.st, a, 0);
+    }
+    {
+        Timed t(c, KC_TR_BISECT);
+        launch_tr_update(c.st, a, 1);
+    }
+    {
+        Timed t(c, KC_TR_APPLY);
+        launch_tr_update(c.st, a, 2);
         launch_tr_finalize(c.st, a.partials, nb, c.dstat->tr);
     }
-    c.launches += 2;
+    c.launches += 4;
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->bad_index, &c.dstat->bad_index,
                               offsetof(DevStatus, scalar) - offsetof(DevStatus, bad_index),
                               cudaMemcpyDeviceToHost, c.st));

@@ -149,7 +149,9 @@ struct TrArgs {
     int* queue_count;
 };
 int tr_num_blocks(int K);
-void launch_tr_update(cudaStream_t st, const TrArgs& a);
+// phase 0: K14a (EMAs, direction, radii), 1: K14b (queued bisections),
+// 2: K14c (clip, apply, clamp)
+void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase);
 // 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
 // (partials hold 2 * tr_num_blocks(K) rows of 5)
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5);

@@ -436,6 +436,113 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     }
 }
 
+// ------------------------------------------------------------------ K10, PPL pixels per lane
+// As k_raster_vjp_warp, but each lane owns PPL pixels of one column (rows
+// r, r+2, ..): a warp covers 16 x 2*PPL pixels, sums each fragment's adjoints
+// over its PPL pixels in registers (fixed order) before the one warp
+// reduction, and the PPL independent pixel recurrences give the FP64
+// pipeline instruction-level parallelism.  8/PPL warps per tile.
+template <int PPL>
+__global__ void __launch_bounds__(32 * (8 / PPL))
+    k_raster_vjp_ppl(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                     const double* __restrict__ adj, const double* __restrict__ tfinal,
+                     const int* __restrict__ last, double* __restrict__ part,
+                     unsigned char* __restrict__ mask) {
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
+    const int px = X0 + (lane & 15);
+    const int ybase = Y0 + warp * 2 * PPL;
+    const double pxc = px + 0.5;
+    const double wx0 = X0 + 0.5, wx1 = X0 + 15.5;
+    const double wy0 = ybase + 0.5, wy1 = ybase + 2 * PPL - 0.5;
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H;
+    double T[PPL], u0[PPL], u1[PPL], u2[PPL], b0[PPL], b1[PPL], b2[PPL], pyc[PPL];
+    int lastp[PPL];
+    int lmax = 0;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+        const int py = ybase + (lane >> 4) + 2 * k;
+        pyc[k] = py + 0.5;
+        u0[k] = u1[k] = u2[k] = 0.0;
+        T[k] = 0.0;
+        lastp[k] = 0;
+        if (px < W && py < H) {
+            const long long p = (long long)py * W + px;
+            u0[k] = adj[p];
+            u1[k] = adj[P + p];
+            u2[k] = adj[2 * P + p];
+            T[k] = tfinal[p];
+            lastp[k] = last[p];
+            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
+        }
+        b0[k] = ro.bg[0] * T[k];
+        b1[k] = ro.bg[1] * T[k];
+        b2[k] = ro.bg[2] * T[k];
+        lmax = max(lmax, lastp[k]);
+    }
+    const int wlast = __reduce_max_sync(kFull, lmax);
+    for (int j = start + wlast - 1; j >= start; --j) {
+        const int id = __ldg(tl.tile_ids + j);
+        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
+        if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
+        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
+        const double2 c01 = __ldg(r2 + 5), c2 = __ldg(r2 + 6);
+        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                              c01.x, c01.y, c2.x};
+        const int rel = j - start;
+        double g[kAdj];
+#pragma unroll
+        for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+        bool contrib = false;
+        const bool col_in = !(pxc < f[R_BX0] || pxc > f[R_BX1]);
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+            if (!col_in || rel >= lastp[k] || pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1]) continue;
+            const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
+            const double gauss = exp(eval_expo(dx, dy, f));
+            double abar = __dmul_rn(f[R_ALPHA], gauss);
+            const bool clamped = abar >= ro.alpha_clamp;
+            if (clamped) abar = ro.alpha_clamp;
+            if (abar < ro.alpha_skip) continue;
+            contrib = true;
+            const double rom = 1.0 / __dsub_rn(1.0, abar);
+            const double t_in = T[k] * rom;
+            const double at = abar * t_in;
+            g[6] += u0[k] * at;
+            g[7] += u1[k] * at;
+            g[8] += u2[k] * at;
+            const double dab = u0[k] * (f[R_C0] * t_in - b0[k] * rom) +
+                               u1[k] * (f[R_C1] * t_in - b1[k] * rom) +
+                               u2[k] * (f[R_C2] * t_in - b2[k] * rom);
+            b0[k] += f[R_C0] * at;
+            b1[k] += f[R_C1] * at;
+            b2[k] += f[R_C2] * at;
+            if (!clamped) {
+                g[5] += gauss * dab;
+                const double de = abar * dab;
+                g[2] += de * (-0.5 * dx * dx);
+                g[3] += de * (-dx * dy);
+                g[4] += de * (-0.5 * dy * dy);
+                g[0] += de * (f[R_I00] * dx + f[R_I01] * dy);
+                g[1] += de * (f[R_I01] * dx + f[R_I11] * dy);
+            }
+            T[k] = t_in;
+        }
+        if (!__any_sync(kFull, contrib)) continue;
+        double v, v8;
+        warp_reduce9(g, lane, v, v8);
+        double* o = part + ((long long)j * kWarps + warp) * kAdj;
+        if ((lane & 3) == 0) o[lane >> 2] = v;
+        if (lane == 0) {
+            o[8] = v8;
+            mask[(long long)j * kWarps + warp] = 1;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K12 (raster)
 template <bool kWarpCull>
 __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
@@ -508,6 +615,7 @@ int knob(const char* name, int dflt) {
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
 const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
+const int g_vjp_ppl = knob("SGTR_VJP_PPL", 4);
 
 }  // namespace
 
@@ -551,7 +659,11 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    if (g_vjp_min_blocks == 3)
+    if (g_vjp_ppl == 4)
+        k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
+    else if (g_vjp_ppl == 2)
+        k_raster_vjp_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
+    else if (g_vjp_min_blocks == 3)
         k_raster_vjp_warp<3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
                                                      mask);
     else

@@ -440,20 +440,22 @@ __global__ void k_fill_int(int* p, long long n, int v) {
 
 int tr_num_blocks(int K) { return ceil_div(K, kThreads); }
 
-void launch_tr_update(cudaStream_t st, const TrArgs& a) {
+void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
     if (a.K == 0) return;
     const int nb = tr_num_blocks(a.K);
-    SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
-    k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
-    SGTR_CUDA(cudaGetLastError());
-    if (a.ghat_only) {
-        SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
-        return;
+    if (phase == 0) {
+        SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
+        k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
+        SGTR_CUDA(cudaGetLastError());
+        if (a.ghat_only)
+            SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
+    } else if (phase == 1 && !a.ghat_only) {
+        k_tr_bisect<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
+        SGTR_CUDA(cudaGetLastError());
+    } else if (phase == 2 && !a.ghat_only) {
+        k_tr_apply<<<nb, kThreads, 0, st>>>(a);
+        SGTR_CUDA(cudaGetLastError());
     }
-    k_tr_bisect<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
-    SGTR_CUDA(cudaGetLastError());
-    k_tr_apply<<<nb, kThreads, 0, st>>>(a);
-    SGTR_CUDA(cudaGetLastError());
 }
 
 // partials: [nblocks][5] from K14a (sum g^2, sum dx^2) then [nblocks][5] from
