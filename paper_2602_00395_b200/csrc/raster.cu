@@ -196,6 +196,86 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K7, PPL pixels per lane
+// Barrier-free forward: warps walk the tile list on their own (records through
+// L1), each lane blends PPL pixels of one column (independent recurrences =
+// FP64 instruction-level parallelism); a warp stops once all its pixels
+// terminated.  Same per-pixel operation sequence as k_raster_fwd.
+template <int PPL>
+__global__ void __launch_bounds__(32 * (8 / PPL))
+    k_raster_fwd_ppl(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                     double* __restrict__ img, double* __restrict__ tfinal,
+                     int* __restrict__ last) {
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
+    const int px = X0 + (lane & 15);
+    const int ybase = Y0 + warp * 2 * PPL;
+    const double pxc = px + 0.5;
+    const double wx0 = X0 + 0.5, wx1 = X0 + 15.5;
+    const double wy0 = ybase + 0.5, wy1 = ybase + 2 * PPL - 0.5;
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T[PPL], c0[PPL], c1[PPL], c2[PPL], pyc[PPL];
+    int processed[PPL];
+    bool done[PPL];
+    bool all_done = true;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+        const int py = ybase + (lane >> 4) + 2 * k;
+        pyc[k] = py + 0.5;
+        T[k] = 1.0;
+        c0[k] = c1[k] = c2[k] = 0.0;
+        processed[k] = end - start;
+        done[k] = !(px < W && py < H);
+        all_done = all_done && done[k];
+    }
+    for (int j = start; j < end; ++j) {
+        if (__all_sync(kFull, all_done)) break;
+        const int id = __ldg(tl.tile_ids + j);
+        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
+        if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
+        if (pxc < bx.x || pxc > bx.y) continue;
+        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
+        const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
+        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                              c01.x, c01.y, cc2.x};
+        all_done = true;
+#pragma unroll
+        for (int k = 0; k < PPL; ++k) {
+            if (!done[k] && !(pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1])) {
+                const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
+                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T[k];
+                    c0[k] += f[R_C0] * w;
+                    c1[k] += f[R_C1] * w;
+                    c2[k] += f[R_C2] * w;
+                    T[k] = __dmul_rn(T[k], __dsub_rn(1.0, abar));
+                    if (T[k] < ro.t_stop) {
+                        done[k] = true;
+                        processed[k] = j - start + 1;
+                    }
+                }
+            }
+            all_done = all_done && done[k];
+        }
+    }
+    const long long P = (long long)W * H;
+#pragma unroll
+    for (int k = 0; k < PPL; ++k) {
+        const int py = ybase + (lane >> 4) + 2 * k;
+        if (px >= W || py >= H) continue;
+        const long long p = (long long)py * W + px;
+        img[p] = c0[k] + ro.bg[0] * T[k];
+        img[P + p] = c1[k] + ro.bg[1] * T[k];
+        img[2 * P + p] = c2[k] + ro.bg[2] * T[k];
+        tfinal[p] = T[k];
+        last[p] = processed[k];
+    }
+}
+
 // ------------------------------------------------------------------ K10
 // Transposed butterfly: sums g[0..7] over the warp so that lane l with
 // (l & 3) == 0 ends with the total of g[l >> 2] (9 shuffles instead of 40),
@@ -615,7 +695,8 @@ int knob(const char* name, int dflt) {
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
 const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
-const int g_vjp_ppl = knob("SGTR_VJP_PPL", 4);
+const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
+const int g_fwd_ppl = knob("SGTR_FWD_PPL", 4);
 
 }  // namespace
 
@@ -627,6 +708,10 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
+    else if (g_fwd_ppl == 4)
+        k_raster_fwd_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    else if (g_fwd_ppl == 2)
+        k_raster_fwd_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_warp_cull)
         k_raster_fwd<false, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           nullptr);
