@@ -1404,7 +1404,8 @@ static double contrib_rho2(double alpha, double alpha_skip) {
 }
 
 static bool ellipse_may_hit(double mx, double my, double i00, double i01, double i11,
-                            double rho2, int x0, int x1, int y0, int y1) {
+                            double k11, double k00, double rho2, int x0, int x1, int y0,
+                            int y1) {
     if (!(rho2 < INFINITY)) return true;
     if (rho2 < 0.0) return false;
     const double ax = (x0 + 0.5) - mx, bx = (x1 + 0.5) - mx;
@@ -1414,10 +1415,10 @@ static bool ellipse_may_hit(double mx, double my, double i00, double i01, double
         return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy;
     };
     auto clampd = [](double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); };
-    double qmin = q(ax, clampd(-i01 * ax / i11, ay, by));
-    qmin = std::fmin(qmin, q(bx, clampd(-i01 * bx / i11, ay, by)));
-    qmin = std::fmin(qmin, q(clampd(-i01 * ay / i00, ax, bx), ay));
-    qmin = std::fmin(qmin, q(clampd(-i01 * by / i00, ax, bx), by));
+    double qmin = q(ax, clampd(-(k11 * ax), ay, by));
+    qmin = std::fmin(qmin, q(bx, clampd(-(k11 * bx), ay, by)));
+    qmin = std::fmin(qmin, q(clampd(-(k00 * ay), ax, bx), ay));
+    qmin = std::fmin(qmin, q(clampd(-(k00 * by), ax, bx), by));
     const double mxd = std::fmax(std::fabs(ax), std::fabs(bx));
     const double myd = std::fmax(std::fabs(ay), std::fabs(by));
     const double bound = std::fabs(i00) * mxd * mxd + std::fabs(i11) * myd * myd +
@@ -1471,9 +1472,10 @@ int orc_binning(const double* x, int64_t k, const orc_camera* cam,
             prange(f.by0, f.by1, H, y0, y1);
             if (x0 > x1 || y0 > y1) continue;
             const double rho2 = contrib_rho2(f.alpha, ro->alpha_skip);
+            const double k11 = f.i01 / f.i11, k00 = f.i01 / f.i00;
             for (int ty = y0 / tile; ty <= y1 / tile; ++ty)
                 for (int tx = x0 / tile; tx <= x1 / tile; ++tx)
-                    if (ellipse_may_hit(f.mx, f.my, f.i00, f.i01, f.i11, rho2,
+                    if (ellipse_may_hit(f.mx, f.my, f.i00, f.i01, f.i11, k11, k00, rho2,
                                         std::max(x0, tx * tile), std::min(x1, tx * tile + tile - 1),
                                         std::max(y0, ty * tile), std::min(y1, ty * tile + tile - 1)))
                         per[(size_t)ty * tw + tx].push_back((int32_t)f.splat);

@@ -339,7 +339,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     double* htail = nullptr;     // pinned staging for the fused tail
@@ -409,6 +409,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.ids_alt = c.ids_alt.as<int>(K + 1);
     b.rect = c.rect.as<int4>(K + 1);
     b.tcount = c.tcount.as<int>(K + 1);
+    b.tmask = c.tmask.as<unsigned long long>(K + 1);
     b.off_r = c.off_r.as<long long>(K + 1);
     b.tile_start = c.tile_start.as<int>(n_tiles);
     b.tile_end = c.tile_end.as<int>(n_tiles);
@@ -424,7 +425,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
                               cudaMemcpyHostToDevice, c.st));
     {
         Timed t(c, KC_PROJECT);
-        launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount,
+        launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, b.tmask,
                        &c.dstat->vs);
     }
     {

@@ -30,6 +30,7 @@ __global__ void k_gather_counts(const int* __restrict__ sorted_ids,
 __global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids,
                                               const int* __restrict__ tcount,
                                               const int4* __restrict__ rect,
+                                              const unsigned long long* __restrict__ tmask,
                                               const double* __restrict__ rec,
                                               const long long* __restrict__ off_r,
                                               int n_visible, int tiles_x,
@@ -43,11 +44,22 @@ __global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids
     if (tcount[id] == 0) return;
     const int4 pr = rect[id];  // pixel range x0, y0, x1, y1
     const double* f = rec + (long long)kRec * id;
-    const double mx = f[R_MX], my = f[R_MY], i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
-    const double rho2 = f[R_RHO2];
     const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
     const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
     long long base = off_r[warp];
+    if (w * h <= 64) {  // hit bits recorded by K1
+        const unsigned long long bits = tmask[id];
+        for (int j = lane; j < w * h; j += 32) {
+            if (!((bits >> j) & 1ull)) continue;
+            const long long d = base + __popcll(bits & ((1ull << j) - 1ull));
+            tkeys[d] = (unsigned int)((ty0 + j / w) * tiles_x + tx0 + j % w);
+            dval[d] = (int)d;
+            dup_id[d] = id;
+        }
+        return;
+    }
+    const double mx = f[R_MX], my = f[R_MY], i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
+    const double rho2 = f[R_RHO2], k11 = f[R_K11], k00 = f[R_K00];
     for (int j0 = 0; j0 < w * h; j0 += 32) {
         const int j = j0 + lane;
         bool hit = false;
@@ -55,7 +67,7 @@ __global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids
         if (j < w * h) {
             ty = ty0 + j / w;
             tx = tx0 + j % w;
-            hit = ellipse_may_hit(mx, my, i00, i01, i11, rho2, max(pr.x, tx * kTile),
+            hit = ellipse_may_hit(mx, my, i00, i01, i11, k11, k00, rho2, max(pr.x, tx * kTile),
                                   min(pr.z, tx * kTile + kTile - 1), max(pr.y, ty * kTile),
                                   min(pr.w, ty * kTile + kTile - 1));
         }
@@ -146,8 +158,8 @@ void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long lon
     SGTR_CUDA(cudaMemsetAsync(b.tile_end, 0, sizeof(int) * n_tiles, st));
     if (n_dup == 0) return;
     k_emit<<<ceil_div((long long)n_visible * 32, 256), 256, 0, st>>>(
-        b.ids_alt, b.tcount, b.rect, b.rec, b.off_r, n_visible, tiles_x, b.tkeys, b.dval,
-        b.dup_id);
+        b.ids_alt, b.tcount, b.rect, b.tmask, b.rec, b.off_r, n_visible, tiles_x, b.tkeys,
+        b.dval, b.dup_id);
     SGTR_CUDA(cudaGetLastError());
     size_t bytes = b.temp_bytes;
     SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,

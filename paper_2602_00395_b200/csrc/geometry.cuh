@@ -290,8 +290,10 @@ SGTR_HD double contrib_rho2(double alpha, double alpha_skip) {
 // q = d^T Sigma^-1 d certainly above rho2 (the minimum of the convex q over
 // the rectangle, with a margin far above the rounding of the reference's own
 // exponent), i.e. when the reference would skip every one of these pairs.
+// k11 = i01 / i11 and k00 = i01 / i00 are the edge-minimiser slopes.
 SGTR_HD bool ellipse_may_hit(double mx, double my, double i00, double i01, double i11,
-                             double rho2, int x0, int x1, int y0, int y1) {
+                             double k11, double k00, double rho2, int x0, int x1, int y0,
+                             int y1) {
     if (!(rho2 < INFINITY)) return true;
     if (rho2 < 0.0) return false;
     const double ax = (x0 + 0.5) - mx, bx = (x1 + 0.5) - mx;
@@ -301,10 +303,10 @@ SGTR_HD bool ellipse_may_hit(double mx, double my, double i00, double i01, doubl
         return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy;
     };
     auto clampd = [](double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); };
-    double qmin = q(ax, clampd(-i01 * ax / i11, ay, by));
-    qmin = fmin(qmin, q(bx, clampd(-i01 * bx / i11, ay, by)));
-    qmin = fmin(qmin, q(clampd(-i01 * ay / i00, ax, bx), ay));
-    qmin = fmin(qmin, q(clampd(-i01 * by / i00, ax, bx), by));
+    double qmin = q(ax, clampd(-(k11 * ax), ay, by));
+    qmin = fmin(qmin, q(bx, clampd(-(k11 * bx), ay, by)));
+    qmin = fmin(qmin, q(clampd(-(k00 * ay), ax, bx), ay));
+    qmin = fmin(qmin, q(clampd(-(k00 * by), ax, bx), by));
     const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
     const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
     return qmin <= rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12;

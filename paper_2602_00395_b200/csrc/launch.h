@@ -9,9 +9,11 @@ namespace sgtr {
 // ---------------------------------------------------------------- project.cu
 // K1: per-splat projection -> 128-byte fragment record, order-preserving
 // 64-bit depth key (culled = ~0), tile rectangle and tile count.
+// tmask: per splat, the hit bits of its tile rectangle in row-major order
+// (rectangles of <= 64 tiles)
 void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
-                    int4* rect, int* tcount, ViewStatus* status);
+                    int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status);
 // parity dump: 12 doubles per splat (culled, depth, px, py, bx0..by1, i00..i11, 0)
 void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& cam,
                          const RenderP& ro, double* out);
@@ -38,6 +40,7 @@ struct BinBuffers {
     int4* rect;            // bbox pixel range (x0, y0, x1, y1) per splat
     const double* rec;     // fragment records (K1)
     int* tcount;
+    unsigned long long* tmask;  // tile-hit bits per splat (rects <= 64 tiles)
     long long* off_r;      // n+1 exclusive offsets in depth-rank order
     unsigned int *tkeys, *tkeys_alt;
     int *dval, *dval_alt;  // duplicate index carried through the tile sort

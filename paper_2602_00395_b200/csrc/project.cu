@@ -53,7 +53,9 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
                                                  RenderP ro, double* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys,
                                                  int* __restrict__ ids, int4* __restrict__ rect,
-                                                 int* __restrict__ tcount, ViewStatus* status) {
+                                                 int* __restrict__ tcount,
+                                                 unsigned long long* __restrict__ tmask,
+                                                 ViewStatus* status) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool visible = false;
     if (i < K) {
@@ -73,9 +75,9 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             double i00, i01, i11;
             invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
             const double rho2 = ro.cull ? contrib_rho2(p.alpha, ro.alpha_skip) : INFINITY;
-            double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,   py,       i00,  i01,
-                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], i01 / i11, rho2,
-                              i01 / i00};
+            const double k11 = i01 / i11, k00 = i01 / i00;
+            double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,  py,  i00, i01,
+                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], k11, rho2, k00};
             double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
 #pragma unroll
             for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);
@@ -89,14 +91,19 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
                 // tiles whose pixel centres inside the bbox can reach
                 // alpha_bar >= alpha_skip (geometry.cuh: ellipse_may_hit)
                 rect[i] = make_int4(x0, y0, x1, y1);
-                int n = 0;
+                int n = 0, j = 0;
+                unsigned long long bits = 0ull;  // row-major tile hits (rects <= 64 tiles)
                 for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx)
-                        n += ellipse_may_hit(px, py, i00, i01, i11, rho2, max(x0, tx * kTile),
-                                             min(x1, tx * kTile + kTile - 1),
-                                             max(y0, ty * kTile),
-                                             min(y1, ty * kTile + kTile - 1));
+                    for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx, ++j) {
+                        const bool hit = ellipse_may_hit(
+                            px, py, i00, i01, i11, k11, k00, rho2, max(x0, tx * kTile),
+                            min(x1, tx * kTile + kTile - 1), max(y0, ty * kTile),
+                            min(y1, ty * kTile + kTile - 1));
+                        n += hit;
+                        if (hit && j < 64) bits |= 1ull << j;
+                    }
                 tcount[i] = n;
+                tmask[i] = bits;
             }
         }
     }
@@ -297,10 +304,10 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
 
 void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
-                    int4* rect, int* tcount, ViewStatus* status) {
+                    int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status) {
     if (K == 0) return;
     k_project<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, rec, keys, ids, rect, tcount,
-                                                 status);
+                                                 tmask, status);
     SGTR_CUDA(cudaGetLastError());
 }
 
