@@ -80,7 +80,7 @@ struct DevStatus {
     double tr[5];
     double scalar;
     int queue_count;
-    int pad;
+    int n_large;
 };
 
 // RNG with the reference's variate mappings (rng.hpp:15-72)
@@ -339,7 +339,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, tbox;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     double* htail = nullptr;     // pinned staging for the fused tail
@@ -410,6 +410,8 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.rect = c.rect.as<int4>(K + 1);
     b.tcount = c.tcount.as<int>(K + 1);
     b.tmask = c.tmask.as<unsigned long long>(K + 1);
+    b.large = c.large.as<int>(K + 1);
+    b.n_large = &c.dstat->n_large;
     b.off_r = c.off_r.as<long long>(K + 1);
     b.tile_start = c.tile_start.as<int>(n_tiles);
     b.tile_end = c.tile_end.as<int>(n_tiles);
@@ -467,14 +469,16 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
         Timed t(c, KC_TILE_BIN);
         emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
     }
-    c.launches += vr.n_dup ? 5 : 0;  // emit, tile sort (histogram + 2 passes), ranges
+    c.launches += vr.n_dup ? 6 : 0;  // emit (2), tile sort (histogram + 2 passes), ranges
     int* tids = c.tile_ids.as<int>(nd);
     {
         Timed t(c, KC_TILE_BIN);
-        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, tids, c.inv.as<int>(nd));
+        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, rec, tids, c.inv.as<int>(nd),
+                        c.tbox.as<float4>(nd));
     }
     c.launches += vr.n_dup ? 1 : 0;
-    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt, b.dup_id, tids};
+    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start,          b.tile_end,
+                      b.dval_alt, b.dup_id,  tids, c.tbox.get<float4>()};
     const int P = dc.W * dc.H;
     Timed t(c, KC_RASTER_FWD);
     launch_raster_fwd(c.st, vr.tl, rec, dc.W, dc.H, ro, img_ptr(c, c.img, P),

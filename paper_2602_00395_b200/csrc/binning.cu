@@ -24,61 +24,86 @@ __global__ void k_gather_counts(const int* __restrict__ sorted_ids,
     if (r == K) cnt[r] = 0;
 }
 
-// one warp per splat: lanes stride over the tiles of the splat's bbox pixel
-// range, keep the ones ellipse_may_hit admits (the same test K1 counted) and
-// write them compacted in row-major tile order
-__global__ void __launch_bounds__(256) k_emit(const int* __restrict__ sorted_ids,
-                                              const int* __restrict__ tcount,
-                                              const int4* __restrict__ rect,
-                                              const unsigned long long* __restrict__ tmask,
-                                              const double* __restrict__ rec,
-                                              const long long* __restrict__ off_r,
-                                              int n_visible, int tiles_x,
-                                              unsigned int* __restrict__ tkeys,
-                                              int* __restrict__ dval,
-                                              int* __restrict__ dup_id) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n_visible) return;
-    const int id = sorted_ids[warp];
+// K4a: one thread per visible splat (depth-rank order).  Rectangles of <= 64
+// tiles are emitted from the hit bits K1 recorded, in row-major tile order;
+// larger ones are queued for K4b.
+__global__ void __launch_bounds__(256) k_emit_small(const int* __restrict__ sorted_ids,
+                                                    const int* __restrict__ tcount,
+                                                    const int4* __restrict__ rect,
+                                                    const unsigned long long* __restrict__ tmask,
+                                                    const long long* __restrict__ off_r,
+                                                    int n_visible, int tiles_x,
+                                                    unsigned int* __restrict__ tkeys,
+                                                    int* __restrict__ dval,
+                                                    int* __restrict__ dup_id,
+                                                    int* __restrict__ large,
+                                                    int* __restrict__ n_large) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_visible) return;
+    const int id = sorted_ids[r];
     if (tcount[id] == 0) return;
-    const int4 pr = rect[id];  // pixel range x0, y0, x1, y1
-    const double* f = rec + (long long)kRec * id;
+    const int4 pr = rect[id];
     const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
     const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
-    long long base = off_r[warp];
-    if (w * h <= 64) {  // hit bits recorded by K1
-        const unsigned long long bits = tmask[id];
-        for (int j = lane; j < w * h; j += 32) {
-            if (!((bits >> j) & 1ull)) continue;
-            const long long d = base + __popcll(bits & ((1ull << j) - 1ull));
-            tkeys[d] = (unsigned int)((ty0 + j / w) * tiles_x + tx0 + j % w);
-            dval[d] = (int)d;
-            dup_id[d] = id;
-        }
+    if (w * h > 64) {
+        large[atomicAdd(n_large, 1)] = r;
         return;
     }
-    const double mx = f[R_MX], my = f[R_MY], i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
-    const double rho2 = f[R_RHO2], k11 = f[R_K11], k00 = f[R_K00];
-    for (int j0 = 0; j0 < w * h; j0 += 32) {
-        const int j = j0 + lane;
-        bool hit = false;
-        int tx = 0, ty = 0;
-        if (j < w * h) {
-            ty = ty0 + j / w;
-            tx = tx0 + j % w;
-            hit = ellipse_may_hit(mx, my, i00, i01, i11, k11, k00, rho2, max(pr.x, tx * kTile),
-                                  min(pr.z, tx * kTile + kTile - 1), max(pr.y, ty * kTile),
-                                  min(pr.w, ty * kTile + kTile - 1));
+    unsigned long long bits = tmask[id];
+    long long d = off_r[r];
+    while (bits) {
+        const int j = __ffsll((long long)bits) - 1;
+        bits &= bits - 1ull;
+        tkeys[d] = (unsigned int)((ty0 + j / w) * tiles_x + tx0 + j % w);
+        dval[d] = (int)d;
+        dup_id[d] = id;
+        ++d;
+    }
+}
+
+// K4b: one warp per queued large rectangle: lanes re-evaluate ellipse_may_hit
+// (the K1 test) per tile and write the hits compacted in row-major order
+__global__ void __launch_bounds__(256) k_emit_large(const int* __restrict__ sorted_ids,
+                                                    const int4* __restrict__ rect,
+                                                    const double* __restrict__ rec,
+                                                    const long long* __restrict__ off_r,
+                                                    int tiles_x, const int* __restrict__ large,
+                                                    const int* __restrict__ n_large,
+                                                    unsigned int* __restrict__ tkeys,
+                                                    int* __restrict__ dval,
+                                                    int* __restrict__ dup_id) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < *n_large; q += nw) {
+        const int r = large[q];
+        const int id = sorted_ids[r];
+        const int4 pr = rect[id];
+        const double* f = rec + (long long)kRec * id;
+        const double mx = f[R_MX], my = f[R_MY], i00 = f[R_I00], i01 = f[R_I01];
+        const double i11 = f[R_I11], rho2 = f[R_RHO2], k11 = f[R_K11], k00 = f[R_K00];
+        const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
+        const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
+        long long base = off_r[r];
+        for (int j0 = 0; j0 < w * h; j0 += 32) {
+            const int j = j0 + lane;
+            bool hit = false;
+            int tx = 0, ty = 0;
+            if (j < w * h) {
+                ty = ty0 + j / w;
+                tx = tx0 + j % w;
+                hit = ellipse_may_hit(mx, my, i00, i01, i11, k11, k00, rho2,
+                                      max(pr.x, tx * kTile), min(pr.z, tx * kTile + kTile - 1),
+                                      max(pr.y, ty * kTile), min(pr.w, ty * kTile + kTile - 1));
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const long long d = base + __popc(m & ((1u << lane) - 1u));
+                tkeys[d] = (unsigned int)(ty * tiles_x + tx);
+                dval[d] = (int)d;
+                dup_id[d] = id;
+            }
+            base += __popc(m);
         }
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-            const long long d = base + __popc(m & ((1u << lane) - 1u));
-            tkeys[d] = (unsigned int)(ty * tiles_x + tx);
-            dval[d] = (int)d;
-            dup_id[d] = id;
-        }
-        base += __popc(m);
     }
 }
 
@@ -92,12 +117,18 @@ __global__ void k_ranges(const unsigned int* __restrict__ tkeys, long long n,
 }
 
 __global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restrict__ dup_id,
-                           long long n, int* __restrict__ tile_ids, int* __restrict__ inv) {
+                           long long n, const double* __restrict__ rec,
+                           int* __restrict__ tile_ids, int* __restrict__ inv,
+                           float4* __restrict__ tbox) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int d = sorted_d[j];
-    tile_ids[j] = dup_id[d];
+    const int id = dup_id[d];
+    tile_ids[j] = id;
     inv[d] = (int)j;
+    const double4 b = *reinterpret_cast<const double4*>(rec + (long long)kRec * id);
+    tbox[j] = make_float4(__double2float_rd(b.x), __double2float_ru(b.y),
+                          __double2float_rd(b.z), __double2float_ru(b.w));
 }
 
 int bits_for(int n) {
@@ -109,9 +140,9 @@ int bits_for(int n) {
 }  // namespace
 
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     int* tile_ids, int* inv) {
+                     const double* rec, int* tile_ids, int* inv, float4* tbox) {
     if (n == 0) return;
-    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, tile_ids, inv);
+    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, rec, tile_ids, inv, tbox);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -157,9 +188,13 @@ void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long lon
     SGTR_CUDA(cudaMemsetAsync(b.tile_start, 0, sizeof(int) * n_tiles, st));
     SGTR_CUDA(cudaMemsetAsync(b.tile_end, 0, sizeof(int) * n_tiles, st));
     if (n_dup == 0) return;
-    k_emit<<<ceil_div((long long)n_visible * 32, 256), 256, 0, st>>>(
-        b.ids_alt, b.tcount, b.rect, b.tmask, b.rec, b.off_r, n_visible, tiles_x, b.tkeys,
-        b.dval, b.dup_id);
+    SGTR_CUDA(cudaMemsetAsync(b.n_large, 0, sizeof(int), st));
+    k_emit_small<<<ceil_div(n_visible, 256), 256, 0, st>>>(
+        b.ids_alt, b.tcount, b.rect, b.tmask, b.off_r, n_visible, tiles_x, b.tkeys, b.dval,
+        b.dup_id, b.large, b.n_large);
+    SGTR_CUDA(cudaGetLastError());
+    k_emit_large<<<148 * 4, 256, 0, st>>>(b.ids_alt, b.rect, b.rec, b.off_r, tiles_x, b.large,
+                                          b.n_large, b.tkeys, b.dval, b.dup_id);
     SGTR_CUDA(cudaGetLastError());
     size_t bytes = b.temp_bytes;
     SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,

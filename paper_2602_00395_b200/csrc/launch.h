@@ -41,6 +41,8 @@ struct BinBuffers {
     const double* rec;     // fragment records (K1)
     int* tcount;
     unsigned long long* tmask;  // tile-hit bits per splat (rects <= 64 tiles)
+    int* large;            // depth ranks of splats with > 64-tile rectangles
+    int* n_large;
     long long* off_r;      // n+1 exclusive offsets in depth-rank order
     unsigned int *tkeys, *tkeys_alt;
     int *dval, *dval_alt;  // duplicate index carried through the tile sort
@@ -67,6 +69,7 @@ struct TileLists {
     const int* sorted_d;  // tile-sorted duplicate indices
     const int* dup_id;    // duplicate -> splat id
     const int* tile_ids;  // splat id per tile-sorted position (dup_id[sorted_d[j]])
+    const float4* tbox;   // outward-rounded float bbox (x0, x1, y0, y1) per position
 };
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
@@ -89,9 +92,10 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const 
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
                        const uint32_t* zbits, double* acc, double* nonfinite_flag);
-// tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j
+// tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j, tbox[j] = the
+// splat's bbox rounded outward to float
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     int* tile_ids, int* inv);
+                     const double* rec, int* tile_ids, int* inv, float4* tbox);
 // K12 (raster half): tangent image along the tangent records
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro,

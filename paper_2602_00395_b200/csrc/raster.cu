@@ -310,6 +310,34 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
     v8 = s;
 }
 
+// Warp reduction of 9 doubles through a warp-private shared scratch: lanes
+// store their 9 values (component-major, padded stride 33), 27 lanes each sum
+// an 11-lane third of one component, 9 lanes add the three thirds and write
+// the totals to out[0..8].  ~40 instructions instead of the shuffle
+// butterfly's selects and shuffles; fixed order, so deterministic.
+constexpr int kRedStride = 33;
+constexpr int kRedScratch = kAdj * kRedStride + 27;
+__device__ __forceinline__ void warp_reduce9_smem(const double* g, int lane, double* scr,
+                                                  double* out) {
+#pragma unroll
+    for (int c = 0; c < kAdj; ++c) scr[c * kRedStride + lane] = g[c];
+    __syncwarp();
+    if (lane < 27) {
+        const int c = lane / 3, q = lane % 3;
+        const double* col = scr + c * kRedStride + q * 11;
+        const int n = q == 2 ? 10 : 11;
+        double s = col[0];
+        for (int k = 1; k < n; ++k) s += col[k];
+        scr[kAdj * kRedStride + lane] = s;
+    }
+    __syncwarp();
+    if (lane < kAdj) {
+        const double* t = scr + kAdj * kRedStride + 3 * lane;
+        out[lane] = (t[0] + t[1]) + t[2];
+    }
+    __syncwarp();
+}
+
 template <bool kWarpCull, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists tl,
                                                          const double* __restrict__ rec, int W,
@@ -434,12 +462,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
 // stores them in its own partial slot (tile-sorted position j, warp w),
 // flagging mask[j * 8 + w]; K11 sums the flagged partials of each duplicate in
 // warp order (deterministic, no atomics).
-template <int kMinBlocks>
+template <int kMinBlocks, bool kSmemRed>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_raster_vjp_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       const double* __restrict__ adj, const double* __restrict__ tfinal,
                       const int* __restrict__ last, double* __restrict__ part,
                       unsigned char* __restrict__ mask) {
+    __shared__ double s_red[kWarps][kRedScratch];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -458,11 +487,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     if (!active) lastp = 0;
     double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;
     const int wlast = __reduce_max_sync(kFull, lastp);
+    // warp-span test on the outward-rounded float bbox of each tile-sorted
+    // position (contiguous, prefetched one entry ahead); the record is only
+    // fetched when the span test passes
+    float4 nb = wlast > 0 ? __ldg(tl.tbox + start + wlast - 1) : make_float4(0, 0, 0, 0);
     for (int j = start + wlast - 1; j >= start; --j) {
+        const float4 bb = nb;
+        if (j > start) nb = __ldg(tl.tbox + j - 1);
+        if (pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w) continue;
         const int id = __ldg(tl.tile_ids + j);
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-        if (pc.wx1 < bx.x || pc.wx0 > bx.y || pc.wy1 < by.x || pc.wy0 > by.y) continue;
         const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
         const double2 c01 = __ldg(r2 + 5), c2 = __ldg(r2 + 6);
         const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
@@ -505,14 +540,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             }
         }
         if (!__any_sync(kFull, contrib)) continue;
-        double v, v8;
-        warp_reduce9(g, lane, v, v8);
         double* o = part + ((long long)j * kWarps + warp) * kAdj;
-        if ((lane & 3) == 0) o[lane >> 2] = v;
-        if (lane == 0) {
-            o[8] = v8;
-            mask[(long long)j * kWarps + warp] = 1;
+        if (kSmemRed) {
+            warp_reduce9_smem(g, lane, s_red[warp], o);
+        } else {
+            double v, v8;
+            warp_reduce9(g, lane, v, v8);
+            if ((lane & 3) == 0) o[lane >> 2] = v;
+            if (lane == 0) o[8] = v8;
         }
+        if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
     }
 }
 
@@ -697,6 +734,7 @@ const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
+const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 
 }  // namespace
 
@@ -748,12 +786,12 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
         k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
     else if (g_vjp_ppl == 2)
         k_raster_vjp_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
-    else if (g_vjp_min_blocks == 3)
-        k_raster_vjp_warp<3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                     mask);
+    else if (g_smem_red)
+        k_raster_vjp_warp<3, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                           part, mask);
     else
-        k_raster_vjp_warp<2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                     mask);
+        k_raster_vjp_warp<3, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                            part, mask);
     SGTR_CUDA(cudaGetLastError());
 }
 

@@ -315,30 +315,40 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
                 eta[11 + c] = cap_radius(sqrt(4.0 * p.c[c] * a.eps / p.alpha), a.caps[4]);
             }
             eta[10] = cap_radius(sqrt(4.0 * p.alpha * a.eps), a.caps[3]);
-            // rotation (trust_region.cpp:198-234): Taylor radius + certification
-            const double lf = log_factor(a.eps, p.alpha);
-            double sigma[9];
-            if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
-                for (int c = 0; c < 4; ++c) eta[6 + c] = a.caps[2];
-            } else {
-                const double tol = a.eps * (1.0 + 1e-9);
-                for (int c = 0; c < 4; ++c) {
-                    const double beta = beta_rotation(p, c);
-                    const double r =
-                        beta <= 1e-12 ? a.caps[2] : cap_radius(sqrt(lf / beta), a.caps[2]);
-                    eta[6 + c] = r;
-                    RotAxis ra;
-                    rot_axis_setup(p, sigma, c, ra);
-                    if (!rot_within(ra, r, tol)) {
-                        const int slot = atomicAdd(a.queue_count, 1);
-                        a.queue[slot] = 4 * i + c;
-                    }
-                }
-            }
-            for (int j = 0; j < 14; ++j) a.eta_buf[flat_index(K, i, j)] = eta[j];
+            for (int j = 0; j < 3; ++j) a.eta_buf[3LL * i + j] = eta[j];
+            for (int j = 0; j < 3; ++j) a.eta_buf[3 * K + 3LL * i + j] = eta[3 + j];
+            a.eta_buf[10 * K + i] = eta[10];
+            for (int j = 0; j < 3; ++j) a.eta_buf[11 * K + 3LL * i + j] = eta[11 + j];
         }
     }
     block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
+}
+
+// K14a': one thread per (splat, rotation axis) (trust_region.cpp:198-234):
+// curvature beta_c, Taylor radius, certification against the exact
+// rotation-only H^2; axes failing certification are queued for K14b
+__global__ void __launch_bounds__(kThreads) k_tr_rot(TrArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 4LL * a.K) return;
+    const int i = (int)(t >> 2), c = (int)(t & 3);
+    const long long K = a.K;
+    const Prim p = load_prim(a.x, K, i);
+    const long long k = 6 * K + 4LL * i + c;
+    const double lf = log_factor(a.eps, p.alpha);
+    double sigma[9];
+    if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
+        a.eta_buf[k] = a.caps[2];
+        return;
+    }
+    const double beta = beta_rotation(p, c);
+    const double r = beta <= 1e-12 ? a.caps[2] : cap_radius(sqrt(lf / beta), a.caps[2]);
+    a.eta_buf[k] = r;
+    RotAxis ra;
+    rot_axis_setup(p, sigma, c, ra);
+    if (!rot_within(ra, r, a.eps * (1.0 + 1e-9))) {
+        const int slot = atomicAdd(a.queue_count, 1);
+        a.queue[slot] = 4 * i + c;
+    }
 }
 
 // K14b: one thread per queued (splat, rotation axis): the 60-step bisection
@@ -447,6 +457,10 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
         SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
         k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
+        if (!a.ghat_only) {
+            k_tr_rot<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
+            SGTR_CUDA(cudaGetLastError());
+        }
         if (a.ghat_only)
             SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
     } else if (phase == 1 && !a.ghat_only) {
