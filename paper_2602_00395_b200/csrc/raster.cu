@@ -196,6 +196,81 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K7, warp-filtered
+// Barrier-free forward: each warp (8x4 pixels) walks its tile's list front to
+// back in chunks of kChunkF positions; a chunk is filtered lane-parallel
+// (warp-span test on the outward-rounded float bbox, ballot-compacted into a
+// warp-private shared list), then the surviving entries are blended in order
+// with the same per-pixel operation sequence as k_raster_fwd.  The warp stops
+// once all its pixels terminated.
+constexpr int kChunkF = 256;
+__global__ void __launch_bounds__(kThreads)
+    k_raster_fwd_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                      double* __restrict__ img, double* __restrict__ tfinal,
+                      int* __restrict__ last) {
+    __shared__ int s_list[kWarps][kChunkF];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool done = !pc.inside;
+    int processed = end - start;
+    int* my_list = s_list[warp];
+    for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
+        if (__all_sync(kFull, done)) break;
+        const int cend = min(end, cbeg + kChunkF);
+        int nl = 0;
+        for (int base = cbeg; base < cend; base += 32) {
+            const int jj = base + lane;
+            bool pass = false;
+            if (jj < cend) {
+                const float4 bb = __ldg(tl.tbox + jj);
+                pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
+            }
+            const unsigned m = __ballot_sync(kFull, pass);
+            if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+            nl += __popc(m);
+        }
+        __syncwarp();
+        for (int e = 0; e < nl; ++e) {
+            const int j = my_list[e];
+            const int id = __ldg(tl.tile_ids + j);
+            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+            const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
+            if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
+                const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
+                const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
+                const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                                      c01.x, c01.y, cc2.x};
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T;
+                    c0 += f[R_C0] * w;
+                    c1 += f[R_C1] * w;
+                    c2 += f[R_C2] * w;
+                    T = __dmul_rn(T, __dsub_rn(1.0, abar));
+                    if (T < ro.t_stop) {
+                        done = true;
+                        processed = j - start + 1;
+                    }
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    img[p] = c0 + ro.bg[0] * T;
+    img[P + p] = c1 + ro.bg[1] * T;
+    img[2 * P + p] = c2 + ro.bg[2] * T;
+    tfinal[p] = T;
+    last[p] = processed;
+}
+
 // ------------------------------------------------------------------ K7, PPL pixels per lane
 // Barrier-free forward: warps walk the tile list on their own (records through
 // L1), each lane blends PPL pixels of one column (independent recurrences =
@@ -315,6 +390,7 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
 // an 11-lane third of one component, 9 lanes add the three thirds and write
 // the totals to out[0..8].  ~40 instructions instead of the shuffle
 // butterfly's selects and shuffles; fixed order, so deterministic.
+constexpr int kChunk = 256;
 constexpr int kRedStride = 33;
 constexpr int kRedScratch = kAdj * kRedStride + 27;
 __device__ __forceinline__ void warp_reduce9_smem(const double* g, int lane, double* scr,
@@ -469,6 +545,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                       const int* __restrict__ last, double* __restrict__ part,
                       unsigned char* __restrict__ mask) {
     __shared__ double s_red[kWarps][kRedScratch];
+    __shared__ int s_list[kWarps][kChunk];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -487,14 +564,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     if (!active) lastp = 0;
     double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;
     const int wlast = __reduce_max_sync(kFull, lastp);
-    // warp-span test on the outward-rounded float bbox of each tile-sorted
-    // position (contiguous, prefetched one entry ahead); the record is only
-    // fetched when the span test passes
-    float4 nb = wlast > 0 ? __ldg(tl.tbox + start + wlast - 1) : make_float4(0, 0, 0, 0);
-    for (int j = start + wlast - 1; j >= start; --j) {
-        const float4 bb = nb;
-        if (j > start) nb = __ldg(tl.tbox + j - 1);
-        if (pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w) continue;
+    // The list is walked back to front in chunks of kChunk positions.  Each
+    // chunk is first filtered lane-parallel (one warp-span test per lane on the
+    // outward-rounded float bbox, ballot-compacted into this warp's shared
+    // list), so the sequential pass only visits entries that can touch the
+    // warp's 8x4 pixels.
+    int* my_list = s_list[warp];
+    for (int cend = start + wlast; cend > start; cend -= kChunk) {
+    const int cbeg = max(start, cend - kChunk);
+    int nl = 0;
+    for (int base = cbeg; base < cend; base += 32) {
+        const int jj = base + lane;
+        bool pass = false;
+        if (jj < cend) {
+            const float4 bb = __ldg(tl.tbox + jj);
+            pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+        nl += __popc(m);
+    }
+    __syncwarp();
+    for (int e = nl - 1; e >= 0; --e) {
+        const int j = my_list[e];
         const int id = __ldg(tl.tile_ids + j);
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
@@ -550,6 +642,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             if (lane == 0) o[8] = v8;
         }
         if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
+    }
+    __syncwarp();
     }
 }
 
@@ -734,6 +828,7 @@ const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
+const int g_fwd_warp = knob("SGTR_FWD_WARP", 1);
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 
 }  // namespace
@@ -746,6 +841,8 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
+    else if (g_fwd_warp)
+        k_raster_fwd_warp<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_ppl == 4)
         k_raster_fwd_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_ppl == 2)

@@ -17,6 +17,7 @@
 // Images are planar (3, H, W); for a planar image the residual block index
 // c*H*W + y*W + x (residuals.cpp:19-22) is the plane index itself.
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 #include "geometry.cuh"
@@ -25,7 +26,8 @@
 namespace sgtr {
 namespace {
 
-constexpr int TX = 32, TY = 8, HALO = 5;
+constexpr int TX = 32, TY = 16, HALO = 5;
+constexpr int kThreads = 256;  // TX * TY / 2: two output rows per thread
 constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 18
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
@@ -39,6 +41,13 @@ __device__ __forceinline__ int reflect(int i, int n) {
 
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
+template <typename S>
+__device__ __forceinline__ S mk(double v, double d);
+template <>
+__device__ __forceinline__ double mk<double>(double v, double) { return v; }
+template <>
+__device__ __forceinline__ Dual mk<Dual>(double v, double d) { return Dual(v, d); }
+
 template <int MODE>
 struct ModeTraits {
     static constexpr bool kTangent = MODE == SSIM_JVP || MODE == RES_JVP || MODE == HUTCH;
@@ -47,7 +56,7 @@ struct ModeTraits {
 
 // moments: 0 mu_a, 1 mu_b, 2 maa, 3 mbb, 4 mab, (5 dmu_a, 6 dmaa, 7 dmab)
 template <int MODE>
-__global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
+__global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
     using Tr = ModeTraits<MODE>;
     constexpr int NM = Tr::kMoments;
     extern __shared__ __align__(16) double smem[];
@@ -62,7 +71,7 @@ __global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
     const double* A = args.a + c * P;
     const double* B = args.b + c * P;
     const double* DA = Tr::kTangent ? args.da + c * P : nullptr;
-    for (int i = threadIdx.x; i < SY * SX; i += TX * TY) {
+    for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
         const int sy = i / SX, sx = i % SX;
         const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
         double va = 0.0, vb = 0.0, vd = 0.0;
@@ -78,7 +87,7 @@ __global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
     }
     __syncthreads();
     // horizontal pass over all SY rows
-    for (int i = threadIdx.x; i < SY * TX; i += TX * TY) {
+    for (int i = threadIdx.x; i < SY * TX; i += kThreads) {
         const int sy = i / TX, tx = i % TX;
         double m[NM];
 #pragma unroll
@@ -103,7 +112,10 @@ __global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
         for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TX + tx] = m[j];
     }
     __syncthreads();
-    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
+    const int tx = threadIdx.x % TX;
+    double partial = 0.0;
+    for (int ty = threadIdx.x / TX; ty < TY; ty += kThreads / TX) {
     const int gx = x0 + tx, gy = y0 + ty;
     double m[NM];
 #pragma unroll
@@ -114,49 +126,51 @@ __global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
 #pragma unroll
         for (int j = 0; j < NM; ++j) m[j] += w * s_h[(j * SY + ty + d) * TX + tx];
     }
-    double partial = 0.0;
     if (gx < W && gy < H) {
         const long long p = (long long)gy * W + gx;
         const long long pi = c * P + p;
-        // SSIM with its tangent (ssim.cpp:50-58 with Dual a)
-        const Dual mu_a(m[0], Tr::kTangent ? m[5] : 0.0);
-        const Dual maa(m[2], Tr::kTangent ? m[6] : 0.0);
-        const Dual mab(m[4], Tr::kTangent ? m[7] : 0.0);
+        // SSIM (with its tangent in the JVP modes), ssim.cpp:50-58
+        const S mu_a = mk<S>(m[0], Tr::kTangent ? m[5] : 0.0);
+        const S maa = mk<S>(m[2], Tr::kTangent ? m[6] : 0.0);
+        const S mab = mk<S>(m[4], Tr::kTangent ? m[7] : 0.0);
         const double mu_b = m[1], mbb = m[3];
-        const Dual n1 = 2.0 * mu_a * mu_b + kC1;
-        const Dual d1 = mu_a * mu_a + mu_b * mu_b + kC1;
-        const Dual n2 = 2.0 * (mab - mu_a * mu_b) + kC2;
-        const Dual d2 = (maa - mu_a * mu_a) + (mbb - mu_b * mu_b) + kC2;
-        const Dual s = (n1 * n2) / (d1 * d2);
+        const S n1 = 2.0 * mu_a * mu_b + kC1;
+        const S d1 = mu_a * mu_a + mu_b * mu_b + kC1;
+        const S n2 = 2.0 * (mab - mu_a * mu_b) + kC2;
+        const S d2 = (maa - mu_a * mu_a) + (mbb - mu_b * mu_b) + kC2;
+        const S sv = (n1 * n2) / (d1 * d2);
+        const double s_v = primal(sv), s_d = tangent(sv);
+        const double n1v = primal(n1), d1v = primal(d1), n2v = primal(n2), d2v = primal(d2);
+        const double mu_av = primal(mu_a);
         const double av = s_a[(ty + HALO) * SX + tx + HALO];
         const double bv = s_b[(ty + HALO) * SX + tx + HALO];
         const double diff = av - bv;
         const double lam = args.lambda, fl = args.floor;
         const double u1 = (1.0 - lam) * fabs(diff);
-        const double u2 = lam * (1.0 - s.v) / 2.0;
+        const double u2 = lam * (1.0 - s_v) / 2.0;
         if (MODE == SSIM_MAP) {
-            args.out0[pi] = s.v;
+            args.out0[pi] = s_v;
         } else if (MODE == SSIM_JVP) {
-            args.out0[pi] = s.v;
-            args.out1[pi] = s.d;
+            args.out0[pi] = s_v;
+            args.out1[pi] = s_d;
         } else if (MODE == RES_VEC) {
             args.out0[pi] = sqrt(fmax(u1, fl));
             args.out0[3 * P + pi] = sqrt(fmax(u2, fl));
         } else if (MODE == RES_JVP) {
             const double t = s_da[(ty + HALO) * SX + tx + HALO];
             args.out0[pi] = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
-            args.out0[3 * P + pi] = u2 > fl ? -lam * s.d / (4.0 * sqrt(u2)) : 0.0;
+            args.out0[3 * P + pi] = u2 > fl ? -lam * s_d / (4.0 * sqrt(u2)) : 0.0;
         } else {
             // image-space adjoint of the residual chain (residuals.cpp:81-117)
             double ur1, ur2;  // residual-space upstream for this entry
             if (MODE == GRAD) {
                 ur1 = sqrt(fmax(u1, fl));
                 ur2 = sqrt(fmax(u2, fl));
-                partial = ur1 * ur1 + ur2 * ur2;
+                partial += ur1 * ur1 + ur2 * ur2;
             } else if (MODE == HUTCH) {
                 const double t = s_da[(ty + HALO) * SX + tx + HALO];
                 ur1 = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
-                ur2 = u2 > fl ? -lam * s.d / (4.0 * sqrt(u2)) : 0.0;
+                ur2 = u2 > fl ? -lam * s_d / (4.0 * sqrt(u2)) : 0.0;
             } else if (MODE == RES_VJP) {
                 ur1 = args.u[pi];
                 ur2 = args.u[3 * P + pi];
@@ -172,26 +186,27 @@ __global__ void __launch_bounds__(TX* TY) k_ssim(SsimArgs args) {
                 up = u2 > fl ? ur2 * (-lam / (4.0 * sqrt(u2))) : 0.0;
             }
             // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155)
-            const double pp = n1.v / d1.v, qq = n2.v / d2.v;
-            const double ds_dmu = qq * (2.0 * mu_b * d1.v - 2.0 * mu_a.v * n1.v) / (d1.v * d1.v) +
-                                  pp * (2.0 * mu_a.v * n2.v - 2.0 * mu_b * d2.v) / (d2.v * d2.v);
-            const double ds_dmaa = -pp * n2.v / (d2.v * d2.v);
-            const double ds_dmab = pp * 2.0 / d2.v;
+            const double pp = n1v / d1v, qq = n2v / d2v;
+            const double ds_dmu = qq * (2.0 * mu_b * d1v - 2.0 * mu_av * n1v) / (d1v * d1v) +
+                                  pp * (2.0 * mu_av * n2v - 2.0 * mu_b * d2v) / (d2v * d2v);
+            const double ds_dmaa = -pp * n2v / (d2v * d2v);
+            const double ds_dmab = pp * 2.0 / d2v;
             args.P[pi] = up * ds_dmu;
             args.Q[pi] = up * ds_dmaa * 2.0;
             args.R[pi] = up * ds_dmab;
         }
     }
+    }
     if (MODE == GRAD) {
         // deterministic block sum -> one partial per block
-        __shared__ double s_red[TX * TY / 32];
+        __shared__ double s_red[kThreads / 32];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) partial += __shfl_xor_sync(0xffffffffu, partial, o);
         if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = partial;
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
-            for (int w = 0; w < TX * TY / 32; ++w) t += s_red[w];
+            for (int w = 0; w < kThreads / 32; ++w) t += s_red[w];
             const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
             args.loss_partials[blk] = t;
         }
@@ -216,7 +231,7 @@ __device__ __forceinline__ double transposed_1d(int p, int n, Ld ld) {
     return t;
 }
 
-__global__ void __launch_bounds__(TX* TY) k_gather(int W, int H, const double* __restrict__ a,
+__global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double* __restrict__ a,
                                                    const double* __restrict__ b,
                                                    const double* __restrict__ adjl1,
                                                    const double* __restrict__ Pf,
@@ -228,7 +243,7 @@ __global__ void __launch_bounds__(TX* TY) k_gather(int W, int H, const double* _
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    for (int i = threadIdx.x; i < SY * SX; i += TX * TY) {
+    for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
         const int sy = i / SX, sx = i % SX;
         const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
         const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
@@ -239,7 +254,7 @@ __global__ void __launch_bounds__(TX* TY) k_gather(int W, int H, const double* _
     }
     __syncthreads();
     // horizontal transposed pass for every staged row
-    for (int i = threadIdx.x; i < SY * TX; i += TX * TY) {
+    for (int i = threadIdx.x; i < SY * TX; i += kThreads) {
         const int sy = i / TX, tx = i % TX;
         const int gx = x0 + tx;
 #pragma unroll
@@ -251,16 +266,18 @@ __global__ void __launch_bounds__(TX* TY) k_gather(int W, int H, const double* _
         }
     }
     __syncthreads();
-    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-    const int gx = x0 + tx, gy = y0 + ty;
-    if (gx >= W || gy >= H) return;
-    double t[3];
+    const int tx = threadIdx.x % TX;
+    for (int ty = threadIdx.x / TX; ty < TY; ty += kThreads / TX) {
+        const int gx = x0 + tx, gy = y0 + ty;
+        if (gx >= W || gy >= H) continue;
+        double t[3];
 #pragma unroll
-    for (int f = 0; f < 3; ++f)
-        t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
-    const long long p = c * P + (long long)gy * W + gx;
-    const double base = adjl1 ? adjl1[p] : 0.0;
-    adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
+        for (int f = 0; f < 3; ++f)
+            t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
+        const long long p = c * P + (long long)gy * W + gx;
+        const double base = adjl1 ? adjl1[p] : 0.0;
+        adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
+    }
 }
 
 __global__ void k_sum_partials(const double* __restrict__ partials, int n, double* out) {
@@ -327,7 +344,7 @@ void run_ssim(cudaStream_t st, const SsimArgs& a) {
         attr = true;
     }
     dim3 grid(ceil_div(a.W, TX), ceil_div(a.H, TY), 3);
-    k_ssim<MODE><<<grid, TX * TY, smem, st>>>(a);
+    k_ssim<MODE><<<grid, kThreads, smem, st>>>(a);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -355,7 +372,7 @@ void launch_ssim_gather(cudaStream_t st, int W, int H, const double* a, const do
                         double* adj) {
     init_constants();
     dim3 grid(ceil_div(W, TX), ceil_div(H, TY), 3);
-    k_gather<<<grid, TX * TY, 0, st>>>(W, H, a, b, adjl1, P, Q, R, adj);
+    k_gather<<<grid, kThreads, 0, st>>>(W, H, a, b, adjl1, P, Q, R, adj);
     SGTR_CUDA(cudaGetLastError());
 }
 
