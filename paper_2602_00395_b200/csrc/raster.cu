@@ -824,7 +824,7 @@ int knob(const char* name, int dflt) {
     return v ? atoi(v) : dflt;
 }
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
-const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);
+const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);  // (slot-form VJP only)
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
