@@ -502,6 +502,15 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                                    part, mask);
         }
         Timed t(c, KC_CHAIN);
+        if (chain_mode() == 1) {
+            double* slots = c.slots.as<double>((size_t)kAdj * nd);
+            launch_partials_to_slots(c.st, vr.tl.sorted_d, vr.n_dup, part, mask, slots);
+            launch_chain(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+                         c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits,
+                         acc, flag);
+            c.launches += 3;
+            return;
+        }
         launch_chain_warp(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                           c.off_r.get<long long>(), c.tcount.get<int>(), c.inv.get<int>(), part,
                           mask, zdense, zbits, acc, flag);

@@ -92,6 +92,10 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const 
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
                        const uint32_t* zbits, double* acc, double* nonfinite_flag);
+// per-warp partials of the barrier-free K10 -> per-duplicate slots (warp order)
+void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
+                              const double* part, const unsigned char* mask, double* slots);
+int chain_mode();
 // tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j, tbox[j] = the
 // splat's bbox rounded outward to float
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,

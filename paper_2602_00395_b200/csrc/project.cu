@@ -300,7 +300,40 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
 
+// per tile-sorted position j: the duplicate's 9 adjoints are the sum of the
+// per-warp partials flagged in mask[j] (warp order), stored at slot
+// sorted_d[j] so that K11 reads each splat's slots contiguously
+__global__ void __launch_bounds__(256) k_partials_to_slots(const int* __restrict__ sorted_d,
+                                                           long long n,
+                                                           const double* __restrict__ part,
+                                                           const unsigned char* __restrict__ mask,
+                                                           double* __restrict__ slots) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * j);
+    double a[kAdj];
+#pragma unroll
+    for (int c = 0; c < kAdj; ++c) a[c] = 0.0;
+    const double* pp = part + j * 8 * kAdj;
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+        if ((m >> (8 * w)) & 0xffull) {
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+        }
+    double* o = slots + (long long)kAdj * sorted_d[j];
+#pragma unroll
+    for (int c = 0; c < kAdj; ++c) o[c] = a[c];
+}
+
 }  // namespace
+
+void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
+                              const double* part, const unsigned char* mask, double* slots) {
+    if (n == 0) return;
+    k_partials_to_slots<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, n, part, mask, slots);
+    SGTR_CUDA(cudaGetLastError());
+}
 
 void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,

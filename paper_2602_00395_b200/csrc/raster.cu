@@ -271,6 +271,90 @@ __global__ void __launch_bounds__(kThreads)
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K12 (raster), warp-filtered
+// Forward-mode tangent image with the same chunked, warp-filtered walk as
+// k_raster_fwd_warp; records and tangent records read through L1.
+__global__ void __launch_bounds__(kThreads)
+    k_raster_jvp_warp(TileLists tl, const double* __restrict__ rec,
+                      const double* __restrict__ trec, int W, int H, RenderP ro,
+                      double* __restrict__ tangent) {
+    __shared__ int s_list[kWarps][kChunkF];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, dT = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    bool done = !pc.inside;
+    int* my_list = s_list[warp];
+    for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
+        if (__all_sync(kFull, done)) break;
+        const int cend = min(end, cbeg + kChunkF);
+        int nl = 0;
+        for (int base = cbeg; base < cend; base += 32) {
+            const int jj = base + lane;
+            bool pass = false;
+            if (jj < cend) {
+                const float4 bb = __ldg(tl.tbox + jj);
+                pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
+            }
+            const unsigned m = __ballot_sync(kFull, pass);
+            if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+            nl += __popc(m);
+        }
+        __syncwarp();
+        for (int e = 0; e < nl; ++e) {
+            const int j = my_list[e];
+            const int id = __ldg(tl.tile_ids + j);
+            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+            const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
+            if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
+                const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
+                const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
+                const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                                      c01.x, c01.y, cc2.x};
+                const double* tp = trec + (long long)kTRec * id;
+                double t[kTRec];
+#pragma unroll
+                for (int q = 0; q < kTRec / 2; ++q) {
+                    const double2 v = __ldg(reinterpret_cast<const double2*>(tp) + q);
+                    t[2 * q] = v.x;
+                    t[2 * q + 1] = v.y;
+                }
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                const double ex0 = exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], ex0);
+                const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
+                const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
+                    I11(f[R_I11], t[T_I11]);
+                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
+                double dabar = t[T_ALPHA] * ex0 + f[R_ALPHA] * (ex0 * ex.d);
+                if (abar >= ro.alpha_clamp) {
+                    abar = ro.alpha_clamp;
+                    dabar = 0.0;
+                }
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T;
+                    const double dw = dabar * T + abar * dT;
+                    d0 += t[T_C0] * w + f[R_C0] * dw;
+                    d1 += t[T_C1] * w + f[R_C1] * dw;
+                    d2 += t[T_C2] * w + f[R_C2] * dw;
+                    const double om = __dsub_rn(1.0, abar);
+                    dT = dT * om + T * (-dabar);
+                    T = __dmul_rn(T, om);
+                    if (T < ro.t_stop) done = true;
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    tangent[p] = d0 + ro.bg[0] * dT;
+    tangent[P + p] = d1 + ro.bg[1] * dT;
+    tangent[2 * P + p] = d2 + ro.bg[2] * dT;
+}
+
 // ------------------------------------------------------------------ K7, PPL pixels per lane
 // Barrier-free forward: warps walk the tile list on their own (records through
 // L1), each lane blends PPL pixels of one column (independent recurrences =
@@ -873,6 +957,7 @@ void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, 
 }
 
 int vjp_mode() { return g_vjp_mode; }
+int chain_mode() { return knob("SGTR_CHAIN_MODE", 1); }
 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
@@ -896,7 +981,9 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    if (g_warp_cull)
+    if (g_fwd_warp)
+        k_raster_jvp_warp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    else if (g_warp_cull)
         k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     else
         k_raster_jvp<false><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);

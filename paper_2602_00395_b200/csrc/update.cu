@@ -102,21 +102,25 @@ __device__ double beta_rotation(const Prim& p, int axis) {
     d2rt[0] = (axis == 0 || axis == 3) ? 2.0 : -2.0;
     d2rt[4] = (axis == 1 || axis == 3) ? 2.0 : -2.0;
     d2rt[8] = (axis == 2 || axis == 3) ? 2.0 : -2.0;
+    // reciprocals instead of the reference's per-entry divisions (same
+    // quantities; rounding-level differences only)
+    const double ir2 = 1.0 / r2, ir4 = ir2 * ir2;
     double r[9];
-    for (int i = 0; i < 9; ++i) r[i] = rt[i] / r2;
-    const double k1 = 2.0 * qc / (r2 * r2);
-    const double k2 = 4.0 * qc / (r2 * r2);
-    const double k3 = 8.0 * qc * qc / (r2 * r2 * r2) - 2.0 / (r2 * r2);
+    for (int i = 0; i < 9; ++i) r[i] = rt[i] * ir2;
+    const double k1 = 2.0 * qc * ir4;
+    const double k2 = 4.0 * qc * ir4;
+    const double k3 = 8.0 * qc * qc * ir4 * ir2 - 2.0 * ir4;
     double in1[9], in2[9];
     for (int i = 0; i < 9; ++i) {
-        in1[i] = drt[i] / r2 - k1 * rt[i];
-        in2[i] = d2rt[i] / r2 - k2 * drt[i] + k3 * rt[i];
+        in1[i] = drt[i] * ir2 - k1 * rt[i];
+        in2[i] = d2rt[i] * ir2 - k2 * drt[i] + k3 * rt[i];
     }
+    const double is[3] = {1.0 / p.s[0], 1.0 / p.s[1], 1.0 / p.s[2]};
     double frob = 0.0, tr = 0.0;
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j) {
             const double de = r[i] * in1[j] + r[3 + i] * in1[3 + j] + r[6 + i] * in1[6 + j];
-            const double v = p.s[i] * de / p.s[j];
+            const double v = p.s[i] * de * is[j];
             frob += v * v;
         }
     // trace of r^T in2, summed over the diagonal in order
@@ -182,7 +186,29 @@ __device__ double rot_h2(const RotAxis& ra, double dq) {
                            0.5 * (ra.sigma[8] + c[5])};
     const double dm = det3(mid);
     if (!(dm > 0.0)) return CUDART_INF;
-    return ra.alpha * (1.0 - ra.det_s / sqrt(dm));
+    return ra.alpha * (1.0 - ra.det_s * rsqrt(dm));
+}
+
+// Sigma = R^T diag(s^2) R with R = R~(q) * (1/|q|^2): the covariance of
+// geometry.cuh with one division instead of nine (rotation certification only)
+__device__ bool cov_fast(const double* s, const double* q, double* cov) {
+    const double x = q[0], y = q[1], z = q[2], w = q[3];
+    const double r2 = x * x + y * y + z * z + w * w;
+    if (r2 < 1e-24) return false;
+    const double ir2 = 1.0 / r2;
+    const double r[9] = {(r2 - 2.0 * (y * y + z * z)) * ir2, 2.0 * (x * y - w * z) * ir2,
+                         2.0 * (x * z + w * y) * ir2,         2.0 * (x * y + w * z) * ir2,
+                         (r2 - 2.0 * (z * z + x * x)) * ir2, 2.0 * (y * z - w * x) * ir2,
+                         2.0 * (x * z - w * y) * ir2,         2.0 * (y * z + w * x) * ir2,
+                         (r2 - 2.0 * (x * x + y * y)) * ir2};
+    const double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            cov[3 * i + j] = r[i] * s2[0] * r[j] + r[3 + i] * s2[1] * r[3 + j] +
+                             r[6 + i] * s2[2] * r[6 + j];
+    return true;
 }
 
 __device__ __forceinline__ bool rot_within(const RotAxis& ra, double st, double tol) {
@@ -194,6 +220,9 @@ __device__ double rot_bisect(const RotAxis& ra, double r, double tol) {
     double lo = 0.0, hi = r;
     for (int it = 0; it < 60; ++it) {
         const double mid = 0.5 * (lo + hi);
+        // once mid rounds onto an endpoint the remaining iterations cannot
+        // move lo: the reference's 60-step result is reached
+        if (mid == lo || mid == hi) break;
         if (rot_within(ra, mid, tol))
             lo = mid;
         else
@@ -212,7 +241,7 @@ __device__ void radii(const Prim& p, double eps, const double* caps, double* eta
     // rotation (trust_region.cpp:198-234)
     const double lf = log_factor(eps, p.alpha);
     double sigma[9];
-    if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
+    if (lf <= 0.0 || !cov_fast(p.s, p.q, sigma)) {
         for (int c = 0; c < 4; ++c) eta[6 + c] = caps[2];
         return;
     }
@@ -336,7 +365,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_rot(TrArgs a) {
     const long long k = 6 * K + 4LL * i + c;
     const double lf = log_factor(a.eps, p.alpha);
     double sigma[9];
-    if (lf <= 0.0 || !covariance(p.s, p.q, sigma)) {
+    if (lf <= 0.0 || !cov_fast(p.s, p.q, sigma)) {
         a.eta_buf[k] = a.caps[2];
         return;
     }
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_bisect(TrArgs a) {
     const long long K = a.K;
     const Prim p = load_prim(a.x, K, i);
     double sigma[9];
-    covariance(p.s, p.q, sigma);
+    cov_fast(p.s, p.q, sigma);
     RotAxis ra;
     rot_axis_setup(p, sigma, c, ra);
     const long long k = 6 * K + 4LL * i + c;
