@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kThreads)
                       double* __restrict__ img, double* __restrict__ tfinal,
                       int* __restrict__ last) {
     __shared__ int s_list[kWarps][kChunkF];
+    __shared__ int s_ids[kWarps][kChunkF];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kThreads)
     bool done = !pc.inside;
     int processed = end - start;
     int* my_list = s_list[warp];
+    int* my_ids = s_ids[warp];
     for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
         if (__all_sync(kFull, done)) break;
         const int cend = min(end, cbeg + kChunkF);
@@ -229,13 +231,17 @@ __global__ void __launch_bounds__(kThreads)
                 pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
             }
             const unsigned m = __ballot_sync(kFull, pass);
-            if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+            if (pass) {
+                const int q = nl + __popc(m & ((1u << lane) - 1u));
+                my_list[q] = jj;
+                my_ids[q] = __ldg(tl.tile_ids + jj);
+            }
             nl += __popc(m);
         }
         __syncwarp();
         for (int e = 0; e < nl; ++e) {
             const int j = my_list[e];
-            const int id = __ldg(tl.tile_ids + j);
+            const int id = my_ids[e];
             const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
             const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
             if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
@@ -279,6 +285,7 @@ __global__ void __launch_bounds__(kThreads)
                       const double* __restrict__ trec, int W, int H, RenderP ro,
                       double* __restrict__ tangent) {
     __shared__ int s_list[kWarps][kChunkF];
+    __shared__ int s_ids[kWarps][kChunkF];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -286,6 +293,7 @@ __global__ void __launch_bounds__(kThreads)
     double T = 1.0, dT = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
     bool done = !pc.inside;
     int* my_list = s_list[warp];
+    int* my_ids = s_ids[warp];
     for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
         if (__all_sync(kFull, done)) break;
         const int cend = min(end, cbeg + kChunkF);
@@ -298,13 +306,17 @@ __global__ void __launch_bounds__(kThreads)
                 pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
             }
             const unsigned m = __ballot_sync(kFull, pass);
-            if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+            if (pass) {
+                const int q = nl + __popc(m & ((1u << lane) - 1u));
+                my_list[q] = jj;
+                my_ids[q] = __ldg(tl.tile_ids + jj);
+            }
             nl += __popc(m);
         }
         __syncwarp();
         for (int e = 0; e < nl; ++e) {
             const int j = my_list[e];
-            const int id = __ldg(tl.tile_ids + j);
+            const int id = my_ids[e];
             const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
             const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
             if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
     }
     for (int j = start; j < end; ++j) {
         if (__all_sync(kFull, all_done)) break;
-        const int id = __ldg(tl.tile_ids + j);
+        const int id = my_ids[e];
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
         if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
@@ -630,6 +642,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
                       unsigned char* __restrict__ mask) {
     __shared__ double s_red[kWarps][kRedScratch];
     __shared__ int s_list[kWarps][kChunk];
+    __shared__ int s_ids[kWarps][kChunk];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
@@ -654,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     // list), so the sequential pass only visits entries that can touch the
     // warp's 8x4 pixels.
     int* my_list = s_list[warp];
+    int* my_ids = s_ids[warp];
     for (int cend = start + wlast; cend > start; cend -= kChunk) {
     const int cbeg = max(start, cend - kChunk);
     int nl = 0;
@@ -665,13 +679,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
             pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
         }
         const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) my_list[nl + __popc(m & ((1u << lane) - 1u))] = jj;
+        if (pass) {
+                const int q = nl + __popc(m & ((1u << lane) - 1u));
+                my_list[q] = jj;
+                my_ids[q] = __ldg(tl.tile_ids + jj);
+            }
         nl += __popc(m);
     }
     __syncwarp();
     for (int e = nl - 1; e >= 0; --e) {
         const int j = my_list[e];
-        const int id = __ldg(tl.tile_ids + j);
+        const int id = my_ids[e];
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
         const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
@@ -779,7 +797,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
     }
     const int wlast = __reduce_max_sync(kFull, lmax);
     for (int j = start + wlast - 1; j >= start; --j) {
-        const int id = __ldg(tl.tile_ids + j);
+        const int id = my_ids[e];
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
         if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;

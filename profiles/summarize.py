@@ -61,10 +61,12 @@ def full(path):
                     x = to_mb(v, units[ix[metric]]) if "bytes" in metric else float(v)
                 except ValueError:
                     continue
-                xs.append(x * scale if key == "time_us" and units[ix[metric]] == "nsecond" else x)
-            if key == "time_us" and units[ix[metric]] == "msecond":
+                xs.append(x * scale if key == "time_us" and units[ix[metric]] in ("nsecond", "ns")
+                          else x)
+            u = units[ix[metric]]
+            if key == "time_us" and u in ("msecond", "ms"):
                 xs = [x * 1e3 for x in xs]
-            elif key == "time_us" and units[ix[metric]] == "usecond":
+            elif key == "time_us" and u in ("usecond", "us"):
                 xs = [x / scale for x in xs]
             vals.append(f"{sum(xs) / len(xs):.4g}" if xs else "?")
         st = {}
@@ -95,7 +97,7 @@ def launches(path):
         name = r[ix["Kernel Name"]].split("(")[0].split("::")[-1]
         v = float(r[ix["Metric Value"]].replace(",", ""))
         unit = r[ix["Metric Unit"]]
-        us = v / 1e3 if unit == "nsecond" else v if unit == "usecond" else v * 1e3
+        us = v / 1e3 if unit in ("nsecond", "ns") else v if unit in ("usecond", "us") else v * 1e3
         tot[name] += us
         cnt[name] += 1
     s = sum(tot.values())
