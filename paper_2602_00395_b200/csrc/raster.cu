@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
     }
     for (int j = start; j < end; ++j) {
         if (__all_sync(kFull, all_done)) break;
-        const int id = my_ids[e];
+        const int id = __ldg(tl.tile_ids + j);
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
         if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
     }
     const int wlast = __reduce_max_sync(kFull, lmax);
     for (int j = start + wlast - 1; j >= start; --j) {
-        const int id = my_ids[e];
+        const int id = __ldg(tl.tile_ids + j);
         const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
         const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
         if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
