@@ -975,7 +975,7 @@ void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, 
 }
 
 int vjp_mode() { return g_vjp_mode; }
-int chain_mode() { return knob("SGTR_CHAIN_MODE", 1); }
+int chain_mode() { return knob("SGTR_CHAIN_MODE", 0); }
 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
@@ -999,7 +999,7 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * tl.tiles_y;
     if (n == 0) return;
-    if (g_fwd_warp)
+    if (knob("SGTR_JVP_WARP", 0))
         k_raster_jvp_warp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     else if (g_warp_cull)
         k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
