@@ -238,6 +238,10 @@ int sgtr_view_stats(sgtr_ctx* ctx, const sgtr_camera* cam,
                     int64_t* n_dup);
 /* FP64 FMA-pipe throughput of the device (TFLOP/s), measured */
 int sgtr_fp64_peak(int device, double* tflops);
+/* self-check of the rasterizer's exp (fastexp.cuh) against the CUDA math
+ * library: number of bitwise mismatches over n inputs in [lo, hi] */
+int sgtr_check_fast_exp(int64_t n, double lo, double hi, uint64_t seed,
+                        int64_t* mismatches);
 
 /* ------------------------------------------------------------ multi-GPU */
 /* one process per GPU; views of each step are split round-robin over

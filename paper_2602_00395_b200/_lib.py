@@ -124,6 +124,8 @@ _SIGS = {
     "sgtr_blend_stats": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "sgtr_view_stats": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "sgtr_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)]),
+    "sgtr_check_fast_exp": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_uint64,
+                                      C.POINTER(C.c_int64)]),
     "sgtr_nccl_unique_id": (C.c_int, [VP]),
     "sgtr_shard_views": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, VP,
                                    C.POINTER(C.c_int32)]),

@@ -25,7 +25,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xptxas", "-warn-spills"]
 NO_FMA = {"project.cu", "update.cu", "binning.cu"}
 SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu", "probe.cu"]
-HEADERS = ["common.cuh", "geometry.cuh", "launch.h"]
+HEADERS = ["common.cuh", "fastexp.cuh", "geometry.cuh", "launch.h"]
 
 
 def _deps_mtime():

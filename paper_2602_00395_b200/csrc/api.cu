@@ -1730,6 +1730,13 @@ int sgtr_fp64_peak(int device, double* tflops) {
     return guarded([&] { *tflops = fp64_fma_peak_tflops(device); });
 }
 
+int sgtr_check_fast_exp(int64_t n, double lo, double hi, uint64_t seed, int64_t* mismatches) {
+    return guarded([&] {
+        if (n < 0 || !(lo <= hi)) throw invalid("check_fast_exp: bad range");
+        *mismatches = fast_exp_mismatches(n, lo, hi, seed);
+    });
+}
+
 int sgtr_shard_views(int32_t n, int32_t rank, int32_t nranks, int32_t* positions,
                      int32_t* count) {
     return guarded([&] {

@@ -171,6 +171,7 @@ void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
 void launch_scale(cudaStream_t st, double* v, long long n, double s);
 // probe.cu
 double fp64_fma_peak_tflops(int device);
+long long fast_exp_mismatches(long long n, double lo, double hi, unsigned long long seed);
 void launch_fill_int(cudaStream_t st, int* p, long long n, int v);
 
 }  // namespace sgtr

@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "fastexp.cuh"
 
 namespace sgtr {
 namespace {
@@ -27,7 +28,37 @@ __global__ void __launch_bounds__(256) k_fma_probe(double* out, int iters, doubl
     if (s == 1234.5678) out[0] = s;  // keeps the chains live
 }
 
+// fast_exp against the library exp over n inputs spread across
+// [lo, hi] (a splitmix sequence, so every ulp pattern class appears)
+__global__ void k_exp_check(long long n, double lo, double hi, unsigned long long seed,
+                            unsigned long long* mismatches) {
+    unsigned long long bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long z = seed + (unsigned long long)i * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        const double u = (double)(z >> 11) * 0x1.0p-53;
+        const double x = lo + (hi - lo) * u;
+        if (__double_as_longlong(fast_exp(x)) != __double_as_longlong(exp(x))) ++bad;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
 }  // namespace
+
+long long fast_exp_mismatches(long long n, double lo, double hi, unsigned long long seed) {
+    unsigned long long* d = nullptr;
+    SGTR_CUDA(cudaMalloc(&d, sizeof(*d)));
+    SGTR_CUDA(cudaMemset(d, 0, sizeof(*d)));
+    k_exp_check<<<148 * 8, 256>>>(n, lo, hi, seed, d);
+    SGTR_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    SGTR_CUDA(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return (long long)h;
+}
 
 double fp64_fma_peak_tflops(int device) {
     SGTR_CUDA(cudaSetDevice(device));

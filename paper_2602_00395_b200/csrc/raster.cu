@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "fastexp.cuh"
 #include "geometry.cuh"
 #include "launch.h"
 
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
             if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
                 if (kCount) ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads)
                 const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
                                       c01.x, c01.y, cc2.x};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kThreads)
                     t[2 * q + 1] = v.y;
                 }
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ex0 = exp(eval_expo(dx, dy, f));
+                const double ex0 = fast_exp(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], ex0);
                 const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
                 const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
         for (int k = 0; k < PPL; ++k) {
             if (!done[k] && !(pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1])) {
                 const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T[k];
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
             bool contrib = false;
             if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double gauss = exp(eval_expo(dx, dy, f));
+                const double gauss = fast_exp(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
                 const bool clamped = abar >= ro.alpha_clamp;
                 if (clamped) abar = ro.alpha_clamp;
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         bool contrib = false;
         if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
             const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-            const double gauss = exp(eval_expo(dx, dy, f));
+            const double gauss = fast_exp(eval_expo(dx, dy, f));
             double abar = __dmul_rn(f[R_ALPHA], gauss);
             const bool clamped = abar >= ro.alpha_clamp;
             if (clamped) abar = ro.alpha_clamp;
@@ -815,7 +816,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
         for (int k = 0; k < PPL; ++k) {
             if (!col_in || rel >= lastp[k] || pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1]) continue;
             const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-            const double gauss = exp(eval_expo(dx, dy, f));
+            const double gauss = fast_exp(eval_expo(dx, dy, f));
             double abar = __dmul_rn(f[R_ALPHA], gauss);
             const bool clamped = abar >= ro.alpha_clamp;
             if (clamped) abar = ro.alpha_clamp;
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double* t = s_t + kTRec * jj;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double e = exp(eval_expo(dx, dy, f));
+                const double e = fast_exp(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], e);
                 // tangent of the same expression (dual.hpp semantics)
                 const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);

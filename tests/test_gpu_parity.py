@@ -419,3 +419,14 @@ def test_c2_scale_crop_parity(sp, orc):
     assert loss == pytest.approx(losso, rel=1e-9)
     for a, b in zip(_gpu_binning(sp, init.x, crop), orc.binning(init.x, oc)):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("lo,hi", [(-30.0, 0.0), (-760.0, 10.0), (-1e-6, 1e-6)])
+def test_fast_exp_bit_identical(sp, lo, hi):
+    # the rasterizer's exp (csrc/fastexp.cuh) is a constant-bank copy of the
+    # CUDA library exp; every bit must agree over 2^24 inputs per range
+    import ctypes as C
+    from paper_2602_00395_b200 import _lib
+    bad = C.c_int64(-1)
+    _lib.check(_lib.lib().sgtr_check_fast_exp(1 << 24, lo, hi, 12345, C.byref(bad)))
+    assert bad.value == 0
