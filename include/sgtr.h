@@ -68,6 +68,18 @@ typedef struct sgtr_optimizer_options {
     sgtr_render_options render;
 } sgtr_optimizer_options;
 
+/* splat::AdamOptions (optimizer.hpp:21-34) + OptimizerOptions::scene_extent
+ * (:50); used by the ADAM kinds together with sgtr_optimizer_options
+ * (batch_size, the TR schedule/caps for ADAM-TR, bounds, residual, render) */
+typedef struct sgtr_adam_options {
+    double beta1, beta2, eps, lr_position, lr_position_final;
+    int32_t lr_position_decay_steps, pad;
+    double lr_scale, lr_rotation, lr_opacity, lr_color, scene_extent;
+} sgtr_adam_options;
+
+/* splat::OptimizerKind (optimizer.hpp:17) */
+enum { SGTR_KIND_3DGS2TR = 0, SGTR_KIND_ADAM = 1, SGTR_KIND_ADAM_TR = 2 };
+
 /* splat::StepDiagnostics (optimizer.hpp:74-83); applied_step is fetched with
  * sgtr_get_applied_step when record_applied_step was set */
 typedef struct sgtr_step_diagnostics {
@@ -135,6 +147,28 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
                                int32_t n2, const uint32_t* probe_bits,
                                int32_t nu, sgtr_step_diagnostics* diag);
 int sgtr_get_applied_step(sgtr_ctx* ctx, double* out);
+
+/* step_adam / step_adam_tr (optimizer.cpp:222-253): one S1 draw from the
+ * state's Rng, ADAM direction (adam_direction, :153-185), then the plain
+ * update (apply_unclipped) or the trust-region clip (apply_clipped) */
+int sgtr_step_adam(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                   const sgtr_adam_options* adam, sgtr_step_diagnostics* diag);
+int sgtr_step_adam_tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                      const sgtr_adam_options* adam, sgtr_step_diagnostics* diag);
+/* teacher-forced: S1 supplied (trust_region 0: ADAM, 1: ADAM-TR) */
+int sgtr_step_adam_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                            const sgtr_adam_options* adam, int32_t trust_region,
+                            const int32_t* s1, int32_t n1,
+                            sgtr_step_diagnostics* diag);
+/* optimizer_step (optimizer.cpp:255-263): dispatch on SGTR_KIND_* */
+int sgtr_optimizer_step(sgtr_ctx* ctx, int32_t kind,
+                        const sgtr_optimizer_options* opt,
+                        const sgtr_adam_options* adam,
+                        sgtr_step_diagnostics* diag);
+/* OptimizerState::adam_m / adam_v (optimizer.hpp:58-72); zeroed by
+ * sgtr_state_reset */
+int sgtr_state_set_adam(sgtr_ctx* ctx, const double* m, const double* v);
+int sgtr_state_get_adam(sgtr_ctx* ctx, double* m, double* v);
 
 /* ------------------------------------------------------------ seams */
 /* rasterize (render.hpp:73-74) */

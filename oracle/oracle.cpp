@@ -1131,10 +1131,11 @@ double eps_at(double e0, double e1, int total, int t) {  // trust_region.cpp:261
 }  // namespace
 
 struct orc_state {
-    std::vector<double> g_hat, d_hat;
+    std::vector<double> g_hat, d_hat, adam_m, adam_v;
     int64_t t = 0;
     Rng rng;
-    orc_state(int64_t dim, uint64_t seed) : g_hat(dim, 0.0), d_hat(dim, 0.0), rng(seed) {}
+    orc_state(int64_t dim, uint64_t seed)
+        : g_hat(dim, 0.0), d_hat(dim, 0.0), adam_m(dim, 0.0), adam_v(dim, 0.0), rng(seed) {}
 };
 
 struct orc_rng {
@@ -1145,6 +1146,9 @@ struct orc_rng {
 namespace {
 
 double vnorm(const std::vector<double>& v) { return std::sqrt(sq_norm(v)); }
+
+void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
+                   const std::vector<double>& dx, orc_diag& dg, double* applied);
 
 // optimizer.cpp:189-220 with the draws either taken from the state's Rng
 // (reference order: S1, then on refresh S2 and nu probes coordinate-
@@ -1181,7 +1185,28 @@ void step_tr(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
     for (int64_t i = 0; i < dim; ++i)
         dx[i] = -st->g_hat[i] / std::max(st->d_hat[i], o.gamma_d);
     dg.step_pre = vnorm(dx);
-    // apply_clipped, optimizer.cpp:124-142
+    apply_clipped(st, x, pb, o, dx, dg, applied);
+    *diag = dg;
+}
+
+// Scene::clamp, scene.cpp:49-57
+void clamp_scene(double* x, int64_t k, const orc_tr_opts& o) {
+    for (int64_t i = 0; i < k; ++i) {
+        for (int a = 0; a < 3; ++a) {
+            double& s = x[3 * k + 3 * i + a];
+            s = std::max(s, o.s_min);
+            double& c = x[11 * k + 3 * i + a];
+            c = std::min(std::max(c, o.c_min), o.c_max);
+        }
+        double& al = x[10 * k + i];
+        al = std::min(std::max(al, o.alpha_min), o.alpha_max);
+    }
+}
+
+// apply_clipped, optimizer.cpp:124-142
+void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
+                   const std::vector<double>& dx, orc_diag& dg, double* applied) {
+    const int64_t k = pb.sc.k, dim = 14 * k;
     const double eps = eps_at(o.eps_start, o.eps_end, o.total_steps, (int)st->t);
     const double caps[5] = {o.cap_mean, o.cap_scale, o.cap_rotation, o.cap_opacity,
                             o.cap_color};
@@ -1204,17 +1229,67 @@ void step_tr(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
     dg.max_step_over_radius = mr;
     if (applied) std::copy(cl.begin(), cl.end(), applied);
     for (int64_t i = 0; i < dim; ++i) x[i] = x[i] + cl[i];
-    // Scene::clamp, scene.cpp:49-57
-    for (int64_t i = 0; i < k; ++i) {
-        for (int a = 0; a < 3; ++a) {
-            double& s = x[3 * k + 3 * i + a];
-            s = std::max(s, o.s_min);
-            double& c = x[11 * k + 3 * i + a];
-            c = std::min(std::max(c, o.c_min), o.c_max);
-        }
-        double& al = x[10 * k + i];
-        al = std::min(std::max(al, o.alpha_min), o.alpha_max);
+    clamp_scene(x, k, o);
+}
+
+// apply_unclipped, optimizer.cpp:145-151
+void apply_unclipped(double* x, int64_t k, const orc_tr_opts& o, const std::vector<double>& dx,
+                     orc_diag& dg, double* applied) {
+    const int64_t dim = 14 * k;
+    for (int64_t i = 0; i < dim; ++i)
+        if (!std::isfinite(dx[i]))
+            throw NumericErr(std::string("non-finite update in group ") + kGroup[group_of(k, i)]);
+    dg.step_post = vnorm(dx);
+    if (applied) std::copy(dx.begin(), dx.end(), applied);
+    for (int64_t i = 0; i < dim; ++i) x[i] = x[i] + dx[i];
+    clamp_scene(x, k, o);
+}
+
+// adam_direction, optimizer.cpp:153-185: bias-corrected moments, per-group
+// rates, the position rate scaled by the scene extent and decayed
+// geometrically over lr_position_decay_steps
+std::vector<double> adam_direction(orc_state* st, int64_t k, const std::vector<double>& g,
+                                   const orc_adam_opts& a) {
+    const int64_t dim = 14 * k;
+    for (int64_t i = 0; i < dim; ++i) {
+        st->adam_m[i] = a.beta1 * st->adam_m[i] + (1.0 - a.beta1) * g[i];
+        st->adam_v[i] = a.beta2 * st->adam_v[i] + (1.0 - a.beta2) * (g[i] * g[i]);
     }
+    const double c1 = 1.0 - std::pow(a.beta1, static_cast<double>(st->t));
+    const double c2 = 1.0 - std::pow(a.beta2, static_cast<double>(st->t));
+    const double span = std::max(1, a.lr_position_decay_steps);
+    const double frac = std::min(1.0, static_cast<double>(st->t) / span);
+    const double lr_pos =
+        a.scene_extent * a.lr_position * std::pow(a.lr_position_final / a.lr_position, frac);
+    const double lrs[5] = {lr_pos, a.lr_scale, a.lr_rotation, a.lr_opacity, a.lr_color};
+    std::vector<double> dx(dim);
+    for (int64_t i = 0; i < dim; ++i) {
+        const double lr = lrs[group_of(k, i)];
+        const double mhat = st->adam_m[i] / c1;
+        const double vhat = st->adam_v[i] / c2;
+        dx[i] = -lr * mhat / (std::sqrt(vhat) + a.eps);
+    }
+    return dx;
+}
+
+// step_adam / step_adam_tr, optimizer.cpp:222-253: one S1 draw, gradient,
+// ADAM direction, then the plain or the trust-region-clipped update
+void step_adam(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
+               const orc_adam_opts& a, bool trust_region, const std::vector<int>* s1_in,
+               orc_diag* diag, double* applied) {
+    const int64_t k = pb.sc.k;
+    orc_diag dg{0, 0, 0, 0, -1, -1, 0};
+    st->t += 1;
+    const int mv = static_cast<int>(pb.cams.size());
+    const std::vector<int> s1 = s1_in ? *s1_in : st->rng.sample(mv, o.batch_size);
+    const std::vector<double> g = stochastic_gradient(pb, s1, &dg.batch_loss);
+    dg.gnorm = vnorm(g);
+    const std::vector<double> dx = adam_direction(st, k, g, a);
+    dg.step_pre = vnorm(dx);
+    if (trust_region)
+        apply_clipped(st, x, pb, o, dx, dg, applied);
+    else
+        apply_unclipped(x, k, o, dx, dg, applied);
     *diag = dg;
 }
 
@@ -1729,6 +1804,34 @@ int orc_step_3dgs2tr_explicit(orc_state* s, double* x, int64_t k, const orc_came
         const Problem pb = make_problem(x, k, cams, gts, n_views, rs, ro, workers);
         const std::vector<int> v1(s1, s1 + n1), v2(s2, s2 + n2);
         step_tr(s, x, pb, *o, &v1, &v2, probes, diag, applied_step);
+    });
+}
+
+int orc_state_get_adam(const orc_state* s, double* m, double* v) {
+    if (m) std::copy(s->adam_m.begin(), s->adam_m.end(), m);
+    if (v) std::copy(s->adam_v.begin(), s->adam_v.end(), v);
+    return 0;
+}
+
+int orc_state_set_adam(orc_state* s, const double* m, const double* v) {
+    if (m) std::copy(m, m + s->adam_m.size(), s->adam_m.begin());
+    if (v) std::copy(v, v + s->adam_v.size(), s->adam_v.begin());
+    return 0;
+}
+
+int orc_step_adam(orc_state* s, double* x, int64_t k, const orc_camera* cams,
+                  const double* const* gts, int32_t n_views, const orc_tr_opts* o,
+                  const orc_adam_opts* a, int32_t trust_region, const orc_residual_opts* rs,
+                  const orc_render_opts* ro, int workers, const int32_t* s1, int32_t n1,
+                  orc_diag* diag, double* applied_step) {
+    return guarded([&] {
+        const Problem pb = make_problem(x, k, cams, gts, n_views, rs, ro, workers);
+        if (s1) {
+            const std::vector<int> v1(s1, s1 + n1);
+            step_adam(s, x, pb, *o, *a, trust_region != 0, &v1, diag, applied_step);
+        } else {
+            step_adam(s, x, pb, *o, *a, trust_region != 0, nullptr, diag, applied_step);
+        }
     });
 }
 

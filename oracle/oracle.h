@@ -59,6 +59,13 @@ typedef struct orc_tr_opts {
     double s_min, alpha_min, alpha_max, c_min, c_max;
 } orc_tr_opts;
 
+/* AdamOptions (optimizer.hpp:21-34) + OptimizerOptions::scene_extent */
+typedef struct orc_adam_opts {
+    double beta1, beta2, eps, lr_position, lr_position_final;
+    int32_t lr_position_decay_steps, pad;
+    double lr_scale, lr_rotation, lr_opacity, lr_color, scene_extent;
+} orc_adam_opts;
+
 typedef struct orc_diag {
     double batch_loss, gnorm, step_pre, step_post, clip_frac, eps,
         max_step_over_radius;
@@ -180,6 +187,18 @@ int orc_step_3dgs2tr_explicit(orc_state* s, double* x, int64_t k,
                               const int32_t* s1, int32_t n1, const int32_t* s2,
                               int32_t n2, const double* probes, orc_diag* diag,
                               double* applied_step);
+
+/* --- ADAM / ADAM-TR (optimizer.cpp:153-185, 222-253) --- */
+int orc_state_get_adam(const orc_state* s, double* m, double* v);
+int orc_state_set_adam(orc_state* s, const double* m, const double* v);
+/* trust_region = 0: step_adam (apply_unclipped), 1: step_adam_tr
+ * (apply_clipped); s1 = NULL draws S1 from the state's Rng */
+int orc_step_adam(orc_state* s, double* x, int64_t k, const orc_camera* cams,
+                  const double* const* gts, int32_t n_views, const orc_tr_opts* o,
+                  const orc_adam_opts* a, int32_t trust_region,
+                  const orc_residual_opts* rs, const orc_render_opts* ro,
+                  int workers, const int32_t* s1, int32_t n1, orc_diag* diag,
+                  double* applied_step);
 
 /* --- reference Rng (rng.hpp:15-72) --- */
 typedef struct orc_rng orc_rng;

@@ -64,6 +64,15 @@ class TrOpts(C.Structure):
                 ("c_max", C.c_double)]
 
 
+class AdamOpts(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("lr_position", C.c_double), ("lr_position_final", C.c_double),
+                ("lr_position_decay_steps", C.c_int32), ("pad", C.c_int32),
+                ("lr_scale", C.c_double), ("lr_rotation", C.c_double),
+                ("lr_opacity", C.c_double), ("lr_color", C.c_double),
+                ("scene_extent", C.c_double)]
+
+
 class Diag(C.Structure):
     _fields_ = [("batch_loss", C.c_double), ("gnorm", C.c_double),
                 ("step_pre", C.c_double), ("step_post", C.c_double),
@@ -172,6 +181,26 @@ class TrOptions:  # optimizer.hpp:37-53 (3dgs2tr subset) + trust_region.hpp
         return TrOpts(self.theta1, self.theta2, self.hess_interval, self.hutch_samples,
                       self.batch_size, self.hutch_batch_size, self.gamma_d, self.eps_start,
                       self.eps_end, self.total_steps, 0, *self.caps, *self.bounds)
+
+
+@dataclass
+class AdamOptions:  # optimizer.hpp:21-34 (+ OptimizerOptions::scene_extent)
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    lr_position: float = 1.6e-4
+    lr_position_final: float = 1.6e-6
+    lr_position_decay_steps: int = 30000
+    lr_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_opacity: float = 5e-2
+    lr_color: float = 2.5e-3
+    scene_extent: float = 1.0
+
+    def c(self):
+        return AdamOpts(self.beta1, self.beta2, self.eps, self.lr_position,
+                        self.lr_position_final, self.lr_position_decay_steps, 0, self.lr_scale,
+                        self.lr_rotation, self.lr_opacity, self.lr_color, self.scene_extent)
 
 
 def camera(id=0, width=16, height=16, fx=1.0, fy=1.0, cx=0.0, cy=0.0,
@@ -439,6 +468,15 @@ class State:
         g, d = _f64(g_hat), _f64(d_hat)
         lib().orc_state_set(self._h, _p(g), _p(d), C.c_int64(t))
 
+    def get_adam(self):
+        m, v = np.empty(self.dim), np.empty(self.dim)
+        lib().orc_state_get_adam(self._h, _p(m), _p(v))
+        return m, v
+
+    def set_adam(self, m, v):
+        m, v = _f64(m), _f64(v)
+        lib().orc_state_set_adam(self._h, _p(m), _p(v))
+
 
 def step_3dgs2tr(state, x, cams, gts, opts, rs=None, ro=None, *, s1=None, s2=None,
                  probes=None, want_applied=False):
@@ -579,3 +617,23 @@ def unpack(x):
     k = x.size // 14
     return (x[:3 * k].reshape(k, 3), x[3 * k:6 * k].reshape(k, 3),
             x[6 * k:10 * k].reshape(k, 4), x[10 * k:11 * k], x[11 * k:].reshape(k, 3))
+
+
+def step_adam(state, x, cams, gts, opts, adam, trust_region=False, rs=None, ro=None, *,
+              s1=None, want_applied=False):
+    """step_adam / step_adam_tr (optimizer.cpp:222-253); x updated in place."""
+    rs, ro = rs or ResidualOptions(), ro or RenderOptions()
+    assert x.dtype == np.float64 and x.flags.c_contiguous
+    keep, ptrs = _gts(gts)
+    diag = Diag()
+    applied = np.empty(x.size) if want_applied else None
+    a1 = np.ascontiguousarray(s1 if s1 is not None else [], dtype=np.int32)
+    _check(lib().orc_step_adam(
+        state._h, _p(x), C.c_int64(x.size // 14), _cams(cams), ptrs, len(cams),
+        C.byref(opts.c()), C.byref(adam.c()), int(bool(trust_region)), C.byref(rs.c()),
+        C.byref(ro.c()), ro.workers, _p(a1) if s1 is not None else None, a1.size,
+        C.byref(diag), _p(applied) if want_applied else None))
+    out = {f: getattr(diag, f) for f, _ in Diag._fields_}
+    if want_applied:
+        out["applied_step"] = applied
+    return out

@@ -58,6 +58,15 @@ class OptimizerOpts(C.Structure):
                 ("residual", ResidualOpts), ("render", RenderOpts)]
 
 
+class AdamOpts(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("lr_position", C.c_double), ("lr_position_final", C.c_double),
+                ("lr_position_decay_steps", C.c_int32), ("pad", C.c_int32),
+                ("lr_scale", C.c_double), ("lr_rotation", C.c_double),
+                ("lr_opacity", C.c_double), ("lr_color", C.c_double),
+                ("scene_extent", C.c_double)]
+
+
 class StepDiag(C.Structure):
     _fields_ = [("batch_loss", C.c_double), ("gnorm", C.c_double), ("step_pre", C.c_double),
                 ("step_post", C.c_double), ("clip_frac", C.c_double), ("eps", C.c_double),
@@ -99,6 +108,12 @@ _SIGS = {
     "sgtr_step_3dgs2tr_explicit": (C.c_int, [VP, VP, VP, C.c_int32, VP, C.c_int32, VP,
                                              C.c_int32, VP]),
     "sgtr_get_applied_step": (C.c_int, [VP, VP]),
+    "sgtr_step_adam": (C.c_int, [VP, VP, VP, VP]),
+    "sgtr_step_adam_tr": (C.c_int, [VP, VP, VP, VP]),
+    "sgtr_step_adam_explicit": (C.c_int, [VP, VP, VP, C.c_int32, VP, C.c_int32, VP]),
+    "sgtr_optimizer_step": (C.c_int, [VP, C.c_int32, VP, VP, VP]),
+    "sgtr_state_set_adam": (C.c_int, [VP, VP, VP]),
+    "sgtr_state_get_adam": (C.c_int, [VP, VP, VP]),
     "sgtr_rasterize": (C.c_int, [VP, VP, VP, VP, VP]),
     "sgtr_rasterize_jvp": (C.c_int, [VP, VP, VP, VP, VP]),
     "sgtr_rasterize_vjp": (C.c_int, [VP, VP, VP, VP, VP]),

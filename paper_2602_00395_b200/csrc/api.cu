@@ -327,7 +327,7 @@ struct Ctx {
     long long launches = 0;
     KTimer timer;
     int K = 0;
-    Buf x, x_alt, ghat, dhat, fused, applied, vecbuf;
+    Buf x, x_alt, ghat, dhat, adam_m, adam_v, fused, applied, vecbuf;
     bool have_applied = false;
     std::vector<View> views;
     Buf gt;  // planar targets, one (3, H, W) block per view
@@ -617,9 +617,12 @@ void allreduce(Ctx& c, double* buf, size_t n) {
 // One step with its draws given.  `rng_ckpt` (if any) is the state to restore
 // when the step fails inside the gradient phase, where the reference throws
 // before drawing S2 and the probes.
+// `kind` selects the update (TrArgs::kind): 0 the 3DGS2-TR Newton step,
+// 1 ADAM, 2 ADAM-TR; the ADAM kinds never refresh.
 void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& s1,
                const std::vector<int>& s2, const std::vector<uint32_t>& zbits, int nu,
-               bool refresh, const Rng* rng_ckpt, sgtr_step_diagnostics* diag) {
+               bool refresh, const Rng* rng_ckpt, sgtr_step_diagnostics* diag, int kind = 0,
+               const sgtr_adam_options* adam = nullptr) {
     const int M = (int)c.views.size();
     const int W = c.views[0].dc.W, H = c.views[0].dc.H, P = W * H;
     const long long dim = c.dim();
@@ -734,10 +737,34 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         hutch_fail = hutch_err != 0 || ht[2 * n1] != 0.0;
     }
     // K14
-    if (!(o.eps_start >= o.eps_end) || !(o.eps_end > 0.0)) throw invalid("eps_at: bad schedule");
-    double eps;
-    sgtr_eps_at(o.eps_start, o.eps_end, o.total_steps, (int)c.t, &eps);
+    double eps = -1.0;
+    if (kind != 1) {
+        if (!(o.eps_start >= o.eps_end) || !(o.eps_end > 0.0))
+            throw invalid("eps_at: bad schedule");
+        sgtr_eps_at(o.eps_start, o.eps_end, o.total_steps, (int)c.t, &eps);
+    }
     TrArgs a{};
+    a.kind = kind;
+    if (kind != 0) {
+        // adam_direction's scalars (optimizer.cpp:159-169), host std::pow as
+        // in the reference
+        const long long n = std::max<long long>(dim, 1);
+        a.adam_m = c.adam_m.as<double>(n);
+        a.adam_v = c.adam_v.as<double>(n);
+        a.beta1 = adam->beta1;
+        a.beta2 = adam->beta2;
+        a.adam_eps = adam->eps;
+        a.bc1 = 1.0 - std::pow(adam->beta1, static_cast<double>(c.t));
+        a.bc2 = 1.0 - std::pow(adam->beta2, static_cast<double>(c.t));
+        const double span = std::max(1, adam->lr_position_decay_steps);
+        const double frac = std::min(1.0, static_cast<double>(c.t) / span);
+        a.lr[0] = adam->scene_extent * adam->lr_position *
+                  std::pow(adam->lr_position_final / adam->lr_position, frac);
+        a.lr[1] = adam->lr_scale;
+        a.lr[2] = adam->lr_rotation;
+        a.lr[3] = adam->lr_opacity;
+        a.lr[4] = adam->lr_color;
+    }
     a.K = c.K;
     a.x = c.X();
     a.x_out = c.x_alt.as<double>(std::max<long long>(dim, 1));
@@ -805,12 +832,22 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     if (c.hstat->bad_index != INT_MAX)
         throw numeric(std::string("non-finite update in group ") +
                       kGroupNames[group_of(c.K, c.hstat->bad_index)]);
-    diag->eps = eps;
-    diag->clip_frac = dim ? c.hstat->tr[3] / static_cast<double>(dim) : 0.0;
     diag->step_post = std::sqrt(c.hstat->tr[2]);
-    diag->max_step_over_radius = c.hstat->tr[4];
+    if (kind != 1) {  // apply_clipped fills the trust-region fields
+        diag->eps = eps;
+        diag->clip_frac = dim ? c.hstat->tr[3] / static_cast<double>(dim) : 0.0;
+        diag->max_step_over_radius = c.hstat->tr[4];
+    }
     std::swap(c.x.p, c.x_alt.p);
     std::swap(c.x.bytes, c.x_alt.bytes);
+}
+
+// OptimizerState(dim, seed)'s vectors (optimizer.hpp:58-72): g_hat, d_hat,
+// adam_m, adam_v all zero
+void zero_state(Ctx& c) {
+    const long long n = std::max<long long>(c.dim(), 1);
+    for (Buf* b : {&c.ghat, &c.dhat, &c.adam_m, &c.adam_v})
+        SGTR_CUDA(cudaMemsetAsync(b->as<double>(n), 0, sizeof(double) * n, c.st));
 }
 
 void validate_opts(const sgtr_optimizer_options& o) {
@@ -911,10 +948,7 @@ int sgtr_set_scene(sgtr_ctx* ctx, const double* x, int64_t n_splats) {
             SGTR_CUDA(cudaMemcpyAsync(d, x, sizeof(double) * dim, cudaMemcpyHostToDevice, c.st));
         if (resized) {
             // OptimizerState(dim, seed) lives with the scene dimension
-            c.ghat.as<double>(std::max<long long>(dim, 1));
-            c.dhat.as<double>(std::max<long long>(dim, 1));
-            SGTR_CUDA(cudaMemsetAsync(c.ghat.p, 0, sizeof(double) * std::max<long long>(dim, 1), c.st));
-            SGTR_CUDA(cudaMemsetAsync(c.dhat.p, 0, sizeof(double) * std::max<long long>(dim, 1), c.st));
+            zero_state(c);
         }
         SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
@@ -999,9 +1033,7 @@ int sgtr_state_reset(sgtr_ctx* ctx, uint64_t seed) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
         bind(c);
-        const long long n = std::max<long long>(c.dim(), 1);
-        SGTR_CUDA(cudaMemsetAsync(c.ghat.as<double>(n), 0, sizeof(double) * n, c.st));
-        SGTR_CUDA(cudaMemsetAsync(c.dhat.as<double>(n), 0, sizeof(double) * n, c.st));
+        zero_state(c);
         c.prefetch.reset();
         c.t = 0;
         c.rng = Rng(seed);
@@ -1128,6 +1160,97 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
             bits.assign(probe_bits, probe_bits + words * nu);
         }
         step_core(c, *opt, v1, v2, bits, nu, refresh, nullptr, diag);
+    });
+}
+
+namespace {
+// step_adam / step_adam_tr (optimizer.cpp:222-253): t += 1, one S1 draw
+// (the ADAM kinds consume nothing else, optimizer.hpp:55-57), gradient,
+// ADAM direction, plain or clipped update
+void adam_step(sgtr_ctx* ctx, const sgtr_optimizer_options* opt, const sgtr_adam_options* adam,
+               int kind, const int32_t* s1, int32_t n1, sgtr_step_diagnostics* diag) {
+    Ctx& c = ctx_ref(ctx);
+    bind(c);
+    need_scene(c);
+    check_views(c, true);
+    if (!opt || !adam) throw invalid("step_adam: null options");
+    *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
+    c.prefetch.reset();
+    const int M = (int)c.views.size();
+    std::vector<int> v1;
+    if (s1) {
+        if (n1 < 1) throw invalid("stochastic_gradient: empty batch");
+        v1.assign(s1, s1 + n1);
+        for (int v : v1)
+            if (v < 0 || v >= M) throw invalid("stochastic_gradient: view index out of range");
+        c.t += 1;
+    } else {
+        if (opt->batch_size < 1) throw invalid("stochastic_gradient: empty batch");
+        c.t += 1;
+        v1 = c.rng.sample(M, opt->batch_size);
+    }
+    step_core(c, *opt, v1, {}, {}, 1, false, nullptr, diag, kind, adam);
+}
+}  // namespace
+
+int sgtr_step_adam(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                   const sgtr_adam_options* adam, sgtr_step_diagnostics* diag) {
+    return guarded([&] { adam_step(ctx, opt, adam, 1, nullptr, 0, diag); });
+}
+
+int sgtr_step_adam_tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                      const sgtr_adam_options* adam, sgtr_step_diagnostics* diag) {
+    return guarded([&] { adam_step(ctx, opt, adam, 2, nullptr, 0, diag); });
+}
+
+int sgtr_step_adam_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
+                            const sgtr_adam_options* adam, int32_t trust_region,
+                            const int32_t* s1, int32_t n1, sgtr_step_diagnostics* diag) {
+    return guarded([&] {
+        if (!s1) throw invalid("step_adam: null S1");
+        adam_step(ctx, opt, adam, trust_region ? 2 : 1, s1, n1, diag);
+    });
+}
+
+int sgtr_optimizer_step(sgtr_ctx* ctx, int32_t kind, const sgtr_optimizer_options* opt,
+                        const sgtr_adam_options* adam, sgtr_step_diagnostics* diag) {
+    switch (kind) {
+        case SGTR_KIND_3DGS2TR: return sgtr_step_3dgs2tr(ctx, opt, diag);
+        case SGTR_KIND_ADAM: return sgtr_step_adam(ctx, opt, adam, diag);
+        case SGTR_KIND_ADAM_TR: return sgtr_step_adam_tr(ctx, opt, adam, diag);
+        default:
+            g_last_error = "optimizer_step: unknown optimizer kind";
+            return SGTR_INVALID_ARGUMENT;
+    }
+}
+
+int sgtr_state_set_adam(sgtr_ctx* ctx, const double* m, const double* v) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const long long n = c.dim();
+        if (m && n)
+            SGTR_CUDA(cudaMemcpyAsync(c.adam_m.as<double>(n), m, sizeof(double) * n,
+                                      cudaMemcpyHostToDevice, c.st));
+        if (v && n)
+            SGTR_CUDA(cudaMemcpyAsync(c.adam_v.as<double>(n), v, sizeof(double) * n,
+                                      cudaMemcpyHostToDevice, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_state_get_adam(sgtr_ctx* ctx, double* m, double* v) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const long long n = c.dim();
+        if (m && n)
+            SGTR_CUDA(cudaMemcpyAsync(m, c.adam_m.as<double>(n), sizeof(double) * n,
+                                      cudaMemcpyDeviceToHost, c.st));
+        if (v && n)
+            SGTR_CUDA(cudaMemcpyAsync(v, c.adam_v.as<double>(n), sizeof(double) * n,
+                                      cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
 }
 

@@ -158,6 +158,14 @@ struct TrArgs {
     double* eta_buf;      // trust-region radii (dim)
     int* queue;           // (splat, rotation axis) pairs needing bisection (4K)
     int* queue_count;
+    // direction: 0 = 3DGS2-TR Newton step, 1 = ADAM (unclipped update),
+    // 2 = ADAM-TR (ADAM direction, trust-region clip) (optimizer.cpp:153-253)
+    int kind;
+    double* adam_m;
+    double* adam_v;
+    double beta1, beta2, adam_eps;
+    double bc1, bc2;      // 1 - beta^t bias corrections (host std::pow)
+    double lr[5];         // per-group rates, lr[0] already decayed and scaled
 };
 int tr_num_blocks(int K);
 // phase 0: K14a (EMAs, direction, radii), 1: K14b (queued bisections),

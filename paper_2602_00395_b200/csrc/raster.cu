@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
 // stores them in its own partial slot (tile-sorted position j, warp w),
 // flagging mask[j * 8 + w]; K11 sums the flagged partials of each duplicate in
 // warp order (deterministic, no atomics).
-template <int kMinBlocks, bool kSmemRed>
+template <int kMinBlocks, bool kSmemRed, bool kPrefetch>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     k_raster_vjp_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       const double* __restrict__ adj, const double* __restrict__ tfinal,
@@ -688,15 +688,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         nl += __popc(m);
     }
     __syncwarp();
+    // kPrefetch: the next entry's record is loaded while the current one is
+    // processed (its loads are independent of the T recurrence)
+    double2 nr[7];
+    int nj = 0;
+    if (kPrefetch && nl > 0) {
+        nj = my_list[nl - 1];
+        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[nl - 1]);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) nr[k] = __ldg(r2 + k);
+    }
     for (int e = nl - 1; e >= 0; --e) {
-        const int j = my_list[e];
-        const int id = my_ids[e];
-        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
-        const double2 c01 = __ldg(r2 + 5), c2 = __ldg(r2 + 6);
-        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
-                              c01.x, c01.y, c2.x};
+        int j;
+        double2 cr[7];
+        if (kPrefetch) {
+            j = nj;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) cr[k] = nr[k];
+            if (e > 0) {
+                nj = my_list[e - 1];
+                const double2* r2 =
+                    reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[e - 1]);
+#pragma unroll
+                for (int k = 0; k < 7; ++k) nr[k] = __ldg(r2 + k);
+            }
+        } else {
+            j = my_list[e];
+            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[e]);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) cr[k] = __ldg(r2 + k);
+        }
+        const double f[13] = {cr[0].x, cr[0].y, cr[1].x, cr[1].y, cr[2].x, cr[2].y, cr[3].x,
+                              cr[3].y, cr[4].x, cr[4].y, cr[5].x, cr[5].y, cr[6].x};
         const int rel = j - start;
         double g[kAdj];
 #pragma unroll
@@ -933,6 +956,7 @@ const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
 const int g_fwd_warp = knob("SGTR_FWD_WARP", 1);
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
+const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
 
 }  // namespace
 
@@ -987,12 +1011,18 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
         k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
     else if (g_vjp_ppl == 2)
         k_raster_vjp_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
+    else if (g_vjp_prefetch == 2)
+        k_raster_vjp_warp<2, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
+                                                                 last, part, mask);
+    else if (g_vjp_prefetch == 3)
+        k_raster_vjp_warp<3, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
+                                                                 last, part, mask);
     else if (g_smem_red)
-        k_raster_vjp_warp<3, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                           part, mask);
+        k_raster_vjp_warp<3, true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
+                                                                  last, part, mask);
     else
-        k_raster_vjp_warp<3, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                            part, mask);
+        k_raster_vjp_warp<3, false, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
+                                                                   last, part, mask);
     SGTR_CUDA(cudaGetLastError());
 }
 

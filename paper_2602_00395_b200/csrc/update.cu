@@ -317,8 +317,28 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
         const Prim p = load_prim(a.x, K, i);
         const bool degenerate =
             p.q[0] * p.q[0] + p.q[1] * p.q[1] + p.q[2] * p.q[2] + p.q[3] * p.q[3] < 1e-24;
-        if (!a.ghat_only && degenerate) atomicOr(a.degenerate_flag, 1);
-        for (int j = 0; j < 14; ++j) {
+        // shd_radii (and its degenerate-quaternion throw) runs for the
+        // trust-region kinds only
+        if (!a.ghat_only && a.kind != 1 && degenerate) atomicOr(a.degenerate_flag, 1);
+        if (a.kind != 0) {
+            // adam_direction (optimizer.cpp:153-185)
+            for (int j = 0; j < 14; ++j) {
+                const long long k = flat_index(K, i, j);
+                const double g = a.g_acc[k] * a.gscale;
+                v[0] += g * g;
+                const double m = a.beta1 * a.adam_m[k] + (1.0 - a.beta1) * g;
+                const double vv = a.beta2 * a.adam_v[k] + (1.0 - a.beta2) * (g * g);
+                a.adam_m[k] = m;
+                a.adam_v[k] = vv;
+                const int grp = j < 3 ? 0 : j < 6 ? 1 : j < 10 ? 2 : j == 10 ? 3 : 4;
+                const double mhat = m / a.bc1;
+                const double vhat = vv / a.bc2;
+                const double dx = -a.lr[grp] * mhat / (sqrt(vhat) + a.adam_eps);
+                v[1] += dx * dx;
+                a.dx_buf[k] = dx;
+            }
+        }
+        for (int j = 0; j < 14 && a.kind == 0; ++j) {
             const long long k = flat_index(K, i, j);
             const double g = a.g_acc[k] * a.gscale;
             v[0] += g * g;
@@ -336,7 +356,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
             v[1] += dx * dx;
             a.dx_buf[k] = dx;
         }
-        if (!a.ghat_only && !degenerate) {
+        if (!a.ghat_only && a.kind != 1 && !degenerate) {
             double eta[14];
             radius_mean(p, a.eps, a.caps[0], eta);
             for (int c = 0; c < 3; ++c) {
@@ -405,14 +425,18 @@ __global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
         double xo[14];
         for (int j = 0; j < 14; ++j) {
             const long long k = flat_index(K, i, j);
-            const double dx = a.dx_buf[k], eta = a.eta_buf[k];
-            // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
-            double c = dx < -eta ? -eta : dx;
-            c = eta < c ? eta : c;
+            const double dx = a.dx_buf[k];
+            double c = dx;
+            if (a.kind != 1) {
+                // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
+                const double eta = a.eta_buf[k];
+                c = dx < -eta ? -eta : dx;
+                c = eta < c ? eta : c;
+                if (fabs(dx) > eta) v[3] += 1.0;
+                const double ratio = fabs(c) / eta;
+                v[4] = v[4] < ratio ? ratio : v[4];
+            }
             if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
-            if (fabs(dx) > eta) v[3] += 1.0;
-            const double ratio = fabs(c) / eta;
-            v[4] = v[4] < ratio ? ratio : v[4];
             v[2] += c * c;
             if (a.applied) a.applied[k] = c;
             xo[j] = a.x[k] + c;
@@ -486,13 +510,13 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
         SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
         k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
-        if (!a.ghat_only) {
+        if (!a.ghat_only && a.kind != 1) {
             k_tr_rot<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
             SGTR_CUDA(cudaGetLastError());
         }
         if (a.ghat_only)
             SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
-    } else if (phase == 1 && !a.ghat_only) {
+    } else if (phase == 1 && !a.ghat_only && a.kind != 1) {
         k_tr_bisect<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
     } else if (phase == 2 && !a.ghat_only) {

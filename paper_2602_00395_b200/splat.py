@@ -35,6 +35,7 @@ __all__ = [
     "mean_ssim", "residual_vector", "residual_jvp", "residual_vjp", "view_jacobian_apply",
     "view_jacobian_applyT", "stochastic_gradient", "rademacher_probes", "hutchinson_diag",
     "ema", "newton_step", "shd_radii", "clip_step", "eps_at", "step_3dgs2tr",
+    "step_adam", "step_adam_tr", "AdamOptions", "optimizer_kind_from_string",
     "optimizer_step", "psnr", "quantize8", "make_synthetic", "look_at_camera",
 ]
 
@@ -103,7 +104,38 @@ class ParamBounds:  # scene.hpp:29-35
 
 
 @dataclass
-class OptimizerOptions:  # optimizer.hpp:37-53 (3DGS²-TR kind)
+class AdamOptions:  # optimizer.hpp:21-34
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+    lr_position: float = 1.6e-4
+    lr_position_final: float = 1.6e-6
+    lr_position_decay_steps: int = 30000
+    lr_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_opacity: float = 5e-2
+    lr_color: float = 2.5e-3
+
+    def _c(self, scene_extent: float) -> _lib.AdamOpts:
+        return _lib.AdamOpts(self.beta1, self.beta2, self.eps, self.lr_position,
+                             self.lr_position_final, self.lr_position_decay_steps, 0,
+                             self.lr_scale, self.lr_rotation, self.lr_opacity, self.lr_color,
+                             scene_extent)
+
+
+# OptimizerKind (optimizer.hpp:17) and optimizer_kind_from_string's spellings
+_KINDS = {"3dgs2tr": 0, "adam": 1, "adam-tr": 2}
+
+
+def optimizer_kind_from_string(s: str) -> str:
+    """optimizer.cpp optimizer_kind_from_string: the accepted spellings."""
+    if s not in _KINDS:
+        raise InvalidArgument(f"unknown optimizer '{s}'")
+    return s
+
+
+@dataclass
+class OptimizerOptions:  # optimizer.hpp:37-53
     kind: str = "3dgs2tr"
     theta1: float = 0.9
     theta2: float = 0.999
@@ -117,11 +149,14 @@ class OptimizerOptions:  # optimizer.hpp:37-53 (3DGS²-TR kind)
     bounds: ParamBounds = field(default_factory=ParamBounds)
     residual: ResidualOptions = field(default_factory=ResidualOptions)
     render: RenderOptions = field(default_factory=RenderOptions)
+    adam: AdamOptions = field(default_factory=AdamOptions)
+    scene_extent: float = 1.0
     record_applied_step: bool = True
 
+    def _kind(self) -> int:
+        return _KINDS[optimizer_kind_from_string(self.kind)]
+
     def _c(self) -> _lib.OptimizerOpts:
-        if self.kind != "3dgs2tr":
-            raise InvalidArgument(f"optimizer kind '{self.kind}' is not on the B200 path")
         s, c, b = self.schedule, self.caps, self.bounds
         return _lib.OptimizerOpts(
             self.theta1, self.theta2, self.hess_interval, self.hutch_samples, self.batch_size,
@@ -347,6 +382,16 @@ class Context:
         d = None if d_hat is None else _f64(d_hat)
         check(lib().sgtr_state_set(self._h, _ptr(g), _ptr(d), t))
 
+    def state_get_adam(self):
+        m, v = np.empty(14 * self.k), np.empty(14 * self.k)
+        check(lib().sgtr_state_get_adam(self._h, _ptr(m), _ptr(v)))
+        return m, v
+
+    def state_set_adam(self, m, v) -> None:
+        m = None if m is None else _f64(m)
+        v = None if v is None else _f64(v)
+        check(lib().sgtr_state_set_adam(self._h, _ptr(m), _ptr(v)))
+
     def step(self, opt: OptimizerOptions, *, s1=None, s2=None, probe_bits=None,
              nu: int = 1) -> StepDiagnostics:
         """One Algorithm-1 step on the resident scene (optimizer.cpp:189-220).
@@ -355,7 +400,18 @@ class Context:
         nu * ceil(dim/32) words); otherwise they come from the state's Rng."""
         d = _lib.StepDiag()
         co = opt._c()
-        if s1 is None:
+        kind = opt._kind()
+        if kind != 0:  # step_adam / step_adam_tr (optimizer.cpp:222-253)
+            ao = opt.adam._c(opt.scene_extent)
+            if s1 is None:
+                check(lib().sgtr_optimizer_step(self._h, kind, C.byref(co), C.byref(ao),
+                                                C.byref(d)))
+            else:
+                a1 = np.ascontiguousarray(s1, np.int32)
+                check(lib().sgtr_step_adam_explicit(self._h, C.byref(co), C.byref(ao),
+                                                    1 if kind == 2 else 0, _ptr(a1), a1.size,
+                                                    C.byref(d)))
+        elif s1 is None:
             check(lib().sgtr_step_3dgs2tr(self._h, C.byref(co), C.byref(d)))
         else:
             a1 = np.ascontiguousarray(s1, np.int32)
@@ -758,15 +814,27 @@ class OptimizerState:
     def t(self) -> int:
         return self.ctx.state_get()[2]
 
+    @property
+    def adam_m(self) -> np.ndarray:
+        return self.ctx.state_get_adam()[0]
+
+    @property
+    def adam_v(self) -> np.ndarray:
+        return self.ctx.state_get_adam()[1]
+
 
 def step_3dgs2tr(state: OptimizerState, scene: Scene, views: Sequence[Camera],
                  opt: OptimizerOptions) -> StepDiagnostics:
     """optimizer.hpp:129-131.  ``scene`` is updated in place (host copy in and
     out, like the reference's Scene&); state stays on the device."""
+    return _step_host(state, scene, views, _with_kind(opt, "3dgs2tr"), "step_3dgs2tr")
+
+
+def _step_host(state: OptimizerState, scene: Scene, views: Sequence[Camera],
+               opt: OptimizerOptions, what: str) -> StepDiagnostics:
     if scene.dim() != state.dim:
-        raise InvalidArgument("step_3dgs2tr: scene/state dimension mismatch")
+        raise InvalidArgument(f"{what}: scene/state dimension mismatch")
     c = state.ctx
-    g, d, t = (None, None, None)
     check(lib().sgtr_set_scene(c.handle, _ptr(scene.x), scene.size()))
     _views_ctx(c, views)
     diag = c.step(opt)
@@ -774,12 +842,27 @@ def step_3dgs2tr(state: OptimizerState, scene: Scene, views: Sequence[Camera],
     return diag
 
 
+def step_adam(state: OptimizerState, scene: Scene, views: Sequence[Camera],
+              opt: OptimizerOptions) -> StepDiagnostics:
+    """optimizer.hpp:132-134 (optimizer.cpp:222-236)."""
+    return _step_host(state, scene, views, _with_kind(opt, "adam"), "step_adam")
+
+
+def step_adam_tr(state: OptimizerState, scene: Scene, views: Sequence[Camera],
+                 opt: OptimizerOptions) -> StepDiagnostics:
+    """optimizer.hpp:135-137 (optimizer.cpp:238-253)."""
+    return _step_host(state, scene, views, _with_kind(opt, "adam-tr"), "step_adam_tr")
+
+
+def _with_kind(opt: OptimizerOptions, kind: str) -> OptimizerOptions:
+    import dataclasses
+    return dataclasses.replace(opt, kind=kind)
+
+
 def optimizer_step(state: OptimizerState, scene: Scene, views: Sequence[Camera],
                    opt: OptimizerOptions) -> StepDiagnostics:
-    """optimizer.hpp:139-141 (only the 3dgs2tr kind is on the B200 path)."""
-    if opt.kind != "3dgs2tr":
-        raise InvalidArgument(f"optimizer kind '{opt.kind}' is not on the B200 path")
-    return step_3dgs2tr(state, scene, views, opt)
+    """optimizer.hpp:139-141: dispatch on opt.kind."""
+    return _step_host(state, scene, views, opt, "optimizer_step")
 
 
 # ------------------------------------------------------------------ data

@@ -430,3 +430,52 @@ def test_fast_exp_bit_identical(sp, lo, hi):
     bad = C.c_int64(-1)
     _lib.check(_lib.lib().sgtr_check_fast_exp(1 << 24, lo, hi, 12345, C.byref(bad)))
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("kind", ["adam", "adam-tr"])
+def test_adam_step_parity_rng_mode(sp, orc, kind):
+    # step_adam / step_adam_tr (optimizer.cpp:222-253) against the oracle with
+    # both drawing S1 from the same seeded Rng
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=300, init_splats=300, views=6,
+                                            image_size=48, seed=3))
+    views = cams_of(sp, ds.cams, ds.gts)
+    st = sp.OptimizerState(ds.init_x.size, 77)
+    scene = sp.Scene(ds.init_x)
+    ost = orc.State(ds.init_x.size, 77)
+    xo = ds.init_x.copy()
+    opts = _tr_opts(sp, 25, batch_size=2, kind=kind, scene_extent=1.3,
+                    adam=sp.AdamOptions(lr_position_decay_steps=4))
+    oopts = orc.TrOptions(total_steps=25, batch_size=2)
+    oadam = orc.AdamOptions(lr_position_decay_steps=4, scene_extent=1.3)
+    for t in range(1, 7):
+        dg = sp.optimizer_step(st, scene, views, opts)
+        do = orc.step_adam(ost, xo, ds.cams, ds.gts, oopts, oadam, kind == "adam-tr",
+                           want_applied=True)
+        m, v = st.ctx.state_get_adam()
+        mo, vo = ost.get_adam()
+        assert st.t == t
+        assert rel(m, mo) < GRAD_TOL and rel(v, vo) < GRAD_TOL
+        # the ADAM direction normalises each coordinate by its own RMS, so a
+        # coordinate's relative gradient error (not the vector's) reaches
+        # the step: the accumulated-gradient tolerance applies
+        assert rel(dg.applied_step, do["applied_step"]) < GRAD_TOL
+        # ADAM's unit-RMS steps move the scene far more per step than the
+        # trust region, so trajectory differences grow faster than in
+        # test_step_parity_rng_mode
+        assert rel(scene.x, xo) < IMG_TOL
+        assert dg.batch_loss == pytest.approx(do["batch_loss"], rel=1e-8)
+        assert dg.step_pre == pytest.approx(do["step_pre"], rel=GRAD_TOL)
+        assert dg.eps == do["eps"]
+        assert not dg.refreshed
+        if kind == "adam":
+            assert dg.clip_frac == -1.0 and dg.max_step_over_radius == 0.0
+        else:
+            assert dg.clip_frac == pytest.approx(do["clip_frac"], abs=2.0 / xo.size)
+    g_hat, d_hat, _ = st.ctx.state_get()
+    assert not g_hat.any() and not d_hat.any()
+
+
+def test_optimizer_kind_from_string(sp):
+    with pytest.raises(sp.InvalidArgument, match="unknown optimizer 'sgd'"):
+        sp.optimizer_kind_from_string("sgd")
+    assert sp.optimizer_kind_from_string("adam-tr") == "adam-tr"
