@@ -117,6 +117,21 @@ int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro,
                         int32_t quantize);
 int sgtr_get_target(sgtr_ctx* ctx, int32_t view, double* gt);
 
+/* ------------------------------------------------------------ evaluation */
+/* held-out views for evaluate_scene (harness.cpp:43-58); any image sizes,
+ * targets (H*W*3 doubles) required and kept on the device */
+int sgtr_set_eval_views(sgtr_ctx* ctx, const sgtr_camera* cams, int32_t n,
+                        const double* const* gts);
+/* evaluate_scene on the device: per view PSNR (residuals.cpp:133-144) and
+ * mean SSIM (ssim.cpp:170-175) of quantize8(rasterize(scene, cam).color)
+ * against the target, and their means.  which = 0: the eval views,
+ * 1: the training views.  view_psnr / view_ssim hold one entry per view
+ * (either may be NULL). */
+int sgtr_evaluate_scene(sgtr_ctx* ctx, int32_t which,
+                        const sgtr_render_options* ro, double* view_psnr,
+                        double* view_ssim, double* mean_psnr,
+                        double* mean_ssim);
+
 /* ------------------------------------------------------------ optimizer state */
 /* OptimizerState(dim, seed) (optimizer.hpp:58-72): g_hat = d_hat = 0, t = 0,
  * Rng(seed) */

@@ -97,6 +97,9 @@ _SIGS = {
     "sgtr_set_views": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sgtr_render_targets": (C.c_int, [VP, VP, C.c_int32]),
     "sgtr_get_target": (C.c_int, [VP, C.c_int32, VP]),
+    "sgtr_set_eval_views": (C.c_int, [VP, VP, C.c_int32, VP]),
+    "sgtr_evaluate_scene": (C.c_int, [VP, C.c_int32, VP, VP, VP, C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
     "sgtr_state_reset": (C.c_int, [VP, C.c_uint64]),
     "sgtr_state_set": (C.c_int, [VP, VP, VP, C.c_int64]),
     "sgtr_state_get": (C.c_int, [VP, VP, VP, C.POINTER(C.c_int64)]),

@@ -332,6 +332,11 @@ struct Ctx {
     std::vector<View> views;
     Buf gt;  // planar targets, one (3, H, W) block per view
     bool has_gt = false;
+    // held-out views for evaluate_scene (any sizes; planar targets packed
+    // back to back at eval_off[i])
+    std::vector<View> eval_views;
+    std::vector<long long> eval_off;
+    Buf eval_gt, eval_sums;
     long long t = 0;
     Rng rng{1};       // committed state: all draws of completed steps
     Prefetcher prefetch;
@@ -1015,6 +1020,93 @@ int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro, int32_t qu
         }
         c.has_gt = true;
         SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_set_eval_views(sgtr_ctx* ctx, const sgtr_camera* cams, int32_t n,
+                        const double* const* gts) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (n < 0) throw invalid("sgtr_set_eval_views: negative count");
+        if (n > 0 && !gts) throw invalid("sgtr_set_eval_views: targets required");
+        std::vector<View> vs;
+        std::vector<long long> off;
+        long long total = 0;
+        for (int i = 0; i < n; ++i) {
+            if (cams[i].width <= 0 || cams[i].height <= 0)
+                throw invalid("sgtr_set_eval_views: empty image");
+            vs.push_back({cams[i], make_devcam(cams[i])});
+            off.push_back(total);
+            total += 3LL * cams[i].width * cams[i].height;
+        }
+        double* g = c.eval_gt.as<double>(std::max(total, 1LL));
+        for (int i = 0; i < n; ++i) {
+            const int P = cams[i].width * cams[i].height;
+            double* tmp = c.vecbuf.as<double>(3LL * P);
+            SGTR_CUDA(cudaMemcpyAsync(tmp, gts[i], sizeof(double) * 3 * P,
+                                      cudaMemcpyHostToDevice, c.st));
+            launch_to_planar(c.st, tmp, P, g + off[i]);
+            SGTR_CUDA(cudaStreamSynchronize(c.st));  // vecbuf is reused per view
+        }
+        c.eval_views = vs;
+        c.eval_off = off;
+    });
+}
+
+int sgtr_evaluate_scene(sgtr_ctx* ctx, int32_t which, const sgtr_render_options* ro,
+                        double* view_psnr, double* view_ssim, double* mean_psnr,
+                        double* mean_ssim) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        if (which != 0 && which != 1) throw invalid("evaluate_scene: bad view set");
+        const std::vector<View>& vs = which == 0 ? c.eval_views : c.views;
+        if (vs.empty()) throw invalid("evaluate_scene: empty view list");
+        if (which == 1) check_views(c, true);
+        const RenderP rp = render_params(*ro);
+        const int n = (int)vs.size();
+        double* sums = c.eval_sums.as<double>(2LL * n);
+        for (int i = 0; i < n; ++i) {
+            const int W = vs[i].dc.W, H = vs[i].dc.H, P = W * H;
+            check_ssim_size(W, H);
+            const double* gt = which == 0 ? c.eval_gt.get<double>() + c.eval_off[i]
+                                          : view_gt(c, i);
+            // quantize8(rasterize(scene, cam).color) (harness.cpp:50)
+            render_view(c, vs[i].dc, rp, true);
+            launch_quantize8(c.st, c.img.get<double>(), 3LL * P);
+            SsimArgs a{};
+            a.mode = EVAL;
+            a.W = W;
+            a.H = H;
+            a.a = c.img.get<double>();
+            a.b = gt;
+            const int nb = ssim_num_blocks(W, H);
+            a.loss_partials = c.partials.as<double>(2LL * nb);
+            launch_ssim(c.st, a);
+            launch_sum_partials(c.st, a.loss_partials, nb, sums + 2 * i);
+            launch_sum_partials(c.st, a.loss_partials + nb, nb, sums + 2 * i + 1);
+            c.launches += 4;
+        }
+        std::vector<double> h(2LL * n);
+        SGTR_CUDA(cudaMemcpyAsync(h.data(), sums, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost,
+                                  c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        double mp = 0.0, ms = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double cnt = 3.0 * vs[i].dc.W * vs[i].dc.H;
+            // psnr (residuals.cpp:133-144), mean_ssim (ssim.cpp:170-175)
+            const double mse = h[2 * i + 1] / cnt;
+            const double p = mse < 1e-10 ? 100.0 : 10.0 * std::log10(1.0 / mse);
+            const double sv = h[2 * i] / cnt;
+            if (view_psnr) view_psnr[i] = p;
+            if (view_ssim) view_ssim[i] = sv;
+            mp += p;
+            ms += sv;
+        }
+        if (mean_psnr) *mean_psnr = mp / n;
+        if (mean_ssim) *mean_ssim = ms / n;
     });
 }
 

@@ -114,7 +114,9 @@ enum SsimMode {
     GRAD,          // u = f: loss partials, adjL1 and P, Q, R (K8)
     HUTCH,         // u = J t: adjL1 and P, Q, R (K13)
     RES_VJP,       // u given (6P, in `u`): adjL1 and P, Q, R
-    SSIM_VJP       // upstream given (3P planar, in `u`): P, Q, R
+    SSIM_VJP,      // upstream given (3P planar, in `u`): P, Q, R
+    EVAL           // per-block sums of SSIM and (a-b)^2 into loss_partials
+                   // [blk] and [nblocks + blk] (mean_ssim, psnr)
 };
 struct SsimArgs {
     int mode, W, H;

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
     __syncthreads();
     using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
     const int tx = threadIdx.x % TX;
-    double partial = 0.0;
+    double partial = 0.0, partial2 = 0.0;
     for (int ty = threadIdx.x / TX; ty < TY; ty += kThreads / TX) {
     const int gx = x0 + tx, gy = y0 + ty;
     double m[NM];
@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
         const double lam = args.lambda, fl = args.floor;
         const double u1 = (1.0 - lam) * fabs(diff);
         const double u2 = lam * (1.0 - s_v) / 2.0;
-        if (MODE == SSIM_MAP) {
+        if (MODE == EVAL) {
+            partial += s_v;
+            partial2 += diff * diff;
+        } else if (MODE == SSIM_MAP) {
             args.out0[pi] = s_v;
         } else if (MODE == SSIM_JVP) {
             args.out0[pi] = s_v;
@@ -197,18 +200,29 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
         }
     }
     }
-    if (MODE == GRAD) {
+    if (MODE == GRAD || MODE == EVAL) {
         // deterministic block sum -> one partial per block
-        __shared__ double s_red[kThreads / 32];
+        __shared__ double s_red[2][kThreads / 32];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) partial += __shfl_xor_sync(0xffffffffu, partial, o);
-        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = partial;
+        for (int o = 16; o > 0; o >>= 1) {
+            partial += __shfl_xor_sync(0xffffffffu, partial, o);
+            if (MODE == EVAL) partial2 += __shfl_xor_sync(0xffffffffu, partial2, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            s_red[0][threadIdx.x >> 5] = partial;
+            s_red[1][threadIdx.x >> 5] = partial2;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) t += s_red[w];
+            double t = 0.0, t2 = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                t += s_red[0][w];
+                t2 += s_red[1][w];
+            }
+            const int nblk = gridDim.x * gridDim.y * gridDim.z;
             const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
             args.loss_partials[blk] = t;
+            if (MODE == EVAL) args.loss_partials[nblk + blk] = t2;
         }
     }
 }
@@ -363,6 +377,7 @@ void launch_ssim(cudaStream_t st, const SsimArgs& a) {
         case HUTCH: run_ssim<HUTCH>(st, a); break;
         case RES_VJP: run_ssim<RES_VJP>(st, a); break;
         case SSIM_VJP: run_ssim<SSIM_VJP>(st, a); break;
+        case EVAL: run_ssim<EVAL>(st, a); break;
         default: throw Error(SGTR_RUNTIME, "launch_ssim: bad mode");
     }
 }

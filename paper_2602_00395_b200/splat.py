@@ -36,7 +36,7 @@ __all__ = [
     "view_jacobian_applyT", "stochastic_gradient", "rademacher_probes", "hutchinson_diag",
     "ema", "newton_step", "shd_radii", "clip_step", "eps_at", "step_3dgs2tr",
     "step_adam", "step_adam_tr", "AdamOptions", "optimizer_kind_from_string",
-    "optimizer_step", "psnr", "quantize8", "make_synthetic", "look_at_camera",
+    "optimizer_step", "psnr", "quantize8", "evaluate_scene", "EvalResult", "make_synthetic", "look_at_camera",
 ]
 
 
@@ -331,6 +331,35 @@ class Context:
         return out
 
     # views
+    def set_eval_views(self, views: Sequence[Camera]) -> None:
+        """Held-out views (with targets) for evaluate(); kept on the device."""
+        n = len(views)
+        arr = (_lib.Camera * max(n, 1))()
+        keep = []
+        for i, v in enumerate(views):
+            if v.gt is None:
+                raise InvalidArgument("evaluate_scene: view has no target image")
+            g = _f64(v.gt)
+            if g.shape != (v.height, v.width, 3):
+                raise InvalidArgument("Camera.gt shape does not match the camera")
+            arr[i] = v._c()
+            keep.append(g)
+        gts = (C.c_void_p * max(n, 1))(*[g.ctypes.data for g in keep])
+        check(lib().sgtr_set_eval_views(self._h, arr, n, gts))
+        self.n_eval_views = n
+
+    def evaluate(self, ro: Optional[RenderOptions] = None, training_views: bool = False):
+        """evaluate_scene (harness.cpp:43-58) on the resident scene: the eval
+        views (or the training views) rendered, quantised and scored on the
+        device; returns an EvalResult."""
+        ro = ro or RenderOptions()
+        n = self.n_views if training_views else getattr(self, "n_eval_views", 0)
+        vp, vs = np.empty(max(n, 1)), np.empty(max(n, 1))
+        mp, ms = C.c_double(), C.c_double()
+        check(lib().sgtr_evaluate_scene(self._h, 1 if training_views else 0, C.byref(ro._c()),
+                                        _ptr(vp), _ptr(vs), C.byref(mp), C.byref(ms)))
+        return EvalResult(vp[:n].tolist(), vs[:n].tolist(), mp.value, ms.value)
+
     def set_views(self, views: Sequence[Camera], with_gt: bool = True) -> None:
         n = len(views)
         arr = (_lib.Camera * max(n, 1))()
@@ -602,6 +631,26 @@ def psnr(a, b) -> float:
     a, b = _img_pair(a, b, "psnr")
     mse = float(np.mean((a - b) ** 2))
     return 100.0 if mse < 1e-10 else 10.0 * math.log10(1.0 / mse)
+
+
+@dataclass
+class EvalResult:  # harness.hpp:29-35
+    view_psnr: List[float]
+    view_ssim: List[float]
+    mean_psnr: float
+    mean_ssim: float
+
+
+def evaluate_scene(scene: Scene, views: Sequence[Camera],
+                   ropt: Optional[RenderOptions] = None,
+                   ctx: Optional[Context] = None) -> EvalResult:
+    """harness.cpp:43-58 on the GPU: per view, PSNR and mean SSIM of
+    quantize8(rasterize(scene, cam).color) against cam.gt."""
+    if not views:
+        raise InvalidArgument("evaluate_scene: empty view list")
+    c = _scene_ctx(scene, ctx)
+    c.set_eval_views(views)
+    return c.evaluate(ropt)
 
 
 def quantize8(img) -> np.ndarray:

@@ -479,3 +479,28 @@ def test_optimizer_kind_from_string(sp):
     with pytest.raises(sp.InvalidArgument, match="unknown optimizer 'sgd'"):
         sp.optimizer_kind_from_string("sgd")
     assert sp.optimizer_kind_from_string("adam-tr") == "adam-tr"
+
+
+def test_evaluate_scene_parity(sp, orc):
+    # evaluate_scene (harness.cpp:43-58): quantize8(render) -> psnr, mean_ssim
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=400, init_splats=400, views=3,
+                                            image_size=40, seed=8))
+    x = ds.init_x
+    # a second, non-square eval size through the W != H extension
+    ds2 = orc.make_synthetic(orc.SynthConfig(gt_splats=400, init_splats=400, views=2,
+                                             image_size=40, seed=8, width=56, height=36))
+    cams = list(ds.cams) + list(ds2.cams)
+    gts = list(ds.gts) + list(ds2.gts)
+    views = cams_of(sp, cams, gts)
+    ev = sp.evaluate_scene(sp.Scene(x), views)
+    for i, (c, g) in enumerate(zip(cams, gts)):
+        q = orc.quantize8(orc.rasterize(x, c)[0])
+        assert ev.view_psnr[i] == pytest.approx(orc.psnr(q, g), abs=1e-9)
+        assert ev.view_ssim[i] == pytest.approx(orc.mean_ssim(q, g), abs=1e-12)
+    assert ev.mean_psnr == pytest.approx(np.mean(ev.view_psnr), rel=1e-15)
+    assert ev.mean_ssim == pytest.approx(np.mean(ev.view_ssim), rel=1e-15)
+    # a perfect render scores the reference's 100 dB cap (residuals.cpp:142)
+    perfect = [sp.Camera.from_c(c, orc.quantize8(orc.rasterize(x, c)[0])) for c in ds.cams]
+    assert sp.evaluate_scene(sp.Scene(x), perfect).view_psnr == [100.0] * 3
+    with pytest.raises(sp.InvalidArgument, match="evaluate_scene: empty view list"):
+        sp.evaluate_scene(sp.Scene(x), [])
