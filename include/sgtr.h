@@ -117,6 +117,35 @@ int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro,
                         int32_t quantize);
 int sgtr_get_target(sgtr_ctx* ctx, int32_t view, double* gt);
 
+/* ------------------------------------------------------------ files */
+/* splat::ParamBounds (scene.hpp:29-35); NULL selects the defaults */
+typedef struct sgtr_param_bounds {
+    double s_min, alpha_min, alpha_max, c_min, c_max;
+} sgtr_param_bounds;
+/* save_scene (scene_io.cpp:34-53) of the resident scene: binary little-endian
+ * PLY, 14 double properties per vertex, bitwise round trip */
+int sgtr_save_scene_ply(sgtr_ctx* ctx, const char* path);
+/* load_scene (scene_io.cpp:55-116) straight into the context (replaces the
+ * scene; Scene::validate runs on the device, errors name the splat) */
+int sgtr_load_scene_ply(sgtr_ctx* ctx, const char* path,
+                        const sgtr_param_bounds* bounds);
+/* the same file format on host buffers (group-major x of 14*K doubles);
+ * sgtr_ply_load with x == NULL only reports the splat count */
+int sgtr_ply_save(const double* x, int64_t n_splats, const char* path);
+int sgtr_ply_load(const char* path, const sgtr_param_bounds* bounds, double* x,
+                  int64_t* n_splats);
+/* save_cameras / load_cameras (scene_io.cpp:118-167; images not loaded):
+ * one camera per line "id fx fy cx cy width height qw qx qy qz tx ty tz
+ * image"; load reports the count in *n and fills up to cap entries, image
+ * names NUL-terminated at image_names + i * name_stride */
+int sgtr_save_cameras(const char* path, const sgtr_camera* cams,
+                      const char* const* image_names, int32_t n);
+int sgtr_load_cameras(const char* path, sgtr_camera* cams, char* image_names,
+                      int32_t name_stride, int32_t cap, int32_t* n);
+/* scene_extent (scene.cpp:83-92): max camera-centre distance from the
+ * centroid (1 for fewer than two cameras); OptimizerOptions::scene_extent */
+int sgtr_scene_extent(const sgtr_camera* cams, int32_t n, double* out);
+
 /* ------------------------------------------------------------ evaluation */
 /* held-out views for evaluate_scene (harness.cpp:43-58); any image sizes,
  * targets (H*W*3 doubles) required and kept on the device */

@@ -58,6 +58,11 @@ class OptimizerOpts(C.Structure):
                 ("residual", ResidualOpts), ("render", RenderOpts)]
 
 
+class ParamBounds(C.Structure):
+    _fields_ = [("s_min", C.c_double), ("alpha_min", C.c_double), ("alpha_max", C.c_double),
+                ("c_min", C.c_double), ("c_max", C.c_double)]
+
+
 class AdamOpts(C.Structure):
     _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("lr_position", C.c_double), ("lr_position_final", C.c_double),
@@ -97,6 +102,14 @@ _SIGS = {
     "sgtr_set_views": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sgtr_render_targets": (C.c_int, [VP, VP, C.c_int32]),
     "sgtr_get_target": (C.c_int, [VP, C.c_int32, VP]),
+    "sgtr_save_scene_ply": (C.c_int, [VP, C.c_char_p]),
+    "sgtr_load_scene_ply": (C.c_int, [VP, C.c_char_p, VP]),
+    "sgtr_ply_save": (C.c_int, [VP, C.c_int64, C.c_char_p]),
+    "sgtr_ply_load": (C.c_int, [C.c_char_p, VP, VP, C.POINTER(C.c_int64)]),
+    "sgtr_save_cameras": (C.c_int, [C.c_char_p, VP, VP, C.c_int32]),
+    "sgtr_load_cameras": (C.c_int, [C.c_char_p, VP, VP, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_int32)]),
+    "sgtr_scene_extent": (C.c_int, [VP, C.c_int32, C.POINTER(C.c_double)]),
     "sgtr_set_eval_views": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sgtr_evaluate_scene": (C.c_int, [VP, C.c_int32, VP, VP, VP, C.POINTER(C.c_double),
                                       C.POINTER(C.c_double)]),

@@ -24,7 +24,8 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
                  "-Xptxas", "-warn-spills"]
 NO_FMA = {"project.cu", "update.cu", "binning.cu"}
-SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu", "probe.cu"]
+SOURCES = ["api.cu", "project.cu", "binning.cu", "raster.cu", "ssim.cu", "update.cu", "probe.cu",
+           "io.cu"]
 HEADERS = ["common.cuh", "fastexp.cuh", "geometry.cuh", "launch.h"]
 
 

@@ -1110,6 +1110,133 @@ int sgtr_evaluate_scene(sgtr_ctx* ctx, int32_t which, const sgtr_render_options*
     });
 }
 
+// ------------------------------------------------------------------ files
+namespace {
+const double* bounds_or_default(const sgtr_param_bounds* b, double out[5]) {
+    // ParamBounds defaults (scene.hpp:29-35)
+    const double d[5] = {1e-6, 1e-4, 0.995, 1e-6, 1.5};
+    if (b) {
+        out[0] = b->s_min;
+        out[1] = b->alpha_min;
+        out[2] = b->alpha_max;
+        out[3] = b->c_min;
+        out[4] = b->c_max;
+    } else {
+        std::copy(d, d + 5, out);
+    }
+    return out;
+}
+
+struct PinnedHost {
+    void* p = nullptr;
+    explicit PinnedHost(size_t n) { SGTR_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 8))); }
+    ~PinnedHost() { cudaFreeHost(p); }
+};
+}  // namespace
+
+int sgtr_save_scene_ply(sgtr_ctx* ctx, const char* path) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        const long long K = c.K, n = 14 * K;
+        PinnedHost h(sizeof(double) * n);
+        double* aos = c.vecbuf.as<double>(std::max(n, 1LL));
+        launch_soa_to_aos(c.st, c.X(), K, aos);
+        c.launches += K > 0;
+        if (n)
+            SGTR_CUDA(cudaMemcpyAsync(h.p, aos, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                      c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        ply_write(path, static_cast<const double*>(h.p), K);
+    });
+}
+
+int sgtr_load_scene_ply(sgtr_ctx* ctx, const char* path, const sgtr_param_bounds* b) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        const PlyHeader hd = ply_read_header(path);
+        const long long K = hd.count, n = 14 * K;
+        if (K > (1LL << 28)) throw invalid("load_scene: too many splats");
+        PinnedHost h(sizeof(double) * n);
+        ply_read_payload(path, hd, static_cast<double*>(h.p));
+        double* aos = c.vecbuf.as<double>(std::max(n, 1LL));
+        double* soa = c.x_alt.as<double>(std::max(n, 1LL));
+        if (n)
+            SGTR_CUDA(cudaMemcpyAsync(aos, h.p, sizeof(double) * n, cudaMemcpyHostToDevice,
+                                      c.st));
+        launch_aos_to_soa(c.st, aos, K, soa);
+        double bd[5];
+        unsigned long long* first = reinterpret_cast<unsigned long long*>(
+            c.partials.as<double>(1));
+        launch_validate(c.st, soa, K, bounds_or_default(b, bd), first);
+        c.launches += 2 * (K > 0);
+        unsigned long long hf = ~0ull;
+        SGTR_CUDA(cudaMemcpyAsync(&hf, first, sizeof(hf), cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        throw_invalid_splat(hf);  // Scene::validate (scene.cpp:59-81)
+        const bool resized = K != c.K;
+        std::swap(c.x.p, c.x_alt.p);
+        std::swap(c.x.bytes, c.x_alt.bytes);
+        c.K = (int)K;
+        if (resized) zero_state(c);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+    });
+}
+
+int sgtr_ply_save(const double* x, int64_t n_splats, const char* path) {
+    return guarded([&] {
+        if (n_splats < 0) throw invalid("save_scene: negative splat count");
+        std::vector<double> aos(14 * n_splats);
+        host_soa_to_aos(x, n_splats, aos.data());
+        ply_write(path, aos.data(), n_splats);
+    });
+}
+
+int sgtr_ply_load(const char* path, const sgtr_param_bounds* b, double* x, int64_t* n_splats) {
+    return guarded([&] {
+        const PlyHeader hd = ply_read_header(path);
+        if (n_splats) *n_splats = hd.count;
+        if (!x) return;
+        std::vector<double> aos(14 * hd.count);
+        ply_read_payload(path, hd, aos.data());
+        std::vector<double> soa(14 * hd.count);
+        host_aos_to_soa(aos.data(), hd.count, soa.data());
+        double bd[5];
+        host_validate(soa.data(), hd.count, bounds_or_default(b, bd));
+        std::copy(soa.begin(), soa.end(), x);
+    });
+}
+
+int sgtr_save_cameras(const char* path, const sgtr_camera* cams, const char* const* image_names,
+                      int32_t n) {
+    return guarded([&] {
+        if (n < 0) throw invalid("save_cameras: negative count");
+        save_cameras(path, cams, image_names, n);
+    });
+}
+
+int sgtr_load_cameras(const char* path, sgtr_camera* cams, char* image_names, int32_t name_stride,
+                      int32_t cap, int32_t* n) {
+    return guarded([&] {
+        const std::vector<CameraLine> cl = load_cameras(path);
+        *n = (int32_t)cl.size();
+        for (size_t i = 0; i < cl.size() && (int)i < cap; ++i) {
+            if (cams) cams[i] = cl[i].cam;
+            if (image_names && name_stride > 0) {
+                char* dst = image_names + i * name_stride;
+                std::strncpy(dst, cl[i].image_name.c_str(), name_stride - 1);
+                dst[name_stride - 1] = 0;
+            }
+        }
+    });
+}
+
+int sgtr_scene_extent(const sgtr_camera* cams, int32_t n, double* out) {
+    return guarded([&] { *out = scene_extent(cams, n); });
+}
+
 int sgtr_get_target(sgtr_ctx* ctx, int32_t view, double* gt) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);

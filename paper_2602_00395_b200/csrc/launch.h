@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <string>
+#include <vector>
+
 #include "common.cuh"
 
 namespace sgtr {
@@ -179,6 +182,30 @@ void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, do
 void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
                       const double caps[5], double* eta);
 void launch_scale(cudaStream_t st, double* v, long long n, double s);
+// io.cu
+struct PlyHeader {
+    long long count;
+    long long data_offset;
+};
+struct CameraLine {
+    sgtr_camera cam;
+    std::string image_name;
+};
+PlyHeader ply_read_header(const std::string& path);
+void ply_read_payload(const std::string& path, const PlyHeader& h, double* aos);
+void ply_write(const std::string& path, const double* aos, long long count);
+void host_aos_to_soa(const double* aos, long long K, double* soa);
+void host_soa_to_aos(const double* soa, long long K, double* aos);
+void host_validate(const double* x, long long K, const double b[5]);
+void throw_invalid_splat(unsigned long long first);
+void launch_aos_to_soa(cudaStream_t st, const double* aos, long long K, double* soa);
+void launch_soa_to_aos(cudaStream_t st, const double* soa, long long K, double* aos);
+void launch_validate(cudaStream_t st, const double* x, long long K, const double b[5],
+                     unsigned long long* first);
+void save_cameras(const std::string& path, const sgtr_camera* cams, const char* const* names,
+                  int n);
+std::vector<CameraLine> load_cameras(const std::string& path);
+double scene_extent(const sgtr_camera* cams, int n);
 // probe.cu
 double fp64_fma_peak_tflops(int device);
 long long fast_exp_mismatches(long long n, double lo, double hi, unsigned long long seed);

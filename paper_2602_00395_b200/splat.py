@@ -36,7 +36,8 @@ __all__ = [
     "view_jacobian_applyT", "stochastic_gradient", "rademacher_probes", "hutchinson_diag",
     "ema", "newton_step", "shd_radii", "clip_step", "eps_at", "step_3dgs2tr",
     "step_adam", "step_adam_tr", "AdamOptions", "optimizer_kind_from_string",
-    "optimizer_step", "psnr", "quantize8", "evaluate_scene", "EvalResult", "make_synthetic", "look_at_camera",
+    "optimizer_step", "psnr", "quantize8", "evaluate_scene", "EvalResult", "save_scene",
+    "load_scene", "save_cameras", "load_cameras", "scene_extent", "make_synthetic", "look_at_camera",
 ]
 
 
@@ -238,6 +239,7 @@ class Camera:  # scene.hpp:70-81
     q_wc: Sequence[float] = (0.0, 0.0, 0.0, 1.0)
     t_wc: Sequence[float] = (0.0, 0.0, 0.0)
     gt: Optional[np.ndarray] = None  # (H, W, 3) float64
+    image_name: str = ""
 
     def _c(self) -> _lib.Camera:
         return _lib.Camera(self.id, self.width, self.height, 0, self.fx, self.fy, self.cx,
@@ -331,6 +333,15 @@ class Context:
         return out
 
     # views
+    def save_scene(self, path: str) -> None:
+        """save_scene of the resident scene (device transpose, one copy)."""
+        check(lib().sgtr_save_scene_ply(self._h, str(path).encode()))
+
+    def load_scene(self, path: str, bounds: Optional[ParamBounds] = None) -> None:
+        """load_scene straight into HBM (validation on the device)."""
+        check(lib().sgtr_load_scene_ply(self._h, str(path).encode(), _bounds_c(bounds)))
+        self.k = int(lib().sgtr_scene_size(self._h))
+
     def set_eval_views(self, views: Sequence[Camera]) -> None:
         """Held-out views (with targets) for evaluate(); kept on the device."""
         n = len(views)
@@ -631,6 +642,66 @@ def psnr(a, b) -> float:
     a, b = _img_pair(a, b, "psnr")
     mse = float(np.mean((a - b) ** 2))
     return 100.0 if mse < 1e-10 else 10.0 * math.log10(1.0 / mse)
+
+
+# ------------------------------------------------------------------ files
+def _bounds_c(b: Optional[ParamBounds]):
+    if b is None:
+        return None
+    return C.byref(_lib.ParamBounds(b.s_min, b.alpha_min, b.alpha_max, b.c_min, b.c_max))
+
+
+def save_scene(scene: Scene, path: str) -> None:
+    """scene_io.hpp:17 (binary little-endian PLY, bitwise round trip)."""
+    check(lib().sgtr_ply_save(_ptr(scene.x), scene.size(), str(path).encode()))
+
+
+def load_scene(path: str, bounds: Optional[ParamBounds] = None) -> Scene:
+    """scene_io.hpp:18-19: parse, then Scene::validate(bounds); errors are
+    SgtrError (std::runtime_error) naming the line or the splat."""
+    k = C.c_int64()
+    check(lib().sgtr_ply_load(str(path).encode(), None, None, C.byref(k)))
+    x = np.empty(14 * k.value)
+    check(lib().sgtr_ply_load(str(path).encode(), _bounds_c(bounds), _ptr(x), C.byref(k)))
+    return Scene(x)
+
+
+def save_cameras(cams: Sequence[Camera], path: str) -> None:
+    """scene_io.hpp:24 (one camera per line, %.17g)."""
+    n = len(cams)
+    arr = (_lib.Camera * max(n, 1))()
+    for i, c in enumerate(cams):
+        arr[i] = c._c()
+    names = (C.c_char_p * max(n, 1))(*[c.image_name.encode() for c in cams])
+    check(lib().sgtr_save_cameras(str(path).encode(), arr, names, n))
+
+
+def load_cameras(path: str) -> List[Camera]:
+    """scene_io.hpp:25-26 with load_images = false (targets are set through
+    Context.set_views / render_targets)."""
+    n = C.c_int32()
+    check(lib().sgtr_load_cameras(str(path).encode(), None, None, 0, 0, C.byref(n)))
+    arr = (_lib.Camera * max(n.value, 1))()
+    stride = 4096
+    names = C.create_string_buffer(stride * max(n.value, 1))
+    check(lib().sgtr_load_cameras(str(path).encode(), arr, names, stride, n.value, C.byref(n)))
+    out = []
+    for i in range(n.value):
+        cam = Camera.from_c(arr[i])
+        cam.image_name = names.raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode()
+        out.append(cam)
+    return out
+
+
+def scene_extent(cams: Sequence[Camera]) -> float:
+    """scene.hpp:83-85 (OptimizerOptions.scene_extent for the ADAM kinds)."""
+    n = len(cams)
+    arr = (_lib.Camera * max(n, 1))()
+    for i, c in enumerate(cams):
+        arr[i] = c._c()
+    out = C.c_double()
+    check(lib().sgtr_scene_extent(arr, n, C.byref(out)))
+    return out.value
 
 
 @dataclass
