@@ -142,6 +142,12 @@ int sgtr_save_cameras(const char* path, const sgtr_camera* cams,
                       const char* const* image_names, int32_t n);
 int sgtr_load_cameras(const char* path, sgtr_camera* cams, char* image_names,
                       int32_t name_stride, int32_t cap, int32_t* n);
+/* optimizer-state checkpoint / resume (beyond the reference, which only
+ * saves the scene PLY): scene x, g_hat, d_hat, adam_m, adam_v, t and the
+ * Rng state, so a resumed run draws the identical S1/S2/probe stream and
+ * continues bit for bit */
+int sgtr_checkpoint_save(sgtr_ctx* ctx, const char* path);
+int sgtr_checkpoint_load(sgtr_ctx* ctx, const char* path);
 /* scene_extent (scene.cpp:83-92): max camera-centre distance from the
  * centroid (1 for fewer than two cameras); OptimizerOptions::scene_extent */
 int sgtr_scene_extent(const sgtr_camera* cams, int32_t n, double* out);

@@ -109,6 +109,8 @@ _SIGS = {
     "sgtr_save_cameras": (C.c_int, [C.c_char_p, VP, VP, C.c_int32]),
     "sgtr_load_cameras": (C.c_int, [C.c_char_p, VP, VP, C.c_int32, C.c_int32,
                                     C.POINTER(C.c_int32)]),
+    "sgtr_checkpoint_save": (C.c_int, [VP, C.c_char_p]),
+    "sgtr_checkpoint_load": (C.c_int, [VP, C.c_char_p]),
     "sgtr_scene_extent": (C.c_int, [VP, C.c_int32, C.POINTER(C.c_double)]),
     "sgtr_set_eval_views": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sgtr_evaluate_scene": (C.c_int, [VP, C.c_int32, VP, VP, VP, C.POINTER(C.c_double),

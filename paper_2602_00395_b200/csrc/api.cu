@@ -8,6 +8,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <sstream>
+#include <fstream>
 #include <atomic>
 #include <climits>
 #include <condition_variable>
@@ -1230,6 +1232,87 @@ int sgtr_load_cameras(const char* path, sgtr_camera* cams, char* image_names, in
                 dst[name_stride - 1] = 0;
             }
         }
+    });
+}
+
+// Optimizer-state checkpoint (the reference only checkpoints
+// the scene PLY, harness.cpp:157-164).  Layout: "SGTRCKP1", K, t, the
+// mt19937_64 state as its standard text form (length-prefixed), the Rng's
+// normal() spare, then x | g_hat | d_hat | adam_m | adam_v (group-major).
+int sgtr_checkpoint_save(sgtr_ctx* ctx, const char* path) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        need_scene(c);
+        c.prefetch.reset();
+        const long long dim = c.dim();
+        std::ostringstream rs;
+        rs << c.rng.gen;
+        const std::string rtxt = rs.str();
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw Error(SGTR_RUNTIME, std::string("checkpoint: cannot open ") + path);
+        const long long hdr[3] = {(long long)c.K, c.t, (long long)rtxt.size()};
+        out.write("SGTRCKP1", 8);
+        out.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+        out.write(rtxt.data(), rtxt.size());
+        const double spare[2] = {c.rng.have_spare ? 1.0 : 0.0, c.rng.spare};
+        out.write(reinterpret_cast<const char*>(spare), sizeof(spare));
+        std::vector<double> h(std::max(dim, 1LL));
+        const double* vecs[5] = {c.X(), c.ghat.as<double>(std::max(dim, 1LL)),
+                                 c.dhat.as<double>(std::max(dim, 1LL)),
+                                 c.adam_m.as<double>(std::max(dim, 1LL)),
+                                 c.adam_v.as<double>(std::max(dim, 1LL))};
+        for (const double* v : vecs) {
+            if (dim)
+                SGTR_CUDA(cudaMemcpyAsync(h.data(), v, sizeof(double) * dim,
+                                          cudaMemcpyDeviceToHost, c.st));
+            SGTR_CUDA(cudaStreamSynchronize(c.st));
+            out.write(reinterpret_cast<const char*>(h.data()), sizeof(double) * dim);
+        }
+        if (!out) throw Error(SGTR_RUNTIME, std::string("checkpoint: write failed for ") + path);
+    });
+}
+
+int sgtr_checkpoint_load(sgtr_ctx* ctx, const char* path) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw Error(SGTR_RUNTIME, std::string("checkpoint: cannot open ") + path);
+        char magic[8];
+        long long hdr[3];
+        in.read(magic, 8);
+        in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+        if (!in || std::memcmp(magic, "SGTRCKP1", 8) != 0 || hdr[0] < 0 || hdr[2] <= 0 ||
+            hdr[2] > (1 << 20))
+            throw Error(SGTR_RUNTIME, std::string("checkpoint: not a checkpoint file: ") + path);
+        std::string rtxt(hdr[2], '\0');
+        in.read(&rtxt[0], hdr[2]);
+        double spare[2];
+        in.read(reinterpret_cast<char*>(spare), sizeof(spare));
+        const long long K = hdr[0], dim = 14 * K;
+        std::vector<double> h(5 * std::max(dim, 1LL));
+        in.read(reinterpret_cast<char*>(h.data()), sizeof(double) * 5 * dim);
+        if (!in) throw Error(SGTR_RUNTIME, std::string("checkpoint: truncated file ") + path);
+        Rng r;
+        std::istringstream is(rtxt);
+        is >> r.gen;
+        if (!is) throw Error(SGTR_RUNTIME, std::string("checkpoint: bad Rng state in ") + path);
+        r.have_spare = spare[0] != 0.0;
+        r.spare = spare[1];
+        c.prefetch.reset();
+        c.K = (int)K;
+        const long long n = std::max(dim, 1LL);
+        Buf* dst[5] = {&c.x, &c.ghat, &c.dhat, &c.adam_m, &c.adam_v};
+        for (int v = 0; v < 5; ++v)
+            if (dim)
+                SGTR_CUDA(cudaMemcpyAsync(dst[v]->as<double>(n), h.data() + v * dim,
+                                          sizeof(double) * dim, cudaMemcpyHostToDevice, c.st));
+            else
+                dst[v]->as<double>(n);
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        c.t = hdr[1];
+        c.rng = r;
     });
 }
 

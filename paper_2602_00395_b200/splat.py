@@ -342,6 +342,15 @@ class Context:
         check(lib().sgtr_load_scene_ply(self._h, str(path).encode(), _bounds_c(bounds)))
         self.k = int(lib().sgtr_scene_size(self._h))
 
+    def checkpoint_save(self, path: str) -> None:
+        """Scene + full optimizer state (g_hat, d_hat, ADAM moments, t, Rng)."""
+        check(lib().sgtr_checkpoint_save(self._h, str(path).encode()))
+
+    def checkpoint_load(self, path: str) -> None:
+        """Resume from checkpoint_save: the next step continues bit for bit."""
+        check(lib().sgtr_checkpoint_load(self._h, str(path).encode()))
+        self.k = int(lib().sgtr_scene_size(self._h))
+
     def set_eval_views(self, views: Sequence[Camera]) -> None:
         """Held-out views (with targets) for evaluate(); kept on the device."""
         n = len(views)
