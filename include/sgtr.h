@@ -331,6 +331,11 @@ int sgtr_check_fast_exp(int64_t n, double lo, double hi, uint64_t seed,
 /* one process per GPU; views of each step are split round-robin over
  * ranks and g | z.w | loss are summed with one ncclAllReduce per step */
 int sgtr_nccl_unique_id(uint8_t out[128]);
+/* Refresh (Hutchinson) views are split into row bands of tiles when there are
+ * fewer S2 views than ranks: B = nranks * bands_per_rank bands per view,
+ * rank r renders bands r, r + nranks, ... (default bands_per_rank = 1; > 1
+ * also splits on one rank, which tests use to check the band sums) */
+int sgtr_set_refresh_bands(sgtr_ctx* ctx, int32_t bands_per_rank);
 /* positions of a step's view batch (S1 or S2) that `rank` renders: the
  * round-robin split the step uses; host-only, no device needed */
 int sgtr_shard_views(int32_t n, int32_t rank, int32_t nranks, int32_t* positions,

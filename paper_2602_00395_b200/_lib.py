@@ -162,6 +162,7 @@ _SIGS = {
     "sgtr_nccl_unique_id": (C.c_int, [VP]),
     "sgtr_shard_views": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, VP,
                                    C.POINTER(C.c_int32)]),
+    "sgtr_set_refresh_bands": (C.c_int, [VP, C.c_int32]),
     "sgtr_comm_init": (C.c_int, [VP, VP, C.c_int32, C.c_int32]),
 }
 

@@ -352,6 +352,7 @@ struct Ctx {
     double* htail = nullptr;     // pinned staging for the fused tail
     size_t htail_n = 0;
     int nranks = 1, rank = 0;
+    int refresh_bands = 1;  // bands per rank of each refresh view (sgtr_set_refresh_bands)
     void* comm = nullptr;
 
     ~Ctx() {
@@ -402,7 +403,10 @@ void harvest_timing(Ctx& c) {
 double* img_ptr(Ctx& c, Buf& b, int P) { return b.as<double>(3LL * P); }
 
 // K1..K7 for one camera on the context's scene
-ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_errors) {
+// row0/row1: the tile rows the forward raster covers (a refresh band plus
+// its halo); row1 < 0 renders the whole view
+ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_errors,
+                       int row0 = 0, int row1 = -1) {
     ViewRender vr{};
     vr.W = dc.W;
     vr.H = dc.H;
@@ -484,8 +488,9 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
                         c.tbox.as<float4>(nd));
     }
     c.launches += vr.n_dup ? 1 : 0;
-    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start,          b.tile_end,
-                      b.dval_alt, b.dup_id,  tids, c.tbox.get<float4>()};
+    vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt,
+                      b.dup_id,  tids,    c.tbox.get<float4>(), row0,
+                      row1 < 0 ? tiles_y : row1};
     const int P = dc.W * dc.H;
     Timed t(c, KC_RASTER_FWD);
     launch_raster_fwd(c.st, vr.tl, rec, dc.W, dc.H, ro, img_ptr(c, c.img, P),
@@ -541,8 +546,11 @@ struct SsimOut {
 };
 
 // K8/K13 + K9: residual chain adjoint of the rendered image into c.adj
+// by0/by1: SSIM block rows to evaluate, gy0/gy1: block rows of the gathered
+// adjoint (a refresh band: the band's rows, SSIM on the band +- one block)
 void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const double* tangent,
-                      const double* u, double lambda, double floor_, double* loss_out) {
+                      const double* u, double lambda, double floor_, double* loss_out,
+                      int by0 = 0, int by1 = 0, int gy0 = 0, int gy1 = 0) {
     const int P = W * H;
     SsimArgs a{};
     a.mode = mode;
@@ -558,6 +566,8 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
     a.P = img_ptr(c, c.Pf, P);
     a.Q = img_ptr(c, c.Qf, P);
     a.R = img_ptr(c, c.Rf, P);
+    a.by0 = by0;
+    a.by1 = by1;
     const int nb = ssim_num_blocks(W, H);
     a.loss_partials = c.partials.as<double>(std::max(nb, 10 * tr_num_blocks(c.K) + 8));
     {
@@ -571,7 +581,7 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
     }
     Timed t(c, KC_GATHER);
     launch_ssim_gather(c.st, W, H, c.img.get<double>(), gt, a.adjl1, a.P, a.Q, a.R,
-                       img_ptr(c, c.adj, P));
+                       img_ptr(c, c.adj, P), gy0, gy1);
     c.launches += 1;
 }
 
@@ -676,31 +686,61 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         uint32_t* dz = c.zbits.as<uint32_t>(std::max<long long>(words * nu, 1));
         SGTR_CUDA(cudaMemcpyAsync(dz, zbits.data(), sizeof(uint32_t) * words * nu,
                                   cudaMemcpyHostToDevice, c.st));
+        // Work items: whole S2 views round-robin over ranks when there are
+        // enough of them; otherwise every view is cut into B bands of tile
+        // rows (B = ranks x refresh_bands) and rank r takes the bands
+        // b = r (mod ranks).  A band renders its rows plus one tile row of
+        // halo each side (the residual chain reaches 10 px: SSIM window 5 px
+        // forward, its transpose 5 px back), evaluates SSIM on the band
+        // +- 1 block row, gathers the adjoint on the band rows only and runs
+        // the VJP on the band tiles, so the bands' sums add up to the view's.
+        const int tiles_y = ceil_div(H, kTile);
+        const bool by_view = c.refresh_bands <= 1 && n2 >= c.nranks;
+        const int B = by_view ? 1 : std::min(tiles_y, c.nranks * c.refresh_bands);
         for (int s = 0; s < nu && !local_error; ++s) {
             const uint32_t* zb = dz + words * s;
-            for (int q = c.rank; q < n2; q += c.nranks) {
-                const View& v = c.views[s2[q]];
-                const ViewRender vr = render_view(c, v.dc, ro, false);
-                if (vr.err_kind) {
-                    herr[n1 + q] = vr.err_kind;
-                    herr[(n1 + n2) + n1 + q] = vr.err_index;
-                    local_error = true;
-                    break;
+            for (int q = 0; q < n2 && !local_error; ++q) {
+                if (by_view && q % c.nranks != c.rank) continue;
+                for (int band = 0; band < B && !local_error; ++band) {
+                    if (!by_view && band % c.nranks != c.rank) continue;
+                    const int tr0 = band * tiles_y / B, tr1 = (band + 1) * tiles_y / B;
+                    if (tr1 <= tr0) continue;
+                    const int r0 = std::max(0, tr0 - 1), r1 = std::min(tiles_y, tr1 + 1);
+                    const View& v = c.views[s2[q]];
+                    const ViewRender vr =
+                        B == 1 ? render_view(c, v.dc, ro, false)
+                               : render_view(c, v.dc, ro, false, r0, r1);
+                    if (vr.err_kind) {
+                        herr[n1 + q] = vr.err_kind;
+                        herr[(n1 + n2) + n1 + q] = vr.err_index;
+                        local_error = true;
+                        break;
+                    }
+                    double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
+                    {
+                        Timed t(c, KC_PROJECT_JVP);
+                        launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
+                    }
+                    {
+                        Timed t(c, KC_RASTER_JVP);
+                        launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, ro,
+                                          img_ptr(c, c.tan, P));
+                    }
+                    c.launches += 2;
+                    if (B == 1) {
+                        residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(),
+                                         nullptr, o.residual.lambda, o.residual.floor, nullptr);
+                        backward_view(c, v.dc, ro, vr, 1, nullptr, zb, w_acc, hflag);
+                    } else {
+                        residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(),
+                                         nullptr, o.residual.lambda, o.residual.floor, nullptr,
+                                         r0, r1, tr0, tr1);
+                        ViewRender vb = vr;
+                        vb.tl.row0 = tr0;
+                        vb.tl.row1 = tr1;
+                        backward_view(c, v.dc, ro, vb, 1, nullptr, zb, w_acc, hflag);
+                    }
                 }
-                double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
-                {
-                    Timed t(c, KC_PROJECT_JVP);
-                    launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
-                }
-                {
-                    Timed t(c, KC_RASTER_JVP);
-                    launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, ro,
-                                      img_ptr(c, c.tan, P));
-                }
-                c.launches += 2;
-                residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(), nullptr,
-                                 o.residual.lambda, o.residual.floor, nullptr);
-                backward_view(c, v.dc, ro, vr, 1, nullptr, zb, w_acc, hflag);
             }
         }
     }
@@ -2179,6 +2219,13 @@ int sgtr_nccl_unique_id(uint8_t out[128]) {
     return guarded([&] {
         g_nccl.load();
         g_nccl.check(g_nccl.get_unique_id(out), "ncclGetUniqueId");
+    });
+}
+
+int sgtr_set_refresh_bands(sgtr_ctx* ctx, int32_t bands_per_rank) {
+    return guarded([&] {
+        if (bands_per_rank < 1) throw invalid("sgtr_set_refresh_bands: need >= 1 band");
+        ctx_ref(ctx).refresh_bands = bands_per_rank;
     });
 }
 

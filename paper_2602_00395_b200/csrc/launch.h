@@ -73,6 +73,8 @@ struct TileLists {
     const int* dup_id;    // duplicate -> splat id
     const int* tile_ids;  // splat id per tile-sorted position (dup_id[sorted_d[j]])
     const float4* tbox;   // outward-rounded float bbox (x0, x1, y0, y1) per position
+    int row0, row1;       // tile rows the raster kernels process (a band on refresh
+                          // views split over ranks; [0, tiles_y) otherwise)
 };
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
@@ -126,13 +128,14 @@ struct SsimArgs {
     const double *a, *da, *b, *u;
     double lambda, floor;
     double *out0, *out1, *adjl1, *P, *Q, *R, *loss_partials;
+    int by0, by1;  // block rows (16 image rows each) to compute; by1 <= 0: all
 };
 int ssim_num_blocks(int W, int H);
 void launch_ssim(cudaStream_t st, const SsimArgs& a);
 // K9: adj = adjL1 + W^T P + a (.) W^T Q + b (.) W^T R (reflection-aware gather)
 void launch_ssim_gather(cudaStream_t st, int W, int H, const double* a, const double* b,
                         const double* adjl1, const double* P, const double* Q,
-                        const double* R, double* adj);
+                        const double* R, double* adj, int by0 = 0, int by1 = 0);
 void launch_sum_partials(cudaStream_t st, const double* partials, int n, double* out);
 // layout conversions: interleaved (H,W,3) <-> planar (3,H,W)
 void launch_to_planar(cudaStream_t st, const double* in, int P, double* out);

@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                                                          int* __restrict__ last,
                                                          unsigned long long* counters) {
     __shared__ __align__(16) double s_rec[kFwdBatch * kRec];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
     double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThreads)
                       int* __restrict__ last) {
     __shared__ int s_list[kWarps][kChunkF];
     __shared__ int s_ids[kWarps][kChunkF];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads)
                       double* __restrict__ tangent) {
     __shared__ int s_list[kWarps][kChunkF];
     __shared__ int s_ids[kWarps][kChunkF];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
     k_raster_fwd_ppl(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                      double* __restrict__ img, double* __restrict__ tfinal,
                      int* __restrict__ last) {
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
     const int px = X0 + (lane & 15);
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
     __shared__ int s_d[kVjpBatch];
     __shared__ unsigned s_mask[kVjpBatch];
     __shared__ int s_maxlast[kWarps];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     __shared__ double s_red[kWarps][kRedScratch];
     __shared__ int s_list[kWarps][kChunk];
     __shared__ int s_ids[kWarps][kChunk];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile];
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
                      const double* __restrict__ adj, const double* __restrict__ tfinal,
                      const int* __restrict__ last, double* __restrict__ part,
                      unsigned char* __restrict__ mask) {
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
     const int px = X0 + (lane & 15);
@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
                                                          double* __restrict__ tangent) {
     __shared__ __align__(16) double s_rec[kJvpBatch * kRec];
     __shared__ __align__(16) double s_t[kJvpBatch * kTRec];
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
     double T = 1.0, dT = 0.0;
@@ -963,7 +963,7 @@ const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
                        const RenderP& ro, double* img, double* tfinal, int* last,
                        unsigned long long* counters) {
-    const int n = tl.tiles_x * tl.tiles_y;
+    const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
@@ -986,7 +986,7 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
 void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
                        const RenderP& ro, const double* adj, const double* tfinal,
                        const int* last, double* slots) {
-    const int n = tl.tiles_x * tl.tiles_y;
+    const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
     if (g_warp_cull && g_vjp_min_blocks == 3)
         k_raster_vjp<true, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
@@ -1005,7 +1005,7 @@ int chain_mode() { return knob("SGTR_CHAIN_MODE", 0); }
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask) {
-    const int n = tl.tiles_x * tl.tiles_y;
+    const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
     if (g_vjp_ppl == 4)
         k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
@@ -1028,7 +1028,7 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
 
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
-    const int n = tl.tiles_x * tl.tiles_y;
+    const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
     if (knob("SGTR_JVP_WARP", 0))
         k_raster_jvp_warp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
     const int W = args.W, H = args.H;
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int x0 = blockIdx.x * TX, y0 = (blockIdx.y + args.by0) * TY;
     const double* A = args.a + c * P;
     const double* B = args.b + c * P;
     const double* DA = Tr::kTangent ? args.da + c * P : nullptr;
@@ -251,12 +251,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
                                                    const double* __restrict__ Pf,
                                                    const double* __restrict__ Qf,
                                                    const double* __restrict__ Rf,
-                                                   double* __restrict__ adj) {
+                                                   double* __restrict__ adj, int by0) {
     __shared__ double s_f[3][SY][SX];
     __shared__ double s_h[3][SY][TX];
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int x0 = blockIdx.x * TX, y0 = (blockIdx.y + by0) * TY;
     for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
         const int sy = i / SX, sx = i % SX;
         const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
@@ -357,7 +357,9 @@ void run_ssim(cudaStream_t st, const SsimArgs& a) {
                                        (int)smem));
         attr = true;
     }
-    dim3 grid(ceil_div(a.W, TX), ceil_div(a.H, TY), 3);
+    const int by1 = a.by1 > 0 ? a.by1 : ceil_div(a.H, TY);
+    if (by1 <= a.by0) return;
+    dim3 grid(ceil_div(a.W, TX), by1 - a.by0, 3);
     k_ssim<MODE><<<grid, kThreads, smem, st>>>(a);
     SGTR_CUDA(cudaGetLastError());
 }
@@ -384,10 +386,12 @@ void launch_ssim(cudaStream_t st, const SsimArgs& a) {
 
 void launch_ssim_gather(cudaStream_t st, int W, int H, const double* a, const double* b,
                         const double* adjl1, const double* P, const double* Q, const double* R,
-                        double* adj) {
+                        double* adj, int by0, int by1) {
     init_constants();
-    dim3 grid(ceil_div(W, TX), ceil_div(H, TY), 3);
-    k_gather<<<grid, kThreads, 0, st>>>(W, H, a, b, adjl1, P, Q, R, adj);
+    if (by1 <= 0) by1 = ceil_div(H, TY);
+    if (by1 <= by0) return;
+    dim3 grid(ceil_div(W, TX), by1 - by0, 3);
+    k_gather<<<grid, kThreads, 0, st>>>(W, H, a, b, adjl1, P, Q, R, adj, by0);
     SGTR_CUDA(cudaGetLastError());
 }
 

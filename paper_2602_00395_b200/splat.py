@@ -476,6 +476,10 @@ class Context:
             check(lib().sgtr_get_applied_step(self._h, _ptr(out.applied_step)))
         return out
 
+    def set_refresh_bands(self, bands_per_rank: int) -> None:
+        """Split each refresh view into nranks * bands_per_rank row bands."""
+        check(lib().sgtr_set_refresh_bands(self._h, bands_per_rank))
+
     def comm_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         check(lib().sgtr_comm_init(self._h, buf, nranks, rank))

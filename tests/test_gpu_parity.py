@@ -539,3 +539,27 @@ def test_checkpoint_resume_is_bitwise(sp, orc, tmp_path):
         assert np.array_equal(u, v)
     for u, v in zip(a.state_get_adam(), b.state_get_adam()):
         assert np.array_equal(u, v)
+
+
+@pytest.mark.parametrize("bands", [2, 4])
+def test_refresh_bands_sum_to_the_view(sp, orc, bands):
+    # a refresh view split into row bands (one per rank, with a
+    # one-tile halo for the 11x11 SSIM chain) must give the unsplit view's
+    # Hutchinson sum; on one GPU the bands run back to back
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=600, init_splats=600, views=4,
+                                            image_size=96, seed=21))
+    views = cams_of(sp, ds.cams, ds.gts)
+    out = []
+    for b in (1, bands):
+        c = sp.Context()
+        c.set_scene(ds.init_x)
+        c.set_views(views)
+        c.state_reset(3)
+        c.set_refresh_bands(b)
+        c.step(_tr_opts(sp, 10, batch_size=2, hutch_samples=2))  # t = 1 refreshes
+        out.append((c.state_get(), c.get_scene()))
+    (g1, d1, _), x1 = out[0]
+    (g2, d2, _), x2 = out[1]
+    assert np.array_equal(g1, g2)          # the gradient phase is not banded
+    assert rel(d2, d1) < 1e-12             # only the summation order differs
+    assert rel(x2, x1) < 1e-12
