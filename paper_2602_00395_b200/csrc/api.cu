@@ -349,6 +349,25 @@ struct Ctx {
     Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, tbox;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
+    // second view lane (stream + per-view workspace), swapped in by use_lane
+    // so consecutive gradient views overlap: one view's projection, sorts,
+    // binning and SSIM run beside the other's raster passes
+    struct Lane {
+        cudaStream_t st = nullptr;
+        DevStatus* dstat = nullptr;
+        DevStatus* hstat = nullptr;
+#define SGTR_LANE_BUFS(X)                                                                    \
+    X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
+    X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp) X(slots)    \
+    X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
+    X(part) X(mask) X(tmask) X(large) X(tbox)
+#define SGTR_DECL(n) Buf n;
+        SGTR_LANE_BUFS(SGTR_DECL)
+#undef SGTR_DECL
+    } spare;
+    int cur_lane = 0;
+    Buf gacc1;                   // lane 1's gradient accumulator
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double* htail = nullptr;     // pinned staging for the fused tail
     size_t htail_n = 0;
     int nranks = 1, rank = 0;
@@ -357,10 +376,15 @@ struct Ctx {
 
     ~Ctx() {
         prefetch.reset();
-        if (dstat) cudaFree(dstat);
-        if (hstat) cudaFreeHost(hstat);
+        for (DevStatus* d : {dstat, spare.dstat})
+            if (d) cudaFree(d);
+        for (DevStatus* h : {hstat, spare.hstat})
+            if (h) cudaFreeHost(h);
         if (htail) cudaFreeHost(htail);
-        if (st) cudaStreamDestroy(st);
+        for (cudaEvent_t e : {ev_fork, ev_join})
+            if (e) cudaEventDestroy(e);
+        for (cudaStream_t s : {st, spare.st})
+            if (s) cudaStreamDestroy(s);
     }
     long long dim() const { return 14LL * K; }
     double* X() const { return x.get<double>(); }
@@ -378,6 +402,25 @@ struct ViewRender {
 };
 
 void bind(Ctx& c) { SGTR_CUDA(cudaSetDevice(c.device)); }
+
+// make lane L the context's current stream + per-view workspace
+void use_lane(Ctx& c, int L) {
+    if (L == c.cur_lane) return;
+    std::swap(c.st, c.spare.st);
+    std::swap(c.dstat, c.spare.dstat);
+    std::swap(c.hstat, c.spare.hstat);
+#define SGTR_SWAP(n)                     \
+    std::swap(c.n.p, c.spare.n.p);       \
+    std::swap(c.n.bytes, c.spare.n.bytes);
+    SGTR_LANE_BUFS(SGTR_SWAP)
+#undef SGTR_SWAP
+    c.cur_lane = L;
+}
+
+int lanes_knob() {
+    const char* v = getenv("SGTR_LANES");
+    return v ? std::max(1, std::min(2, atoi(v))) : 2;  // (1 disables the overlap)
+}
 
 struct Timed {
     Ctx& c;
@@ -666,8 +709,28 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     std::vector<double> herr(2 * (n1 + n2), 0.0);
     bool local_error = false;
     // gradient phase: stochastic_gradient (optimizer.cpp:36-65), views of S1
-    // split round-robin over ranks (sgtr_shard_views)
-    for (int p = c.rank; p < n1 && !local_error; p += c.nranks) {
+    // split round-robin over ranks (sgtr_shard_views).  The local views
+    // alternate between two lanes (streams with their own workspace); lane 1
+    // accumulates into its own buffer, added to lane 0's after the join, so
+    // the sum order is fixed.
+    struct LaneReset {  // an exception mid-loop must not leave lane 1 current
+        Ctx& c;
+        ~LaneReset() { use_lane(c, 0); }
+    } lane_reset{c};
+    int n_local = 0;
+    for (int p = c.rank; p < n1; p += c.nranks) ++n_local;
+    const int lanes = (n_local > 1) ? lanes_knob() : 1;
+    double* gacc1 = nullptr;
+    if (lanes == 2) {
+        gacc1 = c.gacc1.as<double>(std::max<long long>(dim, 1));
+        SGTR_CUDA(cudaEventRecord(c.ev_fork, c.st));
+        SGTR_CUDA(cudaStreamWaitEvent(c.spare.st, c.ev_fork, 0));
+        SGTR_CUDA(cudaMemsetAsync(gacc1, 0, sizeof(double) * dim, c.spare.st));
+    }
+    int li = 0;
+    for (int p = c.rank; p < n1 && !local_error; p += c.nranks, ++li) {
+        const int L = li % lanes;
+        use_lane(c, L);
         const View& v = c.views[s1[p]];
         const ViewRender vr = render_view(c, v.dc, ro, false);
         if (vr.err_kind) {
@@ -678,7 +741,15 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         }
         residual_adjoint(c, GRAD, W, H, view_gt(c, s1[p]), nullptr, nullptr, o.residual.lambda,
                          o.residual.floor, loss + p);
-        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, g_acc, gflag + p);
+        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, L == 0 ? g_acc : gacc1, gflag + p);
+    }
+    if (lanes == 2) {
+        use_lane(c, 1);
+        SGTR_CUDA(cudaEventRecord(c.ev_join, c.st));
+        use_lane(c, 0);
+        SGTR_CUDA(cudaStreamWaitEvent(c.st, c.ev_join, 0));
+        launch_add(c.st, g_acc, gacc1, dim);
+        c.launches += 1;
     }
     // Hutchinson phase (optimizer.cpp:75-104), views of S2 split over ranks
     if (refresh && !local_error) {
@@ -948,6 +1019,11 @@ int sgtr_create(int device, sgtr_ctx** out) {
             SGTR_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
             SGTR_CUDA(cudaMalloc(&c->dstat, sizeof(DevStatus)));
             SGTR_CUDA(cudaMallocHost(&c->hstat, sizeof(DevStatus)));
+            SGTR_CUDA(cudaStreamCreateWithFlags(&c->spare.st, cudaStreamNonBlocking));
+            SGTR_CUDA(cudaMalloc(&c->spare.dstat, sizeof(DevStatus)));
+            SGTR_CUDA(cudaMallocHost(&c->spare.hstat, sizeof(DevStatus)));
+            SGTR_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+            SGTR_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         } catch (...) {
             delete c;
             throw;

@@ -185,6 +185,7 @@ void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, do
 void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
                       const double caps[5], double* eta);
 void launch_scale(cudaStream_t st, double* v, long long n, double s);
+void launch_add(cudaStream_t st, double* dst, const double* src, long long n);
 // io.cu
 struct PlyHeader {
     long long count;

@@ -41,9 +41,11 @@ struct PixelCtx {
 };
 
 // warp w covers columns (w & 1) * 8 .. +7 and rows (w >> 1) * 4 .. +3
-__device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H) {
+__device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H,
+                                              int warp = -1) {
     PixelCtx p;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp < 0) warp = threadIdx.x >> 5;
     const int x0 = (tile % tiles_x) * kTile + (warp & 1) * 8;
     const int y0 = (tile / tiles_x) * kTile + (warp >> 1) * 4;
     p.px = x0 + (lane & 7);
@@ -205,21 +207,27 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
 // with the same per-pixel operation sequence as k_raster_fwd.  The warp stops
 // once all its pixels terminated.
 constexpr int kChunkF = 256;
-__global__ void __launch_bounds__(kThreads)
+// WPB warps per CTA: a tile's 8 warps are spread over 8 / WPB CTAs, so a CTA
+// retires as soon as its own warps finish (warps of one tile end at very
+// different list positions)
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB)
     k_raster_fwd_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       double* __restrict__ img, double* __restrict__ tfinal,
                       int* __restrict__ last) {
-    __shared__ int s_list[kWarps][kChunkF];
-    __shared__ int s_ids[kWarps][kChunkF];
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    constexpr int SUB = kWarps / WPB;
+    __shared__ int s_list[WPB][kChunkF];
+    __shared__ int s_ids[WPB][kChunkF];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
     double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
     bool done = !pc.inside;
     int processed = end - start;
-    int* my_list = s_list[warp];
-    int* my_ids = s_ids[warp];
+    int* my_list = s_list[lw];
+    int* my_ids = s_ids[lw];
     for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
         if (__all_sync(kFull, done)) break;
         const int cend = min(end, cbeg + kChunkF);
@@ -635,18 +643,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
 // stores them in its own partial slot (tile-sorted position j, warp w),
 // flagging mask[j * 8 + w]; K11 sums the flagged partials of each duplicate in
 // warp order (deterministic, no atomics).
-template <int kMinBlocks, bool kSmemRed, bool kPrefetch>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
+template <int kMinBlocks, bool kSmemRed, bool kPrefetch, int WPB = kWarps>
+__global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
     k_raster_vjp_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       const double* __restrict__ adj, const double* __restrict__ tfinal,
                       const int* __restrict__ last, double* __restrict__ part,
                       unsigned char* __restrict__ mask) {
-    __shared__ double s_red[kWarps][kRedScratch];
-    __shared__ int s_list[kWarps][kChunk];
-    __shared__ int s_ids[kWarps][kChunk];
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
+    constexpr int SUB = kWarps / WPB;
+    __shared__ double s_red[WPB][kRedScratch];
+    __shared__ int s_list[WPB][kChunk];
+    __shared__ int s_ids[WPB][kChunk];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
     const int start = tl.tile_start[tile];
     const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
     double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
@@ -667,8 +677,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     // outward-rounded float bbox, ballot-compacted into this warp's shared
     // list), so the sequential pass only visits entries that can touch the
     // warp's 8x4 pixels.
-    int* my_list = s_list[warp];
-    int* my_ids = s_ids[warp];
+    int* my_list = s_list[lw];
+    int* my_ids = s_ids[lw];
     for (int cend = start + wlast; cend > start; cend -= kChunk) {
     const int cbeg = max(start, cend - kChunk);
     int nl = 0;
@@ -760,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
         if (!__any_sync(kFull, contrib)) continue;
         double* o = part + ((long long)j * kWarps + warp) * kAdj;
         if (kSmemRed) {
-            warp_reduce9_smem(g, lane, s_red[warp], o);
+            warp_reduce9_smem(g, lane, s_red[lw], o);
         } else {
             double v, v8;
             warp_reduce9(g, lane, v, v8);
@@ -957,6 +967,9 @@ const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
 const int g_fwd_warp = knob("SGTR_FWD_WARP", 1);
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
+// warps per CTA of the warp-filtered forward / VJP kernels
+const int g_fwd_wpb = knob("SGTR_FWD_WPB", 2);
+const int g_wpb = knob("SGTR_WPB", 8);
 
 }  // namespace
 
@@ -968,8 +981,14 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp)
-        k_raster_fwd_warp<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    else if (g_fwd_warp) {
+        if (g_fwd_wpb == 2)
+            k_raster_fwd_warp<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+        else if (g_fwd_wpb == 4)
+            k_raster_fwd_warp<4><<<n * 2, 128, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+        else
+            k_raster_fwd_warp<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    }
     else if (g_fwd_ppl == 4)
         k_raster_fwd_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_ppl == 2)
@@ -1017,6 +1036,12 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
     else if (g_vjp_prefetch == 3)
         k_raster_vjp_warp<3, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
                                                                  last, part, mask);
+    else if (g_smem_red && g_wpb == 2)
+        k_raster_vjp_warp<3, true, false, 2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj,
+                                                                    tfinal, last, part, mask);
+    else if (g_smem_red && g_wpb == 4)
+        k_raster_vjp_warp<3, true, false, 4><<<n * 2, 128, 0, st>>>(tl, rec, W, H, ro, adj,
+                                                                     tfinal, last, part, mask);
     else if (g_smem_red)
         k_raster_vjp_warp<3, true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
                                                                   last, part, mask);

@@ -494,6 +494,11 @@ __global__ void k_scale(double* v, long long n, double s) {
     if (i < n) v[i] = v[i] * s;
 }
 
+__global__ void k_add(double* __restrict__ dst, const double* __restrict__ src, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = dst[i] + src[i];
+}
+
 __global__ void k_fill_int(int* p, long long n, int v) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -543,6 +548,12 @@ void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps, const
 void launch_scale(cudaStream_t st, double* v, long long n, double s) {
     if (n == 0) return;
     k_scale<<<ceil_div(n, 256), 256, 0, st>>>(v, n, s);
+    SGTR_CUDA(cudaGetLastError());
+}
+
+void launch_add(cudaStream_t st, double* dst, const double* src, long long n) {
+    if (n == 0) return;
+    k_add<<<ceil_div(n, 256), 256, 0, st>>>(dst, src, n);
     SGTR_CUDA(cudaGetLastError());
 }
 
