@@ -566,10 +566,15 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
             c.launches += 3;
             return;
         }
+        // SGTR_CHAIN_MODE=2: separate partial-sum kernel (K11a) before the
+        // chain (measured slower than the fused form, kept as an option)
+        double* adj9 = chain_mode() == 2
+                           ? c.slots.as<double>((size_t)kAdj * std::max(vr.n_visible, 1))
+                           : nullptr;
         launch_chain_warp(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                           c.off_r.get<long long>(), c.tcount.get<int>(), c.inv.get<int>(), part,
-                          mask, zdense, zbits, acc, flag);
-        c.launches += 2;
+                          mask, zdense, zbits, acc, flag, adj9);
+        c.launches += adj9 ? 3 : 2;
         return;
     }
     double* slots = c.slots.as<double>((size_t)kAdj * nd);

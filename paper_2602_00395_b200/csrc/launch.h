@@ -96,7 +96,8 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const 
                        const RenderP& ro, const int* sorted_ids, int n_visible,
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag);
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag,
+                       double* adj9 = nullptr);  // adj9 (9 x n_visible): split K11a/K11b
 // per-warp partials of the barrier-free K10 -> per-duplicate slots (warp order)
 void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
                               const double* part, const unsigned char* mask, double* slots);

@@ -237,6 +237,45 @@ __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restric
 // the fixed-order sum of its (tile, fragment) slots; the transpose of the 5x10
 // Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
 // reference evaluates with 10 dual seeds, is applied in one reverse sweep.
+// K11a: per visible splat (depth rank r), the sum over its duplicates (in
+// K4 order) of the per-warp partials flagged in mask (warp order), stored
+// component-major adj9[c * n_visible + r].  Few registers and no FP64 math,
+// so enough warps are resident to hide the scattered partial loads.
+__global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ sorted_ids,
+                                                      int n_visible,
+                                                      const long long* __restrict__ off_r,
+                                                      const int* __restrict__ tcount,
+                                                      const int* __restrict__ inv,
+                                                      const double* __restrict__ part,
+                                                      const unsigned char* __restrict__ mask,
+                                                      double* __restrict__ adj9) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_visible) return;
+    const int cnt = tcount[sorted_ids[r]];
+    double a[kAdj];
+#pragma unroll
+    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
+    const long long off = off_r[r];
+    for (int t = 0; t < cnt; ++t) {
+        const long long jpos = inv[off + t];
+        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * jpos);
+        if (m == 0ull) continue;
+        const double* pp = part + jpos * 8 * kAdj;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            if ((m >> (8 * w)) & 0xffull) {
+#pragma unroll
+                for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < kAdj; ++c) adj9[(long long)c * n_visible + r] = a[c];
+}
+
+// K11b: the chain of each visible splat from its summed adjoints
+// (kPre) or, without kPre, summing the partials itself (one kernel)
+template <bool kPre>
 __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
@@ -247,6 +286,7 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
                                                const unsigned char* __restrict__ mask,
                                                const double* __restrict__ zdense,
                                                const uint32_t* __restrict__ zbits,
+                                               const double* __restrict__ adj9,
                                                double* __restrict__ acc,
                                                double* nonfinite_flag) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -256,10 +296,10 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     if (cnt == 0) return;
     double a[kAdj];
 #pragma unroll
-    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
+    for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
     // the <= 8 per-warp partials of each duplicate, in warp order
     const long long off = off_r[r];
-    for (int t = 0; t < cnt; ++t) {
+    for (int t = 0; t < (kPre ? 0 : cnt); ++t) {
         const long long jpos = inv[off + t];
         const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * jpos);
         if (m == 0ull) continue;
@@ -363,12 +403,21 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const 
                        const RenderP& ro, const int* sorted_ids, int n_visible,
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag) {
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag,
+                       double* adj9) {
     if (n_visible == 0) return;
-    k_chain_warp<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, cam, ro, sorted_ids,
-                                                            n_visible, off_r, tcount, inv, part,
-                                                            mask, zdense, zbits, acc,
-                                                            nonfinite_flag);
+    if (adj9) {
+        k_sum_adjoints<<<ceil_div(n_visible, 256), 256, 0, st>>>(sorted_ids, n_visible, off_r,
+                                                                  tcount, inv, part, mask, adj9);
+        SGTR_CUDA(cudaGetLastError());
+        k_chain_warp<true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+            mode, x, K, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
+            zbits, adj9, acc, nonfinite_flag);
+    } else {
+        k_chain_warp<false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+            mode, x, K, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
+            zbits, nullptr, acc, nonfinite_flag);
+    }
     SGTR_CUDA(cudaGetLastError());
 }
 
