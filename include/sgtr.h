@@ -103,6 +103,16 @@ int64_t sgtr_launch_count(const sgtr_ctx* ctx);
 int sgtr_set_scene(sgtr_ctx* ctx, const double* x, int64_t n_splats);
 int sgtr_get_scene(sgtr_ctx* ctx, double* x);
 int64_t sgtr_scene_size(const sgtr_ctx* ctx);
+/* SH colour extension (parity unpinned; the reference is degree 0):
+ * x = [the 14 reference groups | SH group], the SH group splat-major with
+ * 3 * ((d+1)^2 - 1) coefficients per splat (basis j major, rgb minor);
+ * c_view = c + sum_j Y_j(normalize(mu - camera centre)) k_j (3DGS real-SH
+ * basis, DC = the reference's linear RGB, no offset, no clamp).  Trust-region
+ * radius of k_j = the splat's colour radius / max|Y_j|; ADAM rate lr_color/20.
+ * sgtr_set_scene is sgtr_set_scene_sh with degree 0. */
+int sgtr_set_scene_sh(sgtr_ctx* ctx, const double* x, int64_t n_splats,
+                      int32_t sh_degree);
+int32_t sgtr_scene_sh_degree(const sgtr_ctx* ctx);
 
 /* ------------------------------------------------------------ views */
 /* the training views passed to step_3dgs2tr (optimizer.hpp:129-131);
@@ -302,6 +312,10 @@ typedef struct sgtr_synth_config {
     uint64_t seed;
     double sigma_init, init_scale, init_opacity, camera_radius, camera_height,
         focal_factor, size_scale;
+    /* SH colour extension: degree 0..3; GT coefficients 0.1 N(0,1) from a
+     * separate stream (seed + 0x5348), init coefficients 0; x vectors are
+     * (14 + 3 ((d+1)^2 - 1)) * K long */
+    int32_t sh_degree, pad2;
 } sgtr_synth_config;
 int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x,
                         double* init_x, sgtr_camera* cams);

@@ -87,6 +87,11 @@ inline Dual dexp(const Dual& a) {
     return {e, e * a.d};
 }
 inline double dexp(double a) { return std::exp(a); }
+inline Dual dsqrt(const Dual& a) {
+    const double r = std::sqrt(a.v);
+    return {r, a.d / (2.0 * r)};
+}
+inline double dsqrt(double a) { return std::sqrt(a); }
 inline double P(double a) { return a; }
 inline double P(const Dual& a) { return a.v; }
 
@@ -132,17 +137,98 @@ struct Rng {
 };
 
 // ---------------------------------------------------------------- scene view
+// SH extension (parity unpinned: the reference is SH degree 0).
+// Degree d adds nb = (d+1)^2 - 1 real-SH coefficients per colour channel,
+// stored after the reference's 14 groups as one more splat-major group
+// [k_1..k_nb (rgb interleaved) x K]; the view colour is
+//   c_view = c + sum_j Y_j(dir) k_j,  dir = normalize(mu - camera centre),
+// with the DC term the reference's linear RGB (degree 0 is the reference
+// bit for bit), no offset and no clamp.  Set per process with
+// orc_set_sh_degree (test infrastructure).
+int g_sh_nb = 0;
+
 // group-major layout, scene.hpp:37-52
 struct SceneView {
     const double* x;
     int64_t k;
+    int nb = g_sh_nb;
     const double* mu(int64_t i) const { return x + 3 * i; }
     const double* s(int64_t i) const { return x + 3 * k + 3 * i; }
     const double* q(int64_t i) const { return x + 6 * k + 4 * i; }
     double alpha(int64_t i) const { return x[10 * k + i]; }
     const double* c(int64_t i) const { return x + 11 * k + 3 * i; }
-    int64_t dim() const { return 14 * k; }
+    const double* sh(int64_t i) const { return x + 14 * k + 3LL * nb * i; }
+    int64_t sh_off(int64_t i) const { return 14 * k + 3LL * nb * i; }
+    int64_t dim() const { return (14 + 3LL * nb) * k; }
 };
+
+// real SH basis of degrees 1..3 at a unit direction (3DGS constants and
+// sign conventions), and max over the sphere of |Y_j| (numerically
+// maximised; used for the SH trust-region radii)
+const double kShC1 = 0.4886025119029199;
+const double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+                         -1.0925484305920792, 0.5462742152960396};
+const double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+                         0.3731763325901154,  -0.4570457994644658, 1.445305721320277,
+                         -0.5900435899266435};
+const double kShMax[15] = {0.4886025119029199, 0.4886025119029199, 0.4886025119029199,
+                           0.5462742152960397, 0.5462742152960397, 0.6307831305050401,
+                           0.5462742152960397, 0.5462742152960396, 0.5900435899266437,
+                           0.5562984315103788, 0.6293798292550865, 0.7463526651802308,
+                           0.6293798292550866, 0.5562984315103789, 0.5900435899266437};
+
+template <typename T>
+void sh_basis(const T& x, const T& y, const T& z, int nb, T* Y) {
+    if (nb >= 3) {
+        Y[0] = -kShC1 * y;
+        Y[1] = kShC1 * z;
+        Y[2] = -kShC1 * x;
+    }
+    if (nb >= 8) {
+        const T xx = x * x, yy = y * y, zz = z * z;
+        Y[3] = kShC2[0] * (x * y);
+        Y[4] = kShC2[1] * (y * z);
+        Y[5] = kShC2[2] * (2.0 * zz - xx - yy);
+        Y[6] = kShC2[3] * (x * z);
+        Y[7] = kShC2[4] * (xx - yy);
+        if (nb >= 15) {
+            Y[8] = kShC3[0] * y * (3.0 * xx - yy);
+            Y[9] = kShC3[1] * (x * y) * z;
+            Y[10] = kShC3[2] * y * (4.0 * zz - xx - yy);
+            Y[11] = kShC3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            Y[12] = kShC3[4] * x * (4.0 * zz - xx - yy);
+            Y[13] = kShC3[5] * z * (xx - yy);
+            Y[14] = kShC3[6] * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+// unit direction from the camera centre to mu
+template <typename T>
+void sh_dir(const T mu[3], const double cen[3], T d[3]) {
+    const T vx = mu[0] - cen[0], vy = mu[1] - cen[1], vz = mu[2] - cen[2];
+    const T inv = 1.0 / dsqrt(vx * vx + vy * vy + vz * vz);
+    d[0] = vx * inv;
+    d[1] = vy * inv;
+    d[2] = vz * inv;
+}
+
+// c_view = c + sum_j Y_j k_j, the sum accumulated in j order per channel
+template <typename T>
+void sh_color(const T mu[3], const T c[3], const T* k, int nb, const double cen[3], T out[3]) {
+    if (nb == 0) {
+        for (int a = 0; a < 3; ++a) out[a] = c[a];
+        return;
+    }
+    T d[3], Y[15];
+    sh_dir(mu, cen, d);
+    sh_basis(d[0], d[1], d[2], nb, Y);
+    for (int a = 0; a < 3; ++a) {
+        T acc = Y[0] * k[a];
+        for (int j = 1; j < nb; ++j) acc = acc + Y[j] * k[3 * j + a];
+        out[a] = c[a] + acc;
+    }
+}
 
 const char* const kGroup[5] = {"position", "scale", "rotation", "opacity",
                                "color"};
@@ -188,13 +274,16 @@ void covariance(const T s[3], const T q[4], T cov[9]) {
 
 struct Cam {
     orc_camera c;
-    double w[9];  // world->camera rotation, quat_to_rotation(q_wc)
+    double w[9];    // world->camera rotation, quat_to_rotation(q_wc)
+    double cen[3];  // camera centre -W^T t (scene.hpp:80)
 };
 
 Cam make_cam(const orc_camera& c) {
     Cam out;
     out.c = c;
     quat_rot(c.q_wc, out.w);
+    for (int a = 0; a < 3; ++a)
+        out.cen[a] = -(out.w[a] * c.t_wc[0] + out.w[3 + a] * c.t_wc[1] + out.w[6 + a] * c.t_wc[2]);
     return out;
 }
 
@@ -275,6 +364,7 @@ void check_finite(const SceneView& sc) {
             ok = ok && std::isfinite(sc.mu(i)[a]) && std::isfinite(sc.s(i)[a]) &&
                  std::isfinite(sc.c(i)[a]);
         for (int a = 0; a < 4; ++a) ok = ok && std::isfinite(sc.q(i)[a]);
+        for (int a = 0; a < 3 * sc.nb; ++a) ok = ok && std::isfinite(sc.sh(i)[a]);
         if (!ok)
             throw NumericErr("rasterize: non-finite parameter in splat " +
                              std::to_string(i));
@@ -318,8 +408,9 @@ std::vector<Frag<double>> build_frags(const SceneView& sc, const Cam& cam,
     fr.reserve(sc.k);
     for (int64_t i = 0; i < sc.k; ++i) {
         Frag<double> f;
-        if (make_frag<double>(i, sc.mu(i), sc.s(i), sc.q(i), sc.alpha(i),
-                              sc.c(i), cam, o, f))
+        double col[3];
+        sh_color<double>(sc.mu(i), sc.c(i), sc.sh(i), sc.nb, cam.cen, col);
+        if (make_frag<double>(i, sc.mu(i), sc.s(i), sc.q(i), sc.alpha(i), col, cam, o, f))
             fr.push_back(f);
     }
     sort_frags(fr);
@@ -341,8 +432,11 @@ std::vector<Frag<Dual>> build_frags_dual(const SceneView& sc, const Cam& cam,
         }
         for (int a = 0; a < 4; ++a) q[a] = Dual(sc.q(i)[a], v[6 * k + 4 * i + a]);
         const Dual alpha(sc.alpha(i), v[10 * k + i]);
+        Dual shk[45], vcol[3];
+        for (int a = 0; a < 3 * sc.nb; ++a) shk[a] = Dual(sc.sh(i)[a], v[sc.sh_off(i) + a]);
+        sh_color<Dual>(mu, col, shk, sc.nb, cam.cen, vcol);
         Frag<Dual> f;
-        if (make_frag<Dual>(i, mu, s, q, alpha, col, cam, o, f)) fr.push_back(f);
+        if (make_frag<Dual>(i, mu, s, q, alpha, vcol, cam, o, f)) fr.push_back(f);
     }
     sort_frags(fr);
     return fr;
@@ -510,6 +604,24 @@ void chain_splat(const SceneView& sc, const Cam& cam, const orc_render_opts& o,
     const int64_t k = sc.k;
     grad[10 * k + i] += a[5];
     for (int ch = 0; ch < 3; ++ch) grad[11 * k + 3 * i + ch] += a[6 + ch];
+    if (sc.nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0)) {
+        // SH extension: dL/dk_j = Y_j a_rgb, and the colour's dependence on
+        // mu through the view direction (3 dual seeds)
+        double d[3], Y[15];
+        sh_dir<double>(sc.mu(i), cam.cen, d);
+        sh_basis<double>(d[0], d[1], d[2], sc.nb, Y);
+        for (int j = 0; j < sc.nb; ++j)
+            for (int ch = 0; ch < 3; ++ch) grad[sc.sh_off(i) + 3 * j + ch] += Y[j] * a[6 + ch];
+        Dual shk[45], c0[3], col[3];
+        for (int t = 0; t < 3 * sc.nb; ++t) shk[t] = Dual(sc.sh(i)[t]);
+        for (int ch = 0; ch < 3; ++ch) c0[ch] = Dual(sc.c(i)[ch]);
+        for (int seed = 0; seed < 3; ++seed) {
+            Dual mu[3];
+            for (int c = 0; c < 3; ++c) mu[c] = Dual(sc.mu(i)[c], seed == c ? 1.0 : 0.0);
+            sh_color<Dual>(mu, c0, shk, sc.nb, cam.cen, col);
+            grad[3 * i + seed] += a[6] * col[0].d + a[7] * col[1].d + a[8] * col[2].d;
+        }
+    }
     bool any = false;
     for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
     if (!any) return;
@@ -590,7 +702,7 @@ void rasterize_vjp(const SceneView& sc, const Cam& cam,
         for (size_t t = 0; t < rp.idx.size(); ++t)
             for (int j = 0; j < 9; ++j) adj[9 * rp.idx[t] + j] += rp.val[9 * t + j];
     }
-    std::fill(grad, grad + 14 * k, 0.0);
+    std::fill(grad, grad + sc.dim(), 0.0);
     for (int64_t i = 0; i < k; ++i) chain_splat(sc, cam, o, i, adj.data() + 9 * i, grad);
 }
 
@@ -1116,6 +1228,11 @@ void shd_radii(const SceneView& sc, double eps, const double caps[5], double* et
         }
         for (int c = 0; c < 4; ++c) eta[6 * k + 4 * i + c] = rq[c];
         eta[10 * k + i] = cap_radius(std::sqrt(4.0 * p.alpha * eps), caps[3]);
+        // SH extension: a single-coefficient step moves the view colour by
+        // at most the reference's colour radius in any direction
+        for (int j = 0; j < sc.nb; ++j)
+            for (int c = 0; c < 3; ++c)
+                eta[sc.sh_off(i) + 3 * j + c] = eta[11 * k + 3 * i + c] / kShMax[j];
     }
 }
 
@@ -1156,7 +1273,7 @@ void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opt
 void step_tr(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
              const std::vector<int>* s1_in, const std::vector<int>* s2_in,
              const double* probes_in, orc_diag* diag, double* applied) {
-    const int64_t k = pb.sc.k, dim = 14 * k;
+    const int64_t k = pb.sc.k, dim = pb.sc.dim();
     orc_diag dg{0, 0, 0, 0, -1, -1, 0};
     st->t += 1;
     const int mv = static_cast<int>(pb.cams.size());
@@ -1206,7 +1323,7 @@ void clamp_scene(double* x, int64_t k, const orc_tr_opts& o) {
 // apply_clipped, optimizer.cpp:124-142
 void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
                    const std::vector<double>& dx, orc_diag& dg, double* applied) {
-    const int64_t k = pb.sc.k, dim = 14 * k;
+    const int64_t k = pb.sc.k, dim = pb.sc.dim();
     const double eps = eps_at(o.eps_start, o.eps_end, o.total_steps, (int)st->t);
     const double caps[5] = {o.cap_mean, o.cap_scale, o.cap_rotation, o.cap_opacity,
                             o.cap_color};
@@ -1235,7 +1352,7 @@ void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opt
 // apply_unclipped, optimizer.cpp:145-151
 void apply_unclipped(double* x, int64_t k, const orc_tr_opts& o, const std::vector<double>& dx,
                      orc_diag& dg, double* applied) {
-    const int64_t dim = 14 * k;
+    const int64_t dim = (14 + 3LL * g_sh_nb) * k;
     for (int64_t i = 0; i < dim; ++i)
         if (!std::isfinite(dx[i]))
             throw NumericErr(std::string("non-finite update in group ") + kGroup[group_of(k, i)]);
@@ -1250,7 +1367,7 @@ void apply_unclipped(double* x, int64_t k, const orc_tr_opts& o, const std::vect
 // geometrically over lr_position_decay_steps
 std::vector<double> adam_direction(orc_state* st, int64_t k, const std::vector<double>& g,
                                    const orc_adam_opts& a) {
-    const int64_t dim = 14 * k;
+    const int64_t dim = (14 + 3LL * g_sh_nb) * k;
     for (int64_t i = 0; i < dim; ++i) {
         st->adam_m[i] = a.beta1 * st->adam_m[i] + (1.0 - a.beta1) * g[i];
         st->adam_v[i] = a.beta2 * st->adam_v[i] + (1.0 - a.beta2) * (g[i] * g[i]);
@@ -1264,7 +1381,9 @@ std::vector<double> adam_direction(orc_state* st, int64_t k, const std::vector<d
     const double lrs[5] = {lr_pos, a.lr_scale, a.lr_rotation, a.lr_opacity, a.lr_color};
     std::vector<double> dx(dim);
     for (int64_t i = 0; i < dim; ++i) {
-        const double lr = lrs[group_of(k, i)];
+        // SH coefficients (extension) at the colour rate / 20 (3DGS's
+        // feature_rest convention)
+        const double lr = i >= 14 * k ? a.lr_color / 20.0 : lrs[group_of(k, i)];
         const double mhat = st->adam_m[i] / c1;
         const double vhat = st->adam_v[i] / c2;
         dx[i] = -lr * mhat / (std::sqrt(vhat) + a.eps);
@@ -1394,6 +1513,12 @@ extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
 
+int orc_set_sh_degree(int32_t degree) {
+    if (degree < 0 || degree > 3) return 1;
+    g_sh_nb = (degree + 1) * (degree + 1) - 1;
+    return 0;
+}
+
 int orc_rasterize(const double* x, int64_t k, const orc_camera* cam,
                   const orc_render_opts* ro, int workers, double* color,
                   double* t_final) {
@@ -1404,7 +1529,8 @@ int orc_rasterize_jvp(const double* x, int64_t k, const orc_camera* cam,
                       const orc_render_opts* ro, int workers, const double* v,
                       int64_t v_len, double* tangent) {
     return guarded([&] {
-        if (v_len != 14 * k) throw InvalidArg("rasterize_jvp: direction length mismatch");
+        if (v_len != (14 + 3LL * g_sh_nb) * k)
+            throw InvalidArg("rasterize_jvp: direction length mismatch");
         rasterize_jvp({x, k}, make_cam(*cam), *ro, workers, v, tangent);
     });
 }
@@ -1665,7 +1791,7 @@ int orc_hutchinson_diag(const double* x, int64_t k, const orc_camera* cams,
     return guarded([&] {
         const Problem pb = make_problem(x, k, cams, gts, n_views, rs, ro, workers);
         const std::vector<int> b(batch, batch + n_batch);
-        const int64_t dim = 14 * k;
+        const int64_t dim = (14 + 3LL * g_sh_nb) * k;
         const auto r = hutchinson_diag(pb, b, nu, [&](int s) {
             return std::vector<double>(probes + s * dim, probes + (s + 1) * dim);
         });
@@ -1702,7 +1828,7 @@ int orc_exact_gn_diagonal(const double* x, int64_t k, const orc_camera* cams,
                           int workers, double* d) {
     return guarded([&] {  // checks.cpp:127-141
         const Problem pb = make_problem(x, k, cams, gts, n_views, rs, ro, workers);
-        const int64_t dim = 14 * k;
+        const int64_t dim = (14 + 3LL * g_sh_nb) * k;
         const long m = 6L * pb.W() * pb.H() * n_views;
         std::vector<double> e(dim, 0.0);
         for (int64_t j = 0; j < dim; ++j) {
@@ -1890,6 +2016,14 @@ int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro, int 
             for (int a = 0; a < 3; ++a) p.c[a] = 0.5;
             set_prim(init_x, ki, i, p);
         }
+        if ((cfg->sh_degree + 1) * (cfg->sh_degree + 1) - 1 != g_sh_nb)
+            throw InvalidArg("make_synthetic: sh_degree differs from orc_set_sh_degree");
+        if (g_sh_nb > 0) {
+            Rng rs(cfg->seed + 0x5348ULL);
+            const int64_t nsh = 3LL * g_sh_nb;
+            for (int64_t t = 0; t < nsh * kg; ++t) gt_x[14 * kg + t] = 0.1 * rs.normal();
+            for (int64_t t = 0; t < nsh * ki; ++t) init_x[14 * ki + t] = 0.0;
+        }
         const double focal = cfg->focal_factor * H;
         const int64_t n = 3LL * W * H;
         std::vector<double> img(n);
@@ -1951,7 +2085,9 @@ int orc_make_check_scene(int32_t splats, int32_t image_size, int32_t n_views,
                 c.id = v;
                 cams[v] = c;
                 const Cam cc = make_cam(c);
-                if (gts) rasterize({tx.data(), splats}, cc, kDefaultRender, 0, gts[v], nullptr);
+                // the check scenes are degree-0 scenes whatever orc_set_sh_degree says
+                if (gts)
+                    rasterize({tx.data(), splats, 0}, cc, kDefaultRender, 0, gts[v], nullptr);
                 std::vector<double> depths;
                 for (const Prim& p : sc)
                     depths.push_back(cc.w[6] * p.mu[0] + cc.w[7] * p.mu[1] +

@@ -73,6 +73,11 @@ typedef struct orc_diag {
 
 const char* orc_last_error(void);
 
+/* SH colour extension (parity unpinned; degree 0 = the reference): scene
+ * vectors become (14 + 3 * ((d+1)^2 - 1)) * K long, the SH block appended
+ * after the reference's groups.  Process-wide setting. */
+int orc_set_sh_degree(int32_t degree);
+
 /* --- renderer (render.cpp:155-331) --- */
 int orc_rasterize(const double* x, int64_t k, const orc_camera* cam,
                   const orc_render_opts* ro, int workers, double* color,
@@ -221,6 +226,9 @@ typedef struct orc_synth_cfg {
      * GT scale range, init_scale and sigma_init multiplied by size_scale */
     int32_t width, height;
     double size_scale;
+    /* SH colour extension: GT coefficients 0.1 N(0,1) from a separate
+     * stream (seed + 0x5348), init 0; must equal orc_set_sh_degree's */
+    int32_t sh_degree, pad2;
 } orc_synth_cfg;
 /* gt_x[14*gt], init_x[14*init], cams[views], gts[views][H*W*3] */
 int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro,

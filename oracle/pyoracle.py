@@ -87,7 +87,7 @@ class SynthCfg(C.Structure):
                 ("init_scale", C.c_double), ("init_opacity", C.c_double),
                 ("camera_radius", C.c_double), ("camera_height", C.c_double),
                 ("focal_factor", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
-                ("size_scale", C.c_double)]
+                ("size_scale", C.c_double), ("sh_degree", C.c_int32), ("pad2", C.c_int32)]
 
 
 def build(force: bool = False) -> str:
@@ -134,6 +134,26 @@ def _check(rc):
 
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# SH colour extension (parity unpinned; degree 0 = the reference): the
+# process-wide degree of the oracle, mirrored here for the vector lengths
+_SH_NB = 0
+
+
+def set_sh_degree(degree: int) -> None:
+    global _SH_NB
+    if lib().orc_set_sh_degree(int(degree)) != 0:
+        raise OracleInvalidArgument("sh degree must be in 0..3")
+    _SH_NB = (degree + 1) ** 2 - 1
+
+
+def params_per_splat() -> int:
+    return 14 + 3 * _SH_NB
+
+
+def _k(x):
+    return x.size // params_per_splat()
 
 
 # --------------------------------------------------------------- options
@@ -228,7 +248,7 @@ def rasterize(x, cam, ro=None):
     x = _f64(x)
     col = np.empty((cam.height, cam.width, 3))
     t = np.empty((cam.height, cam.width))
-    _check(lib().orc_rasterize(_p(x), C.c_int64(x.size // 14), C.byref(cam), C.byref(ro.c()),
+    _check(lib().orc_rasterize(_p(x), C.c_int64(_k(x)), C.byref(cam), C.byref(ro.c()),
                                ro.workers, _p(col), _p(t)))
     return col, t
 
@@ -237,7 +257,7 @@ def rasterize_jvp(x, cam, v, ro=None):
     ro = ro or RenderOptions()
     x, v = _f64(x), _f64(v)
     out = np.empty((cam.height, cam.width, 3))
-    _check(lib().orc_rasterize_jvp(_p(x), C.c_int64(x.size // 14), C.byref(cam),
+    _check(lib().orc_rasterize_jvp(_p(x), C.c_int64(_k(x)), C.byref(cam),
                                    C.byref(ro.c()), ro.workers, _p(v), C.c_int64(v.size),
                                    _p(out)))
     return out
@@ -247,7 +267,7 @@ def rasterize_vjp(x, cam, adjoint, ro=None):
     ro = ro or RenderOptions()
     x, a = _f64(x), _f64(adjoint)
     g = np.empty(x.size)
-    _check(lib().orc_rasterize_vjp(_p(x), C.c_int64(x.size // 14), C.byref(cam),
+    _check(lib().orc_rasterize_vjp(_p(x), C.c_int64(_k(x)), C.byref(cam),
                                    C.byref(ro.c()), ro.workers, _p(a), a.shape[1],
                                    a.shape[0], _p(g)))
     return g
@@ -257,7 +277,7 @@ def blend_stats(x, cam, ro=None):
     ro = ro or RenderOptions()
     x = _f64(x)
     e, c = C.c_int64(), C.c_int64()
-    _check(lib().orc_blend_stats(_p(x), C.c_int64(x.size // 14), C.byref(cam),
+    _check(lib().orc_blend_stats(_p(x), C.c_int64(_k(x)), C.byref(cam),
                                  C.byref(ro.c()), ro.workers, C.byref(e), C.byref(c)))
     return e.value, c.value
 
@@ -265,7 +285,7 @@ def blend_stats(x, cam, ro=None):
 def project(x, cam, ro=None):
     ro = ro or RenderOptions()
     x = _f64(x)
-    k = x.size // 14
+    k = _k(x)
     out = np.empty((k, 12))
     _check(lib().orc_project(_p(x), C.c_int64(k), C.byref(cam), C.byref(ro.c()), _p(out)))
     return out
@@ -275,7 +295,7 @@ def binning(x, cam, tile=16, ro=None):
     """Returns (order, tile_start, tile_end, lists) of the restated binning."""
     ro = ro or RenderOptions()
     x = _f64(x)
-    k = x.size // 14
+    k = _k(x)
     nv, nd = C.c_int32(), C.c_int64()
     L = lib()
     _check(L.orc_binning(_p(x), C.c_int64(k), C.byref(cam), C.byref(ro.c()), tile,
@@ -362,7 +382,7 @@ def view_jacobian_apply(x, cam, gt, v, rs=None, ro=None):
     rs, ro = rs or ResidualOptions(), ro or RenderOptions()
     x, gt, v = _f64(x), _f64(gt), _f64(v)
     out = np.empty(2 * gt.size)
-    _check(lib().orc_view_jacobian_apply(_p(x), C.c_int64(x.size // 14), C.byref(cam),
+    _check(lib().orc_view_jacobian_apply(_p(x), C.c_int64(_k(x)), C.byref(cam),
                                          _p(gt), _p(v), C.byref(rs.c()), C.byref(ro.c()),
                                          ro.workers, _p(out)))
     return out
@@ -372,7 +392,7 @@ def view_jacobian_applyT(x, cam, gt, u, rs=None, ro=None):
     rs, ro = rs or ResidualOptions(), ro or RenderOptions()
     x, gt, u = _f64(x), _f64(gt), _f64(u)
     g = np.empty(x.size)
-    _check(lib().orc_view_jacobian_applyT(_p(x), C.c_int64(x.size // 14), C.byref(cam),
+    _check(lib().orc_view_jacobian_applyT(_p(x), C.c_int64(_k(x)), C.byref(cam),
                                           _p(gt), _p(u), C.byref(rs.c()), C.byref(ro.c()),
                                           ro.workers, _p(g)))
     return g
@@ -385,7 +405,7 @@ def stochastic_gradient(x, cams, gts, batch, rs=None, ro=None):
     b = np.ascontiguousarray(batch, dtype=np.int32)
     g = np.empty(x.size)
     loss = C.c_double()
-    _check(lib().orc_stochastic_gradient(_p(x), C.c_int64(x.size // 14), _cams(cams), ptrs,
+    _check(lib().orc_stochastic_gradient(_p(x), C.c_int64(_k(x)), _cams(cams), ptrs,
                                          len(cams), _p(b), b.size, C.byref(rs.c()),
                                          C.byref(ro.c()), ro.workers, _p(g), C.byref(loss)))
     return g, loss.value
@@ -399,7 +419,7 @@ def hutchinson_diag(x, cams, gts, batch, probes, rs=None, ro=None):
     b = np.ascontiguousarray(batch, dtype=np.int32)
     z = _f64(np.atleast_2d(probes))
     d = np.empty(x.size)
-    _check(lib().orc_hutchinson_diag(_p(x), C.c_int64(x.size // 14), _cams(cams), ptrs,
+    _check(lib().orc_hutchinson_diag(_p(x), C.c_int64(_k(x)), _cams(cams), ptrs,
                                      len(cams), _p(b), b.size, z.shape[0], _p(z),
                                      C.byref(rs.c()), C.byref(ro.c()), ro.workers, _p(d)))
     return d
@@ -409,7 +429,7 @@ def objective(x, cams, gts, rs=None, ro=None):
     rs, ro = rs or ResidualOptions(), ro or RenderOptions()
     x = _f64(x)
     keep, ptrs = _gts(gts)
-    return lib().orc_objective(_p(x), C.c_int64(x.size // 14), _cams(cams), ptrs, len(cams),
+    return lib().orc_objective(_p(x), C.c_int64(_k(x)), _cams(cams), ptrs, len(cams),
                                C.byref(rs.c()), C.byref(ro.c()), ro.workers)
 
 
@@ -418,7 +438,7 @@ def exact_gn_diagonal(x, cams, gts, rs=None, ro=None):
     x = _f64(x)
     keep, ptrs = _gts(gts)
     d = np.empty(x.size)
-    _check(lib().orc_exact_gn_diagonal(_p(x), C.c_int64(x.size // 14), _cams(cams), ptrs,
+    _check(lib().orc_exact_gn_diagonal(_p(x), C.c_int64(_k(x)), _cams(cams), ptrs,
                                        len(cams), C.byref(rs.c()), C.byref(ro.c()),
                                        ro.workers, _p(d)))
     return d
@@ -428,7 +448,7 @@ def shd_radii(x, eps, caps=(1.0, 1.0, 1.0, 1.0, 1.0)):
     x = _f64(x)
     c = (C.c_double * 5)(*caps)
     eta = np.empty(x.size)
-    _check(lib().orc_shd_radii(_p(x), C.c_int64(x.size // 14), C.c_double(eps), c, _p(eta)))
+    _check(lib().orc_shd_radii(_p(x), C.c_int64(_k(x)), C.c_double(eps), c, _p(eta)))
     return eta
 
 
@@ -487,7 +507,7 @@ def step_3dgs2tr(state, x, cams, gts, opts, rs=None, ro=None, *, s1=None, s2=Non
     diag = Diag()
     applied = np.empty(x.size) if want_applied else None
     ap = _p(applied) if want_applied else None
-    k = C.c_int64(x.size // 14)
+    k = C.c_int64(_k(x))
     if s1 is None:
         _check(lib().orc_step_3dgs2tr(state._h, _p(x), k, _cams(cams), ptrs, len(cams),
                                       C.byref(opts.c()), C.byref(rs.c()), C.byref(ro.c()),
@@ -560,6 +580,7 @@ class SynthConfig:  # config.hpp:83-95 defaults
     width: int = 0        # 0: image_size (reference); W x H is a declared extension
     height: int = 0
     size_scale: float = 1.0
+    sh_degree: int = 0     # SH colour extension (GT coefficients 0.1 N(0,1), init 0)
 
 
 @dataclass
@@ -574,9 +595,10 @@ def make_synthetic(cfg: SynthConfig, ro=None, with_gt=True) -> Dataset:
     ro = ro or RenderOptions()
     c = SynthCfg(cfg.gt_splats, cfg.init_splats, cfg.views, cfg.image_size, cfg.seed,
                  cfg.sigma_init, cfg.init_scale, cfg.init_opacity, cfg.camera_radius,
-                 cfg.camera_height, cfg.focal_factor, cfg.width, cfg.height, cfg.size_scale)
-    gt_x = np.empty(14 * cfg.gt_splats)
-    init_x = np.empty(14 * cfg.init_splats)
+                 cfg.camera_height, cfg.focal_factor, cfg.width, cfg.height, cfg.size_scale,
+                 cfg.sh_degree)
+    gt_x = np.empty(params_per_splat() * cfg.gt_splats)
+    init_x = np.empty(params_per_splat() * cfg.init_splats)
     cams = (Camera * cfg.views)()
     W, H = cfg.width or cfg.image_size, cfg.height or cfg.image_size
     gts = [np.empty((H, W, 3)) for _ in range(cfg.views)]
@@ -614,7 +636,7 @@ def pack(mu, s, q, alpha, c):
 
 
 def unpack(x):
-    k = x.size // 14
+    k = _k(x)
     return (x[:3 * k].reshape(k, 3), x[3 * k:6 * k].reshape(k, 3),
             x[6 * k:10 * k].reshape(k, 4), x[10 * k:11 * k], x[11 * k:].reshape(k, 3))
 
@@ -629,7 +651,7 @@ def step_adam(state, x, cams, gts, opts, adam, trust_region=False, rs=None, ro=N
     applied = np.empty(x.size) if want_applied else None
     a1 = np.ascontiguousarray(s1 if s1 is not None else [], dtype=np.int32)
     _check(lib().orc_step_adam(
-        state._h, _p(x), C.c_int64(x.size // 14), _cams(cams), ptrs, len(cams),
+        state._h, _p(x), C.c_int64(_k(x)), _cams(cams), ptrs, len(cams),
         C.byref(opts.c()), C.byref(adam.c()), int(bool(trust_region)), C.byref(rs.c()),
         C.byref(ro.c()), ro.workers, _p(a1) if s1 is not None else None, a1.size,
         C.byref(diag), _p(applied) if want_applied else None))

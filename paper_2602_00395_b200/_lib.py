@@ -85,7 +85,7 @@ class SynthConfig(C.Structure):
                 ("seed", C.c_uint64), ("sigma_init", C.c_double), ("init_scale", C.c_double),
                 ("init_opacity", C.c_double), ("camera_radius", C.c_double),
                 ("camera_height", C.c_double), ("focal_factor", C.c_double),
-                ("size_scale", C.c_double)]
+                ("size_scale", C.c_double), ("sh_degree", C.c_int32), ("pad2", C.c_int32)]
 
 
 VP = C.c_void_p
@@ -99,6 +99,8 @@ _SIGS = {
     "sgtr_set_scene": (C.c_int, [VP, VP, C.c_int64]),
     "sgtr_get_scene": (C.c_int, [VP, VP]),
     "sgtr_scene_size": (C.c_int64, [VP]),
+    "sgtr_set_scene_sh": (C.c_int, [VP, VP, C.c_int64, C.c_int32]),
+    "sgtr_scene_sh_degree": (C.c_int32, [VP]),
     "sgtr_set_views": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sgtr_render_targets": (C.c_int, [VP, VP, C.c_int32]),
     "sgtr_get_target": (C.c_int, [VP, C.c_int32, VP]),

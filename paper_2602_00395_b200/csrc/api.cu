@@ -243,6 +243,8 @@ DevCam make_devcam(const sgtr_camera& c) {
     d.cy = c.cy;
     if (!quat_rot(c.q_wc, d.w)) throw invalid("quat_to_rotation: degenerate quaternion");
     for (int i = 0; i < 3; ++i) d.t[i] = c.t_wc[i];
+    for (int a = 0; a < 3; ++a)
+        d.cen[a] = -(d.w[a] * c.t_wc[0] + d.w[3 + a] * c.t_wc[1] + d.w[6 + a] * c.t_wc[2]);
     return d;
 }
 
@@ -386,7 +388,8 @@ struct Ctx {
         for (cudaStream_t s : {st, spare.st})
             if (s) cudaStreamDestroy(s);
     }
-    long long dim() const { return 14LL * K; }
+    int nb = 0;  // SH coefficients per channel beyond DC ((d+1)^2 - 1; extension)
+    long long dim() const { return (14LL + 3LL * nb) * K; }
     double* X() const { return x.get<double>(); }
 };
 
@@ -481,7 +484,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
                               cudaMemcpyHostToDevice, c.st));
     {
         Timed t(c, KC_PROJECT);
-        launch_project(c.st, c.X(), K, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, b.tmask,
+        launch_project(c.st, c.X(), K, c.nb, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, b.tmask,
                        &c.dstat->vs);
     }
     {
@@ -560,7 +563,7 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
         if (chain_mode() == 1) {
             double* slots = c.slots.as<double>((size_t)kAdj * nd);
             launch_partials_to_slots(c.st, vr.tl.sorted_d, vr.n_dup, part, mask, slots);
-            launch_chain(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+            launch_chain(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                          c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits,
                          acc, flag);
             c.launches += 3;
@@ -571,7 +574,7 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
         double* adj9 = chain_mode() == 2
                            ? c.slots.as<double>((size_t)kAdj * std::max(vr.n_visible, 1))
                            : nullptr;
-        launch_chain_warp(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+        launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                           c.off_r.get<long long>(), c.tcount.get<int>(), c.inv.get<int>(), part,
                           mask, zdense, zbits, acc, flag, adj9);
         c.launches += adj9 ? 3 : 2;
@@ -584,7 +587,7 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                           c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(), slots);
     }
     Timed t(c, KC_CHAIN);
-    launch_chain(c.st, mode, c.X(), c.K, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+    launch_chain(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
                  c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits, acc, flag);
     c.launches += 2;
 }
@@ -795,7 +798,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                     double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
                     {
                         Timed t(c, KC_PROJECT_JVP);
-                        launch_project_jvp(c.st, c.X(), c.K, v.dc, ro, nullptr, zb, trec);
+                        launch_project_jvp(c.st, c.X(), c.K, c.nb, v.dc, ro, nullptr, zb, trec);
                     }
                     {
                         Timed t(c, KC_RASTER_JVP);
@@ -868,6 +871,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     }
     TrArgs a{};
     a.kind = kind;
+    a.nb = c.nb;
     if (kind != 0) {
         // adam_direction's scalars (optimizer.cpp:159-169), host std::pow as
         // in the reference
@@ -1063,14 +1067,43 @@ int64_t sgtr_launch_count(const sgtr_ctx* ctx) {
     return ctx ? reinterpret_cast<const Ctx*>(ctx)->launches : 0;
 }
 
+namespace {
+void set_scene_impl(Ctx& c, const double* x, int64_t n_splats, int sh_degree) {
+    bind(c);
+    if (n_splats < 0 || n_splats > (1LL << 28)) throw invalid("sgtr_set_scene: bad splat count");
+    if (sh_degree < 0 || sh_degree > 3) throw invalid("sgtr_set_scene: SH degree must be 0..3");
+    const int nb = (sh_degree + 1) * (sh_degree + 1) - 1;
+    const bool resized = n_splats != c.K || nb != c.nb;
+    c.K = (int)n_splats;
+    c.nb = nb;
+    const long long dim = c.dim();
+    double* d = c.x.as<double>(std::max<long long>(dim, 1));
+    if (dim)
+        SGTR_CUDA(cudaMemcpyAsync(d, x, sizeof(double) * dim, cudaMemcpyHostToDevice, c.st));
+    if (resized) zero_state(c);  // OptimizerState(dim, seed) lives with the dimension
+    SGTR_CUDA(cudaStreamSynchronize(c.st));
+}
+}  // namespace
+
+int sgtr_set_scene_sh(sgtr_ctx* ctx, const double* x, int64_t n_splats, int32_t sh_degree) {
+    return guarded([&] { set_scene_impl(ctx_ref(ctx), x, n_splats, sh_degree); });
+}
+
+int32_t sgtr_scene_sh_degree(const sgtr_ctx* ctx) {
+    if (!ctx) return -1;
+    const int nb = reinterpret_cast<const Ctx*>(ctx)->nb;
+    return nb == 0 ? 0 : nb == 3 ? 1 : nb == 8 ? 2 : 3;
+}
+
 int sgtr_set_scene(sgtr_ctx* ctx, const double* x, int64_t n_splats) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
         bind(c);
         if (n_splats < 0 || n_splats > (1LL << 28)) throw invalid("sgtr_set_scene: bad splat count");
         const long long dim = 14LL * n_splats;
-        const bool resized = n_splats != c.K;
+        const bool resized = n_splats != c.K || c.nb != 0;
         c.K = (int)n_splats;
+        c.nb = 0;
         double* d = c.x.as<double>(std::max<long long>(dim, 1));
         if (dim)
             SGTR_CUDA(cudaMemcpyAsync(d, x, sizeof(double) * dim, cudaMemcpyHostToDevice, c.st));
@@ -1262,6 +1295,9 @@ int sgtr_save_scene_ply(sgtr_ctx* ctx, const char* path) {
         Ctx& c = ctx_ref(ctx);
         bind(c);
         need_scene(c);
+        if (c.nb)
+            throw invalid("save_scene: SH coefficients have no place in the reference's PLY "
+                          "(use sgtr_checkpoint_save)");
         const long long K = c.K, n = 14 * K;
         PinnedHost h(sizeof(double) * n);
         double* aos = c.vecbuf.as<double>(std::max(n, 1LL));
@@ -1302,8 +1338,10 @@ int sgtr_load_scene_ply(sgtr_ctx* ctx, const char* path, const sgtr_param_bounds
         const bool resized = K != c.K;
         std::swap(c.x.p, c.x_alt.p);
         std::swap(c.x.bytes, c.x_alt.bytes);
+        const bool sh_reset = c.nb != 0;
         c.K = (int)K;
-        if (resized) zero_state(c);
+        c.nb = 0;
+        if (resized || sh_reset) zero_state(c);
         SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
 }
@@ -1372,8 +1410,8 @@ int sgtr_checkpoint_save(sgtr_ctx* ctx, const char* path) {
         const std::string rtxt = rs.str();
         std::ofstream out(path, std::ios::binary);
         if (!out) throw Error(SGTR_RUNTIME, std::string("checkpoint: cannot open ") + path);
-        const long long hdr[3] = {(long long)c.K, c.t, (long long)rtxt.size()};
-        out.write("SGTRCKP1", 8);
+        const long long hdr[4] = {(long long)c.K, c.t, (long long)rtxt.size(), (long long)c.nb};
+        out.write("SGTRCKP2", 8);
         out.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
         out.write(rtxt.data(), rtxt.size());
         const double spare[2] = {c.rng.have_spare ? 1.0 : 0.0, c.rng.spare};
@@ -1401,17 +1439,17 @@ int sgtr_checkpoint_load(sgtr_ctx* ctx, const char* path) {
         std::ifstream in(path, std::ios::binary);
         if (!in) throw Error(SGTR_RUNTIME, std::string("checkpoint: cannot open ") + path);
         char magic[8];
-        long long hdr[3];
+        long long hdr[4];
         in.read(magic, 8);
         in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
-        if (!in || std::memcmp(magic, "SGTRCKP1", 8) != 0 || hdr[0] < 0 || hdr[2] <= 0 ||
-            hdr[2] > (1 << 20))
+        if (!in || std::memcmp(magic, "SGTRCKP2", 8) != 0 || hdr[0] < 0 || hdr[2] <= 0 ||
+            hdr[2] > (1 << 20) || !(hdr[3] == 0 || hdr[3] == 3 || hdr[3] == 8 || hdr[3] == 15))
             throw Error(SGTR_RUNTIME, std::string("checkpoint: not a checkpoint file: ") + path);
         std::string rtxt(hdr[2], '\0');
         in.read(&rtxt[0], hdr[2]);
         double spare[2];
         in.read(reinterpret_cast<char*>(spare), sizeof(spare));
-        const long long K = hdr[0], dim = 14 * K;
+        const long long K = hdr[0], dim = (14 + 3 * hdr[3]) * K;
         std::vector<double> h(5 * std::max(dim, 1LL));
         in.read(reinterpret_cast<char*>(h.data()), sizeof(double) * 5 * dim);
         if (!in) throw Error(SGTR_RUNTIME, std::string("checkpoint: truncated file ") + path);
@@ -1423,6 +1461,7 @@ int sgtr_checkpoint_load(sgtr_ctx* ctx, const char* path) {
         r.spare = spare[1];
         c.prefetch.reset();
         c.K = (int)K;
+        c.nb = (int)hdr[3];
         const long long n = std::max(dim, 1LL);
         Buf* dst[5] = {&c.x, &c.ghat, &c.dhat, &c.adam_m, &c.adam_v};
         for (int v = 0; v < 5; ++v)
@@ -1718,7 +1757,7 @@ int sgtr_rasterize_jvp(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_
         double* dv = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
         SGTR_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * c.dim(), cudaMemcpyHostToDevice, c.st));
         double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
-        launch_project_jvp(c.st, c.X(), c.K, dc, rp, dv, nullptr, trec);
+        launch_project_jvp(c.st, c.X(), c.K, c.nb, dc, rp, dv, nullptr, trec);
         launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, dc.W, dc.H, rp,
                           img_ptr(c, c.tan, P));
         c.launches += 2;
@@ -1862,7 +1901,7 @@ int sgtr_view_jacobian_apply(sgtr_ctx* ctx, int32_t view, const double* v,
         double* dv = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
         SGTR_CUDA(cudaMemcpyAsync(dv, v, sizeof(double) * c.dim(), cudaMemcpyHostToDevice, c.st));
         double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
-        launch_project_jvp(c.st, c.X(), c.K, vw.dc, rp, dv, nullptr, trec);
+        launch_project_jvp(c.st, c.X(), c.K, c.nb, vw.dc, rp, dv, nullptr, trec);
         launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, rp, img_ptr(c, c.tan, P));
         SsimArgs s{};
         s.mode = RES_JVP;
@@ -1983,7 +2022,7 @@ int sgtr_hutchinson_diag(sgtr_ctx* ctx, const int32_t* batch, int32_t n, int32_t
                 const View& v = c.views[batch[q]];
                 const ViewRender vr = render_view(c, v.dc, rp, true);
                 double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
-                launch_project_jvp(c.st, c.X(), c.K, v.dc, rp, z, nullptr, trec);
+                launch_project_jvp(c.st, c.X(), c.K, c.nb, v.dc, rp, z, nullptr, trec);
                 launch_raster_jvp(c.st, vr.tl, c.rec.get<double>(), trec, W, H, rp,
                                   img_ptr(c, c.tan, P));
                 c.launches += 2;
@@ -2010,7 +2049,7 @@ int sgtr_shd_radii(sgtr_ctx* ctx, double eps, const double caps[5], double* eta)
         bind(c);
         need_scene(c);
         double* e = c.seam0.as<double>(std::max<long long>(c.dim(), 1));
-        launch_shd_radii(c.st, c.K, c.X(), eps, caps, e);
+        launch_shd_radii(c.st, c.K, c.nb, c.X(), eps, caps, e);
         c.launches += 1;
         SGTR_CUDA(cudaMemcpyAsync(eta, e, sizeof(double) * c.dim(), cudaMemcpyDeviceToHost, c.st));
         SGTR_CUDA(cudaStreamSynchronize(c.st));
@@ -2128,6 +2167,16 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
             const double q[4] = {0, 0, 0, 1};
             const double c[3] = {0.5, 0.5, 0.5};
             put(init_x, ki, i, mu, s, q, cfg->init_opacity, c);
+        }
+        if (cfg->sh_degree < 0 || cfg->sh_degree > 3)
+            throw invalid("sgtr_make_synthetic: SH degree must be 0..3");
+        const long long nsh = 3LL * ((cfg->sh_degree + 1) * (cfg->sh_degree + 1) - 1);
+        if (nsh) {
+            // SH extension: GT coefficients 0.1 N(0,1) from their own stream
+            // (so degree 0 data are unchanged), init coefficients 0
+            Rng rs(cfg->seed + 0x5348ULL);
+            for (long long t = 0; t < nsh * kg; ++t) gt_x[14 * kg + t] = 0.1 * rs.normal();
+            for (long long t = 0; t < nsh * ki; ++t) init_x[14 * ki + t] = 0.0;
         }
         const double focal = cfg->focal_factor * cfg->height;
         for (int v = 0; v < cfg->views; ++v) {

@@ -49,6 +49,7 @@ struct DevCam {
     double fx, fy, cx, cy;
     double w[9];
     double t[3];
+    double cen[3];  // camera centre -W^T t (scene.hpp:80), for the SH view direction
 };
 
 struct RenderP {

@@ -41,6 +41,11 @@ SGTR_HD Dual operator/(const Dual& a, double b) { return Dual(a.v / b, a.d / b);
 SGTR_HD Dual operator/(double a, const Dual& b) {
     return Dual(a / b.v, -a * b.d / (b.v * b.v));
 }
+SGTR_HD Dual dsqrt(const Dual& a) {
+    const double r = sqrt(a.v);
+    return Dual(r, a.d / (2.0 * r));
+}
+SGTR_HD double dsqrt(double a) { return sqrt(a); }
 SGTR_HD double primal(double a) { return a; }
 SGTR_HD double primal(const Dual& a) { return a.v; }
 SGTR_HD double tangent(double) { return 0.0; }
@@ -332,6 +337,82 @@ SGTR_HD void pixel_range(double lo, double hi, int n, int& p0, int& p1) {
     p1 = hi >= n - 0.5 ? n - 1 : (int)floor(hi - 0.5);
     while (p1 < n - 1 && (p1 + 1) + 0.5 <= hi) ++p1;
     while (p1 + 0.5 > hi) --p1;
+}
+
+// ---------------------------------------------------------------- SH colour
+// Extension beyond the reference (SH degree 0, parity unpinned,
+// restated identically in oracle/oracle.cpp): nb = (d+1)^2 - 1 real-SH
+// coefficients per channel appended after the 14 reference groups as a
+// splat-major group, and
+//   c_view = c + sum_j Y_j(dir) k_j,  dir = normalize(mu - camera centre)
+// with the reference's linear RGB as the DC term (degree 0 is the reference
+// bit for bit), no offset and no clamp.  3DGS basis constants and signs.
+template <typename T>
+SGTR_HD void sh_basis(const T& x, const T& y, const T& z, int nb, T* Y) {
+    if (nb >= 3) {
+        Y[0] = -0.4886025119029199 * y;
+        Y[1] = 0.4886025119029199 * z;
+        Y[2] = -0.4886025119029199 * x;
+    }
+    if (nb >= 8) {
+        const T xx = x * x, yy = y * y, zz = z * z;
+        Y[3] = 1.0925484305920792 * (x * y);
+        Y[4] = -1.0925484305920792 * (y * z);
+        Y[5] = 0.31539156525252005 * (2.0 * zz - xx - yy);
+        Y[6] = -1.0925484305920792 * (x * z);
+        Y[7] = 0.5462742152960396 * (xx - yy);
+        if (nb >= 15) {
+            Y[8] = -0.5900435899266435 * y * (3.0 * xx - yy);
+            Y[9] = 2.890611442640554 * (x * y) * z;
+            Y[10] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
+            Y[11] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+            Y[12] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
+            Y[13] = 1.445305721320277 * z * (xx - yy);
+            Y[14] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+        }
+    }
+}
+
+// max over unit directions of |Y_j| (the SH trust-region radius divisor)
+SGTR_HD double sh_max(int j) {
+    switch (j) {
+        case 0: case 1: case 2: return 0.4886025119029199;
+        case 3: case 4: case 6: return 0.5462742152960397;
+        case 5: return 0.6307831305050401;
+        case 7: return 0.5462742152960396;
+        case 8: case 14: return 0.5900435899266437;
+        case 9: return 0.5562984315103788;
+        case 10: return 0.6293798292550865;
+        case 11: return 0.7463526651802308;
+        case 12: return 0.6293798292550866;
+        default: return 0.5562984315103789;  // 13
+    }
+}
+
+template <typename T>
+SGTR_HD void sh_dir(const T* mu, const double* cen, T* d) {
+    const T vx = mu[0] - cen[0], vy = mu[1] - cen[1], vz = mu[2] - cen[2];
+    const T inv = 1.0 / dsqrt(vx * vx + vy * vy + vz * vz);
+    d[0] = vx * inv;
+    d[1] = vy * inv;
+    d[2] = vz * inv;
+}
+
+// view colour; k points at the splat's 3 * nb coefficients (rgb interleaved)
+template <typename T, typename KT>
+SGTR_HD void sh_color(const T* mu, const T* c, const KT* k, int nb, const double* cen, T* out) {
+    if (nb == 0) {
+        for (int a = 0; a < 3; ++a) out[a] = c[a];
+        return;
+    }
+    T d[3], Y[15];
+    sh_dir(mu, cen, d);
+    sh_basis(d[0], d[1], d[2], nb, Y);
+    for (int a = 0; a < 3; ++a) {
+        T acc = Y[0] * k[a];
+        for (int j = 1; j < nb; ++j) acc = acc + Y[j] * k[3 * j + a];
+        out[a] = c[a] + acc;
+    }
 }
 
 }  // namespace sgtr

@@ -14,7 +14,7 @@ namespace sgtr {
 // 64-bit depth key (culled = ~0), tile rectangle and tile count.
 // tmask: per splat, the hit bits of its tile rectangle in row-major order
 // (rectangles of <= 64 tiles)
-void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
+void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
                     int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status);
 // parity dump: 12 doubles per splat (culled, depth, px, py, bx0..by1, i00..i11, 0)
@@ -22,7 +22,7 @@ void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& 
                          const RenderP& ro, double* out);
 // K12 (projection half): tangent records along a dense direction v (seam) or
 // along probe bits (bit set -> +1)
-void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& cam,
+void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                         const RenderP& ro, const double* v, const uint32_t* zbits,
                         double* trec);
 // K11: segmented reduce of the (tile, fragment) adjoint slots of each visible
@@ -30,7 +30,7 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& c
 // gradient into acc; mode 1 adds z (.) contribution (Hutchinson).
 // The probe is dense (zdense) or packed bits (zbits); a non-finite
 // contribution stores 1.0 into *nonfinite_flag.
-void launch_chain(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+void launch_chain(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                   const RenderP& ro, const int* sorted_ids, int n_visible,
                   const long long* off_r, const int* tcount, const double* slots,
                   const double* zdense, const uint32_t* zbits, double* acc,
@@ -92,7 +92,7 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
 // K11 over the per-warp partials of the barrier-free K10
-void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                        const RenderP& ro, const int* sorted_ids, int n_visible,
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
@@ -175,6 +175,7 @@ struct TrArgs {
     double beta1, beta2, adam_eps;
     double bc1, bc2;      // 1 - beta^t bias corrections (host std::pow)
     double lr[5];         // per-group rates, lr[0] already decayed and scaled
+    int nb;               // SH coefficients per channel (extension; 0 = reference)
 };
 int tr_num_blocks(int K);
 // phase 0: K14a (EMAs, direction, radii), 1: K14b (queued bisections),
@@ -183,7 +184,7 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase);
 // 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
 // (partials hold 2 * tr_num_blocks(K) rows of 5)
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5);
-void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps,
+void launch_shd_radii(cudaStream_t st, int K, int nb, const double* x, double eps,
                       const double caps[5], double* eta);
 void launch_scale(cudaStream_t st, double* v, long long n, double s);
 void launch_add(cudaStream_t st, double* dst, const double* src, long long n);

@@ -49,8 +49,12 @@ __device__ __forceinline__ Proj<double> project_primal(const Splat& p, const Dev
                            ro.z_near, ro.lowpass);
 }
 
-__global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, int K, DevCam cam,
-                                                 RenderP ro, double* __restrict__ rec,
+__device__ __forceinline__ const double* sh_ptr(const double* x, int K, int nb, int i) {
+    return x + 14LL * K + 3LL * nb * i;
+}
+
+__global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, int K, int nb,
+                                                 DevCam cam, RenderP ro, double* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys,
                                                  int* __restrict__ ids, int4* __restrict__ rect,
                                                  int* __restrict__ tcount,
@@ -61,7 +65,10 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
     if (i < K) {
         const Splat p = load_splat(x, K, i);
         ids[i] = i;
-        if (!splat_finite(p)) atomicMin(&status->nonfinite_splat, i);
+        bool finite = splat_finite(p);
+        const double* shk = sh_ptr(x, K, nb, i);
+        for (int t = 0; t < 3 * nb; ++t) finite = finite && isfinite(shk[t]);
+        if (!finite) atomicMin(&status->nonfinite_splat, i);
         const Proj<double> pr = project_primal(p, cam, ro);
         if (!pr.culled && pr.degenerate) atomicMin(&status->degenerate_splat, i);
         if (pr.culled || pr.degenerate) {
@@ -76,8 +83,10 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
             const double rho2 = ro.cull ? contrib_rho2(p.alpha, ro.alpha_skip) : INFINITY;
             const double k11 = i01 / i11, k00 = i01 / i00;
+            double col[3];
+            sh_color<double, double>(p.mu, p.c, shk, nb, cam.cen, col);
             double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,  py,  i00, i01,
-                              i11,     p.alpha, p.c[0], p.c[1], p.c[2], k11, rho2, k00};
+                              i11,     p.alpha, col[0], col[1], col[2], k11, rho2, k00};
             double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
 #pragma unroll
             for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);
@@ -146,7 +155,7 @@ __device__ __forceinline__ double probe_at(const double* v, const uint32_t* zbit
 
 // tangent records along v: build_fragments_dual (render.cpp:91-120)
 __global__ void __launch_bounds__(256) k_project_jvp(const double* __restrict__ x, int K,
-                                                     DevCam cam, RenderP ro,
+                                                     int nb, DevCam cam, RenderP ro,
                                                      const double* __restrict__ v,
                                                      const uint32_t* __restrict__ zbits,
                                                      double* __restrict__ trec) {
@@ -174,8 +183,46 @@ __global__ void __launch_bounds__(256) k_project_jvp(const double* __restrict__ 
     o[T_I01] = i01.d;
     o[T_I11] = i11.d;
     o[T_ALPHA] = probe_at(v, zbits, 10 * k + i);
+    if (nb == 0) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) o[T_C0 + a] = probe_at(v, zbits, 11 * k + 3LL * i + a);
+        for (int a = 0; a < 3; ++a) o[T_C0 + a] = probe_at(v, zbits, 11 * k + 3LL * i + a);
+        return;
+    }
+    // SH extension: tangent of the view colour (coefficients and direction)
+    Dual c[3], shk[45], col[3];
+    const double* kp = sh_ptr(x, K, nb, i);
+    const long long off = 14 * k + 3LL * nb * i;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c[a] = Dual(p.c[a], probe_at(v, zbits, 11 * k + 3LL * i + a));
+    for (int t = 0; t < 3 * nb; ++t) shk[t] = Dual(kp[t], probe_at(v, zbits, off + t));
+    sh_color<Dual, Dual>(mu, c, shk, nb, cam.cen, col);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) o[T_C0 + a] = col[a].d;
+}
+
+// SH extension of the adjoint chain (oracle chain_splat): dL/dk_j = Y_j a_rgb
+// and the view-direction term of dL/dmu (3 dual seeds), returned in gmu_sh
+template <typename Add>
+__device__ __forceinline__ void chain_sh(const double* x, int K, int nb, int id,
+                                         const DevCam& cam, const Splat& p, const double* a,
+                                         Add add, double* gmu_sh) {
+    const double* kp = sh_ptr(x, K, nb, id);
+    const long long off = 14LL * K + 3LL * nb * id;
+    double d[3], Y[15];
+    sh_dir<double>(p.mu, cam.cen, d);
+    sh_basis<double>(d[0], d[1], d[2], nb, Y);
+    for (int j = 0; j < nb; ++j)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) add(off + 3 * j + ch, Y[j] * a[6 + ch]);
+    const Dual c0[3] = {Dual(p.c[0]), Dual(p.c[1]), Dual(p.c[2])};
+#pragma unroll 1
+    for (int seed = 0; seed < 3; ++seed) {
+        Dual mu[3], col[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) mu[q] = Dual(p.mu[q], seed == q ? 1.0 : 0.0);
+        sh_color<Dual, double>(mu, c0, kp, nb, cam.cen, col);
+        gmu_sh[seed] = a[6] * col[0].d + a[7] * col[1].d + a[8] * col[2].d;
+    }
 }
 
 // K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
@@ -183,7 +230,7 @@ __global__ void __launch_bounds__(256) k_project_jvp(const double* __restrict__ 
 // Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
 // reference evaluates with 10 dual seeds, is applied in one reverse sweep.
 __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restrict__ x, int K,
-                                               DevCam cam, RenderP ro,
+                                               int nb, DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
                                                const long long* __restrict__ off_r,
                                                const int* __restrict__ tcount,
@@ -215,6 +262,9 @@ __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restric
     add(10 * k + id, a[5]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
+    const bool sh = nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
+    double gmu_sh[3] = {0.0, 0.0, 0.0};
+    if (sh) chain_sh(x, K, nb, id, cam, load_splat(x, K, id), a, add, gmu_sh);
     bool any = false;
 #pragma unroll
     for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
@@ -224,11 +274,14 @@ __global__ void __launch_bounds__(128) k_chain(int mode, const double* __restric
         double gmu[3], gs[3], gq[4];
         chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu[c]);
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, sh ? gmu_sh[c] + gmu[c] : gmu[c]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
+    } else if (sh) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu_sh[c]);
     }
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
@@ -277,7 +330,7 @@ __global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ so
 // (kPre) or, without kPre, summing the partials itself (one kernel)
 template <bool kPre>
 __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __restrict__ x, int K,
-                                               DevCam cam, RenderP ro,
+                                               int nb, DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
                                                const long long* __restrict__ off_r,
                                                const int* __restrict__ tcount,
@@ -322,6 +375,9 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     add(10 * k + id, a[5]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
+    const bool sh = nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
+    double gmu_sh[3] = {0.0, 0.0, 0.0};
+    if (sh) chain_sh(x, K, nb, id, cam, load_splat(x, K, id), a, add, gmu_sh);
     bool any = false;
 #pragma unroll
     for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
@@ -331,11 +387,14 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
         double gmu[3], gs[3], gq[4];
         chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu[c]);
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, sh ? gmu_sh[c] + gmu[c] : gmu[c]);
 #pragma unroll
         for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
+    } else if (sh) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu_sh[c]);
     }
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
@@ -375,11 +434,11 @@ void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_project(cudaStream_t st, const double* x, int K, const DevCam& cam,
+void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
                     int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status) {
     if (K == 0) return;
-    k_project<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, rec, keys, ids, rect, tcount,
+    k_project<<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids, rect, tcount,
                                                  tmask, status);
     SGTR_CUDA(cudaGetLastError());
 }
@@ -391,15 +450,16 @@ void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& 
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_project_jvp(cudaStream_t st, const double* x, int K, const DevCam& cam,
+void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                         const RenderP& ro, const double* v, const uint32_t* zbits,
                         double* trec) {
     if (K == 0) return;
-    k_project_jvp<<<ceil_div(K, 256), 256, 0, st>>>(x, K, cam, ro, v, zbits, trec);
+    k_project_jvp<<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, v, zbits, trec);
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb,
+                       const DevCam& cam,
                        const RenderP& ro, const int* sorted_ids, int n_visible,
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
@@ -411,23 +471,23 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, const 
                                                                   tcount, inv, part, mask, adj9);
         SGTR_CUDA(cudaGetLastError());
         k_chain_warp<true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
-            mode, x, K, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
+            mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
             zbits, adj9, acc, nonfinite_flag);
     } else {
         k_chain_warp<false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
-            mode, x, K, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
+            mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
             zbits, nullptr, acc, nonfinite_flag);
     }
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_chain(cudaStream_t st, int mode, const double* x, int K, const DevCam& cam,
+void launch_chain(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                   const RenderP& ro, const int* sorted_ids, int n_visible,
                   const long long* off_r, const int* tcount, const double* slots,
                   const double* zdense, const uint32_t* zbits, double* acc,
                   double* nonfinite_flag) {
     if (n_visible == 0) return;
-    k_chain<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, cam, ro, sorted_ids,
+    k_chain<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, sorted_ids,
                                                        n_visible, off_r, tcount, slots, zdense,
                                                        zbits, acc, nonfinite_flag);
     SGTR_CUDA(cudaGetLastError());

@@ -265,6 +265,12 @@ __device__ __forceinline__ long long flat_index(long long K, int i, int j) {
     return 11 * K + 3LL * i + (j - 11);
 }
 
+// flat index of coordinate j (0..13 reference groups, 14.. the SH group of
+// 3 * nb coefficients) of splat i
+__device__ __forceinline__ long long coord_index(long long K, int nb, int i, int j) {
+    return j < 14 ? flat_index(K, i, j) : 14 * K + 3LL * nb * i + (j - 14);
+}
+
 __device__ __forceinline__ Prim load_prim(const double* __restrict__ x, long long K, int i) {
     Prim p;
     for (int a = 0; a < 3; ++a) {
@@ -320,10 +326,12 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
         // shd_radii (and its degenerate-quaternion throw) runs for the
         // trust-region kinds only
         if (!a.ghat_only && a.kind != 1 && degenerate) atomicOr(a.degenerate_flag, 1);
+        const int npp = 14 + 3 * a.nb;
         if (a.kind != 0) {
-            // adam_direction (optimizer.cpp:153-185)
-            for (int j = 0; j < 14; ++j) {
-                const long long k = flat_index(K, i, j);
+            // adam_direction (optimizer.cpp:153-185); SH coefficients at the
+            // colour rate / 20 (extension)
+            for (int j = 0; j < npp; ++j) {
+                const long long k = coord_index(K, a.nb, i, j);
                 const double g = a.g_acc[k] * a.gscale;
                 v[0] += g * g;
                 const double m = a.beta1 * a.adam_m[k] + (1.0 - a.beta1) * g;
@@ -331,15 +339,16 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
                 a.adam_m[k] = m;
                 a.adam_v[k] = vv;
                 const int grp = j < 3 ? 0 : j < 6 ? 1 : j < 10 ? 2 : j == 10 ? 3 : 4;
+                const double lr = j < 14 ? a.lr[grp] : a.lr[4] / 20.0;
                 const double mhat = m / a.bc1;
                 const double vhat = vv / a.bc2;
-                const double dx = -a.lr[grp] * mhat / (sqrt(vhat) + a.adam_eps);
+                const double dx = -lr * mhat / (sqrt(vhat) + a.adam_eps);
                 v[1] += dx * dx;
                 a.dx_buf[k] = dx;
             }
         }
-        for (int j = 0; j < 14 && a.kind == 0; ++j) {
-            const long long k = flat_index(K, i, j);
+        for (int j = 0; j < npp && a.kind == 0; ++j) {
+            const long long k = coord_index(K, a.nb, i, j);
             const double g = a.g_acc[k] * a.gscale;
             v[0] += g * g;
             const double gh = a.theta1 * a.g_hat[k] + (1.0 - a.theta1) * g;
@@ -368,6 +377,10 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
             for (int j = 0; j < 3; ++j) a.eta_buf[3 * K + 3LL * i + j] = eta[3 + j];
             a.eta_buf[10 * K + i] = eta[10];
             for (int j = 0; j < 3; ++j) a.eta_buf[11 * K + 3LL * i + j] = eta[11 + j];
+            // SH extension: colour radius / max|Y_m|
+            for (int m = 0; m < a.nb; ++m)
+                for (int c = 0; c < 3; ++c)
+                    a.eta_buf[14 * K + 3LL * a.nb * i + 3 * m + c] = eta[11 + c] / sh_max(m);
         }
     }
     block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
@@ -423,8 +436,8 @@ __global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
     int bad = INT_MAX;
     if (i < a.K) {
         double xo[14];
-        for (int j = 0; j < 14; ++j) {
-            const long long k = flat_index(K, i, j);
+        for (int j = 0; j < 14 + 3 * a.nb; ++j) {
+            const long long k = coord_index(K, a.nb, i, j);
             const double dx = a.dx_buf[k];
             double c = dx;
             if (a.kind != 1) {
@@ -439,7 +452,10 @@ __global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
             if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
             v[2] += c * c;
             if (a.applied) a.applied[k] = c;
-            xo[j] = a.x[k] + c;
+            if (j < 14)
+                xo[j] = a.x[k] + c;
+            else
+                a.x_out[k] = a.x[k] + c;  // SH coefficients are not clamped
         }
         // Scene::clamp (scene.cpp:49-57)
         for (int c = 0; c < 3; ++c) {
@@ -477,7 +493,7 @@ __global__ void k_tr_finalize(const double* __restrict__ partials, int nblocks, 
     }
 }
 
-__global__ void k_shd_radii(int K, const double* __restrict__ x, double eps, double c0,
+__global__ void k_shd_radii(int K, int nb, const double* __restrict__ x, double eps, double c0,
                             double c1, double c2, double c3, double c4,
                             double* __restrict__ eta) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -487,6 +503,9 @@ __global__ void k_shd_radii(int K, const double* __restrict__ x, double eps, dou
     double e[14];
     radii(p, eps, caps, e);
     for (int j = 0; j < 14; ++j) eta[flat_index(K, i, j)] = e[j];
+    for (int m = 0; m < nb; ++m)
+        for (int c = 0; c < 3; ++c)
+            eta[14LL * K + 3LL * nb * i + 3 * m + c] = e[11 + c] / sh_max(m);
 }
 
 __global__ void k_scale(double* v, long long n, double s) {
@@ -537,11 +556,11 @@ void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, do
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_shd_radii(cudaStream_t st, int K, const double* x, double eps, const double caps[5],
-                      double* eta) {
+void launch_shd_radii(cudaStream_t st, int K, int nb, const double* x, double eps,
+                      const double caps[5], double* eta) {
     if (K == 0) return;
-    k_shd_radii<<<ceil_div(K, 128), 128, 0, st>>>(K, x, eps, caps[0], caps[1], caps[2], caps[3],
-                                                  caps[4], eta);
+    k_shd_radii<<<ceil_div(K, 128), 128, 0, st>>>(K, nb, x, eps, caps[0], caps[1], caps[2],
+                                                  caps[3], caps[4], eta);
     SGTR_CUDA(cudaGetLastError());
 }
 

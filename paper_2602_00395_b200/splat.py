@@ -168,17 +168,28 @@ class OptimizerOptions:  # optimizer.hpp:37-53
 
 
 # ------------------------------------------------------------------ scene / camera
+def params_per_splat(sh_degree: int = 0) -> int:
+    """14 (the reference) + 3 SH coefficients per basis function of degree
+    1..sh_degree (the SH colour extension, include/sgtr.h)."""
+    return 14 + 3 * ((sh_degree + 1) ** 2 - 1)
+
+
 class Scene:
-    """Flat group-major parameter vector (scene.hpp:37-64)."""
+    """Flat group-major parameter vector (scene.hpp:37-64), optionally with
+    the SH group appended (sh_degree > 0, extension)."""
 
     kParamsPerSplat = 14
 
-    def __init__(self, x=None, k: Optional[int] = None):
+    def __init__(self, x=None, k: Optional[int] = None, sh_degree: int = 0):
+        if not 0 <= sh_degree <= 3:
+            raise InvalidArgument("Scene: SH degree must be 0..3")
+        self.sh_degree = sh_degree
+        npp = params_per_splat(sh_degree)
         if x is None:
-            x = np.zeros(14 * (k or 0))
+            x = np.zeros(npp * (k or 0))
         self.x = _f64(x).copy()
-        if self.x.size % 14:
-            raise InvalidArgument("Scene: vector length is not a multiple of 14")
+        if self.x.size % npp:
+            raise InvalidArgument(f"Scene: vector length is not a multiple of {npp}")
 
     @classmethod
     def from_primitives(cls, mu, scale, quat, opacity, color) -> "Scene":
@@ -188,7 +199,7 @@ class Scene:
                                    np.asarray(opacity, np.float64).ravel(), color.ravel()]))
 
     def size(self) -> int:
-        return self.x.size // 14
+        return self.x.size // params_per_splat(self.sh_degree)
 
     def dim(self) -> int:
         return self.x.size
@@ -218,13 +229,19 @@ class Scene:
         self.x[:] = x
 
     def copy(self) -> "Scene":
-        return Scene(self.x)
+        return Scene(self.x, sh_degree=self.sh_degree)
 
     def primitives(self):
         k = self.size()
         x = self.x
         return (x[:3 * k].reshape(k, 3), x[3 * k:6 * k].reshape(k, 3),
-                x[6 * k:10 * k].reshape(k, 4), x[10 * k:11 * k], x[11 * k:].reshape(k, 3))
+                x[6 * k:10 * k].reshape(k, 4), x[10 * k:11 * k],
+                x[11 * k:14 * k].reshape(k, 3))
+
+    def sh_coefficients(self) -> np.ndarray:
+        """(K, nb, 3) view of the SH group (empty for degree 0)."""
+        k = self.size()
+        return self.x[14 * k:].reshape(k, (self.sh_degree + 1) ** 2 - 1, 3)
 
 
 @dataclass
@@ -294,6 +311,7 @@ class Context:
         self._views_key = None
         self.n_views = 0
         self.k = 0
+        self.sh_degree = 0
 
     def close(self):
         if getattr(self, "_h", None):
@@ -322,13 +340,21 @@ class Context:
         return int(lib().sgtr_launch_count(self._h))
 
     # scene
-    def set_scene(self, x: np.ndarray) -> None:
+    def set_scene(self, x: np.ndarray, sh_degree: int = 0) -> None:
         x = _f64(x)
-        check(lib().sgtr_set_scene(self._h, _ptr(x), x.size // 14))
-        self.k = x.size // 14
+        npp = params_per_splat(sh_degree)
+        if x.size % npp:
+            raise InvalidArgument(f"set_scene: vector length is not a multiple of {npp}")
+        check(lib().sgtr_set_scene_sh(self._h, _ptr(x), x.size // npp, sh_degree))
+        self.k = x.size // npp
+        self.sh_degree = sh_degree
+
+    @property
+    def dim(self) -> int:
+        return params_per_splat(getattr(self, "sh_degree", 0)) * self.k
 
     def get_scene(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        out = np.empty(14 * self.k) if out is None else out
+        out = np.empty(self.dim) if out is None else out
         check(lib().sgtr_get_scene(self._h, _ptr(out)))
         return out
 
@@ -341,6 +367,7 @@ class Context:
         """load_scene straight into HBM (validation on the device)."""
         check(lib().sgtr_load_scene_ply(self._h, str(path).encode(), _bounds_c(bounds)))
         self.k = int(lib().sgtr_scene_size(self._h))
+        self.sh_degree = 0
 
     def checkpoint_save(self, path: str) -> None:
         """Scene + full optimizer state (g_hat, d_hat, ADAM moments, t, Rng)."""
@@ -350,6 +377,7 @@ class Context:
         """Resume from checkpoint_save: the next step continues bit for bit."""
         check(lib().sgtr_checkpoint_load(self._h, str(path).encode()))
         self.k = int(lib().sgtr_scene_size(self._h))
+        self.sh_degree = int(lib().sgtr_scene_sh_degree(self._h))
 
     def set_eval_views(self, views: Sequence[Camera]) -> None:
         """Held-out views (with targets) for evaluate(); kept on the device."""
@@ -422,7 +450,7 @@ class Context:
         check(lib().sgtr_state_reset(self._h, C.c_uint64(seed)))
 
     def state_get(self):
-        g, d, t = np.empty(14 * self.k), np.empty(14 * self.k), C.c_int64()
+        g, d, t = np.empty(self.dim), np.empty(self.dim), C.c_int64()
         check(lib().sgtr_state_get(self._h, _ptr(g), _ptr(d), C.byref(t)))
         return g, d, t.value
 
@@ -432,7 +460,7 @@ class Context:
         check(lib().sgtr_state_set(self._h, _ptr(g), _ptr(d), t))
 
     def state_get_adam(self):
-        m, v = np.empty(14 * self.k), np.empty(14 * self.k)
+        m, v = np.empty(self.dim), np.empty(self.dim)
         check(lib().sgtr_state_get_adam(self._h, _ptr(m), _ptr(v)))
         return m, v
 
@@ -472,7 +500,7 @@ class Context:
         out = StepDiagnostics(d.batch_loss, d.gnorm, d.step_pre, d.step_post, d.clip_frac,
                               d.eps, d.max_step_over_radius, None, bool(d.refreshed))
         if opt.record_applied_step:
-            out.applied_step = np.empty(14 * self.k)
+            out.applied_step = np.empty(self.dim)
             check(lib().sgtr_get_applied_step(self._h, _ptr(out.applied_step)))
         return out
 
@@ -512,7 +540,7 @@ def default_context(device: int = 0) -> Context:
 
 def _scene_ctx(scene: Scene, ctx: Optional[Context]) -> Context:
     ctx = ctx or default_context()
-    ctx.set_scene(scene.x)
+    ctx.set_scene(scene.x, scene.sh_degree)
     return ctx
 
 
@@ -927,11 +955,12 @@ class OptimizerState:
     """OptimizerState (optimizer.hpp:58-72), resident in its own context:
     g_hat, d_hat and t live on the GPU, the Rng on the host side of libsgtr."""
 
-    def __init__(self, dim: int, seed: int, device: int = 0):
-        if dim % 14:
-            raise InvalidArgument("OptimizerState: dim is not a multiple of 14")
+    def __init__(self, dim: int, seed: int, device: int = 0, sh_degree: int = 0):
+        if dim % params_per_splat(sh_degree):
+            raise InvalidArgument(
+                f"OptimizerState: dim is not a multiple of {params_per_splat(sh_degree)}")
         self.ctx = Context(device)
-        self.ctx.set_scene(np.zeros(dim))
+        self.ctx.set_scene(np.zeros(dim), sh_degree)
         self.ctx.state_reset(seed)
         self.dim = dim
 
@@ -968,7 +997,7 @@ def _step_host(state: OptimizerState, scene: Scene, views: Sequence[Camera],
     if scene.dim() != state.dim:
         raise InvalidArgument(f"{what}: scene/state dimension mismatch")
     c = state.ctx
-    check(lib().sgtr_set_scene(c.handle, _ptr(scene.x), scene.size()))
+    c.set_scene(scene.x, scene.sh_degree)
     _views_ctx(c, views)
     diag = c.step(opt)
     check(lib().sgtr_get_scene(c.handle, _ptr(scene.x)))
@@ -1001,19 +1030,21 @@ def optimizer_step(state: OptimizerState, scene: Scene, views: Sequence[Camera],
 # ------------------------------------------------------------------ data
 def make_synthetic(gt_splats=64, init_splats=96, views=25, width=64, height=None, seed=1,
                    sigma_init=0.04, init_scale=0.08, init_opacity=0.5, camera_radius=2.2,
-                   camera_height=0.77, focal_factor=2.0, size_scale=1.0):
-    """dataset.cpp:25-67 (scene + cameras) with the declared W != H and
-    size-scale extensions; returns (gt Scene, init Scene, [Camera]) without
-    targets (render them with Context.render_targets)."""
+                   camera_height=0.77, focal_factor=2.0, size_scale=1.0, sh_degree=0):
+    """dataset.cpp:25-67 (scene + cameras) with the declared W != H,
+    size-scale and SH extensions; returns (gt Scene, init Scene, [Camera])
+    without targets (render them with Context.render_targets)."""
     height = width if height is None else height
     cfg = _lib.SynthConfig(gt_splats, init_splats, views, width, height, 0, seed, sigma_init,
                            init_scale, init_opacity, camera_radius, camera_height, focal_factor,
-                           size_scale)
-    gx = np.empty(14 * gt_splats)
-    ix = np.empty(14 * init_splats)
+                           size_scale, sh_degree, 0)
+    npp = params_per_splat(sh_degree)
+    gx = np.empty(npp * gt_splats)
+    ix = np.empty(npp * init_splats)
     cams = (_lib.Camera * max(views, 1))()
     check(lib().sgtr_make_synthetic(C.byref(cfg), _ptr(gx), _ptr(ix), cams))
-    return Scene(gx), Scene(ix), [Camera.from_c(cams[i]) for i in range(views)]
+    return (Scene(gx, sh_degree=sh_degree), Scene(ix, sh_degree=sh_degree),
+            [Camera.from_c(cams[i]) for i in range(views)])
 
 
 def look_at_camera(eye, target, fx, fy, width, height) -> Camera:
