@@ -37,11 +37,25 @@ sys.path.insert(0, ROOT)
 METRIC = "TR iterations/sec @1M Gaussians 1080p at 1/2/4/8 B200 vs CPU ref; PSNR delta"
 
 CONFIGS = {
-    # name: (splats, views, width, height, batch)
-    "c3": (1_000_000, 64, 1920, 1080, 8),
-    "c2": (100_000, 16, 512, 512, 8),
-    "c1": (10_000, 4, 128, 128, 1),
+    # name: (splats, views, width, height, batch, SH degree)
+    "c3": (1_000_000, 64, 1920, 1080, 8, 0),
+    "c2": (100_000, 16, 512, 512, 8, 3),
+    "c1": (10_000, 4, 128, 128, 1, 0),
 }
+
+
+def npp_of(sh):
+    return 14 + 3 * ((sh + 1) ** 2 - 1)
+
+
+def splat_subset(x, k, sub, sh):
+    """The first `sub` splats of a group-major vector (every group)."""
+    out, off = [], 0
+    for n in (3, 3, 4, 1, 3, 3 * ((sh + 1) ** 2 - 1)):
+        if n:
+            out.append(x[off:off + n * k].reshape(k, n)[:sub].ravel())
+        off += n * k
+    return np.concatenate(out)
 
 
 def parse():
@@ -62,9 +76,9 @@ def size_scale(k: int) -> float:
 
 
 def workload_desc(cfg):
-    k, v, w, h, b = CONFIGS[cfg]
+    k, v, w, h, b, sh = CONFIGS[cfg]
     return (f"{cfg.upper()}: {k} Gaussians, {v} views {w}x{h}, view batch {b}, "
-            f"refresh l=10 |S2|=1 nu=1, SH0, FP64")
+            f"refresh l=10 |S2|=1 nu=1, SH{sh}, FP64")
 
 
 # ------------------------------------------------------------------ clocks
@@ -124,7 +138,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=None):
+def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=None, sh=0):
     """Time the CPU reference path (the oracle port) on small central crops of
     a view and extrapolate to one full iteration: |S1| gradient views + 1/l of
     a refresh view + shd_radii at full K.  A call's cost is modelled as
@@ -133,7 +147,8 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=
     from 320 x T and 320 x 3T crops, T = host threads (>= 6 rows for SSIM).  Returns
     (it/s, model)."""
     from oracle import pyoracle as orc
-    k = x_init.size // 14
+    orc.set_sh_degree(sh)
+    k = x_init.size // npp_of(sh)
     W, H = cam_full.width, cam_full.height
 
     def crop(rows, cols=320):
@@ -175,11 +190,7 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=
         fixed = a_g / g1 if g1 > 0 else 0.0
         a_h, b_h = h1 * fixed, h1 * (1 - fixed) / p1
         sub = min(k, 100_000)
-        xs = np.concatenate([x_init[:3 * k].reshape(k, 3)[:sub].ravel(),
-                             x_init[3 * k:6 * k].reshape(k, 3)[:sub].ravel(),
-                             x_init[6 * k:10 * k].reshape(k, 4)[:sub].ravel(),
-                             x_init[10 * k:11 * k][:sub],
-                             x_init[11 * k:].reshape(k, 3)[:sub].ravel()])
+        xs = splat_subset(x_init, k, sub, sh)
         t0 = time.perf_counter()
         orc.shd_radii(xs, 1e-6)
         t_radii = (time.perf_counter() - t0) * k / sub
@@ -203,13 +214,14 @@ def cpu_cores():
 
 # ------------------------------------------------------------------ dataset
 def make_dataset(sp, ctx, cfg, seed):
-    k, v, w, h, b = CONFIGS[cfg]
+    k, v, w, h, b, sh = CONFIGS[cfg]
     gt, init, cams = sp.make_synthetic(gt_splats=k, init_splats=k, views=v, width=w, height=h,
-                                       seed=seed, size_scale=size_scale(k) if k > 64 else 1.0)
-    ctx.set_scene(gt.x)
+                                       seed=seed, size_scale=size_scale(k) if k > 64 else 1.0,
+                                       sh_degree=sh)
+    ctx.set_scene(gt.x, sh)
     ctx.set_cameras(cams)
     ctx.render_targets(quantize=True)
-    ctx.set_scene(init.x)
+    ctx.set_scene(init.x, sh)
     return gt, init, cams
 
 
@@ -220,10 +232,11 @@ def run_reference(args):
     from paper_2602_00395_b200 import splat as sp  # host-side generator only (no GPU)
     from oracle import pyoracle as orc
     orc.build()
-    k, v, w, h, b = CONFIGS[args.config]
+    k, v, w, h, b, sh = CONFIGS[args.config]
     gt, init, cams = sp.make_synthetic(gt_splats=k, init_splats=k, views=v, width=w, height=h,
                                        seed=args.seed,
-                                       size_scale=size_scale(k) if k > 64 else 1.0)
+                                       size_scale=size_scale(k) if k > 64 else 1.0,
+                                       sh_degree=sh)
     cam = orc.Camera()
     src = cams[1]._c()
     for f, _ in orc.Camera._fields_:
@@ -231,11 +244,11 @@ def run_reference(args):
     model = None
     # warm-up: builds the cost model (320 x T and 320 x 3T gradient crops, a
     # 320 x T refresh crop, shd_radii on a 100K subset; T = host threads)
-    _, model = cpu_reference_sample(init.x, gt.x, cam, b)
+    _, model = cpu_reference_sample(init.x, gt.x, cam, b, sh=sh)
     rates = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r, model = cpu_reference_sample(init.x, gt.x, cam, b, model=model)
+        r, model = cpu_reference_sample(init.x, gt.x, cam, b, model=model, sh=sh)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
@@ -287,7 +300,7 @@ def main():
 
     torch.cuda.set_device(local)
     ctx = sp.Context(local)
-    k, v, w, h, b = CONFIGS[args.config]
+    k, v, w, h, b, sh = CONFIGS[args.config]
     gt, init, cams = make_dataset(sp, ctx, args.config, args.seed)
     ctx.state_reset(args.seed)
     if world > 1:
@@ -336,7 +349,8 @@ def main():
     # ---- e2e: the reference-facing C-ABI call with host buffers each step
     e2e = None
     if not args.no_e2e:
-        x_host = torch.empty(14 * k, dtype=torch.float64, pin_memory=True).numpy()
+        npp = npp_of(sh)
+        x_host = torch.empty(npp * k, dtype=torch.float64, pin_memory=True).numpy()
         x_host[:] = ctx.get_scene()
         n_e2e = args.steps
         if world > 1:
@@ -345,8 +359,8 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(n_e2e):
-            _lib.check(_lib.lib().sgtr_set_scene(ctx.handle, x_host.ctypes.data_as(C.c_void_p),
-                                                 k))
+            _lib.check(_lib.lib().sgtr_set_scene_sh(ctx.handle,
+                                                    x_host.ctypes.data_as(C.c_void_p), k, sh))
             ctx.step(opt)
             _lib.check(_lib.lib().sgtr_get_scene(ctx.handle, x_host.ctypes.data_as(C.c_void_p)))
         f1.record(stream)
@@ -357,8 +371,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_e2e = float(t.item())
         e2e = {"value": 1000.0 * n_e2e / ms_e2e, "unit": "it/s",
-               "h2d_bytes_per_step": 8 * 14 * k, "d2h_bytes_per_step": 8 * 14 * k + 72,
-               "path": "sgtr_set_scene(host x) -> sgtr_step_3dgs2tr -> sgtr_get_scene(host x)"}
+               "h2d_bytes_per_step": 8 * npp * k, "d2h_bytes_per_step": 8 * npp * k + 72,
+               "path": "sgtr_set_scene_sh(host x) -> sgtr_step_3dgs2tr -> sgtr_get_scene(host x)"}
 
     # ---- algorithmic work of the dominant kernels (outside timed regions)
     E = Cc = 0
@@ -408,7 +422,7 @@ def main():
                             f"E={E:.4g} evaluated, C={Cc:.4g} contributing (pixel, fragment) "
                             f"pairs per view"}
     else:
-        dim = 14 * k
+        dim = npp_of(sh) * k
         bytes_per = {"tr_update": 56 * dim, "depth_sort_scan": 24 * k * 8}.get(dom, 0)
         achieved = bytes_per / (avg_ms * 1e-3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
@@ -418,7 +432,7 @@ def main():
     # + D_hat write and z.w read on the 1-in-10 refresh steps
     tr_cnt = ktimes.get("tr_update", [0, 0.0])[0]
     tr_tot = sum(ktimes.get(n, [0, 0.0])[1] for n in ("tr_update", "tr_bisect", "tr_apply"))
-    tr_bytes = 8 * 14 * k * (6 + 2.0 / 10)
+    tr_bytes = 8 * npp_of(sh) * k * (6 + 2.0 / 10)
     roofline_tr = {"bound": "hbm", "kernel": "tr_update+tr_bisect+tr_apply",
                    "achieved": tr_bytes / (tr_tot / max(tr_cnt, 1) * 1e-3) / 1e9 if tr_cnt else None,
                    "peak": hbm_peak, "unit": "GB/s",
@@ -435,7 +449,7 @@ def main():
         src = cams[1]._c()
         for f, _ in orc.Camera._fields_:
             setattr(cam, f, getattr(src, f))
-        rate, model = cpu_reference_sample(init.x, gt.x, cam, b)
+        rate, model = cpu_reference_sample(init.x, gt.x, cam, b, sh=sh)
         cores = cpu_cores()
         cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "port",
                "sample": (f"oracle port of the reference path, {cores} threads; central 320xT "
@@ -454,7 +468,9 @@ def main():
             "config": {"workload": workload_desc(args.config), "global_batch": b,
                        "resolution": f"{w}x{h}", "splats": k, "views": v,
                        "parallelism": f"view-parallel dp{world} + 1 ncclAllReduce/step",
-                       "l2": "inputs exceed L2 (scene 112 MB + per-view records, slots, images)",
+                       "l2": (f"per-step working set exceeds L2: scene {8 * npp_of(sh) * k / 1e6:.0f} MB"
+                              f" + {b} views x (records {128 * k / 1e6:.0f} MB, FP64 images"
+                              f" {8 * 3 * w * h * 8 / 1e6:.0f} MB, partials) vs 126 MB L2"),
                        "mean_visible": nvis, "mean_tile_duplicates": ndup},
             "roofline": roofline,
             "roofline_tr_update": roofline_tr,
