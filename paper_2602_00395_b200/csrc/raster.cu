@@ -1036,6 +1036,12 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
     else if (g_vjp_prefetch == 3)
         k_raster_vjp_warp<3, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
                                                                  last, part, mask);
+    else if (g_smem_red && g_wpb == 2 && g_vjp_min_blocks == 4)
+        k_raster_vjp_warp<4, true, false, 2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj,
+                                                                    tfinal, last, part, mask);
+    else if (g_smem_red && g_wpb == 8 && g_vjp_min_blocks == 2)
+        k_raster_vjp_warp<2, true, false, 8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj,
+                                                                     tfinal, last, part, mask);
     else if (g_smem_red && g_wpb == 2)
         k_raster_vjp_warp<3, true, false, 2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj,
                                                                     tfinal, last, part, mask);
