@@ -348,7 +348,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, tbox;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     // second view lane (stream + per-view workspace), swapped in by use_lane
@@ -362,7 +362,7 @@ struct Ctx {
     X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp) X(slots)    \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
-    X(part) X(mask) X(tmask) X(large) X(tbox)
+    X(part) X(mask) X(tmask) X(large) X(trect)
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
@@ -530,12 +530,12 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     int* tids = c.tile_ids.as<int>(nd);
     {
         Timed t(c, KC_TILE_BIN);
-        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, rec, tids, c.inv.as<int>(nd),
-                        c.tbox.as<float4>(nd));
+        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids, c.inv.as<int>(nd),
+                        c.trect.as<int4>(nd));
     }
     c.launches += vr.n_dup ? 1 : 0;
     vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt,
-                      b.dup_id,  tids,    c.tbox.get<float4>(), row0,
+                      b.dup_id,  tids,    c.trect.get<int4>(), row0,
                       row1 < 0 ? tiles_y : row1};
     const int P = dc.W * dc.H;
     Timed t(c, KC_RASTER_FWD);

@@ -116,19 +116,20 @@ __global__ void k_ranges(const unsigned int* __restrict__ tkeys, long long n,
     if (i == n - 1 || tkeys[i + 1] != k) end[k] = (int)(i + 1);
 }
 
+// tile-sorted copies of the splat id and its exact pixel rectangle (K1's
+// pixel_range of the FP64 bbox), which the rasterisers test per warp and
+// per pixel; and the duplicate -> position inverse used by K11
 __global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restrict__ dup_id,
-                           long long n, const double* __restrict__ rec,
+                           long long n, const int4* __restrict__ rect,
                            int* __restrict__ tile_ids, int* __restrict__ inv,
-                           float4* __restrict__ tbox) {
+                           int4* __restrict__ trect) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int d = sorted_d[j];
     const int id = dup_id[d];
     tile_ids[j] = id;
     inv[d] = (int)j;
-    const double4 b = *reinterpret_cast<const double4*>(rec + (long long)kRec * id);
-    tbox[j] = make_float4(__double2float_rd(b.x), __double2float_ru(b.y),
-                          __double2float_rd(b.z), __double2float_ru(b.w));
+    trect[j] = rect[id];
 }
 
 int bits_for(int n) {
@@ -140,9 +141,10 @@ int bits_for(int n) {
 }  // namespace
 
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     const double* rec, int* tile_ids, int* inv, float4* tbox) {
+                     const int4* rect, int* tile_ids, int* inv, int4* trect) {
     if (n == 0) return;
-    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, rec, tile_ids, inv, tbox);
+    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, rect, tile_ids, inv,
+                                                  trect);
     SGTR_CUDA(cudaGetLastError());
 }
 

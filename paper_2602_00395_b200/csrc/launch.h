@@ -72,7 +72,7 @@ struct TileLists {
     const int* sorted_d;  // tile-sorted duplicate indices
     const int* dup_id;    // duplicate -> splat id
     const int* tile_ids;  // splat id per tile-sorted position (dup_id[sorted_d[j]])
-    const float4* tbox;   // outward-rounded float bbox (x0, x1, y0, y1) per position
+    const int4* trect;    // per position: the splat's pixel rectangle (x0, y0, x1, y1)
     int row0, row1;       // tile rows the raster kernels process (a band on refresh
                           // views split over ranks; [0, tiles_y) otherwise)
 };
@@ -105,7 +105,7 @@ int chain_mode();
 // tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j, tbox[j] = the
 // splat's bbox rounded outward to float
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     const double* rec, int* tile_ids, int* inv, float4* tbox);
+                     const int4* rect, int* tile_ids, int* inv, int4* trect);
 // K12 (raster half): tangent image along the tangent records
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro,

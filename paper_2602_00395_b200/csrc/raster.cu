@@ -38,7 +38,19 @@ struct PixelCtx {
     bool inside;
     double pxc, pyc;
     double wx0, wx1, wy0, wy1;  // the warp's span of pixel centres
+    int ix0, iy0;               // the warp's first pixel column / row
 };
+
+// exact overlap of a splat's pixel rectangle (K1's pixel_range: the pixels
+// whose centre lies in the closed FP64 bbox, clipped to the image) with the
+// warp's 8x4 pixel block
+__device__ __forceinline__ bool rect_hits_warp(const PixelCtx& p, int4 r) {
+    return !(p.ix0 + 7 < r.x || p.ix0 > r.z || p.iy0 + 3 < r.y || p.iy0 > r.w);
+}
+// the reference's per-pixel bbox test (render.cpp:128-131) on that rectangle
+__device__ __forceinline__ bool rect_has_pixel(const PixelCtx& p, int4 r) {
+    return p.px >= r.x && p.px <= r.z && p.py >= r.y && p.py <= r.w;
+}
 
 // warp w covers columns (w & 1) * 8 .. +7 and rows (w >> 1) * 4 .. +3
 __device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H,
@@ -53,6 +65,8 @@ __device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int 
     p.inside = p.px < W && p.py < H;
     p.pxc = p.px + 0.5;
     p.pyc = p.py + 0.5;
+    p.ix0 = x0;
+    p.iy0 = y0;
     p.wx0 = x0 + 0.5;
     p.wx1 = x0 + 7.5;
     p.wy0 = y0 + 0.5;
@@ -218,6 +232,7 @@ __global__ void __launch_bounds__(32 * WPB)
     constexpr int SUB = kWarps / WPB;
     __shared__ int s_list[WPB][kChunkF];
     __shared__ int s_ids[WPB][kChunkF];
+    __shared__ int4 s_rect[WPB][kChunkF];
     const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
@@ -228,6 +243,7 @@ __global__ void __launch_bounds__(32 * WPB)
     int processed = end - start;
     int* my_list = s_list[lw];
     int* my_ids = s_ids[lw];
+    int4* my_rect = s_rect[lw];
     for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
         if (__all_sync(kFull, done)) break;
         const int cend = min(end, cbeg + kChunkF);
@@ -235,15 +251,17 @@ __global__ void __launch_bounds__(32 * WPB)
         for (int base = cbeg; base < cend; base += 32) {
             const int jj = base + lane;
             bool pass = false;
+            int4 rr;
             if (jj < cend) {
-                const float4 bb = __ldg(tl.tbox + jj);
-                pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
+                rr = __ldg(tl.trect + jj);
+                pass = rect_hits_warp(pc, rr);
             }
             const unsigned m = __ballot_sync(kFull, pass);
             if (pass) {
                 const int q = nl + __popc(m & ((1u << lane) - 1u));
                 my_list[q] = jj;
                 my_ids[q] = __ldg(tl.tile_ids + jj);
+                my_rect[q] = rr;
             }
             nl += __popc(m);
         }
@@ -252,11 +270,10 @@ __global__ void __launch_bounds__(32 * WPB)
             const int j = my_list[e];
             const int id = my_ids[e];
             const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-            const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-            if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
+            if (!done && rect_has_pixel(pc, my_rect[e])) {
                 const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
                 const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
-                const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
+                const double f[13] = {0.0, 0.0, 0.0, 0.0, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
                                       c01.x, c01.y, cc2.x};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
@@ -310,10 +327,7 @@ __global__ void __launch_bounds__(kThreads)
         for (int base = cbeg; base < cend; base += 32) {
             const int jj = base + lane;
             bool pass = false;
-            if (jj < cend) {
-                const float4 bb = __ldg(tl.tbox + jj);
-                pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
-            }
+            if (jj < cend) pass = rect_hits_warp(pc, __ldg(tl.trect + jj));
             const unsigned m = __ballot_sync(kFull, pass);
             if (pass) {
                 const int q = nl + __popc(m & ((1u << lane) - 1u));
@@ -324,7 +338,6 @@ __global__ void __launch_bounds__(kThreads)
         }
         __syncwarp();
         for (int e = 0; e < nl; ++e) {
-            const int j = my_list[e];
             const int id = my_ids[e];
             const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
             const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
@@ -495,7 +508,7 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
 // an 11-lane third of one component, 9 lanes add the three thirds and write
 // the totals to out[0..8].  ~40 instructions instead of the shuffle
 // butterfly's selects and shuffles; fixed order, so deterministic.
-constexpr int kChunk = 256;
+constexpr int kChunk = 128;  // VJP list chunk (48 KB static smem per 8-warp CTA)
 constexpr int kRedStride = 33;
 constexpr int kRedScratch = kAdj * kRedStride + 27;
 __device__ __forceinline__ void warp_reduce9_smem(const double* g, int lane, double* scr,
@@ -653,6 +666,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
     __shared__ double s_red[WPB][kRedScratch];
     __shared__ int s_list[WPB][kChunk];
     __shared__ int s_ids[WPB][kChunk];
+    __shared__ int4 s_rect[WPB][kChunk];
     const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
@@ -679,22 +693,25 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
     // warp's 8x4 pixels.
     int* my_list = s_list[lw];
     int* my_ids = s_ids[lw];
+    int4* my_rect = s_rect[lw];
     for (int cend = start + wlast; cend > start; cend -= kChunk) {
     const int cbeg = max(start, cend - kChunk);
     int nl = 0;
     for (int base = cbeg; base < cend; base += 32) {
         const int jj = base + lane;
         bool pass = false;
+        int4 rr;
         if (jj < cend) {
-            const float4 bb = __ldg(tl.tbox + jj);
-            pass = !(pc.wx1 < bb.x || pc.wx0 > bb.y || pc.wy1 < bb.z || pc.wy0 > bb.w);
+            rr = __ldg(tl.trect + jj);
+            pass = rect_hits_warp(pc, rr);
         }
         const unsigned m = __ballot_sync(kFull, pass);
         if (pass) {
-                const int q = nl + __popc(m & ((1u << lane) - 1u));
-                my_list[q] = jj;
-                my_ids[q] = __ldg(tl.tile_ids + jj);
-            }
+            const int q = nl + __popc(m & ((1u << lane) - 1u));
+            my_list[q] = jj;
+            my_ids[q] = __ldg(tl.tile_ids + jj);
+            my_rect[q] = rr;
+        }
         nl += __popc(m);
     }
     __syncwarp();
@@ -726,16 +743,16 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
             j = my_list[e];
             const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[e]);
 #pragma unroll
-            for (int k = 0; k < 7; ++k) cr[k] = __ldg(r2 + k);
+            for (int k = 2; k < 7; ++k) cr[k] = __ldg(r2 + k);
         }
-        const double f[13] = {cr[0].x, cr[0].y, cr[1].x, cr[1].y, cr[2].x, cr[2].y, cr[3].x,
+        const double f[13] = {0.0,     0.0,     0.0,     0.0,     cr[2].x, cr[2].y, cr[3].x,
                               cr[3].y, cr[4].x, cr[4].y, cr[5].x, cr[5].y, cr[6].x};
         const int rel = j - start;
         double g[kAdj];
 #pragma unroll
         for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
         bool contrib = false;
-        if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
+        if (rel < lastp && rect_has_pixel(pc, my_rect[e])) {
             const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
             const double gauss = fast_exp(eval_expo(dx, dy, f));
             double abar = __dmul_rn(f[R_ALPHA], gauss);
