@@ -303,6 +303,96 @@ __global__ void __launch_bounds__(32 * WPB)
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K7, batch-staged
+// As k_raster_fwd_warp, but the list is walked in batches of 32 positions:
+// each lane tests one position against the warp's pixel block and, if it
+// passes, loads that fragment's 9 raster fields into a warp-private shared
+// slot (ballot-compacted), so the 32 record fetches of a batch are in flight
+// together instead of one dependent fetch per blended entry.
+struct StagedRec {
+    double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
+};
+
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB)
+    k_raster_fwd_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                        double* __restrict__ img, double* __restrict__ tfinal,
+                        int* __restrict__ last) {
+    constexpr int SUB = kWarps / WPB;
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool done = !pc.inside;
+    int processed = end - start;
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done)) break;
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < end) {
+            rr = __ldg(tl.trect + jj);
+            pass = rect_hits_warp(pc, rr);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+        }
+        __syncwarp();
+        const int n = __popc(m);
+        for (int e = 0; e < n; ++e) {
+            if (!done && rect_has_pixel(pc, my_rect[e])) {
+                const StagedRec r = my_rec[e];
+                const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
+                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T;
+                    c0 += f[R_C0] * w;
+                    c1 += f[R_C1] * w;
+                    c2 += f[R_C2] * w;
+                    T = __dmul_rn(T, __dsub_rn(1.0, abar));
+                    if (T < ro.t_stop) {
+                        done = true;
+                        processed = my_pos[e] - start + 1;
+                    }
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    img[p] = c0 + ro.bg[0] * T;
+    img[P + p] = c1 + ro.bg[1] * T;
+    img[2 * P + p] = c2 + ro.bg[2] * T;
+    tfinal[p] = T;
+    last[p] = processed;
+}
+
 // ------------------------------------------------------------------ K12 (raster), warp-filtered
 // Forward-mode tangent image with the same chunked, warp-filtered walk as
 // k_raster_fwd_warp; records and tangent records read through L1.
@@ -800,6 +890,124 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
     }
 }
 
+// ------------------------------------------------------------------ K10, batch-staged
+// As k_raster_vjp_warp, with k_raster_fwd_staged's batches: the list is
+// walked back to front 32 positions at a time, the passing fragments' raster
+// fields are fetched by their filtering lanes in parallel into a
+// warp-private shared batch, then processed last-to-first.
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
+    k_raster_vjp_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                        const double* __restrict__ adj, const double* __restrict__ tfinal,
+                        const int* __restrict__ last, double* __restrict__ part,
+                        unsigned char* __restrict__ mask) {
+    constexpr int SUB = kWarps / WPB;
+    __shared__ double s_red[WPB][kRedScratch];
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
+    int lastp = 0;
+    if (pc.inside) {
+        u0 = adj[p];
+        u1 = adj[P + p];
+        u2 = adj[2 * P + p];
+        T = tfinal[p];
+        lastp = last[p];
+    }
+    // pixels with an all-zero adjoint are skipped (render.cpp:283)
+    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
+    if (!active) lastp = 0;
+    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;  // "behind"
+    const int wlast = __reduce_max_sync(kFull, lastp);
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < top) {
+            rr = __ldg(tl.trect + jj);
+            pass = rect_hits_warp(pc, rr);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+        }
+        __syncwarp();
+        for (int e = __popc(m) - 1; e >= 0; --e) {
+            const int j = my_pos[e];
+            const int rel = j - start;
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            if (rel < lastp && rect_has_pixel(pc, my_rect[e])) {
+                const StagedRec r = my_rec[e];
+                const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
+                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                const double gauss = fast_exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], gauss);
+                const bool clamped = abar >= ro.alpha_clamp;
+                if (clamped) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    contrib = true;
+                    // one reciprocal for T_in = T / (1 - abar) and the three
+                    // behind / (1 - abar) terms (render.cpp:243-245)
+                    const double rom = 1.0 / __dsub_rn(1.0, abar);
+                    const double t_in = T * rom;
+                    const double at = abar * t_in;
+                    g[6] = u0 * at;
+                    g[7] = u1 * at;
+                    g[8] = u2 * at;
+                    const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
+                                       u1 * (f[R_C1] * t_in - b1 * rom) +
+                                       u2 * (f[R_C2] * t_in - b2 * rom);
+                    b0 += f[R_C0] * at;
+                    b1 += f[R_C1] * at;
+                    b2 += f[R_C2] * at;
+                    if (!clamped) {
+                        g[5] = gauss * dab;
+                        const double de = abar * dab;
+                        g[2] = de * (-0.5 * dx * dx);
+                        g[3] = de * (-dx * dy);
+                        g[4] = de * (-0.5 * dy * dy);
+                        g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
+                        g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
+                    }
+                    T = t_in;
+                }
+            }
+            if (!__any_sync(kFull, contrib)) continue;
+            double* o = part + ((long long)j * kWarps + warp) * kAdj;
+            warp_reduce9_smem(g, lane, s_red[lw], o);
+            if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
+        }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ K10, PPL pixels per lane
 // As k_raster_vjp_warp, but each lane owns PPL pixels of one column (rows
 // r, r+2, ..): a warp covers 16 x 2*PPL pixels, sums each fragment's adjoints
@@ -981,12 +1189,13 @@ const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);  // (slot-form VJP o
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
-const int g_fwd_warp = knob("SGTR_FWD_WARP", 1);
+const int g_fwd_warp = knob("SGTR_FWD_WARP", 2);  // 2: batch-staged, 1: chunk-filtered
+const int g_vjp_staged = knob("SGTR_VJP_STAGED", 1);  // batch-staged K10
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
 // warps per CTA of the warp-filtered forward / VJP kernels
 const int g_fwd_wpb = knob("SGTR_FWD_WPB", 2);
-const int g_wpb = knob("SGTR_WPB", 8);
+const int g_wpb = knob("SGTR_WPB", 2);
 
 }  // namespace
 
@@ -998,7 +1207,12 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp) {
+    else if (g_fwd_warp == 2) {
+        if (g_fwd_wpb == 2)
+            k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+        else
+            k_raster_fwd_staged<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    } else if (g_fwd_warp) {
         if (g_fwd_wpb == 2)
             k_raster_fwd_warp<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
         else if (g_fwd_wpb == 4)
@@ -1043,7 +1257,13 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_ppl == 4)
+    if (g_vjp_staged && g_wpb == 2)
+        k_raster_vjp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                     mask);
+    else if (g_vjp_staged)
+        k_raster_vjp_staged<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                       part, mask);
+    else if (g_vjp_ppl == 4)
         k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
     else if (g_vjp_ppl == 2)
         k_raster_vjp_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
