@@ -350,18 +350,29 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
-    // the <= 8 per-warp partials of each duplicate, in warp order
+    // the <= 8 per-warp partials of each duplicate, in (duplicate, warp)
+    // order; positions and masks of 4 duplicates are fetched together so the
+    // dependent loads overlap (the sum order is unchanged)
     const long long off = off_r[r];
-    for (int t = 0; t < (kPre ? 0 : cnt); ++t) {
-        const long long jpos = inv[off + t];
-        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * jpos);
-        if (m == 0ull) continue;
-        const double* pp = part + jpos * 8 * kAdj;
+    for (int t0 = 0; t0 < (kPre ? 0 : cnt); t0 += 4) {
+        long long jp[4];
+        unsigned long long mk[4];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            if ((m >> (8 * w)) & 0xffull) {
+        for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? (long long)inv[off + t0 + u] : -1;
 #pragma unroll
-                for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+        for (int u = 0; u < 4; ++u)
+            mk[u] = jp[u] >= 0 ? *reinterpret_cast<const unsigned long long*>(mask + 8 * jp[u])
+                               : 0ull;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (mk[u] == 0ull) continue;
+            const double* pp = part + jp[u] * 8 * kAdj;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                if ((mk[u] >> (8 * w)) & 0xffull) {
+#pragma unroll
+                    for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+                }
             }
         }
     }
