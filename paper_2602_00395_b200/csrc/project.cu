@@ -53,6 +53,7 @@ __device__ __forceinline__ const double* sh_ptr(const double* x, int K, int nb, 
     return x + 14LL * K + 3LL * nb * i;
 }
 
+template <bool kSH>
 __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, int K, int nb,
                                                  DevCam cam, RenderP ro, double* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys,
@@ -67,7 +68,8 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
         ids[i] = i;
         bool finite = splat_finite(p);
         const double* shk = sh_ptr(x, K, nb, i);
-        for (int t = 0; t < 3 * nb; ++t) finite = finite && isfinite(shk[t]);
+        if (kSH)
+            for (int t = 0; t < 3 * nb; ++t) finite = finite && isfinite(shk[t]);
         if (!finite) atomicMin(&status->nonfinite_splat, i);
         const Proj<double> pr = project_primal(p, cam, ro);
         if (!pr.culled && pr.degenerate) atomicMin(&status->degenerate_splat, i);
@@ -83,8 +85,8 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
             invert2x2(pr.c00, pr.c01, pr.c11, i00, i01, i11);
             const double rho2 = ro.cull ? contrib_rho2(p.alpha, ro.alpha_skip) : INFINITY;
             const double k11 = i01 / i11, k00 = i01 / i00;
-            double col[3];
-            sh_color<double, double>(p.mu, p.c, shk, nb, cam.cen, col);
+            double col[3] = {p.c[0], p.c[1], p.c[2]};
+            if (kSH) sh_color<double, double>(p.mu, p.c, shk, nb, cam.cen, col);
             double r[kRec] = {px - rx, px + rx, py - ry, py + ry, px,  py,  i00, i01,
                               i11,     p.alpha, col[0], col[1], col[2], k11, rho2, k00};
             double2* dst = reinterpret_cast<double2*>(rec + (long long)kRec * i);
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ so
 
 // K11b: the chain of each visible splat from its summed adjoints
 // (kPre) or, without kPre, summing the partials itself (one kernel)
-template <bool kPre>
+template <bool kPre, bool kSH>
 __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     add(10 * k + id, a[5]);
 #pragma unroll
     for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
-    const bool sh = nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
+    const bool sh = kSH && nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
     double gmu_sh[3] = {0.0, 0.0, 0.0};
     if (sh) chain_sh(x, K, nb, id, cam, load_splat(x, K, id), a, add, gmu_sh);
     bool any = false;
@@ -449,8 +451,12 @@ void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCa
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
                     int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status) {
     if (K == 0) return;
-    k_project<<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids, rect, tcount,
-                                                 tmask, status);
+    if (nb)
+        k_project<true><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids, rect,
+                                                          tcount, tmask, status);
+    else
+        k_project<false><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids,
+                                                           rect, tcount, tmask, status);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -481,11 +487,20 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb
         k_sum_adjoints<<<ceil_div(n_visible, 256), 256, 0, st>>>(sorted_ids, n_visible, off_r,
                                                                   tcount, inv, part, mask, adj9);
         SGTR_CUDA(cudaGetLastError());
-        k_chain_warp<true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+        if (nb)
+            k_chain_warp<true, true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+                mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
+                zdense, zbits, adj9, acc, nonfinite_flag);
+        else
+            k_chain_warp<true, false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+                mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
+                zdense, zbits, adj9, acc, nonfinite_flag);
+    } else if (nb) {
+        k_chain_warp<false, true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
-            zbits, adj9, acc, nonfinite_flag);
+            zbits, nullptr, acc, nonfinite_flag);
     } else {
-        k_chain_warp<false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+        k_chain_warp<false, false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
             zbits, nullptr, acc, nonfinite_flag);
     }
