@@ -66,8 +66,7 @@ def full(path):
             u = units[ix[metric]]
             if key == "time_us" and u in ("msecond", "ms"):
                 xs = [x * 1e3 for x in xs]
-            elif key == "time_us" and u in ("usecond", "us"):
-                xs = [x / scale for x in xs]
+            # "usecond"/"us": already microseconds
             vals.append(f"{sum(xs) / len(xs):.4g}" if xs else "?")
         st = {}
         for h, i in ix.items():
