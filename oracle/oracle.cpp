@@ -1681,13 +1681,16 @@ int orc_binning(const double* x, int64_t k, const orc_camera* cam,
                                         std::max(y0, ty * tile), std::min(y1, ty * tile + tile - 1)))
                         per[(size_t)ty * tw + tx].push_back((int32_t)f.splat);
         }
+        // empty tiles are reported as [0, 0) (the GPU leaves their range
+        // unset); non-empty ones as their [start, end) in the tile-major list
         int64_t total = 0;
         for (size_t t = 0; t < per.size(); ++t) {
-            if (tile_start) tile_start[t] = total;
+            const bool empty = per[t].empty();
+            if (tile_start) tile_start[t] = empty ? 0 : total;
             if (lists)
                 std::copy(per[t].begin(), per[t].end(), lists + total);
             total += (int64_t)per[t].size();
-            if (tile_end) tile_end[t] = total;
+            if (tile_end) tile_end[t] = empty ? 0 : total;
         }
         *n_dup = total;
     });

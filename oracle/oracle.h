@@ -96,7 +96,8 @@ int orc_blend_stats(const double* x, int64_t k, const orc_camera* cam,
                     int64_t* contributing);
 /* restated tile binning (the GPU build's new stage; no reference
  * counterpart): depth order of visible splats and per-tile lists.
- * order[n_visible]; tile_start/tile_end[n_tiles]; lists[n_dup].
+ * order[n_visible]; tile_start/tile_end[n_tiles] (empty tiles [0, 0));
+ * lists[n_dup].
  * Call with lists == NULL to get n_dup only. */
 int orc_binning(const double* x, int64_t k, const orc_camera* cam,
                 const orc_render_opts* ro, int32_t tile, int32_t* n_visible,

@@ -491,7 +491,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
         Timed t(c, KC_DEPTH_SORT);
         depth_sort_and_scan(c.st, b, K);
     }
-    c.launches += 1 + 9 + 3;  // project, onesweep sort (histogram + 8 passes), counts + scan
+    c.launches += 1 + 6 + 1 + 3;  // project, onesweep sort (histogram + 5 passes), tie fix, counts + scan
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs.n_dup, b.off_r + K, sizeof(long long),
                               cudaMemcpyDeviceToHost, c.st));
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs, &c.dstat->vs, offsetof(ViewStatus, n_dup),

@@ -16,6 +16,36 @@
 namespace sgtr {
 namespace {
 
+// After a radix sort on key bits [kDepthLoBit, 64) only, keys that agree on
+// those bits keep their input (= splat index) order; each such run is put
+// into full-key order here (insertion sort, stable, so equal keys stay in
+// index order) -- the same (depth, index) order as a full 64-bit sort
+// (render.cpp:83-87).  Runs are rare and short: the ignored 24 low bits are
+// below 2^-28 relative depth.
+constexpr int kDepthLoBit = 24;
+
+__global__ void k_fix_depth_ties(unsigned long long* __restrict__ keys, int* __restrict__ ids,
+                                 int K) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= K) return;
+    const unsigned long long hi = keys[i] >> kDepthLoBit;
+    if (i > 0 && (keys[i - 1] >> kDepthLoBit) == hi) return;  // not a run start
+    int e = i + 1;
+    while (e < K && (keys[e] >> kDepthLoBit) == hi) ++e;
+    for (int a = i + 1; a < e; ++a) {
+        const unsigned long long k = keys[a];
+        const int id = ids[a];
+        int b = a - 1;
+        while (b >= i && keys[b] > k) {
+            keys[b + 1] = keys[b];
+            ids[b + 1] = ids[b];
+            --b;
+        }
+        keys[b + 1] = k;
+        ids[b + 1] = id;
+    }
+}
+
 __global__ void k_gather_counts(const int* __restrict__ sorted_ids,
                                 const int* __restrict__ tcount, int K,
                                 long long* __restrict__ cnt) {
@@ -152,7 +182,7 @@ size_t depth_sort_temp_bytes(int K) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
                                     (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr,
-                                    K);
+                                    K, kDepthLoBit, 64);
     return bytes;
 }
 
@@ -175,7 +205,9 @@ void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
     if (K > 0) {
         size_t bytes = b.temp_bytes;
         SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.keys, b.keys_alt, b.ids,
-                                                  b.ids_alt, K, 0, 64, st));
+                                                  b.ids_alt, K, kDepthLoBit, 64, st));
+        k_fix_depth_ties<<<ceil_div(K, 256), 256, 0, st>>>(b.keys_alt, b.ids_alt, K);
+        SGTR_CUDA(cudaGetLastError());
     }
     // counts in depth-rank order (reuses keys as a long long scratch of K+1)
     long long* cnt = reinterpret_cast<long long*>(b.keys);

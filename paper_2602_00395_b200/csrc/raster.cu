@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
 // walked back to front 32 positions at a time, the passing fragments' raster
 // fields are fetched by their filtering lanes in parallel into a
 // warp-private shared batch, then processed last-to-first.
-template <int WPB>
+template <int WPB, bool kSmemRed = true>
 __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
     k_raster_vjp_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                         const double* __restrict__ adj, const double* __restrict__ tfinal,
@@ -1001,7 +1001,14 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
             }
             if (!__any_sync(kFull, contrib)) continue;
             double* o = part + ((long long)j * kWarps + warp) * kAdj;
-            warp_reduce9_smem(g, lane, s_red[lw], o);
+            if (kSmemRed) {
+                warp_reduce9_smem(g, lane, s_red[lw], o);
+            } else {
+                double v, v8;
+                warp_reduce9(g, lane, v, v8);
+                if ((lane & 3) == 0) o[lane >> 2] = v;
+                if (lane == 0) o[8] = v8;
+            }
             if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
         }
         __syncwarp();
@@ -1257,7 +1264,10 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_staged && g_wpb == 2)
+    if (g_vjp_staged && g_wpb == 2 && !g_smem_red)
+        k_raster_vjp_staged<2, false><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                            part, mask);
+    else if (g_vjp_staged && g_wpb == 2)
         k_raster_vjp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
                                                      mask);
     else if (g_vjp_staged)

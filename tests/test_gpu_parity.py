@@ -180,6 +180,25 @@ def test_binning_edge_cases(sp, orc):
             assert np.array_equal(a, b)
 
 
+def test_depth_order_near_ties(sp, orc):
+    # depths that differ only in their lowest mantissa bits, in reverse index
+    # order, plus exact ties: the depth sort runs on the high key bits and
+    # repairs runs of equal high bits by the full key (binning.cu), which must
+    # still give the reference's (depth, index) order (render.cpp:83-87)
+    k = 300
+    rng = np.random.default_rng(9)
+    z = 2.0 + np.ldexp(np.arange(k)[::-1] % 37, -50)  # 37 distinct, ulp-scale apart
+    mu = np.column_stack([rng.uniform(-0.2, 0.2, k), rng.uniform(-0.2, 0.2, k), z])
+    s = np.full((k, 3), 0.05)
+    q = np.tile([0.0, 0.0, 0.0, 1.0], (k, 1))
+    x = orc.pack(mu, s, q, np.full(k, 0.5), rng.uniform(0, 1, (k, 3)))
+    oc = orc.camera(width=48, height=40, fx=60.0, fy=60.0, cx=24.0, cy=20.0)
+    g = _gpu_binning(sp, x, sp.Camera.from_c(oc))
+    r = orc.binning(x, oc)
+    for a, b in zip(g, r):
+        assert np.array_equal(a, b)
+
+
 # ------------------------------------------------------------------ renderer parity
 def test_rasterize_parity(sp, orc, c1):
     for x in (c1.gt_x, c1.init_x):
