@@ -312,10 +312,10 @@ __global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ so
     for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
     const long long off = off_r[r];
     for (int t = 0; t < cnt; ++t) {
-        const long long jpos = inv[off + t];
-        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * jpos);
+        const long long d = off + t;  // partials are stored by splat-major slot
+        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * d);
         if (m == 0ull) continue;
-        const double* pp = part + jpos * 8 * kAdj;
+        const double* pp = part + d * 8 * kAdj;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
             if ((m >> (8 * w)) & 0xffull) {
@@ -353,14 +353,14 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
     // the <= 8 per-warp partials of each duplicate, in (duplicate, warp)
-    // order; positions and masks of 4 duplicates are fetched together so the
-    // dependent loads overlap (the sum order is unchanged)
+    // order; the partials are stored by splat-major duplicate slot, so a
+    // splat's are contiguous; masks of 4 duplicates are fetched together
     const long long off = off_r[r];
     for (int t0 = 0; t0 < (kPre ? 0 : cnt); t0 += 4) {
         long long jp[4];
         unsigned long long mk[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? (long long)inv[off + t0 + u] : -1;
+        for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? off + t0 + u : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             mk[u] = jp[u] >= 0 ? *reinterpret_cast<const unsigned long long*>(mask + 8 * jp[u])
@@ -420,20 +420,20 @@ __global__ void __launch_bounds__(256) k_partials_to_slots(const int* __restrict
                                                            const double* __restrict__ part,
                                                            const unsigned char* __restrict__ mask,
                                                            double* __restrict__ slots) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * j);
+    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // splat-major slot
+    if (d >= n) return;
+    const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * d);
     double a[kAdj];
 #pragma unroll
     for (int c = 0; c < kAdj; ++c) a[c] = 0.0;
-    const double* pp = part + j * 8 * kAdj;
+    const double* pp = part + d * 8 * kAdj;
 #pragma unroll
     for (int w = 0; w < 8; ++w)
         if ((m >> (8 * w)) & 0xffull) {
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
         }
-    double* o = slots + (long long)kAdj * sorted_d[j];
+    double* o = slots + (long long)kAdj * d;
 #pragma unroll
     for (int c = 0; c < kAdj; ++c) o[c] = a[c];
 }

@@ -744,7 +744,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
 // shared-memory staging, no CTA barriers and no cross-warp reduction are
 // needed.  A warp reduces each fragment's 9 adjoints over its 32 pixels and
 // stores them in its own partial slot (tile-sorted position j, warp w),
-// flagging mask[j * 8 + w]; K11 sums the flagged partials of each duplicate in
+// flagging mask[d * 8 + w] (d = the duplicate's splat-major slot,
+// sorted_d[j]); K11 sums the flagged partials of each duplicate in
 // warp order (deterministic, no atomics).
 template <int kMinBlocks, bool kSmemRed, bool kPrefetch, int WPB = kWarps>
 __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
@@ -875,7 +876,8 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
             }
         }
         if (!__any_sync(kFull, contrib)) continue;
-        double* o = part + ((long long)j * kWarps + warp) * kAdj;
+        const long long dslot = __ldg(tl.sorted_d + j);  // splat-major duplicate slot
+        double* o = part + (dslot * kWarps + warp) * kAdj;
         if (kSmemRed) {
             warp_reduce9_smem(g, lane, s_red[lw], o);
         } else {
@@ -884,7 +886,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
             if ((lane & 3) == 0) o[lane >> 2] = v;
             if (lane == 0) o[8] = v8;
         }
-        if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
+        if (lane == 0) mask[dslot * kWarps + warp] = 1;
     }
     __syncwarp();
     }
@@ -906,6 +908,7 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
     __shared__ __align__(16) StagedRec s_rec[WPB][32];
     __shared__ int4 s_rect[WPB][32];
     __shared__ int s_pos[WPB][32];
+    __shared__ int s_slot[WPB][32];
     const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
@@ -929,6 +932,7 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
     StagedRec* my_rec = s_rec[lw];
     int4* my_rect = s_rect[lw];
     int* my_pos = s_pos[lw];
+    int* my_slot = s_slot[lw];
     for (int top = start + wlast; top > start; top -= 32) {
         const int base = max(start, top - 32);
         const int jj = base + lane;
@@ -953,6 +957,7 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
             o[4] = e;
             my_rect[q] = rr;
             my_pos[q] = jj;
+            my_slot[q] = __ldg(tl.sorted_d + jj);
         }
         __syncwarp();
         for (int e = __popc(m) - 1; e >= 0; --e) {
@@ -1000,7 +1005,8 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
                 }
             }
             if (!__any_sync(kFull, contrib)) continue;
-            double* o = part + ((long long)j * kWarps + warp) * kAdj;
+            const long long dslot = my_slot[e];  // splat-major duplicate slot
+            double* o = part + (dslot * kWarps + warp) * kAdj;
             if (kSmemRed) {
                 warp_reduce9_smem(g, lane, s_red[lw], o);
             } else {
@@ -1009,7 +1015,7 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
                 if ((lane & 3) == 0) o[lane >> 2] = v;
                 if (lane == 0) o[8] = v8;
             }
-            if (lane == 0) mask[(long long)j * kWarps + warp] = 1;
+            if (lane == 0) mask[dslot * kWarps + warp] = 1;
         }
         __syncwarp();
     }
@@ -1113,11 +1119,12 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
         if (!__any_sync(kFull, contrib)) continue;
         double v, v8;
         warp_reduce9(g, lane, v, v8);
-        double* o = part + ((long long)j * kWarps + warp) * kAdj;
+        const long long dslot = __ldg(tl.sorted_d + j);  // splat-major duplicate slot
+        double* o = part + (dslot * kWarps + warp) * kAdj;
         if ((lane & 3) == 0) o[lane >> 2] = v;
         if (lane == 0) {
             o[8] = v8;
-            mask[(long long)j * kWarps + warp] = 1;
+            mask[dslot * kWarps + warp] = 1;
         }
     }
 }
