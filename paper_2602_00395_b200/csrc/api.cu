@@ -336,6 +336,8 @@ struct Ctx {
     std::vector<View> views;
     Buf gt;  // planar targets, one (3, H, W) block per view
     bool has_gt = false;
+    Buf gtmom;  // per view [mu_b (3, H, W) | mbb (3, H, W)] of its target (SSIM windows)
+    bool has_gtmom = false;
     // held-out views for evaluate_scene (any sizes; planar targets packed
     // back to back at eval_off[i])
     std::vector<View> eval_views;
@@ -619,6 +621,14 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
     a.R = img_ptr(c, c.Rf, P);
     a.by0 = by0;
     a.by1 = by1;
+    if ((mode == GRAD || mode == HUTCH) && c.has_gtmom && !c.views.empty() &&
+        W == c.views[0].dc.W && H == c.views[0].dc.H) {
+        // a training view's target: its windowed mean / second moment are
+        // fixed and were filtered once (refresh_gt_moments)
+        const long long off = gt - c.gt.get<double>();
+        if (off >= 0 && off % (3LL * P) == 0 && off / (3LL * P) < (long long)c.views.size())
+            a.bmom = c.gtmom.get<double>() + 2 * off;
+    }
     const int nb = ssim_num_blocks(W, H);
     a.loss_partials = c.partials.as<double>(std::max(nb, 10 * tr_num_blocks(c.K) + 8));
     {
@@ -639,6 +649,30 @@ void residual_adjoint(Ctx& c, int mode, int W, int H, const double* gt, const do
 void check_views(Ctx& c, bool need_gt) {
     if (c.views.empty()) throw invalid("no views set");
     if (need_gt && !c.has_gt) throw invalid("views have no target images");
+}
+
+// the windowed mean and second moment of every training target (k_ssim
+// BMOM), reused by every GRAD / HUTCH SSIM pass over that view
+void refresh_gt_moments(Ctx& c) {
+    c.has_gtmom = false;
+    if (c.views.empty() || !c.has_gt) return;
+    const int W = c.views[0].dc.W, H = c.views[0].dc.H;
+    if (W < 6 || H < 6) return;
+    const long long P = (long long)W * H;
+    double* m = c.gtmom.as<double>(6 * P * c.views.size());
+    for (size_t v = 0; v < c.views.size(); ++v) {
+        SsimArgs a{};
+        a.mode = BMOM;
+        a.W = W;
+        a.H = H;
+        a.a = c.gt.get<double>() + 3 * P * v;
+        a.b = a.a;
+        a.out0 = m + 6 * P * v;
+        a.out1 = m + 6 * P * v + 3 * P;
+        launch_ssim(c.st, a);
+        c.launches += 1;
+    }
+    c.has_gtmom = true;
 }
 
 const double* view_gt(Ctx& c, int v) {
@@ -1156,6 +1190,7 @@ int sgtr_set_views(sgtr_ctx* ctx, const sgtr_camera* cams, int32_t n, const doub
             }
             c.has_gt = true;
         }
+        refresh_gt_moments(c);
         SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
 }
@@ -1175,6 +1210,7 @@ int sgtr_render_targets(sgtr_ctx* ctx, const sgtr_render_options* ro, int32_t qu
             if (quantize) launch_quantize8(c.st, g + 3LL * P * i, 3LL * P);
         }
         c.has_gt = true;
+        refresh_gt_moments(c);
         SGTR_CUDA(cudaStreamSynchronize(c.st));
     });
 }

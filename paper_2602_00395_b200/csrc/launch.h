@@ -121,8 +121,9 @@ enum SsimMode {
     HUTCH,         // u = J t: adjL1 and P, Q, R (K13)
     RES_VJP,       // u given (6P, in `u`): adjL1 and P, Q, R
     SSIM_VJP,      // upstream given (3P planar, in `u`): P, Q, R
-    EVAL           // per-block sums of SSIM and (a-b)^2 into loss_partials
+    EVAL,          // per-block sums of SSIM and (a-b)^2 into loss_partials
                    // [blk] and [nblocks + blk] (mean_ssim, psnr)
+    BMOM           // out0 = windowed mean of b, out1 = windowed E[b^2] (fixed per view)
 };
 struct SsimArgs {
     int mode, W, H;
@@ -130,6 +131,7 @@ struct SsimArgs {
     double lambda, floor;
     double *out0, *out1, *adjl1, *P, *Q, *R, *loss_partials;
     int by0, by1;  // block rows (16 image rows each) to compute; by1 <= 0: all
+    const double* bmom;  // optional (GRAD/HUTCH): [mu_b planes | mbb planes] from BMOM
 };
 int ssim_num_blocks(int W, int H);
 void launch_ssim(cudaStream_t st, const SsimArgs& a);

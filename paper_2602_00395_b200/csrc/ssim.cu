@@ -48,16 +48,23 @@ __device__ __forceinline__ double mk<double>(double v, double) { return v; }
 template <>
 __device__ __forceinline__ Dual mk<Dual>(double v, double d) { return Dual(v, d); }
 
-template <int MODE>
+template <int MODE, bool kPre = false>
 struct ModeTraits {
     static constexpr bool kTangent = MODE == SSIM_JVP || MODE == RES_JVP || MODE == HUTCH;
-    static constexpr int kMoments = kTangent ? 8 : 5;
+    // kPre: the target's windowed mean and second moment (mu_b, mbb) come
+    // precomputed (they are fixed per training view), so only mu_a, maa, mab
+    // (and their tangents) are filtered here
+    static constexpr int kMoments = kPre ? (kTangent ? 6 : 3) : (kTangent ? 8 : 5);
+    static constexpr int MUA = 0, MUB = kPre ? -1 : 1, MAA = kPre ? 1 : 2, MBB = kPre ? -1 : 3,
+                         MAB = kPre ? 2 : 4, DMUA = kPre ? 3 : 5, DMAA = kPre ? 4 : 6,
+                         DMAB = kPre ? 5 : 7;
 };
 
-// moments: 0 mu_a, 1 mu_b, 2 maa, 3 mbb, 4 mab, (5 dmu_a, 6 dmaa, 7 dmab)
-template <int MODE>
+// moments (kPre = false): 0 mu_a, 1 mu_b, 2 maa, 3 mbb, 4 mab, (5 dmu_a, 6 dmaa,
+// 7 dmab); with kPre the b moments are read from args.bmom instead
+template <int MODE, bool kPre = false>
 __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
-    using Tr = ModeTraits<MODE>;
+    using Tr = ModeTraits<MODE, kPre>;
     constexpr int NM = Tr::kMoments;
     extern __shared__ __align__(16) double smem[];
     double* s_a = smem;                      // SY x SX
@@ -96,16 +103,16 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
         for (int d = 0; d < 11; ++d) {
             const int si = sy * SX + tx + d;
             const double w = c_k[d], av = s_a[si], bv = s_b[si];
-            m[0] += w * av;
-            m[1] += w * bv;
-            m[2] += w * av * av;
-            m[3] += w * bv * bv;
-            m[4] += w * av * bv;
+            m[Tr::MUA] += w * av;
+            if (!kPre) m[Tr::MUB < 0 ? 0 : Tr::MUB] += w * bv;
+            m[Tr::MAA] += w * av * av;
+            if (!kPre) m[Tr::MBB < 0 ? 0 : Tr::MBB] += w * bv * bv;
+            m[Tr::MAB] += w * av * bv;
             if (Tr::kTangent) {
                 const double dv = s_da[si];
-                m[5] += w * dv;
-                m[6] += w * 2.0 * av * dv;
-                m[7] += w * bv * dv;
+                m[Tr::DMUA] += w * dv;
+                m[Tr::DMAA] += w * 2.0 * av * dv;
+                m[Tr::DMAB] += w * bv * dv;
             }
         }
 #pragma unroll
@@ -129,11 +136,17 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
     if (gx < W && gy < H) {
         const long long p = (long long)gy * W + gx;
         const long long pi = c * P + p;
+        if (MODE == BMOM) {  // the target's moments for later kPre launches
+            args.out0[pi] = m[1];
+            args.out1[pi] = m[3];
+            continue;
+        }
         // SSIM (with its tangent in the JVP modes), ssim.cpp:50-58
-        const S mu_a = mk<S>(m[0], Tr::kTangent ? m[5] : 0.0);
-        const S maa = mk<S>(m[2], Tr::kTangent ? m[6] : 0.0);
-        const S mab = mk<S>(m[4], Tr::kTangent ? m[7] : 0.0);
-        const double mu_b = m[1], mbb = m[3];
+        const S mu_a = mk<S>(m[Tr::MUA], Tr::kTangent ? m[Tr::DMUA] : 0.0);
+        const S maa = mk<S>(m[Tr::MAA], Tr::kTangent ? m[Tr::DMAA] : 0.0);
+        const S mab = mk<S>(m[Tr::MAB], Tr::kTangent ? m[Tr::DMAB] : 0.0);
+        const double mu_b = kPre ? args.bmom[pi] : m[Tr::MUB < 0 ? 0 : Tr::MUB];
+        const double mbb = kPre ? args.bmom[3 * P + pi] : m[Tr::MBB < 0 ? 0 : Tr::MBB];
         const S n1 = 2.0 * mu_a * mu_b + kC1;
         const S d1 = mu_a * mu_a + mu_b * mu_b + kC1;
         const S n2 = 2.0 * (mab - mu_a * mu_b) + kC2;
@@ -346,21 +359,21 @@ void init_constants() {
     g_kernel_ready = true;
 }
 
-template <int MODE>
+template <int MODE, bool kPre = false>
 void run_ssim(cudaStream_t st, const SsimArgs& a) {
-    using Tr = ModeTraits<MODE>;
+    using Tr = ModeTraits<MODE, kPre>;
     const size_t smem = sizeof(double) * (SY * SX * (Tr::kTangent ? 3 : 2) +
                                           Tr::kMoments * SY * TX);
     static bool attr = false;
     if (!attr) {
-        SGTR_CUDA(cudaFuncSetAttribute(k_ssim<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+        SGTR_CUDA(cudaFuncSetAttribute(k_ssim<MODE, kPre>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     const int by1 = a.by1 > 0 ? a.by1 : ceil_div(a.H, TY);
     if (by1 <= a.by0) return;
     dim3 grid(ceil_div(a.W, TX), by1 - a.by0, 3);
-    k_ssim<MODE><<<grid, kThreads, smem, st>>>(a);
+    k_ssim<MODE, kPre><<<grid, kThreads, smem, st>>>(a);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -375,8 +388,19 @@ void launch_ssim(cudaStream_t st, const SsimArgs& a) {
         case SSIM_JVP: run_ssim<SSIM_JVP>(st, a); break;
         case RES_VEC: run_ssim<RES_VEC>(st, a); break;
         case RES_JVP: run_ssim<RES_JVP>(st, a); break;
-        case GRAD: run_ssim<GRAD>(st, a); break;
-        case HUTCH: run_ssim<HUTCH>(st, a); break;
+        case GRAD:
+            if (a.bmom)
+                run_ssim<GRAD, true>(st, a);
+            else
+                run_ssim<GRAD>(st, a);
+            break;
+        case HUTCH:
+            if (a.bmom)
+                run_ssim<HUTCH, true>(st, a);
+            else
+                run_ssim<HUTCH>(st, a);
+            break;
+        case BMOM: run_ssim<BMOM>(st, a); break;
         case RES_VJP: run_ssim<RES_VJP>(st, a); break;
         case SSIM_VJP: run_ssim<SSIM_VJP>(st, a); break;
         case EVAL: run_ssim<EVAL>(st, a); break;
