@@ -582,3 +582,47 @@ def test_refresh_bands_sum_to_the_view(sp, orc, bands):
     assert np.array_equal(g1, g2)          # the gradient phase is not banded
     assert rel(d2, d1) < 1e-12             # only the summation order differs
     assert rel(x2, x1) < 1e-12
+
+
+# ---- ADAM known-answer tests of the reference on the device (test_optimizer.cpp:204-267)
+def test_kat_adam_zero_gradient_stream(sp, orc):
+    x, ocams, _ = orc.make_check_scene(4, 12, 2, 101)
+    views = [sp.Camera.from_c(c, orc.rasterize(x, c)[0]) for c in ocams]
+    st = sp.OptimizerState(x.size, 9)
+    scene = sp.Scene(x)
+    for _ in range(3):
+        sp.step_adam(st, scene, views, sp.OptimizerOptions())
+    assert np.array_equal(scene.x, x)
+
+
+def test_kat_adam_first_step_is_the_group_rate(sp, orc):
+    x, ocams, gts = orc.make_check_scene(4, 12, 2, 103)
+    views = cams_of(sp, ocams, gts)
+    opt = sp.OptimizerOptions(scene_extent=1.7)
+    st = sp.OptimizerState(x.size, 11)
+    d = sp.step_adam(st, sp.Scene(x), views, opt)
+    a = opt.adam
+    k = x.size // 14
+    lr_pos = 1.7 * a.lr_position * (a.lr_position_final / a.lr_position) ** (
+        1.0 / a.lr_position_decay_steps)
+    lr = np.concatenate([np.full(3 * k, lr_pos), np.full(3 * k, a.lr_scale),
+                         np.full(4 * k, a.lr_rotation), np.full(k, a.lr_opacity),
+                         np.full(3 * k, a.lr_color)])
+    sel = np.abs(st.adam_m) >= 1e-12
+    assert sel.any()
+    ap = np.abs(d.applied_step[sel])
+    # doctest's Approx(lr).epsilon(1e-9): |a - b| < 1e-9 * (1 + max(|a|, |b|))
+    assert np.all(np.abs(ap - lr[sel]) < 1e-9 * (1.0 + np.maximum(ap, lr[sel])))
+
+
+def test_kat_adam_tr_vacuous_region_is_adam(sp, orc):
+    x, ocams, gts = orc.make_check_scene(5, 12, 3, 107)
+    views = cams_of(sp, ocams, gts)
+    a, b = sp.Scene(x), sp.Scene(x)
+    sa, sb = sp.OptimizerState(x.size, 77), sp.OptimizerState(x.size, 77)
+    ob = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e100, 1e100, 10),
+                             caps=sp.RadiusCaps(1e100, 1e100, 1e100, 1e100, 1e100))
+    for _ in range(5):
+        sp.step_adam(sa, a, views, sp.OptimizerOptions())
+        sp.step_adam_tr(sb, b, views, ob)
+    assert np.array_equal(a.x, b.x)

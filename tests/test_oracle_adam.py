@@ -85,3 +85,47 @@ def test_adam_consumes_only_s1_draws(orc):
                       orc.AdamOptions(), want_applied=True)
     g, _ = orc.stochastic_gradient(x, cams, gts, s_expected)
     assert d["gnorm"] == pytest.approx(np.linalg.norm(g), rel=1e-14)
+
+
+# ---- the reference's own ADAM known-answer tests (test_optimizer.cpp:204-267)
+def _lr_table(a, k, t):
+    frac = min(1.0, t / max(1, a.lr_position_decay_steps))
+    lr_pos = a.scene_extent * a.lr_position * (a.lr_position_final / a.lr_position) ** frac
+    return np.concatenate([np.full(3 * k, lr_pos), np.full(3 * k, a.lr_scale),
+                           np.full(4 * k, a.lr_rotation), np.full(k, a.lr_opacity),
+                           np.full(3 * k, a.lr_color)])
+
+
+def test_kat_adam_zero_gradient_stream(orc):  # test_optimizer.cpp:204-217
+    x, cams, _ = orc.make_check_scene(4, 12, 2, 101)
+    gts = [orc.rasterize(x, c)[0] for c in cams]
+    st = orc.State(x.size, 9)
+    before = x.copy()
+    for _ in range(3):
+        orc.step_adam(st, x, cams, gts, orc.TrOptions(), orc.AdamOptions())
+    assert np.array_equal(x, before)
+
+
+def test_kat_adam_first_step_is_the_group_rate(orc):  # test_optimizer.cpp:219-247
+    x, cams, gts = orc.make_check_scene(4, 12, 2, 103)
+    a = orc.AdamOptions(scene_extent=1.7)
+    st = orc.State(x.size, 11)
+    d = orc.step_adam(st, x, cams, gts, orc.TrOptions(), a, want_applied=True)
+    m, _ = st.get_adam()
+    lr = _lr_table(a, x.size // 14, 1)
+    sel = np.abs(m) >= 1e-12
+    assert sel.any()
+    ap = np.abs(d["applied_step"][sel])
+    # doctest's Approx(lr).epsilon(1e-9): |a - b| < 1e-9 * (1 + max(|a|, |b|))
+    assert np.all(np.abs(ap - lr[sel]) < 1e-9 * (1.0 + np.maximum(ap, lr[sel])))
+
+
+def test_kat_adam_tr_vacuous_region_is_adam(orc):  # test_optimizer.cpp:249-267
+    x, cams, gts = orc.make_check_scene(5, 12, 3, 107)
+    xa, xb = x.copy(), x.copy()
+    sa, sb = orc.State(x.size, 77), orc.State(x.size, 77)
+    ob = orc.TrOptions(eps_start=1e100, eps_end=1e100, total_steps=10, caps=(1e100,) * 5)
+    for _ in range(5):
+        orc.step_adam(sa, xa, cams, gts, orc.TrOptions(), orc.AdamOptions())
+        orc.step_adam(sb, xb, cams, gts, ob, orc.AdamOptions(), True)
+    assert np.array_equal(xa, xb)
