@@ -626,3 +626,22 @@ def test_kat_adam_tr_vacuous_region_is_adam(sp, orc):
         sp.step_adam(sa, a, views, sp.OptimizerOptions())
         sp.step_adam_tr(sb, b, views, ob)
     assert np.array_equal(a.x, b.x)
+
+
+def test_kat_refresh_cadence_clip_eps(sp, orc):  # test_optimizer.cpp:163-185
+    x, ocams, gts = orc.make_check_scene(4, 12, 3, 89)
+    views = cams_of(sp, ocams, gts)
+    total = 25
+    opt = _tr_opts(sp, total)
+    st = sp.OptimizerState(x.size, 123)
+    scene = sp.Scene(x)
+    last = st.d_hat
+    for t in range(1, total + 1):
+        d = sp.step_3dgs2tr(st, scene, views, opt)
+        dh = st.d_hat
+        assert (np.linalg.norm(dh - last) > 0.0) == (t % 10 == 1)
+        last = dh
+        assert d.max_step_over_radius <= 1.0
+        assert d.eps == sp.eps_at(opt.schedule, t)
+        assert 0.0 <= d.clip_frac <= 1.0
+    assert st.t == total
