@@ -532,7 +532,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     int* tids = c.tile_ids.as<int>(nd);
     {
         Timed t(c, KC_TILE_BIN);
-        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids, c.inv.as<int>(nd),
+        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids, nullptr,
                         c.trect.as<int4>(nd));
     }
     c.launches += vr.n_dup ? 1 : 0;
@@ -577,7 +577,7 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                            ? c.slots.as<double>((size_t)kAdj * std::max(vr.n_visible, 1))
                            : nullptr;
         launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                          c.off_r.get<long long>(), c.tcount.get<int>(), c.inv.get<int>(), part,
+                          c.off_r.get<long long>(), c.tcount.get<int>(), nullptr, part,
                           mask, zdense, zbits, acc, flag, adj9);
         c.launches += adj9 ? 3 : 2;
         return;

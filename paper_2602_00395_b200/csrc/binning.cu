@@ -158,7 +158,7 @@ __global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restri
     const int d = sorted_d[j];
     const int id = dup_id[d];
     tile_ids[j] = id;
-    inv[d] = (int)j;
+    if (inv) inv[d] = (int)j;  // (optional: nothing on the step path reads it)
     trect[j] = rect[id];
 }
 
