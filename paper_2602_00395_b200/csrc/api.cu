@@ -255,6 +255,7 @@ struct Nccl {
     int (*comm_init_rank)(void**, int, const char*, int) = nullptr;
     int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     const char* (*get_error)(int) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
     void load() {
         if (lib) return;
         lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -263,6 +264,7 @@ struct Nccl {
         all_reduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
             lib, "ncclAllReduce");
         get_error = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+        comm_destroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
         if (!get_unique_id || !all_reduce)
             throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks the required symbols");
     }
@@ -380,6 +382,11 @@ struct Ctx {
 
     ~Ctx() {
         prefetch.reset();
+        if (comm && g_nccl.comm_destroy) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(st);
+            g_nccl.comm_destroy(comm);
+        }
         for (DevStatus* d : {dstat, spare.dstat})
             if (d) cudaFree(d);
         for (DevStatus* h : {hstat, spare.hstat})
@@ -710,7 +717,7 @@ void ensure_tail(Ctx& c, size_t n) {
 }
 
 void allreduce(Ctx& c, double* buf, size_t n) {
-    if (c.nranks <= 1 || n == 0) return;
+    if (!c.comm || n == 0) return;
     g_nccl.check(g_nccl.all_reduce(buf, buf, n, /*ncclFloat64*/ 8, /*ncclSum*/ 0, c.comm, c.st),
                  "ncclAllReduce");
 }
@@ -2402,7 +2409,8 @@ int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t
         if (nranks < 1 || rank < 0 || rank >= nranks) throw invalid("sgtr_comm_init: bad rank");
         c.nranks = nranks;
         c.rank = rank;
-        if (nranks == 1) return;
+        // a 1-rank communicator is created too (it runs the same allreduce
+        // path; tests use it to exercise the NCCL plumbing on one GPU)
         g_nccl.load();
         auto init = (CommInitRankFn)dlsym(g_nccl.lib, "ncclCommInitRank");
         if (!init) throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks ncclCommInitRank");

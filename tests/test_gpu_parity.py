@@ -645,3 +645,26 @@ def test_kat_refresh_cadence_clip_eps(sp, orc):  # test_optimizer.cpp:163-185
         assert d.eps == sp.eps_at(opt.schedule, t)
         assert 0.0 <= d.clip_frac <= 1.0
     assert st.t == total
+
+
+def test_nccl_single_rank_communicator(sp, orc):
+    # the multi-GPU plumbing on one GPU: dlopen of libnccl, ncclGetUniqueId,
+    # ncclCommInitRank (unique id passed by value) and the per-step
+    # ncclAllReduce over a 1-rank communicator must leave results unchanged
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=200, init_splats=200, views=4,
+                                            image_size=32, seed=3))
+    views = cams_of(sp, ds.cams, ds.gts)
+    out = []
+    for use_comm in (False, True):
+        c = sp.Context()
+        c.set_scene(ds.init_x)
+        c.set_views(views)
+        c.state_reset(2)
+        if use_comm:
+            c.comm_init(sp.nccl_unique_id(), 1, 0)
+        for _ in range(3):
+            c.step(_tr_opts(sp, 10, batch_size=2))
+        out.append((c.get_scene(), c.state_get()))
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a, b)
