@@ -165,6 +165,7 @@ _SIGS = {
     "sgtr_shard_views": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, VP,
                                    C.POINTER(C.c_int32)]),
     "sgtr_set_refresh_bands": (C.c_int, [VP, C.c_int32]),
+    "sgtr_set_tr_shards": (C.c_int, [VP, C.c_int32]),
     "sgtr_comm_init": (C.c_int, [VP, VP, C.c_int32, C.c_int32]),
 }
 

@@ -256,6 +256,7 @@ struct Nccl {
     int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     const char* (*get_error)(int) = nullptr;
     int (*comm_destroy)(void*) = nullptr;
+    int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
     void load() {
         if (lib) return;
         lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -265,6 +266,8 @@ struct Nccl {
             lib, "ncclAllReduce");
         get_error = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
         comm_destroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
+        all_gather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(
+            lib, "ncclAllGather");
         if (!get_unique_id || !all_reduce)
             throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks the required symbols");
     }
@@ -378,6 +381,8 @@ struct Ctx {
     size_t htail_n = 0;
     int nranks = 1, rank = 0;
     int refresh_bands = 1;  // bands per rank of each refresh view (sgtr_set_refresh_bands)
+    int tr_shards = 1;      // radius shards run back to back on one rank (sgtr_set_tr_shards)
+    Buf stage;              // shard-major staging for the radius all-gather
     void* comm = nullptr;
 
     ~Ctx() {
@@ -966,20 +971,60 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                               cudaMemcpyHostToDevice, c.st));
     a.bad_index = &c.dstat->bad_index;
     a.degenerate_flag = &c.dstat->degenerate;
-    {
-        Timed t(c, KC_TR_UPDATE);
-        launch_tr_update(c.st, a, 0);
+    // The elementwise part (EMAs, direction, clip, apply) runs on all splats
+    // on every rank; the radii -- the expensive part: Hellinger radii,
+    // rotation certification and bisection -- are sharded over ranks by splat
+    // range and all-gathered before the clip (multi-GPU), or computed shard
+    // by shard on one rank (sgtr_set_tr_shards, which exercises the same
+    // staging).  Radii are per splat, so the result does not depend on the
+    // sharding.
+    const bool multi = c.comm && c.nranks > 1 && a.kind != 1 && !a.ghat_only;
+    const int shards = multi ? c.nranks : (a.kind != 1 && !a.ghat_only ? c.tr_shards : 1);
+    const long long Kp = (c.K + shards - 1) / shards;
+    auto shard_range = [&](int r, int& i0, int& n) {
+        const long long lo = std::min<long long>((long long)r * Kp, c.K);
+        const long long hi = std::min<long long>(lo + Kp, c.K);
+        i0 = (int)lo;
+        n = (int)(hi - lo);
+    };
+    const int r_first = multi ? c.rank : 0, r_last = multi ? c.rank : shards - 1;
+    for (int r = r_first; r <= r_last; ++r) {
+        shard_range(r, a.i0, a.n);
+        a.elementwise = r == r_first;
+        {
+            Timed t(c, KC_TR_UPDATE);
+            launch_tr_update(c.st, a, 0);
+        }
+        {
+            Timed t(c, KC_TR_BISECT);
+            launch_tr_update(c.st, a, 1);
+        }
+        c.launches += 3;
     }
-    {
-        Timed t(c, KC_TR_BISECT);
-        launch_tr_update(c.st, a, 1);
+    if (shards > 1) {
+        // shard-major staging of the radii, all-gather over ranks (a round
+        // trip on one rank)
+        const int npp = 14 + 3 * c.nb;
+        const long long B = (long long)npp * Kp;
+        double* S = c.stage.as<double>(std::max<long long>(B * shards, 1));
+        double* eta = a.eta_buf;
+        for (int r = r_first; r <= r_last; ++r) {
+            int i0, n;
+            shard_range(r, i0, n);
+            launch_stage(c.st, eta, S, c.K, c.nb, Kp, i0, n, true);
+        }
+        if (multi)
+            g_nccl.check(g_nccl.all_gather(S + B * c.rank, S, B, /*ncclFloat64*/ 8, c.comm, c.st),
+                         "ncclAllGather");
+        launch_stage(c.st, eta, S, c.K, c.nb, Kp, 0, c.K, false);
+        c.launches += (r_last - r_first + 1) + 1;
     }
     {
         Timed t(c, KC_TR_APPLY);
         launch_tr_update(c.st, a, 2);
         launch_tr_finalize(c.st, a.partials, nb, c.dstat->tr);
     }
-    c.launches += 4;
+    c.launches += 2;
     SGTR_CUDA(cudaMemcpyAsync(&c.hstat->bad_index, &c.dstat->bad_index,
                               offsetof(DevStatus, scalar) - offsetof(DevStatus, bad_index),
                               cudaMemcpyDeviceToHost, c.st));
@@ -2399,6 +2444,13 @@ int sgtr_set_refresh_bands(sgtr_ctx* ctx, int32_t bands_per_rank) {
     return guarded([&] {
         if (bands_per_rank < 1) throw invalid("sgtr_set_refresh_bands: need >= 1 band");
         ctx_ref(ctx).refresh_bands = bands_per_rank;
+    });
+}
+
+int sgtr_set_tr_shards(sgtr_ctx* ctx, int32_t shards) {
+    return guarded([&] {
+        if (shards < 1) throw invalid("sgtr_set_tr_shards: need >= 1 shard");
+        ctx_ref(ctx).tr_shards = shards;
     });
 }
 

@@ -315,19 +315,25 @@ __device__ void block_reduce5(double* v, int bad, double* out, int* bad_out) {
 
 // K14a: EMAs, Newton direction and all radii; rotation axes whose Taylor
 // radius fails certification are queued for K14b
+//
+// With `elementwise` the launch covers all K splats (EMAs, direction, the
+// block partials) and computes the radii of the splats in [i0, i0 + n);
+// without it, it covers [i0, i0 + n) and computes only their radii (the
+// other shards of a sharded update).
 __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ew = a.elementwise;
+    const int i = (ew ? 0 : a.i0) + blockIdx.x * blockDim.x + threadIdx.x;
     const long long K = a.K;
     double v[5] = {0, 0, 0, 0, 0};  // sum g^2, sum dx^2
-    if (i < a.K) {
+    if (i < (ew ? a.K : a.i0 + a.n)) {
         const Prim p = load_prim(a.x, K, i);
         const bool degenerate =
             p.q[0] * p.q[0] + p.q[1] * p.q[1] + p.q[2] * p.q[2] + p.q[3] * p.q[3] < 1e-24;
         // shd_radii (and its degenerate-quaternion throw) runs for the
         // trust-region kinds only
-        if (!a.ghat_only && a.kind != 1 && degenerate) atomicOr(a.degenerate_flag, 1);
+        if (ew && !a.ghat_only && a.kind != 1 && degenerate) atomicOr(a.degenerate_flag, 1);
         const int npp = 14 + 3 * a.nb;
-        if (a.kind != 0) {
+        if (ew && a.kind != 0) {
             // adam_direction (optimizer.cpp:153-185); SH coefficients at the
             // colour rate / 20 (extension)
             for (int j = 0; j < npp; ++j) {
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
                 a.dx_buf[k] = dx;
             }
         }
-        for (int j = 0; j < npp && a.kind == 0; ++j) {
+        for (int j = 0; j < npp && ew && a.kind == 0; ++j) {
             const long long k = coord_index(K, a.nb, i, j);
             const double g = a.g_acc[k] * a.gscale;
             v[0] += g * g;
@@ -365,7 +371,8 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
             v[1] += dx * dx;
             a.dx_buf[k] = dx;
         }
-        if (!a.ghat_only && a.kind != 1 && !degenerate) {
+        const bool in_shard = i >= a.i0 && i < a.i0 + a.n;
+        if (in_shard && !a.ghat_only && a.kind != 1 && !degenerate) {
             double eta[14];
             radius_mean(p, a.eps, a.caps[0], eta);
             for (int c = 0; c < 3; ++c) {
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
                     a.eta_buf[14 * K + 3LL * a.nb * i + 3 * m + c] = eta[11 + c] / sh_max(m);
         }
     }
-    block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
+    if (ew) block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
 }
 
 // K14a': one thread per (splat, rotation axis) (trust_region.cpp:198-234):
@@ -391,8 +398,8 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
 // rotation-only H^2; axes failing certification are queued for K14b
 __global__ void __launch_bounds__(kThreads) k_tr_rot(TrArgs a) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= 4LL * a.K) return;
-    const int i = (int)(t >> 2), c = (int)(t & 3);
+    if (t >= 4LL * a.n) return;
+    const int i = a.i0 + (int)(t >> 2), c = (int)(t & 3);
     const long long K = a.K;
     const Prim p = load_prim(a.x, K, i);
     const long long k = 6 * K + 4LL * i + c;
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_bisect(TrArgs a) {
 
 // K14c: clip, step statistics, apply and clamp (optimizer.cpp:124-142)
 __global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // all K splats
     const long long K = a.K;
     double v[5] = {0, 0, 0, 0, 0};  // -, -, sum clipped^2, n clipped, max ratio
     int bad = INT_MAX;
@@ -529,24 +536,55 @@ int tr_num_blocks(int K) { return ceil_div(K, kThreads); }
 
 void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
     if (a.K == 0) return;
-    const int nb = tr_num_blocks(a.K);
+    const int nbK = tr_num_blocks(a.K);
     if (phase == 0) {
         SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
-        k_tr_prepare<<<nb, kThreads, 0, st>>>(a);
-        SGTR_CUDA(cudaGetLastError());
-        if (!a.ghat_only && a.kind != 1) {
-            k_tr_rot<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
+        const int nbp = a.elementwise ? nbK : tr_num_blocks(a.n);
+        if (nbp > 0) {
+            k_tr_prepare<<<nbp, kThreads, 0, st>>>(a);
             SGTR_CUDA(cudaGetLastError());
         }
-        if (a.ghat_only)
-            SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nb, 0, sizeof(double) * 5 * nb, st));
-    } else if (phase == 1 && !a.ghat_only && a.kind != 1) {
-        k_tr_bisect<<<ceil_div(4LL * a.K, kThreads), kThreads, 0, st>>>(a);
+        if (!a.ghat_only && a.kind != 1 && a.n > 0) {
+            k_tr_rot<<<ceil_div(4LL * a.n, kThreads), kThreads, 0, st>>>(a);
+            SGTR_CUDA(cudaGetLastError());
+        }
+        if (a.ghat_only && a.elementwise)
+            SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nbK, 0, sizeof(double) * 5 * nbK, st));
+    } else if (phase == 1 && !a.ghat_only && a.kind != 1 && a.n > 0) {
+        k_tr_bisect<<<ceil_div(4LL * a.n, kThreads), kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
     } else if (phase == 2 && !a.ghat_only) {
-        k_tr_apply<<<nb, kThreads, 0, st>>>(a);
+        k_tr_apply<<<nbK, kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
     }
+}
+
+// shard-major staging of a scene-layout vector (sharded trust-region update):
+// shard r = splats [r Kp, (r+1) Kp) occupies block r of B = (14 + 3 nb) Kp
+// doubles, itself in the scene's group-major layout over Kp splats, so one
+// reduce-scatter / all-gather moves each shard as a contiguous block
+__global__ void k_stage(double* __restrict__ vec, double* __restrict__ staged, long long K, int nb,
+                        long long Kp, long long i0, long long n, int to_staged) {
+    const int npp = 14 + 3 * nb;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * npp) return;
+    const long long i = i0 + t / npp;
+    const int j = (int)(t % npp);
+    const long long r = i / Kp, il = i - r * Kp;
+    const long long si = r * npp * Kp + coord_index(Kp, nb, (int)il, j);
+    const long long vi = coord_index(K, nb, (int)i, j);
+    if (to_staged)
+        staged[si] = vec[vi];
+    else
+        vec[vi] = staged[si];
+}
+
+void launch_stage(cudaStream_t st, double* vec, double* staged, long long K, int nb, long long Kp,
+                  long long i0, long long n, bool to_staged) {
+    if (n <= 0) return;
+    k_stage<<<ceil_div(n * (14 + 3 * nb), 256), 256, 0, st>>>(vec, staged, K, nb, Kp, i0, n,
+                                                             to_staged ? 1 : 0);
+    SGTR_CUDA(cudaGetLastError());
 }
 
 // partials: [nblocks][5] from K14a (sum g^2, sum dx^2) then [nblocks][5] from

@@ -508,6 +508,11 @@ class Context:
         """Split each refresh view into nranks * bands_per_rank row bands."""
         check(lib().sgtr_set_refresh_bands(self._h, bands_per_rank))
 
+    def set_tr_shards(self, shards: int) -> None:
+        """Run the trust-region radii as `shards` splat-range shards (the
+        multi-GPU split, back to back on one rank)."""
+        check(lib().sgtr_set_tr_shards(self._h, shards))
+
     def comm_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         check(lib().sgtr_comm_init(self._h, buf, nranks, rank))

@@ -668,3 +668,28 @@ def test_nccl_single_rank_communicator(sp, orc):
     assert np.array_equal(out[0][0], out[1][0])
     for a, b in zip(out[0][1], out[1][1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("shards", [3, 7])
+@pytest.mark.parametrize("kind", ["3dgs2tr", "adam-tr"])
+def test_sharded_radii_match_unsharded(sp, orc, shards, kind):
+    # the multi-GPU trust-region split (radii by splat range, shard-major
+    # staging, all-gather) run back to back on one GPU: bit-identical steps
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=500, init_splats=500, views=4,
+                                            image_size=40, seed=13))
+    views = cams_of(sp, ds.cams, ds.gts)
+    out = []
+    for s in (1, shards):
+        c = sp.Context()
+        c.set_scene(ds.init_x)
+        c.set_views(views)
+        c.state_reset(4)
+        c.set_tr_shards(s)
+        diags = [c.step(_tr_opts(sp, 10, batch_size=2, kind=kind)) for _ in range(3)]
+        out.append((c.get_scene(), c.state_get(), c.state_get_adam(), diags))
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1][:2] + out[0][2], out[1][1][:2] + out[1][2]):
+        assert np.array_equal(a, b)
+    for da, db in zip(out[0][3], out[1][3]):
+        assert (da.step_post, da.clip_frac, da.max_step_over_radius) == \
+            (db.step_post, db.clip_frac, db.max_step_over_radius)
