@@ -897,8 +897,8 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
 // walked back to front 32 positions at a time, the passing fragments' raster
 // fields are fetched by their filtering lanes in parallel into a
 // warp-private shared batch, then processed last-to-first.
-template <int WPB, bool kSmemRed = true>
-__global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
+template <int WPB, bool kSmemRed = true, int kMinB = 3>
+__global__ void __launch_bounds__(32 * WPB, kMinB * (kWarps / WPB))
     k_raster_vjp_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                         const double* __restrict__ adj, const double* __restrict__ tfinal,
                         const int* __restrict__ last, double* __restrict__ part,
@@ -1004,9 +1004,20 @@ __global__ void __launch_bounds__(32 * WPB, 3 * (kWarps / WPB))
                     T = t_in;
                 }
             }
-            if (!__any_sync(kFull, contrib)) continue;
+            const unsigned cm = __ballot_sync(kFull, contrib);
+            if (cm == 0u) continue;
             const long long dslot = my_slot[e];  // splat-major duplicate slot
             double* o = part + (dslot * kWarps + warp) * kAdj;
+            if ((cm & (cm - 1u)) == 0u) {
+                // a single contributing pixel: its adjoints are the partial
+                // (the other lanes' terms are exact zeros)
+                if (contrib) {
+#pragma unroll
+                    for (int c = 0; c < kAdj; ++c) o[c] = g[c];
+                    mask[dslot * kWarps + warp] = 1;
+                }
+                continue;
+            }
             if (kSmemRed) {
                 warp_reduce9_smem(g, lane, s_red[lw], o);
             } else {
@@ -1274,6 +1285,9 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
     if (g_vjp_staged && g_wpb == 2 && !g_smem_red)
         k_raster_vjp_staged<2, false><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                             part, mask);
+    else if (g_vjp_staged && g_wpb == 2 && g_vjp_min_blocks == 4)
+        k_raster_vjp_staged<2, true, 4><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
+                                                              last, part, mask);
     else if (g_vjp_staged && g_wpb == 2)
         k_raster_vjp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
                                                      mask);
