@@ -41,6 +41,10 @@ CONFIGS = {
     "c3": (1_000_000, 64, 1920, 1080, 8, 0),
     "c2": (100_000, 16, 512, 512, 8, 3),
     "c1": (10_000, 4, 128, 128, 1, 0),
+    # BASELINE configs 4-5 (multi-GPU scale; the 1080p resolution and 64 views
+    # are assumed)
+    "c4": (3_000_000, 64, 1920, 1080, 32, 0),
+    "c5": (10_000_000, 64, 1920, 1080, 8, 0),
 }
 
 
