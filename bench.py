@@ -429,10 +429,16 @@ def main():
     dom = max(ktimes, key=lambda n: ktimes[n][1])
     cnt, tot = ktimes[dom]
     avg_ms = tot / max(cnt, 1)
+    traffic = None
+    try:  # per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[dom]["bytes"]
+    except Exception:
+        pass
     if dom in flops_per:
         achieved = flops_per[dom] / (avg_ms * 1e-3) / 1e12
         roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": fp64_peak,
-                    "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                    "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                    "traffic_note": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
                     "peak_source": "FP64 FMA-pipe microbenchmark on this GPU (sgtr_fp64_peak); "
                                    "MEASURED_PEAKS.json has no FP64 figure",
                     "work": f"{flops_per[dom]:.4g} FP64 flops/launch = 32 E + k C with "
