@@ -595,6 +595,8 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
         return;
     }
     double* slots = c.slots.as<double>((size_t)kAdj * nd);
+    if (vr.tl.row0 != 0 || vr.tl.row1 != vr.tl.tiles_y)  // a band: other tiles' slots stay 0
+        SGTR_CUDA(cudaMemsetAsync(slots, 0, sizeof(double) * kAdj * nd, c.st));
     {
         Timed t(c, KC_RASTER_VJP);
         launch_raster_vjp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
