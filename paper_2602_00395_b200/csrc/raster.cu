@@ -1032,6 +1032,142 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * (kWarps / WPB))
     }
 }
 
+// ------------------------------------------------------------------ K10, batch-staged, 2 px/lane
+// As k_raster_vjp_staged, but a warp owns an 8x8 block (lane: column
+// lane & 7, rows lane >> 3 and 4 + (lane >> 3)): one list walk, record fetch
+// and 9-value reduction per entry now serve 64 pixels, and the two pixels'
+// independent recurrences give each lane instruction-level parallelism.  A
+// tile is 4 such warps (partial slots 0..3 of the duplicate).
+template <int WPB, int kMinB = 10>
+__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
+    k_raster_vjp_staged2(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                         const double* __restrict__ adj, const double* __restrict__ tfinal,
+                         const int* __restrict__ last, double* __restrict__ part,
+                         unsigned char* __restrict__ mask) {
+    constexpr int SUB = 4 / WPB;
+    __shared__ double s_red[WPB][kRedScratch];
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    __shared__ int s_slot[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;  // 0..3: 8x8 block of the tile
+    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
+    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
+    const int px = bx0 + (lane & 7);
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H;
+    double u0[2], u1[2], u2[2], T[2], b0[2], b1[2], b2[2];
+    int lastp[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = by0 + (lane >> 3) + 4 * k;
+        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
+        lastp[k] = 0;
+        if (px < W && py < H) {
+            const long long p = (long long)py * W + px;
+            u0[k] = adj[p];
+            u1[k] = adj[P + p];
+            u2[k] = adj[2 * P + p];
+            T[k] = tfinal[p];
+            lastp[k] = last[p];
+            // pixels with an all-zero adjoint are skipped (render.cpp:283)
+            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;
+        }
+        b0[k] = ro.bg[0] * T[k];
+        b1[k] = ro.bg[1] * T[k];
+        b2[k] = ro.bg[2] * T[k];
+    }
+    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    int* my_slot = s_slot[lw];
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < top) {
+            rr = __ldg(tl.trect + jj);
+            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+            my_slot[q] = __ldg(tl.sorted_d + jj);
+        }
+        __syncwarp();
+        for (int e = __popc(m) - 1; e >= 0; --e) {
+            const int j = my_pos[e];
+            const int rel = j - start;
+            const int4 r4 = my_rect[e];
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            const bool colin = px >= r4.x && px <= r4.z;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int py = by0 + (lane >> 3) + 4 * k;
+                if (!(rel < lastp[k] && colin && py >= r4.y && py <= r4.w)) continue;
+                const StagedRec r = my_rec[e];
+                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+                const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
+                const double gauss = fast_exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], gauss);
+                const bool clamped = abar >= ro.alpha_clamp;
+                if (clamped) abar = ro.alpha_clamp;
+                if (abar < ro.alpha_skip) continue;
+                contrib = true;
+                const double rom = 1.0 / __dsub_rn(1.0, abar);
+                const double t_in = T[k] * rom;
+                const double at = abar * t_in;
+                g[6] += u0[k] * at;
+                g[7] += u1[k] * at;
+                g[8] += u2[k] * at;
+                const double dab = u0[k] * (f[R_C0] * t_in - b0[k] * rom) +
+                                   u1[k] * (f[R_C1] * t_in - b1[k] * rom) +
+                                   u2[k] * (f[R_C2] * t_in - b2[k] * rom);
+                b0[k] += f[R_C0] * at;
+                b1[k] += f[R_C1] * at;
+                b2[k] += f[R_C2] * at;
+                if (!clamped) {
+                    g[5] += gauss * dab;
+                    const double de = abar * dab;
+                    g[2] += de * (-0.5 * dx * dx);
+                    g[3] += de * (-dx * dy);
+                    g[4] += de * (-0.5 * dy * dy);
+                    g[0] += de * (f[R_I00] * dx + f[R_I01] * dy);
+                    g[1] += de * (f[R_I01] * dx + f[R_I11] * dy);
+                }
+                T[k] = t_in;
+            }
+            const unsigned cm = __ballot_sync(kFull, contrib);
+            if (cm == 0u) continue;
+            const long long dslot = my_slot[e];
+            double* o = part + (dslot * kWarps + warp) * kAdj;
+            warp_reduce9_smem(g, lane, s_red[lw], o);
+            if (lane == 0) mask[dslot * kWarps + warp] = 1;
+        }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ K10, PPL pixels per lane
 // As k_raster_vjp_warp, but each lane owns PPL pixels of one column (rows
 // r, r+2, ..): a warp covers 16 x 2*PPL pixels, sums each fragment's adjoints
@@ -1215,7 +1351,7 @@ const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
 const int g_fwd_warp = knob("SGTR_FWD_WARP", 2);  // 2: batch-staged, 1: chunk-filtered
-const int g_vjp_staged = knob("SGTR_VJP_STAGED", 1);  // batch-staged K10
+const int g_vjp_staged = knob("SGTR_VJP_STAGED", 2);  // 2: batch-staged K10, 2 px/lane
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
 // warps per CTA of the warp-filtered forward / VJP kernels
@@ -1282,7 +1418,19 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_staged && g_wpb == 2 && !g_smem_red)
+    if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 12)
+        k_raster_vjp_staged2<2, 12><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                           part, mask);
+    else if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 8)
+        k_raster_vjp_staged2<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                          part, mask);
+    else if (g_vjp_staged == 2 && g_wpb == 2)
+        k_raster_vjp_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                      mask);
+    else if (g_vjp_staged == 2)
+        k_raster_vjp_staged2<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                      mask);
+    else if (g_vjp_staged && g_wpb == 2 && !g_smem_red)
         k_raster_vjp_staged<2, false><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                             part, mask);
     else if (g_vjp_staged && g_wpb == 2 && g_vjp_min_blocks == 4)
