@@ -393,6 +393,102 @@ __global__ void __launch_bounds__(32 * WPB)
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K7, batch-staged, 2 px/lane
+// k_raster_fwd_staged with 8x8 warp blocks (the layout of k_raster_vjp_staged2)
+template <int WPB, int kMinB = 10>
+__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
+    k_raster_fwd_staged2(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                         double* __restrict__ img, double* __restrict__ tfinal,
+                         int* __restrict__ last) {
+    constexpr int SUB = 4 / WPB;
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
+    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
+    const int px = bx0 + (lane & 7);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T[2] = {1.0, 1.0}, c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+    bool done[2];
+    int processed[2] = {end - start, end - start};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) done[k] = !(px < W && by0 + (lane >> 3) + 4 * k < H);
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done[0] && done[1])) break;
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < end) {
+            rr = __ldg(tl.trect + jj);
+            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+        }
+        __syncwarp();
+        const int n = __popc(m);
+        for (int e = 0; e < n; ++e) {
+            const int4 r4 = my_rect[e];
+            const bool colin = px >= r4.x && px <= r4.z;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int py = by0 + (lane >> 3) + 4 * k;
+                if (done[k] || !colin || py < r4.y || py > r4.w) continue;
+                const StagedRec r = my_rec[e];
+                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+                const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T[k];
+                    c0[k] += f[R_C0] * w;
+                    c1[k] += f[R_C1] * w;
+                    c2[k] += f[R_C2] * w;
+                    T[k] = __dmul_rn(T[k], __dsub_rn(1.0, abar));
+                    if (T[k] < ro.t_stop) {
+                        done[k] = true;
+                        processed[k] = my_pos[e] - start + 1;
+                    }
+                }
+            }
+            if (__all_sync(kFull, done[0] && done[1])) break;
+        }
+        __syncwarp();
+    }
+    const long long P = (long long)W * H;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = by0 + (lane >> 3) + 4 * k;
+        if (px >= W || py >= H) continue;
+        const long long p = (long long)py * W + px;
+        img[p] = c0[k] + ro.bg[0] * T[k];
+        img[P + p] = c1[k] + ro.bg[1] * T[k];
+        img[2 * P + p] = c2[k] + ro.bg[2] * T[k];
+        tfinal[p] = T[k];
+        last[p] = processed[k];
+    }
+}
+
 // ------------------------------------------------------------------ K12 (raster), warp-filtered
 // Forward-mode tangent image with the same chunked, warp-filtered walk as
 // k_raster_fwd_warp; records and tangent records read through L1.
@@ -1368,7 +1464,9 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp == 2) {
+    else if (g_fwd_warp == 3) {
+        k_raster_fwd_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    } else if (g_fwd_warp == 2) {
         if (g_fwd_wpb == 2)
             k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
         else
