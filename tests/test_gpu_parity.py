@@ -693,3 +693,40 @@ def test_sharded_radii_match_unsharded(sp, orc, shards, kind):
     for da, db in zip(out[0][3], out[1][3]):
         assert (da.step_post, da.clip_frac, da.max_step_over_radius) == \
             (db.step_post, db.clip_frac, db.max_step_over_radius)
+
+
+# ---- more of the reference's renderer / optimizer KATs on the device
+def test_kat_transmittance_range_and_finite_image(sp, orc):  # test_render.cpp:102-112
+    x, ocams, _ = orc.make_check_scene(12, 16, 2, 7)
+    for oc in ocams:
+        r = sp.rasterize(sp.Scene(x), sp.Camera.from_c(oc))
+        assert np.all(r.t_final >= 0.0) and np.all(r.t_final <= 1.0)
+        assert np.all(np.isfinite(r.color))
+
+
+def test_kat_full_batch_is_the_single_view_average(sp, orc):  # test_optimizer.cpp:62-75
+    x, ocams, gts = orc.make_check_scene(5, 12, 4, 67)
+    views = cams_of(sp, ocams, gts)
+    full, _ = sp.stochastic_gradient(sp.Scene(x), views, list(range(4)))
+    mean = sum(sp.stochastic_gradient(sp.Scene(x), views, [i])[0] for i in range(4)) / 4.0
+    assert np.linalg.norm(full - mean) / max(1e-30, np.linalg.norm(full)) <= 1e-12
+
+
+def test_kat_invisible_splat_zero_diagonal(sp, orc):  # test_optimizer.cpp:110-130
+    x, ocams, gts = orc.make_check_scene(4, 12, 2, 79)
+    k = 4
+    mu, s, q, a, c = orc.unpack(x)
+    mu = np.vstack([mu, [0.0, 0.0, 100.0]])  # behind every ring camera
+    s, q = np.vstack([s, s[0]]), np.vstack([q, q[0]])
+    a, c = np.concatenate([a, a[:1]]), np.vstack([c, c[0]])
+    x2 = orc.pack(mu, s, q, a, c)
+    views = cams_of(sp, ocams, gts)
+    rng = sp.Rng(5)
+    d = sp.hutchinson_diag(sp.Scene(x2), views, [0, 1], 2, sp.rademacher_probes(rng, x2.size))
+    kk = k  # index of the hidden splat (K = 5)
+    K = k + 1
+    idx = [3 * kk + c_ for c_ in range(3)] + [3 * K + 3 * kk + c_ for c_ in range(3)] + \
+          [6 * K + 4 * kk + c_ for c_ in range(4)] + [10 * K + kk] + \
+          [11 * K + 3 * kk + c_ for c_ in range(3)]
+    assert np.all(d[idx] == 0.0)
+    assert np.any(d != 0.0)
