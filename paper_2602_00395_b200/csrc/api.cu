@@ -358,9 +358,10 @@ struct Ctx {
     Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
-    // second view lane (stream + per-view workspace), swapped in by use_lane
-    // so consecutive gradient views overlap: one view's projection, sorts,
-    // binning and SSIM run beside the other's raster passes
+    // further view lanes (stream + per-view workspace), swapped in by
+    // use_lane so consecutive gradient views overlap: one view's projection,
+    // sorts, binning and SSIM run beside another's raster passes
+    static constexpr int kMaxLanes = 3;
     struct Lane {
         cudaStream_t st = nullptr;
         DevStatus* dstat = nullptr;
@@ -373,10 +374,11 @@ struct Ctx {
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
-    } spare;
+    } spare[kMaxLanes - 1];
     int cur_lane = 0;
-    Buf gacc1;                   // lane 1's gradient accumulator
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int slot_of[kMaxLanes] = {-1, 0, 1};  // where each lane's workspace sits (-1: active)
+    Buf gacc[kMaxLanes];         // lanes 1.. accumulate their gradients here
+    cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
     double* htail = nullptr;     // pinned staging for the fused tail
     size_t htail_n = 0;
     int nranks = 1, rank = 0;
@@ -392,15 +394,18 @@ struct Ctx {
             cudaStreamSynchronize(st);
             g_nccl.comm_destroy(comm);
         }
-        for (DevStatus* d : {dstat, spare.dstat})
-            if (d) cudaFree(d);
-        for (DevStatus* h : {hstat, spare.hstat})
-            if (h) cudaFreeHost(h);
+        if (dstat) cudaFree(dstat);
+        if (hstat) cudaFreeHost(hstat);
+        if (st) cudaStreamDestroy(st);
+        for (Lane& l : spare) {
+            if (l.dstat) cudaFree(l.dstat);
+            if (l.hstat) cudaFreeHost(l.hstat);
+            if (l.st) cudaStreamDestroy(l.st);
+        }
         if (htail) cudaFreeHost(htail);
-        for (cudaEvent_t e : {ev_fork, ev_join})
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        for (cudaEvent_t e : ev_join)
             if (e) cudaEventDestroy(e);
-        for (cudaStream_t s : {st, spare.st})
-            if (s) cudaStreamDestroy(s);
     }
     int nb = 0;  // SH coefficients per channel beyond DC ((d+1)^2 - 1; extension)
     long long dim() const { return (14LL + 3LL * nb) * K; }
@@ -423,20 +428,29 @@ void bind(Ctx& c) { SGTR_CUDA(cudaSetDevice(c.device)); }
 // make lane L the context's current stream + per-view workspace
 void use_lane(Ctx& c, int L) {
     if (L == c.cur_lane) return;
-    std::swap(c.st, c.spare.st);
-    std::swap(c.dstat, c.spare.dstat);
-    std::swap(c.hstat, c.spare.hstat);
-#define SGTR_SWAP(n)                     \
-    std::swap(c.n.p, c.spare.n.p);       \
-    std::swap(c.n.bytes, c.spare.n.bytes);
+    const int slot = c.slot_of[L];
+    Ctx::Lane& sp = c.spare[slot];
+    std::swap(c.st, sp.st);
+    std::swap(c.dstat, sp.dstat);
+    std::swap(c.hstat, sp.hstat);
+#define SGTR_SWAP(n)                \
+    std::swap(c.n.p, sp.n.p);       \
+    std::swap(c.n.bytes, sp.n.bytes);
     SGTR_LANE_BUFS(SGTR_SWAP)
 #undef SGTR_SWAP
+    c.slot_of[c.cur_lane] = slot;
+    c.slot_of[L] = -1;
     c.cur_lane = L;
+}
+
+// stream of lane L whether or not it is the active one
+cudaStream_t lane_stream(Ctx& c, int L) {
+    return L == c.cur_lane ? c.st : c.spare[c.slot_of[L]].st;
 }
 
 int lanes_knob() {
     const char* v = getenv("SGTR_LANES");
-    return v ? std::max(1, std::min(2, atoi(v))) : 2;  // (1 disables the overlap)
+    return v ? std::max(1, std::min(Ctx::kMaxLanes, atoi(v))) : 2;  // (1 disables the overlap)
 }
 
 struct Timed {
@@ -775,13 +789,16 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     } lane_reset{c};
     int n_local = 0;
     for (int p = c.rank; p < n1; p += c.nranks) ++n_local;
-    const int lanes = (n_local > 1) ? lanes_knob() : 1;
-    double* gacc1 = nullptr;
-    if (lanes == 2) {
-        gacc1 = c.gacc1.as<double>(std::max<long long>(dim, 1));
+    const int lanes = std::min(n_local, lanes_knob());
+    double* gl[Ctx::kMaxLanes] = {g_acc, nullptr, nullptr};
+    if (lanes > 1) {
         SGTR_CUDA(cudaEventRecord(c.ev_fork, c.st));
-        SGTR_CUDA(cudaStreamWaitEvent(c.spare.st, c.ev_fork, 0));
-        SGTR_CUDA(cudaMemsetAsync(gacc1, 0, sizeof(double) * dim, c.spare.st));
+        for (int L = 1; L < lanes; ++L) {
+            gl[L] = c.gacc[L].as<double>(std::max<long long>(dim, 1));
+            cudaStream_t ls = lane_stream(c, L);
+            SGTR_CUDA(cudaStreamWaitEvent(ls, c.ev_fork, 0));
+            SGTR_CUDA(cudaMemsetAsync(gl[L], 0, sizeof(double) * dim, ls));
+        }
     }
     int li = 0;
     for (int p = c.rank; p < n1 && !local_error; p += c.nranks, ++li) {
@@ -797,15 +814,16 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         }
         residual_adjoint(c, GRAD, W, H, view_gt(c, s1[p]), nullptr, nullptr, o.residual.lambda,
                          o.residual.floor, loss + p);
-        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, L == 0 ? g_acc : gacc1, gflag + p);
+        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, gl[L], gflag + p);
     }
-    if (lanes == 2) {
-        use_lane(c, 1);
-        SGTR_CUDA(cudaEventRecord(c.ev_join, c.st));
+    if (lanes > 1) {
         use_lane(c, 0);
-        SGTR_CUDA(cudaStreamWaitEvent(c.st, c.ev_join, 0));
-        launch_add(c.st, g_acc, gacc1, dim);
-        c.launches += 1;
+        for (int L = 1; L < lanes; ++L) {  // fixed lane order: deterministic sum
+            SGTR_CUDA(cudaEventRecord(c.ev_join[L], lane_stream(c, L)));
+            SGTR_CUDA(cudaStreamWaitEvent(c.st, c.ev_join[L], 0));
+            launch_add(c.st, g_acc, gl[L], dim);
+            c.launches += 1;
+        }
     }
     // Hutchinson phase (optimizer.cpp:75-104), views of S2 split over ranks
     if (refresh && !local_error) {
@@ -1116,11 +1134,14 @@ int sgtr_create(int device, sgtr_ctx** out) {
             SGTR_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
             SGTR_CUDA(cudaMalloc(&c->dstat, sizeof(DevStatus)));
             SGTR_CUDA(cudaMallocHost(&c->hstat, sizeof(DevStatus)));
-            SGTR_CUDA(cudaStreamCreateWithFlags(&c->spare.st, cudaStreamNonBlocking));
-            SGTR_CUDA(cudaMalloc(&c->spare.dstat, sizeof(DevStatus)));
-            SGTR_CUDA(cudaMallocHost(&c->spare.hstat, sizeof(DevStatus)));
+            for (Ctx::Lane& l : c->spare) {
+                SGTR_CUDA(cudaStreamCreateWithFlags(&l.st, cudaStreamNonBlocking));
+                SGTR_CUDA(cudaMalloc(&l.dstat, sizeof(DevStatus)));
+                SGTR_CUDA(cudaMallocHost(&l.hstat, sizeof(DevStatus)));
+            }
             SGTR_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-            SGTR_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+            for (cudaEvent_t& e : c->ev_join)
+                SGTR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         } catch (...) {
             delete c;
             throw;
