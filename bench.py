@@ -236,6 +236,7 @@ def run_reference(args):
     from paper_2602_00395_b200 import splat as sp  # host-side generator only (no GPU)
     from oracle import pyoracle as orc
     orc.build()
+    timing_lib = orc.use_timing_build()
     k, v, w, h, b, sh = CONFIGS[args.config]
     gt, init, cams = sp.make_synthetic(gt_splats=k, init_splats=k, views=v, width=w, height=h,
                                        seed=args.seed,
@@ -262,7 +263,8 @@ def run_reference(args):
               f"parallel.hpp): each step times one central 320xT crop (T = threads) of a gradient view with "
               f"all {k} splats; cost model a+b*pixels from 320xT/320x3T crops, the refresh view "
               f"and shd_radii (100K subset) measured once in warm-up; extrapolated to "
-              f"{w}x{h} x {b} views + 1/10 refresh view + shd_radii at full K")
+              f"{w}x{h} x {b} views + 1/10 refresh view + shd_radii at full K; "
+              f"oracle build {os.path.basename(timing_lib)} (-O3 -march=native when it built)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -468,6 +470,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import pyoracle as orc
         orc.build()
+        timing_lib = orc.use_timing_build()
         cam = orc.Camera()
         src = cams[1]._c()
         for f, _ in orc.Camera._fields_:
@@ -479,7 +482,8 @@ def main():
                           f"and 320x3T crops (T = threads) of one gradient view + a 320xT refresh crop, all "
                           f"{k} splats, shd_radii on a 100K subset; cost a+b*pixels "
                           f"extrapolated to {b} views x {w}x{h} + 1/10 refresh view + "
-                          f"shd_radii at full K"),
+                          f"shd_radii at full K; oracle build {os.path.basename(timing_lib)} "
+                          f"(-O3 -march=native when it built)"),
                "model_s": {kk: float(vv) for kk, vv in model.items()}}
 
     if rank == 0:

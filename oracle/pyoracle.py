@@ -101,18 +101,43 @@ def build(force: bool = False) -> str:
 _lib = None
 
 
+def use_timing_build() -> str:
+    """Switch this process to the oracle's timing build (-O3 -march=native,
+    compiled here on first use by `make native`) for the CPU-baseline
+    measurements; falls back to the parity build if that fails.  Returns
+    the loaded library path."""
+    global _lib
+    path = os.path.join(_HERE, "build_native", "liboracle_native.so")
+    try:
+        subprocess.run(["make", "-s", "-C", _HERE, "native"], check=True,
+                       capture_output=True, timeout=600)
+        L = C.CDLL(path)
+    except Exception:
+        build()
+        return _LIB_PATH
+    _setup(L)
+    _lib = L
+    if _SH_NB:
+        L.orc_set_sh_degree(int(round((_SH_NB + 1) ** 0.5)) - 1)
+    return path
+
+
+def _setup(L):
+    L.orc_last_error.restype = C.c_char_p
+    for name in ("orc_mean_ssim", "orc_psnr", "orc_objective", "orc_beta_rotation",
+                 "orc_eps_at", "orc_hellinger_sq"):
+        getattr(L, name).restype = C.c_double
+    L.orc_state_create.restype = C.c_void_p
+    L.orc_rng_create.restype = C.c_void_p
+
+
 def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(_LIB_PATH):
             build()
         L = C.CDLL(_LIB_PATH)
-        L.orc_last_error.restype = C.c_char_p
-        for name in ("orc_mean_ssim", "orc_psnr", "orc_objective", "orc_beta_rotation",
-                     "orc_eps_at", "orc_hellinger_sq"):
-            getattr(L, name).restype = C.c_double
-        L.orc_state_create.restype = C.c_void_p
-        L.orc_rng_create.restype = C.c_void_p
+        _setup(L)
         _lib = L
     return _lib
 
