@@ -1435,6 +1435,107 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
     tangent[2 * P + p] = d2 + ro.bg[2] * dT;
 }
 
+// ------------------------------------------------------------------ K12, batch-staged
+// The tangent image with k_raster_fwd_staged's batches: the passing
+// fragments' 9 raster fields and 9 tangent fields are fetched lane-parallel
+// into warp-private shared slots, then blended in list order with the same
+// per-pixel operations as k_raster_jvp.
+struct StagedTan {
+    double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
+};
+
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB)
+    k_raster_jvp_staged(TileLists tl, const double* __restrict__ rec,
+                        const double* __restrict__ trec, int W, int H, RenderP ro,
+                        double* __restrict__ tangent) {
+    constexpr int SUB = kWarps / WPB;
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ __align__(16) StagedTan s_tan[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, dT = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    bool done = !pc.inside;
+    StagedRec* my_rec = s_rec[lw];
+    StagedTan* my_tan = s_tan[lw];
+    int4* my_rect = s_rect[lw];
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done)) break;
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < end) {
+            rr = __ldg(tl.trect + jj);
+            pass = rect_hits_warp(pc, rr);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const int id = __ldg(tl.tile_ids + jj);
+            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) o[k] = __ldg(r2 + 2 + k);
+            const double* t = trec + (long long)kTRec * id;
+            StagedTan& u = my_tan[q];
+            u.mx = __ldg(t + T_MX);
+            u.my = __ldg(t + T_MY);
+            u.i00 = __ldg(t + T_I00);
+            u.i01 = __ldg(t + T_I01);
+            u.i11 = __ldg(t + T_I11);
+            u.alpha = __ldg(t + T_ALPHA);
+            u.c0 = __ldg(t + T_C0);
+            u.c1 = __ldg(t + T_C0 + 1);
+            u.c2 = __ldg(t + T_C0 + 2);
+            my_rect[q] = rr;
+        }
+        __syncwarp();
+        const int n = __popc(m);
+        for (int e = 0; e < n; ++e) {
+            if (!done && rect_has_pixel(pc, my_rect[e])) {
+                const StagedRec r = my_rec[e];
+                const StagedTan t = my_tan[e];
+                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+                const double ev = fast_exp(eval_expo(dx, dy, f));
+                double abar = __dmul_rn(f[R_ALPHA], ev);
+                // tangent of the same expression (dual.hpp semantics)
+                const Dual Dx(dx, -t.mx), Dy(dy, -t.my);
+                const Dual I00(f[R_I00], t.i00), I01(f[R_I01], t.i01), I11(f[R_I11], t.i11);
+                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
+                double dabar = t.alpha * ev + f[R_ALPHA] * (ev * ex.d);
+                if (abar >= ro.alpha_clamp) {
+                    abar = ro.alpha_clamp;
+                    dabar = 0.0;
+                }
+                if (abar >= ro.alpha_skip) {
+                    const double w = abar * T;
+                    const double dw = dabar * T + abar * dT;
+                    d0 += t.c0 * w + f[R_C0] * dw;
+                    d1 += t.c1 * w + f[R_C1] * dw;
+                    d2 += t.c2 * w + f[R_C2] * dw;
+                    const double om = __dsub_rn(1.0, abar);
+                    dT = dT * om + T * (-dabar);
+                    T = __dmul_rn(T, om);
+                    if (T < ro.t_stop) done = true;
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    tangent[p] = d0 + ro.bg[0] * dT;
+    tangent[P + p] = d1 + ro.bg[1] * dT;
+    tangent[2 * P + p] = d2 + ro.bg[2] * dT;
+}
+
 // experiment knobs (read once): SGTR_WARP_CULL=1 enables the warp-level
 // contribution filter, SGTR_VJP_MINBLOCKS in {2, 3} the VJP register budget
 int knob(const char* name, int dflt) {
@@ -1575,7 +1676,10 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (knob("SGTR_JVP_WARP", 0))
+    const int jvp = knob("SGTR_JVP_WARP", 2);
+    if (jvp == 2)
+        k_raster_jvp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    else if (jvp == 1)
         k_raster_jvp_warp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     else if (g_warp_cull)
         k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
