@@ -1162,7 +1162,10 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     const int px = bx0 + (lane & 7);
     const int start = tl.tile_start[tile];
     const long long P = (long long)W * H;
-    double u0[2], u1[2], u2[2], T[2], b0[2], b1[2], b2[2];
+    // ub = u . behind: the adjoint-weighted colour composited behind the
+    // current fragment (the reference keeps the 3 channels, render.cpp:238-245;
+    // only this dot product enters dL/dalpha_bar)
+    double u0[2], u1[2], u2[2], T[2], ub[2];
     int lastp[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
@@ -1179,9 +1182,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             // pixels with an all-zero adjoint are skipped (render.cpp:283)
             if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;
         }
-        b0[k] = ro.bg[0] * T[k];
-        b1[k] = ro.bg[1] * T[k];
-        b2[k] = ro.bg[2] * T[k];
+        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
     }
     const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
     StagedRec* my_rec = s_rec[lw];
@@ -1245,12 +1246,9 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                 g[6] += u0[k] * at;
                 g[7] += u1[k] * at;
                 g[8] += u2[k] * at;
-                const double dab = u0[k] * (f[R_C0] * t_in - b0[k] * rom) +
-                                   u1[k] * (f[R_C1] * t_in - b1[k] * rom) +
-                                   u2[k] * (f[R_C2] * t_in - b2[k] * rom);
-                b0[k] += f[R_C0] * at;
-                b1[k] += f[R_C1] * at;
-                b2[k] += f[R_C2] * at;
+                const double uc = u0[k] * f[R_C0] + u1[k] * f[R_C1] + u2[k] * f[R_C2];
+                const double dab = uc * t_in - ub[k] * rom;
+                ub[k] += uc * at;
                 if (!clamped) {
                     g[5] += gauss * dab;
                     const double de = abar * dab;
