@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
             if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (kCount) ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(32 * WPB)
                 const double f[13] = {0.0, 0.0, 0.0, 0.0, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
                                       c01.x, c01.y, cc2.x};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(32 * WPB)
                 const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                 const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T[k];
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kThreads)
                     t[2 * q + 1] = v.y;
                 }
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ex0 = fast_exp(eval_expo(dx, dy, f));
+                const double ex0 = fast_exp_neg(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], ex0);
                 const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
                 const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
         for (int k = 0; k < PPL; ++k) {
             if (!done[k] && !(pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1])) {
                 const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (abar >= ro.alpha_skip) {
                     const double w = abar * T[k];
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
             bool contrib = false;
             if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double gauss = fast_exp(eval_expo(dx, dy, f));
+                const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
                 const bool clamped = abar >= ro.alpha_clamp;
                 if (clamped) abar = ro.alpha_clamp;
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
         bool contrib = false;
         if (rel < lastp && rect_has_pixel(pc, my_rect[e])) {
             const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-            const double gauss = fast_exp(eval_expo(dx, dy, f));
+            const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
             double abar = __dmul_rn(f[R_ALPHA], gauss);
             const bool clamped = abar >= ro.alpha_clamp;
             if (clamped) abar = ro.alpha_clamp;
@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * (kWarps / WPB))
                 const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double gauss = fast_exp(eval_expo(dx, dy, f));
+                const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
                 const bool clamped = abar >= ro.alpha_clamp;
                 if (clamped) abar = ro.alpha_clamp;
@@ -1234,7 +1234,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
                 double ax, ay;
-                const double gauss = fast_exp(eval_expo(dx, dy, f, ax, ay));
+                const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
                 const bool clamped = abar >= ro.alpha_clamp;
                 if (clamped) abar = ro.alpha_clamp;
@@ -1337,7 +1337,7 @@ __global__ void __launch_bounds__(32 * (8 / PPL))
         for (int k = 0; k < PPL; ++k) {
             if (!col_in || rel >= lastp[k] || pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1]) continue;
             const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-            const double gauss = fast_exp(eval_expo(dx, dy, f));
+            const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
             double abar = __dmul_rn(f[R_ALPHA], gauss);
             const bool clamped = abar >= ro.alpha_clamp;
             if (clamped) abar = ro.alpha_clamp;
@@ -1407,7 +1407,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double* t = s_t + kTRec * jj;
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double e = fast_exp(eval_expo(dx, dy, f));
+                const double e = fast_exp_neg(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], e);
                 // tangent of the same expression (dual.hpp semantics)
                 const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
@@ -1509,7 +1509,7 @@ __global__ void __launch_bounds__(32 * WPB)
                 const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ev = fast_exp(eval_expo(dx, dy, f));
+                const double ev = fast_exp_neg(eval_expo(dx, dy, f));
                 double abar = __dmul_rn(f[R_ALPHA], ev);
                 // tangent of the same expression (dual.hpp semantics)
                 const Dual Dx(dx, -t.mx), Dy(dy, -t.my);
