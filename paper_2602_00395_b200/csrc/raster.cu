@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                 if (clamped) abar = ro.alpha_clamp;
                 if (abar < ro.alpha_skip) continue;
                 contrib = true;
-                const double rom = 1.0 / __dsub_rn(1.0, abar);
+                const double rom = rcp_unit(__dsub_rn(1.0, abar));
                 const double t_in = T[k] * rom;
                 const double at = abar * t_in;
                 g[6] += u0[k] * at;
