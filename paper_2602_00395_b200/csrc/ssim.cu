@@ -280,16 +280,42 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
         s_f[2][sy][sx] = in ? Rf[q] : 0.0;
     }
     __syncthreads();
+    // blocks whose windows never meet the image border (most of a 1080p
+    // view): the transposed filter is a plain 11-tap correlation there
+    const bool in_x = x0 >= 2 * HALO && x0 + TX + 2 * HALO <= W;
+    const bool in_y = y0 >= 2 * HALO && y0 + TY + 2 * HALO <= H;
     // horizontal transposed pass for every staged row
-    for (int i = threadIdx.x; i < SY * TX; i += kThreads) {
-        const int sy = i / TX, tx = i % TX;
-        const int gx = x0 + tx;
+    if (in_x) {
+        // two adjacent columns per thread share 10 of their 11 taps
+        for (int i = threadIdx.x; i < SY * (TX / 2); i += kThreads) {
+            const int sy = i / (TX / 2), tx = 2 * (i % (TX / 2));
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-            s_h[f][sy][tx] = gx < W ? transposed_1d(gx, W, [&](int q) {
-                return s_f[f][sy][q - x0 + HALO];
-            })
-                                    : 0.0;
+            for (int f = 0; f < 3; ++f) {
+                const double* row = &s_f[f][sy][tx];
+                double v0 = 0.0, v1 = 0.0;
+                double prev = row[0];
+#pragma unroll
+                for (int d = 0; d < 2 * HALO + 1; ++d) {
+                    const double nxt = row[d + 1];
+                    v0 += c_k[d] * prev;
+                    v1 += c_k[d] * nxt;
+                    prev = nxt;
+                }
+                s_h[f][sy][tx] = v0;
+                s_h[f][sy][tx + 1] = v1;
+            }
+        }
+    } else {
+        for (int i = threadIdx.x; i < SY * TX; i += kThreads) {
+            const int sy = i / TX, tx = i % TX;
+            const int gx = x0 + tx;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                s_h[f][sy][tx] = gx < W ? transposed_1d(gx, W, [&](int q) {
+                    return s_f[f][sy][q - x0 + HALO];
+                })
+                                        : 0.0;
+            }
         }
     }
     __syncthreads();
@@ -298,9 +324,19 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
         const int gx = x0 + tx, gy = y0 + ty;
         if (gx >= W || gy >= H) continue;
         double t[3];
+        if (in_y) {
 #pragma unroll
-        for (int f = 0; f < 3; ++f)
-            t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
+            for (int f = 0; f < 3; ++f) {
+                double v = 0.0;
+#pragma unroll
+                for (int d = 0; d < 2 * HALO + 1; ++d) v += c_k[d] * s_h[f][ty + d][tx];
+                t[f] = v;
+            }
+        } else {
+#pragma unroll
+            for (int f = 0; f < 3; ++f)
+                t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
+        }
         const long long p = c * P + (long long)gy * W + gx;
         const double base = adjl1 ? adjl1[p] : 0.0;
         adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
