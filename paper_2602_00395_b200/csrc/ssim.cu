@@ -93,30 +93,38 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
         if (Tr::kTangent) s_da[i] = vd;
     }
     __syncthreads();
-    // horizontal pass over all SY rows
-    for (int i = threadIdx.x; i < SY * TX; i += kThreads) {
-        const int sy = i / TX, tx = i % TX;
-        double m[NM];
+    // horizontal pass over all SY rows; two adjacent columns per thread share
+    // 10 of their 11 staged taps
+    auto acc = [&](double* m, double w, double av, double bv, double dv) {
+        m[Tr::MUA] += w * av;
+        if (!kPre) m[Tr::MUB < 0 ? 0 : Tr::MUB] += w * bv;
+        m[Tr::MAA] += w * av * av;
+        if (!kPre) m[Tr::MBB < 0 ? 0 : Tr::MBB] += w * bv * bv;
+        m[Tr::MAB] += w * av * bv;
+        if (Tr::kTangent) {
+            m[Tr::DMUA] += w * dv;
+            m[Tr::DMAA] += w * 2.0 * av * dv;
+            m[Tr::DMAB] += w * bv * dv;
+        }
+    };
+    for (int i = threadIdx.x; i < SY * (TX / 2); i += kThreads) {
+        const int sy = i / (TX / 2), tx = 2 * (i % (TX / 2));
+        double m0[NM], m1[NM];
 #pragma unroll
-        for (int j = 0; j < NM; ++j) m[j] = 0.0;
+        for (int j = 0; j < NM; ++j) m0[j] = m1[j] = 0.0;
 #pragma unroll
-        for (int d = 0; d < 11; ++d) {
+        for (int d = 0; d < 12; ++d) {
             const int si = sy * SX + tx + d;
-            const double w = c_k[d], av = s_a[si], bv = s_b[si];
-            m[Tr::MUA] += w * av;
-            if (!kPre) m[Tr::MUB < 0 ? 0 : Tr::MUB] += w * bv;
-            m[Tr::MAA] += w * av * av;
-            if (!kPre) m[Tr::MBB < 0 ? 0 : Tr::MBB] += w * bv * bv;
-            m[Tr::MAB] += w * av * bv;
-            if (Tr::kTangent) {
-                const double dv = s_da[si];
-                m[Tr::DMUA] += w * dv;
-                m[Tr::DMAA] += w * 2.0 * av * dv;
-                m[Tr::DMAB] += w * bv * dv;
-            }
+            const double av = s_a[si], bv = s_b[si];
+            const double dv = Tr::kTangent ? s_da[si] : 0.0;
+            if (d < 11) acc(m0, c_k[d], av, bv, dv);
+            if (d > 0) acc(m1, c_k[d - 1], av, bv, dv);
         }
 #pragma unroll
-        for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TX + tx] = m[j];
+        for (int j = 0; j < NM; ++j) {
+            s_h[(j * SY + sy) * TX + tx] = m0[j];
+            s_h[(j * SY + sy) * TX + tx + 1] = m1[j];
+        }
     }
     __syncthreads();
     using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
