@@ -188,9 +188,11 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
             // image-space adjoint of the residual chain (residuals.cpp:81-117)
             double ur1, ur2;  // residual-space upstream for this entry
             if (MODE == GRAD) {
-                ur1 = sqrt(fmax(u1, fl));
-                ur2 = sqrt(fmax(u2, fl));
-                partial += ur1 * ur1 + ur2 * ur2;
+                // f = sqrt(max(u, floor)): f^2 = max(u, floor), and the
+                // Gauss-Newton adjoint f * d f / d u = 1/2 (below, masked)
+                ur1 = 0.0;
+                ur2 = 0.0;
+                partial += fmax(u1, fl) + fmax(u2, fl);
             } else if (MODE == HUTCH) {
                 const double t = s_da[(ty + HALO) * SX + tx + HALO];
                 ur1 = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
@@ -205,16 +207,35 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
             double up;
             if (MODE == SSIM_VJP) {
                 up = args.u[pi];
+            } else if (MODE == GRAD) {
+                // u * (1-l) sgn / (2 sqrt(u1)) and u * (-l / (4 sqrt(u2))) with
+                // u = sqrt(u1), sqrt(u2) (residuals.cpp:81-117): the square
+                // roots cancel
+                args.adjl1[pi] = u1 > fl ? 0.5 * (1.0 - lam) * sgn(diff) : 0.0;
+                up = u2 > fl ? -0.25 * lam : 0.0;
             } else {
                 args.adjl1[pi] = u1 > fl ? ur1 * (1.0 - lam) * sgn(diff) / (2.0 * sqrt(u1)) : 0.0;
                 up = u2 > fl ? ur2 * (-lam / (4.0 * sqrt(u2))) : 0.0;
             }
-            // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155)
+            // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155), with the
+            // two reciprocals shared
+#ifndef SGTR_SSIM_RCP
+#define SGTR_SSIM_RCP 0
+#endif
+#if SGTR_SSIM_RCP
+            const double r1 = 1.0 / d1v, r2 = 1.0 / d2v;
+            const double pp = n1v * r1, qq = n2v * r2;
+            const double ds_dmu = qq * (2.0 * mu_b * d1v - 2.0 * mu_av * n1v) * (r1 * r1) +
+                                  pp * (2.0 * mu_av * n2v - 2.0 * mu_b * d2v) * (r2 * r2);
+            const double ds_dmaa = -pp * n2v * (r2 * r2);
+            const double ds_dmab = pp * 2.0 * r2;
+#else
             const double pp = n1v / d1v, qq = n2v / d2v;
             const double ds_dmu = qq * (2.0 * mu_b * d1v - 2.0 * mu_av * n1v) / (d1v * d1v) +
                                   pp * (2.0 * mu_av * n2v - 2.0 * mu_b * d2v) / (d2v * d2v);
             const double ds_dmaa = -pp * n2v / (d2v * d2v);
             const double ds_dmab = pp * 2.0 / d2v;
+#endif
             args.P[pi] = up * ds_dmu;
             args.Q[pi] = up * ds_dmaa * 2.0;
             args.R[pi] = up * ds_dmab;
