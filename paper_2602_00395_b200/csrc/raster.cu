@@ -1271,6 +1271,215 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     }
 }
 
+// ------------------------------------------------------------------ K10, batch-staged, 2 px/lane, interleaved
+// As k_raster_vjp_staged2, with three changes that leave every partial
+// bit-identical:
+//  * the two pixels' evaluations run in one straight-line block when both
+//    rows of the warp's block meet the fragment, so the two exp polynomials
+//    and reciprocals are independent dependency chains the FP64 pipe
+//    interleaves (with a branch per pixel the compiler serialises them); a
+//    pixel outside the fragment still runs the arithmetic (its lane would
+//    idle in the other branch anyway) and only its state updates are
+//    predicated off;
+//  * the conic adjoints accumulate de * dx^2, de * dx dy, de * dy^2 and take
+//    their factors -1/2, -1, -1/2 once at the write (scaling by a power of two
+//    commutes with rounding, so each running sum is the old one scaled);
+//  * the per-fragment warp reduction is deferred: lanes park their 9 values
+//    in a ring of kRing fragments and one flush sums 9 * kRing columns, one
+//    per lane, in the same order as warp_reduce9_smem ((0..10) + (11..21)) +
+//    (22..31) — a third of the reduction instructions per fragment.
+template <int WPB, int kMinB = 10>
+__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
+    k_raster_vjp_staged3(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                         const double* __restrict__ adj, const double* __restrict__ tfinal,
+                         const int* __restrict__ last, double* __restrict__ part,
+                         unsigned char* __restrict__ mask) {
+    constexpr int SUB = 4 / WPB;
+    constexpr int kRing = 3;  // 27 columns: one per lane
+    __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
+    __shared__ long long s_ring_out[WPB][kRing];
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    __shared__ int s_slot[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
+    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
+    const int px = bx0 + (lane & 7);
+    const int py0 = by0 + (lane >> 3);
+    const double pxc = px + 0.5;
+    const double pyc[2] = {py0 + 0.5, py0 + 4.5};
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H;
+    double u0[2], u1[2], u2[2], T[2], ub[2];
+    int lastp[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = py0 + 4 * k;
+        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
+        lastp[k] = 0;
+        if (px < W && py < H) {
+            const long long p = (long long)py * W + px;
+            u0[k] = adj[p];
+            u1[k] = adj[P + p];
+            u2[k] = adj[2 * P + p];
+            T[k] = tfinal[p];
+            lastp[k] = last[p];
+            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
+        }
+        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
+    }
+    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    int* my_slot = s_slot[lw];
+    double(*ring)[kRedStride] = s_ring[lw];
+    long long* ring_out = s_ring_out[lw];
+    int nring = 0;  // warp-uniform
+    // sum the parked columns (lane = fragment * 9 + adjoint) and write them
+    auto flush = [&](int n) {
+        __syncwarp();
+        if (lane < n * kAdj) {
+            const double* col = ring[lane];
+            double t0 = col[0], t1 = col[11], t2 = col[22];
+#pragma unroll
+            for (int k = 1; k < 11; ++k) {
+                t0 += col[k];
+                t1 += col[11 + k];
+                if (k < 10) t2 += col[22 + k];
+            }
+            const int fe = lane / kAdj, c = lane - fe * kAdj;
+            double v = (t0 + t1) + t2;
+            if (c == 2 || c == 4) v *= -0.5;
+            if (c == 3) v = -v;
+            part[(ring_out[fe] * kWarps + warp) * kAdj + c] = v;
+        }
+        __syncwarp();
+    };
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < top) {
+            rr = __ldg(tl.trect + jj);
+            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+            my_slot[q] = __ldg(tl.sorted_d + jj);
+        }
+        __syncwarp();
+        for (int e = __popc(m) - 1; e >= 0; --e) {
+            const int rel = my_pos[e] - start;
+            const int4 r4 = my_rect[e];
+            const bool colin = px >= r4.x && px <= r4.z;
+            bool lv[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int py = py0 + 4 * k;
+                lv[k] = rel < lastp[k] && colin && py >= r4.y && py <= r4.w;
+            }
+            const bool any0 = __any_sync(kFull, lv[0]), any1 = __any_sync(kFull, lv[1]);
+            if (!any0 && !any1) continue;
+            const StagedRec r = my_rec[e];
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            // one pixel's contribution given its falloff (render.cpp:238-283)
+            auto accumulate = [&](int k, double dx, double dy, double ax, double ay, double gauss,
+                                  double abar, bool clamped, double rom) {
+                contrib = true;
+                const double t_in = T[k] * rom;
+                const double at = abar * t_in;
+                g[6] += u0[k] * at;
+                g[7] += u1[k] * at;
+                g[8] += u2[k] * at;
+                const double uc = u0[k] * r.c0 + u1[k] * r.c1 + u2[k] * r.c2;
+                const double dab = uc * t_in - ub[k] * rom;
+                ub[k] += uc * at;
+                if (!clamped) {
+                    g[5] += gauss * dab;
+                    const double de = abar * dab;
+                    g[2] += de * (dx * dx);  // x -1/2 at the write
+                    g[3] += de * (dx * dy);  // x -1
+                    g[4] += de * (dy * dy);  // x -1/2
+                    g[0] += de * ax;
+                    g[1] += de * ay;
+                }
+                T[k] = t_in;
+            };
+            const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                  r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+            const double dx = pxc - r.mx;
+            if (any0 && any1) {
+                double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
+                bool cl[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    dy[k] = pyc[k] - r.my;
+                    gauss[k] = fast_exp_neg(eval_expo(dx, dy[k], f, ax[k], ay[k]));
+                    abar[k] = __dmul_rn(r.alpha, gauss[k]);
+                    cl[k] = abar[k] >= ro.alpha_clamp;
+                    if (cl[k]) abar[k] = ro.alpha_clamp;
+                    lv[k] = lv[k] && abar[k] >= ro.alpha_skip;
+                    rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if (lv[k])
+                        accumulate(k, dx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k], rom[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
+                    const double dy = pyc[k] - r.my;
+                    double ax, ay;
+                    const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
+                    double abar = __dmul_rn(r.alpha, gauss);
+                    const bool clamped = abar >= ro.alpha_clamp;
+                    if (clamped) abar = ro.alpha_clamp;
+                    if (abar < ro.alpha_skip) continue;
+                    accumulate(k, dx, dy, ax, ay, gauss, abar, clamped,
+                               rcp_unit(__dsub_rn(1.0, abar)));
+                }
+            }
+            const unsigned cm = __ballot_sync(kFull, contrib);
+            if (cm == 0u) continue;
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) ring[nring * kAdj + c][lane] = g[c];
+            if (lane == 0) {
+                const long long dslot = my_slot[e];
+                ring_out[nring] = dslot;
+                mask[dslot * kWarps + warp] = 1;
+            }
+            if (++nring == kRing) {
+                flush(kRing);
+                nring = 0;
+            }
+        }
+        __syncwarp();
+    }
+    if (nring) flush(nring);
+}
+
 // ------------------------------------------------------------------ K10, PPL pixels per lane
 // As k_raster_vjp_warp, but each lane owns PPL pixels of one column (rows
 // r, r+2, ..): a warp covers 16 x 2*PPL pixels, sums each fragment's adjoints
@@ -1555,7 +1764,7 @@ const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
 const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
 const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
 const int g_fwd_warp = knob("SGTR_FWD_WARP", 2);  // 2: batch-staged, 1: chunk-filtered
-const int g_vjp_staged = knob("SGTR_VJP_STAGED", 2);  // 2: batch-staged K10, 2 px/lane
+const int g_vjp_staged = knob("SGTR_VJP_STAGED", 3);  // 3: batch-staged K10, 2 px/lane interleaved, ring reduction
 const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
 const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
 // warps per CTA of the warp-filtered forward / VJP kernels
@@ -1624,7 +1833,13 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 12)
+    if (g_vjp_staged == 3 && g_vjp_min_blocks == 8)
+        k_raster_vjp_staged3<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                          part, mask);
+    else if (g_vjp_staged == 3)
+        k_raster_vjp_staged3<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                      mask);
+    else if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 12)
         k_raster_vjp_staged2<2, 12><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                            part, mask);
     else if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 8)
