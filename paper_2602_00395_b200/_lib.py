@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgtr.so")
+# SGTR_LIB: an alternative build of the same library (A/B checks in tools/)
+LIB_PATH = os.environ.get("SGTR_LIB") or os.path.join(HERE, "libsgtr.so")
 
 SGTR_OK, SGTR_INVALID_ARGUMENT, SGTR_NUMERIC, SGTR_RUNTIME = 0, 1, 2, 3
 

@@ -401,6 +401,110 @@ __global__ void __launch_bounds__(32 * WPB)
     last[p] = processed;
 }
 
+// ------------------------------------------------------------------ K7, batch-staged, paired entries
+// As k_raster_fwd_staged, blending the staged batch two entries at a time:
+// the two falloffs (exp polynomial, clamp, skip test) do not depend on the
+// blend state, so when both entries meet the warp's block they are computed
+// in one straight-line block — two independent FP64 dependency chains the
+// pipe interleaves — and then blended in list order, the second only if the
+// pixel did not stop at the first.  Per pixel the operations and their order
+// are those of k_raster_fwd_staged, so the outputs are bit-identical.
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB)
+    k_raster_fwd_paired(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                        double* __restrict__ img, double* __restrict__ tfinal,
+                        int* __restrict__ last) {
+    constexpr int SUB = kWarps / WPB;
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int4 s_rect[WPB][32];
+    __shared__ int s_pos[WPB][32];
+    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool done = !pc.inside;
+    int processed = end - start;
+    StagedRec* my_rec = s_rec[lw];
+    int4* my_rect = s_rect[lw];
+    int* my_pos = s_pos[lw];
+    auto falloff = [&](const StagedRec& r) {
+        const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
+                              r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+        const double dx = pc.pxc - r.mx, dy = pc.pyc - r.my;
+        double abar = __dmul_rn(r.alpha, fast_exp_neg(eval_expo(dx, dy, f)));
+        if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+        return abar;
+    };
+    auto blend = [&](const StagedRec& r, double abar, int e) {
+        const double w = abar * T;
+        c0 += r.c0 * w;
+        c1 += r.c1 * w;
+        c2 += r.c2 * w;
+        T = __dmul_rn(T, __dsub_rn(1.0, abar));
+        if (T < ro.t_stop) {
+            done = true;
+            processed = my_pos[e] - start + 1;
+        }
+    };
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done)) break;
+        const int jj = base + lane;
+        bool pass = false;
+        int4 rr;
+        if (jj < end) {
+            rr = __ldg(tl.trect + jj);
+            pass = rect_hits_warp(pc, rr);
+        }
+        const unsigned m = __ballot_sync(kFull, pass);
+        if (pass) {
+            const int q = __popc(m & ((1u << lane) - 1u));
+            const double2* r2 =
+                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            o[0] = a;
+            o[1] = b;
+            o[2] = c;
+            o[3] = d;
+            o[4] = e;
+            my_rect[q] = rr;
+            my_pos[q] = jj;
+        }
+        __syncwarp();
+        const int n = __popc(m);
+        for (int e = 0; e < n; e += 2) {
+            const bool h0 = !done && rect_has_pixel(pc, my_rect[e]);
+            const bool h1 = e + 1 < n && !done && rect_has_pixel(pc, my_rect[e + 1]);
+            const bool a0 = __any_sync(kFull, h0), a1 = __any_sync(kFull, h1);
+            if (a0 && a1) {
+                const StagedRec r0 = my_rec[e], r1 = my_rec[e + 1];
+                const double ab0 = falloff(r0), ab1 = falloff(r1);
+                if (h0 && ab0 >= ro.alpha_skip) blend(r0, ab0, e);
+                if (h1 && !done && ab1 >= ro.alpha_skip) blend(r1, ab1, e + 1);
+            } else if (a0 || a1) {
+                const int ee = a0 ? e : e + 1;
+                if (a0 ? h0 : h1) {
+                    const StagedRec r = my_rec[ee];
+                    const double ab = falloff(r);
+                    if (ab >= ro.alpha_skip) blend(r, ab, ee);
+                }
+            }
+            if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    img[p] = c0 + ro.bg[0] * T;
+    img[P + p] = c1 + ro.bg[1] * T;
+    img[2 * P + p] = c2 + ro.bg[2] * T;
+    tfinal[p] = T;
+    last[p] = processed;
+}
+
 // ------------------------------------------------------------------ K7, batch-staged, 2 px/lane
 // k_raster_fwd_staged with 8x8 warp blocks (the layout of k_raster_vjp_staged2)
 template <int WPB, int kMinB = 10>
@@ -1781,7 +1885,9 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp == 3) {
+    else if (g_fwd_warp == 4) {
+        k_raster_fwd_paired<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    } else if (g_fwd_warp == 3) {
         k_raster_fwd_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     } else if (g_fwd_warp == 2) {
         if (g_fwd_wpb == 2)

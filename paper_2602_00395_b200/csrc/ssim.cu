@@ -28,6 +28,7 @@ namespace {
 
 constexpr int TX = 32, TY = 16, HALO = 5;
 constexpr int kThreads = 256;  // TX * TY / 2: two output rows per thread
+constexpr int kHC = 4;         // horizontal pass: output columns per thread
 constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 18
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
@@ -107,40 +108,52 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
             m[Tr::DMAB] += w * bv * dv;
         }
     };
-    for (int i = threadIdx.x; i < SY * (TX / 2); i += kThreads) {
-        const int sy = i / (TX / 2), tx = 2 * (i % (TX / 2));
-        double m0[NM], m1[NM];
+    // (kHC adjacent columns per thread share the staged taps between them)
+    for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
+        const int sy = i / (TX / kHC), tx = kHC * (i % (TX / kHC));
+        double mo[kHC][NM];
 #pragma unroll
-        for (int j = 0; j < NM; ++j) m0[j] = m1[j] = 0.0;
+        for (int o = 0; o < kHC; ++o)
 #pragma unroll
-        for (int d = 0; d < 12; ++d) {
+            for (int j = 0; j < NM; ++j) mo[o][j] = 0.0;
+#pragma unroll
+        for (int d = 0; d < 10 + kHC; ++d) {
             const int si = sy * SX + tx + d;
             const double av = s_a[si], bv = s_b[si];
             const double dv = Tr::kTangent ? s_da[si] : 0.0;
-            if (d < 11) acc(m0, c_k[d], av, bv, dv);
-            if (d > 0) acc(m1, c_k[d - 1], av, bv, dv);
+#pragma unroll
+            for (int o = 0; o < kHC; ++o)
+                if (d >= o && d - o < 11) acc(mo[o], c_k[d - o], av, bv, dv);
         }
 #pragma unroll
-        for (int j = 0; j < NM; ++j) {
-            s_h[(j * SY + sy) * TX + tx] = m0[j];
-            s_h[(j * SY + sy) * TX + tx + 1] = m1[j];
-        }
+        for (int o = 0; o < kHC; ++o)
+#pragma unroll
+            for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TX + tx + o] = mo[o][j];
     }
     __syncthreads();
     using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
     const int tx = threadIdx.x % TX;
-    double partial = 0.0, partial2 = 0.0;
-    for (int ty = threadIdx.x / TX; ty < TY; ty += kThreads / TX) {
-    const int gx = x0 + tx, gy = y0 + ty;
-    double m[NM];
+    // vertical pass: two adjacent output rows per thread share 10 of their
+    // 11 taps
+    const int ty0 = 2 * (threadIdx.x / TX);
+    double mv[2][NM];
 #pragma unroll
-    for (int j = 0; j < NM; ++j) m[j] = 0.0;
+    for (int j = 0; j < NM; ++j) mv[0][j] = mv[1][j] = 0.0;
 #pragma unroll
-    for (int d = 0; d < 11; ++d) {
-        const double w = c_k[d];
+    for (int d = 0; d < 12; ++d) {
 #pragma unroll
-        for (int j = 0; j < NM; ++j) m[j] += w * s_h[(j * SY + ty + d) * TX + tx];
+        for (int j = 0; j < NM; ++j) {
+            const double v = s_h[(j * SY + ty0 + d) * TX + tx];
+            if (d < 11) mv[0][j] += c_k[d] * v;
+            if (d > 0) mv[1][j] += c_k[d - 1] * v;
+        }
     }
+    double partial = 0.0, partial2 = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+    const int ty = ty0 + rr;
+    const int gx = x0 + tx, gy = y0 + ty;
+    const double* m = mv[rr];
     if (gx < W && gy < H) {
         const long long p = (long long)gy * W + gx;
         const long long pi = c * P + p;
@@ -315,23 +328,24 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
     const bool in_y = y0 >= 2 * HALO && y0 + TY + 2 * HALO <= H;
     // horizontal transposed pass for every staged row
     if (in_x) {
-        // two adjacent columns per thread share 10 of their 11 taps
-        for (int i = threadIdx.x; i < SY * (TX / 2); i += kThreads) {
-            const int sy = i / (TX / 2), tx = 2 * (i % (TX / 2));
+        // kHC adjacent columns per thread share the staged taps
+        for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
+            const int sy = i / (TX / kHC), tx = kHC * (i % (TX / kHC));
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 const double* row = &s_f[f][sy][tx];
-                double v0 = 0.0, v1 = 0.0;
-                double prev = row[0];
+                double v[kHC];
 #pragma unroll
-                for (int d = 0; d < 2 * HALO + 1; ++d) {
-                    const double nxt = row[d + 1];
-                    v0 += c_k[d] * prev;
-                    v1 += c_k[d] * nxt;
-                    prev = nxt;
+                for (int o = 0; o < kHC; ++o) v[o] = 0.0;
+#pragma unroll
+                for (int d = 0; d < 10 + kHC; ++d) {
+                    const double x = row[d];
+#pragma unroll
+                    for (int o = 0; o < kHC; ++o)
+                        if (d >= o && d - o < 11) v[o] += c_k[d - o] * x;
                 }
-                s_h[f][sy][tx] = v0;
-                s_h[f][sy][tx + 1] = v1;
+#pragma unroll
+                for (int o = 0; o < kHC; ++o) s_h[f][sy][tx + o] = v[o];
             }
         }
     } else {
@@ -349,23 +363,38 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
     }
     __syncthreads();
     const int tx = threadIdx.x % TX;
-    for (int ty = threadIdx.x / TX; ty < TY; ty += kThreads / TX) {
-        const int gx = x0 + tx, gy = y0 + ty;
-        if (gx >= W || gy >= H) continue;
-        double t[3];
-        if (in_y) {
+    const int ty0 = 2 * (threadIdx.x / TX);  // two adjacent output rows per thread
+    double t2[2][3];
+    if (in_y) {
 #pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                double v = 0.0;
+        for (int f = 0; f < 3; ++f) {
+            double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-                for (int d = 0; d < 2 * HALO + 1; ++d) v += c_k[d] * s_h[f][ty + d][tx];
-                t[f] = v;
+            for (int d = 0; d < 12; ++d) {
+                const double x = s_h[f][ty0 + d][tx];
+                if (d < 11) v0 += c_k[d] * x;
+                if (d > 0) v1 += c_k[d - 1] * x;
             }
-        } else {
+            t2[0][f] = v0;
+            t2[1][f] = v1;
+        }
+    } else {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int gy = y0 + ty0 + rr;
 #pragma unroll
             for (int f = 0; f < 3; ++f)
-                t[f] = transposed_1d(gy, H, [&](int q) { return s_h[f][q - y0 + HALO][tx]; });
+                t2[rr][f] = gy < H ? transposed_1d(gy, H, [&](int q) {
+                    return s_h[f][q - y0 + HALO][tx];
+                })
+                                   : 0.0;
         }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int gx = x0 + tx, gy = y0 + ty0 + rr;
+        if (gx >= W || gy >= H) continue;
+        const double* t = t2[rr];
         const long long p = c * P + (long long)gy * W + gx;
         const double base = adjl1 ? adjl1[p] : 0.0;
         adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
