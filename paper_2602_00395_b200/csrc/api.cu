@@ -578,11 +578,11 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
     const long long nd = std::max(vr.n_dup, 1LL);
     if (vjp_mode() == 1) {
-        double* part = c.part.as<double>((size_t)8 * kAdj * nd);
-        unsigned char* mask = c.mask.as<unsigned char>((size_t)8 * nd);
+        double* part = c.part.as<double>((size_t)kVjpSlots * kAdj * nd);
+        unsigned char* mask = c.mask.as<unsigned char>((size_t)kVjpSlots * nd);
         {
             Timed t(c, KC_RASTER_VJP);
-            SGTR_CUDA(cudaMemsetAsync(mask, 0, (size_t)8 * nd, c.st));
+            SGTR_CUDA(cudaMemsetAsync(mask, 0, (size_t)kVjpSlots * nd, c.st));
             launch_raster_vjp_warp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
                                    c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(),
                                    part, mask);

@@ -313,12 +313,12 @@ __global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ so
     const long long off = off_r[r];
     for (int t = 0; t < cnt; ++t) {
         const long long d = off + t;  // partials are stored by splat-major slot
-        const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * d);
-        if (m == 0ull) continue;
-        const double* pp = part + d * 8 * kAdj;
+        const unsigned m = *reinterpret_cast<const unsigned*>(mask + kVjpSlots * d);
+        if (m == 0u) continue;
+        const double* pp = part + d * kVjpSlots * kAdj;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            if ((m >> (8 * w)) & 0xffull) {
+        for (int w = 0; w < kVjpSlots; ++w) {
+            if ((m >> (8 * w)) & 0xffu) {
 #pragma unroll
                 for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
             }
@@ -352,26 +352,26 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
-    // the <= 8 per-warp partials of each duplicate, in (duplicate, warp)
+    // the <= 4 per-warp partials of each duplicate, in (duplicate, warp)
     // order; the partials are stored by splat-major duplicate slot, so a
-    // splat's are contiguous; masks of 4 duplicates are fetched together
+    // splat's are one contiguous run of 288-byte records; masks of 4
+    // duplicates (4 bytes each) are fetched together
     const long long off = off_r[r];
     for (int t0 = 0; t0 < (kPre ? 0 : cnt); t0 += 4) {
         long long jp[4];
-        unsigned long long mk[4];
+        unsigned mk[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? off + t0 + u : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            mk[u] = jp[u] >= 0 ? *reinterpret_cast<const unsigned long long*>(mask + 8 * jp[u])
-                               : 0ull;
+            mk[u] = jp[u] >= 0 ? *reinterpret_cast<const unsigned*>(mask + kVjpSlots * jp[u]) : 0u;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            if (mk[u] == 0ull) continue;
-            const double* pp = part + jp[u] * 8 * kAdj;
+            if (mk[u] == 0u) continue;
+            const double* pp = part + jp[u] * kVjpSlots * kAdj;
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                if ((mk[u] >> (8 * w)) & 0xffull) {
+            for (int w = 0; w < kVjpSlots; ++w) {
+                if ((mk[u] >> (8 * w)) & 0xffu) {
 #pragma unroll
                     for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
                 }
@@ -422,14 +422,14 @@ __global__ void __launch_bounds__(256) k_partials_to_slots(const int* __restrict
                                                            double* __restrict__ slots) {
     const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // splat-major slot
     if (d >= n) return;
-    const unsigned long long m = *reinterpret_cast<const unsigned long long*>(mask + 8 * d);
+    const unsigned m = *reinterpret_cast<const unsigned*>(mask + kVjpSlots * d);
     double a[kAdj];
 #pragma unroll
     for (int c = 0; c < kAdj; ++c) a[c] = 0.0;
-    const double* pp = part + d * 8 * kAdj;
+    const double* pp = part + d * kVjpSlots * kAdj;
 #pragma unroll
-    for (int w = 0; w < 8; ++w)
-        if ((m >> (8 * w)) & 0xffull) {
+    for (int w = 0; w < kVjpSlots; ++w)
+        if ((m >> (8 * w)) & 0xffu) {
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
         }

@@ -221,99 +221,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
     last[p] = processed;
 }
 
-// ------------------------------------------------------------------ K7, warp-filtered
-// Barrier-free forward: each warp (8x4 pixels) walks its tile's list front to
-// back in chunks of kChunkF positions; a chunk is filtered lane-parallel
-// (warp-span test on the outward-rounded float bbox, ballot-compacted into a
-// warp-private shared list), then the surviving entries are blended in order
-// with the same per-pixel operation sequence as k_raster_fwd.  The warp stops
-// once all its pixels terminated.
-constexpr int kChunkF = 256;
-// WPB warps per CTA: a tile's 8 warps are spread over 8 / WPB CTAs, so a CTA
-// retires as soon as its own warps finish (warps of one tile end at very
-// different list positions)
-template <int WPB>
-__global__ void __launch_bounds__(32 * WPB)
-    k_raster_fwd_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                      double* __restrict__ img, double* __restrict__ tfinal,
-                      int* __restrict__ last) {
-    constexpr int SUB = kWarps / WPB;
-    __shared__ int s_list[WPB][kChunkF];
-    __shared__ int s_ids[WPB][kChunkF];
-    __shared__ int4 s_rect[WPB][kChunkF];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    bool done = !pc.inside;
-    int processed = end - start;
-    int* my_list = s_list[lw];
-    int* my_ids = s_ids[lw];
-    int4* my_rect = s_rect[lw];
-    for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
-        if (__all_sync(kFull, done)) break;
-        const int cend = min(end, cbeg + kChunkF);
-        int nl = 0;
-        for (int base = cbeg; base < cend; base += 32) {
-            const int jj = base + lane;
-            bool pass = false;
-            int4 rr;
-            if (jj < cend) {
-                rr = __ldg(tl.trect + jj);
-                pass = rect_hits_warp(pc, rr);
-            }
-            const unsigned m = __ballot_sync(kFull, pass);
-            if (pass) {
-                const int q = nl + __popc(m & ((1u << lane) - 1u));
-                my_list[q] = jj;
-                my_ids[q] = __ldg(tl.tile_ids + jj);
-                my_rect[q] = rr;
-            }
-            nl += __popc(m);
-        }
-        __syncwarp();
-        for (int e = 0; e < nl; ++e) {
-            const int j = my_list[e];
-            const int id = my_ids[e];
-            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-            if (!done && rect_has_pixel(pc, my_rect[e])) {
-                const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
-                const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
-                const double f[13] = {0.0, 0.0, 0.0, 0.0, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
-                                      c01.x, c01.y, cc2.x};
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
-                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
-                    const double w = abar * T;
-                    c0 += f[R_C0] * w;
-                    c1 += f[R_C1] * w;
-                    c2 += f[R_C2] * w;
-                    T = __dmul_rn(T, __dsub_rn(1.0, abar));
-                    if (T < ro.t_stop) {
-                        done = true;
-                        processed = j - start + 1;
-                    }
-                }
-            }
-            if (__all_sync(kFull, done)) break;
-        }
-        __syncwarp();
-    }
-    if (!pc.inside) return;
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    img[p] = c0 + ro.bg[0] * T;
-    img[P + p] = c1 + ro.bg[1] * T;
-    img[2 * P + p] = c2 + ro.bg[2] * T;
-    tfinal[p] = T;
-    last[p] = processed;
-}
-
 // ------------------------------------------------------------------ K7, batch-staged
-// As k_raster_fwd_warp, but the list is walked in batches of 32 positions:
-// each lane tests one position against the warp's pixel block and, if it
+// Each warp owns an 8x4 pixel block and walks its tile's list on its own, in
+// batches of 32 positions: each lane tests one position against the block and, if it
 // passes, loads that fragment's 9 raster fields into a warp-private shared
 // slot (ballot-compacted), so the 32 record fetches of a batch are in flight
 // together instead of one dependent fetch per blended entry.
@@ -505,268 +415,6 @@ __global__ void __launch_bounds__(32 * WPB)
     last[p] = processed;
 }
 
-// ------------------------------------------------------------------ K7, batch-staged, 2 px/lane
-// k_raster_fwd_staged with 8x8 warp blocks (the layout of k_raster_vjp_staged2)
-template <int WPB, int kMinB = 10>
-__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
-    k_raster_fwd_staged2(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                         double* __restrict__ img, double* __restrict__ tfinal,
-                         int* __restrict__ last) {
-    constexpr int SUB = 4 / WPB;
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
-    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
-    const int px = bx0 + (lane & 7);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T[2] = {1.0, 1.0}, c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
-    bool done[2];
-    int processed[2] = {end - start, end - start};
-#pragma unroll
-    for (int k = 0; k < 2; ++k) done[k] = !(px < W && by0 + (lane >> 3) + 4 * k < H);
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    for (int base = start; base < end; base += 32) {
-        if (__all_sync(kFull, done[0] && done[1])) break;
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < end) {
-            rr = __ldg(tl.trect + jj);
-            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-        }
-        __syncwarp();
-        const int n = __popc(m);
-        for (int e = 0; e < n; ++e) {
-            const int4 r4 = my_rect[e];
-            const bool colin = px >= r4.x && px <= r4.z;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int py = by0 + (lane >> 3) + 4 * k;
-                if (done[k] || !colin || py < r4.y || py > r4.w) continue;
-                const StagedRec r = my_rec[e];
-                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
-                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-                const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
-                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
-                    const double w = abar * T[k];
-                    c0[k] += f[R_C0] * w;
-                    c1[k] += f[R_C1] * w;
-                    c2[k] += f[R_C2] * w;
-                    T[k] = __dmul_rn(T[k], __dsub_rn(1.0, abar));
-                    if (T[k] < ro.t_stop) {
-                        done[k] = true;
-                        processed[k] = my_pos[e] - start + 1;
-                    }
-                }
-            }
-            if (__all_sync(kFull, done[0] && done[1])) break;
-        }
-        __syncwarp();
-    }
-    const long long P = (long long)W * H;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int py = by0 + (lane >> 3) + 4 * k;
-        if (px >= W || py >= H) continue;
-        const long long p = (long long)py * W + px;
-        img[p] = c0[k] + ro.bg[0] * T[k];
-        img[P + p] = c1[k] + ro.bg[1] * T[k];
-        img[2 * P + p] = c2[k] + ro.bg[2] * T[k];
-        tfinal[p] = T[k];
-        last[p] = processed[k];
-    }
-}
-
-// ------------------------------------------------------------------ K12 (raster), warp-filtered
-// Forward-mode tangent image with the same chunked, warp-filtered walk as
-// k_raster_fwd_warp; records and tangent records read through L1.
-__global__ void __launch_bounds__(kThreads)
-    k_raster_jvp_warp(TileLists tl, const double* __restrict__ rec,
-                      const double* __restrict__ trec, int W, int H, RenderP ro,
-                      double* __restrict__ tangent) {
-    __shared__ int s_list[kWarps][kChunkF];
-    __shared__ int s_ids[kWarps][kChunkF];
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0, dT = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    bool done = !pc.inside;
-    int* my_list = s_list[warp];
-    int* my_ids = s_ids[warp];
-    for (int cbeg = start; cbeg < end; cbeg += kChunkF) {
-        if (__all_sync(kFull, done)) break;
-        const int cend = min(end, cbeg + kChunkF);
-        int nl = 0;
-        for (int base = cbeg; base < cend; base += 32) {
-            const int jj = base + lane;
-            bool pass = false;
-            if (jj < cend) pass = rect_hits_warp(pc, __ldg(tl.trect + jj));
-            const unsigned m = __ballot_sync(kFull, pass);
-            if (pass) {
-                const int q = nl + __popc(m & ((1u << lane) - 1u));
-                my_list[q] = jj;
-                my_ids[q] = __ldg(tl.tile_ids + jj);
-            }
-            nl += __popc(m);
-        }
-        __syncwarp();
-        for (int e = 0; e < nl; ++e) {
-            const int id = my_ids[e];
-            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-            const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-            if (!done && !(pc.pxc < bx.x || pc.pxc > bx.y || pc.pyc < by.x || pc.pyc > by.y)) {
-                const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
-                const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
-                const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
-                                      c01.x, c01.y, cc2.x};
-                const double* tp = trec + (long long)kTRec * id;
-                double t[kTRec];
-#pragma unroll
-                for (int q = 0; q < kTRec / 2; ++q) {
-                    const double2 v = __ldg(reinterpret_cast<const double2*>(tp) + q);
-                    t[2 * q] = v.x;
-                    t[2 * q + 1] = v.y;
-                }
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ex0 = fast_exp_neg(eval_expo(dx, dy, f));
-                double abar = __dmul_rn(f[R_ALPHA], ex0);
-                const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
-                const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
-                    I11(f[R_I11], t[T_I11]);
-                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
-                double dabar = t[T_ALPHA] * ex0 + f[R_ALPHA] * (ex0 * ex.d);
-                if (abar >= ro.alpha_clamp) {
-                    abar = ro.alpha_clamp;
-                    dabar = 0.0;
-                }
-                if (abar >= ro.alpha_skip) {
-                    const double w = abar * T;
-                    const double dw = dabar * T + abar * dT;
-                    d0 += t[T_C0] * w + f[R_C0] * dw;
-                    d1 += t[T_C1] * w + f[R_C1] * dw;
-                    d2 += t[T_C2] * w + f[R_C2] * dw;
-                    const double om = __dsub_rn(1.0, abar);
-                    dT = dT * om + T * (-dabar);
-                    T = __dmul_rn(T, om);
-                    if (T < ro.t_stop) done = true;
-                }
-            }
-            if (__all_sync(kFull, done)) break;
-        }
-        __syncwarp();
-    }
-    if (!pc.inside) return;
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    tangent[p] = d0 + ro.bg[0] * dT;
-    tangent[P + p] = d1 + ro.bg[1] * dT;
-    tangent[2 * P + p] = d2 + ro.bg[2] * dT;
-}
-
-// ------------------------------------------------------------------ K7, PPL pixels per lane
-// Barrier-free forward: warps walk the tile list on their own (records through
-// L1), each lane blends PPL pixels of one column (independent recurrences =
-// FP64 instruction-level parallelism); a warp stops once all its pixels
-// terminated.  Same per-pixel operation sequence as k_raster_fwd.
-template <int PPL>
-__global__ void __launch_bounds__(32 * (8 / PPL))
-    k_raster_fwd_ppl(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                     double* __restrict__ img, double* __restrict__ tfinal,
-                     int* __restrict__ last) {
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
-    const int px = X0 + (lane & 15);
-    const int ybase = Y0 + warp * 2 * PPL;
-    const double pxc = px + 0.5;
-    const double wx0 = X0 + 0.5, wx1 = X0 + 15.5;
-    const double wy0 = ybase + 0.5, wy1 = ybase + 2 * PPL - 0.5;
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T[PPL], c0[PPL], c1[PPL], c2[PPL], pyc[PPL];
-    int processed[PPL];
-    bool done[PPL];
-    bool all_done = true;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-        const int py = ybase + (lane >> 4) + 2 * k;
-        pyc[k] = py + 0.5;
-        T[k] = 1.0;
-        c0[k] = c1[k] = c2[k] = 0.0;
-        processed[k] = end - start;
-        done[k] = !(px < W && py < H);
-        all_done = all_done && done[k];
-    }
-    for (int j = start; j < end; ++j) {
-        if (__all_sync(kFull, all_done)) break;
-        const int id = __ldg(tl.tile_ids + j);
-        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-        if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
-        if (pxc < bx.x || pxc > bx.y) continue;
-        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
-        const double2 c01 = __ldg(r2 + 5), cc2 = __ldg(r2 + 6);
-        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
-                              c01.x, c01.y, cc2.x};
-        all_done = true;
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-            if (!done[k] && !(pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1])) {
-                const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
-                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
-                    const double w = abar * T[k];
-                    c0[k] += f[R_C0] * w;
-                    c1[k] += f[R_C1] * w;
-                    c2[k] += f[R_C2] * w;
-                    T[k] = __dmul_rn(T[k], __dsub_rn(1.0, abar));
-                    if (T[k] < ro.t_stop) {
-                        done[k] = true;
-                        processed[k] = j - start + 1;
-                    }
-                }
-            }
-            all_done = all_done && done[k];
-        }
-    }
-    const long long P = (long long)W * H;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-        const int py = ybase + (lane >> 4) + 2 * k;
-        if (px >= W || py >= H) continue;
-        const long long p = (long long)py * W + px;
-        img[p] = c0[k] + ro.bg[0] * T[k];
-        img[P + p] = c1[k] + ro.bg[1] * T[k];
-        img[2 * P + p] = c2[k] + ro.bg[2] * T[k];
-        tfinal[p] = T[k];
-        last[p] = processed[k];
-    }
-}
-
 // ------------------------------------------------------------------ K10
 // Transposed butterfly: sums g[0..7] over the warp so that lane l with
 // (l & 3) == 0 ends with the total of g[l >> 2] (9 shuffles instead of 40),
@@ -806,7 +454,6 @@ __device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane
 // an 11-lane third of one component, 9 lanes add the three thirds and write
 // the totals to out[0..8].  ~40 instructions instead of the shuffle
 // butterfly's selects and shuffles; fixed order, so deterministic.
-constexpr int kChunk = 128;  // VJP list chunk (48 KB static smem per 8-warp CTA)
 constexpr int kRedStride = 33;
 constexpr int kRedScratch = kAdj * kRedStride + 27;
 __device__ __forceinline__ void warp_reduce9_smem(const double* g, int lane, double* scr,
@@ -946,300 +593,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
     }
 }
 
-// ------------------------------------------------------------------ K10, barrier-free
-// Every warp walks its tile's list on its own: records are read through L1 as
-// warp-broadcast loads (the 8 warps of a tile hit the same lines), so no
-// shared-memory staging, no CTA barriers and no cross-warp reduction are
-// needed.  A warp reduces each fragment's 9 adjoints over its 32 pixels and
-// stores them in its own partial slot (tile-sorted position j, warp w),
-// flagging mask[d * 8 + w] (d = the duplicate's splat-major slot,
-// sorted_d[j]); K11 sums the flagged partials of each duplicate in
-// warp order (deterministic, no atomics).
-template <int kMinBlocks, bool kSmemRed, bool kPrefetch, int WPB = kWarps>
-__global__ void __launch_bounds__(32 * WPB, kMinBlocks * (kWarps / WPB))
-    k_raster_vjp_warp(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                      const double* __restrict__ adj, const double* __restrict__ tfinal,
-                      const int* __restrict__ last, double* __restrict__ part,
-                      unsigned char* __restrict__ mask) {
-    constexpr int SUB = kWarps / WPB;
-    __shared__ double s_red[WPB][kRedScratch];
-    __shared__ int s_list[WPB][kChunk];
-    __shared__ int s_ids[WPB][kChunk];
-    __shared__ int4 s_rect[WPB][kChunk];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
-    const int start = tl.tile_start[tile];
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
-    int lastp = 0;
-    if (pc.inside) {
-        u0 = adj[p];
-        u1 = adj[P + p];
-        u2 = adj[2 * P + p];
-        T = tfinal[p];
-        lastp = last[p];
-    }
-    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
-    if (!active) lastp = 0;
-    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;
-    const int wlast = __reduce_max_sync(kFull, lastp);
-    // The list is walked back to front in chunks of kChunk positions.  Each
-    // chunk is first filtered lane-parallel (one warp-span test per lane on the
-    // outward-rounded float bbox, ballot-compacted into this warp's shared
-    // list), so the sequential pass only visits entries that can touch the
-    // warp's 8x4 pixels.
-    int* my_list = s_list[lw];
-    int* my_ids = s_ids[lw];
-    int4* my_rect = s_rect[lw];
-    for (int cend = start + wlast; cend > start; cend -= kChunk) {
-    const int cbeg = max(start, cend - kChunk);
-    int nl = 0;
-    for (int base = cbeg; base < cend; base += 32) {
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < cend) {
-            rr = __ldg(tl.trect + jj);
-            pass = rect_hits_warp(pc, rr);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = nl + __popc(m & ((1u << lane) - 1u));
-            my_list[q] = jj;
-            my_ids[q] = __ldg(tl.tile_ids + jj);
-            my_rect[q] = rr;
-        }
-        nl += __popc(m);
-    }
-    __syncwarp();
-    // kPrefetch: the next entry's record is loaded while the current one is
-    // processed (its loads are independent of the T recurrence)
-    double2 nr[7];
-    int nj = 0;
-    if (kPrefetch && nl > 0) {
-        nj = my_list[nl - 1];
-        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[nl - 1]);
-#pragma unroll
-        for (int k = 0; k < 7; ++k) nr[k] = __ldg(r2 + k);
-    }
-    for (int e = nl - 1; e >= 0; --e) {
-        int j;
-        double2 cr[7];
-        if (kPrefetch) {
-            j = nj;
-#pragma unroll
-            for (int k = 0; k < 7; ++k) cr[k] = nr[k];
-            if (e > 0) {
-                nj = my_list[e - 1];
-                const double2* r2 =
-                    reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[e - 1]);
-#pragma unroll
-                for (int k = 0; k < 7; ++k) nr[k] = __ldg(r2 + k);
-            }
-        } else {
-            j = my_list[e];
-            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * my_ids[e]);
-#pragma unroll
-            for (int k = 2; k < 7; ++k) cr[k] = __ldg(r2 + k);
-        }
-        const double f[13] = {0.0,     0.0,     0.0,     0.0,     cr[2].x, cr[2].y, cr[3].x,
-                              cr[3].y, cr[4].x, cr[4].y, cr[5].x, cr[5].y, cr[6].x};
-        const int rel = j - start;
-        double g[kAdj];
-#pragma unroll
-        for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-        bool contrib = false;
-        if (rel < lastp && rect_has_pixel(pc, my_rect[e])) {
-            const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-            const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
-            double abar = __dmul_rn(f[R_ALPHA], gauss);
-            const bool clamped = abar >= ro.alpha_clamp;
-            if (clamped) abar = ro.alpha_clamp;
-            if (abar >= ro.alpha_skip) {
-                contrib = true;
-                const double rom = 1.0 / __dsub_rn(1.0, abar);
-                const double t_in = T * rom;
-                const double at = abar * t_in;
-                g[6] = u0 * at;
-                g[7] = u1 * at;
-                g[8] = u2 * at;
-                const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
-                                   u1 * (f[R_C1] * t_in - b1 * rom) +
-                                   u2 * (f[R_C2] * t_in - b2 * rom);
-                b0 += f[R_C0] * at;
-                b1 += f[R_C1] * at;
-                b2 += f[R_C2] * at;
-                if (!clamped) {
-                    g[5] = gauss * dab;
-                    const double de = abar * dab;
-                    g[2] = de * (-0.5 * dx * dx);
-                    g[3] = de * (-dx * dy);
-                    g[4] = de * (-0.5 * dy * dy);
-                    g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
-                    g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
-                }
-                T = t_in;
-            }
-        }
-        if (!__any_sync(kFull, contrib)) continue;
-        const long long dslot = __ldg(tl.sorted_d + j);  // splat-major duplicate slot
-        double* o = part + (dslot * kWarps + warp) * kAdj;
-        if (kSmemRed) {
-            warp_reduce9_smem(g, lane, s_red[lw], o);
-        } else {
-            double v, v8;
-            warp_reduce9(g, lane, v, v8);
-            if ((lane & 3) == 0) o[lane >> 2] = v;
-            if (lane == 0) o[8] = v8;
-        }
-        if (lane == 0) mask[dslot * kWarps + warp] = 1;
-    }
-    __syncwarp();
-    }
-}
-
-// ------------------------------------------------------------------ K10, batch-staged
-// As k_raster_vjp_warp, with k_raster_fwd_staged's batches: the list is
-// walked back to front 32 positions at a time, the passing fragments' raster
-// fields are fetched by their filtering lanes in parallel into a
-// warp-private shared batch, then processed last-to-first.
-template <int WPB, bool kSmemRed = true, int kMinB = 3>
-__global__ void __launch_bounds__(32 * WPB, kMinB * (kWarps / WPB))
-    k_raster_vjp_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                        const double* __restrict__ adj, const double* __restrict__ tfinal,
-                        const int* __restrict__ last, double* __restrict__ part,
-                        unsigned char* __restrict__ mask) {
-    constexpr int SUB = kWarps / WPB;
-    __shared__ double s_red[WPB][kRedScratch];
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    __shared__ int s_slot[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
-    const int start = tl.tile_start[tile];
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
-    int lastp = 0;
-    if (pc.inside) {
-        u0 = adj[p];
-        u1 = adj[P + p];
-        u2 = adj[2 * P + p];
-        T = tfinal[p];
-        lastp = last[p];
-    }
-    // pixels with an all-zero adjoint are skipped (render.cpp:283)
-    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
-    if (!active) lastp = 0;
-    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;  // "behind"
-    const int wlast = __reduce_max_sync(kFull, lastp);
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    int* my_slot = s_slot[lw];
-    for (int top = start + wlast; top > start; top -= 32) {
-        const int base = max(start, top - 32);
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < top) {
-            rr = __ldg(tl.trect + jj);
-            pass = rect_hits_warp(pc, rr);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-            my_slot[q] = __ldg(tl.sorted_d + jj);
-        }
-        __syncwarp();
-        for (int e = __popc(m) - 1; e >= 0; --e) {
-            const int j = my_pos[e];
-            const int rel = j - start;
-            double g[kAdj];
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-            bool contrib = false;
-            if (rel < lastp && rect_has_pixel(pc, my_rect[e])) {
-                const StagedRec r = my_rec[e];
-                const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
-                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
-                double abar = __dmul_rn(f[R_ALPHA], gauss);
-                const bool clamped = abar >= ro.alpha_clamp;
-                if (clamped) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
-                    contrib = true;
-                    // one reciprocal for T_in = T / (1 - abar) and the three
-                    // behind / (1 - abar) terms (render.cpp:243-245)
-                    const double rom = 1.0 / __dsub_rn(1.0, abar);
-                    const double t_in = T * rom;
-                    const double at = abar * t_in;
-                    g[6] = u0 * at;
-                    g[7] = u1 * at;
-                    g[8] = u2 * at;
-                    const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
-                                       u1 * (f[R_C1] * t_in - b1 * rom) +
-                                       u2 * (f[R_C2] * t_in - b2 * rom);
-                    b0 += f[R_C0] * at;
-                    b1 += f[R_C1] * at;
-                    b2 += f[R_C2] * at;
-                    if (!clamped) {
-                        g[5] = gauss * dab;
-                        const double de = abar * dab;
-                        g[2] = de * (-0.5 * dx * dx);
-                        g[3] = de * (-dx * dy);
-                        g[4] = de * (-0.5 * dy * dy);
-                        g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
-                        g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
-                    }
-                    T = t_in;
-                }
-            }
-            const unsigned cm = __ballot_sync(kFull, contrib);
-            if (cm == 0u) continue;
-            const long long dslot = my_slot[e];  // splat-major duplicate slot
-            double* o = part + (dslot * kWarps + warp) * kAdj;
-            if ((cm & (cm - 1u)) == 0u) {
-                // a single contributing pixel: its adjoints are the partial
-                // (the other lanes' terms are exact zeros)
-                if (contrib) {
-#pragma unroll
-                    for (int c = 0; c < kAdj; ++c) o[c] = g[c];
-                    mask[dslot * kWarps + warp] = 1;
-                }
-                continue;
-            }
-            if (kSmemRed) {
-                warp_reduce9_smem(g, lane, s_red[lw], o);
-            } else {
-                double v, v8;
-                warp_reduce9(g, lane, v, v8);
-                if ((lane & 3) == 0) o[lane >> 2] = v;
-                if (lane == 0) o[8] = v8;
-            }
-            if (lane == 0) mask[dslot * kWarps + warp] = 1;
-        }
-        __syncwarp();
-    }
-}
-
 // ------------------------------------------------------------------ K10, batch-staged, 2 px/lane
 // As k_raster_vjp_staged, but a warp owns an 8x8 block (lane: column
 // lane & 7, rows lane >> 3 and 4 + (lane >> 3)): one list walk, record fetch
@@ -1367,9 +720,9 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             const unsigned cm = __ballot_sync(kFull, contrib);
             if (cm == 0u) continue;
             const long long dslot = my_slot[e];
-            double* o = part + (dslot * kWarps + warp) * kAdj;
+            double* o = part + (dslot * kVjpSlots + warp) * kAdj;
             warp_reduce9_smem(g, lane, s_red[lw], o);
-            if (lane == 0) mask[dslot * kWarps + warp] = 1;
+            if (lane == 0) mask[dslot * kVjpSlots + warp] = 1;
         }
         __syncwarp();
     }
@@ -1459,7 +812,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             double v = (t0 + t1) + t2;
             if (c == 2 || c == 4) v *= -0.5;
             if (c == 3) v = -v;
-            part[(ring_out[fe] * kWarps + warp) * kAdj + c] = v;
+            part[(ring_out[fe] * kVjpSlots + warp) * kAdj + c] = v;
         }
         __syncwarp();
     };
@@ -1572,7 +925,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             if (lane == 0) {
                 const long long dslot = my_slot[e];
                 ring_out[nring] = dslot;
-                mask[dslot * kWarps + warp] = 1;
+                mask[dslot * kVjpSlots + warp] = 1;
             }
             if (++nring == kRing) {
                 flush(kRing);
@@ -1582,114 +935,6 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
         __syncwarp();
     }
     if (nring) flush(nring);
-}
-
-// ------------------------------------------------------------------ K10, PPL pixels per lane
-// As k_raster_vjp_warp, but each lane owns PPL pixels of one column (rows
-// r, r+2, ..): a warp covers 16 x 2*PPL pixels, sums each fragment's adjoints
-// over its PPL pixels in registers (fixed order) before the one warp
-// reduction, and the PPL independent pixel recurrences give the FP64
-// pipeline instruction-level parallelism.  8/PPL warps per tile.
-template <int PPL>
-__global__ void __launch_bounds__(32 * (8 / PPL))
-    k_raster_vjp_ppl(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                     const double* __restrict__ adj, const double* __restrict__ tfinal,
-                     const int* __restrict__ last, double* __restrict__ part,
-                     unsigned char* __restrict__ mask) {
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int X0 = (tile % tl.tiles_x) * kTile, Y0 = (tile / tl.tiles_x) * kTile;
-    const int px = X0 + (lane & 15);
-    const int ybase = Y0 + warp * 2 * PPL;
-    const double pxc = px + 0.5;
-    const double wx0 = X0 + 0.5, wx1 = X0 + 15.5;
-    const double wy0 = ybase + 0.5, wy1 = ybase + 2 * PPL - 0.5;
-    const int start = tl.tile_start[tile];
-    const long long P = (long long)W * H;
-    double T[PPL], u0[PPL], u1[PPL], u2[PPL], b0[PPL], b1[PPL], b2[PPL], pyc[PPL];
-    int lastp[PPL];
-    int lmax = 0;
-#pragma unroll
-    for (int k = 0; k < PPL; ++k) {
-        const int py = ybase + (lane >> 4) + 2 * k;
-        pyc[k] = py + 0.5;
-        u0[k] = u1[k] = u2[k] = 0.0;
-        T[k] = 0.0;
-        lastp[k] = 0;
-        if (px < W && py < H) {
-            const long long p = (long long)py * W + px;
-            u0[k] = adj[p];
-            u1[k] = adj[P + p];
-            u2[k] = adj[2 * P + p];
-            T[k] = tfinal[p];
-            lastp[k] = last[p];
-            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
-        }
-        b0[k] = ro.bg[0] * T[k];
-        b1[k] = ro.bg[1] * T[k];
-        b2[k] = ro.bg[2] * T[k];
-        lmax = max(lmax, lastp[k]);
-    }
-    const int wlast = __reduce_max_sync(kFull, lmax);
-    for (int j = start + wlast - 1; j >= start; --j) {
-        const int id = __ldg(tl.tile_ids + j);
-        const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-        const double2 bx = __ldg(r2), by = __ldg(r2 + 1);
-        if (wx1 < bx.x || wx0 > bx.y || wy1 < by.x || wy0 > by.y) continue;
-        const double2 m = __ldg(r2 + 2), i0 = __ldg(r2 + 3), i1 = __ldg(r2 + 4);
-        const double2 c01 = __ldg(r2 + 5), c2 = __ldg(r2 + 6);
-        const double f[13] = {bx.x, bx.y, by.x, by.y, m.x, m.y, i0.x, i0.y, i1.x, i1.y,
-                              c01.x, c01.y, c2.x};
-        const int rel = j - start;
-        double g[kAdj];
-#pragma unroll
-        for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-        bool contrib = false;
-        const bool col_in = !(pxc < f[R_BX0] || pxc > f[R_BX1]);
-#pragma unroll
-        for (int k = 0; k < PPL; ++k) {
-            if (!col_in || rel >= lastp[k] || pyc[k] < f[R_BY0] || pyc[k] > f[R_BY1]) continue;
-            const double dx = pxc - f[R_MX], dy = pyc[k] - f[R_MY];
-            const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
-            double abar = __dmul_rn(f[R_ALPHA], gauss);
-            const bool clamped = abar >= ro.alpha_clamp;
-            if (clamped) abar = ro.alpha_clamp;
-            if (abar < ro.alpha_skip) continue;
-            contrib = true;
-            const double rom = 1.0 / __dsub_rn(1.0, abar);
-            const double t_in = T[k] * rom;
-            const double at = abar * t_in;
-            g[6] += u0[k] * at;
-            g[7] += u1[k] * at;
-            g[8] += u2[k] * at;
-            const double dab = u0[k] * (f[R_C0] * t_in - b0[k] * rom) +
-                               u1[k] * (f[R_C1] * t_in - b1[k] * rom) +
-                               u2[k] * (f[R_C2] * t_in - b2[k] * rom);
-            b0[k] += f[R_C0] * at;
-            b1[k] += f[R_C1] * at;
-            b2[k] += f[R_C2] * at;
-            if (!clamped) {
-                g[5] += gauss * dab;
-                const double de = abar * dab;
-                g[2] += de * (-0.5 * dx * dx);
-                g[3] += de * (-dx * dy);
-                g[4] += de * (-0.5 * dy * dy);
-                g[0] += de * (f[R_I00] * dx + f[R_I01] * dy);
-                g[1] += de * (f[R_I01] * dx + f[R_I11] * dy);
-            }
-            T[k] = t_in;
-        }
-        if (!__any_sync(kFull, contrib)) continue;
-        double v, v8;
-        warp_reduce9(g, lane, v, v8);
-        const long long dslot = __ldg(tl.sorted_d + j);  // splat-major duplicate slot
-        double* o = part + (dslot * kWarps + warp) * kAdj;
-        if ((lane & 3) == 0) o[lane >> 2] = v;
-        if (lane == 0) {
-            o[8] = v8;
-            mask[dslot * kWarps + warp] = 1;
-        }
-    }
 }
 
 // ------------------------------------------------------------------ K12 (raster)
@@ -1856,24 +1101,24 @@ __global__ void __launch_bounds__(32 * WPB)
     tangent[2 * P + p] = d2 + ro.bg[2] * dT;
 }
 
-// experiment knobs (read once): SGTR_WARP_CULL=1 enables the warp-level
-// contribution filter, SGTR_VJP_MINBLOCKS in {2, 3} the VJP register budget
+// kernel-variant knobs (read once; tools/variants.sh runs the GPU suite under
+// each): SGTR_FWD_WARP 4 = paired-entry K7 (default), 2 = one entry at a
+// time, 0 = the CTA form; SGTR_VJP_MODE 1 = per-warp partials (default), 0 =
+// the CTA slot form; SGTR_VJP_STAGED 3 = interleaved K10 with the ring
+// reduction (default), 2 = a branch per pixel and a reduction per fragment;
+// SGTR_VJP_MINBLOCKS the register budget (CTAs per SM) of those;
+// SGTR_JVP_WARP 2 = batch-staged K12 (default), 0 = the CTA form;
+// SGTR_WARP_CULL=1 the warp-level contribution filter of the CTA forms
 int knob(const char* name, int dflt) {
     const char* v = getenv(name);
     return v ? atoi(v) : dflt;
 }
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
-const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", 3);  // (slot-form VJP only)
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
-const int g_vjp_ppl = knob("SGTR_VJP_PPL", 1);
-const int g_fwd_ppl = knob("SGTR_FWD_PPL", 0);
-const int g_fwd_warp = knob("SGTR_FWD_WARP", 2);  // 2: batch-staged, 1: chunk-filtered
-const int g_vjp_staged = knob("SGTR_VJP_STAGED", 3);  // 3: batch-staged K10, 2 px/lane interleaved, ring reduction
-const int g_smem_red = knob("SGTR_VJP_SMEMRED", 1);
-const int g_vjp_prefetch = knob("SGTR_VJP_PREFETCH", 0);
-// warps per CTA of the warp-filtered forward / VJP kernels
-const int g_fwd_wpb = knob("SGTR_FWD_WPB", 2);
-const int g_wpb = knob("SGTR_WPB", 2);
+const int g_fwd_warp = knob("SGTR_FWD_WARP", 4);
+const int g_vjp_staged = knob("SGTR_VJP_STAGED", 3);
+const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", g_vjp_mode == 1 ? 10 : 3);
+const int g_jvp_warp = knob("SGTR_JVP_WARP", 2);
 
 }  // namespace
 
@@ -1885,27 +1130,10 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp == 4) {
+    else if (g_fwd_warp == 4)
         k_raster_fwd_paired<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    } else if (g_fwd_warp == 3) {
-        k_raster_fwd_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    } else if (g_fwd_warp == 2) {
-        if (g_fwd_wpb == 2)
-            k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-        else
-            k_raster_fwd_staged<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    } else if (g_fwd_warp) {
-        if (g_fwd_wpb == 2)
-            k_raster_fwd_warp<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-        else if (g_fwd_wpb == 4)
-            k_raster_fwd_warp<4><<<n * 2, 128, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-        else
-            k_raster_fwd_warp<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    }
-    else if (g_fwd_ppl == 4)
-        k_raster_fwd_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    else if (g_fwd_ppl == 2)
-        k_raster_fwd_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    else if (g_fwd_warp == 2)
+        k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_warp_cull)
         k_raster_fwd<false, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           nullptr);
@@ -1939,64 +1167,20 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_staged == 3 && g_vjp_min_blocks == 8)
+    if (g_vjp_staged == 2) {
+        if (g_vjp_min_blocks == 8)
+            k_raster_vjp_staged2<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                              part, mask);
+        else
+            k_raster_vjp_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
+                                                          part, mask);
+    } else if (g_vjp_min_blocks == 8) {
         k_raster_vjp_staged3<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                           part, mask);
-    else if (g_vjp_staged == 3)
+    } else {
         k_raster_vjp_staged3<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
                                                       mask);
-    else if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 12)
-        k_raster_vjp_staged2<2, 12><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                           part, mask);
-    else if (g_vjp_staged == 2 && g_wpb == 2 && g_vjp_min_blocks == 8)
-        k_raster_vjp_staged2<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                          part, mask);
-    else if (g_vjp_staged == 2 && g_wpb == 2)
-        k_raster_vjp_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                      mask);
-    else if (g_vjp_staged == 2)
-        k_raster_vjp_staged2<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                      mask);
-    else if (g_vjp_staged && g_wpb == 2 && !g_smem_red)
-        k_raster_vjp_staged<2, false><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                            part, mask);
-    else if (g_vjp_staged && g_wpb == 2 && g_vjp_min_blocks == 4)
-        k_raster_vjp_staged<2, true, 4><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
-                                                              last, part, mask);
-    else if (g_vjp_staged && g_wpb == 2)
-        k_raster_vjp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                     mask);
-    else if (g_vjp_staged)
-        k_raster_vjp_staged<8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                       part, mask);
-    else if (g_vjp_ppl == 4)
-        k_raster_vjp_ppl<4><<<n, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
-    else if (g_vjp_ppl == 2)
-        k_raster_vjp_ppl<2><<<n, 128, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
-    else if (g_vjp_prefetch == 2)
-        k_raster_vjp_warp<2, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
-                                                                 last, part, mask);
-    else if (g_vjp_prefetch == 3)
-        k_raster_vjp_warp<3, true, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
-                                                                 last, part, mask);
-    else if (g_smem_red && g_wpb == 2 && g_vjp_min_blocks == 4)
-        k_raster_vjp_warp<4, true, false, 2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj,
-                                                                    tfinal, last, part, mask);
-    else if (g_smem_red && g_wpb == 8 && g_vjp_min_blocks == 2)
-        k_raster_vjp_warp<2, true, false, 8><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj,
-                                                                     tfinal, last, part, mask);
-    else if (g_smem_red && g_wpb == 2)
-        k_raster_vjp_warp<3, true, false, 2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, adj,
-                                                                    tfinal, last, part, mask);
-    else if (g_smem_red && g_wpb == 4)
-        k_raster_vjp_warp<3, true, false, 4><<<n * 2, 128, 0, st>>>(tl, rec, W, H, ro, adj,
-                                                                     tfinal, last, part, mask);
-    else if (g_smem_red)
-        k_raster_vjp_warp<3, true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
-                                                                  last, part, mask);
-    else
-        k_raster_vjp_warp<3, false, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal,
-                                                                   last, part, mask);
+    }
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -2004,11 +1188,8 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    const int jvp = knob("SGTR_JVP_WARP", 2);
-    if (jvp == 2)
+    if (g_jvp_warp == 2)
         k_raster_jvp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
-    else if (jvp == 1)
-        k_raster_jvp_warp<<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     else if (g_warp_cull)
         k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     else
