@@ -300,7 +300,7 @@ __device__ __forceinline__ double transposed_1d(int p, int n, Ld ld) {
     return t;
 }
 
-__global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double* __restrict__ a,
+__global__ void __launch_bounds__(kThreads, 4) k_gather(int W, int H, const double* __restrict__ a,
                                                    const double* __restrict__ b,
                                                    const double* __restrict__ adjl1,
                                                    const double* __restrict__ Pf,
@@ -312,6 +312,19 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = (blockIdx.y + by0) * TY;
+    // this thread's two output pixels: their a, b, adjL1 fetched now so the
+    // latency overlaps the staging
+    double pa[2] = {0.0, 0.0}, pb[2] = {0.0, 0.0}, pl[2] = {0.0, 0.0};
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int gx = x0 + threadIdx.x % TX, gy = y0 + 2 * (threadIdx.x / TX) + rr;
+        if (gx < W && gy < H) {
+            const long long p = c * P + (long long)gy * W + gx;
+            pa[rr] = a[p];
+            pb[rr] = b[p];
+            if (adjl1) pl[rr] = adjl1[p];
+        }
+    }
     for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
         const int sy = i / SX, sx = i % SX;
         const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
@@ -396,8 +409,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(int W, int H, const double*
         if (gx >= W || gy >= H) continue;
         const double* t = t2[rr];
         const long long p = c * P + (long long)gy * W + gx;
-        const double base = adjl1 ? adjl1[p] : 0.0;
-        adj[p] = base + t[0] + a[p] * t[1] + b[p] * t[2];
+        adj[p] = pl[rr] + t[0] + pa[rr] * t[1] + pb[rr] * t[2];
     }
 }
 
