@@ -772,7 +772,6 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     double* gflag = tail + n1;
     double* hflag = tail + 2 * n1;
     double* errk = tail + 2 * n1 + 1;
-    double* erri = errk + (n1 + n2);
     const size_t fused_n = dim + tail_n + (refresh ? dim : 0);
     SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
     ensure_tail(c, tail_n);
