@@ -64,7 +64,7 @@ struct ModeTraits {
 // moments (kPre = false): 0 mu_a, 1 mu_b, 2 maa, 3 mbb, 4 mab, (5 dmu_a, 6 dmaa,
 // 7 dmab); with kPre the b moments are read from args.bmom instead
 template <int MODE, bool kPre = false>
-__global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
+__global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ssim(SsimArgs args) {
     using Tr = ModeTraits<MODE, kPre>;
     constexpr int NM = Tr::kMoments;
     extern __shared__ __align__(16) double smem[];
@@ -79,6 +79,20 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
     const double* A = args.a + c * P;
     const double* B = args.b + c * P;
     const double* DA = Tr::kTangent ? args.da + c * P : nullptr;
+    // the target moments of this thread's two output pixels, fetched now so
+    // their latency overlaps the staging (kPre)
+    double pre_mu_b[2] = {0.0, 0.0}, pre_mbb[2] = {0.0, 0.0};
+    if (kPre) {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int gx = x0 + threadIdx.x % TX, gy = y0 + 2 * (threadIdx.x / TX) + rr;
+            if (gx < W && gy < H) {
+                const long long pi = c * P + (long long)gy * W + gx;
+                pre_mu_b[rr] = args.bmom[pi];
+                pre_mbb[rr] = args.bmom[3 * P + pi];
+            }
+        }
+    }
     for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
         const int sy = i / SX, sx = i % SX;
         const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
@@ -166,8 +180,8 @@ __global__ void __launch_bounds__(kThreads) k_ssim(SsimArgs args) {
         const S mu_a = mk<S>(m[Tr::MUA], Tr::kTangent ? m[Tr::DMUA] : 0.0);
         const S maa = mk<S>(m[Tr::MAA], Tr::kTangent ? m[Tr::DMAA] : 0.0);
         const S mab = mk<S>(m[Tr::MAB], Tr::kTangent ? m[Tr::DMAB] : 0.0);
-        const double mu_b = kPre ? args.bmom[pi] : m[Tr::MUB < 0 ? 0 : Tr::MUB];
-        const double mbb = kPre ? args.bmom[3 * P + pi] : m[Tr::MBB < 0 ? 0 : Tr::MBB];
+        const double mu_b = kPre ? pre_mu_b[rr] : m[Tr::MUB < 0 ? 0 : Tr::MUB];
+        const double mbb = kPre ? pre_mbb[rr] : m[Tr::MBB < 0 ? 0 : Tr::MBB];
         const S n1 = 2.0 * mu_a * mu_b + kC1;
         const S d1 = mu_a * mu_a + mu_b * mu_b + kC1;
         const S n2 = 2.0 * (mab - mu_a * mu_b) + kC2;
