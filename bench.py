@@ -218,6 +218,35 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=
     return 1.0 / t_iter, model
 
 
+def c1_psnr_delta(sp, orc, iters=100):
+    """BASELINE's "PSNR delta": the C1 run (10K splats, 4 views of 128x128,
+    seed 1, view 0 held out, |S1| = 1, refresh every 10th step) for `iters`
+    3DGS2-TR iterations through the library and through the oracle port (its
+    parity build) from the same seed; final held-out PSNR of each
+    (evaluate_scene: quantize8 + psnr).  tests/test_gpu_c1_run.py holds the
+    same run to 0.05 dB."""
+    orc.set_sh_degree(0)
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=10000, init_splats=10000, views=4,
+                                            image_size=128, seed=1))
+    train = [1, 2, 3]
+    o_cams, o_gts = [ds.cams[i] for i in train], [ds.gts[i] for i in train]
+    views = [sp.Camera.from_c(c, g) for c, g in zip(o_cams, o_gts)]
+    st = sp.OptimizerState(ds.init_x.size, 1)
+    scene = sp.Scene(ds.init_x)
+    opts = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, iters),
+                               batch_size=1, record_applied_step=False)
+    ost, xo = orc.State(ds.init_x.size, 1), ds.init_x.copy()
+    oopts = orc.TrOptions(total_steps=iters, batch_size=1)
+    for _ in range(iters):
+        sp.step_3dgs2tr(st, scene, views, opts)
+        orc.step_3dgs2tr(ost, xo, o_cams, o_gts, oopts)
+    p_gpu = sp.evaluate_scene(scene, [sp.Camera.from_c(ds.cams[0], ds.gts[0])]).mean_psnr
+    p_cpu = orc.psnr(orc.quantize8(orc.rasterize(xo, ds.cams[0])[0]), ds.gts[0])
+    return {"config": f"C1: 10K splats, 4 views 128x128, seed 1, view 0 held out, {iters} "
+                      "iterations, |S1|=1, refresh every 10th",
+            "gpu_db": float(p_gpu), "cpu_db": float(p_cpu), "delta_db": float(p_gpu - p_cpu)}
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -480,6 +509,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import pyoracle as orc
         orc.build()
+        psnr_delta = c1_psnr_delta(sp, orc)  # parity build, before the timing build loads
         timing_lib = orc.use_timing_build()
         cam = orc.Camera()
         src = cams[1]._c()
@@ -494,7 +524,8 @@ def main():
                           f"extrapolated to {b} views x {w}x{h} + 1/10 refresh view + "
                           f"shd_radii at full K; oracle build {os.path.basename(timing_lib)} "
                           f"(-O3 -march=native when it built)"),
-               "model_s": {kk: float(vv) for kk, vv in model.items()}}
+               "model_s": {kk: float(vv) for kk, vv in model.items()},
+               "psnr_delta": psnr_delta}
 
     if rank == 0:
         line = {
