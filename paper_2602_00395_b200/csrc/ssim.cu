@@ -463,10 +463,18 @@ __global__ void k_quantize8(double* img, long long n) {
     img[i] = round(c * 255.0) / 255.0;
 }
 
-bool g_kernel_ready = false;
+// per-device state: __constant__ data and function attributes are set per
+// device, and a process may hold contexts on several devices
+int current_device() {
+    int dev = 0;
+    SGTR_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+unsigned long long g_kernel_ready = 0;  // bit d: c_k uploaded on device d
 
 void init_constants() {
-    if (g_kernel_ready) return;
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    if (g_kernel_ready & bit) return;
     // kernel1d (ssim.cpp:21-34), computed on the host exactly as the oracle
     double k[11], sum = 0.0;
     for (int i = 0; i < 11; ++i) {
@@ -476,7 +484,7 @@ void init_constants() {
     }
     for (double& v : k) v /= sum;
     SGTR_CUDA(cudaMemcpyToSymbol(c_k, k, sizeof(k)));
-    g_kernel_ready = true;
+    g_kernel_ready |= bit;
 }
 
 template <int MODE, bool kPre = false>
@@ -484,11 +492,12 @@ void run_ssim(cudaStream_t st, const SsimArgs& a) {
     using Tr = ModeTraits<MODE, kPre>;
     const size_t smem = sizeof(double) * (SY * SX * (Tr::kTangent ? 3 : 2) +
                                           Tr::kMoments * SY * TX);
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // bit d: attribute set on device d
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    if (!(attr & bit)) {
         SGTR_CUDA(cudaFuncSetAttribute(k_ssim<MODE, kPre>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
+        attr |= bit;
     }
     const int by1 = a.by1 > 0 ? a.by1 : ceil_div(a.H, TY);
     if (by1 <= a.by0) return;
