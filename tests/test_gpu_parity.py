@@ -730,3 +730,30 @@ def test_kat_invisible_splat_zero_diagonal(sp, orc):  # test_optimizer.cpp:110-1
           [11 * K + 3 * kk + c_ for c_ in range(3)]
     assert np.all(d[idx] == 0.0)
     assert np.any(d != 0.0)
+
+
+def test_alpha_clamp_branch_parity(sp, orc):
+    # opacities near the box top (scene.cpp:49-57 clamps to 0.995) put the
+    # centre pixels on render.cpp's alpha_bar >= 0.99 clamp, whose frozen
+    # branch zeroes the alpha / conic tangents and adjoints of those pairs
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=200, init_splats=200, views=3,
+                                            image_size=40, seed=21))
+    mu, s, q, alpha, c = orc.unpack(ds.gt_x)
+    rng = np.random.default_rng(5)
+    alpha = rng.uniform(0.985, 0.995, size=alpha.shape)
+    x = orc.pack(mu, s * 2.0, q, alpha, c)
+    for oc in ds.cams:
+        cam = sp.Camera.from_c(oc)
+        img, t = orc.rasterize(x, oc)
+        out = sp.rasterize(sp.Scene(x), cam)
+        assert rel(out.color, img) < IMG_TOL and rel(out.t_final, t) < IMG_TOL
+        v = rng.normal(size=x.size)
+        u = rng.normal(size=img.shape)
+        jv = sp.rasterize_jvp(sp.Scene(x), cam, v)
+        assert rel(jv, orc.rasterize_jvp(x, oc, v)) < IMG_TOL
+        vj = sp.rasterize_vjp(sp.Scene(x), cam, u)
+        assert rel(vj, orc.rasterize_vjp(x, oc, u)) < GRAD_TOL
+        lhs, rhs = float(np.sum(u * jv)), float(vj @ v)
+        assert abs(lhs - rhs) <= 1e-9 * (1 + abs(lhs))
+    e, cc = orc.blend_stats(x, ds.cams[0])
+    assert cc > 0
