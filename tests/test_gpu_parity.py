@@ -757,3 +757,31 @@ def test_alpha_clamp_branch_parity(sp, orc):
         assert abs(lhs - rhs) <= 1e-9 * (1 + abs(lhs))
     e, cc = orc.blend_stats(x, ds.cams[0])
     assert cc > 0
+
+
+def test_binning_and_render_large_rectangles(sp, orc):
+    # fragments whose pixel rectangles span more than 64 tiles take K4's
+    # warp-per-rectangle path (k_emit_large); mixed with small ones
+    rng = np.random.default_rng(11)
+    k = 120
+    mu = np.column_stack([rng.uniform(-0.6, 0.6, k), rng.uniform(-0.6, 0.6, k),
+                          rng.uniform(0.8, 2.5, k)])
+    s = np.exp(rng.uniform(np.log(0.005), np.log(0.05), (k, 3)))
+    s[:6] = [[0.6, 0.5, 0.4]] * 6  # > 64 tiles each at 320x256
+    q = rng.normal(size=(k, 4))
+    x = orc.pack(mu, s, q, rng.uniform(0.05, 0.6, k), rng.uniform(0, 1, (k, 3)))
+    oc = orc.camera(width=320, height=256, fx=300.0, fy=300.0, cx=160.0, cy=128.0)
+    pr = orc.project(x, oc)
+    vis = pr[:, 0] == 0
+    tiles = ((pr[vis, 5] - pr[vis, 4]) / 16 + 1) * ((pr[vis, 7] - pr[vis, 6]) / 16 + 1)
+    assert np.sum(tiles > 64) >= 3
+    cam = sp.Camera.from_c(oc)
+    g = _gpu_binning(sp, x, cam)
+    r = orc.binning(x, oc)
+    for a, b in zip(g, r):
+        assert np.array_equal(a, b)
+    img, t = orc.rasterize(x, oc)
+    out = sp.rasterize(sp.Scene(x), cam)
+    assert rel(out.color, img) < IMG_TOL and rel(out.t_final, t) < IMG_TOL
+    u = rng.normal(size=img.shape)
+    assert rel(sp.rasterize_vjp(sp.Scene(x), cam, u), orc.rasterize_vjp(x, oc, u)) < GRAD_TOL
