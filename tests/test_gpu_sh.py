@@ -123,3 +123,38 @@ def test_checkpoint_keeps_sh_degree(sp, orc3, tmp_path):
     assert d.sh_degree == 3 and np.array_equal(d.get_scene(), ds.init_x)
     with pytest.raises(sp.InvalidArgument, match="PLY"):
         c.save_scene(tmp_path / "sh.ply")
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_lower_degrees_render_gradient_step(sp, orc, deg):
+    # degrees 1 and 2 (3 and 8 coefficients per channel): render, JVP, VJP,
+    # gradient and a few 3DGS2-TR steps against the oracle
+    orc.set_sh_degree(deg)
+    try:
+        nb = (deg + 1) ** 2 - 1
+        ds = orc.make_synthetic(orc.SynthConfig(gt_splats=300, init_splats=300, views=4,
+                                                image_size=40, seed=13 + deg, sh_degree=deg))
+        x = ds.gt_x
+        scene = sp.Scene(x, sh_degree=deg)
+        r = np.random.default_rng(deg)
+        for c in ds.cams[:2]:
+            cam = sp.Camera.from_c(c)
+            assert rel(sp.rasterize(scene, cam).color, orc.rasterize(x, c)[0]) < IMG_TOL
+            v = r.normal(size=x.size) * 1e-2
+            assert rel(sp.rasterize_jvp(scene, cam, v), orc.rasterize_jvp(x, c, v)) < IMG_TOL
+            u = r.normal(size=(c.height, c.width, 3))
+            assert rel(sp.rasterize_vjp(scene, cam, u), orc.rasterize_vjp(x, c, u)) < GRAD_TOL
+        views = [sp.Camera.from_c(c, g) for c, g in zip(ds.cams, ds.gts)]
+        st = sp.OptimizerState(ds.init_x.size, 3, sh_degree=deg)
+        sc = sp.Scene(ds.init_x, sh_degree=deg)
+        ost, xo = orc.State(ds.init_x.size, 3), ds.init_x.copy()
+        opts = sp.OptimizerOptions(batch_size=2, schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 20))
+        oopts = orc.TrOptions(total_steps=20, batch_size=2)
+        for _ in range(3):
+            dg = sp.step_3dgs2tr(st, sc, views, opts)
+            do = orc.step_3dgs2tr(ost, xo, ds.cams, ds.gts, oopts)
+            assert dg.batch_loss == pytest.approx(do["batch_loss"], rel=1e-8)
+            assert rel(sc.x, xo) < IMG_TOL
+        assert sc.x.size == (14 + 3 * nb) * 300
+    finally:
+        orc.set_sh_degree(0)
