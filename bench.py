@@ -223,8 +223,8 @@ def c1_psnr_delta(sp, orc, iters=100):
     seed 1, view 0 held out, |S1| = 1, refresh every 10th step) for `iters`
     3DGS2-TR iterations through the library and through the oracle port (its
     parity build) from the same seed; final held-out PSNR of each
-    (evaluate_scene: quantize8 + psnr).  tests/test_gpu_c1_run.py holds the
-    same run to 0.05 dB."""
+    (evaluate_scene: quantize8 + psnr).  tests/test_c1_training.py holds the
+    same run to 0.05 dB against a committed oracle trajectory."""
     orc.set_sh_degree(0)
     ds = orc.make_synthetic(orc.SynthConfig(gt_splats=10000, init_splats=10000, views=4,
                                             image_size=128, seed=1))
