@@ -355,7 +355,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, id_rank;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     // further view lanes (stream + per-view workspace), swapped in by
@@ -370,7 +370,7 @@ struct Ctx {
     X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp) X(slots)    \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
-    X(part) X(mask) X(tmask) X(large) X(trect)
+    X(part) X(mask) X(tmask) X(large) X(trect) X(id_rank)
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
@@ -602,10 +602,12 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
         double* adj9 = chain_mode() == 2
                            ? c.slots.as<double>((size_t)kAdj * std::max(vr.n_visible, 1))
                            : nullptr;
+        int* rank = c.id_rank.as<int>(std::max(c.K, 1));
+        launch_rank_of(c.st, c.ids_alt.get<int>(), c.K, rank);
         launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                          c.off_r.get<long long>(), c.tcount.get<int>(), nullptr, part,
+                          c.off_r.get<long long>(), c.tcount.get<int>(), rank, part,
                           mask, zdense, zbits, acc, flag, adj9);
-        c.launches += adj9 ? 3 : 2;
+        c.launches += adj9 ? 4 : 3;
         return;
     }
     double* slots = c.slots.as<double>((size_t)kAdj * nd);

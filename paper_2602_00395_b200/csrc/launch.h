@@ -92,9 +92,12 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
 // K11 over the per-warp partials of the barrier-free K10
+// splat id -> depth rank (inverse of the depth order), for launch_chain_warp's inv
+void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank);
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                        const RenderP& ro, const int* sorted_ids, int n_visible,
-                       const long long* off_r, const int* tcount, const int* inv,
+                       const long long* off_r, const int* tcount,
+                       const int* inv,  // splat id -> depth rank: id-order threads (or null)
                        const double* part, const unsigned char* mask, const double* zdense,
                        const uint32_t* zbits, double* acc, double* nonfinite_flag,
                        double* adj9 = nullptr);  // adj9 (9 x n_visible): split K11a/K11b

@@ -344,11 +344,17 @@ __global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __re
                                                const double* __restrict__ adj9,
                                                double* __restrict__ acc,
                                                double* nonfinite_flag) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_visible) return;
-    const int id = sorted_ids[r];
+    // with inv (splat id -> depth rank) the threads run in splat-id order, so
+    // the scene reads and the gradient read-modify-writes below are
+    // coalesced (at C5's 10M splats they no longer fit in L2, and a
+    // depth-order walk would touch a 32-byte sector per 8-byte access); the
+    // partials are found through the rank.  Without it, in depth-rank order.
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (inv ? K : n_visible)) return;
+    const int id = inv ? t : sorted_ids[t];
     const int cnt = tcount[id];
     if (cnt == 0) return;
+    const int r = inv ? inv[id] : t;
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
@@ -438,7 +444,19 @@ __global__ void __launch_bounds__(256) k_partials_to_slots(const int* __restrict
     for (int c = 0; c < kAdj; ++c) o[c] = a[c];
 }
 
+// splat id -> depth rank (the inverse of K2's order), for K11's id-order walk
+__global__ void k_rank_of(const int* __restrict__ sorted_ids, int K, int* __restrict__ rank) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < K) rank[sorted_ids[r]] = r;
+}
+
 }  // namespace
+
+void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank) {
+    if (K == 0) return;
+    k_rank_of<<<ceil_div(K, 256), 256, 0, st>>>(sorted_ids, K, rank);
+    SGTR_CUDA(cudaGetLastError());
+}
 
 void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
                               const double* part, const unsigned char* mask, double* slots) {
@@ -483,24 +501,25 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb
                        const uint32_t* zbits, double* acc, double* nonfinite_flag,
                        double* adj9) {
     if (n_visible == 0) return;
+    const int nt = inv ? K : n_visible;  // threads: splat ids or depth ranks
     if (adj9) {
         k_sum_adjoints<<<ceil_div(n_visible, 256), 256, 0, st>>>(sorted_ids, n_visible, off_r,
                                                                   tcount, inv, part, mask, adj9);
         SGTR_CUDA(cudaGetLastError());
         if (nb)
-            k_chain_warp<true, true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+            k_chain_warp<true, true><<<ceil_div(nt, 128), 128, 0, st>>>(
                 mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
                 zdense, zbits, adj9, acc, nonfinite_flag);
         else
-            k_chain_warp<true, false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+            k_chain_warp<true, false><<<ceil_div(nt, 128), 128, 0, st>>>(
                 mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
                 zdense, zbits, adj9, acc, nonfinite_flag);
     } else if (nb) {
-        k_chain_warp<false, true><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+        k_chain_warp<false, true><<<ceil_div(nt, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
             zbits, nullptr, acc, nonfinite_flag);
     } else {
-        k_chain_warp<false, false><<<ceil_div(n_visible, 128), 128, 0, st>>>(
+        k_chain_warp<false, false><<<ceil_div(nt, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
             zbits, nullptr, acc, nonfinite_flag);
     }
