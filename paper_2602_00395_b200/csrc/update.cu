@@ -161,30 +161,47 @@ __device__ void rot_axis_setup(const Prim& p, const double* sigma, int axis, Rot
     ra.alpha = p.alpha;
 }
 
+// rotation-only H^2 at quaternion offset dq along the axis.  This TU is
+// compiled without FMA contraction (bit-exact projection-side arithmetic);
+// here the products are fused explicitly: the certification and the 60-step
+// bisection evaluate it ~100 times per queued axis, and its ~1e-8 relative
+// floor (the 1 - det_s / sqrt(det) cancellation) is far above the rounding
+// the fusion changes.
 __device__ double rot_h2(const RotAxis& ra, double dq) {
-    const double r2p = ra.r2 + dq * (2.0 * ra.qc + dq);
+    const double r2p = __fma_rn(dq, 2.0 * ra.qc + dq, ra.r2);
     if (r2p < 1e-24) return CUDART_INF;
+    const double dq2 = dq * dq;
     double m[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) m[i] = ra.rt[i] + dq * ra.drt[i];
-    m[0] += dq * dq * ra.h[0];
-    m[4] += dq * dq * ra.h[1];
-    m[8] += dq * dq * ra.h[2];
+    for (int i = 0; i < 9; ++i) m[i] = __fma_rn(dq, ra.drt[i], ra.rt[i]);
+    m[0] = __fma_rn(dq2, ra.h[0], m[0]);
+    m[4] = __fma_rn(dq2, ra.h[1], m[4]);
+    m[8] = __fma_rn(dq2, ra.h[2], m[8]);
     const double inv = 1.0 / (r2p * r2p);
+    double ms[9];  // m[3a + i] * s_a^2
+#pragma unroll
+    for (int a3 = 0; a3 < 3; ++a3)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ms[3 * a3 + i] = m[3 * a3 + i] * ra.s2[a3];
     double c[6];  // (R~^T S^2 R~)_{00,01,02,11,12,22}
     const int ij[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 #pragma unroll
     for (int e = 0; e < 6; ++e) {
         const int i = ij[e][0], j = ij[e][1];
-        c[e] = (m[i] * ra.s2[0] * m[j] + m[3 + i] * ra.s2[1] * m[3 + j] +
-                m[6 + i] * ra.s2[2] * m[6 + j]) * inv;
+        double t = ms[i] * m[j];
+        t = __fma_rn(ms[3 + i], m[3 + j], t);
+        t = __fma_rn(ms[6 + i], m[6 + j], t);
+        c[e] = t * inv;
     }
     const double mid[9] = {0.5 * (ra.sigma[0] + c[0]), 0.5 * (ra.sigma[1] + c[1]),
                            0.5 * (ra.sigma[2] + c[2]), 0.5 * (ra.sigma[3] + c[1]),
                            0.5 * (ra.sigma[4] + c[3]), 0.5 * (ra.sigma[5] + c[4]),
                            0.5 * (ra.sigma[6] + c[2]), 0.5 * (ra.sigma[7] + c[4]),
                            0.5 * (ra.sigma[8] + c[5])};
-    const double dm = det3(mid);
+    const double d0 = __fma_rn(mid[4], mid[8], -(mid[5] * mid[7]));
+    const double d1 = __fma_rn(mid[3], mid[8], -(mid[5] * mid[6]));
+    const double d2 = __fma_rn(mid[3], mid[7], -(mid[4] * mid[6]));
+    const double dm = __fma_rn(mid[2], d2, __fma_rn(mid[0], d0, -(mid[1] * d1)));
     if (!(dm > 0.0)) return CUDART_INF;
     return ra.alpha * (1.0 - ra.det_s * rsqrt(dm));
 }
