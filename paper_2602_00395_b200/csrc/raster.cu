@@ -1130,8 +1130,8 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
-    else if (g_fwd_warp == 4)
-        k_raster_fwd_paired<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    else if (g_fwd_warp == 4)  // one-warp CTAs: each retires as soon as its block is done
+        k_raster_fwd_paired<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_warp == 2)
         k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_warp_cull)
