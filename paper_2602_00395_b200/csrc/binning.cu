@@ -162,6 +162,15 @@ __global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restri
     trect[j] = rect[id];
 }
 
+__global__ void k_tile_order_keys(const int* __restrict__ start, const int* __restrict__ end,
+                                  int n, unsigned int* __restrict__ keys,
+                                  int* __restrict__ vals) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    keys[t] = 0xffffu - (unsigned int)min(end[t] - start[t], 0xffff);
+    vals[t] = t;
+}
+
 int bits_for(int n) {
     int b = 1;
     while ((1LL << b) < n) ++b;
@@ -199,6 +208,25 @@ size_t tile_sort_temp_bytes(long long n_dup, int n_tiles) {
                                     (unsigned int*)nullptr, (int*)nullptr, (int*)nullptr,
                                     (int)n_dup, 0, bits_for(n_tiles));
     return bytes;
+}
+
+size_t tile_order_temp_bytes(int n_tiles) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned int*)nullptr,
+                                    (unsigned int*)nullptr, (int*)nullptr, (int*)nullptr,
+                                    n_tiles, 0, 16);
+    return bytes;
+}
+
+void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_end, int n_tiles,
+                       unsigned int* keys, unsigned int* keys_alt, int* vals, int* order,
+                       void* temp, size_t temp_bytes) {
+    if (n_tiles == 0) return;
+    k_tile_order_keys<<<ceil_div(n_tiles, 256), 256, 0, st>>>(tile_start, tile_end, n_tiles,
+                                                              keys, vals);
+    SGTR_CUDA(cudaGetLastError());
+    SGTR_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, vals, order,
+                                              n_tiles, 0, 16, st));
 }
 
 void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {

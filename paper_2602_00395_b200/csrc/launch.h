@@ -75,7 +75,15 @@ struct TileLists {
     const int4* trect;    // per position: the splat's pixel rectangle (x0, y0, x1, y1)
     int row0, row1;       // tile rows the raster kernels process (a band on refresh
                           // views split over ranks; [0, tiles_y) otherwise)
+    const int* order = nullptr;  // full frames: tiles by decreasing list length (the
+                                 // raster kernels' launch order), else row-major
 };
+// tiles by decreasing list length (ties by index) into order[0, n_tiles):
+// the long tiles start first, so the grid's tail is short ones
+size_t tile_order_temp_bytes(int n_tiles);
+void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_end, int n_tiles,
+                       unsigned int* keys, unsigned int* keys_alt, int* vals, int* order,
+                       void* temp, size_t temp_bytes);
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, double* img, double* tfinal, int* last,

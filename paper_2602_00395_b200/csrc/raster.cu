@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(32 * WPB)
     __shared__ __align__(16) StagedRec s_rec[WPB][32];
     __shared__ int4 s_rect[WPB][32];
     __shared__ int s_pos[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
@@ -759,7 +760,8 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     __shared__ int4 s_rect[WPB][32];
     __shared__ int s_pos[WPB][32];
     __shared__ int s_slot[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
     const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
@@ -1018,7 +1020,8 @@ __global__ void __launch_bounds__(32 * WPB)
     __shared__ __align__(16) StagedRec s_rec[WPB][32];
     __shared__ __align__(16) StagedTan s_tan[WPB][32];
     __shared__ int4 s_rect[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
     const int warp = (blockIdx.x % SUB) * WPB + lw;
     const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
