@@ -1180,8 +1180,8 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
     } else if (g_vjp_min_blocks == 8) {
         k_raster_vjp_staged3<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                           part, mask);
-    } else {
-        k_raster_vjp_staged3<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+    } else {  // one-warp CTAs, as K7
+        k_raster_vjp_staged3<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
                                                       mask);
     }
     SGTR_CUDA(cudaGetLastError());
