@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ so
 // K11b: the chain of each visible splat from its summed adjoints
 // (kPre) or, without kPre, summing the partials itself (one kernel)
 template <bool kPre, bool kSH>
-__global__ void __launch_bounds__(128) k_chain_warp(int mode, const double* __restrict__ x, int K,
+__global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
                                                const long long* __restrict__ off_r,
