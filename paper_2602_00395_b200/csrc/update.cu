@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
 // K14a': one thread per (splat, rotation axis) (trust_region.cpp:198-234):
 // curvature beta_c, Taylor radius, certification against the exact
 // rotation-only H^2; axes failing certification are queued for K14b
-__global__ void __launch_bounds__(kThreads) k_tr_rot(TrArgs a) {
+__global__ void __launch_bounds__(kThreads, 5) k_tr_rot(TrArgs a) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 4LL * a.n) return;
     const int i = a.i0 + (int)(t >> 2), c = (int)(t & 3);
