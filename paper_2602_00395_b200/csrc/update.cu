@@ -337,7 +337,7 @@ __device__ void block_reduce5(double* v, int bad, double* out, int* bad_out) {
 // block partials) and computes the radii of the splats in [i0, i0 + n);
 // without it, it covers [i0, i0 + n) and computes only their radii (the
 // other shards of a sharded update).
-__global__ void __launch_bounds__(kThreads) k_tr_prepare(TrArgs a) {
+__global__ void __launch_bounds__(kThreads, 8) k_tr_prepare(TrArgs a) {
     const bool ew = a.elementwise;
     const int i = (ew ? 0 : a.i0) + blockIdx.x * blockDim.x + threadIdx.x;
     const long long K = a.K;
