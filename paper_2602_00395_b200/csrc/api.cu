@@ -141,6 +141,9 @@ struct StepDraws {
     std::vector<uint32_t> bits;
     Rng after_s1;  // state to restore when the gradient phase fails
     Rng after;     // state after all of the step's draws
+    // state after probe s (the reference draws each probe lazily,
+    // optimizer.cpp:67-73, :86-87): restored when Hutchinson sample s fails
+    std::vector<Rng> after_probe;
 };
 
 StepDraws draw_step(Rng& rng, long long t, const DrawKey& k, const std::atomic<bool>* stop) {
@@ -162,6 +165,7 @@ StepDraws draw_step(Rng& rng, long long t, const DrawKey& k, const std::atomic<b
                 for (int b = 0; b < n; ++b) word |= (uint32_t)(rng.gen() & 1u) << b;
                 w[base >> 5] = word;
             }
+            d.after_probe.push_back(rng);
         }
     }
     d.after = rng;
@@ -761,14 +765,15 @@ void allreduce(Ctx& c, double* buf, size_t n) {
 }
 
 // ------------------------------------------------------------------ Algorithm 1
-// One step with its draws given.  `rng_ckpt` (if any) is the state to restore
-// when the step fails inside the gradient phase, where the reference throws
-// before drawing S2 and the probes.
+// One step with its draws given.  `draws` (if any) carries the Rng states to
+// restore when the step fails: inside the gradient phase the reference throws
+// before drawing S2 and the probes; at Hutchinson sample s it has drawn
+// probes 0..s only.
 // `kind` selects the update (TrArgs::kind): 0 the 3DGS2-TR Newton step,
 // 1 ADAM, 2 ADAM-TR; the ADAM kinds never refresh.
 void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& s1,
                const std::vector<int>& s2, const std::vector<uint32_t>& zbits, int nu,
-               bool refresh, const Rng* rng_ckpt, sgtr_step_diagnostics* diag, int kind = 0,
+               bool refresh, const StepDraws* draws, sgtr_step_diagnostics* diag, int kind = 0,
                const sgtr_adam_options* adam = nullptr) {
     const int M = (int)c.views.size();
     const int W = c.views[0].dc.W, H = c.views[0].dc.H, P = W * H;
@@ -777,9 +782,10 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     const RenderP ro = render_params(o.render);
     const int n1 = (int)s1.size(), n2 = refresh ? (int)s2.size() : 0;
     // fused buffer, summed by one allreduce per step:
-    //   [g_acc (dim) | loss[n1] | gflag[n1] | hflag | err_kind[n1+n2] |
+    //   [g_acc (dim) | loss[n1] | gflag[n1] | hflag[nu] | err_kind[n1+n2] |
     //    err_index[n1+n2] | w_acc (dim, refresh steps only)]
-    const size_t tail_n = 2 * n1 + 1 + 2 * (n1 + n2);
+    const int nflag = refresh ? nu : 1;
+    const size_t tail_n = 2 * n1 + nflag + 2 * (n1 + n2);
     const size_t tail_off = dim;
     double* fused = c.fused.as<double>(2 * dim + tail_n);
     double* g_acc = fused;
@@ -788,7 +794,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     double* loss = tail;
     double* gflag = tail + n1;
     double* hflag = tail + 2 * n1;
-    double* errk = tail + 2 * n1 + 1;
+    double* errk = tail + 2 * n1 + nflag;
     const size_t fused_n = dim + tail_n + (refresh ? dim : 0);
     SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
     ensure_tail(c, tail_n);
@@ -891,7 +897,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                     if (B == 1) {
                         residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(),
                                          nullptr, o.residual.lambda, o.residual.floor, nullptr);
-                        backward_view(c, v.dc, ro, vr, 1, nullptr, zb, w_acc, hflag);
+                        backward_view(c, v.dc, ro, vr, 1, nullptr, zb, w_acc, hflag + s);
                     } else {
                         residual_adjoint(c, HUTCH, W, H, view_gt(c, s2[q]), c.tan.get<double>(),
                                          nullptr, o.residual.lambda, o.residual.floor, nullptr,
@@ -899,7 +905,10 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                         ViewRender vb = vr;
                         vb.tl.row0 = tr0;
                         vb.tl.row1 = tr1;
-                        backward_view(c, v.dc, ro, vb, 1, nullptr, zb, w_acc, hflag);
+                        // the length order covers the whole frame; a band
+                        // walks its own tile rows in row-major order
+                        vb.tl.order = nullptr;
+                        backward_view(c, v.dc, ro, vb, 1, nullptr, zb, w_acc, hflag + s);
                     }
                 }
             }
@@ -913,14 +922,14 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                               c.st));
     SGTR_CUDA(cudaStreamSynchronize(c.st));
     const double* ht = c.htail;
-    const double* hk = ht + 2 * n1 + 1;
+    const double* hk = ht + 2 * n1 + nflag;
     const double* hi = hk + (n1 + n2);
     // gradient-phase failures: nothing but t and the S1 draw has happened
     for (int p = 0; p < n1; ++p) {
         if (hk[p] != 0.0 || ht[n1 + p] != 0.0) {
-            if (rng_ckpt) {
+            if (draws) {
                 c.prefetch.reset();
-                c.rng = *rng_ckpt;
+                c.rng = draws->after_s1;
             }
             if (hk[p] == 1.0)
                 throw numeric("rasterize: non-finite parameter in splat " +
@@ -936,13 +945,23 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     int hutch_err = 0;
     long long hutch_idx = 0;
     bool hutch_fail = false;
+    int fail_sample = 0;  // the reference throws at the first failing sample
     if (refresh) {
         for (int q = 0; q < n2 && !hutch_err; ++q)
             if (hk[n1 + q] != 0.0) {
                 hutch_err = (int)hk[n1 + q];
                 hutch_idx = (long long)hi[n1 + q];
             }
-        hutch_fail = hutch_err != 0 || ht[2 * n1] != 0.0;
+        hutch_fail = hutch_err != 0;  // a render error fails sample 0
+        for (int s = 0; s < nu && !hutch_fail; ++s)
+            if (ht[2 * n1 + s] != 0.0) {
+                hutch_fail = true;
+                fail_sample = s;
+            }
+        if (hutch_fail && draws && fail_sample < (int)draws->after_probe.size()) {
+            c.prefetch.reset();
+            c.rng = draws->after_probe[fail_sample];
+        }
     }
     // K14
     double eps = -1.0;
@@ -1522,9 +1541,10 @@ int sgtr_load_cameras(const char* path, sgtr_camera* cams, char* image_names, in
 }
 
 // Optimizer-state checkpoint (the reference only checkpoints
-// the scene PLY, harness.cpp:157-164).  Layout: "SGTRCKP1", K, t, the
-// mt19937_64 state as its standard text form (length-prefixed), the Rng's
-// normal() spare, then x | g_hat | d_hat | adam_m | adam_v (group-major).
+// the scene PLY, harness.cpp:157-164).  Layout: "SGTRCKP2", then four int64
+// header fields K, t, the length of the Rng text and the SH basis count nb,
+// the mt19937_64 state as its standard text form, the Rng's normal() spare
+// (flag, value), then x | g_hat | d_hat | adam_m | adam_v (group-major).
 int sgtr_checkpoint_save(sgtr_ctx* ctx, const char* path) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
@@ -1569,7 +1589,8 @@ int sgtr_checkpoint_load(sgtr_ctx* ctx, const char* path) {
         long long hdr[4];
         in.read(magic, 8);
         in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
-        if (!in || std::memcmp(magic, "SGTRCKP2", 8) != 0 || hdr[0] < 0 || hdr[2] <= 0 ||
+        if (!in || std::memcmp(magic, "SGTRCKP2", 8) != 0 || hdr[0] < 0 || hdr[0] > (1LL << 28) ||
+            hdr[2] <= 0 ||
             hdr[2] > (1 << 20) || !(hdr[3] == 0 || hdr[3] == 3 || hdr[3] == 8 || hdr[3] == 15))
             throw Error(SGTR_RUNTIME, std::string("checkpoint: not a checkpoint file: ") + path);
         std::string rtxt(hdr[2], '\0');
@@ -1715,8 +1736,7 @@ int sgtr_step_3dgs2tr(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
         c.t = t_new;
         c.rng = d.after;
         if (c.prefetch.exhausted()) c.prefetch.start(c.rng, t_new + 1, key);
-        const Rng ckpt = d.after_s1;
-        step_core(c, *opt, d.s1, d.s2, d.bits, opt->hutch_samples, d.refresh, &ckpt, diag);
+        step_core(c, *opt, d.s1, d.s2, d.bits, opt->hutch_samples, d.refresh, &d, diag);
     });
 }
 
@@ -1729,11 +1749,13 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
         bind(c);
         need_scene(c);
         check_views(c, true);
+        if (!opt || !diag) throw invalid("step_3dgs2tr: null options or diagnostics");
         *diag = sgtr_step_diagnostics{0, 0, 0, 0, -1, -1, 0, 0, 0};
         c.prefetch.reset();
         c.t += 1;
         const int M = (int)c.views.size();
         if (n1 < 1) throw invalid("stochastic_gradient: empty batch");
+        if (!s1) throw invalid("stochastic_gradient: null batch");
         std::vector<int> v1(s1, s1 + n1), v2;
         for (int v : v1)
             if (v < 0 || v >= M) throw invalid("stochastic_gradient: view index out of range");
@@ -1742,6 +1764,8 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
         if (refresh) {
             if (nu < 1) throw invalid("hutchinson_diag: nu must be >= 1");
             if (n2 < 1) throw invalid("hutchinson_diag: empty batch");
+            if (!s2) throw invalid("hutchinson_diag: null batch");
+            if (!probe_bits) throw invalid("hutchinson_diag: null probe bits");
             v2.assign(s2, s2 + n2);
             for (int v : v2)
                 if (v < 0 || v >= M) throw invalid("hutchinson_diag: view index out of range");
@@ -2498,8 +2522,8 @@ int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t
         Ctx& c = ctx_ref(ctx);
         bind(c);
         if (nranks < 1 || rank < 0 || rank >= nranks) throw invalid("sgtr_comm_init: bad rank");
-        c.nranks = nranks;
-        c.rank = rank;
+        if (!id) throw invalid("sgtr_comm_init: null unique id");
+        if (c.comm) throw invalid("sgtr_comm_init: communicator already initialised");
         // a 1-rank communicator is created too (it runs the same allreduce
         // path; tests use it to exercise the NCCL plumbing on one GPU)
         g_nccl.load();
@@ -2507,7 +2531,13 @@ int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t
         if (!init) throw Error(SGTR_RUNTIME, "libnccl.so.2 lacks ncclCommInitRank");
         UniqueId u;
         std::memcpy(u.internal, id, 128);
-        g_nccl.check(init(&c.comm, nranks, u, rank), "ncclCommInitRank");
+        void* comm = nullptr;
+        g_nccl.check(init(&comm, nranks, u, rank), "ncclCommInitRank");
+        // the view split only changes once the communicator exists: a failed
+        // init leaves the context a single-rank one
+        c.comm = comm;
+        c.nranks = nranks;
+        c.rank = rank;
     });
 }
 
