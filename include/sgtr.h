@@ -207,6 +207,12 @@ int sgtr_step_3dgs2tr_explicit(sgtr_ctx* ctx, const sgtr_optimizer_options* opt,
                                int32_t n2, const uint32_t* probe_bits,
                                int32_t nu, sgtr_step_diagnostics* diag);
 int sgtr_get_applied_step(sgtr_ctx* ctx, double* out);
+/* Hutchinson sample s at which the last step raised "hutchinson_diag:
+ * non-finite sample" (-1 otherwise).  The reference draws each probe
+ * lazily (optimizer.cpp:67-73, :86-87), so at that point it has consumed
+ * probes 0..s; a caller that draws the probes itself for
+ * sgtr_step_3dgs2tr_explicit restores its Rng to after probe s. */
+int sgtr_step_failed_sample(sgtr_ctx* ctx, int32_t* sample);
 
 /* step_adam / step_adam_tr (optimizer.cpp:222-253): one S1 draw from the
  * state's Rng, ADAM direction (adam_direction, :153-185), then the plain

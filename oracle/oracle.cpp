@@ -240,6 +240,23 @@ int group_of(int64_t k, int64_t idx) {  // scene.cpp:41-47
     return 4;
 }
 
+// ---------------------------------------------------------------- Eigen order
+// The reference's Eigen 3.4 (x86-64, SSE2) reduction orders, as modelled by
+// oracle/refshim/Eigen/Core (which documents the evidence):
+//  * a small product coefficient over k = 0..2 with a column-major lhs is
+//    split in halves, a0 b0 + (a1 b1 + a2 b2) (W mu, W Sigma, (W Sigma) W^T,
+//    (R^T S^2) R); with a transposed lhs it is vectorised: left to right;
+//  * a trace is d0 + (d1 + d2); a 4-vector's squaredNorm / norm is
+//    (q0^2 + q2^2) + (q1^2 + q3^2); a 3-vector's is left to right;
+//  * a VectorXd squaredNorm / norm runs two SSE2 packet accumulators.
+template <typename T>
+inline T tree3(const T& a, const T& b, const T& c) {
+    return a + (b + c);
+}
+inline double sqnorm4(const double q[4]) {
+    return (q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]);
+}
+
 // ---------------------------------------------------------------- geometry
 // geometry.hpp:25-54: R = R~(q)/|q|^2; throws on |q|^2 < 1e-24
 template <typename T>
@@ -260,7 +277,8 @@ void quat_rot(const T q[4], T m[9]) {
     for (int i = 0; i < 9; ++i) m[i] = m[i] / r2;
 }
 
-// geometry.hpp:57-65: Sigma = R^T diag(s^2) R, sums over k left to right
+// geometry.hpp:57-65: Sigma = (R^T diag(s^2)) R.  The first product has one
+// non-zero term per coefficient (exact); the second sums in halves.
 template <typename T>
 void covariance(const T s[3], const T q[4], T cov[9]) {
     T r[9];
@@ -268,8 +286,8 @@ void covariance(const T s[3], const T q[4], T cov[9]) {
     const T s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
-            cov[3 * i + j] = r[i] * s2[0] * r[j] + r[3 + i] * s2[1] * r[3 + j] +
-                             r[6 + i] * s2[2] * r[6 + j];
+            cov[3 * i + j] = tree3<T>(r[i] * s2[0] * r[j], r[3 + i] * s2[1] * r[3 + j],
+                                      r[6 + i] * s2[2] * r[6 + j]);
 }
 
 struct Cam {
@@ -302,7 +320,7 @@ Proj<T> project(const T mu[3], const T s[3], const T q[4], const Cam& cam,
     const double* w = cam.w;
     T pc[3];
     for (int i = 0; i < 3; ++i)
-        pc[i] = w[3 * i] * mu[0] + w[3 * i + 1] * mu[1] + w[3 * i + 2] * mu[2] +
+        pc[i] = tree3<T>(w[3 * i] * mu[0], w[3 * i + 1] * mu[1], w[3 * i + 2] * mu[2]) +
                 cam.c.t_wc[i];
     out.depth = P(pc[2]);
     if (out.depth <= o.z_near) return out;
@@ -315,12 +333,12 @@ Proj<T> project(const T mu[3], const T s[3], const T q[4], const Cam& cam,
     T ws[9], sc[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
-            ws[3 * i + j] = w[3 * i] * sig[j] + w[3 * i + 1] * sig[3 + j] +
-                            w[3 * i + 2] * sig[6 + j];
+            ws[3 * i + j] = tree3<T>(w[3 * i] * sig[j], w[3 * i + 1] * sig[3 + j],
+                                     w[3 * i + 2] * sig[6 + j]);
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
-            sc[3 * i + j] = ws[3 * i] * w[3 * j] + ws[3 * i + 1] * w[3 * j + 1] +
-                            ws[3 * i + 2] * w[3 * j + 2];
+            sc[3 * i + j] = tree3<T>(ws[3 * i] * w[3 * j], ws[3 * i + 1] * w[3 * j + 1],
+                                     ws[3 * i + 2] * w[3 * j + 2]);
     const T j00 = cam.c.fx * inv_z;
     const T j02 = -cam.c.fx * pc[0] * inv_z * inv_z;
     const T j11 = cam.c.fy * inv_z;
@@ -934,9 +952,29 @@ void residual_vjp(const double* img, const double* gt, int W, int H,
     }
 }
 
+// VectorXd::squaredNorm(): two SSE2 packet accumulators over the aligned
+// body, lanes added, scalar tail (Redux.h, LinearVectorized/NoUnrolling)
 double sq_norm(const std::vector<double>& v) {
-    double s = 0.0;
-    for (double e : v) s += e * e;
+    const size_t n = v.size(), n4 = n / 4 * 4, n2 = n / 2 * 2;
+    if (n2 == 0) return n ? v[0] * v[0] : 0.0;
+    double a0 = v[0] * v[0], a1 = v[1] * v[1];
+    if (n2 > 2) {
+        double b0 = v[2] * v[2], b1 = v[3] * v[3];
+        for (size_t k = 4; k < n4; k += 4) {
+            a0 += v[k] * v[k];
+            a1 += v[k + 1] * v[k + 1];
+            b0 += v[k + 2] * v[k + 2];
+            b1 += v[k + 3] * v[k + 3];
+        }
+        a0 += b0;
+        a1 += b1;
+        if (n2 > n4) {
+            a0 += v[n4] * v[n4];
+            a1 += v[n4 + 1] * v[n4 + 1];
+        }
+    }
+    double s = a0 + a1;
+    for (size_t k = n2; k < n; ++k) s += v[k] * v[k];
     return s;
 }
 
@@ -1128,15 +1166,16 @@ void quat_d2R(int axis, double d[9]) {
 // trust_region.cpp:132-155
 double beta_rotation(const Prim& p, int axis) {
     const double* q = p.q;
-    const double r2 = q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3];
+    const double r2 = sqnorm4(q);  // q.squaredNorm()
     if (r2 < 1e-24) throw InvalidArg("beta_rotation: degenerate quaternion");
     const double qc = q[axis];
     const double x = q[0], y = q[1], z = q[2], w = q[3];
-    const double rt[9] = {r2 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z),
+    const double ru = x * x + y * y + z * z + w * w;  // quat_rotation_unnormalized's own
+    const double rt[9] = {ru - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z),
                           2.0 * (x * z + w * y),      2.0 * (x * y + w * z),
-                          r2 - 2.0 * (z * z + x * x), 2.0 * (y * z - w * x),
+                          ru - 2.0 * (z * z + x * x), 2.0 * (y * z - w * x),
                           2.0 * (x * z - w * y),      2.0 * (y * z + w * x),
-                          r2 - 2.0 * (x * x + y * y)};
+                          ru - 2.0 * (x * x + y * y)};
     double r[9], drt[9], d2rt[9];
     for (int i = 0; i < 9; ++i) r[i] = rt[i] / r2;
     quat_dR(q, axis, drt);
@@ -1160,7 +1199,7 @@ double beta_rotation(const Prim& p, int axis) {
             const double v = p.s[i] * de[3 * i + j] / p.s[j];
             frob += v * v;
         }
-    return 2.0 * frob + 2.0 * (d2e[0] + d2e[4] + d2e[8]);
+    return 2.0 * frob + 2.0 * tree3(d2e[0], d2e[4], d2e[8]);
 }
 
 // trust_region.cpp:183-194
@@ -1415,7 +1454,7 @@ void step_adam(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o
 // ---------------------------------------------------------------- datasets
 // scene.cpp:94-128 (Shepperd), returns unit (x, y, z, w)
 void rotation_to_quat(const double r[9], double q[4]) {
-    const double tr = r[0] + r[4] + r[8];
+    const double tr = tree3(r[0], r[4], r[8]);
     if (tr > 0.0) {
         const double s = std::sqrt(tr + 1.0) * 2.0;
         q[3] = 0.25 * s;
@@ -1441,7 +1480,7 @@ void rotation_to_quat(const double r[9], double q[4]) {
         q[1] = (r[5] + r[7]) / s;
         q[2] = 0.25 * s;
     }
-    const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const double n = std::sqrt(sqnorm4(q));
     for (int i = 0; i < 4; ++i) q[i] = q[i] / n;
 }
 
@@ -1483,7 +1522,7 @@ orc_camera look_at(const double eye[3], const double tgt[3], double fx, double f
     c.height = h;
     rotation_to_quat(r, c.q_wc);
     for (int i = 0; i < 3; ++i)
-        c.t_wc[i] = -r[3 * i] * eye[0] + -r[3 * i + 1] * eye[1] + -r[3 * i + 2] * eye[2];
+        c.t_wc[i] = tree3(-r[3 * i] * eye[0], -r[3 * i + 1] * eye[1], -r[3 * i + 2] * eye[2]);
     return c;
 }
 
@@ -1999,7 +2038,7 @@ int orc_make_synthetic(const orc_synth_cfg* cfg, const orc_render_opts* ro, int 
             for (int a = 0; a < 3; ++a) p.s[a] = rng.log_uniform(0.02 * ss, 0.2 * ss);
             double q[4];
             for (int a = 0; a < 4; ++a) q[a] = rng.normal();
-            const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            const double n = std::sqrt(sqnorm4(q));  // random_unit_quat: q.norm()
             if (n > 1e-9)
                 for (int a = 0; a < 4; ++a) p.q[a] = q[a] / n;
             else
@@ -2059,7 +2098,7 @@ int orc_make_check_scene(int32_t splats, int32_t image_size, int32_t n_views,
                 for (int a = 0; a < 3; ++a) p.s[a] = rng.log_uniform(0.06, 0.22);
                 double q[4];
                 for (int a = 0; a < 4; ++a) q[a] = rng.normal();
-                double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+                double n = std::sqrt(sqnorm4(q));  // q.normalized()
                 for (int a = 0; a < 4; ++a) p.q[a] = q[a] / n;
                 p.alpha = rng.uniform(0.3, 0.8);
                 for (int a = 0; a < 3; ++a) p.c[a] = rng.uniform(0.15, 1.0);

@@ -257,7 +257,8 @@ def camera(id=0, width=16, height=16, fx=1.0, fy=1.0, cx=0.0, cy=0.0,
 def _cams(cams):
     arr = (Camera * len(cams))()
     for i, c in enumerate(cams):
-        arr[i] = c
+        # a Camera of another binding instance (pyref) has the same layout
+        arr[i] = c if isinstance(c, Camera) else Camera.from_buffer_copy(bytes(c))
     return arr
 
 

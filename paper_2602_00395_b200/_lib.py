@@ -129,6 +129,7 @@ _SIGS = {
     "sgtr_step_3dgs2tr_explicit": (C.c_int, [VP, VP, VP, C.c_int32, VP, C.c_int32, VP,
                                              C.c_int32, VP]),
     "sgtr_get_applied_step": (C.c_int, [VP, VP]),
+    "sgtr_step_failed_sample": (C.c_int, [VP, VP]),
     "sgtr_step_adam": (C.c_int, [VP, VP, VP, VP]),
     "sgtr_step_adam_tr": (C.c_int, [VP, VP, VP, VP]),
     "sgtr_step_adam_explicit": (C.c_int, [VP, VP, VP, C.c_int32, VP, C.c_int32, VP]),

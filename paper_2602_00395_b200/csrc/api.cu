@@ -389,6 +389,7 @@ struct Ctx {
     int nranks = 1, rank = 0;
     int refresh_bands = 1;  // bands per rank of each refresh view (sgtr_set_refresh_bands)
     int tr_shards = 1;      // radius shards run back to back on one rank (sgtr_set_tr_shards)
+    int fail_sample = -1;   // Hutchinson sample of the last step's failure (sgtr_step_failed_sample)
     Buf stage;              // shard-major staging for the radius all-gather
     void* comm = nullptr;
 
@@ -781,6 +782,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     const long long m = 6LL * P * M;
     const RenderP ro = render_params(o.render);
     const int n1 = (int)s1.size(), n2 = refresh ? (int)s2.size() : 0;
+    c.fail_sample = -1;
     // fused buffer, summed by one allreduce per step:
     //   [g_acc (dim) | loss[n1] | gflag[n1] | hflag[nu] | err_kind[n1+n2] |
     //    err_index[n1+n2] | w_acc (dim, refresh steps only)]
@@ -958,6 +960,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                 hutch_fail = true;
                 fail_sample = s;
             }
+        if (hutch_fail) c.fail_sample = fail_sample;
         if (hutch_fail && draws && fail_sample < (int)draws->after_probe.size()) {
             c.prefetch.reset();
             c.rng = draws->after_probe[fail_sample];
@@ -1867,6 +1870,13 @@ int sgtr_state_get_adam(sgtr_ctx* ctx, double* m, double* v) {
     });
 }
 
+int sgtr_step_failed_sample(sgtr_ctx* ctx, int32_t* sample) {
+    return guarded([&] {
+        if (!ctx || !sample) throw invalid("sgtr_step_failed_sample: null argument");
+        *sample = ctx_ref(ctx).fail_sample;
+    });
+}
+
 int sgtr_get_applied_step(sgtr_ctx* ctx, double* out) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
@@ -2298,7 +2308,8 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
             for (int a = 0; a < 3; ++a) mu[a] = rng.uniform(-0.5, 0.5);
             for (int a = 0; a < 3; ++a) s[a] = rng.log_uniform(0.02 * ss, 0.2 * ss);
             for (int a = 0; a < 4; ++a) q[a] = rng.normal();
-            const double n = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            // random_unit_quat's q.norm(): Eigen's SSE2 order for a 4-vector
+            const double n = std::sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]));
             if (n > 1e-9) {
                 for (int a = 0; a < 4; ++a) q[a] = q[a] / n;
             } else {
@@ -2369,7 +2380,7 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
             cam.cy = cfg->height / 2.0;
             // rotation_to_quat (scene.cpp:94-128)
             double* q = cam.q_wc;
-            const double tr = r[0] + r[4] + r[8];
+            const double tr = r[0] + (r[4] + r[8]);  // trace(): halves
             if (tr > 0.0) {
                 const double s = std::sqrt(tr + 1.0) * 2.0;
                 q[3] = 0.25 * s;
@@ -2395,10 +2406,11 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
                 q[1] = (r[5] + r[7]) / s;
                 q[2] = 0.25 * s;
             }
-            const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+            const double qn = std::sqrt((q[0] * q[0] + q[2] * q[2]) + (q[1] * q[1] + q[3] * q[3]));
             for (int i = 0; i < 4; ++i) q[i] = q[i] / qn;
             for (int i = 0; i < 3; ++i)
-                cam.t_wc[i] = -r[3 * i] * eye[0] + -r[3 * i + 1] * eye[1] + -r[3 * i + 2] * eye[2];
+                cam.t_wc[i] =  // -r * eye: a column-major product row, summed in halves
+                    -r[3 * i] * eye[0] + (-r[3 * i + 1] * eye[1] + -r[3 * i + 2] * eye[2]);
             cams[v] = cam;
         }
     });

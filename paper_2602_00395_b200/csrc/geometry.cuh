@@ -72,7 +72,17 @@ SGTR_HD bool quat_rot(const T* q, T* m) {
     return true;
 }
 
-// Sigma = R^T diag(s^2) R, each entry summed over k left to right
+// The reference's Eigen 3.4 build sums a small product coefficient with a
+// column-major lhs in halves, a0 b0 + (a1 b1 + a2 b2) (oracle/refshim/Eigen/Core
+// documents the model and its evidence); this TU is built without FMA
+// contraction, so the projection is bit-identical to the reference's.
+template <typename T>
+SGTR_HD T tree3(const T& a, const T& b, const T& c) {
+    return a + (b + c);
+}
+
+// Sigma = (R^T diag(s^2)) R: one non-zero term per coefficient in the first
+// product, the second summed in halves
 template <typename T>
 SGTR_HD bool covariance(const T* s, const T* q, T* cov) {
     T r[9];
@@ -82,8 +92,8 @@ SGTR_HD bool covariance(const T* s, const T* q, T* cov) {
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            cov[3 * i + j] = r[i] * s2[0] * r[j] + r[3 + i] * s2[1] * r[3 + j] +
-                             r[6 + i] * s2[2] * r[6 + j];
+            cov[3 * i + j] = tree3<T>(r[i] * s2[0] * r[j], r[3 + i] * s2[1] * r[3 + j],
+                                      r[6 + i] * s2[2] * r[6 + j]);
     return true;
 }
 
@@ -105,7 +115,7 @@ SGTR_HD Proj<T> project(const T* mu, const T* s, const T* q, const double* w,
     T pc[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-        pc[i] = w[3 * i] * mu[0] + w[3 * i + 1] * mu[1] + w[3 * i + 2] * mu[2] + t[i];
+        pc[i] = tree3<T>(w[3 * i] * mu[0], w[3 * i + 1] * mu[1], w[3 * i + 2] * mu[2]) + t[i];
     out.depth = primal(pc[2]);
     if (out.depth <= z_near) return out;
     out.culled = false;
@@ -122,14 +132,14 @@ SGTR_HD Proj<T> project(const T* mu, const T* s, const T* q, const double* w,
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            ws[3 * i + j] = w[3 * i] * sig[j] + w[3 * i + 1] * sig[3 + j] +
-                            w[3 * i + 2] * sig[6 + j];
+            ws[3 * i + j] = tree3<T>(w[3 * i] * sig[j], w[3 * i + 1] * sig[3 + j],
+                                     w[3 * i + 2] * sig[6 + j]);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            sc[3 * i + j] = ws[3 * i] * w[3 * j] + ws[3 * i + 1] * w[3 * j + 1] +
-                            ws[3 * i + 2] * w[3 * j + 2];
+            sc[3 * i + j] = tree3<T>(ws[3 * i] * w[3 * j], ws[3 * i + 1] * w[3 * j + 1],
+                                     ws[3 * i + 2] * w[3 * j + 2]);
     const T j00 = fx * inv_z;
     const T j02 = -fx * pc[0] * inv_z * inv_z;
     const T j11 = fy * inv_z;
@@ -167,7 +177,7 @@ SGTR_HD void chain_reverse(const double* mu, const double* s, const double* q,
     double pc[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-        pc[i] = w[3 * i] * mu[0] + w[3 * i + 1] * mu[1] + w[3 * i + 2] * mu[2] + t[i];
+        pc[i] = tree3(w[3 * i] * mu[0], w[3 * i + 1] * mu[1], w[3 * i + 2] * mu[2]) + t[i];
     const double iz = 1.0 / pc[2];
     const double x = q[0], y = q[1], z = q[2], qw = q[3];
     const double r2 = x * x + y * y + z * z + qw * qw;
@@ -186,19 +196,19 @@ SGTR_HD void chain_reverse(const double* mu, const double* s, const double* q,
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            sig[3 * i + j] = R[i] * s2[0] * R[j] + R[3 + i] * s2[1] * R[3 + j] +
-                             R[6 + i] * s2[2] * R[6 + j];
+            sig[3 * i + j] = tree3(R[i] * s2[0] * R[j], R[3 + i] * s2[1] * R[3 + j],
+                                   R[6 + i] * s2[2] * R[6 + j]);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            ws[3 * i + j] = w[3 * i] * sig[j] + w[3 * i + 1] * sig[3 + j] + w[3 * i + 2] * sig[6 + j];
+            ws[3 * i + j] = tree3(w[3 * i] * sig[j], w[3 * i + 1] * sig[3 + j], w[3 * i + 2] * sig[6 + j]);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            sc[3 * i + j] = ws[3 * i] * w[3 * j] + ws[3 * i + 1] * w[3 * j + 1] +
-                            ws[3 * i + 2] * w[3 * j + 2];
+            sc[3 * i + j] = tree3(ws[3 * i] * w[3 * j], ws[3 * i + 1] * w[3 * j + 1],
+                                  ws[3 * i + 2] * w[3 * j + 2]);
     const double j00 = fx * iz, j02 = -fx * pc[0] * iz * iz;
     const double j11 = fy * iz, j12 = -fy * pc[1] * iz * iz;
     const double js00 = j00 * sc[0] + j02 * sc[6], js01 = j00 * sc[1] + j02 * sc[7];

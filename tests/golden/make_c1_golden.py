@@ -1,9 +1,12 @@
-"""Generates tests/golden/c1_oracle.npz: BASELINE config 1 (10K splats, 4 views
+"""Generates tests/golden/c1_reference.npz (the compiled reference,
+oracle/_ref via oracle/pyref.py -- the default) or, with ``--oracle``, the
+same run of the restatement into /tmp/c1_oracle.npz (bit-identical to the
+reference's): BASELINE config 1 (10K splats, 4 views
 at 128x128, id 0 held out as in split_views, dataset.cpp:79-85) trained for
 100 3DGS²-TR iterations (seed 1, nu 1, |S1| = |S2| = 1, l = 10, eps 1e-6 ->
-1e-8 over 100 steps) by the CPU oracle.  Stores the per-step diagnostics, the
+1e-8 over 100 steps) on the CPU.  Stores the per-step diagnostics, the
 held-out PSNR after the last step (evaluate_scene, harness.cpp:43-58) and the
-final scene.  Run:  python tests/golden/make_c1_golden.py
+final scene.  Run:  python tests/golden/make_c1_golden.py [--oracle]
 """
 import os
 import sys
@@ -14,7 +17,14 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle import pyoracle as orc  # noqa: E402
+if "--oracle" in sys.argv:
+    from oracle import pyoracle as orc  # noqa: E402
+    OUT = "/tmp/c1_oracle.npz"
+else:
+    from oracle import pyref  # noqa: E402
+    pyref.build()
+    orc = pyref.ref
+    OUT = "c1_reference.npz"
 
 ITERS = 100
 
@@ -37,7 +47,7 @@ def main():
         diag.append([d[k] for k in ("batch_loss", "gnorm", "step_pre", "step_post",
                                     "clip_frac", "eps", "max_step_over_radius")])
     psnr = [orc.psnr(orc.quantize8(orc.rasterize(x, ds.cams[i])[0]), ds.gts[i]) for i in held]
-    np.savez_compressed(os.path.join(HERE, "c1_oracle.npz"), diag=np.array(diag),
+    np.savez_compressed(os.path.join(HERE, OUT), diag=np.array(diag),
                         psnr=np.array(psnr), final_x=x, init_x=ds.init_x)
     print(f"done in {time.time() - t0:.1f}s: held-out PSNR {psnr}")
 
