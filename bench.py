@@ -14,8 +14,10 @@ interval so the 1-in-10 refresh is included in proportion) are timed.
 N > 1: launched by torch.distributed.run, one process per GPU; each step's
 view batch is split round-robin over the ranks and g | z.w | loss are summed
 by one ncclAllReduce per step inside libsgtr (strong scaling: the batch is
-fixed).  ``--impl reference`` times the CPU reference path (the oracle port,
-all host threads) on a bounded band sample of the same workload.
+fixed).  ``--impl reference`` times the compiled reference (oracle/_ref: the
+unmodified reference sources, its Release flags, all host threads) on
+bounded central crops of the same workload, extrapolated to a full
+iteration, plus a fully measured C1 anchor; it never loads libsgtr.so.
 """
 from __future__ import annotations
 
@@ -150,50 +152,69 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ CPU reference (oracle port)
-def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=None, sh=0):
-    """Time the CPU reference path (the oracle port) on small central crops of
-    a view and extrapolate to one full iteration: |S1| gradient views + 1/l of
-    a refresh view + shd_radii at full K.  A call's cost is modelled as
-    a + b * pixels (projection + depth sort of all K splats, then the
-    reference's Theta(P K) per-pixel scans, render.cpp:122-151); a and b come
-    from 320 x T and 320 x 3T crops, T = host threads (>= 6 rows for SSIM).  Returns
-    (it/s, model)."""
-    from oracle import pyoracle as orc
-    orc.set_sh_degree(sh)
-    k = x_init.size // npp_of(sh)
+# ------------------------------------------------------------------ CPU reference (compiled)
+# The CPU arm times the reference ITSELF: oracle/_ref/libsplat_ref.so is the
+# unmodified /root/reference/proj sources compiled with the reference's own
+# Release flags (-O3 -DNDEBUG) against oracle/refshim (oracle/ref.mk), bound
+# by oracle/pyref.py.  Scenes and cameras come from the oracle's host-only
+# generator (the reference generator plus the declared W != H / size-scale
+# extensions; equal to the reference's make_synthetic where both apply), and
+# each crop's target is rendered by the reference itself -- libsgtr is never
+# loaded on this arm.
+def ref_lib():
+    from oracle import pyref
+    if not pyref.available():
+        pyref.build()
+    return pyref.ref
+
+
+def crop_camera(ref, cam_full, rows, cols=320):
+    """A central rows x cols window of cam_full (same rays, shifted centre)."""
+    W, H = cam_full.width, cam_full.height
+    y0, x0 = (H - rows) // 2, (W - cols) // 2
+    c = ref.Camera.from_buffer_copy(bytes(cam_full))
+    c.height, c.width = rows, cols
+    c.cy, c.cx = cam_full.cy - y0, cam_full.cx - x0
+    return c
+
+
+def crop_rows():
+    # the reference splits rows round-robin over all hardware threads
+    # (parallel.hpp:21-44); its VJP buffer is H x 9 x K doubles
+    # (render.cpp:272-274), 72 MB per row at K = 1M, so the crops are capped
+    # at 48 and 144 rows
+    return max(6, min(cpu_cores(), 48))
+
+
+def cpu_reference_sample(ref, x_init, x_gt, cam_full, batch, refresh_every=10, model=None):
+    """Time the reference on central crops of a view and extrapolate to one
+    full iteration: |S1| gradient views + 1/l of a refresh view + shd_radii
+    at full K.  A call's cost is modelled as a + b * pixels (projection,
+    depth sort and fragment build of all K splats, then the Theta(P K)
+    per-pixel scans, render.cpp:122-151); a and b come from 320 x T and
+    320 x 3T crops (T = min(threads, 48)).  Returns (it/s, model)."""
+    k = x_init.size // 14
     W, H = cam_full.width, cam_full.height
 
-    def crop(rows, cols=320):
-        y0, x0 = (H - rows) // 2, (W - cols) // 2
-        c = orc.Camera()
-        for f, _ in orc.Camera._fields_:
-            setattr(c, f, getattr(cam_full, f))
-        c.height, c.width = rows, cols
-        c.cy, c.cx = cam_full.cy - y0, cam_full.cx - x0
-        return c
-
     def gt_of(c):
-        img, _ = orc.rasterize(x_gt, c)
-        return orc.quantize8(img)
+        img, _ = ref.rasterize(x_gt, c)
+        return ref.quantize8(img)
 
     def t_grad(c):
         g = gt_of(c)
         t0 = time.perf_counter()
-        orc.stochastic_gradient(x_init, [c], [g], [0])
+        ref.stochastic_gradient(x_init, [c], [g], [0])
         return time.perf_counter() - t0
 
     def t_hutch(c):
         g = gt_of(c)
-        z = orc.Rng(7).rademacher(x_init.size)
+        z = ref.Rng(7).rademacher(x_init.size)
         t0 = time.perf_counter()
-        orc.hutchinson_diag(x_init, [c], [g], [0], z)
+        ref.hutchinson_diag(x_init, [c], [g], [0], z)
         return time.perf_counter() - t0
 
-    # row counts are multiples of the worker count: the reference splits rows
-    # round-robin over hardware threads (parallel.hpp:21-44)
-    rows = max(6, cpu_cores())
-    c1, c2 = crop(rows), crop(3 * rows)
+    rows = crop_rows()
+    c1, c2 = crop_camera(ref, cam_full, rows), crop_camera(ref, cam_full, 3 * rows)
     p1, p2 = c1.width * c1.height, c2.width * c2.height
     if model is None:
         g1, g2 = t_grad(c1), t_grad(c2)
@@ -203,9 +224,9 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=
         fixed = a_g / g1 if g1 > 0 else 0.0
         a_h, b_h = h1 * fixed, h1 * (1 - fixed) / p1
         sub = min(k, 100_000)
-        xs = splat_subset(x_init, k, sub, sh)
+        xs = splat_subset(x_init, k, sub, 0)
         t0 = time.perf_counter()
-        orc.shd_radii(xs, 1e-6)
+        ref.shd_radii(xs, 1e-6)
         t_radii = (time.perf_counter() - t0) * k / sub
         model = dict(a_g=a_g, b_g=b_g, a_h=a_h, b_h=b_h, t_radii=t_radii)
     else:
@@ -218,33 +239,114 @@ def cpu_reference_sample(x_init, x_gt, cam_full, batch, refresh_every=10, model=
     return 1.0 / t_iter, model
 
 
-def c1_psnr_delta(sp, orc, iters=100):
-    """BASELINE's "PSNR delta": the C1 run (10K splats, 4 views of 128x128,
-    seed 1, view 0 held out, |S1| = 1, refresh every 10th step) for `iters`
-    3DGS2-TR iterations through the library and through the oracle port (its
-    parity build) from the same seed; final held-out PSNR of each
-    (evaluate_scene: quantize8 + psnr).  tests/test_c1_training.py holds the
-    same run to 0.05 dB against a committed oracle trajectory."""
-    orc.set_sh_degree(0)
-    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=10000, init_splats=10000, views=4,
+C1_ANCHOR = "C1: 10K Gaussians, 4 views 128x128 (view 0 held out), |S1|=1, refresh l=10"
+
+
+def c1_data(mod):
+    ds = mod.make_synthetic(mod.SynthConfig(gt_splats=10000, init_splats=10000, views=4,
                                             image_size=128, seed=1))
-    train = [1, 2, 3]
-    o_cams, o_gts = [ds.cams[i] for i in train], [ds.gts[i] for i in train]
-    views = [sp.Camera.from_c(c, g) for c, g in zip(o_cams, o_gts)]
-    st = sp.OptimizerState(ds.init_x.size, 1)
-    scene = sp.Scene(ds.init_x)
+    train = [1, 2, 3]  # split_views (dataset.cpp:79-85)
+    return ds, [ds.cams[i] for i in train], [ds.gts[i] for i in train]
+
+
+def ref_c1_rate(ref, steps=20):
+    """Fully measured anchor: `steps` reference iterations (2 refreshes in
+    20) at BASELINE config 1, wall clock, all host threads."""
+    ds, cams, gts = c1_data(ref)
+    x = ds.init_x.copy()
+    st = ref.State(x.size, 1)
+    opts = ref.TrOptions(total_steps=100, batch_size=1)
+    ref.step_3dgs2tr(st, x, cams, gts, opts)  # warm-up (t = 1, a refresh step)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ref.step_3dgs2tr(st, x, cams, gts, opts)
+    return steps / (time.perf_counter() - t0)
+
+
+def c1_psnr_delta(sp, iters=100):
+    """BASELINE's "PSNR delta": the C1 run (10K splats, 4 views of 128x128,
+    seed 1, view 0 held out, |S1| = 1, refresh every 10th step) for 100
+    3DGS2-TR iterations through the library, against the same run of the
+    compiled reference committed as tests/golden/c1_reference.npz (made by
+    tests/golden/make_c1_golden.py); held-out PSNR of each (evaluate_scene:
+    quantize8 + psnr)."""
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "c1_reference.npz"))
+    gt, init, cams = sp.make_synthetic(gt_splats=10000, init_splats=10000, views=4, width=128,
+                                       height=128, seed=1)
+    assert np.array_equal(init.x, gold["init_x"])
+    ctx = sp.Context()
+    ctx.set_scene(gt.x)
+    ctx.set_cameras(cams)
+    ctx.render_targets(quantize=True)
+    gts = [ctx.get_target(i, 128, 128) for i in range(4)]
+    ctx.close()
+    views = [sp.Camera.from_c(cams[i]._c(), gts[i]) for i in (1, 2, 3)]
+    st = sp.OptimizerState(init.x.size, 1)
+    scene = sp.Scene(init.x)
     opts = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, iters),
                                batch_size=1, record_applied_step=False)
-    ost, xo = orc.State(ds.init_x.size, 1), ds.init_x.copy()
-    oopts = orc.TrOptions(total_steps=iters, batch_size=1)
     for _ in range(iters):
         sp.step_3dgs2tr(st, scene, views, opts)
-        orc.step_3dgs2tr(ost, xo, o_cams, o_gts, oopts)
-    p_gpu = sp.evaluate_scene(scene, [sp.Camera.from_c(ds.cams[0], ds.gts[0])]).mean_psnr
-    p_cpu = orc.psnr(orc.quantize8(orc.rasterize(xo, ds.cams[0])[0]), ds.gts[0])
+    p_gpu = sp.evaluate_scene(scene, [sp.Camera.from_c(cams[0]._c(), gts[0])]).mean_psnr
+    p_ref = float(gold["psnr"][0])
     return {"config": f"C1: 10K splats, 4 views 128x128, seed 1, view 0 held out, {iters} "
                       "iterations, |S1|=1, refresh every 10th",
-            "gpu_db": float(p_gpu), "cpu_db": float(p_cpu), "delta_db": float(p_gpu - p_cpu)}
+            "gpu_db": float(p_gpu), "cpu_db": p_ref, "delta_db": float(p_gpu - p_ref),
+            "cpu_source": "compiled reference (tests/golden/c1_reference.npz)"}
+
+
+def gpu_c1_rate(sp, steps=20):
+    """The C1 anchor on the device: `steps` full iterations (2 refreshes in 20)
+    through a resident context, CUDA events around them."""
+    import torch
+    gt, init, cams = sp.make_synthetic(gt_splats=10000, init_splats=10000, views=4, width=128,
+                                       height=128, seed=1)
+    ctx = sp.Context()
+    ctx.set_scene(gt.x)
+    ctx.set_cameras(cams)
+    ctx.render_targets(quantize=True)
+    gts = [ctx.get_target(i, 128, 128) for i in range(4)]
+    ctx.set_scene(init.x)
+    ctx.set_views([sp.Camera.from_c(cams[i]._c(), gts[i]) for i in (1, 2, 3)])
+    ctx.state_reset(1)
+    opt = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 100), batch_size=1,
+                              record_applied_step=False)
+    ctx.step(opt)
+    ctx.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.step(opt)
+    e1.record(stream)
+    e1.synchronize()
+    rate = 1000.0 * steps / e0.elapsed_time(e1)
+    ctx.close()
+    return rate
+
+
+def repo_libs_loaded():
+    """Shared objects of this repo mapped into the process (the reference
+    arm maps oracle/ libraries only, never libsgtr.so)."""
+    libs = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            path = ln.split()[-1] if ln.strip() else ""
+            if path.startswith(ROOT) and ".so" in path:
+                libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def config_of(cfg):
+    """The `config` object both arms print (identical by construction)."""
+    k, v, w, h, b, sh = CONFIGS[cfg]
+    return {"workload": workload_desc(cfg), "global_batch": b, "resolution": f"{w}x{h}",
+            "splats": k, "views": v, "sh_degree": sh,
+            "l2": (f"per-step working set exceeds L2: scene {8 * npp_of(sh) * k / 1e6:.0f} MB"
+                   f" + {b} views x (records {128 * k / 1e6:.0f} MB, FP64 images"
+                   f" {8 * 3 * w * h * 8 / 1e6:.0f} MB, partials) vs 126 MB L2")}
 
 
 def cpu_cores():
@@ -268,53 +370,59 @@ def make_dataset(sp, ctx, cfg, seed):
 
 
 def run_reference(args):
+    """--impl reference: the compiled reference on the host cores, rank 0."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2602_00395_b200 import splat as sp  # host-side generator only (no GPU)
     from oracle import pyoracle as orc
-    orc.build()
-    timing_lib = orc.use_timing_build()
+    ref = ref_lib()
     k, v, w, h, b, sh = CONFIGS[args.config]
-    gt, init, cams = sp.make_synthetic(gt_splats=k, init_splats=k, views=v, width=w, height=h,
-                                       seed=args.seed,
-                                       size_scale=size_scale(k) if k > 64 else 1.0,
-                                       sh_degree=sh)
-    cam = orc.Camera()
-    src = cams[1]._c()
-    for f, _ in orc.Camera._fields_:
-        setattr(cam, f, getattr(src, f))
-    model = None
-    # warm-up: builds the cost model (320 x T and 320 x 3T gradient crops, a
-    # 320 x T refresh crop, shd_radii on a 100K subset; T = host threads)
-    _, model = cpu_reference_sample(init.x, gt.x, cam, b, sh=sh)
+    if sh:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference has no SH colour (degree 0 only)"}))
+        return 0
+    ds = orc.make_synthetic(orc.SynthConfig(gt_splats=k, init_splats=k, views=v, width=w,
+                                            height=h, image_size=h, seed=args.seed,
+                                            size_scale=size_scale(k) if k > 64 else 1.0),
+                            with_gt=False)
+    cam = ref.Camera.from_buffer_copy(bytes(ds.cams[1]))
+    t_start = time.perf_counter()
+    anchor = ref_c1_rate(ref)
+    # warm-up: the cost model (320 x T and 320 x 3T gradient crops, a
+    # 320 x T refresh crop, shd_radii on a 100K subset)
+    for _ in range(max(args.warmup, 1)):
+        _, model = cpu_reference_sample(ref, ds.init_x, ds.gt_x, cam, b)
     rates = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r, model = cpu_reference_sample(init.x, gt.x, cam, b, model=model, sh=sh)
+        r, model = cpu_reference_sample(ref, ds.init_x, ds.gt_x, cam, b, model=model)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
     cores = cpu_cores()
-    sample = (f"CPU reference path (oracle port of render/ssim/residuals/optimizer/"
-              f"trust_region, FP64, {cores} threads for the row-parallel raster passes as in "
-              f"parallel.hpp): each step times one central 320xT crop (T = threads) of a gradient view with "
-              f"all {k} splats; cost model a+b*pixels from 320xT/320x3T crops, the refresh view "
-              f"and shd_radii (100K subset) measured once in warm-up; extrapolated to "
-              f"{w}x{h} x {b} views + 1/10 refresh view + shd_radii at full K; "
-              f"oracle build {os.path.basename(timing_lib)} (-O3 -march=native when it built)")
+    rows = crop_rows()
+    sample = (f"compiled reference (oracle/_ref: unmodified proj/src, -O3 -DNDEBUG), "
+              f"{cores} host threads; each step times one central 320x{rows} crop of a "
+              f"gradient view with all {k} splats; cost model a+b*pixels from 320x{rows}/"
+              f"320x{3 * rows} crops, a 320x{rows} refresh crop and shd_radii (100K subset) "
+              f"timed in warm-up; EXTRAPOLATED to {w}x{h} x {b} views + 1/10 refresh view + "
+              f"shd_radii at full K (a full C3 iteration takes hours and needs a 78 GB VJP "
+              f"buffer); anchor_c1 is fully measured")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(args.config), "global_batch": b,
-                   "resolution": f"{w}x{h}", "splats": k},
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "port",
+        "config": config_of(args.config),
+        "extrapolated": True,
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "sample_wall_s": wall,
+        "anchor_c1": {"value": anchor, "unit": "it/s", "workload": C1_ANCHOR,
+                      "measured": "20 full reference iterations, wall clock"},
+        "sample_wall_s": wall, "total_wall_s": time.perf_counter() - t_start,
+        "native_libs": repo_libs_loaded(),
         "cost_model_s": {kk: float(vv) for kk, vv in model.items()},
     }
     print(json.dumps(line), flush=True)
@@ -504,26 +612,30 @@ def main():
     if roofline_tr["achieved"]:
         roofline_tr["frac"] = roofline_tr["achieved"] / hbm_peak
 
-    # ---- CPU baseline (oracle port, rank 0, N = 1)
+    # ---- C1 anchor on the device: the same fully measured 20 iterations the
+    # reference arm times (BASELINE config 1), outside the timed region
+    anchor = None
+    if rank == 0 and world == 1:
+        anchor = {"value": gpu_c1_rate(sp), "unit": "it/s", "workload": C1_ANCHOR,
+                  "measured": "20 full iterations, CUDA events on the library stream"}
+
+    # ---- CPU baseline (the compiled reference, rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import pyoracle as orc
-        orc.build()
-        psnr_delta = c1_psnr_delta(sp, orc)  # parity build, before the timing build loads
-        timing_lib = orc.use_timing_build()
-        cam = orc.Camera()
-        src = cams[1]._c()
-        for f, _ in orc.Camera._fields_:
-            setattr(cam, f, getattr(src, f))
-        rate, model = cpu_reference_sample(init.x, gt.x, cam, b, sh=sh)
+        psnr_delta = c1_psnr_delta(sp)
+        ref = ref_lib()
+        x_gt, x_init = gt.x, init.x
+        cam = ref.Camera.from_buffer_copy(bytes(cams[1]._c()))
+        rate, model = (cpu_reference_sample(ref, x_init, x_gt, cam, b) if sh == 0 else
+                       (None, {}))
         cores = cpu_cores()
-        cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "port",
-               "sample": (f"oracle port of the reference path, {cores} threads; central 320xT "
-                          f"and 320x3T crops (T = threads) of one gradient view + a 320xT refresh crop, all "
-                          f"{k} splats, shd_radii on a 100K subset; cost a+b*pixels "
-                          f"extrapolated to {b} views x {w}x{h} + 1/10 refresh view + "
-                          f"shd_radii at full K; oracle build {os.path.basename(timing_lib)} "
-                          f"(-O3 -march=native when it built)"),
+        rows = crop_rows()
+        cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "reference",
+               "sample": (f"compiled reference (oracle/_ref: unmodified proj/src, -O3 -DNDEBUG), "
+                          f"{cores} threads; central 320x{rows} and 320x{3 * rows} crops of one "
+                          f"gradient view + a 320x{rows} refresh crop, all {k} splats, "
+                          f"shd_radii on a 100K subset; cost a+b*pixels EXTRAPOLATED to {b} "
+                          f"views x {w}x{h} + 1/10 refresh view + shd_radii at full K"),
                "model_s": {kk: float(vv) for kk, vv in model.items()},
                "psnr_delta": psnr_delta}
 
@@ -533,13 +645,10 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(args.config), "global_batch": b,
-                       "resolution": f"{w}x{h}", "splats": k, "views": v,
-                       "parallelism": f"view-parallel dp{world} + 1 ncclAllReduce/step",
-                       "l2": (f"per-step working set exceeds L2: scene {8 * npp_of(sh) * k / 1e6:.0f} MB"
-                              f" + {b} views x (records {128 * k / 1e6:.0f} MB, FP64 images"
-                              f" {8 * 3 * w * h * 8 / 1e6:.0f} MB, partials) vs 126 MB L2"),
-                       "mean_visible": nvis, "mean_tile_duplicates": ndup},
+            "config": config_of(args.config),
+            "parallelism": f"view-parallel dp{world} + 1 ncclAllReduce/step",
+            "workload_stats": {"mean_visible": nvis, "mean_tile_duplicates": ndup},
+            "anchor_c1": anchor,
             "roofline": roofline,
             "roofline_tr_update": roofline_tr,
             "cpu_baseline": cpu,

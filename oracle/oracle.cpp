@@ -469,6 +469,7 @@ inline bool outside(const Frag<Dual>& f, double px, double py) {
 
 struct BlendCount {
     int64_t evaluated = 0, contributing = 0;
+    std::vector<int32_t>* contrib = nullptr;  // splat ids of the contributing pairs
 };
 
 // render.cpp:122-151: front-to-back blend of one pixel
@@ -487,7 +488,10 @@ void blend(const std::vector<Frag<T>>& fr, double px, double py,
         if (cnt) ++cnt->evaluated;
         if (P(abar) >= o.alpha_clamp) abar = T(o.alpha_clamp);
         if (P(abar) < o.alpha_skip) continue;
-        if (cnt) ++cnt->contributing;
+        if (cnt) {
+            ++cnt->contributing;
+            if (cnt->contrib) cnt->contrib->push_back(static_cast<int32_t>(f.splat));
+        }
         const T w = abar * tr;
         acc[0] += f.col[0] * w;
         acc[1] += f.col[1] * w;
@@ -1581,6 +1585,44 @@ int orc_rasterize_vjp(const double* x, int64_t k, const orc_camera* cam,
         if (adj_w != cam->width || adj_h != cam->height)
             throw InvalidArg("rasterize_vjp: adjoint shape mismatch");
         rasterize_vjp({x, k}, make_cam(*cam), *ro, workers, adjoint, grad);
+    });
+}
+
+int orc_blend_pairs(const double* x, int64_t k, const orc_camera* cam,
+                    const orc_render_opts* ro, int workers, int32_t x0, int32_t y0,
+                    int32_t w, int32_t h, int64_t* offsets, int32_t* ids, int64_t cap) {
+    return guarded([&] {
+        const SceneView sc{x, k};
+        check_finite(sc);
+        const Cam c = make_cam(*cam);
+        const auto fr = build_frags(sc, c, *ro);
+        if (x0 < 0 || y0 < 0 || x0 + w > c.c.width || y0 + h > c.c.height || w < 1 || h < 1)
+            throw InvalidArg("blend_pairs: window outside the image");
+        std::vector<std::vector<int32_t>> rows(h);
+        std::vector<std::vector<int64_t>> cnts(h);
+        parallel_rows(h, workers, [&](int r) {
+            BlendCount bc;
+            bc.contrib = &rows[r];
+            cnts[r].resize(w);
+            for (int xx = 0; xx < w; ++xx) {
+                double col[3], t;
+                const size_t before = rows[r].size();
+                blend<double>(fr, x0 + xx + 0.5, y0 + r + 0.5, *ro, col, t, &bc);
+                cnts[r][xx] = static_cast<int64_t>(rows[r].size() - before);
+            }
+        });
+        int64_t n = 0;
+        offsets[0] = 0;
+        for (int r = 0; r < h; ++r)
+            for (int xx = 0; xx < w; ++xx) {
+                n += cnts[r][xx];
+                offsets[static_cast<int64_t>(r) * w + xx + 1] = n;
+            }
+        if (ids && n <= cap) {
+            int64_t o = 0;
+            for (int r = 0; r < h; ++r)
+                for (int32_t id : rows[r]) ids[o++] = id;
+        }
     });
 }
 

@@ -7,14 +7,19 @@
  * time.  The product (paper_2602_00395_b200/libsgtr.so) never links, loads or
  * calls it.
  *
- * Pinning: the reference itself cannot be built in this image (it needs
- * Eigen3 + libpng via pkg-config and a vendored doctest, none present, no
- * network: proj/CMakeLists.txt:10,14-15), so this restatement is pinned by
- * the known-answer tests the reference's own suites embed
- * (tests/test_oracle_kat.py lists each one with its reference file:line) and
- * by the C++-standard-mandated mt19937_64 stream the reference Rng wraps.
- * Bitwise parity with a reference binary is unpinned (Eigen's internal
- * summation order is not knowable here); every sum below is left-to-right.
+ * Pinning: the reference itself IS built here as a second checker
+ * (oracle/ref.mk: the unmodified /root/reference sources against the
+ * Eigen-3.4-order / libpng / doctest stand-ins in oracle/refshim, into
+ * oracle/_ref), and tests/test_reference.py shows this restatement equals it
+ * bit for bit on every entry point both have (dataset, cameras, projection,
+ * render / JVP / VJP, SSIM and residual chain, gradient, Hutchinson, radii,
+ * full 3DGS2-TR / ADAM / ADAM-TR steps, Rng, error messages).  It is further
+ * pinned by the reference's own KATs (tests/test_oracle_kat.py) and the
+ * C++-standard mt19937_64 stream.  Sums follow Eigen 3.4's SSE2 order where
+ * the reference's Eigen calls sum (see "Eigen order" in oracle.cpp), left to
+ * right everywhere else.  The restatement additionally holds what the
+ * reference has no counterpart for: the tile binning the GPU build adds, the
+ * blend counters, the SH extension and teacher-forced steps.
  *
  * Layouts follow the reference exactly:
  *   x      : group-major double[14K] [mu 3K | s 3K | q 4K | alpha K | c 3K]
@@ -94,6 +99,13 @@ int orc_rasterize_vjp(const double* x, int64_t k, const orc_camera* cam,
 int orc_blend_stats(const double* x, int64_t k, const orc_camera* cam,
                     const orc_render_opts* ro, int workers, int64_t* evaluated,
                     int64_t* contributing);
+/* the contributing (pixel, splat) pairs of the blend (alpha_bar >= skip,
+ * before termination) for the w x h window at (x0, y0): offsets[w*h+1]
+ * (row-major pixels of the window) and the splat ids in blend order;
+ * ids are written only when ids != NULL and offsets[w*h] <= cap */
+int orc_blend_pairs(const double* x, int64_t k, const orc_camera* cam,
+                    const orc_render_opts* ro, int workers, int32_t x0, int32_t y0,
+                    int32_t w, int32_t h, int64_t* offsets, int32_t* ids, int64_t cap);
 /* restated tile binning (the GPU build's new stage; no reference
  * counterpart): depth order of visible splats and per-tile lists.
  * order[n_visible]; tile_start/tile_end[n_tiles] (empty tiles [0, 0));

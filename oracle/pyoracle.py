@@ -308,6 +308,24 @@ def blend_stats(x, cam, ro=None):
     return e.value, c.value
 
 
+def blend_pairs(x, cam, x0, y0, w, h, ro=None):
+    """Contributing (pixel, splat) pairs of the blend in a window:
+    (offsets[w*h+1], ids) with pixel p = row-major index in the window."""
+    ro = ro or RenderOptions()
+    x = _f64(x)
+    off = np.empty(w * h + 1, np.int64)
+    cap = 64 * w * h
+    ids = np.empty(cap, np.int32)
+    _check(lib().orc_blend_pairs(_p(x), C.c_int64(_k(x)), C.byref(cam), C.byref(ro.c()),
+                                 ro.workers, x0, y0, w, h, _p(off), _p(ids), C.c_int64(cap)))
+    if off[-1] > cap:
+        ids = np.empty(int(off[-1]), np.int32)
+        _check(lib().orc_blend_pairs(_p(x), C.c_int64(_k(x)), C.byref(cam), C.byref(ro.c()),
+                                     ro.workers, x0, y0, w, h, _p(off), _p(ids),
+                                     C.c_int64(ids.size)))
+    return off, ids[:int(off[-1])]
+
+
 def project(x, cam, ro=None):
     ro = ro or RenderOptions()
     x = _f64(x)

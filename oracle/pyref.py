@@ -31,15 +31,12 @@ ACCEPTANCE_TESTS = os.path.join(REF_DIR, "acceptance_tests")
 REFERENCE_SRC = os.environ.get("SGTR_REFERENCE", "/root/reference/proj")
 
 
-def build(native: bool = False) -> bool:
+def build() -> bool:
     """Compile oracle/_ref with oracle/ref.mk when the reference sources are
     present (this container); returns whether the library exists."""
     if os.path.isdir(os.path.join(REFERENCE_SRC, "src")):
-        args = ["make", "-s", "-j", str(os.cpu_count() or 4), "-f",
-                os.path.join(_HERE, "ref.mk"), f"REF={REFERENCE_SRC}"]
-        if native:
-            args.append("native")
-        subprocess.run(args, check=True)
+        subprocess.run(["make", "-s", "-j", str(os.cpu_count() or 4), "-f",
+                        os.path.join(_HERE, "ref.mk"), f"REF={REFERENCE_SRC}"], check=True)
     return os.path.exists(LIB_PATH)
 
 

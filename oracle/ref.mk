@@ -8,9 +8,12 @@
 # stand-ins under oracle/refshim/ provide the subset it uses (Eigen dense
 # algebra, a libpng stub -- PNG I/O is out of scope -- and doctest-lite).
 #
-#   make -f oracle/ref.mk            parity build (-O2 -ffp-contract=off)
-#   make -f oracle/ref.mk native     timing build (-O3 -march=native) for the
-#                                    CPU baseline, built on the host that runs it
+#   make -f oracle/ref.mk
+#
+# One build serves as checker and as the CPU baseline: the flags are the
+# reference's own CMake Release configuration (CMakeLists.txt:6-8: -O3
+# -DNDEBUG, no -march, so x86-64 SSE2 and no FMA contraction; the explicit
+# -ffp-contract=off only documents that).
 #
 # Products:
 #   _ref/libsplat_ref.so      splat_core (all 12 sources) + oracle/ref_capi.cpp
@@ -20,7 +23,7 @@ REF ?= /root/reference/proj
 CXX ?= g++
 HERE := $(dir $(abspath $(lastword $(MAKEFILE_LIST))))
 OUT ?= $(HERE)_ref
-OPT ?= -O2 -ffp-contract=off
+OPT ?= -O3 -DNDEBUG -ffp-contract=off
 CXXFLAGS := -std=c++20 $(OPT) -fPIC -pthread -I$(REF)/include -I$(HERE)refshim -w
 
 CORE := scene image scene_io render ssim residuals trust_region optimizer dataset config harness checks
@@ -54,11 +57,7 @@ $(OUT)/unit_tests: $(TEST_O) $(CORE_O)
 $(OUT)/acceptance_tests: $(OUT)/obj/acceptance.o $(CORE_O)
 	$(CXX) -pthread -o $@ $^ -lz
 
-native:
-	$(MAKE) -f $(lastword $(MAKEFILE_LIST)) OUT=$(HERE)_ref_native OPT="-O3 -march=native" \
-	    $(HERE)_ref_native/libsplat_ref.so
-
 clean:
-	rm -rf $(OUT) $(HERE)_ref_native
+	rm -rf $(OUT)
 
-.PHONY: all native clean
+.PHONY: all clean

@@ -2346,7 +2346,7 @@ int sgtr_make_synthetic(const sgtr_synth_config* cfg, double* gt_x, double* init
             const double eye[3] = {cfg->camera_radius * std::cos(ang),
                                    cfg->camera_radius * std::sin(ang), cfg->camera_height};
             // look_at_camera (scene.cpp:130-147)
-            double z[3] = {-eye[0], -eye[1], -eye[2]};
+            double z[3] = {0.0 - eye[0], 0.0 - eye[1], 0.0 - eye[2]};  // target - eye: +0, not -0
             auto normalize = [](double* u) {
                 const double n2 = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
                 if (n2 > 0.0) {

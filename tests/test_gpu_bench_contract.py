@@ -41,10 +41,16 @@ def test_bench_json_contract():
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["clocks"]["sm_mhz"] > 0 and "reasons" in d["clocks"]
+    assert d["anchor_c1"]["value"] > 0
 
 
-@pytest.mark.gpu
 def test_bench_reference_arm_contract():
+    """No GPU needed: the reference arm is CPU-only."""
+    from oracle import pyref
+    if not pyref.available():
+        pytest.skip("oracle/_ref not built")
+    sys.path.insert(0, ROOT)
+    import bench
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c1",
                         "--steps", "2", "--warmup", "1"], cwd=ROOT, capture_output=True,
                        text=True, timeout=900)
@@ -55,5 +61,11 @@ def test_bench_reference_arm_contract():
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["unit"] == "it/s" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "reference"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    # the reference arm runs the compiled reference, never the product
+    assert not any("libsgtr" in lib for lib in d["native_libs"]), d["native_libs"]
+    assert any("oracle/_ref" in lib for lib in d["native_libs"]), d["native_libs"]
+    assert d["anchor_c1"]["value"] > 0
+    assert d["config"] == bench.config_of("c1")
