@@ -220,7 +220,7 @@ void sh_color(const T mu[3], const T c[3], const T* k, int nb, const double cen[
         for (int a = 0; a < 3; ++a) out[a] = c[a];
         return;
     }
-    T d[3], Y[15];
+    T d[3], Y[15] = {};
     sh_dir(mu, cen, d);
     sh_basis(d[0], d[1], d[2], nb, Y);
     for (int a = 0; a < 3; ++a) {
@@ -1316,7 +1316,7 @@ void apply_clipped(orc_state* st, double* x, const Problem& pb, const orc_tr_opt
 void step_tr(orc_state* st, double* x, const Problem& pb, const orc_tr_opts& o,
              const std::vector<int>* s1_in, const std::vector<int>* s2_in,
              const double* probes_in, orc_diag* diag, double* applied) {
-    const int64_t k = pb.sc.k, dim = pb.sc.dim();
+    const int64_t dim = pb.sc.dim();
     orc_diag dg{0, 0, 0, 0, -1, -1, 0};
     st->t += 1;
     const int mv = static_cast<int>(pb.cams.size());
@@ -1977,6 +1977,9 @@ double orc_hellinger_sq(double ma, const double* mua, const double* sa, double m
 }
 
 orc_state* orc_state_create(int64_t dim, uint64_t seed) { return new orc_state(dim, seed); }
+void orc_state_rng_raw(orc_state* s, int64_t n, uint64_t* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = s->rng.raw();
+}
 void orc_state_destroy(orc_state* s) { delete s; }
 
 int orc_state_get(const orc_state* s, double* g_hat, double* d_hat, int64_t* t) {

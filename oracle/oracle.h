@@ -186,6 +186,8 @@ double orc_hellinger_sq(double mass_a, const double* mu_a,
 typedef struct orc_state orc_state;
 orc_state* orc_state_create(int64_t dim, uint64_t seed);
 void orc_state_destroy(orc_state* s);
+/* n raw draws from the state's Rng (continues the optimizer's stream) */
+void orc_state_rng_raw(orc_state* s, int64_t n, uint64_t* out);
 int orc_state_get(const orc_state* s, double* g_hat, double* d_hat,
                   int64_t* t);
 int orc_state_set(orc_state* s, const double* g_hat, const double* d_hat,

@@ -532,6 +532,12 @@ class State:
         g, d = _f64(g_hat), _f64(d_hat)
         lib().orc_state_set(self._h, _p(g), _p(d), C.c_int64(t))
 
+    def rng_raw(self, n):
+        """n raw draws continuing the state's Rng stream."""
+        out = np.empty(n, np.uint64)
+        lib().orc_state_rng_raw(self._h, C.c_int64(n), _p(out))
+        return out
+
     def get_adam(self):
         m, v = np.empty(self.dim), np.empty(self.dim)
         lib().orc_state_get_adam(self._h, _p(m), _p(v))

@@ -408,6 +408,9 @@ double orc_hellinger_sq(double mass_a, const double* mu_a, const double* sigma_a
 // optimizer.hpp:58-72 + optimizer.cpp:189-253
 orc_state* orc_state_create(int64_t dim, uint64_t seed) { return new orc_state(dim, seed); }
 void orc_state_destroy(orc_state* s) { delete s; }
+void orc_state_rng_raw(orc_state* s, int64_t n, uint64_t* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = s->st.rng.raw();
+}
 int orc_state_get(const orc_state* s, double* g_hat, double* d_hat, int64_t* t) {
     if (g_hat) put(s->st.g_hat, g_hat);
     if (d_hat) put(s->st.d_hat, d_hat);

@@ -366,7 +366,7 @@ struct Ctx {
     // further view lanes (stream + per-view workspace), swapped in by
     // use_lane so consecutive gradient views overlap: one view's projection,
     // sorts, binning and SSIM run beside another's raster passes
-    static constexpr int kMaxLanes = 3;
+    static constexpr int kMaxLanes = 2;
     struct Lane {
         cudaStream_t st = nullptr;
         DevStatus* dstat = nullptr;
@@ -381,8 +381,8 @@ struct Ctx {
 #undef SGTR_DECL
     } spare[kMaxLanes - 1];
     int cur_lane = 0;
-    int slot_of[kMaxLanes] = {-1, 0, 1};  // where each lane's workspace sits (-1: active)
-    Buf gacc[kMaxLanes];         // lanes 1.. accumulate their gradients here
+    int slot_of[kMaxLanes] = {-1, 0};  // where each lane's workspace sits (-1: active)
+    Buf gacc[kMaxLanes];         // gacc[1]: the second gradient accumulator (odd local views)
     cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
     double* htail = nullptr;     // pinned staging for the fused tail
     size_t htail_n = 0;
@@ -456,7 +456,7 @@ cudaStream_t lane_stream(Ctx& c, int L) {
 
 int lanes_knob() {
     const char* v = getenv("SGTR_LANES");
-    return v ? std::max(1, std::min(Ctx::kMaxLanes, atoi(v))) : 2;  // (1 disables the overlap)
+    return v ? std::max(1, std::min(2, atoi(v))) : 2;  // (1 disables the overlap)
 }
 
 struct Timed {
@@ -803,10 +803,12 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     std::vector<double> herr(2 * (n1 + n2), 0.0);
     bool local_error = false;
     // gradient phase: stochastic_gradient (optimizer.cpp:36-65), views of S1
-    // split round-robin over ranks (sgtr_shard_views).  The local views
-    // alternate between two lanes (streams with their own workspace); lane 1
-    // accumulates into its own buffer, added to lane 0's after the join, so
-    // the sum order is fixed.
+    // split round-robin over ranks (sgtr_shard_views).  Local view li adds
+    // its gradient into accumulator li % 2 and accumulator 1 is added to
+    // accumulator 0 at the end, whatever the lane count, so the summation
+    // order -- and every bit of g -- does not depend on SGTR_LANES.  With two
+    // lanes (streams with their own workspace) view li runs on lane li % 2,
+    // so each accumulator has one writer.
     struct LaneReset {  // an exception mid-loop must not leave lane 1 current
         Ctx& c;
         ~LaneReset() { use_lane(c, 0); }
@@ -814,20 +816,18 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     int n_local = 0;
     for (int p = c.rank; p < n1; p += c.nranks) ++n_local;
     const int lanes = std::min(n_local, lanes_knob());
-    double* gl[Ctx::kMaxLanes] = {g_acc, nullptr, nullptr};
-    if (lanes > 1) {
+    const int slots = std::min(n_local, 2);
+    double* gl[2] = {g_acc, nullptr};
+    if (slots > 1) {
+        gl[1] = c.gacc[1].as<double>(std::max<long long>(dim, 1));
         SGTR_CUDA(cudaEventRecord(c.ev_fork, c.st));
-        for (int L = 1; L < lanes; ++L) {
-            gl[L] = c.gacc[L].as<double>(std::max<long long>(dim, 1));
-            cudaStream_t ls = lane_stream(c, L);
-            SGTR_CUDA(cudaStreamWaitEvent(ls, c.ev_fork, 0));
-            SGTR_CUDA(cudaMemsetAsync(gl[L], 0, sizeof(double) * dim, ls));
-        }
+        cudaStream_t ls = lanes > 1 ? lane_stream(c, 1) : c.st;
+        if (lanes > 1) SGTR_CUDA(cudaStreamWaitEvent(ls, c.ev_fork, 0));
+        SGTR_CUDA(cudaMemsetAsync(gl[1], 0, sizeof(double) * dim, ls));
     }
     int li = 0;
     for (int p = c.rank; p < n1 && !local_error; p += c.nranks, ++li) {
-        const int L = li % lanes;
-        use_lane(c, L);
+        use_lane(c, li % lanes);
         const View& v = c.views[s1[p]];
         const ViewRender vr = render_view(c, v.dc, ro, false);
         if (vr.err_kind) {
@@ -838,16 +838,16 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         }
         residual_adjoint(c, GRAD, W, H, view_gt(c, s1[p]), nullptr, nullptr, o.residual.lambda,
                          o.residual.floor, loss + p);
-        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, gl[L], gflag + p);
+        backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, gl[li % 2], gflag + p);
     }
-    if (lanes > 1) {
+    if (slots > 1) {
         use_lane(c, 0);
-        for (int L = 1; L < lanes; ++L) {  // fixed lane order: deterministic sum
-            SGTR_CUDA(cudaEventRecord(c.ev_join[L], lane_stream(c, L)));
-            SGTR_CUDA(cudaStreamWaitEvent(c.st, c.ev_join[L], 0));
-            launch_add(c.st, g_acc, gl[L], dim);
-            c.launches += 1;
+        if (lanes > 1) {
+            SGTR_CUDA(cudaEventRecord(c.ev_join[1], lane_stream(c, 1)));
+            SGTR_CUDA(cudaStreamWaitEvent(c.st, c.ev_join[1], 0));
         }
+        launch_add(c.st, g_acc, gl[1], dim);
+        c.launches += 1;
     }
     // Hutchinson phase (optimizer.cpp:75-104), views of S2 split over ranks
     if (refresh && !local_error) {

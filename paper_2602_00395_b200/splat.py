@@ -459,6 +459,12 @@ class Context:
         d = None if d_hat is None else _f64(d_hat)
         check(lib().sgtr_state_set(self._h, _ptr(g), _ptr(d), t))
 
+    def rng_raw(self, n: int) -> np.ndarray:
+        """n raw mt19937_64 draws continuing the state's Rng (rng.hpp:24)."""
+        out = np.empty(n, np.uint64)
+        check(lib().sgtr_rng_raw(self._h, C.c_int64(n), _ptr(out)))
+        return out
+
     def state_get_adam(self):
         m, v = np.empty(self.dim), np.empty(self.dim)
         check(lib().sgtr_state_get_adam(self._h, _ptr(m), _ptr(v)))

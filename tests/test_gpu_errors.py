@@ -1,0 +1,112 @@
+"""Error-path parity of step_3dgs2tr on the device against the compiled
+reference: the three NumericError locators of optimizer.cpp and the state the
+reference leaves behind after each (t, g_hat, D_hat, x and where its Rng
+stream continues):
+
+* "stochastic_gradient: non-finite gradient from view N" (optimizer.cpp:54-56):
+  t incremented, S1 drawn, nothing else changed;
+* "hutchinson_diag: non-finite sample" (optimizer.cpp:97-98): g_hat updated,
+  S2 and the failing sample's probe drawn, D_hat and x unchanged;
+* "non-finite update in group G" (optimizer.cpp:116-121): g_hat (and D_hat on
+  a refresh) updated, x unchanged.
+"""
+import numpy as np
+import pytest
+
+from oracle import pyref
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not pyref.available(), reason="oracle/_ref not built")]
+
+VIEWS = 5
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2602_00395_b200 import splat
+    return splat
+
+
+@pytest.fixture(scope="module")
+def ds():
+    ref = pyref.ref
+    return ref.make_synthetic(ref.SynthConfig(gt_splats=60, init_splats=80, views=VIEWS,
+                                              image_size=24, seed=4))
+
+
+def draws(seed):
+    """S1 and S2 of the first step (|S1| = |S2| = 1, optimizer.cpp:195-206)."""
+    r = pyref.ref.Rng(seed)
+    return int(r.sample_without_replacement(VIEWS, 1)[0]), \
+        int(r.sample_without_replacement(VIEWS, 1)[0])
+
+
+def run_both(sp, ds, gts, seed, state=None):
+    ref = pyref.ref
+    x = ds.init_x.copy()
+    rst = ref.State(x.size, seed)
+    ctx = sp.Context()
+    ctx.set_scene(x)
+    ctx.set_views([sp.Camera.from_c(c, g) for c, g in zip(ds.cams, gts)])
+    ctx.state_reset(seed)
+    if state is not None:
+        rst.set(*state)
+        ctx.state_set(*state)
+    opts = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 20))
+    with pytest.raises(sp.NumericError) as eg:
+        ctx.step(opts)
+    with pytest.raises(ref.OracleNumericError) as er:
+        ref.step_3dgs2tr(rst, x, ds.cams, gts, ref.TrOptions(total_steps=20))
+    g, d, t = ctx.state_get()
+    gr, dr, tr = rst.get()
+    out = dict(msg=(str(eg.value), str(er.value)), t=(t, tr), g=(g, gr), d=(d, dr),
+               x=(ctx.get_scene(), x), rng=(ctx.rng_raw(8), rst.rng_raw(8)))
+    ctx.close()
+    return out
+
+
+def test_gradient_failure_names_the_view(sp, ds):
+    seed = 3
+    s1, _ = draws(seed)
+    gts = [g.copy() for g in ds.gts]
+    gts[s1][5, 7, 1] = np.inf
+    r = run_both(sp, ds, gts, seed)
+    assert r["msg"][0] == r["msg"][1] == \
+        f"stochastic_gradient: non-finite gradient from view {ds.cams[s1].id}"
+    assert r["t"] == (1, 1)
+    for k in ("g", "d"):
+        assert not r[k][0].any() and not r[k][1].any()
+    assert np.array_equal(r["x"][0], ds.init_x) and np.array_equal(r["x"][1], ds.init_x)
+    assert np.array_equal(*r["rng"])  # both continue right after S1
+
+
+def test_hutchinson_failure(sp, ds):
+    seed = next(s for s in range(1, 200) if draws(s)[0] != draws(s)[1])
+    s1, s2 = draws(seed)
+    gts = [g.copy() for g in ds.gts]
+    gts[s2][3, 3, 0] = np.inf
+    r = run_both(sp, ds, gts, seed)
+    assert r["msg"][0] == r["msg"][1] == "hutchinson_diag: non-finite sample"
+    assert r["t"] == (1, 1)
+    g, gr = r["g"]
+    assert gr.any() and np.max(np.abs(g - gr)) <= 1e-3 * np.max(np.abs(gr))
+    assert not r["d"][0].any() and not r["d"][1].any()
+    assert np.array_equal(r["x"][0], ds.init_x) and np.array_equal(r["x"][1], ds.init_x)
+    assert np.array_equal(*r["rng"])  # after S2 and the failing sample's probe
+
+
+def test_non_finite_update_names_the_group(sp, ds):
+    k = ds.init_x.size // 14
+    g0 = np.zeros(ds.init_x.size)
+    g0[6 * k + 5] = np.nan  # a rotation coordinate of g_hat
+    r = run_both(sp, ds, ds.gts, 7, state=(g0, np.zeros_like(g0), 1))
+    assert r["msg"][0] == r["msg"][1] == "non-finite update in group rotation"
+    assert r["t"] == (2, 2)  # t = 2: not a refresh step
+    g, gr = r["g"]
+    assert np.isnan(g[6 * k + 5]) and np.isnan(gr[6 * k + 5])
+    fin = np.isfinite(gr)
+    assert np.max(np.abs(g[fin] - gr[fin])) <= 1e-3 * np.max(np.abs(gr[fin]))
+    assert np.array_equal(r["x"][0], ds.init_x) and np.array_equal(r["x"][1], ds.init_x)
+    assert np.array_equal(*r["rng"])
