@@ -1705,7 +1705,9 @@ static bool ellipse_may_hit(double mx, double my, double i00, double i01, double
     const double myd = std::fmax(std::fabs(ay), std::fabs(by));
     const double bound = std::fabs(i00) * mxd * mxd + std::fabs(i11) * myd * myd +
                          2.0 * std::fabs(i01) * mxd * myd;
-    return qmin <= rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12;
+    // NaN (a degenerate conic) keeps the fragment: the reference evaluates every
+    // pair whose bbox test passes, and a NaN alpha_bar is not skipped (render.cpp:136)
+    return !(qmin > rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12);
 }
 
 // Restated tile binning of the GPU build.  A visible fragment belongs to tile

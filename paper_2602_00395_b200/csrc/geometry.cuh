@@ -324,7 +324,9 @@ SGTR_HD bool ellipse_may_hit(double mx, double my, double i00, double i01, doubl
     qmin = fmin(qmin, q(clampd(-(k00 * by), ax, bx), by));
     const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
     const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
-    return qmin <= rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12;
+    // NaN (a degenerate conic) keeps the fragment: the reference evaluates every
+    // pair whose bbox test passes, and a NaN alpha_bar is not skipped (render.cpp:136)
+    return !(qmin > rho2 + 1e-9 * rho2 + 1e-12 * bound + 1e-12);
 }
 
 // pixel-centre range [p0, p1] inside the closed interval [lo, hi], clipped

@@ -12,10 +12,13 @@
 // record as a warp-wide broadcast.
 //
 // Branch parity: the three kernels evaluate the primal alpha with the same
-// pinned operation sequence (no FMA; identical to the oracle's restatement
-// of render.cpp:132-136), so bbox reject, alpha clamp, alpha skip and the
-// transmittance stop take the same branches in forward, VJP and JVP — the
-// reference's "frozen branches" contract (render.hpp:76-79).
+// pinned operation sequence (eval_expo's FMA form and fastexp.cuh's exp, a
+// few ulp from the reference's own order), so bbox reject, alpha clamp,
+// alpha skip and the transmittance stop take the same branches in forward,
+// VJP and JVP — the reference's "frozen branches" contract
+// (render.hpp:76-79).  The skip test is written as the reference's
+// `alpha_bar < alpha_skip -> skip`, so a NaN alpha_bar is kept and
+// propagates as it does in the reference (render.cpp:136).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -122,7 +125,7 @@ __device__ __forceinline__ bool warp_may_hit(const PixelCtx& p, const double* f)
     qmin = fmin(qmin, q(cl(-k00 * by, ax, bx), by));
     const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
     const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
-    return qmin <= rho2 + 1e-8 * rho2 + 1e-11 * bound + 1e-11;
+    return !(qmin > rho2 + 1e-8 * rho2 + 1e-11 * bound + 1e-11);
 }
 
 // cooperative staging: 8 lanes per 128-byte record; entries [b, b+n) of the
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
                 double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (kCount) ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
+                if (!(abar < ro.alpha_skip)) {
                     if (kCount) ++n_contrib;
                     const double w = abar * T;
                     c0 += f[R_C0] * w;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(32 * WPB)
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
+                if (!(abar < ro.alpha_skip)) {
                     const double w = abar * T;
                     c0 += f[R_C0] * w;
                     c1 += f[R_C1] * w;
@@ -393,14 +396,14 @@ __global__ void __launch_bounds__(32 * WPB)
             if (a0 && a1) {
                 const StagedRec r0 = my_rec[e], r1 = my_rec[e + 1];
                 const double ab0 = falloff(r0), ab1 = falloff(r1);
-                if (h0 && ab0 >= ro.alpha_skip) blend(r0, ab0, e);
-                if (h1 && !done && ab1 >= ro.alpha_skip) blend(r1, ab1, e + 1);
+                if (h0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, e);
+                if (h1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, e + 1);
             } else if (a0 || a1) {
                 const int ee = a0 ? e : e + 1;
                 if (a0 ? h0 : h1) {
                     const StagedRec r = my_rec[ee];
                     const double ab = falloff(r);
-                    if (ab >= ro.alpha_skip) blend(r, ab, ee);
+                    if (!(ab < ro.alpha_skip)) blend(r, ab, ee);
                 }
             }
             if (__all_sync(kFull, done)) break;
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists t
                 double abar = __dmul_rn(f[R_ALPHA], gauss);
                 const bool clamped = abar >= ro.alpha_clamp;
                 if (clamped) abar = ro.alpha_clamp;
-                if (abar >= ro.alpha_skip) {
+                if (!(abar < ro.alpha_skip)) {
                     contrib = true;
                     // one reciprocal for T_in = T / (1 - abar) and the three
                     // behind / (1 - abar) terms (render.cpp:243-245)
@@ -898,7 +901,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                     abar[k] = __dmul_rn(r.alpha, gauss[k]);
                     cl[k] = abar[k] >= ro.alpha_clamp;
                     if (cl[k]) abar[k] = ro.alpha_clamp;
-                    lv[k] = lv[k] && abar[k] >= ro.alpha_skip;
+                    lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
                     rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
                 }
 #pragma unroll
@@ -979,7 +982,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
                     abar = ro.alpha_clamp;
                     dabar = 0.0;
                 }
-                if (abar >= ro.alpha_skip) {
+                if (!(abar < ro.alpha_skip)) {
                     // w = abar * T ; acc += c * w ; T = T * (1 - abar)
                     const double w = abar * T;
                     const double dw = dabar * T + abar * dT;
@@ -1081,7 +1084,7 @@ __global__ void __launch_bounds__(32 * WPB)
                     abar = ro.alpha_clamp;
                     dabar = 0.0;
                 }
-                if (abar >= ro.alpha_skip) {
+                if (!(abar < ro.alpha_skip)) {
                     const double w = abar * T;
                     const double dw = dabar * T + abar * dT;
                     d0 += t.c0 * w + f[R_C0] * dw;

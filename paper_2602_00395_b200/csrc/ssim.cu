@@ -30,6 +30,11 @@ constexpr int TX = 32, TY = 16, HALO = 5;
 constexpr int kThreads = 256;  // TX * TY / 2: two output rows per thread
 constexpr int kHC = 4;         // horizontal pass: output columns per thread
 constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 18
+// shared-memory row strides, padded so the FP64 tiles are bank-conflict
+// free: the horizontal passes give consecutive lanes consecutive staged rows
+// (stride 43 doubles = 86 words, 22 mod 32: 16 distinct even banks per
+// half-warp) and write the filtered rows at stride 33 doubles (2 mod 32)
+constexpr int SXP = SX + 1, TXP = TX + 1;
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ double c_k[11];
@@ -69,9 +74,9 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
     constexpr int NM = Tr::kMoments;
     extern __shared__ __align__(16) double smem[];
     double* s_a = smem;                      // SY x SX
-    double* s_b = s_a + SY * SX;
-    double* s_da = s_b + SY * SX;            // (tangent modes)
-    double* s_h = s_da + (Tr::kTangent ? SY * SX : 0);  // NM x SY x TX
+    double* s_b = s_a + SY * SXP;
+    double* s_da = s_b + SY * SXP;            // (tangent modes)
+    double* s_h = s_da + (Tr::kTangent ? SY * SXP : 0);  // NM x SY x TXP
     const int W = args.W, H = args.H;
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
@@ -103,9 +108,9 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
             vb = B[q];
             if (Tr::kTangent) vd = DA[q];
         }
-        s_a[i] = va;
-        s_b[i] = vb;
-        if (Tr::kTangent) s_da[i] = vd;
+        s_a[sy * SXP + sx] = va;
+        s_b[sy * SXP + sx] = vb;
+        if (Tr::kTangent) s_da[sy * SXP + sx] = vd;
     }
     __syncthreads();
     // horizontal pass over all SY rows; two adjacent columns per thread share
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
     };
     // (kHC adjacent columns per thread share the staged taps between them)
     for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
-        const int sy = i / (TX / kHC), tx = kHC * (i % (TX / kHC));
+        const int sy = i % SY, tx = kHC * (i / SY);
         double mo[kHC][NM];
 #pragma unroll
         for (int o = 0; o < kHC; ++o)
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
             for (int j = 0; j < NM; ++j) mo[o][j] = 0.0;
 #pragma unroll
         for (int d = 0; d < 10 + kHC; ++d) {
-            const int si = sy * SX + tx + d;
+            const int si = sy * SXP + tx + d;
             const double av = s_a[si], bv = s_b[si];
             const double dv = Tr::kTangent ? s_da[si] : 0.0;
 #pragma unroll
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
 #pragma unroll
         for (int o = 0; o < kHC; ++o)
 #pragma unroll
-            for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TX + tx + o] = mo[o][j];
+            for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TXP + tx + o] = mo[o][j];
     }
     __syncthreads();
     using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
     for (int d = 0; d < 12; ++d) {
 #pragma unroll
         for (int j = 0; j < NM; ++j) {
-            const double v = s_h[(j * SY + ty0 + d) * TX + tx];
+            const double v = s_h[(j * SY + ty0 + d) * TXP + tx];
             if (d < 11) mv[0][j] += c_k[d] * v;
             if (d > 0) mv[1][j] += c_k[d - 1] * v;
         }
@@ -190,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
         const double s_v = primal(sv), s_d = tangent(sv);
         const double n1v = primal(n1), d1v = primal(d1), n2v = primal(n2), d2v = primal(d2);
         const double mu_av = primal(mu_a);
-        const double av = s_a[(ty + HALO) * SX + tx + HALO];
-        const double bv = s_b[(ty + HALO) * SX + tx + HALO];
+        const double av = s_a[(ty + HALO) * SXP + tx + HALO];
+        const double bv = s_b[(ty + HALO) * SXP + tx + HALO];
         const double diff = av - bv;
         const double lam = args.lambda, fl = args.floor;
         const double u1 = (1.0 - lam) * fabs(diff);
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
             args.out0[pi] = sqrt(fmax(u1, fl));
             args.out0[3 * P + pi] = sqrt(fmax(u2, fl));
         } else if (MODE == RES_JVP) {
-            const double t = s_da[(ty + HALO) * SX + tx + HALO];
+            const double t = s_da[(ty + HALO) * SXP + tx + HALO];
             args.out0[pi] = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
             args.out0[3 * P + pi] = u2 > fl ? -lam * s_d / (4.0 * sqrt(u2)) : 0.0;
         } else {
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
                 ur2 = 0.0;
                 partial += fmax(u1, fl) + fmax(u2, fl);
             } else if (MODE == HUTCH) {
-                const double t = s_da[(ty + HALO) * SX + tx + HALO];
+                const double t = s_da[(ty + HALO) * SXP + tx + HALO];
                 ur1 = u1 > fl ? (1.0 - lam) * sgn(diff) * t / (2.0 * sqrt(u1)) : 0.0;
                 ur2 = u2 > fl ? -lam * s_d / (4.0 * sqrt(u2)) : 0.0;
             } else if (MODE == RES_VJP) {
@@ -321,8 +326,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather(int W, int H, const doub
                                                    const double* __restrict__ Qf,
                                                    const double* __restrict__ Rf,
                                                    double* __restrict__ adj, int by0) {
-    __shared__ double s_f[3][SY][SX];
-    __shared__ double s_h[3][SY][TX];
+    __shared__ double s_f[3][SY][SXP];
+    __shared__ double s_h[3][SY][TXP];
     const long long P = (long long)W * H;
     const int c = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = (blockIdx.y + by0) * TY;
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather(int W, int H, const doub
     if (in_x) {
         // kHC adjacent columns per thread share the staged taps
         for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
-            const int sy = i / (TX / kHC), tx = kHC * (i % (TX / kHC));
+            const int sy = i % SY, tx = kHC * (i / SY);
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 const double* row = &s_f[f][sy][tx];
@@ -490,8 +495,8 @@ void init_constants() {
 template <int MODE, bool kPre = false>
 void run_ssim(cudaStream_t st, const SsimArgs& a) {
     using Tr = ModeTraits<MODE, kPre>;
-    const size_t smem = sizeof(double) * (SY * SX * (Tr::kTangent ? 3 : 2) +
-                                          Tr::kMoments * SY * TX);
+    const size_t smem = sizeof(double) * (SY * SXP * (Tr::kTangent ? 3 : 2) +
+                                          Tr::kMoments * SY * TXP);
     static unsigned long long attr = 0;  // bit d: attribute set on device d
     const unsigned long long bit = 1ull << (current_device() & 63);
     if (!(attr & bit)) {
