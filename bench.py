@@ -456,6 +456,12 @@ def main():
     gt, init, cams = make_dataset(sp, ctx, args.config, args.seed)
     ctx.state_reset(args.seed)
     if world > 1:
+        # the communicator's setup lines in the log, and a pinned algorithm /
+        # protocol so the allreduce's summation order is the same every run
+        # (SURVEY §5); libsgtr loads NCCL at comm init, after these are set
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         uid = [sp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(uid[0], world, rank)
@@ -494,9 +500,14 @@ def main():
     lanes_env = os.environ.get("SGTR_LANES")
     os.environ["SGTR_LANES"] = "1"
     _lib.check(_lib.lib().sgtr_kernel_timing(ctx.handle, 1))
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.synchronize()
+    g0.record(stream)
     for _ in range(args.steps):
         ctx.step(opt)
+    g1.record(stream)
     ctx.synchronize()
+    ms_one_lane = g0.elapsed_time(g1) / args.steps
     buf = C.create_string_buffer(4096)
     _lib.check(_lib.lib().sgtr_kernel_timing_report(ctx.handle, buf, 4096))
     _lib.check(_lib.lib().sgtr_kernel_timing(ctx.handle, 0))
@@ -656,6 +667,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "kernel_ms": {n: {"launches": c_, "total_ms": t_} for n, (c_, t_) in ktimes.items()},
+            "ms_per_step_one_lane": ms_one_lane,
+            "kernel_ms_sum_per_step": sum(t_ for _, t_ in ktimes.values()) / args.steps,
             "kernel_ms_note": ("per kernel class over a second run of the same step count with "
                                "one view lane (SGTR_LANES=1), CUDA events on the library stream; "
                                "the timed region itself overlaps two view lanes"),

@@ -369,6 +369,15 @@ int sgtr_shard_views(int32_t n, int32_t rank, int32_t nranks, int32_t* positions
                      int32_t* count);
 int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks,
                    int32_t rank);
+/* In-process communicator for testing the multi-rank data plane on one GPU
+ * (the product path is NCCL): nranks host threads, each with its own
+ * context on the same device, join one group with ranks 0..nranks-1; a
+ * step's allreduce and the radii all-gather then meet at a host barrier and
+ * sum / copy through device memory in rank order.  1..8 ranks. */
+typedef struct sgtr_group sgtr_group;
+int sgtr_loopback_group_create(int32_t nranks, sgtr_group** out);
+int sgtr_loopback_group_destroy(sgtr_group* g);
+int sgtr_comm_init_loopback(sgtr_ctx* ctx, sgtr_group* group, int32_t rank);
 
 #ifdef __cplusplus
 }

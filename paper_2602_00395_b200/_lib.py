@@ -130,6 +130,9 @@ _SIGS = {
                                              C.c_int32, VP]),
     "sgtr_get_applied_step": (C.c_int, [VP, VP]),
     "sgtr_step_failed_sample": (C.c_int, [VP, VP]),
+    "sgtr_loopback_group_create": (C.c_int, [C.c_int32, C.POINTER(VP)]),
+    "sgtr_loopback_group_destroy": (C.c_int, [VP]),
+    "sgtr_comm_init_loopback": (C.c_int, [VP, VP, C.c_int32]),
     "sgtr_step_adam": (C.c_int, [VP, VP, VP, VP]),
     "sgtr_step_adam_tr": (C.c_int, [VP, VP, VP, VP]),
     "sgtr_step_adam_explicit": (C.c_int, [VP, VP, VP, C.c_int32, VP, C.c_int32, VP]),

@@ -11,6 +11,7 @@
 #include <sstream>
 #include <fstream>
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <condition_variable>
 #include <deque>
@@ -334,6 +335,28 @@ struct KTimer {
 
 }  // namespace
 
+// in-process communicator (see allreduce below)
+struct LoopGroup {
+    int n;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<double*> ptr;
+    explicit LoopGroup(int n_) : n(n_), ptr(n_, nullptr) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++arrived == n) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+            return;
+        }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; }))
+            throw Error(SGTR_RUNTIME, "loopback group: a rank did not reach the collective");
+    }
+};
 struct Ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -392,6 +415,9 @@ struct Ctx {
     int fail_sample = -1;   // Hutchinson sample of the last step's failure (sgtr_step_failed_sample)
     Buf stage;              // shard-major staging for the radius all-gather
     void* comm = nullptr;
+    LoopGroup* loop = nullptr;  // in-process communicator (sgtr_comm_init_loopback)
+    Buf loopbuf;
+    bool collective() const { return (comm || loop) && nranks > 1; }
 
     ~Ctx() {
         prefetch.reset();
@@ -759,10 +785,64 @@ void ensure_tail(Ctx& c, size_t n) {
     c.htail_n = n;
 }
 
+// In-process communicator: n host threads on one GPU, one context each
+// (sgtr_comm_init_loopback).  It runs the multi-rank data plane -- the view
+// split, the fused [g | loss | flags | z.w] buffer, refresh bands, the sharded
+// radii -- with the collectives done through device memory: every rank
+// publishes its buffer, the host threads meet at a barrier, and each rank
+// sums the buffers in rank order (or copies the other ranks' shards).  Tests
+// use it to check the N-rank step against the 1-rank step on one GPU; the
+// product path is NCCL.
+struct RankPtrs {
+    const double* p[8];
+};
+__global__ void k_sum_ranks(RankPtrs in, int n, double* __restrict__ out, long long count) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    double s = in.p[0][i];
+    for (int r = 1; r < n; ++r) s += in.p[r][i];
+    out[i] = s;
+}
+
 void allreduce(Ctx& c, double* buf, size_t n) {
-    if (!c.comm || n == 0) return;
+    if (!c.collective() || n == 0) return;
+    if (c.loop) {
+        LoopGroup& g = *c.loop;
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        g.ptr[c.rank] = buf;
+        g.barrier();
+        RankPtrs rp{};
+        for (int r = 0; r < g.n; ++r) rp.p[r] = g.ptr[r];
+        double* tmp = c.loopbuf.as<double>(n);
+        k_sum_ranks<<<(unsigned)((n + 255) / 256), 256, 0, c.st>>>(rp, g.n, tmp, (long long)n);
+        SGTR_CUDA(cudaGetLastError());
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        g.barrier();  // every rank has read every buffer
+        SGTR_CUDA(cudaMemcpyAsync(buf, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.st));
+        c.launches += 1;
+        return;
+    }
     g_nccl.check(g_nccl.all_reduce(buf, buf, n, /*ncclFloat64*/ 8, /*ncclSum*/ 0, c.comm, c.st),
                  "ncclAllReduce");
+}
+
+// rank r's block [r B, (r + 1) B) of S is gathered to every rank
+void allgather(Ctx& c, double* S, long long B) {
+    if (c.loop) {
+        LoopGroup& g = *c.loop;
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        g.ptr[c.rank] = S;
+        g.barrier();
+        for (int r = 0; r < g.n; ++r)
+            if (r != c.rank)
+                SGTR_CUDA(cudaMemcpyAsync(S + B * r, g.ptr[r] + B * r, sizeof(double) * B,
+                                          cudaMemcpyDeviceToDevice, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        g.barrier();
+        return;
+    }
+    g_nccl.check(g_nccl.all_gather(S + B * c.rank, S, B, /*ncclFloat64*/ 8, c.comm, c.st),
+                 "ncclAllGather");
 }
 
 // ------------------------------------------------------------------ Algorithm 1
@@ -1036,7 +1116,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     // by shard on one rank (sgtr_set_tr_shards, which exercises the same
     // staging).  Radii are per splat, so the result does not depend on the
     // sharding.
-    const bool multi = c.comm && c.nranks > 1 && a.kind != 1 && !a.ghat_only;
+    const bool multi = c.collective() && a.kind != 1 && !a.ghat_only;
     const int shards = multi ? c.nranks : (a.kind != 1 && !a.ghat_only ? c.tr_shards : 1);
     const long long Kp = (c.K + shards - 1) / shards;
     auto shard_range = [&](int r, int& i0, int& n) {
@@ -1071,9 +1151,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
             shard_range(r, i0, n);
             launch_stage(c.st, eta, S, c.K, c.nb, Kp, i0, n, true);
         }
-        if (multi)
-            g_nccl.check(g_nccl.all_gather(S + B * c.rank, S, B, /*ncclFloat64*/ 8, c.comm, c.st),
-                         "ncclAllGather");
+        if (multi) allgather(c, S, B);
         launch_stage(c.st, eta, S, c.K, c.nb, Kp, 0, c.K, false);
         c.launches += (r_last - r_first + 1) + 1;
     }
@@ -2529,13 +2607,39 @@ int sgtr_set_tr_shards(sgtr_ctx* ctx, int32_t shards) {
     });
 }
 
+int sgtr_loopback_group_create(int32_t nranks, sgtr_group** out) {
+    return guarded([&] {
+        if (!out) throw invalid("sgtr_loopback_group_create: null output");
+        if (nranks < 1 || nranks > 8) throw invalid("sgtr_loopback_group_create: 1..8 ranks");
+        *out = reinterpret_cast<sgtr_group*>(new LoopGroup(nranks));
+    });
+}
+
+int sgtr_loopback_group_destroy(sgtr_group* g) {
+    return guarded([&] { delete reinterpret_cast<LoopGroup*>(g); });
+}
+
+int sgtr_comm_init_loopback(sgtr_ctx* ctx, sgtr_group* group, int32_t rank) {
+    return guarded([&] {
+        Ctx& c = ctx_ref(ctx);
+        bind(c);
+        if (!group) throw invalid("sgtr_comm_init_loopback: null group");
+        LoopGroup* g = reinterpret_cast<LoopGroup*>(group);
+        if (rank < 0 || rank >= g->n) throw invalid("sgtr_comm_init: bad rank");
+        if (c.comm || c.loop) throw invalid("sgtr_comm_init: communicator already initialised");
+        c.loop = g;
+        c.nranks = g->n;
+        c.rank = rank;
+    });
+}
+
 int sgtr_comm_init(sgtr_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank) {
     return guarded([&] {
         Ctx& c = ctx_ref(ctx);
         bind(c);
         if (nranks < 1 || rank < 0 || rank >= nranks) throw invalid("sgtr_comm_init: bad rank");
         if (!id) throw invalid("sgtr_comm_init: null unique id");
-        if (c.comm) throw invalid("sgtr_comm_init: communicator already initialised");
+        if (c.comm || c.loop) throw invalid("sgtr_comm_init: communicator already initialised");
         // a 1-rank communicator is created too (it runs the same allreduce
         // path; tests use it to exercise the NCCL plumbing on one GPU)
         g_nccl.load();

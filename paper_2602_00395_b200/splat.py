@@ -523,6 +523,26 @@ class Context:
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
         check(lib().sgtr_comm_init(self._h, buf, nranks, rank))
 
+    def comm_init_loopback(self, group: "LoopbackGroup", rank: int) -> None:
+        """Join an in-process group (one host thread per rank on one GPU)."""
+        check(lib().sgtr_comm_init_loopback(self._h, group.handle, rank))
+
+
+class LoopbackGroup:
+    """In-process communicator over one GPU (sgtr_loopback_group_create):
+    tests run the N-rank data plane with N threads, one Context each."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        check(lib().sgtr_loopback_group_create(nranks, C.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().sgtr_loopback_group_destroy(self.handle))
+            self.handle = None
+
 
 def shard_views(n: int, rank: int, nranks: int) -> List[int]:
     """Positions of an n-view batch that ``rank`` of ``nranks`` renders (the
