@@ -103,6 +103,38 @@ __device__ __forceinline__ bool warp_misses(const PixelCtx& p, const double* f) 
     return p.wx1 < f[R_BX0] || p.wx0 > f[R_BX1] || p.wy1 < f[R_BY0] || p.wy0 > f[R_BY1];
 }
 
+// 32x32 bit-matrix transpose across the warp: lane l holds row l; returns
+// this lane's column (bit l of the result = bit `lane` of row l).  Five
+// exchange stages (__shfl_xor of 16, 8, 4, 2, 1 lanes).
+__device__ __forceinline__ unsigned warp_transpose32(unsigned x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const unsigned m = s == 16 ? 0x0000FFFFu
+                           : s == 8 ? 0x00FF00FFu
+                           : s == 4 ? 0x0F0F0F0Fu
+                           : s == 2 ? 0x33333333u
+                                    : 0x55555555u;
+        const unsigned y = __shfl_xor_sync(0xffffffffu, x, s);
+        x = (lane & s) ? ((x & ~m) | ((y & ~m) >> s)) : ((x & m) | ((y & m) << s));
+    }
+    return x;
+}
+
+// the pixels of an 8-column block (rows from iy0, `rows` <= 8 of them) that
+// lie in the pixel rectangle r (K1's pixel_range of the closed FP64 bbox,
+// render.cpp:128-131), as a mask over slot = row * 8 + column
+__device__ __forceinline__ unsigned long long block_slots(int4 r, int ix0, int iy0, int rows) {
+    const int c0 = max(r.x - ix0, 0), c1 = min(r.z - ix0, 7);
+    const int r0 = max(r.y - iy0, 0), r1 = min(r.w - iy0, rows - 1);
+    if (c0 > c1 || r0 > r1) return 0ull;
+    const unsigned long long cols =
+        ((0xFFull >> (7 - (c1 - c0))) << c0) * 0x0101010101010101ull;
+    const int nr = r1 - r0 + 1;
+    const unsigned long long rowm = (nr >= 8 ? ~0ull : ((1ull << (8 * nr)) - 1ull)) << (8 * r0);
+    return cols & rowm;
+}
+
 // Warp-level contribution filter (after warp_misses): false only when no
 // pixel centre of the warp's 8x4 block can reach alpha_bar >= alpha_skip —
 // the minimum of q = d^T Sigma^-1 d over the block is certainly above
@@ -407,6 +439,106 @@ __global__ void __launch_bounds__(32 * WPB)
                 }
             }
             if (__all_sync(kFull, done)) break;
+        }
+        __syncwarp();
+    }
+    if (!pc.inside) return;
+    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
+    img[p] = c0 + ro.bg[0] * T;
+    img[P + p] = c1 + ro.bg[1] * T;
+    img[2 * P + p] = c2 + ro.bg[2] * T;
+    tfinal[p] = T;
+    last[p] = processed;
+}
+
+// ------------------------------------------------------------------ K7, hit bitmasks
+// The per-pixel bbox test of every (entry, pixel) pair is done once per batch
+// as bit arithmetic: the lane that stages list entry base + j turns its pixel
+// rectangle into the 32-bit mask of the warp block's pixels it covers, and a
+// warp bit-transpose gives every pixel lane the mask of the batch entries
+// covering it.  The warp then visits, two at a time, only the entries that
+// cover some pixel still blending (an OR-reduction of the lane masks, with
+// finished pixels' masks cleared), and each lane's test of an entry is one bit
+// -- no per-entry rectangle loads, compares or votes.  Per pixel the entries,
+// operations and their order are those of k_raster_fwd_paired, so the image,
+// T and the stop index are bit-identical.
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB)
+    k_raster_fwd_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                      double* __restrict__ img, double* __restrict__ tfinal,
+                      int* __restrict__ last) {
+    constexpr int SUB = kWarps / WPB;
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
+    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
+    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    bool done = !pc.inside;
+    int processed = end - start;
+    StagedRec* my_rec = s_rec[lw];
+    auto falloff = [&](const StagedRec& r) {
+        const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
+                              r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+        const double dx = pc.pxc - r.mx, dy = pc.pyc - r.my;
+        double abar = __dmul_rn(r.alpha, fast_exp_neg(eval_expo(dx, dy, f)));
+        if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
+        return abar;
+    };
+    auto blend = [&](const StagedRec& r, double abar, int pos) {
+        const double w = abar * T;
+        c0 += r.c0 * w;
+        c1 += r.c1 * w;
+        c2 += r.c2 * w;
+        T = __dmul_rn(T, __dsub_rn(1.0, abar));
+        if (T < ro.t_stop) {
+            done = true;
+            processed = pos - start + 1;
+        }
+    };
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done)) break;
+        const int jj = base + lane;
+        unsigned slots = 0;
+        if (jj < end) {
+            slots = (unsigned)block_slots(__ldg(tl.trect + jj), pc.ix0, pc.iy0, 4);
+            if (slots) {
+                const double2* r2 = reinterpret_cast<const double2*>(
+                    rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+                const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+                const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+                double2* o = reinterpret_cast<double2*>(my_rec + lane);
+                o[0] = a;
+                o[1] = b;
+                o[2] = c;
+                o[3] = d;
+                o[4] = e;
+            }
+        }
+        unsigned mine = warp_transpose32(slots);  // bit j: entry base + j covers my pixel
+        if (done) mine = 0u;
+        __syncwarp();
+        unsigned wb = __reduce_or_sync(kFull, mine);
+        while (wb) {
+            const int j0 = __ffs(wb) - 1;
+            wb &= wb - 1u;
+            if (wb) {
+                const int j1 = __ffs(wb) - 1;
+                wb &= wb - 1u;
+                const bool h0 = (mine >> j0) & 1u, h1 = (mine >> j1) & 1u;
+                const StagedRec r0 = my_rec[j0], r1 = my_rec[j1];
+                const double ab0 = falloff(r0), ab1 = falloff(r1);
+                if (h0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, base + j0);
+                if (h1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, base + j1);
+            } else if ((mine >> j0) & 1u) {
+                const StagedRec r = my_rec[j0];
+                const double ab = falloff(r);
+                if (!(ab < ro.alpha_skip)) blend(r, ab, base + j0);
+            }
+            if (done) mine = 0u;
+            wb &= __reduce_or_sync(kFull, mine);
         }
         __syncwarp();
     }
@@ -942,6 +1074,203 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     if (nring) flush(nring);
 }
 
+// ------------------------------------------------------------------ K10, hit bitmasks
+// k_raster_vjp_staged3 with the per-(entry, pixel) tests done as bit
+// arithmetic (as k_raster_fwd_bits): the staging lane of list entry base + j
+// turns its pixel rectangle into the 64-bit mask of the 8x8 block's pixels it
+// covers; two warp bit-transposes give each lane the entries covering its two
+// pixels, cut to the entries below each pixel's stored last index (one
+// low-bits mask, render.cpp:238-257 walks [0, last)); an OR-reduction gives
+// the entries the warp visits, back to front.  Records are staged at their
+// list offset (no compaction), and the per-slot written-flag is set by the
+// ring flush.  Per pixel and per partial the operations and their order are
+// those of k_raster_vjp_staged3: the partials are bit-identical.
+template <int WPB, int kMinB = 10>
+__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
+    k_raster_vjp_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                      const double* __restrict__ adj, const double* __restrict__ tfinal,
+                      const int* __restrict__ last, double* __restrict__ part,
+                      unsigned char* __restrict__ mask) {
+    constexpr int SUB = 4 / WPB;
+    constexpr int kRing = 3;  // 27 columns: one per lane
+    __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
+    __shared__ long long s_ring_out[WPB][kRing];
+    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ int s_slot[WPB][32];
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
+    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
+    const int px = bx0 + (lane & 7);
+    const int py0 = by0 + (lane >> 3);
+    const double pxc = px + 0.5;
+    const double pyc[2] = {py0 + 0.5, py0 + 4.5};
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H;
+    double u0[2], u1[2], u2[2], T[2], ub[2];
+    int lastp[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = py0 + 4 * k;
+        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
+        lastp[k] = 0;
+        if (px < W && py < H) {
+            const long long p = (long long)py * W + px;
+            u0[k] = adj[p];
+            u1[k] = adj[P + p];
+            u2[k] = adj[2 * P + p];
+            T[k] = tfinal[p];
+            lastp[k] = last[p];
+            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
+        }
+        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
+    }
+    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
+    StagedRec* my_rec = s_rec[lw];
+    int* my_slot = s_slot[lw];
+    double(*ring)[kRedStride] = s_ring[lw];
+    long long* ring_out = s_ring_out[lw];
+    int nring = 0;  // warp-uniform
+    // sum the parked columns (lane = fragment * 9 + adjoint), write them and
+    // flag the slots
+    auto flush = [&](int n) {
+        __syncwarp();
+        if (lane < n * kAdj) {
+            const double* col = ring[lane];
+            double t0 = col[0], t1 = col[11], t2 = col[22];
+#pragma unroll
+            for (int k = 1; k < 11; ++k) {
+                t0 += col[k];
+                t1 += col[11 + k];
+                if (k < 10) t2 += col[22 + k];
+            }
+            const int fe = lane / kAdj, c = lane - fe * kAdj;
+            double v = (t0 + t1) + t2;
+            if (c == 2 || c == 4) v *= -0.5;
+            if (c == 3) v = -v;
+            const long long slot = ring_out[fe] * kVjpSlots + warp;
+            part[slot * kAdj + c] = v;
+            if (c == 0) mask[slot] = 1;
+        }
+        __syncwarp();
+    };
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        const int jj = base + lane;
+        unsigned long long slots = 0ull;
+        if (jj < top) {
+            slots = block_slots(__ldg(tl.trect + jj), bx0, by0, 8);
+            if (slots) {
+                const double2* r2 = reinterpret_cast<const double2*>(
+                    rec + (long long)kRec * __ldg(tl.tile_ids + jj));
+                const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
+                const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
+                double2* o = reinterpret_cast<double2*>(my_rec + lane);
+                o[0] = a;
+                o[1] = b;
+                o[2] = c;
+                o[3] = d;
+                o[4] = e;
+                my_slot[lane] = __ldg(tl.sorted_d + jj);
+            }
+        }
+        // bit j of m[k]: entry base + j covers pixel k and lies below its
+        // stored last index
+        unsigned m[2] = {warp_transpose32((unsigned)slots),
+                         warp_transpose32((unsigned)(slots >> 32))};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int lim = min(max(start + lastp[k] - base, 0), 32);
+            m[k] &= lim >= 32 ? ~0u : ((1u << lim) - 1u);
+        }
+        const unsigned w0 = __reduce_or_sync(kFull, m[0]), w1 = __reduce_or_sync(kFull, m[1]);
+        unsigned wb = w0 | w1;
+        __syncwarp();
+        while (wb) {
+            const int e = 31 - __clz(wb);  // back to front
+            wb &= ~(1u << e);
+            const bool any0 = (w0 >> e) & 1u, any1 = (w1 >> e) & 1u;
+            bool lv[2] = {(bool)((m[0] >> e) & 1u), (bool)((m[1] >> e) & 1u)};
+            const StagedRec r = my_rec[e];
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            // one pixel's contribution given its falloff (render.cpp:238-283)
+            auto accumulate = [&](int k, double dx, double dy, double ax, double ay, double gauss,
+                                  double abar, bool clamped, double rom) {
+                contrib = true;
+                const double t_in = T[k] * rom;
+                const double at = abar * t_in;
+                g[6] += u0[k] * at;
+                g[7] += u1[k] * at;
+                g[8] += u2[k] * at;
+                const double uc = u0[k] * r.c0 + u1[k] * r.c1 + u2[k] * r.c2;
+                const double dab = uc * t_in - ub[k] * rom;
+                ub[k] += uc * at;
+                if (!clamped) {
+                    g[5] += gauss * dab;
+                    const double de = abar * dab;
+                    g[2] += de * (dx * dx);  // x -1/2 at the write
+                    g[3] += de * (dx * dy);  // x -1
+                    g[4] += de * (dy * dy);  // x -1/2
+                    g[0] += de * ax;
+                    g[1] += de * ay;
+                }
+                T[k] = t_in;
+            };
+            const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                  r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+            const double dx = pxc - r.mx;
+            if (any0 && any1) {
+                double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
+                bool cl[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    dy[k] = pyc[k] - r.my;
+                    gauss[k] = fast_exp_neg(eval_expo(dx, dy[k], f, ax[k], ay[k]));
+                    abar[k] = __dmul_rn(r.alpha, gauss[k]);
+                    cl[k] = abar[k] >= ro.alpha_clamp;
+                    if (cl[k]) abar[k] = ro.alpha_clamp;
+                    lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
+                    rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if (lv[k])
+                        accumulate(k, dx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k], rom[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
+                    const double dy = pyc[k] - r.my;
+                    double ax, ay;
+                    const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
+                    double abar = __dmul_rn(r.alpha, gauss);
+                    const bool clamped = abar >= ro.alpha_clamp;
+                    if (clamped) abar = ro.alpha_clamp;
+                    if (abar < ro.alpha_skip) continue;
+                    accumulate(k, dx, dy, ax, ay, gauss, abar, clamped,
+                               rcp_unit(__dsub_rn(1.0, abar)));
+                }
+            }
+            const unsigned cm = __ballot_sync(kFull, contrib);
+            if (cm == 0u) continue;
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) ring[nring * kAdj + c][lane] = g[c];
+            if (lane == 0) ring_out[nring] = my_slot[e];
+            if (++nring == kRing) {
+                flush(kRing);
+                nring = 0;
+            }
+        }
+        __syncwarp();
+    }
+    if (nring) flush(nring);
+}
+
 // ------------------------------------------------------------------ K12 (raster)
 template <bool kWarpCull>
 __global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
@@ -1121,8 +1450,8 @@ int knob(const char* name, int dflt) {
 }
 const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
 const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
-const int g_fwd_warp = knob("SGTR_FWD_WARP", 4);
-const int g_vjp_staged = knob("SGTR_VJP_STAGED", 3);
+const int g_fwd_warp = knob("SGTR_FWD_WARP", 5);
+const int g_vjp_staged = knob("SGTR_VJP_STAGED", 4);
 const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", g_vjp_mode == 1 ? 10 : 3);
 const int g_jvp_warp = knob("SGTR_JVP_WARP", 2);
 
@@ -1136,6 +1465,8 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (counters)
         k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
                                                           counters);
+    else if (g_fwd_warp == 5)  // one-warp CTAs, hit bitmasks
+        k_raster_fwd_bits<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_warp == 4)  // one-warp CTAs: each retires as soon as its block is done
         k_raster_fwd_paired<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     else if (g_fwd_warp == 2)
@@ -1180,6 +1511,9 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
         else
             k_raster_vjp_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                           part, mask);
+    } else if (g_vjp_staged == 4) {  // one-warp CTAs, hit bitmasks
+        k_raster_vjp_bits<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                   mask);
     } else if (g_vjp_min_blocks == 8) {
         k_raster_vjp_staged3<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
                                                           part, mask);
