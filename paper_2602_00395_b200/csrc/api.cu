@@ -380,7 +380,7 @@ struct Ctx {
     Prefetcher prefetch;
     // per-view workspace
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
-    Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp, slots;
+    Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
     Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, id_rank, okeys,
         ovals, otemp;
@@ -396,7 +396,7 @@ struct Ctx {
         DevStatus* hstat = nullptr;
 #define SGTR_LANE_BUFS(X)                                                                    \
     X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
-    X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp) X(slots)    \
+    X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp)             \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
     X(part) X(mask) X(tmask) X(large) X(trect) X(id_rank) X(okeys) X(ovals) X(otemp)
 #define SGTR_DECL(n) Buf n;
@@ -623,51 +623,22 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
 void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender& vr, int mode,
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
     const long long nd = std::max(vr.n_dup, 1LL);
-    if (vjp_mode() == 1) {
-        double* part = c.part.as<double>((size_t)kVjpSlots * kAdj * nd);
-        unsigned char* mask = c.mask.as<unsigned char>((size_t)kVjpSlots * nd);
-        {
-            Timed t(c, KC_RASTER_VJP);
-            SGTR_CUDA(cudaMemsetAsync(mask, 0, (size_t)kVjpSlots * nd, c.st));
-            launch_raster_vjp_warp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
-                                   c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(),
-                                   part, mask);
-        }
-        Timed t(c, KC_CHAIN);
-        if (chain_mode() == 1) {
-            double* slots = c.slots.as<double>((size_t)kAdj * nd);
-            launch_partials_to_slots(c.st, vr.tl.sorted_d, vr.n_dup, part, mask, slots);
-            launch_chain(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                         c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits,
-                         acc, flag);
-            c.launches += 3;
-            return;
-        }
-        // SGTR_CHAIN_MODE=2: separate partial-sum kernel (K11a) before the
-        // chain (measured slower than the fused form, kept as an option)
-        double* adj9 = chain_mode() == 2
-                           ? c.slots.as<double>((size_t)kAdj * std::max(vr.n_visible, 1))
-                           : nullptr;
-        int* rank = c.id_rank.as<int>(std::max(c.K, 1));
-        launch_rank_of(c.st, c.ids_alt.get<int>(), c.K, rank);
-        launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                          c.off_r.get<long long>(), c.tcount.get<int>(), rank, part,
-                          mask, zdense, zbits, acc, flag, adj9);
-        c.launches += adj9 ? 4 : 3;
-        return;
-    }
-    double* slots = c.slots.as<double>((size_t)kAdj * nd);
-    if (vr.tl.row0 != 0 || vr.tl.row1 != vr.tl.tiles_y)  // a band: other tiles' slots stay 0
-        SGTR_CUDA(cudaMemsetAsync(slots, 0, sizeof(double) * kAdj * nd, c.st));
+    double* part = c.part.as<double>((size_t)kVjpSlots * kAdj * nd);
+    unsigned char* mask = c.mask.as<unsigned char>((size_t)kVjpSlots * nd);
     {
         Timed t(c, KC_RASTER_VJP);
-        launch_raster_vjp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
-                          c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(), slots);
+        SGTR_CUDA(cudaMemsetAsync(mask, 0, (size_t)kVjpSlots * nd, c.st));
+        launch_raster_vjp_warp(c.st, vr.tl, c.rec.get<double>(), vr.W, vr.H, ro,
+                               c.adj.get<double>(), c.tfin.get<double>(), c.last.get<int>(), part,
+                               mask);
     }
     Timed t(c, KC_CHAIN);
-    launch_chain(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                 c.off_r.get<long long>(), c.tcount.get<int>(), slots, zdense, zbits, acc, flag);
-    c.launches += 2;
+    int* rank = c.id_rank.as<int>(std::max(c.K, 1));
+    launch_rank_of(c.st, c.ids_alt.get<int>(), c.K, rank);
+    launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
+                      c.off_r.get<long long>(), c.tcount.get<int>(), rank, part, mask, zdense,
+                      zbits, acc, flag);
+    c.launches += 3;
 }
 
 struct SsimOut {

@@ -25,16 +25,6 @@ void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& 
 void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                         const RenderP& ro, const double* v, const uint32_t* zbits,
                         double* trec);
-// K11: segmented reduce of the (tile, fragment) adjoint slots of each visible
-// splat, then the chain through projection + invert2x2.  mode 0 adds the
-// gradient into acc; mode 1 adds z (.) contribution (Hutchinson).
-// The probe is dense (zdense) or packed bits (zbits); a non-finite
-// contribution stores 1.0 into *nonfinite_flag.
-void launch_chain(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
-                  const RenderP& ro, const int* sorted_ids, int n_visible,
-                  const long long* off_r, const int* tcount, const double* slots,
-                  const double* zdense, const uint32_t* zbits, double* acc,
-                  double* nonfinite_flag);
 
 // ---------------------------------------------------------------- binning.cu
 struct BinBuffers {
@@ -88,18 +78,16 @@ void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_e
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, double* img, double* tfinal, int* last,
                        unsigned long long* counters = nullptr);
-// K10: back-to-front adjoint sweep -> 9 adjoints per (tile, fragment) slot
-void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
-                       int H, const RenderP& ro, const double* adj, const double* tfinal,
-                       const int* last, double* slots);
-// K10 (barrier-free form): each warp walks its tile's list alone and writes
-// its reduced adjoints to part[(j * 8 + warp) * 9 ...], flagging mask[j * 8 +
-// warp]; mask must be zeroed first.  Used when launch_vjp_mode() == 1.
-int vjp_mode();
+// K10: back-to-front adjoint sweep; each warp (one 8x8 block of a tile)
+// writes its reduced adjoints of duplicate d to part[(d * 4 + block) * 9 ...]
+// and flags mask[d * 4 + block]; mask must be zeroed first
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
-// K11 over the per-warp partials of the barrier-free K10
+// K11: per splat, the sum of its flagged K10 partials (duplicate, block order)
+// and the chain through invert2x2 and the projection; mode 0 adds the
+// gradient into acc, mode 1 z (.) it (Hutchinson, probe dense or as bits); a
+// non-finite contribution stores 1.0 into *nonfinite_flag.
 // splat id -> depth rank (inverse of the depth order), for launch_chain_warp's inv
 void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank);
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
@@ -107,12 +95,7 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb
                        const long long* off_r, const int* tcount,
                        const int* inv,  // splat id -> depth rank: id-order threads (or null)
                        const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag,
-                       double* adj9 = nullptr);  // adj9 (9 x n_visible): split K11a/K11b
-// per-warp partials of the barrier-free K10 -> per-duplicate slots (warp order)
-void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
-                              const double* part, const unsigned char* mask, double* slots);
-int chain_mode();
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag);
 // tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j, tbox[j] = the
 // splat's bbox rounded outward to float
 void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,

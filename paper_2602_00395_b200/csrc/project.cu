@@ -228,109 +228,11 @@ __device__ __forceinline__ void chain_sh(const double* x, int K, int nb, int id,
 }
 
 // K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
-// the fixed-order sum of its (tile, fragment) slots; the transpose of the 5x10
-// Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
-// reference evaluates with 10 dual seeds, is applied in one reverse sweep.
-__global__ void __launch_bounds__(128) k_chain(int mode, const double* __restrict__ x, int K,
-                                               int nb, DevCam cam, RenderP ro,
-                                               const int* __restrict__ sorted_ids, int n_visible,
-                                               const long long* __restrict__ off_r,
-                                               const int* __restrict__ tcount,
-                                               const double* __restrict__ slots,
-                                               const double* __restrict__ zdense,
-                                               const uint32_t* __restrict__ zbits,
-                                               double* __restrict__ acc,
-                                               double* nonfinite_flag) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_visible) return;
-    const int id = sorted_ids[r];
-    const int cnt = tcount[id];
-    if (cnt == 0) return;
-    double a[kAdj];
-#pragma unroll
-    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
-    const double* sl = slots + (long long)kAdj * off_r[r];
-    for (int t = 0; t < cnt; ++t) {
-#pragma unroll
-        for (int j = 0; j < kAdj; ++j) a[j] += sl[(long long)kAdj * t + j];
-    }
-    const long long k = K;
-    bool finite = true;
-    auto add = [&](long long idx, double v) {
-        if (mode == 1) v = probe_at(zdense, zbits, idx) * v;
-        finite = finite && isfinite(v);
-        acc[idx] += v;
-    };
-    add(10 * k + id, a[5]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
-    const bool sh = nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
-    double gmu_sh[3] = {0.0, 0.0, 0.0};
-    if (sh) chain_sh(x, K, nb, id, cam, load_splat(x, K, id), a, add, gmu_sh);
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
-    if (any) {
-        // J^T a for (mu, s, q) in one reverse sweep (geometry.cuh)
-        const Splat p = load_splat(x, K, id);
-        double gmu[3], gs[3], gq[4];
-        chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, sh ? gmu_sh[c] + gmu[c] : gmu[c]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
-    } else if (sh) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu_sh[c]);
-    }
-    if (!finite) *nonfinite_flag = 1.0;  // idempotent store
-}
-
-// K11: render.cpp:288-329 restated per splat.  The 9 adjoints of a splat are
-// the fixed-order sum of its (tile, fragment) slots; the transpose of the 5x10
-// Jacobian of (mu2d, inverse covariance) w.r.t. (mu, s, q), which the
-// reference evaluates with 10 dual seeds, is applied in one reverse sweep.
-// K11a: per visible splat (depth rank r), the sum over its duplicates (in
-// K4 order) of the per-warp partials flagged in mask (warp order), stored
-// component-major adj9[c * n_visible + r].  Few registers and no FP64 math,
-// so enough warps are resident to hide the scattered partial loads.
-__global__ void __launch_bounds__(256) k_sum_adjoints(const int* __restrict__ sorted_ids,
-                                                      int n_visible,
-                                                      const long long* __restrict__ off_r,
-                                                      const int* __restrict__ tcount,
-                                                      const int* __restrict__ inv,
-                                                      const double* __restrict__ part,
-                                                      const unsigned char* __restrict__ mask,
-                                                      double* __restrict__ adj9) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_visible) return;
-    const int cnt = tcount[sorted_ids[r]];
-    double a[kAdj];
-#pragma unroll
-    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
-    const long long off = off_r[r];
-    for (int t = 0; t < cnt; ++t) {
-        const long long d = off + t;  // partials are stored by splat-major slot
-        const unsigned m = *reinterpret_cast<const unsigned*>(mask + kVjpSlots * d);
-        if (m == 0u) continue;
-        const double* pp = part + d * kVjpSlots * kAdj;
-#pragma unroll
-        for (int w = 0; w < kVjpSlots; ++w) {
-            if ((m >> (8 * w)) & 0xffu) {
-#pragma unroll
-                for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
-            }
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < kAdj; ++c) adj9[(long long)c * n_visible + r] = a[c];
-}
-
-// K11b: the chain of each visible splat from its summed adjoints
-// (kPre) or, without kPre, summing the partials itself (one kernel)
-template <bool kPre, bool kSH>
+// the fixed-order sum of its K10 partials (duplicate, block order); the
+// transpose of the 5x10 Jacobian of (mu2d, inverse covariance) w.r.t.
+// (mu, s, q), which the reference evaluates with 10 dual seeds, is applied in
+// one reverse sweep (geometry.cuh: chain_reverse).
+template <bool kSH>
 __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
                                                const int* __restrict__ sorted_ids, int n_visible,
@@ -341,7 +243,6 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
                                                const unsigned char* __restrict__ mask,
                                                const double* __restrict__ zdense,
                                                const uint32_t* __restrict__ zbits,
-                                               const double* __restrict__ adj9,
                                                double* __restrict__ acc,
                                                double* nonfinite_flag) {
     // with inv (splat id -> depth rank) the threads run in splat-id order, so
@@ -357,13 +258,13 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     const int r = inv ? inv[id] : t;
     double a[kAdj];
 #pragma unroll
-    for (int j = 0; j < kAdj; ++j) a[j] = kPre ? adj9[(long long)j * n_visible + r] : 0.0;
+    for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
     // the <= 4 per-warp partials of each duplicate, in (duplicate, warp)
     // order; the partials are stored by splat-major duplicate slot, so a
     // splat's are one contiguous run of 288-byte records; masks of 4
     // duplicates (4 bytes each) are fetched together
     const long long off = off_r[r];
-    for (int t0 = 0; t0 < (kPre ? 0 : cnt); t0 += 4) {
+    for (int t0 = 0; t0 < cnt; t0 += 4) {
         long long jp[4];
         unsigned mk[4];
 #pragma unroll
@@ -418,33 +319,6 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
 
-// per tile-sorted position j: the duplicate's 9 adjoints are the sum of the
-// per-warp partials flagged in mask[j] (warp order), stored at slot
-// sorted_d[j] so that K11 reads each splat's slots contiguously
-__global__ void __launch_bounds__(256) k_partials_to_slots(const int* __restrict__ sorted_d,
-                                                           long long n,
-                                                           const double* __restrict__ part,
-                                                           const unsigned char* __restrict__ mask,
-                                                           double* __restrict__ slots) {
-    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // splat-major slot
-    if (d >= n) return;
-    const unsigned m = *reinterpret_cast<const unsigned*>(mask + kVjpSlots * d);
-    double a[kAdj];
-#pragma unroll
-    for (int c = 0; c < kAdj; ++c) a[c] = 0.0;
-    const double* pp = part + d * kVjpSlots * kAdj;
-#pragma unroll
-    for (int w = 0; w < kVjpSlots; ++w)
-        if ((m >> (8 * w)) & 0xffu) {
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
-        }
-    double* o = slots + (long long)kAdj * d;
-#pragma unroll
-    for (int c = 0; c < kAdj; ++c) o[c] = a[c];
-}
-
-// splat id -> depth rank (the inverse of K2's order), for K11's id-order walk
 __global__ void k_rank_of(const int* __restrict__ sorted_ids, int K, int* __restrict__ rank) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < K) rank[sorted_ids[r]] = r;
@@ -455,13 +329,6 @@ __global__ void k_rank_of(const int* __restrict__ sorted_ids, int K, int* __rest
 void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank) {
     if (K == 0) return;
     k_rank_of<<<ceil_div(K, 256), 256, 0, st>>>(sorted_ids, K, rank);
-    SGTR_CUDA(cudaGetLastError());
-}
-
-void launch_partials_to_slots(cudaStream_t st, const int* sorted_d, long long n,
-                              const double* part, const unsigned char* mask, double* slots) {
-    if (n == 0) return;
-    k_partials_to_slots<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, n, part, mask, slots);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -494,48 +361,22 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const D
 }
 
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb,
-                       const DevCam& cam,
-                       const RenderP& ro, const int* sorted_ids, int n_visible,
+                       const DevCam& cam, const RenderP& ro, const int* sorted_ids, int n_visible,
                        const long long* off_r, const int* tcount, const int* inv,
                        const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag,
-                       double* adj9) {
+                       const uint32_t* zbits, double* acc, double* nonfinite_flag) {
     if (n_visible == 0) return;
     const int nt = inv ? K : n_visible;  // threads: splat ids or depth ranks
-    if (adj9) {
-        k_sum_adjoints<<<ceil_div(n_visible, 256), 256, 0, st>>>(sorted_ids, n_visible, off_r,
-                                                                  tcount, inv, part, mask, adj9);
-        SGTR_CUDA(cudaGetLastError());
-        if (nb)
-            k_chain_warp<true, true><<<ceil_div(nt, 128), 128, 0, st>>>(
-                mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
-                zdense, zbits, adj9, acc, nonfinite_flag);
-        else
-            k_chain_warp<true, false><<<ceil_div(nt, 128), 128, 0, st>>>(
-                mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask,
-                zdense, zbits, adj9, acc, nonfinite_flag);
-    } else if (nb) {
-        k_chain_warp<false, true><<<ceil_div(nt, 128), 128, 0, st>>>(
+    if (nb)
+        k_chain_warp<true><<<ceil_div(nt, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
-            zbits, nullptr, acc, nonfinite_flag);
-    } else {
-        k_chain_warp<false, false><<<ceil_div(nt, 128), 128, 0, st>>>(
+            zbits, acc, nonfinite_flag);
+    else
+        k_chain_warp<false><<<ceil_div(nt, 128), 128, 0, st>>>(
             mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
-            zbits, nullptr, acc, nonfinite_flag);
-    }
+            zbits, acc, nonfinite_flag);
     SGTR_CUDA(cudaGetLastError());
 }
 
-void launch_chain(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
-                  const RenderP& ro, const int* sorted_ids, int n_visible,
-                  const long long* off_r, const int* tcount, const double* slots,
-                  const double* zdense, const uint32_t* zbits, double* acc,
-                  double* nonfinite_flag) {
-    if (n_visible == 0) return;
-    k_chain<<<ceil_div(n_visible, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, sorted_ids,
-                                                       n_visible, off_r, tcount, slots, zdense,
-                                                       zbits, acc, nonfinite_flag);
-    SGTR_CUDA(cudaGetLastError());
-}
 
 }  // namespace sgtr

@@ -1,15 +1,18 @@
 // raster.cu — tile rasteriser: K7 forward blend, K10 reverse-order VJP,
 // K12 forward-mode JVP.
 //
-// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
-// block so that the per-fragment bounding-box test can first be done once per
-// warp (uniform branch) against the block's span of pixel centres — most
-// (pixel, fragment) pairs of a tile list fail the reference's bbox test
-// (render.cpp:129-131), and whole warps skip them.  The tile's fragment list
-// (depth order, from binning.cu) is staged through shared memory in batches;
-// each 128-byte fragment record is copied by 8 lanes (one full cache line per
-// record, 4 records per warp instruction), and every pixel reads the staged
-// record as a warp-wide broadcast.
+// Tiles are 16x16 pixels with per-tile fragment lists in depth order
+// (binning.cu).  K7 and K10 run one-warp CTAs, each warp owning one block of
+// its tile (K7: 8x4 pixels, one per lane; K10: 8x8, two per lane, rows r and
+// r + 4) and walking the tile list on its own, 32 entries per batch: the lane
+// of list entry base + j tests that entry's exact pixel rectangle (K1's
+// pixel_range of the FP64 bbox) against the block as a bit mask of covered
+// pixels, stages the fragment's raster fields into warp-private shared
+// memory, and a warp bit-transpose hands every pixel lane the set of batch
+// entries covering it.  The warp visits only entries covering a pixel still
+// in play, reading each staged record as a broadcast.  K12 stages batches
+// per warp the same way with per-pixel rectangle tests.  k_raster_count is
+// the one-thread-per-pixel CTA form kept for the E/C work counters.
 //
 // Branch parity: the three kernels evaluate the primal alpha with the same
 // pinned operation sequence (eval_expo's FMA form and fastexp.cuh's exp, a
@@ -31,8 +34,6 @@ namespace {
 
 constexpr int kThreads = kTilePixels;  // 256
 constexpr int kFwdBatch = 256;
-constexpr int kVjpBatch = 64;
-constexpr int kJvpBatch = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -135,31 +136,6 @@ __device__ __forceinline__ unsigned long long block_slots(int4 r, int ix0, int i
     return cols & rowm;
 }
 
-// Warp-level contribution filter (after warp_misses): false only when no
-// pixel centre of the warp's 8x4 block can reach alpha_bar >= alpha_skip —
-// the minimum of q = d^T Sigma^-1 d over the block is certainly above
-// rho2 (same bound as geometry.cuh:ellipse_may_hit, with the edge-minimiser
-// slopes precomputed in the record).  Warp-uniform.
-__device__ __forceinline__ bool warp_may_hit(const PixelCtx& p, const double* f) {
-    const double rho2 = f[R_RHO2];
-    if (!(rho2 < INFINITY)) return true;
-    if (rho2 < 0.0) return false;
-    const double ax = p.wx0 - f[R_MX], bx = p.wx1 - f[R_MX];
-    const double ay = p.wy0 - f[R_MY], by = p.wy1 - f[R_MY];
-    if (ax <= 0.0 && bx >= 0.0 && ay <= 0.0 && by >= 0.0) return true;
-    const double i00 = f[R_I00], i01 = f[R_I01], i11 = f[R_I11];
-    const double k11 = f[R_K11], k00 = f[R_K00];
-    auto q = [&](double dx, double dy) { return i00 * dx * dx + 2.0 * i01 * dx * dy + i11 * dy * dy; };
-    auto cl = [](double v, double lo, double hi) { return fmin(fmax(v, lo), hi); };
-    double qmin = q(ax, cl(-k11 * ax, ay, by));
-    qmin = fmin(qmin, q(bx, cl(-k11 * bx, ay, by)));
-    qmin = fmin(qmin, q(cl(-k00 * ay, ax, bx), ay));
-    qmin = fmin(qmin, q(cl(-k00 * by, ax, bx), by));
-    const double mxd = fmax(fabs(ax), fabs(bx)), myd = fmax(fabs(ay), fabs(by));
-    const double bound = fabs(i00) * mxd * mxd + fabs(i11) * myd * myd + 2.0 * fabs(i01) * mxd * myd;
-    return !(qmin > rho2 + 1e-8 * rho2 + 1e-11 * bound + 1e-11);
-}
-
 // cooperative staging: 8 lanes per 128-byte record; entries [b, b+n) of the
 // tile-sorted list go to s_rec[0, n)
 __device__ __forceinline__ void stage_records(const TileLists& tl, const double* __restrict__ rec,
@@ -175,24 +151,13 @@ __device__ __forceinline__ void stage_records(const TileLists& tl, const double*
     }
 }
 
-__device__ __forceinline__ void stage_tangents(const TileLists& tl, const double* __restrict__ trec,
-                                               int b, int n, double* s_t) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane >> 3, chunk = lane & 7;
-    for (int e = warp * 4 + sub; e < n; e += kWarps * 4) {
-        if (chunk >= kTRec / 2) continue;
-        const int id = tl.dup_id[tl.sorted_d[b + e]];
-        const double2 v = reinterpret_cast<const double2*>(trec + (long long)kTRec * id)[chunk];
-        reinterpret_cast<double2*>(s_t + kTRec * e)[chunk] = v;
-    }
-}
-
-// ------------------------------------------------------------------ K7
-// kCount: also count the (pixel, fragment) pairs reaching the alpha
-// evaluation (E) and the contributing ones (C), the algorithmic-work units
-// of SURVEY §8(d); used outside timed regions only.
-template <bool kCount, bool kWarpCull>
-__global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
+// ------------------------------------------------------------------ K7 counters
+// The forward blend one CTA per tile (one thread per pixel), counting the
+// (pixel, fragment) pairs reaching the alpha evaluation (E) and the
+// contributing ones (C): the algorithmic-work units of SURVEY §8(d), for the
+// bench's roofline; outside timed regions only.  Same per-pixel operations as
+// k_raster_fwd_bits.
+__global__ void __launch_bounds__(kThreads) k_raster_count(TileLists tl,
                                                          const double* __restrict__ rec, int W,
                                                          int H, RenderP ro,
                                                          double* __restrict__ img,
@@ -215,14 +180,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
         if (__all_sync(kFull, done)) continue;
         for (int jj = 0; jj < n; ++jj) {
             const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
+            if (warp_misses(pc, f)) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
                 double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
-                if (kCount) ++n_eval;
+                ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (!(abar < ro.alpha_skip)) {
-                    if (kCount) ++n_contrib;
+                    ++n_contrib;
                     const double w = abar * T;
                     c0 += f[R_C0] * w;
                     c1 += f[R_C1] * w;
@@ -237,15 +202,13 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
             if (__all_sync(kFull, done)) break;
         }
     }
-    if (kCount) {
-        for (int o = 16; o > 0; o >>= 1) {
-            n_eval += __shfl_xor_sync(kFull, n_eval, o);
-            n_contrib += __shfl_xor_sync(kFull, n_contrib, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(counters, n_eval);
-            atomicAdd(counters + 1, n_contrib);
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+        n_eval += __shfl_xor_sync(kFull, n_eval, o);
+        n_contrib += __shfl_xor_sync(kFull, n_contrib, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(counters, n_eval);
+        atomicAdd(counters + 1, n_contrib);
     }
     if (!pc.inside) return;
     const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
@@ -256,200 +219,10 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(TileLists tl,
     last[p] = processed;
 }
 
-// ------------------------------------------------------------------ K7, batch-staged
-// Each warp owns an 8x4 pixel block and walks its tile's list on its own, in
-// batches of 32 positions: each lane tests one position against the block and, if it
-// passes, loads that fragment's 9 raster fields into a warp-private shared
-// slot (ballot-compacted), so the 32 record fetches of a batch are in flight
-// together instead of one dependent fetch per blended entry.
+// the raster fields K7/K10/K12 stage per fragment (record fields 4..13)
 struct StagedRec {
     double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
 };
-
-template <int WPB>
-__global__ void __launch_bounds__(32 * WPB)
-    k_raster_fwd_staged(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                        double* __restrict__ img, double* __restrict__ tfinal,
-                        int* __restrict__ last) {
-    constexpr int SUB = kWarps / WPB;
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    bool done = !pc.inside;
-    int processed = end - start;
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    for (int base = start; base < end; base += 32) {
-        if (__all_sync(kFull, done)) break;
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < end) {
-            rr = __ldg(tl.trect + jj);
-            pass = rect_hits_warp(pc, rr);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-        }
-        __syncwarp();
-        const int n = __popc(m);
-        for (int e = 0; e < n; ++e) {
-            if (!done && rect_has_pixel(pc, my_rect[e])) {
-                const StagedRec r = my_rec[e];
-                const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
-                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
-                if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-                if (!(abar < ro.alpha_skip)) {
-                    const double w = abar * T;
-                    c0 += f[R_C0] * w;
-                    c1 += f[R_C1] * w;
-                    c2 += f[R_C2] * w;
-                    T = __dmul_rn(T, __dsub_rn(1.0, abar));
-                    if (T < ro.t_stop) {
-                        done = true;
-                        processed = my_pos[e] - start + 1;
-                    }
-                }
-            }
-            if (__all_sync(kFull, done)) break;
-        }
-        __syncwarp();
-    }
-    if (!pc.inside) return;
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    img[p] = c0 + ro.bg[0] * T;
-    img[P + p] = c1 + ro.bg[1] * T;
-    img[2 * P + p] = c2 + ro.bg[2] * T;
-    tfinal[p] = T;
-    last[p] = processed;
-}
-
-// ------------------------------------------------------------------ K7, batch-staged, paired entries
-// As k_raster_fwd_staged, blending the staged batch two entries at a time:
-// the two falloffs (exp polynomial, clamp, skip test) do not depend on the
-// blend state, so when both entries meet the warp's block they are computed
-// in one straight-line block — two independent FP64 dependency chains the
-// pipe interleaves — and then blended in list order, the second only if the
-// pixel did not stop at the first.  Per pixel the operations and their order
-// are those of k_raster_fwd_staged, so the outputs are bit-identical.
-template <int WPB>
-__global__ void __launch_bounds__(32 * WPB)
-    k_raster_fwd_paired(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                        double* __restrict__ img, double* __restrict__ tfinal,
-                        int* __restrict__ last) {
-    constexpr int SUB = kWarps / WPB;
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    const int tile =
-        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H, warp);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    bool done = !pc.inside;
-    int processed = end - start;
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    auto falloff = [&](const StagedRec& r) {
-        const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
-                              r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-        const double dx = pc.pxc - r.mx, dy = pc.pyc - r.my;
-        double abar = __dmul_rn(r.alpha, fast_exp_neg(eval_expo(dx, dy, f)));
-        if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
-        return abar;
-    };
-    auto blend = [&](const StagedRec& r, double abar, int e) {
-        const double w = abar * T;
-        c0 += r.c0 * w;
-        c1 += r.c1 * w;
-        c2 += r.c2 * w;
-        T = __dmul_rn(T, __dsub_rn(1.0, abar));
-        if (T < ro.t_stop) {
-            done = true;
-            processed = my_pos[e] - start + 1;
-        }
-    };
-    for (int base = start; base < end; base += 32) {
-        if (__all_sync(kFull, done)) break;
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < end) {
-            rr = __ldg(tl.trect + jj);
-            pass = rect_hits_warp(pc, rr);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-        }
-        __syncwarp();
-        const int n = __popc(m);
-        for (int e = 0; e < n; e += 2) {
-            const bool h0 = !done && rect_has_pixel(pc, my_rect[e]);
-            const bool h1 = e + 1 < n && !done && rect_has_pixel(pc, my_rect[e + 1]);
-            const bool a0 = __any_sync(kFull, h0), a1 = __any_sync(kFull, h1);
-            if (a0 && a1) {
-                const StagedRec r0 = my_rec[e], r1 = my_rec[e + 1];
-                const double ab0 = falloff(r0), ab1 = falloff(r1);
-                if (h0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, e);
-                if (h1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, e + 1);
-            } else if (a0 || a1) {
-                const int ee = a0 ? e : e + 1;
-                if (a0 ? h0 : h1) {
-                    const StagedRec r = my_rec[ee];
-                    const double ab = falloff(r);
-                    if (!(ab < ro.alpha_skip)) blend(r, ab, ee);
-                }
-            }
-            if (__all_sync(kFull, done)) break;
-        }
-        __syncwarp();
-    }
-    if (!pc.inside) return;
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    img[p] = c0 + ro.bg[0] * T;
-    img[P + p] = c1 + ro.bg[1] * T;
-    img[2 * P + p] = c2 + ro.bg[2] * T;
-    tfinal[p] = T;
-    last[p] = processed;
-}
 
 // ------------------------------------------------------------------ K7, hit bitmasks
 // The per-pixel bbox test of every (entry, pixel) pair is done once per batch
@@ -551,528 +324,7 @@ __global__ void __launch_bounds__(32 * WPB)
     last[p] = processed;
 }
 
-// ------------------------------------------------------------------ K10
-// Transposed butterfly: sums g[0..7] over the warp so that lane l with
-// (l & 3) == 0 ends with the total of g[l >> 2] (9 shuffles instead of 40),
-// and g[8] with a plain butterfly (lane 0 keeps it).  Fixed order, so the
-// result is deterministic.
-__device__ __forceinline__ void warp_reduce9(double* g, int lane, double& v_lane, double& v8) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    double h4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double send = b4 ? g[i] : g[4 + i];
-        const double keep = b4 ? g[4 + i] : g[i];
-        h4[i] = keep + __shfl_xor_sync(kFull, send, 16);
-    }
-    double h2[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double send = b3 ? h4[i] : h4[2 + i];
-        const double keep = b3 ? h4[2 + i] : h4[i];
-        h2[i] = keep + __shfl_xor_sync(kFull, send, 8);
-    }
-    {
-        const double send = b2 ? h2[0] : h2[1];
-        const double keep = b2 ? h2[1] : h2[0];
-        v_lane = keep + __shfl_xor_sync(kFull, send, 4);
-    }
-    v_lane += __shfl_xor_sync(kFull, v_lane, 2);
-    v_lane += __shfl_xor_sync(kFull, v_lane, 1);
-    double s = g[8];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    v8 = s;
-}
-
-// Warp reduction of 9 doubles through a warp-private shared scratch: lanes
-// store their 9 values (component-major, padded stride 33), 27 lanes each sum
-// an 11-lane third of one component, 9 lanes add the three thirds and write
-// the totals to out[0..8].  ~40 instructions instead of the shuffle
-// butterfly's selects and shuffles; fixed order, so deterministic.
 constexpr int kRedStride = 33;
-constexpr int kRedScratch = kAdj * kRedStride + 27;
-__device__ __forceinline__ void warp_reduce9_smem(const double* g, int lane, double* scr,
-                                                  double* out) {
-#pragma unroll
-    for (int c = 0; c < kAdj; ++c) scr[c * kRedStride + lane] = g[c];
-    __syncwarp();
-    if (lane < 27) {
-        const int c = lane / 3, q = lane % 3;
-        const double* col = scr + c * kRedStride + q * 11;
-        const int n = q == 2 ? 10 : 11;
-        double s = col[0];
-        for (int k = 1; k < n; ++k) s += col[k];
-        scr[kAdj * kRedStride + lane] = s;
-    }
-    __syncwarp();
-    if (lane < kAdj) {
-        const double* t = scr + kAdj * kRedStride + 3 * lane;
-        out[lane] = (t[0] + t[1]) + t[2];
-    }
-    __syncwarp();
-}
-
-template <bool kWarpCull, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_raster_vjp(TileLists tl,
-                                                         const double* __restrict__ rec, int W,
-                                                         int H, RenderP ro,
-                                                         const double* __restrict__ adj,
-                                                         const double* __restrict__ tfinal,
-                                                         const int* __restrict__ last,
-                                                         double* __restrict__ slots) {
-    __shared__ __align__(16) double s_rec[kVjpBatch * kRec];
-    __shared__ double s_red[kWarps][kVjpBatch][kAdj];
-    __shared__ int s_d[kVjpBatch];
-    __shared__ unsigned s_mask[kVjpBatch];
-    __shared__ int s_maxlast[kWarps];
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    double u0 = 0, u1 = 0, u2 = 0, T = 0.0;
-    int lastp = 0;
-    if (pc.inside) {
-        u0 = adj[p];
-        u1 = adj[P + p];
-        u2 = adj[2 * P + p];
-        T = tfinal[p];
-        lastp = last[p];
-    }
-    // pixels with an all-zero adjoint are skipped (render.cpp:283)
-    const bool active = pc.inside && !(u0 == 0.0 && u1 == 0.0 && u2 == 0.0);
-    if (!active) lastp = 0;
-    double b0 = ro.bg[0] * T, b1 = ro.bg[1] * T, b2 = ro.bg[2] * T;  // "behind"
-    // entries past every pixel's last processed fragment get zero slots
-    const int wlast = __reduce_max_sync(kFull, lastp);
-    if (lane == 0) s_maxlast[warp] = wlast;
-    __syncthreads();
-    int ml = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) ml = max(ml, s_maxlast[w]);
-    const int hi = start + ml;
-    for (int j = hi + threadIdx.x; j < end; j += kThreads) {
-        double* s = slots + (long long)kAdj * tl.sorted_d[j];
-#pragma unroll
-        for (int c = 0; c < kAdj; ++c) s[c] = 0.0;
-    }
-    for (int bend = hi; bend > start; bend -= kVjpBatch) {
-        const int bstart = max(start, bend - kVjpBatch);
-        const int n = bend - bstart;
-        __syncthreads();
-        stage_records(tl, rec, bstart, n, s_rec, s_d);
-        if (threadIdx.x < n) s_mask[threadIdx.x] = 0u;
-        __syncthreads();
-        for (int jj = n - 1; jj >= 0; --jj) {
-            const int rel = bstart - start + jj;
-            if (rel >= wlast) continue;
-            const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
-            double g[kAdj];
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-            bool contrib = false;
-            if (rel < lastp && !outside_bbox(pc.pxc, pc.pyc, f)) {
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double gauss = fast_exp_neg(eval_expo(dx, dy, f));
-                double abar = __dmul_rn(f[R_ALPHA], gauss);
-                const bool clamped = abar >= ro.alpha_clamp;
-                if (clamped) abar = ro.alpha_clamp;
-                if (!(abar < ro.alpha_skip)) {
-                    contrib = true;
-                    // one reciprocal for T_in = T / (1 - abar) and the three
-                    // behind / (1 - abar) terms (render.cpp:243-245)
-                    const double rom = 1.0 / __dsub_rn(1.0, abar);
-                    const double t_in = T * rom;
-                    const double at = abar * t_in;
-                    g[6] = u0 * at;
-                    g[7] = u1 * at;
-                    g[8] = u2 * at;
-                    const double dab = u0 * (f[R_C0] * t_in - b0 * rom) +
-                                       u1 * (f[R_C1] * t_in - b1 * rom) +
-                                       u2 * (f[R_C2] * t_in - b2 * rom);
-                    b0 += f[R_C0] * at;
-                    b1 += f[R_C1] * at;
-                    b2 += f[R_C2] * at;
-                    if (!clamped) {
-                        g[5] = gauss * dab;
-                        const double de = abar * dab;
-                        g[2] = de * (-0.5 * dx * dx);
-                        g[3] = de * (-dx * dy);
-                        g[4] = de * (-0.5 * dy * dy);
-                        g[0] = de * (f[R_I00] * dx + f[R_I01] * dy);
-                        g[1] = de * (f[R_I01] * dx + f[R_I11] * dy);
-                    }
-                    T = t_in;
-                }
-            }
-            if (!__any_sync(kFull, contrib)) continue;
-            double v, v8;
-            warp_reduce9(g, lane, v, v8);
-            if ((lane & 3) == 0) s_red[warp][jj][lane >> 2] = v;
-            if (lane == 0) {
-                s_red[warp][jj][8] = v8;
-                atomicOr(&s_mask[jj], 1u << warp);
-            }
-        }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < n * kAdj; idx += kThreads) {
-            const int jj = idx / kAdj, c = idx % kAdj;
-            const unsigned m = s_mask[jj];
-            double s = 0.0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w)
-                if (m & (1u << w)) s += s_red[w][jj][c];
-            slots[(long long)kAdj * s_d[jj] + c] = s;
-        }
-    }
-}
-
-// ------------------------------------------------------------------ K10, batch-staged, 2 px/lane
-// As k_raster_vjp_staged, but a warp owns an 8x8 block (lane: column
-// lane & 7, rows lane >> 3 and 4 + (lane >> 3)): one list walk, record fetch
-// and 9-value reduction per entry now serve 64 pixels, and the two pixels'
-// independent recurrences give each lane instruction-level parallelism.  A
-// tile is 4 such warps (partial slots 0..3 of the duplicate).
-template <int WPB, int kMinB = 10>
-__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
-    k_raster_vjp_staged2(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                         const double* __restrict__ adj, const double* __restrict__ tfinal,
-                         const int* __restrict__ last, double* __restrict__ part,
-                         unsigned char* __restrict__ mask) {
-    constexpr int SUB = 4 / WPB;
-    __shared__ double s_red[WPB][kRedScratch];
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    __shared__ int s_slot[WPB][32];
-    const int tile = blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;  // 0..3: 8x8 block of the tile
-    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
-    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
-    const int px = bx0 + (lane & 7);
-    const int start = tl.tile_start[tile];
-    const long long P = (long long)W * H;
-    // ub = u . behind: the adjoint-weighted colour composited behind the
-    // current fragment (the reference keeps the 3 channels, render.cpp:238-245;
-    // only this dot product enters dL/dalpha_bar)
-    double u0[2], u1[2], u2[2], T[2], ub[2];
-    int lastp[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int py = by0 + (lane >> 3) + 4 * k;
-        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
-        lastp[k] = 0;
-        if (px < W && py < H) {
-            const long long p = (long long)py * W + px;
-            u0[k] = adj[p];
-            u1[k] = adj[P + p];
-            u2[k] = adj[2 * P + p];
-            T[k] = tfinal[p];
-            lastp[k] = last[p];
-            // pixels with an all-zero adjoint are skipped (render.cpp:283)
-            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;
-        }
-        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
-    }
-    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    int* my_slot = s_slot[lw];
-    for (int top = start + wlast; top > start; top -= 32) {
-        const int base = max(start, top - 32);
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < top) {
-            rr = __ldg(tl.trect + jj);
-            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-            my_slot[q] = __ldg(tl.sorted_d + jj);
-        }
-        __syncwarp();
-        for (int e = __popc(m) - 1; e >= 0; --e) {
-            const int j = my_pos[e];
-            const int rel = j - start;
-            const int4 r4 = my_rect[e];
-            double g[kAdj];
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-            bool contrib = false;
-            const bool colin = px >= r4.x && px <= r4.z;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int py = by0 + (lane >> 3) + 4 * k;
-                if (!(rel < lastp[k] && colin && py >= r4.y && py <= r4.w)) continue;
-                const StagedRec r = my_rec[e];
-                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
-                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-                const double dx = (px + 0.5) - f[R_MX], dy = (py + 0.5) - f[R_MY];
-                double ax, ay;
-                const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
-                double abar = __dmul_rn(f[R_ALPHA], gauss);
-                const bool clamped = abar >= ro.alpha_clamp;
-                if (clamped) abar = ro.alpha_clamp;
-                if (abar < ro.alpha_skip) continue;
-                contrib = true;
-                const double rom = rcp_unit(__dsub_rn(1.0, abar));
-                const double t_in = T[k] * rom;
-                const double at = abar * t_in;
-                g[6] += u0[k] * at;
-                g[7] += u1[k] * at;
-                g[8] += u2[k] * at;
-                const double uc = u0[k] * f[R_C0] + u1[k] * f[R_C1] + u2[k] * f[R_C2];
-                const double dab = uc * t_in - ub[k] * rom;
-                ub[k] += uc * at;
-                if (!clamped) {
-                    g[5] += gauss * dab;
-                    const double de = abar * dab;
-                    g[2] += de * (-0.5 * dx * dx);
-                    g[3] += de * (-dx * dy);
-                    g[4] += de * (-0.5 * dy * dy);
-                    g[0] += de * ax;
-                    g[1] += de * ay;
-                }
-                T[k] = t_in;
-            }
-            const unsigned cm = __ballot_sync(kFull, contrib);
-            if (cm == 0u) continue;
-            const long long dslot = my_slot[e];
-            double* o = part + (dslot * kVjpSlots + warp) * kAdj;
-            warp_reduce9_smem(g, lane, s_red[lw], o);
-            if (lane == 0) mask[dslot * kVjpSlots + warp] = 1;
-        }
-        __syncwarp();
-    }
-}
-
-// ------------------------------------------------------------------ K10, batch-staged, 2 px/lane, interleaved
-// As k_raster_vjp_staged2, with three changes that leave every partial
-// bit-identical:
-//  * the two pixels' evaluations run in one straight-line block when both
-//    rows of the warp's block meet the fragment, so the two exp polynomials
-//    and reciprocals are independent dependency chains the FP64 pipe
-//    interleaves (with a branch per pixel the compiler serialises them); a
-//    pixel outside the fragment still runs the arithmetic (its lane would
-//    idle in the other branch anyway) and only its state updates are
-//    predicated off;
-//  * the conic adjoints accumulate de * dx^2, de * dx dy, de * dy^2 and take
-//    their factors -1/2, -1, -1/2 once at the write (scaling by a power of two
-//    commutes with rounding, so each running sum is the old one scaled);
-//  * the per-fragment warp reduction is deferred: lanes park their 9 values
-//    in a ring of kRing fragments and one flush sums 9 * kRing columns, one
-//    per lane, in the same order as warp_reduce9_smem ((0..10) + (11..21)) +
-//    (22..31) — a third of the reduction instructions per fragment.
-template <int WPB, int kMinB = 10>
-__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
-    k_raster_vjp_staged3(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
-                         const double* __restrict__ adj, const double* __restrict__ tfinal,
-                         const int* __restrict__ last, double* __restrict__ part,
-                         unsigned char* __restrict__ mask) {
-    constexpr int SUB = 4 / WPB;
-    constexpr int kRing = 3;  // 27 columns: one per lane
-    __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
-    __shared__ long long s_ring_out[WPB][kRing];
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
-    __shared__ int s_pos[WPB][32];
-    __shared__ int s_slot[WPB][32];
-    const int tile =
-        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
-    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
-    const int px = bx0 + (lane & 7);
-    const int py0 = by0 + (lane >> 3);
-    const double pxc = px + 0.5;
-    const double pyc[2] = {py0 + 0.5, py0 + 4.5};
-    const int start = tl.tile_start[tile];
-    const long long P = (long long)W * H;
-    double u0[2], u1[2], u2[2], T[2], ub[2];
-    int lastp[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int py = py0 + 4 * k;
-        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
-        lastp[k] = 0;
-        if (px < W && py < H) {
-            const long long p = (long long)py * W + px;
-            u0[k] = adj[p];
-            u1[k] = adj[P + p];
-            u2[k] = adj[2 * P + p];
-            T[k] = tfinal[p];
-            lastp[k] = last[p];
-            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
-        }
-        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
-    }
-    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
-    StagedRec* my_rec = s_rec[lw];
-    int4* my_rect = s_rect[lw];
-    int* my_pos = s_pos[lw];
-    int* my_slot = s_slot[lw];
-    double(*ring)[kRedStride] = s_ring[lw];
-    long long* ring_out = s_ring_out[lw];
-    int nring = 0;  // warp-uniform
-    // sum the parked columns (lane = fragment * 9 + adjoint) and write them
-    auto flush = [&](int n) {
-        __syncwarp();
-        if (lane < n * kAdj) {
-            const double* col = ring[lane];
-            double t0 = col[0], t1 = col[11], t2 = col[22];
-#pragma unroll
-            for (int k = 1; k < 11; ++k) {
-                t0 += col[k];
-                t1 += col[11 + k];
-                if (k < 10) t2 += col[22 + k];
-            }
-            const int fe = lane / kAdj, c = lane - fe * kAdj;
-            double v = (t0 + t1) + t2;
-            if (c == 2 || c == 4) v *= -0.5;
-            if (c == 3) v = -v;
-            part[(ring_out[fe] * kVjpSlots + warp) * kAdj + c] = v;
-        }
-        __syncwarp();
-    };
-    for (int top = start + wlast; top > start; top -= 32) {
-        const int base = max(start, top - 32);
-        const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
-        if (jj < top) {
-            rr = __ldg(tl.trect + jj);
-            pass = !(bx0 + 7 < rr.x || bx0 > rr.z || by0 + 7 < rr.y || by0 > rr.w);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const double2* r2 =
-                reinterpret_cast<const double2*>(rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-            const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-            const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
-            o[0] = a;
-            o[1] = b;
-            o[2] = c;
-            o[3] = d;
-            o[4] = e;
-            my_rect[q] = rr;
-            my_pos[q] = jj;
-            my_slot[q] = __ldg(tl.sorted_d + jj);
-        }
-        __syncwarp();
-        for (int e = __popc(m) - 1; e >= 0; --e) {
-            const int rel = my_pos[e] - start;
-            const int4 r4 = my_rect[e];
-            const bool colin = px >= r4.x && px <= r4.z;
-            bool lv[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int py = py0 + 4 * k;
-                lv[k] = rel < lastp[k] && colin && py >= r4.y && py <= r4.w;
-            }
-            const bool any0 = __any_sync(kFull, lv[0]), any1 = __any_sync(kFull, lv[1]);
-            if (!any0 && !any1) continue;
-            const StagedRec r = my_rec[e];
-            double g[kAdj];
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
-            bool contrib = false;
-            // one pixel's contribution given its falloff (render.cpp:238-283)
-            auto accumulate = [&](int k, double dx, double dy, double ax, double ay, double gauss,
-                                  double abar, bool clamped, double rom) {
-                contrib = true;
-                const double t_in = T[k] * rom;
-                const double at = abar * t_in;
-                g[6] += u0[k] * at;
-                g[7] += u1[k] * at;
-                g[8] += u2[k] * at;
-                const double uc = u0[k] * r.c0 + u1[k] * r.c1 + u2[k] * r.c2;
-                const double dab = uc * t_in - ub[k] * rom;
-                ub[k] += uc * at;
-                if (!clamped) {
-                    g[5] += gauss * dab;
-                    const double de = abar * dab;
-                    g[2] += de * (dx * dx);  // x -1/2 at the write
-                    g[3] += de * (dx * dy);  // x -1
-                    g[4] += de * (dy * dy);  // x -1/2
-                    g[0] += de * ax;
-                    g[1] += de * ay;
-                }
-                T[k] = t_in;
-            };
-            const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
-                                  r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-            const double dx = pxc - r.mx;
-            if (any0 && any1) {
-                double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
-                bool cl[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    dy[k] = pyc[k] - r.my;
-                    gauss[k] = fast_exp_neg(eval_expo(dx, dy[k], f, ax[k], ay[k]));
-                    abar[k] = __dmul_rn(r.alpha, gauss[k]);
-                    cl[k] = abar[k] >= ro.alpha_clamp;
-                    if (cl[k]) abar[k] = ro.alpha_clamp;
-                    lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
-                    rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
-                }
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    if (lv[k])
-                        accumulate(k, dx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k], rom[k]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
-                    const double dy = pyc[k] - r.my;
-                    double ax, ay;
-                    const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
-                    double abar = __dmul_rn(r.alpha, gauss);
-                    const bool clamped = abar >= ro.alpha_clamp;
-                    if (clamped) abar = ro.alpha_clamp;
-                    if (abar < ro.alpha_skip) continue;
-                    accumulate(k, dx, dy, ax, ay, gauss, abar, clamped,
-                               rcp_unit(__dsub_rn(1.0, abar)));
-                }
-            }
-            const unsigned cm = __ballot_sync(kFull, contrib);
-            if (cm == 0u) continue;
-#pragma unroll
-            for (int c = 0; c < kAdj; ++c) ring[nring * kAdj + c][lane] = g[c];
-            if (lane == 0) {
-                const long long dslot = my_slot[e];
-                ring_out[nring] = dslot;
-                mask[dslot * kVjpSlots + warp] = 1;
-            }
-            if (++nring == kRing) {
-                flush(kRing);
-                nring = 0;
-            }
-        }
-        __syncwarp();
-    }
-    if (nring) flush(nring);
-}
 
 // ------------------------------------------------------------------ K10, hit bitmasks
 // k_raster_vjp_staged3 with the per-(entry, pixel) tests done as bit
@@ -1271,69 +523,6 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     if (nring) flush(nring);
 }
 
-// ------------------------------------------------------------------ K12 (raster)
-template <bool kWarpCull>
-__global__ void __launch_bounds__(kThreads) k_raster_jvp(TileLists tl,
-                                                         const double* __restrict__ rec,
-                                                         const double* __restrict__ trec, int W,
-                                                         int H, RenderP ro,
-                                                         double* __restrict__ tangent) {
-    __shared__ __align__(16) double s_rec[kJvpBatch * kRec];
-    __shared__ __align__(16) double s_t[kJvpBatch * kTRec];
-    const int tile = blockIdx.x + tl.row0 * tl.tiles_x;
-    const PixelCtx pc = pixel_ctx(tile, tl.tiles_x, W, H);
-    const int start = tl.tile_start[tile], end = tl.tile_end[tile];
-    double T = 1.0, dT = 0.0;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    bool done = !pc.inside;
-    for (int b = start; b < end; b += kJvpBatch) {
-        if (__syncthreads_and(done)) break;
-        const int n = min(kJvpBatch, end - b);
-        stage_records(tl, rec, b, n, s_rec, nullptr);
-        stage_tangents(tl, trec, b, n, s_t);
-        __syncthreads();
-        if (__all_sync(kFull, done)) continue;
-        for (int jj = 0; jj < n; ++jj) {
-            const double* f = s_rec + kRec * jj;
-            if (warp_misses(pc, f) || (kWarpCull && !warp_may_hit(pc, f))) continue;
-            if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
-                const double* t = s_t + kTRec * jj;
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double e = fast_exp_neg(eval_expo(dx, dy, f));
-                double abar = __dmul_rn(f[R_ALPHA], e);
-                // tangent of the same expression (dual.hpp semantics)
-                const Dual Dx(dx, -t[T_MX]), Dy(dy, -t[T_MY]);
-                const Dual I00(f[R_I00], t[T_I00]), I01(f[R_I01], t[T_I01]),
-                    I11(f[R_I11], t[T_I11]);
-                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
-                double dabar = t[T_ALPHA] * e + f[R_ALPHA] * (e * ex.d);
-                if (abar >= ro.alpha_clamp) {
-                    abar = ro.alpha_clamp;
-                    dabar = 0.0;
-                }
-                if (!(abar < ro.alpha_skip)) {
-                    // w = abar * T ; acc += c * w ; T = T * (1 - abar)
-                    const double w = abar * T;
-                    const double dw = dabar * T + abar * dT;
-                    d0 += t[T_C0] * w + f[R_C0] * dw;
-                    d1 += t[T_C1] * w + f[R_C1] * dw;
-                    d2 += t[T_C2] * w + f[R_C2] * dw;
-                    const double om = __dsub_rn(1.0, abar);
-                    dT = dT * om + T * (-dabar);
-                    T = __dmul_rn(T, om);
-                    if (T < ro.t_stop) done = true;
-                }
-            }
-            if (__all_sync(kFull, done)) break;
-        }
-    }
-    if (!pc.inside) return;
-    const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
-    tangent[p] = d0 + ro.bg[0] * dT;
-    tangent[P + p] = d1 + ro.bg[1] * dT;
-    tangent[2 * P + p] = d2 + ro.bg[2] * dT;
-}
-
 // ------------------------------------------------------------------ K12, batch-staged
 // The tangent image with k_raster_fwd_staged's batches: the passing
 // fragments' 9 raster fields and 9 tangent fields are fetched lane-parallel
@@ -1436,25 +625,6 @@ __global__ void __launch_bounds__(32 * WPB)
     tangent[2 * P + p] = d2 + ro.bg[2] * dT;
 }
 
-// kernel-variant knobs (read once; tools/variants.sh runs the GPU suite under
-// each): SGTR_FWD_WARP 4 = paired-entry K7 (default), 2 = one entry at a
-// time, 0 = the CTA form; SGTR_VJP_MODE 1 = per-warp partials (default), 0 =
-// the CTA slot form; SGTR_VJP_STAGED 3 = interleaved K10 with the ring
-// reduction (default), 2 = a branch per pixel and a reduction per fragment;
-// SGTR_VJP_MINBLOCKS the register budget (CTAs per SM) of those;
-// SGTR_JVP_WARP 2 = batch-staged K12 (default), 0 = the CTA form;
-// SGTR_WARP_CULL=1 the warp-level contribution filter of the CTA forms
-int knob(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
-const int g_warp_cull = knob("SGTR_WARP_CULL", 0);
-const int g_vjp_mode = knob("SGTR_VJP_MODE", 1);
-const int g_fwd_warp = knob("SGTR_FWD_WARP", 5);
-const int g_vjp_staged = knob("SGTR_VJP_STAGED", 4);
-const int g_vjp_min_blocks = knob("SGTR_VJP_MINBLOCKS", g_vjp_mode == 1 ? 10 : 3);
-const int g_jvp_warp = knob("SGTR_JVP_WARP", 2);
-
 }  // namespace
 
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
@@ -1462,65 +632,19 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
                        unsigned long long* counters) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (counters)
-        k_raster_fwd<true, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
-                                                          counters);
-    else if (g_fwd_warp == 5)  // one-warp CTAs, hit bitmasks
+    if (counters)  // the E / C work counters (outside timed regions)
+        k_raster_count<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last, counters);
+    else  // one-warp CTAs: each retires as soon as its block is done
         k_raster_fwd_bits<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    else if (g_fwd_warp == 4)  // one-warp CTAs: each retires as soon as its block is done
-        k_raster_fwd_paired<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    else if (g_fwd_warp == 2)
-        k_raster_fwd_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
-    else if (g_warp_cull)
-        k_raster_fwd<false, true><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last,
-                                                          nullptr);
-    else
-        k_raster_fwd<false, false><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal,
-                                                           last, nullptr);
     SGTR_CUDA(cudaGetLastError());
 }
-
-void launch_raster_vjp(cudaStream_t st, const TileLists& tl, const double* rec, int W, int H,
-                       const RenderP& ro, const double* adj, const double* tfinal,
-                       const int* last, double* slots) {
-    const int n = tl.tiles_x * (tl.row1 - tl.row0);
-    if (n == 0) return;
-    if (g_warp_cull && g_vjp_min_blocks == 3)
-        k_raster_vjp<true, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
-    else if (g_warp_cull)
-        k_raster_vjp<true, 2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
-    else if (g_vjp_min_blocks == 3)
-        k_raster_vjp<false, 3><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
-    else
-        k_raster_vjp<false, 2><<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, slots);
-    SGTR_CUDA(cudaGetLastError());
-}
-
-int vjp_mode() { return g_vjp_mode; }
-int chain_mode() { return knob("SGTR_CHAIN_MODE", 0); }
 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_vjp_staged == 2) {
-        if (g_vjp_min_blocks == 8)
-            k_raster_vjp_staged2<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                              part, mask);
-        else
-            k_raster_vjp_staged2<2><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                          part, mask);
-    } else if (g_vjp_staged == 4) {  // one-warp CTAs, hit bitmasks
-        k_raster_vjp_bits<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                   mask);
-    } else if (g_vjp_min_blocks == 8) {
-        k_raster_vjp_staged3<2, 8><<<n * 2, 64, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last,
-                                                          part, mask);
-    } else {  // one-warp CTAs, as K7
-        k_raster_vjp_staged3<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
-                                                      mask);
-    }
+    k_raster_vjp_bits<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -1528,12 +652,7 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    if (g_jvp_warp == 2)
-        k_raster_jvp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
-    else if (g_warp_cull)
-        k_raster_jvp<true><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
-    else
-        k_raster_jvp<false><<<n, kThreads, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    k_raster_jvp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     SGTR_CUDA(cudaGetLastError());
 }
 

@@ -1,8 +1,9 @@
-"""The kernel variants DESIGN.md §4 calls bit-identical give bit-identical
-scenes: a few C2 training steps (100K splats, SH degree 3, 512x512, batch 8,
-through refresh) under each variant knob, compared by the scene's hash.  The
-knobs are read once per process, so every variant runs in its own process
-(tools/scene_hash.py)."""
+"""Results do not depend on scheduling knobs: the raster kernels' tile
+launch order (SGTR_TILE_ORDER=0: row-major instead of longest list first)
+and the number of view lanes (SGTR_LANES=1: no overlap) leave a few C2
+training steps (100K splats, SH degree 3, 512x512, batch 8, through a
+refresh) bit-identical.  Knobs are read once per process, so each runs in
+its own process (tools/scene_hash.py)."""
 import os
 import subprocess
 import sys
@@ -22,7 +23,7 @@ def _hash(env_extra):
 
 
 @pytest.mark.gpu
-def test_bit_identical_variants():
+def test_scheduling_knobs_are_bit_identical():
     base = _hash({})
-    for knobs in ({"SGTR_VJP_STAGED": "2"}, {"SGTR_FWD_WARP": "2"}):
+    for knobs in ({"SGTR_TILE_ORDER": "0"}, {"SGTR_LANES": "1"}):
         assert _hash(knobs) == base, knobs
