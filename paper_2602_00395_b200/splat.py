@@ -297,6 +297,7 @@ class StepDiagnostics:  # optimizer.hpp:74-83
     max_step_over_radius: float = 0.0
     applied_step: Optional[np.ndarray] = None
     refreshed: bool = False
+    n_local_views: int = 0  # views of the batch this rank rendered (multi-rank split)
 
 
 # ------------------------------------------------------------------ context
@@ -504,7 +505,8 @@ class Context:
                                                    _ptr(a2), a2.size, _ptr(pb), nu,
                                                    C.byref(d)))
         out = StepDiagnostics(d.batch_loss, d.gnorm, d.step_pre, d.step_post, d.clip_frac,
-                              d.eps, d.max_step_over_radius, None, bool(d.refreshed))
+                              d.eps, d.max_step_over_radius, None, bool(d.refreshed),
+                              int(d.n_local_views))
         if opt.record_applied_step:
             out.applied_step = np.empty(self.dim)
             check(lib().sgtr_get_applied_step(self._h, _ptr(out.applied_step)))
