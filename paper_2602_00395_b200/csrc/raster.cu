@@ -224,6 +224,20 @@ struct StagedRec {
     double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
 };
 
+// cp.async (LDGSTS) 16-byte global -> shared copies, cached in L1 (the
+// records of a tile are read by its 8 warps)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------ K7, hit bitmasks
 // The per-pixel bbox test of every (entry, pixel) pair is done once per batch
 // as bit arithmetic: the lane that stages list entry base + j turns its pixel
@@ -235,13 +249,17 @@ struct StagedRec {
 // -- no per-entry rectangle loads, compares or votes.  Per pixel the entries,
 // operations and their order are those of k_raster_fwd_paired, so the image,
 // T and the stop index are bit-identical.
+// The record staging is software-pipelined: the next batch's rectangles are
+// tested and its records copied into the other half of a double buffer with
+// cp.async (LDGSTS) while the current batch blends (-4.5 % K7 against the
+// synchronous staging, bit-identical).
 template <int WPB>
 __global__ void __launch_bounds__(32 * WPB)
     k_raster_fwd_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       double* __restrict__ img, double* __restrict__ tfinal,
                       int* __restrict__ last) {
     constexpr int SUB = kWarps / WPB;
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
+    __shared__ __align__(16) StagedRec s_rec[WPB][2][32];
     const int tile =
         tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
@@ -251,7 +269,6 @@ __global__ void __launch_bounds__(32 * WPB)
     double T = 1.0, c0 = 0.0, c1 = 0.0, c2 = 0.0;
     bool done = !pc.inside;
     int processed = end - start;
-    StagedRec* my_rec = s_rec[lw];
     auto falloff = [&](const StagedRec& r) {
         const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
                               r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
@@ -271,28 +288,33 @@ __global__ void __launch_bounds__(32 * WPB)
             processed = pos - start + 1;
         }
     };
-    for (int base = start; base < end; base += 32) {
-        if (__all_sync(kFull, done)) break;
+    // stage batch `base` into buffer `buf`: test the rectangle, start the copy
+    auto stage = [&](int base, int buf) -> unsigned {
         const int jj = base + lane;
         unsigned slots = 0;
         if (jj < end) {
             slots = (unsigned)block_slots(__ldg(tl.trect + jj), pc.ix0, pc.iy0, 4);
             if (slots) {
-                const double2* r2 = reinterpret_cast<const double2*>(
-                    rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-                const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-                const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-                double2* o = reinterpret_cast<double2*>(my_rec + lane);
-                o[0] = a;
-                o[1] = b;
-                o[2] = c;
-                o[3] = d;
-                o[4] = e;
+                const double* src = rec + (long long)kRec * __ldg(tl.tile_ids + jj) + 4;
+                double* dst = reinterpret_cast<double*>(&s_rec[lw][buf][lane]);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) cp_async16(dst + 2 * q, src + 2 * q);
             }
         }
-        unsigned mine = warp_transpose32(slots);  // bit j: entry base + j covers my pixel
+        cp_async_commit();
+        return slots;
+    };
+    int buf = 0;
+    unsigned slots_cur = start < end ? stage(start, 0) : 0u;
+    for (int base = start; base < end; base += 32) {
+        if (__all_sync(kFull, done)) break;
+        // the next batch's copies overlap this batch's blending
+        const unsigned slots_next = base + 32 < end ? stage(base + 32, buf ^ 1) : (cp_async_commit(), 0u);
+        unsigned mine = warp_transpose32(slots_cur);  // bit j: entry base + j covers my pixel
         if (done) mine = 0u;
+        cp_async_wait<1>();
         __syncwarp();
+        const StagedRec* my_rec = s_rec[lw][buf];
         unsigned wb = __reduce_or_sync(kFull, mine);
         while (wb) {
             const int j0 = __ffs(wb) - 1;
@@ -314,7 +336,10 @@ __global__ void __launch_bounds__(32 * WPB)
             wb &= __reduce_or_sync(kFull, mine);
         }
         __syncwarp();
+        slots_cur = slots_next;
+        buf ^= 1;
     }
+    cp_async_wait<0>();
     if (!pc.inside) return;
     const long long P = (long long)W * H, p = (long long)pc.py * W + pc.px;
     img[p] = c0 + ro.bg[0] * T;
@@ -335,8 +360,9 @@ constexpr int kRedStride = 33;
 // low-bits mask, render.cpp:238-257 walks [0, last)); an OR-reduction gives
 // the entries the warp visits, back to front.  Records are staged at their
 // list offset (no compaction), and the per-slot written-flag is set by the
-// ring flush.  Per pixel and per partial the operations and their order are
-// those of k_raster_vjp_staged3: the partials are bit-identical.
+// ring flush; the record staging is double-buffered with cp.async as in K7.
+// Per pixel and per partial the operations and their order are those of
+// k_raster_vjp_staged3 (round 1): the partials are bit-identical.
 template <int WPB, int kMinB = 10>
 __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     k_raster_vjp_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
@@ -347,8 +373,8 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     constexpr int kRing = 3;  // 27 columns: one per lane
     __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
     __shared__ long long s_ring_out[WPB][kRing];
-    __shared__ __align__(16) StagedRec s_rec[WPB][32];
-    __shared__ int s_slot[WPB][32];
+    __shared__ __align__(16) StagedRec s_rec[WPB][2][32];
+    __shared__ int s_slot[WPB][2][32];
     const int tile =
         tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
@@ -380,8 +406,6 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
         ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
     }
     const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
-    StagedRec* my_rec = s_rec[lw];
-    int* my_slot = s_slot[lw];
     double(*ring)[kRedStride] = s_ring[lw];
     long long* ring_out = s_ring_out[lw];
     int nring = 0;  // warp-uniform
@@ -408,26 +432,34 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
         }
         __syncwarp();
     };
-    for (int top = start + wlast; top > start; top -= 32) {
+    // stage the batch [base, top) into buffer `buf`: test the rectangles, start
+    // the record copies
+    auto stage = [&](int top, int buf) -> unsigned long long {
         const int base = max(start, top - 32);
         const int jj = base + lane;
         unsigned long long slots = 0ull;
         if (jj < top) {
             slots = block_slots(__ldg(tl.trect + jj), bx0, by0, 8);
             if (slots) {
-                const double2* r2 = reinterpret_cast<const double2*>(
-                    rec + (long long)kRec * __ldg(tl.tile_ids + jj));
-                const double2 a = __ldg(r2 + 2), b = __ldg(r2 + 3), c = __ldg(r2 + 4);
-                const double2 d = __ldg(r2 + 5), e = __ldg(r2 + 6);
-                double2* o = reinterpret_cast<double2*>(my_rec + lane);
-                o[0] = a;
-                o[1] = b;
-                o[2] = c;
-                o[3] = d;
-                o[4] = e;
-                my_slot[lane] = __ldg(tl.sorted_d + jj);
+                const double* src = rec + (long long)kRec * __ldg(tl.tile_ids + jj) + 4;
+                double* dst = reinterpret_cast<double*>(&s_rec[lw][buf][lane]);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) cp_async16(dst + 2 * q, src + 2 * q);
+                s_slot[lw][buf][lane] = __ldg(tl.sorted_d + jj);
             }
         }
+        cp_async_commit();
+        return slots;
+    };
+    int buf = 0;
+    unsigned long long slots_cur = wlast > 0 ? stage(start + wlast, 0) : 0ull;
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        // the next (nearer) batch's copies overlap this batch's sweep
+        const unsigned long long slots = slots_cur;
+        slots_cur = base > start ? stage(base, buf ^ 1) : (cp_async_commit(), 0ull);
+        const StagedRec* my_rec = s_rec[lw][buf];
+        const int* my_slot = s_slot[lw][buf];
         // bit j of m[k]: entry base + j covers pixel k and lies below its
         // stored last index
         unsigned m[2] = {warp_transpose32((unsigned)slots),
@@ -439,6 +471,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
         }
         const unsigned w0 = __reduce_or_sync(kFull, m[0]), w1 = __reduce_or_sync(kFull, m[1]);
         unsigned wb = w0 | w1;
+        cp_async_wait<1>();
         __syncwarp();
         while (wb) {
             const int e = 31 - __clz(wb);  // back to front
@@ -519,7 +552,9 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             }
         }
         __syncwarp();
+        buf ^= 1;
     }
+    cp_async_wait<0>();
     if (nring) flush(nring);
 }
 
