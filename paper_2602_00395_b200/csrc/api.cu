@@ -86,9 +86,83 @@ struct DevStatus {
     int n_large;
 };
 
+// std::mt19937_64, output for output (the reference's Rng wraps it,
+// rng.hpp:15-72), with a block interface for the Hutchinson probes: the
+// reference takes bit 0 of one output per coordinate, and bit 0 of a tempered
+// output is the parity of (state word & kBit0) -- the tempering is linear
+// over GF(2) -- so a probe's bits come straight from the twisted state,
+// 312 words per twist, without the per-output tempering.
+struct MT64 {
+    static constexpr int N = 312, M = 156;
+    static constexpr uint64_t kBit0 = 0x80080824000041ull;
+    uint64_t mt[N];
+    int idx = N;
+    explicit MT64(uint64_t seed = 5489u) {
+        mt[0] = seed;
+        for (int i = 1; i < N; ++i)
+            mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    }
+    void twist() {
+        constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+        constexpr uint64_t A = 0xB5026F5AA96619E9ull;
+        for (int i = 0; i < N - M; ++i) {
+            const uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
+            mt[i] = mt[i + M] ^ (x >> 1) ^ ((0 - (x & 1)) & A);
+        }
+        for (int i = N - M; i < N - 1; ++i) {
+            const uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
+            mt[i] = mt[i + M - N] ^ (x >> 1) ^ ((0 - (x & 1)) & A);
+        }
+        const uint64_t x = (mt[N - 1] & UM) | (mt[0] & LM);
+        mt[N - 1] = mt[M - 1] ^ (x >> 1) ^ ((0 - (x & 1)) & A);
+        idx = 0;
+    }
+    uint64_t operator()() {
+        if (idx >= N) twist();
+        uint64_t y = mt[idx++];
+        y ^= (y >> 29) & 0x5555555555555555ull;
+        y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+        y ^= (y << 37) & 0xFFF7EEE000000000ull;
+        return y ^ (y >> 43);
+    }
+    // the standard text form of std::mt19937_64 (the state words, then the
+    // position), so checkpoints stay readable by either
+    friend std::ostream& operator<<(std::ostream& os, const MT64& g) {
+        os << g.mt[0];
+        for (int i = 1; i < N; ++i) os << ' ' << g.mt[i];
+        return os << ' ' << g.idx;
+    }
+    friend std::istream& operator>>(std::istream& is, MT64& g) {
+        for (int i = 0; i < N; ++i) is >> g.mt[i];
+        return is >> g.idx;
+    }
+    // bit 0 of the next n outputs, packed LSB first into out[0 .. ceil(n/32))
+    void low_bits(uint32_t* out, long long n) {
+        long long w = 0, done = 0;
+        uint32_t word = 0;
+        int nb = 0;
+        while (done < n) {
+            if (idx >= N) twist();
+            const int take = (int)std::min<long long>(N - idx, n - done);
+            const uint64_t* p = mt + idx;
+            for (int k = 0; k < take; ++k) {
+                word |= (uint32_t)__builtin_parityll(p[k] & kBit0) << nb;
+                if (++nb == 32) {
+                    out[w++] = word;
+                    word = 0;
+                    nb = 0;
+                }
+            }
+            idx += take;
+            done += take;
+        }
+        if (nb) out[w] = word;
+    }
+};
+
 // RNG with the reference's variate mappings (rng.hpp:15-72)
 struct Rng {
-    std::mt19937_64 gen;
+    MT64 gen;
     bool have_spare = false;
     double spare = 0.0;
     explicit Rng(uint64_t s = 1) : gen(s) {}
@@ -159,12 +233,10 @@ StepDraws draw_step(Rng& rng, long long t, const DrawKey& k, const std::atomic<b
         d.bits.assign(words * k.nu, 0u);
         for (int s = 0; s < k.nu; ++s) {
             uint32_t* w = d.bits.data() + words * s;
-            for (long long base = 0; base < k.dim; base += 32) {
-                if (stop && (base & ((1 << 20) - 1)) == 0 && stop->load()) return d;
-                const int n = (int)std::min<long long>(32, k.dim - base);
-                uint32_t word = 0;
-                for (int b = 0; b < n; ++b) word |= (uint32_t)(rng.gen() & 1u) << b;
-                w[base >> 5] = word;
+            constexpr long long kChunk = 1 << 20;  // bits between stop checks (a multiple of 32)
+            for (long long base = 0; base < k.dim; base += kChunk) {
+                if (stop && stop->load()) return d;
+                rng.gen.low_bits(w + (base >> 5), std::min(kChunk, k.dim - base));
             }
             d.after_probe.push_back(rng);
         }
