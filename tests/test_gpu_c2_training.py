@@ -11,8 +11,8 @@ coefficients per splat and 12 training views the view-dependent colour
 overfits: measured, training 17.5 -> 38.1 dB while held-out rises to 20.1 dB
 at iteration 50 and then slides to 18.4 dB (the same geometry at SH degree 0:
 training 18.1 -> 31.8, held-out 18.1 -> 23.4 dB, monotone;
-tools/c2_diag.py).  The trajectory is written to $SGTR_C2_LOG (JSON) when set.  There is no CPU
-comparison at this size (a single oracle iteration takes hours); C2's
+tools/c2_diag.py).  The trajectory is written to $SGTR_C2_LOG (JSON) when
+set.  There is no CPU comparison at this size (a single oracle iteration takes hours); C2's
 kernels are covered against the oracle on crops
 (test_gpu_parity.py::test_c2_scale_crop_parity, test_gpu_sh.py)."""
 import json
@@ -42,6 +42,7 @@ def test_c2_500_iterations():
     ctx.state_reset(1)
     opt = sp.OptimizerOptions(batch_size=b, schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 500),
                               record_applied_step=False)
+
     def point(t, loss):
         ev = ctx.evaluate()
         tr = ctx.evaluate(training_views=True)
