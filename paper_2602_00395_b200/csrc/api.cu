@@ -454,8 +454,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, id_rank, okeys,
-        ovals, otemp;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, id_rank, ovals;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     // further view lanes (stream + per-view workspace), swapped in by
@@ -470,7 +469,7 @@ struct Ctx {
     X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp)             \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
-    X(part) X(mask) X(tmask) X(large) X(trect) X(id_rank) X(okeys) X(ovals) X(otemp)
+    X(part) X(mask) X(tmask) X(large) X(trect) X(id_rank) X(ovals)
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
@@ -662,8 +661,8 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     int* tids = c.tile_ids.as<int>(nd);
     {
         Timed t(c, KC_TILE_BIN);
-        launch_tile_ids(c.st, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids, nullptr,
-                        c.trect.as<int4>(nd));
+        launch_tile_ids(c.st, b.tkeys_alt, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids,
+                        c.trect.as<int4>(nd), b.tile_start, b.tile_end);
     }
     c.launches += vr.n_dup ? 1 : 0;
     vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt,
@@ -675,13 +674,10 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     static const bool by_length = getenv("SGTR_TILE_ORDER") ? atoi(getenv("SGTR_TILE_ORDER")) : 1;
     if (by_length && vr.n_dup && vr.tl.row0 == 0 && vr.tl.row1 == tiles_y) {
         Timed t(c, KC_TILE_BIN);
-        unsigned int* k0 = c.okeys.as<unsigned int>(2 * n_tiles);
-        int* v0 = c.ovals.as<int>(2 * n_tiles);
-        void* tmp = c.otemp.ensure(tile_order_temp_bytes(n_tiles));
-        launch_tile_order(c.st, b.tile_start, b.tile_end, n_tiles, k0, k0 + n_tiles, v0,
-                          v0 + n_tiles, tmp, c.otemp.bytes);
-        vr.tl.order = v0 + n_tiles;
-        c.launches += 4;
+        int* order = c.ovals.as<int>(n_tiles);
+        launch_tile_order(c.st, b.tile_start, b.tile_end, n_tiles, order);
+        vr.tl.order = order;
+        c.launches += 1;
     }
     const int P = dc.W * dc.H;
     Timed t(c, KC_RASTER_FWD);

@@ -137,40 +137,49 @@ __global__ void __launch_bounds__(256) k_emit_large(const int* __restrict__ sort
     }
 }
 
-__global__ void k_ranges(const unsigned int* __restrict__ tkeys, long long n,
-                         int* __restrict__ start, int* __restrict__ end) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned int k = tkeys[i];
-    if (i == 0 || tkeys[i - 1] != k) start[k] = (int)i;
-    if (i == n - 1 || tkeys[i + 1] != k) end[k] = (int)(i + 1);
-}
-
-// tile-sorted copies of the splat id and its exact pixel rectangle (K1's
-// pixel_range of the FP64 bbox), which the rasterisers test per warp and
-// per pixel; and the duplicate -> position inverse used by K11
-__global__ void k_tile_ids(const int* __restrict__ sorted_d, const int* __restrict__ dup_id,
-                           long long n, const int4* __restrict__ rect,
-                           int* __restrict__ tile_ids, int* __restrict__ inv,
-                           int4* __restrict__ trect) {
+// per tile-sorted position j: the tile ranges (K6), and tile-sorted copies
+// of the splat id and of its exact pixel rectangle (K1's pixel_range of the
+// FP64 bbox), which the rasterisers test per warp
+__global__ void k_tile_ids(const unsigned int* __restrict__ tkeys, const int* __restrict__ sorted_d,
+                           const int* __restrict__ dup_id, long long n,
+                           const int4* __restrict__ rect, int* __restrict__ tile_ids,
+                           int4* __restrict__ trect, int* __restrict__ start,
+                           int* __restrict__ end) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    const int d = sorted_d[j];
-    const int id = dup_id[d];
+    const unsigned int k = tkeys[j];
+    if (j == 0 || tkeys[j - 1] != k) start[k] = (int)j;
+    if (j == n - 1 || tkeys[j + 1] != k) end[k] = (int)(j + 1);
+    const int id = dup_id[sorted_d[j]];
     tile_ids[j] = id;
-    if (inv) inv[d] = (int)j;  // (optional: nothing on the step path reads it)
     trect[j] = rect[id];
 }
-
-__global__ void k_tile_order_keys(const int* __restrict__ start, const int* __restrict__ end,
-                                  int n, unsigned int* __restrict__ keys,
-                                  int* __restrict__ vals) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    keys[t] = 0xffffu - (unsigned int)min(end[t] - start[t], 0xffff);
-    vals[t] = t;
+__global__ void __launch_bounds__(1024) k_tile_order(const int* __restrict__ start,
+                                                     const int* __restrict__ end, int n,
+                                                     int* __restrict__ order) {
+    __shared__ int s_cnt[256];
+    __shared__ int s_off[256];
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) s_cnt[b] = 0;
+    __syncthreads();
+    auto bucket = [&](int t) { return 255 - min((end[t] - start[t]) >> 4, 255); };
+    for (int t = threadIdx.x; t < n; t += blockDim.x) atomicAdd(&s_cnt[bucket(t)], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 counts by one warp
+        int run = 0;
+        for (int b0 = 0; b0 < 256; b0 += 32) {
+            const int v = s_cnt[b0 + threadIdx.x];
+            int incl = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)threadIdx.x >= o) incl += y;
+            }
+            s_off[b0 + threadIdx.x] = run + incl - v;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += blockDim.x) order[atomicAdd(&s_off[bucket(t)], 1)] = t;
 }
-
 int bits_for(int n) {
     int b = 1;
     while ((1LL << b) < n) ++b;
@@ -179,14 +188,14 @@ int bits_for(int n) {
 
 }  // namespace
 
-void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     const int4* rect, int* tile_ids, int* inv, int4* trect) {
+void launch_tile_ids(cudaStream_t st, const unsigned int* tkeys, const int* sorted_d,
+                     const int* dup_id, long long n, const int4* rect, int* tile_ids, int4* trect,
+                     int* tile_start, int* tile_end) {
     if (n == 0) return;
-    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(sorted_d, dup_id, n, rect, tile_ids, inv,
-                                                  trect);
+    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(tkeys, sorted_d, dup_id, n, rect, tile_ids, trect,
+                                                  tile_start, tile_end);
     SGTR_CUDA(cudaGetLastError());
 }
-
 size_t depth_sort_temp_bytes(int K) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
@@ -210,23 +219,11 @@ size_t tile_sort_temp_bytes(long long n_dup, int n_tiles) {
     return bytes;
 }
 
-size_t tile_order_temp_bytes(int n_tiles) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned int*)nullptr,
-                                    (unsigned int*)nullptr, (int*)nullptr, (int*)nullptr,
-                                    n_tiles, 0, 16);
-    return bytes;
-}
-
 void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_end, int n_tiles,
-                       unsigned int* keys, unsigned int* keys_alt, int* vals, int* order,
-                       void* temp, size_t temp_bytes) {
+                       int* order) {
     if (n_tiles == 0) return;
-    k_tile_order_keys<<<ceil_div(n_tiles, 256), 256, 0, st>>>(tile_start, tile_end, n_tiles,
-                                                              keys, vals);
+    k_tile_order<<<1, 1024, 0, st>>>(tile_start, tile_end, n_tiles, order);
     SGTR_CUDA(cudaGetLastError());
-    SGTR_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_alt, vals, order,
-                                              n_tiles, 0, 16, st));
 }
 
 void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
@@ -262,9 +259,6 @@ void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long lon
     SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,
                                               b.dval_alt, (int)n_dup, 0, bits_for(n_tiles),
                                               st));
-    k_ranges<<<ceil_div(n_dup, 256), 256, 0, st>>>(b.tkeys_alt, n_dup, b.tile_start,
-                                                   b.tile_end);
-    SGTR_CUDA(cudaGetLastError());
 }
 
 }  // namespace sgtr

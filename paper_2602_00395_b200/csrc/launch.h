@@ -50,7 +50,7 @@ size_t tile_sort_temp_bytes(long long n_dup, int n_tiles);
 // K2 (+ the K3 scan): sorts keys, returns sorted ids in b.ids_alt and the
 // exclusive tile-count offsets (total at off_r[K])
 void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K);
-// K4-K6: duplicates, stable tile sort, tile ranges
+// K4-K5: duplicates, stable tile sort (the ranges come with launch_tile_ids)
 void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long long n_dup,
                          int tiles_x, int n_tiles);
 
@@ -68,12 +68,10 @@ struct TileLists {
     const int* order = nullptr;  // full frames: tiles by decreasing list length (the
                                  // raster kernels' launch order), else row-major
 };
-// tiles by decreasing list length (ties by index) into order[0, n_tiles):
-// the long tiles start first, so the grid's tail is short ones
-size_t tile_order_temp_bytes(int n_tiles);
+// tiles by decreasing list length (bucketed) into order[0, n_tiles): the
+// long tiles start first, so the grid's tail is short ones
 void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_end, int n_tiles,
-                       unsigned int* keys, unsigned int* keys_alt, int* vals, int* order,
-                       void* temp, size_t temp_bytes);
+                       int* order);
 // K7: front-to-back blend -> planar image, final T, processed count per pixel
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, double* img, double* tfinal, int* last,
@@ -96,10 +94,11 @@ void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb
                        const int* inv,  // splat id -> depth rank: id-order threads (or null)
                        const double* part, const unsigned char* mask, const double* zdense,
                        const uint32_t* zbits, double* acc, double* nonfinite_flag);
-// tile_ids[j] = dup_id[sorted_d[j]], inv[sorted_d[j]] = j, tbox[j] = the
-// splat's bbox rounded outward to float
-void launch_tile_ids(cudaStream_t st, const int* sorted_d, const int* dup_id, long long n,
-                     const int4* rect, int* tile_ids, int* inv, int4* trect);
+// per tile-sorted position j: tile ranges from the sorted keys (K6),
+// tile_ids[j] = dup_id[sorted_d[j]], trect[j] = rect[tile_ids[j]]
+void launch_tile_ids(cudaStream_t st, const unsigned int* tkeys, const int* sorted_d,
+                     const int* dup_id, long long n, const int4* rect, int* tile_ids, int4* trect,
+                     int* tile_start, int* tile_end);
 // K12 (raster half): tangent image along the tangent records
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro,
