@@ -224,20 +224,6 @@ struct StagedRec {
     double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
 };
 
-// cp.async (LDGSTS) 16-byte global -> shared copies, cached in L1 (the
-// records of a tile are read by its 8 warps)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
 // ------------------------------------------------------------------ K7, hit bitmasks
 // The per-pixel bbox test of every (entry, pixel) pair is done once per batch
 // as bit arithmetic: the lane that stages list entry base + j turns its pixel

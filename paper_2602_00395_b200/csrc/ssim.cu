@@ -29,12 +29,19 @@ namespace {
 constexpr int TX = 32, TY = 16, HALO = 5;
 constexpr int kThreads = 256;  // TX * TY / 2: two output rows per thread
 constexpr int kHC = 4;         // horizontal pass: output columns per thread
-constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 18
-// shared-memory row strides, padded so the FP64 tiles are bank-conflict
-// free: the horizontal passes give consecutive lanes consecutive staged rows
-// (stride 43 doubles = 86 words, 22 mod 32: 16 distinct even banks per
-// half-warp) and write the filtered rows at stride 33 doubles (2 mod 32)
+constexpr int SX = TX + 2 * HALO, SY = TY + 2 * HALO;  // 42 x 26
+// Shared-memory layout, bank-conflict free for FP64 (a half-warp's 16
+// doubles fill the 32 banks once when their indices are distinct mod 16):
+// * staging walks each staged row in 16-column segments, one half-warp per
+//   segment, so a half-warp never straddles two rows (kSegs segments per row);
+// * the horizontal passes give lane l of warp w staged row l and column group
+//   w: row stride 43 doubles (11 mod 16) makes 16 consecutive rows distinct;
+// * the filtered rows are written and read at stride 33 doubles (1 mod 16).
 constexpr int SXP = SX + 1, TXP = TX + 1;
+constexpr int kSegs = (SX + 15) / 16;
+constexpr int kStage = (SY * kSegs * 16 + kThreads - 1) / kThreads;  // staging rounds
+static_assert(SY <= 32 && TX / 4 == kThreads / 32, "horizontal pass: one row per lane, one "
+              "4-column group per warp");
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 __constant__ double c_k[11];
@@ -98,56 +105,72 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
             }
         }
     }
-    for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
-        const int sy = i / SX, sx = i % SX;
-        const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
-        double va = 0.0, vb = 0.0, vd = 0.0;
-        if (gy <= H - 1 + HALO && gx <= W - 1 + HALO) {
-            const long long q = (long long)reflect(gy, H) * W + reflect(gx, W);
-            va = A[q];
-            vb = B[q];
-            if (Tr::kTangent) vd = DA[q];
+    // all of this thread's staged loads are issued before the first store
+    // (kStage rounds), so they are in flight together
+    {
+        constexpr int NP = Tr::kTangent ? 3 : 2;
+        const double* planes[3] = {A, B, DA};
+        double* dst[3] = {s_a, s_b, s_da};
+        double v[kStage][NP];
+#pragma unroll
+        for (int it = 0; it < kStage; ++it) {
+            const int i = threadIdx.x + it * kThreads;
+            const int sy = i / (kSegs * 16), sx = i % (kSegs * 16);
+            const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
+            const bool in = i < SY * kSegs * 16 && sx < SX && gy <= H - 1 + HALO &&
+                            gx <= W - 1 + HALO;
+            const long long q = in ? (long long)reflect(gy, H) * W + reflect(gx, W) : 0;
+#pragma unroll
+            for (int f = 0; f < NP; ++f) v[it][f] = in ? planes[f][q] : 0.0;
         }
-        s_a[sy * SXP + sx] = va;
-        s_b[sy * SXP + sx] = vb;
-        if (Tr::kTangent) s_da[sy * SXP + sx] = vd;
+#pragma unroll
+        for (int it = 0; it < kStage; ++it) {
+            const int i = threadIdx.x + it * kThreads;
+            const int sy = i / (kSegs * 16), sx = i % (kSegs * 16);
+            if (i < SY * kSegs * 16 && sx < SX)
+#pragma unroll
+                for (int f = 0; f < NP; ++f) dst[f][sy * SXP + sx] = v[it][f];
+        }
     }
     __syncthreads();
-    // horizontal pass over all SY rows; two adjacent columns per thread share
-    // 10 of their 11 staged taps
-    auto acc = [&](double* m, double w, double av, double bv, double dv) {
-        m[Tr::MUA] += w * av;
-        if (!kPre) m[Tr::MUB < 0 ? 0 : Tr::MUB] += w * bv;
-        m[Tr::MAA] += w * av * av;
-        if (!kPre) m[Tr::MBB < 0 ? 0 : Tr::MBB] += w * bv * bv;
-        m[Tr::MAB] += w * av * bv;
-        if (Tr::kTangent) {
-            m[Tr::DMUA] += w * dv;
-            m[Tr::DMAA] += w * 2.0 * av * dv;
-            m[Tr::DMAB] += w * bv * dv;
-        }
-    };
-    // (kHC adjacent columns per thread share the staged taps between them)
-    for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
-        const int sy = i % SY, tx = kHC * (i / SY);
-        double mo[kHC][NM];
-#pragma unroll
-        for (int o = 0; o < kHC; ++o)
-#pragma unroll
-            for (int j = 0; j < NM; ++j) mo[o][j] = 0.0;
-#pragma unroll
-        for (int d = 0; d < 10 + kHC; ++d) {
-            const int si = sy * SXP + tx + d;
-            const double av = s_a[si], bv = s_b[si];
-            const double dv = Tr::kTangent ? s_da[si] : 0.0;
+    // horizontal pass over all SY rows: lane = staged row, warp = group of kHC
+    // adjacent output columns, which share the staged taps between them; the
+    // products of a staged pixel are formed once for the kHC windows
+    {
+        const int sy = threadIdx.x & 31, tx = kHC * (threadIdx.x >> 5);
+        if (sy < SY) {
+            double mo[kHC][NM];
 #pragma unroll
             for (int o = 0; o < kHC; ++o)
-                if (d >= o && d - o < 11) acc(mo[o], c_k[d - o], av, bv, dv);
+#pragma unroll
+                for (int j = 0; j < NM; ++j) mo[o][j] = 0.0;
+#pragma unroll
+            for (int d = 0; d < 10 + kHC; ++d) {
+                const int si = sy * SXP + tx + d;
+                const double av = s_a[si], bv = s_b[si];
+                const double dv = Tr::kTangent ? s_da[si] : 0.0;
+                double q[NM];
+                q[Tr::MUA] = av;
+                if (!kPre) q[Tr::MUB < 0 ? 0 : Tr::MUB] = bv;
+                q[Tr::MAA] = av * av;
+                if (!kPre) q[Tr::MBB < 0 ? 0 : Tr::MBB] = bv * bv;
+                q[Tr::MAB] = av * bv;
+                if (Tr::kTangent) {
+                    q[Tr::DMUA] = dv;
+                    q[Tr::DMAA] = 2.0 * av * dv;
+                    q[Tr::DMAB] = bv * dv;
+                }
+#pragma unroll
+                for (int o = 0; o < kHC; ++o)
+                    if (d >= o && d - o < 11)
+#pragma unroll
+                        for (int j = 0; j < NM; ++j) mo[o][j] += c_k[d - o] * q[j];
+            }
+#pragma unroll
+            for (int o = 0; o < kHC; ++o)
+#pragma unroll
+                for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TXP + tx + o] = mo[o][j];
         }
-#pragma unroll
-        for (int o = 0; o < kHC; ++o)
-#pragma unroll
-            for (int j = 0; j < NM; ++j) s_h[(j * SY + sy) * TXP + tx + o] = mo[o][j];
     }
     __syncthreads();
     using S = typename std::conditional<Tr::kTangent, Dual, double>::type;
@@ -249,25 +272,14 @@ __global__ void __launch_bounds__(kThreads, (MODE == GRAD && kPre) ? 4 : 1) k_ss
                 args.adjl1[pi] = u1 > fl ? ur1 * (1.0 - lam) * sgn(diff) / (2.0 * sqrt(u1)) : 0.0;
                 up = u2 > fl ? ur2 * (-lam / (4.0 * sqrt(u2))) : 0.0;
             }
-            // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155), with the
-            // two reciprocals shared
-#ifndef SGTR_SSIM_RCP
-#define SGTR_SSIM_RCP 0
-#endif
-#if SGTR_SSIM_RCP
+            // sensitivities to (mu_a, maa, mab) (ssim.cpp:146-155) through the
+            // two reciprocals 1/d1, 1/d2 (the reference's five divisions)
             const double r1 = 1.0 / d1v, r2 = 1.0 / d2v;
             const double pp = n1v * r1, qq = n2v * r2;
             const double ds_dmu = qq * (2.0 * mu_b * d1v - 2.0 * mu_av * n1v) * (r1 * r1) +
                                   pp * (2.0 * mu_av * n2v - 2.0 * mu_b * d2v) * (r2 * r2);
             const double ds_dmaa = -pp * n2v * (r2 * r2);
             const double ds_dmab = pp * 2.0 * r2;
-#else
-            const double pp = n1v / d1v, qq = n2v / d2v;
-            const double ds_dmu = qq * (2.0 * mu_b * d1v - 2.0 * mu_av * n1v) / (d1v * d1v) +
-                                  pp * (2.0 * mu_av * n2v - 2.0 * mu_b * d2v) / (d2v * d2v);
-            const double ds_dmaa = -pp * n2v / (d2v * d2v);
-            const double ds_dmab = pp * 2.0 / d2v;
-#endif
             args.P[pi] = up * ds_dmu;
             args.Q[pi] = up * ds_dmaa * 2.0;
             args.R[pi] = up * ds_dmab;
@@ -344,14 +356,29 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather(int W, int H, const doub
             if (adjl1) pl[rr] = adjl1[p];
         }
     }
-    for (int i = threadIdx.x; i < SY * SX; i += kThreads) {
-        const int sy = i / SX, sx = i % SX;
-        const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
-        const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-        const long long q = c * P + (long long)gy * W + gx;
-        s_f[0][sy][sx] = in ? Pf[q] : 0.0;
-        s_f[1][sy][sx] = in ? Qf[q] : 0.0;
-        s_f[2][sy][sx] = in ? Rf[q] : 0.0;
+    {
+        // all staged loads in flight together, then the stores
+        double v[kStage][3];
+#pragma unroll
+        for (int it = 0; it < kStage; ++it) {
+            const int i = threadIdx.x + it * kThreads;
+            const int sy = i / (kSegs * 16), sx = i % (kSegs * 16);
+            const int gy = y0 - HALO + sy, gx = x0 - HALO + sx;
+            const bool in = i < SY * kSegs * 16 && sx < SX && gy >= 0 && gy < H && gx >= 0 &&
+                            gx < W;
+            const long long q = in ? c * P + (long long)gy * W + gx : 0;
+            v[it][0] = in ? Pf[q] : 0.0;
+            v[it][1] = in ? Qf[q] : 0.0;
+            v[it][2] = in ? Rf[q] : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < kStage; ++it) {
+            const int i = threadIdx.x + it * kThreads;
+            const int sy = i / (kSegs * 16), sx = i % (kSegs * 16);
+            if (i < SY * kSegs * 16 && sx < SX)
+#pragma unroll
+                for (int f = 0; f < 3; ++f) s_f[f][sy][sx] = v[it][f];
+        }
     }
     __syncthreads();
     // blocks whose windows never meet the image border (most of a 1080p
@@ -360,9 +387,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_gather(int W, int H, const doub
     const bool in_y = y0 >= 2 * HALO && y0 + TY + 2 * HALO <= H;
     // horizontal transposed pass for every staged row
     if (in_x) {
-        // kHC adjacent columns per thread share the staged taps
-        for (int i = threadIdx.x; i < SY * (TX / kHC); i += kThreads) {
-            const int sy = i % SY, tx = kHC * (i / SY);
+        // lane = staged row, warp = group of kHC adjacent columns sharing the
+        // staged taps (the layout note at the top)
+        const int sy = threadIdx.x & 31, tx = kHC * (threadIdx.x >> 5);
+        if (sy < SY) {
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 const double* row = &s_f[f][sy][tx];

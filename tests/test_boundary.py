@@ -89,10 +89,7 @@ def test_host_helpers(built):
     assert (s.scale_offset(), s.quat_offset(), s.opacity_offset(), s.color_offset()) == (3, 6, 10, 11)
 
 
-def test_cpp_caller_of_the_c_abi(built):
-    """A C++ program compiled against include/sgtr.h and linked with
-    libsgtr.so exercises the boundary without Python (host-only part here;
-    the GPU part runs when a device is present)."""
+def run_cpp_host():
     import subprocess
     import tempfile
     exe = os.path.join(tempfile.mkdtemp(), "cpp_host")
@@ -103,3 +100,20 @@ def test_cpp_caller_of_the_c_abi(built):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "host-only C-ABI ok" in r.stdout
+    return r.stdout
+
+
+def test_cpp_caller_of_the_c_abi(built):
+    """A C++ program compiled against include/sgtr.h and linked with
+    libsgtr.so exercises the boundary without Python (host-only part)."""
+    run_cpp_host()
+
+
+@pytest.mark.gpu
+def test_cpp_caller_steps_on_the_device(built):
+    """The same C++ program on a B200: synthetic targets rendered on the
+    device, then three sgtr_step_3dgs2tr calls, each printing its batch loss."""
+    out = run_cpp_host()
+    assert "no CUDA device" not in out, out
+    losses = [float(m) for m in re.findall(r"^step \d loss (\S+)", out, re.M)]
+    assert len(losses) == 3 and all(np.isfinite(losses)) and min(losses) > 0, out

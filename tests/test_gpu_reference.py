@@ -94,6 +94,26 @@ def test_render_jvp_vjp_match_reference(sp, ref, c1):
                        ref.rasterize_vjp(which, oc, adj)) < GRAD_TOL
 
 
+def test_view_jacobian_seams_match_reference(sp, ref, c1):
+    """view_jacobian_apply / applyT (optimizer.cpp:18-34): the residual-space
+    J_i v (the rasterize JVP pushed through the SSIM/L1 residual chain) and
+    J_i^T u, against the reference on two views of each scene, plus the
+    adjoint identity <u, J v> = <J^T u, v> on the device outputs."""
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal(c1.init_x.size)
+    u = rng.standard_normal(6 * 128 * 128)
+    for which in (c1.init_x, c1.gt_x):
+        scene = sp.Scene(which)
+        for oc, gt in list(zip(c1.cams, c1.gts))[1:3]:
+            cam = sp.Camera.from_c(oc, gt)
+            jv = sp.view_jacobian_apply(scene, cam, v)
+            jtu = sp.view_jacobian_applyT(scene, cam, u)
+            assert rel(jv, ref.view_jacobian_apply(which, oc, gt, v)) < IMG_TOL
+            assert rel(jtu, ref.view_jacobian_applyT(which, oc, gt, u)) < GRAD_TOL
+            lhs, rhs = float(u @ jv), float(jtu @ v)
+            assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0), (lhs, rhs)
+
+
 def test_gradient_and_hutchinson_match_reference(sp, ref, c1):
     views = [sp.Camera.from_c(c, g) for c, g in zip(c1.cams, c1.gts)]
     scene = sp.Scene(c1.init_x)
