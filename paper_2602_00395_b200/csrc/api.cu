@@ -454,7 +454,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, id_rank, ovals;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, off_id, ovals;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     // further view lanes (stream + per-view workspace), swapped in by
@@ -469,7 +469,7 @@ struct Ctx {
     X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp)             \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
-    X(part) X(mask) X(tmask) X(large) X(trect) X(id_rank) X(ovals)
+    X(part) X(mask) X(tmask) X(large) X(trect) X(off_id) X(ovals)
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
@@ -701,11 +701,10 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                                mask);
     }
     Timed t(c, KC_CHAIN);
-    int* rank = c.id_rank.as<int>(std::max(c.K, 1));
-    launch_rank_of(c.st, c.ids_alt.get<int>(), c.K, rank);
-    launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, c.ids_alt.get<int>(), vr.n_visible,
-                      c.off_r.get<long long>(), c.tcount.get<int>(), rank, part, mask, zdense,
-                      zbits, acc, flag);
+    long long* off_id = c.off_id.as<long long>(std::max(c.K, 1));
+    launch_offsets_by_id(c.st, c.ids_alt.get<int>(), c.K, c.off_r.get<long long>(), off_id);
+    launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, off_id, c.tcount.get<int>(), part,
+                      mask, zdense, zbits, acc, flag);
     c.launches += 3;
 }
 

@@ -86,12 +86,13 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
 // and the chain through invert2x2 and the projection; mode 0 adds the
 // gradient into acc, mode 1 z (.) it (Hutchinson, probe dense or as bits); a
 // non-finite contribution stores 1.0 into *nonfinite_flag.
-// splat id -> depth rank (inverse of the depth order), for launch_chain_warp's inv
-void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank);
+// splat id -> offset of its duplicates (off_r scattered from depth-rank order)
+void launch_offsets_by_id(cudaStream_t st, const int* sorted_ids, int K, const long long* off_r,
+                          long long* off_id);
+// K11: per splat (id order) the fixed-order sum of its K10 partials and the
+// chain rule to the 14 (+ SH) parameters, added into acc
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
-                       const RenderP& ro, const int* sorted_ids, int n_visible,
-                       const long long* off_r, const int* tcount,
-                       const int* inv,  // splat id -> depth rank: id-order threads (or null)
+                       const RenderP& ro, const long long* off_id, const int* tcount,
                        const double* part, const unsigned char* mask, const double* zdense,
                        const uint32_t* zbits, double* acc, double* nonfinite_flag);
 // per tile-sorted position j: tile ranges from the sorted keys (K6),

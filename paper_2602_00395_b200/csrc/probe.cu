@@ -46,6 +46,10 @@ __global__ void k_exp_check(long long n, double lo, double hi, unsigned long lon
         const double ref = x < -708.0 ? 0.0 : exp(x);
         if (x < 708.0 && __double_as_longlong(fast_exp_neg(x)) != __double_as_longlong(ref))
             ++bad;
+        // exp(-q/2) without the multiply against fast_exp_neg(-0.5 q)
+        if (x <= 0.0 && __double_as_longlong(fast_exp_neg_half(-2.0 * x)) !=
+                            __double_as_longlong(fast_exp_neg(x)))
+            ++bad;
         // rcp_unit against the IEEE division on [0.01, 1]
         const double xr = 0.01 + 0.99 * u;
         if (__double_as_longlong(rcp_unit(xr)) != __double_as_longlong(1.0 / xr)) ++bad;

@@ -235,27 +235,26 @@ __device__ __forceinline__ void chain_sh(const double* x, int K, int nb, int id,
 template <bool kSH>
 __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
-                                               const int* __restrict__ sorted_ids, int n_visible,
-                                               const long long* __restrict__ off_r,
+                                               const long long* __restrict__ off_id,
                                                const int* __restrict__ tcount,
-                                               const int* __restrict__ inv,
                                                const double* __restrict__ part,
                                                const unsigned char* __restrict__ mask,
                                                const double* __restrict__ zdense,
                                                const uint32_t* __restrict__ zbits,
                                                double* __restrict__ acc,
                                                double* nonfinite_flag) {
-    // with inv (splat id -> depth rank) the threads run in splat-id order, so
-    // the scene reads and the gradient read-modify-writes below are
-    // coalesced (at C5's 10M splats they no longer fit in L2, and a
-    // depth-order walk would touch a 32-byte sector per 8-byte access); the
-    // partials are found through the rank.  Without it, in depth-rank order.
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (inv ? K : n_visible)) return;
-    const int id = inv ? t : sorted_ids[t];
+    // threads in splat-id order, so the scene reads and the gradient
+    // read-modify-writes below are coalesced (at C5's 10M splats they no
+    // longer fit in L2); a splat's partials are found through its duplicate
+    // offset (off_id, k_offsets_by_id)
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= K) return;
     const int cnt = tcount[id];
     if (cnt == 0) return;
-    const int r = inv ? inv[id] : t;
+    const long long off = off_id[id];
+    // the splat's parameters, fetched now: their latency overlaps the
+    // partial sums
+    const Splat p = load_splat(x, K, id);
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
@@ -263,7 +262,6 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     // order; the partials are stored by splat-major duplicate slot, so a
     // splat's are one contiguous run of 288-byte records; masks of 4
     // duplicates (4 bytes each) are fetched together
-    const long long off = off_r[r];
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         long long jp[4];
         unsigned mk[4];
@@ -292,43 +290,78 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
         finite = finite && isfinite(v);
         acc[idx] += v;
     };
-    add(10 * k + id, a[5]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) add(11 * k + 3LL * id + c, a[6 + c]);
     const bool sh = kSH && nb > 0 && (a[6] != 0.0 || a[7] != 0.0 || a[8] != 0.0);
     double gmu_sh[3] = {0.0, 0.0, 0.0};
-    if (sh) chain_sh(x, K, nb, id, cam, load_splat(x, K, id), a, add, gmu_sh);
+    if (sh) chain_sh(x, K, nb, id, cam, p, a, add, gmu_sh);
     bool any = false;
 #pragma unroll
     for (int j = 0; j < 5; ++j) any = any || a[j] != 0.0;
+    // the splat's 14 gradient entries (opacity, colour, then mean, scale,
+    // rotation when the 2-D adjoints are non-zero): every acc load is issued
+    // before the first store (acc may alias itself, so the compiler would
+    // otherwise serialise the read-modify-writes)
+    long long ix[14];
+    double v[14];
+    ix[0] = 10 * k + id;
+    v[0] = a[5];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        ix[1 + c] = 11 * k + 3LL * id + c;
+        v[1 + c] = a[6 + c];
+        ix[4 + c] = 3LL * id + c;
+        v[4 + c] = gmu_sh[c];
+        ix[7 + c] = 3 * k + 3LL * id + c;
+        v[7 + c] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        ix[10 + c] = 6 * k + 4LL * id + c;
+        v[10 + c] = 0.0;
+    }
     if (any) {
         // J^T a for (mu, s, q) in one reverse sweep (geometry.cuh)
-        const Splat p = load_splat(x, K, id);
         double gmu[3], gs[3], gq[4];
         chain_reverse(p.mu, p.s, p.q, cam.w, cam.t, cam.fx, cam.fy, ro.lowpass, a, gmu, gs, gq);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, sh ? gmu_sh[c] + gmu[c] : gmu[c]);
+        for (int c = 0; c < 3; ++c) {
+            v[4 + c] = sh ? gmu_sh[c] + gmu[c] : gmu[c];
+            v[7 + c] = gs[c];
+        }
 #pragma unroll
-        for (int c = 0; c < 3; ++c) add(3 * k + 3LL * id + c, gs[c]);
+        for (int c = 0; c < 4; ++c) v[10 + c] = gq[c];
+    }
+    const int n = any ? 14 : (sh ? 7 : 4);
+    double old[14];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) add(6 * k + 4LL * id + c, gq[c]);
-    } else if (sh) {
+    for (int j = 0; j < 14; ++j)
+        if (j < n) old[j] = acc[ix[j]];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) add(3LL * id + c, gmu_sh[c]);
+    for (int j = 0; j < 14; ++j) {
+        if (j < n) {
+            double w = v[j];
+            if (mode == 1) w = probe_at(zdense, zbits, ix[j]) * w;
+            finite = finite && isfinite(w);
+            acc[ix[j]] = old[j] + w;
+        }
     }
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
 
-__global__ void k_rank_of(const int* __restrict__ sorted_ids, int K, int* __restrict__ rank) {
+// the offset of each splat id's duplicates (the K+1 entry scan of the
+// counts in depth-rank order, scattered to id order)
+__global__ void k_offsets_by_id(const int* __restrict__ sorted_ids, int K,
+                                const long long* __restrict__ off_r,
+                                long long* __restrict__ off_id) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < K) rank[sorted_ids[r]] = r;
+    if (r < K) off_id[sorted_ids[r]] = off_r[r];
 }
 
 }  // namespace
 
-void launch_rank_of(cudaStream_t st, const int* sorted_ids, int K, int* rank) {
+void launch_offsets_by_id(cudaStream_t st, const int* sorted_ids, int K, const long long* off_r,
+                          long long* off_id) {
     if (K == 0) return;
-    k_rank_of<<<ceil_div(K, 256), 256, 0, st>>>(sorted_ids, K, rank);
+    k_offsets_by_id<<<ceil_div(K, 256), 256, 0, st>>>(sorted_ids, K, off_r, off_id);
     SGTR_CUDA(cudaGetLastError());
 }
 
@@ -361,22 +394,20 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const D
 }
 
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb,
-                       const DevCam& cam, const RenderP& ro, const int* sorted_ids, int n_visible,
-                       const long long* off_r, const int* tcount, const int* inv,
-                       const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag) {
-    if (n_visible == 0) return;
-    const int nt = inv ? K : n_visible;  // threads: splat ids or depth ranks
+                       const DevCam& cam, const RenderP& ro, const long long* off_id,
+                       const int* tcount, const double* part, const unsigned char* mask,
+                       const double* zdense, const uint32_t* zbits, double* acc,
+                       double* nonfinite_flag) {
+    if (K == 0) return;
     if (nb)
-        k_chain_warp<true><<<ceil_div(nt, 128), 128, 0, st>>>(
-            mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
-            zbits, acc, nonfinite_flag);
+        k_chain_warp<true><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
+                                                             tcount, part, mask, zdense, zbits,
+                                                             acc, nonfinite_flag);
     else
-        k_chain_warp<false><<<ceil_div(nt, 128), 128, 0, st>>>(
-            mode, x, K, nb, cam, ro, sorted_ids, n_visible, off_r, tcount, inv, part, mask, zdense,
-            zbits, acc, nonfinite_flag);
+        k_chain_warp<false><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
+                                                              tcount, part, mask, zdense, zbits,
+                                                              acc, nonfinite_flag);
     SGTR_CUDA(cudaGetLastError());
 }
-
 
 }  // namespace sgtr

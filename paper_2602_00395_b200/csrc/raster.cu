@@ -15,7 +15,7 @@
 // the one-thread-per-pixel CTA form kept for the E/C work counters.
 //
 // Branch parity: the three kernels evaluate the primal alpha with the same
-// pinned operation sequence (eval_expo's FMA form and fastexp.cuh's exp, a
+// pinned operation sequence (eval_q's FMA form and fastexp.cuh's exp, a
 // few ulp from the reference's own order), so bbox reject, alpha clamp,
 // alpha skip and the transmittance stop take the same branches in forward,
 // VJP and JVP — the reference's "frozen branches" contract
@@ -78,20 +78,26 @@ __device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int 
     return p;
 }
 
-// reference: -0.5 * (dx*dx*i00 + dy*dy*i11) - dx*dy*i01  (render.cpp:134-135)
-// evaluated as -0.5 (dx ax + dy ay) with (ax, ay) = Sigma^-1 d (4 FMA-fused
-// steps instead of 9 roundings; a few ulp from the reference's order, the
-// same in every pass, so the clamp/skip/stop branches agree between passes).
-// (ax, ay) is also the VJP's d expo / d mu2d up to sign.
-__device__ __forceinline__ double eval_expo(double dx, double dy, const double* f, double& ax,
-                                            double& ay) {
+// reference: expo = -0.5 * (dx*dx*i00 + dy*dy*i11) - dx*dy*i01  (render.cpp:134-135)
+// evaluated as expo = -0.5 q, q = dx ax + dy ay with (ax, ay) = Sigma^-1 d (4
+// FMA-fused steps instead of 9 roundings; a few ulp from the reference's
+// order, the same in every pass, so the clamp/skip/stop branches agree
+// between passes), and exp(expo) as fast_exp_neg_half(q), bit-identical to
+// fast_exp_neg(-0.5 q) without the multiply.  (ax, ay) is also the VJP's
+// d expo / d mu2d up to sign.
+__device__ __forceinline__ double eval_q(double dx, double dy, const double* f, double& ax,
+                                         double& ay) {
     ax = __fma_rn(f[R_I01], dy, __dmul_rn(f[R_I00], dx));
     ay = __fma_rn(f[R_I11], dy, __dmul_rn(f[R_I01], dx));
-    return __dmul_rn(-0.5, __fma_rn(dy, ay, __dmul_rn(dx, ax)));
+    return __fma_rn(dy, ay, __dmul_rn(dx, ax));
 }
-__device__ __forceinline__ double eval_expo(double dx, double dy, const double* f) {
+__device__ __forceinline__ double falloff_of(double dx, double dy, const double* f, double& ax,
+                                             double& ay) {
+    return fast_exp_neg_half(eval_q(dx, dy, f, ax, ay));
+}
+__device__ __forceinline__ double falloff_of(double dx, double dy, const double* f) {
     double ax, ay;
-    return eval_expo(dx, dy, f, ax, ay);
+    return falloff_of(dx, dy, f, ax, ay);
 }
 
 __device__ __forceinline__ bool outside_bbox(double pxc, double pyc, const double* f) {
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_count(TileLists tl,
             if (warp_misses(pc, f)) continue;
             if (!done && !outside_bbox(pc.pxc, pc.pyc, f)) {
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                double abar = __dmul_rn(f[R_ALPHA], fast_exp_neg(eval_expo(dx, dy, f)));
+                double abar = __dmul_rn(f[R_ALPHA], falloff_of(dx, dy, f));
                 ++n_eval;
                 if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
                 if (!(abar < ro.alpha_skip)) {
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(32 * WPB)
         const double f[13] = {0.0,   0.0,   0.0,   0.0,     r.mx, r.my, r.i00,
                               r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
         const double dx = pc.pxc - r.mx, dy = pc.pyc - r.my;
-        double abar = __dmul_rn(r.alpha, fast_exp_neg(eval_expo(dx, dy, f)));
+        double abar = __dmul_rn(r.alpha, falloff_of(dx, dy, f));
         if (abar >= ro.alpha_clamp) abar = ro.alpha_clamp;
         return abar;
     };
@@ -470,8 +476,8 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
             bool contrib = false;
             // one pixel's contribution given its falloff (render.cpp:238-283)
-            auto accumulate = [&](int k, double dx, double dy, double ax, double ay, double gauss,
-                                  double abar, bool clamped, double rom) {
+            auto accumulate = [&](int k, double dx, double dxx, double dy, double ax, double ay,
+                                  double gauss, double abar, bool clamped, double rom) {
                 contrib = true;
                 const double t_in = T[k] * rom;
                 const double at = abar * t_in;
@@ -484,7 +490,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                 if (!clamped) {
                     g[5] += gauss * dab;
                     const double de = abar * dab;
-                    g[2] += de * (dx * dx);  // x -1/2 at the write
+                    g[2] += de * dxx;  // (dx dx) x -1/2 at the write
                     g[3] += de * (dx * dy);  // x -1
                     g[4] += de * (dy * dy);  // x -1/2
                     g[0] += de * ax;
@@ -495,13 +501,14 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
                                   r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
             const double dx = pxc - r.mx;
+            const double dxx = dx * dx;  // shared by the lane's two pixels (one column)
             if (any0 && any1) {
                 double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
                 bool cl[2];
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     dy[k] = pyc[k] - r.my;
-                    gauss[k] = fast_exp_neg(eval_expo(dx, dy[k], f, ax[k], ay[k]));
+                    gauss[k] = falloff_of(dx, dy[k], f, ax[k], ay[k]);
                     abar[k] = __dmul_rn(r.alpha, gauss[k]);
                     cl[k] = abar[k] >= ro.alpha_clamp;
                     if (cl[k]) abar[k] = ro.alpha_clamp;
@@ -511,19 +518,20 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
 #pragma unroll
                 for (int k = 0; k < 2; ++k)
                     if (lv[k])
-                        accumulate(k, dx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k], rom[k]);
+                        accumulate(k, dx, dxx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k],
+                                   rom[k]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
                     const double dy = pyc[k] - r.my;
                     double ax, ay;
-                    const double gauss = fast_exp_neg(eval_expo(dx, dy, f, ax, ay));
+                    const double gauss = falloff_of(dx, dy, f, ax, ay);
                     double abar = __dmul_rn(r.alpha, gauss);
                     const bool clamped = abar >= ro.alpha_clamp;
                     if (clamped) abar = ro.alpha_clamp;
                     if (abar < ro.alpha_skip) continue;
-                    accumulate(k, dx, dy, ax, ay, gauss, abar, clamped,
+                    accumulate(k, dx, dxx, dy, ax, ay, gauss, abar, clamped,
                                rcp_unit(__dsub_rn(1.0, abar)));
                 }
             }
@@ -612,7 +620,7 @@ __global__ void __launch_bounds__(32 * WPB)
                 const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
                                       r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
                 const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ev = fast_exp_neg(eval_expo(dx, dy, f));
+                const double ev = falloff_of(dx, dy, f);
                 double abar = __dmul_rn(f[R_ALPHA], ev);
                 // tangent of the same expression (dual.hpp semantics)
                 const Dual Dx(dx, -t.mx), Dy(dy, -t.my);

@@ -112,9 +112,17 @@ def test_adam_tr_two_ranks(sp, ds):
     assert np.allclose(two[0]["loss"], one["loss"], rtol=1e-12, atol=0)
 
 
+def visible_gpus():
+    # counted in a child process: importing torch here, after libsgtr brought
+    # in the system libnccl, would clash with torch's bundled NCCL
+    r = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True)
+    n = sum(1 for line in r.stdout.splitlines() if line.startswith("GPU "))
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    return n if cvd is None else min(n, len([d for d in cvd.split(",") if d.strip()]))
+
+
 def test_nccl_two_gpus(tmp_path):
-    import torch
-    if torch.cuda.device_count() < 2:
+    if visible_gpus() < 2:
         pytest.skip("needs two visible GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
