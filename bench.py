@@ -675,6 +675,7 @@ def main():
             "wall_ms_per_step": 1000.0 * t_wall / args.steps,
             "final_loss": diags[-1].batch_loss,
             "refresh_steps_timed": sum(1 for d in diags if d.refreshed),
+            "capacity_reruns_timed": sum(d.reruns for d in diags),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

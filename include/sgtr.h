@@ -86,6 +86,7 @@ typedef struct sgtr_step_diagnostics {
     double batch_loss, gnorm, step_pre, step_post, clip_frac, eps,
         max_step_over_radius;
     int32_t refreshed, n_local_views;
+    int32_t reruns; /* times the step was rerun after a view outgrew the duplicate capacity */
 } sgtr_step_diagnostics;
 
 /* ------------------------------------------------------------ context */
@@ -346,6 +347,13 @@ int sgtr_fp64_peak(int device, double* tflops);
  * library: number of bitwise mismatches over n inputs in [lo, hi] */
 int sgtr_check_fast_exp(int64_t n, double lo, double hi, uint64_t seed,
                         int64_t* mismatches);
+
+/* Capacity of the per-view tile-duplicate arrays (entries).  Views render
+ * without a host round trip and every view sorts `capacity` tile keys; a
+ * training step in which some view outgrows it is rerun with the capacity
+ * grown to fit (before any state changes), so this only presizes (or, for
+ * tests, shrinks) it.  0 restores the default (4 K + 65536, grown on demand). */
+int sgtr_set_dup_capacity(sgtr_ctx* ctx, int64_t capacity);
 
 /* ------------------------------------------------------------ multi-GPU */
 /* one process per GPU; views of each step are split round-robin over

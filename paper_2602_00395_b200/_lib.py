@@ -77,7 +77,7 @@ class StepDiag(C.Structure):
     _fields_ = [("batch_loss", C.c_double), ("gnorm", C.c_double), ("step_pre", C.c_double),
                 ("step_post", C.c_double), ("clip_frac", C.c_double), ("eps", C.c_double),
                 ("max_step_over_radius", C.c_double), ("refreshed", C.c_int32),
-                ("n_local_views", C.c_int32)]
+                ("n_local_views", C.c_int32), ("reruns", C.c_int32)]
 
 
 class SynthConfig(C.Structure):
@@ -170,6 +170,7 @@ _SIGS = {
     "sgtr_shard_views": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, VP,
                                    C.POINTER(C.c_int32)]),
     "sgtr_set_refresh_bands": (C.c_int, [VP, C.c_int32]),
+    "sgtr_set_dup_capacity": (C.c_int, [VP, C.c_int64]),
     "sgtr_set_tr_shards": (C.c_int, [VP, C.c_int32]),
     "sgtr_comm_init": (C.c_int, [VP, VP, C.c_int32, C.c_int32]),
 }

@@ -484,6 +484,7 @@ struct Ctx {
     int refresh_bands = 1;  // bands per rank of each refresh view (sgtr_set_refresh_bands)
     int tr_shards = 1;      // radius shards run back to back on one rank (sgtr_set_tr_shards)
     int fail_sample = -1;   // Hutchinson sample of the last step's failure (sgtr_step_failed_sample)
+    long long dup_cap = 0;  // capacity of the per-view duplicate arrays (grows, never shrinks)
     Buf stage;              // shard-major staging for the radius all-gather
     void* comm = nullptr;
     LoopGroup* loop = nullptr;  // in-process communicator (sgtr_comm_init_loopback)
@@ -519,11 +520,19 @@ namespace {
 
 struct ViewRender {
     int W, H;
-    int n_visible;
-    long long n_dup;
+    int n_visible;   // -1 on a deferred view (not read back)
+    long long n_dup;  // -1 on a deferred view
+    long long cap;    // capacity of the duplicate arrays the view used
     TileLists tl;
     int err_kind;  // 0 none, 1 non-finite parameter, 2 degenerate quaternion
     int err_index;
+};
+
+// where a deferred view (render_view without a host round trip) reports its
+// error, duplicate total and capacity overflow: slots of the step's fused
+// tail (errk/erri/ndup may be null: another rank or band reports them)
+struct ViewSlots {
+    double *errk = nullptr, *erri = nullptr, *ndup = nullptr, *ovf = nullptr;
 };
 
 void bind(Ctx& c) { SGTR_CUDA(cudaSetDevice(c.device)); }
@@ -579,11 +588,22 @@ void harvest_timing(Ctx& c) {
 
 double* img_ptr(Ctx& c, Buf& b, int P) { return b.as<double>(3LL * P); }
 
+// capacity for `need` duplicates.  Every view sorts `cap` tile keys (the
+// tail padded), so the headroom is small: 1/16, enough that the views of later
+// steps (the same scene, slowly changing) rarely outgrow it
+long long grow_cap(long long need) { return need + need / 16 + 4096; }
+
 // K1..K7 for one camera on the context's scene
 // row0/row1: the tile rows the forward raster covers (a refresh band plus
-// its halo); row1 < 0 renders the whole view
+// its halo); row1 < 0 renders the whole view.
+// Without `defer`, the view's status and duplicate total are read back after
+// the depth sort (one host round trip: errors are returned or thrown, the
+// duplicate arrays sized exactly).  With `defer` nothing is read back: the
+// duplicate arrays keep the context's capacity, and the status, the total and
+// an overflow count go to the step's tail slots (k_view_end), checked once
+// per step; an overflowing view renders nothing and the step is rerun.
 ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_errors,
-                       int row0 = 0, int row1 = -1) {
+                       int row0 = 0, int row1 = -1, const ViewSlots* defer = nullptr) {
     ViewRender vr{};
     vr.W = dc.W;
     vr.H = dc.H;
@@ -601,18 +621,15 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.large = c.large.as<int>(K + 1);
     b.n_large = &c.dstat->n_large;
     b.off_r = c.off_r.as<long long>(K + 1);
-    b.tile_start = c.tile_start.as<int>(n_tiles);
-    b.tile_end = c.tile_end.as<int>(n_tiles);
-    size_t tb = std::max(depth_sort_temp_bytes(K), scan_temp_bytes(K));
-    b.temp = c.temp.ensure(tb);
+    b.tile_start = c.tile_start.as<int>(std::max(n_tiles, 1));
+    b.tile_end = c.tile_end.as<int>(std::max(n_tiles, 1));
+    b.temp = c.temp.ensure(std::max(depth_sort_temp_bytes(K), scan_temp_bytes(K)));
     b.temp_bytes = c.temp.bytes;
     double* rec = c.rec.as<double>((size_t)kRec * (K + 1));
     b.rec = rec;
+    if (c.dup_cap == 0) c.dup_cap = 4LL * K + 65536;  // grown on demand
 
-    ViewStatus init{INT_MAX, INT_MAX, 0, 0, 0};
-    c.hstat->vs = init;
-    SGTR_CUDA(cudaMemcpyAsync(&c.dstat->vs, &c.hstat->vs, sizeof(ViewStatus),
-                              cudaMemcpyHostToDevice, c.st));
+    view_begin(c.st, &c.dstat->vs);
     {
         Timed t(c, KC_PROJECT);
         launch_project(c.st, c.X(), K, c.nb, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, b.tmask,
@@ -622,57 +639,65 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
         Timed t(c, KC_DEPTH_SORT);
         depth_sort_and_scan(c.st, b, K);
     }
-    c.launches += 1 + 6 + 1 + 3;  // project, onesweep sort (histogram + 5 passes), tie fix, counts + scan
-    SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs.n_dup, b.off_r + K, sizeof(long long),
-                              cudaMemcpyDeviceToHost, c.st));
-    SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs, &c.dstat->vs, offsetof(ViewStatus, n_dup),
-                              cudaMemcpyDeviceToHost, c.st));
-    SGTR_CUDA(cudaStreamSynchronize(c.st));
-    const ViewStatus vs = c.hstat->vs;
-    if (vs.nonfinite_splat != INT_MAX) {
-        vr.err_kind = 1;
-        vr.err_index = vs.nonfinite_splat;
-    } else if (vs.degenerate_splat != INT_MAX) {
-        vr.err_kind = 2;
-        vr.err_index = vs.degenerate_splat;
+    // view begin, project, onesweep sort (histogram + 5 passes), tie fix, counts + scan
+    c.launches += 1 + 1 + 6 + 1 + 3;
+    if (defer) {
+        view_end(c.st, &c.dstat->vs, b.off_r + K, c.dup_cap, defer->errk, defer->erri,
+                 defer->ndup, defer->ovf);
+        c.launches += 1;
+        vr.n_visible = -1;
+        vr.n_dup = -1;
+    } else {
+        SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs, &c.dstat->vs, sizeof(ViewStatus),
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaMemcpyAsync(&c.hstat->vs.n_dup, b.off_r + K, sizeof(long long),
+                                  cudaMemcpyDeviceToHost, c.st));
+        SGTR_CUDA(cudaStreamSynchronize(c.st));
+        const ViewStatus vs = c.hstat->vs;
+        if (vs.nonfinite_splat != INT_MAX) {
+            vr.err_kind = 1;
+            vr.err_index = vs.nonfinite_splat;
+        } else if (vs.degenerate_splat != INT_MAX) {
+            vr.err_kind = 2;
+            vr.err_index = vs.degenerate_splat;
+        }
+        if (vr.err_kind && throw_errors) {
+            if (vr.err_kind == 1)
+                throw numeric("rasterize: non-finite parameter in splat " +
+                              std::to_string(vr.err_index));
+            throw invalid("quat_to_rotation: degenerate quaternion");
+        }
+        if (vr.err_kind) return vr;
+        vr.n_visible = vs.n_visible;
+        vr.n_dup = vs.n_dup;
+        if (vr.n_dup > INT_MAX) throw Error(SGTR_RUNTIME, "binning: more than 2^31 tile duplicates");
+        if (vr.n_dup > c.dup_cap) c.dup_cap = grow_cap(vr.n_dup);
     }
-    if (vr.err_kind && throw_errors) {
-        if (vr.err_kind == 1)
-            throw numeric("rasterize: non-finite parameter in splat " + std::to_string(vr.err_index));
-        throw invalid("quat_to_rotation: degenerate quaternion");
-    }
-    if (vr.err_kind) return vr;
-    vr.n_visible = vs.n_visible;
-    vr.n_dup = vs.n_dup;
-    if (vr.n_dup > INT_MAX) throw Error(SGTR_RUNTIME, "binning: more than 2^31 tile duplicates");
-    const long long nd = std::max(vr.n_dup, 1LL);
-    b.tkeys = c.tkeys.as<unsigned int>(nd);
-    b.tkeys_alt = c.tkeys_alt.as<unsigned int>(nd);
-    b.dval = c.dval.as<int>(nd);
-    b.dval_alt = c.dval_alt.as<int>(nd);
-    b.dup_id = c.dup_id.as<int>(nd);
-    b.temp = c.temp.ensure(std::max(tb, tile_sort_temp_bytes(vr.n_dup, n_tiles)));
+    const long long cap = c.dup_cap;
+    vr.cap = cap;
+    b.tkeys = c.tkeys.as<unsigned int>(cap);
+    b.tkeys_alt = c.tkeys_alt.as<unsigned int>(cap);
+    b.dval = c.dval.as<int>(cap);
+    b.dval_alt = c.dval_alt.as<int>(cap);
+    b.dup_id = c.dup_id.as<int>(cap);
+    b.tile_ids = c.tile_ids.as<int>(cap);
+    b.trect = c.trect.as<int4>(cap);
+    b.temp = c.temp.ensure(std::max({depth_sort_temp_bytes(K), scan_temp_bytes(K),
+                                     tile_sort_temp_bytes(cap, n_tiles)}));
     b.temp_bytes = c.temp.bytes;
     {
         Timed t(c, KC_TILE_BIN);
-        emit_and_sort_tiles(c.st, b, vr.n_visible, vr.n_dup, tiles_x, n_tiles);
+        bin_tiles(c.st, b, K, tiles_x, n_tiles, cap);
     }
-    c.launches += vr.n_dup ? 6 : 0;  // emit (2), tile sort (histogram + 2 passes), ranges
-    int* tids = c.tile_ids.as<int>(nd);
-    {
-        Timed t(c, KC_TILE_BIN);
-        launch_tile_ids(c.st, b.tkeys_alt, b.dval_alt, b.dup_id, vr.n_dup, b.rect, tids,
-                        c.trect.as<int4>(nd), b.tile_start, b.tile_end);
-    }
-    c.launches += vr.n_dup ? 1 : 0;
+    c.launches += 6;  // emit (2), padding, tile sort (histogram + 2 passes), ranges + ids
     vr.tl = TileLists{tiles_x, tiles_y, b.tile_start, b.tile_end, b.dval_alt,
-                      b.dup_id,  tids,    c.trect.get<int4>(), row0,
+                      b.dup_id,  b.tile_ids, b.trect, row0,
                       row1 < 0 ? tiles_y : row1};
     // the raster kernels' CTAs in order of decreasing tile-list length: the
     // long tiles start first, so the grid does not end on a few of them
     // (SGTR_TILE_ORDER=0: row-major); full frames only
     static const bool by_length = getenv("SGTR_TILE_ORDER") ? atoi(getenv("SGTR_TILE_ORDER")) : 1;
-    if (by_length && vr.n_dup && vr.tl.row0 == 0 && vr.tl.row1 == tiles_y) {
+    if (by_length && vr.tl.row0 == 0 && vr.tl.row1 == tiles_y) {
         Timed t(c, KC_TILE_BIN);
         int* order = c.ovals.as<int>(n_tiles);
         launch_tile_order(c.st, b.tile_start, b.tile_end, n_tiles, order);
@@ -690,7 +715,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
 // K10 + K11 for an image-space adjoint already in c.adj
 void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender& vr, int mode,
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
-    const long long nd = std::max(vr.n_dup, 1LL);
+    const long long nd = std::max(vr.cap, 1LL);
     double* part = c.part.as<double>((size_t)kVjpSlots * kAdj * nd);
     unsigned char* mask = c.mask.as<unsigned char>((size_t)kVjpSlots * nd);
     {
@@ -703,8 +728,8 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
     Timed t(c, KC_CHAIN);
     long long* off_id = c.off_id.as<long long>(std::max(c.K, 1));
     launch_offsets_by_id(c.st, c.ids_alt.get<int>(), c.K, c.off_r.get<long long>(), off_id);
-    launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, off_id, c.tcount.get<int>(), part,
-                      mask, zdense, zbits, acc, flag);
+    launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, off_id, c.tcount.get<int>(), vr.cap,
+                      part, mask, zdense, zbits, acc, flag);
     c.launches += 3;
 }
 
@@ -903,9 +928,14 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     c.fail_sample = -1;
     // fused buffer, summed by one allreduce per step:
     //   [g_acc (dim) | loss[n1] | gflag[n1] | hflag[nu] | err_kind[n1+n2] |
-    //    err_index[n1+n2] | w_acc (dim, refresh steps only)]
+    //    err_index[n1+n2] | n_dup[n1+n2] | overflows | w_acc (dim, refresh steps only)]
+    // The views render without host round trips (render_view's deferred
+    // mode): their errors, duplicate totals and capacity overflows arrive
+    // here, read once per step.  A step in which some view (on any rank)
+    // outgrew the duplicate capacity is rerun with the capacity grown to the
+    // largest total -- before anything but device scratch has changed.
     const int nflag = refresh ? nu : 1;
-    const size_t tail_n = 2 * n1 + nflag + 2 * (n1 + n2);
+    const size_t tail_n = 2 * n1 + nflag + 3 * (n1 + n2) + 1;
     const size_t tail_off = dim;
     double* fused = c.fused.as<double>(2 * dim + tail_n);
     double* g_acc = fused;
@@ -915,11 +945,14 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     double* gflag = tail + n1;
     double* hflag = tail + 2 * n1;
     double* errk = tail + 2 * n1 + nflag;
+    double* erri = errk + (n1 + n2);
+    double* ndup = erri + (n1 + n2);
+    double* novf = ndup + (n1 + n2);
     const size_t fused_n = dim + tail_n + (refresh ? dim : 0);
-    SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
     ensure_tail(c, tail_n);
-    std::vector<double> herr(2 * (n1 + n2), 0.0);
-    bool local_error = false;
+    int reruns = 0;
+    for (;;) {
+    SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
     // gradient phase: stochastic_gradient (optimizer.cpp:36-65), views of S1
     // split round-robin over ranks (sgtr_shard_views).  Local view li adds
     // its gradient into accumulator li % 2 and accumulator 1 is added to
@@ -944,16 +977,11 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         SGTR_CUDA(cudaMemsetAsync(gl[1], 0, sizeof(double) * dim, ls));
     }
     int li = 0;
-    for (int p = c.rank; p < n1 && !local_error; p += c.nranks, ++li) {
+    for (int p = c.rank; p < n1; p += c.nranks, ++li) {
         use_lane(c, li % lanes);
         const View& v = c.views[s1[p]];
-        const ViewRender vr = render_view(c, v.dc, ro, false);
-        if (vr.err_kind) {
-            herr[p] = vr.err_kind;
-            herr[(n1 + n2) + p] = vr.err_index;
-            local_error = true;
-            break;
-        }
+        const ViewSlots vslots{errk + p, erri + p, ndup + p, novf};
+        const ViewRender vr = render_view(c, v.dc, ro, false, 0, -1, &vslots);
         residual_adjoint(c, GRAD, W, H, view_gt(c, s1[p]), nullptr, nullptr, o.residual.lambda,
                          o.residual.floor, loss + p);
         backward_view(c, v.dc, ro, vr, 0, nullptr, nullptr, gl[li % 2], gflag + p);
@@ -968,7 +996,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         c.launches += 1;
     }
     // Hutchinson phase (optimizer.cpp:75-104), views of S2 split over ranks
-    if (refresh && !local_error) {
+    if (refresh) {
         const long long words = (dim + 31) / 32;
         uint32_t* dz = c.zbits.as<uint32_t>(std::max<long long>(words * nu, 1));
         SGTR_CUDA(cudaMemcpyAsync(dz, zbits.data(), sizeof(uint32_t) * words * nu,
@@ -984,25 +1012,22 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         const int tiles_y = ceil_div(H, kTile);
         const bool by_view = c.refresh_bands <= 1 && n2 >= c.nranks;
         const int B = by_view ? 1 : std::min(tiles_y, c.nranks * c.refresh_bands);
-        for (int s = 0; s < nu && !local_error; ++s) {
+        for (int s = 0; s < nu; ++s) {
             const uint32_t* zb = dz + words * s;
-            for (int q = 0; q < n2 && !local_error; ++q) {
+            for (int q = 0; q < n2; ++q) {
                 if (by_view && q % c.nranks != c.rank) continue;
-                for (int band = 0; band < B && !local_error; ++band) {
+                for (int band = 0; band < B; ++band) {
                     if (!by_view && band % c.nranks != c.rank) continue;
                     const int tr0 = band * tiles_y / B, tr1 = (band + 1) * tiles_y / B;
                     if (tr1 <= tr0) continue;
                     const int r0 = std::max(0, tr0 - 1), r1 = std::min(tiles_y, tr1 + 1);
                     const View& v = c.views[s2[q]];
-                    const ViewRender vr =
-                        B == 1 ? render_view(c, v.dc, ro, false)
-                               : render_view(c, v.dc, ro, false, r0, r1);
-                    if (vr.err_kind) {
-                        herr[n1 + q] = vr.err_kind;
-                        herr[(n1 + n2) + n1 + q] = vr.err_index;
-                        local_error = true;
-                        break;
-                    }
+                    // the view's status is reported by its band 0 only (one
+                    // writer per slot across ranks: the tail is summed)
+                    ViewSlots vslots{nullptr, nullptr, nullptr, novf};
+                    if (band == 0) vslots = {errk + n1 + q, erri + n1 + q, ndup + n1 + q, novf};
+                    const ViewRender vr = B == 1 ? render_view(c, v.dc, ro, false, 0, -1, &vslots)
+                                                 : render_view(c, v.dc, ro, false, r0, r1, &vslots);
                     double* trec = c.trec.as<double>((size_t)kTRec * (c.K + 1));
                     {
                         Timed t(c, KC_PROJECT_JVP);
@@ -1034,13 +1059,17 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
             }
         }
     }
-    if (local_error)
-        SGTR_CUDA(cudaMemcpyAsync(errk, herr.data(), sizeof(double) * herr.size(),
-                                  cudaMemcpyHostToDevice, c.st));
     allreduce(c, fused, fused_n);
     SGTR_CUDA(cudaMemcpyAsync(c.htail, tail, sizeof(double) * tail_n, cudaMemcpyDeviceToHost,
                               c.st));
     SGTR_CUDA(cudaStreamSynchronize(c.st));
+    if (c.htail[tail_n - 1] == 0.0) break;
+    double need = 0.0;
+    for (int j = 0; j < n1 + n2; ++j) need = std::max(need, c.htail[2 * n1 + nflag + 2 * (n1 + n2) + j]);
+    if (need > (double)INT_MAX) throw Error(SGTR_RUNTIME, "binning: more than 2^31 tile duplicates");
+    c.dup_cap = std::max(c.dup_cap, grow_cap((long long)need));
+    ++reruns;
+    }
     const double* ht = c.htail;
     const double* hk = ht + 2 * n1 + nflag;
     const double* hi = hk + (n1 + n2);
@@ -1206,6 +1235,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     harvest_timing(c);
     diag->gnorm = std::sqrt(c.hstat->tr[0]);
     diag->refreshed = refresh ? 1 : 0;
+    diag->reruns = reruns;
     diag->n_local_views = 0;
     for (int p = c.rank; p < n1; p += c.nranks) ++diag->n_local_views;
     if (hutch_fail) {
@@ -2390,9 +2420,9 @@ int sgtr_dump_binning(sgtr_ctx* ctx, const sgtr_camera* cam, const sgtr_render_o
         }
         SGTR_CUDA(cudaStreamSynchronize(c.st));
         for (int i = 0; i < vr.n_visible; ++i) order[i] = ids[i];
-        for (int t = 0; t < n_tiles; ++t) {
-            tile_start[t] = ts[t];
-            tile_end[t] = te[t];
+        for (int t = 0; t < n_tiles; ++t) {  // empty tiles as [0, 0) (the oracle's convention)
+            tile_start[t] = ts[t] == te[t] ? 0 : ts[t];
+            tile_end[t] = ts[t] == te[t] ? 0 : te[t];
         }
         for (long long j = 0; j < vr.n_dup; ++j) lists[j] = did[dv[j]];
     });
@@ -2628,6 +2658,14 @@ int sgtr_nccl_unique_id(uint8_t out[128]) {
     return guarded([&] {
         g_nccl.load();
         g_nccl.check(g_nccl.get_unique_id(out), "ncclGetUniqueId");
+    });
+}
+
+int sgtr_set_dup_capacity(sgtr_ctx* ctx, int64_t capacity) {
+    return guarded([&] {
+        if (capacity < 0) throw invalid("sgtr_set_dup_capacity: negative capacity");
+        if (capacity > INT_MAX) throw invalid("sgtr_set_dup_capacity: more than 2^31 entries");
+        ctx_ref(ctx).dup_cap = capacity;
     });
 }
 

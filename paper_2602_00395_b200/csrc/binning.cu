@@ -7,6 +7,13 @@
 // render.cpp:83-87), and duplicates are emitted in depth-rank order so the
 // stable sort on the tile id alone leaves every tile list in (depth, index)
 // order.
+//
+// No size is read back on the host: the duplicate arrays have a capacity
+// `cap`, entries [n_dup, cap) carry a sentinel tile key that sorts last, and
+// a view whose n_dup exceeds cap is binned as empty and reports it (the step
+// reruns with a larger capacity, api.cu step_core).
+#include <climits>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -54,22 +61,22 @@ __global__ void k_gather_counts(const int* __restrict__ sorted_ids,
     if (r == K) cnt[r] = 0;
 }
 
-// K4a: one thread per visible splat (depth-rank order).  Rectangles of <= 64
-// tiles are emitted from the hit bits K1 recorded, in row-major tile order;
-// larger ones are queued for K4b.
+// K4a: one thread per depth rank (n_visible = K: the culled splats sort last
+// with no tiles).  Rectangles of <= 64 tiles are emitted from the hit bits K1
+// recorded, in row-major tile order; larger ones are queued for K4b.
 __global__ void __launch_bounds__(256) k_emit_small(const int* __restrict__ sorted_ids,
                                                     const int* __restrict__ tcount,
                                                     const int4* __restrict__ rect,
                                                     const unsigned long long* __restrict__ tmask,
                                                     const long long* __restrict__ off_r,
-                                                    int n_visible, int tiles_x,
+                                                    int n_visible, int tiles_x, long long cap,
                                                     unsigned int* __restrict__ tkeys,
                                                     int* __restrict__ dval,
                                                     int* __restrict__ dup_id,
                                                     int* __restrict__ large,
                                                     int* __restrict__ n_large) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_visible) return;
+    if (r >= n_visible || off_r[n_visible] > cap) return;
     const int id = sorted_ids[r];
     if (tcount[id] == 0) return;
     const int4 pr = rect[id];
@@ -137,23 +144,60 @@ __global__ void __launch_bounds__(256) k_emit_large(const int* __restrict__ sort
     }
 }
 
-// per tile-sorted position j: the tile ranges (K6), and tile-sorted copies
-// of the splat id and of its exact pixel rectangle (K1's pixel_range of the
-// FP64 bbox), which the rasterisers test per warp
+// K6, per tile-sorted position j < cap: the tile ranges, and tile-sorted
+// copies of the splat id and of its exact pixel rectangle (K1's pixel_range of
+// the FP64 bbox), which the rasterisers test per warp.  Entries with the
+// sentinel key (the padding [n_dup, cap), or everything on an overflow) sort
+// last and are skipped.
 __global__ void k_tile_ids(const unsigned int* __restrict__ tkeys, const int* __restrict__ sorted_d,
-                           const int* __restrict__ dup_id, long long n,
+                           const int* __restrict__ dup_id, long long n, unsigned int sentinel,
                            const int4* __restrict__ rect, int* __restrict__ tile_ids,
                            int4* __restrict__ trect, int* __restrict__ start,
                            int* __restrict__ end) {
     const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const unsigned int k = tkeys[j];
+    if (k == sentinel) return;
     if (j == 0 || tkeys[j - 1] != k) start[k] = (int)j;
     if (j == n - 1 || tkeys[j + 1] != k) end[k] = (int)(j + 1);
     const int id = dup_id[sorted_d[j]];
     tile_ids[j] = id;
     trect[j] = rect[id];
 }
+
+// the sentinel key into [n_dup, cap) (all of [0, cap) when n_dup > cap)
+__global__ void k_pad_keys(const long long* __restrict__ total, long long cap,
+                           unsigned int sentinel, unsigned int* __restrict__ tkeys) {
+    const long long nd = *total;
+    const long long j0 = nd > cap ? 0 : nd;
+    for (long long j = j0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; j < cap;
+         j += (long long)gridDim.x * blockDim.x)
+        tkeys[j] = sentinel;
+}
+
+// per view, before K1: the status block reset
+__global__ void k_view_begin(ViewStatus* __restrict__ vs) {
+    *vs = ViewStatus{INT_MAX, INT_MAX, 0, 0, 0};
+}
+
+// a deferred view: its error, duplicate total and overflow count into the
+// step's fused tail (summed over ranks with the gradient)
+__global__ void k_view_end(const ViewStatus* __restrict__ vs, const long long* __restrict__ total,
+                           long long cap, double* errk, double* erri, double* ndup,
+                           double* ovf) {
+    if (errk) {
+        if (vs->nonfinite_splat != INT_MAX) {
+            *errk = 1.0;
+            *erri = vs->nonfinite_splat;
+        } else if (vs->degenerate_splat != INT_MAX) {
+            *errk = 2.0;
+            *erri = vs->degenerate_splat;
+        }
+    }
+    if (ndup) *ndup = (double)*total;
+    if (*total > cap) atomicAdd(ovf, 1.0);
+}
+
 __global__ void __launch_bounds__(1024) k_tile_order(const int* __restrict__ start,
                                                      const int* __restrict__ end, int n,
                                                      int* __restrict__ order) {
@@ -188,14 +232,17 @@ int bits_for(int n) {
 
 }  // namespace
 
-void launch_tile_ids(cudaStream_t st, const unsigned int* tkeys, const int* sorted_d,
-                     const int* dup_id, long long n, const int4* rect, int* tile_ids, int4* trect,
-                     int* tile_start, int* tile_end) {
-    if (n == 0) return;
-    k_tile_ids<<<ceil_div(n, 256), 256, 0, st>>>(tkeys, sorted_d, dup_id, n, rect, tile_ids, trect,
-                                                  tile_start, tile_end);
+void view_begin(cudaStream_t st, ViewStatus* vs) {
+    k_view_begin<<<1, 1, 0, st>>>(vs);
     SGTR_CUDA(cudaGetLastError());
 }
+
+void view_end(cudaStream_t st, const ViewStatus* vs, const long long* total, long long cap,
+              double* errk, double* erri, double* ndup, double* ovf) {
+    k_view_end<<<1, 1, 0, st>>>(vs, total, cap, errk, erri, ndup, ovf);
+    SGTR_CUDA(cudaGetLastError());
+}
+
 size_t depth_sort_temp_bytes(int K) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
@@ -211,11 +258,11 @@ size_t scan_temp_bytes(int K) {
     return bytes;
 }
 
-size_t tile_sort_temp_bytes(long long n_dup, int n_tiles) {
+size_t tile_sort_temp_bytes(long long cap, int n_tiles) {
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned int*)nullptr,
                                     (unsigned int*)nullptr, (int*)nullptr, (int*)nullptr,
-                                    (int)n_dup, 0, bits_for(n_tiles));
+                                    (int)cap, 0, bits_for(n_tiles + 1));
     return bytes;
 }
 
@@ -242,23 +289,29 @@ void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
     SGTR_CUDA(cub::DeviceScan::ExclusiveSum(b.temp, bytes, cnt, b.off_r, K + 1, st));
 }
 
-void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long long n_dup,
-                         int tiles_x, int n_tiles) {
+void bin_tiles(cudaStream_t st, BinBuffers& b, int K, int tiles_x, int n_tiles, long long cap) {
     SGTR_CUDA(cudaMemsetAsync(b.tile_start, 0, sizeof(int) * n_tiles, st));
     SGTR_CUDA(cudaMemsetAsync(b.tile_end, 0, sizeof(int) * n_tiles, st));
-    if (n_dup == 0) return;
+    if (K == 0 || n_tiles == 0) return;
+    const unsigned int sentinel = (unsigned int)n_tiles;
     SGTR_CUDA(cudaMemsetAsync(b.n_large, 0, sizeof(int), st));
-    k_emit_small<<<ceil_div(n_visible, 256), 256, 0, st>>>(
-        b.ids_alt, b.tcount, b.rect, b.tmask, b.off_r, n_visible, tiles_x, b.tkeys, b.dval,
-        b.dup_id, b.large, b.n_large);
+    k_emit_small<<<ceil_div(K, 256), 256, 0, st>>>(b.ids_alt, b.tcount, b.rect, b.tmask, b.off_r, K,
+                                                   tiles_x, cap, b.tkeys, b.dval, b.dup_id, b.large,
+                                                   b.n_large);
     SGTR_CUDA(cudaGetLastError());
     k_emit_large<<<148 * 4, 256, 0, st>>>(b.ids_alt, b.rect, b.rec, b.off_r, tiles_x, b.large,
                                           b.n_large, b.tkeys, b.dval, b.dup_id);
     SGTR_CUDA(cudaGetLastError());
+    k_pad_keys<<<148 * 4, 256, 0, st>>>(b.off_r + K, cap, sentinel, b.tkeys);
+    SGTR_CUDA(cudaGetLastError());
     size_t bytes = b.temp_bytes;
     SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.tkeys, b.tkeys_alt, b.dval,
-                                              b.dval_alt, (int)n_dup, 0, bits_for(n_tiles),
+                                              b.dval_alt, (int)cap, 0, bits_for(n_tiles + 1),
                                               st));
+    k_tile_ids<<<ceil_div(cap, 256), 256, 0, st>>>(b.tkeys_alt, b.dval_alt, b.dup_id, cap, sentinel,
+                                                   b.rect, b.tile_ids, b.trect, b.tile_start,
+                                                   b.tile_end);
+    SGTR_CUDA(cudaGetLastError());
 }
 
 }  // namespace sgtr

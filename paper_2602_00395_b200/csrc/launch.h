@@ -36,25 +36,36 @@ struct BinBuffers {
     unsigned long long* tmask;  // tile-hit bits per splat (rects <= 64 tiles)
     int* large;            // depth ranks of splats with > 64-tile rectangles
     int* n_large;
-    long long* off_r;      // n+1 exclusive offsets in depth-rank order
+    long long* off_r;      // K+1 exclusive duplicate offsets in depth-rank order
+    // duplicate arrays, capacity `cap` entries
     unsigned int *tkeys, *tkeys_alt;
     int *dval, *dval_alt;  // duplicate index carried through the tile sort
     int* dup_id;           // duplicate -> splat id
+    int* tile_ids;         // per tile-sorted position: splat id
+    int4* trect;           // per tile-sorted position: the splat's pixel rectangle
     int *tile_start, *tile_end;
     void* temp;
     size_t temp_bytes;
 };
 size_t depth_sort_temp_bytes(int K);
 size_t scan_temp_bytes(int K);
-size_t tile_sort_temp_bytes(long long n_dup, int n_tiles);
+size_t tile_sort_temp_bytes(long long cap, int n_tiles);
+// per view, before K1: status reset
+void view_begin(cudaStream_t st, ViewStatus* vs);
 // K2 (+ the K3 scan): sorts keys, returns sorted ids in b.ids_alt and the
-// exclusive tile-count offsets (total at off_r[K])
+// exclusive duplicate offsets (total at off_r[K])
 void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K);
-// K4-K5: duplicates, stable tile sort (the ranges come with launch_tile_ids)
-void emit_and_sort_tiles(cudaStream_t st, BinBuffers& b, int n_visible, long long n_dup,
-                         int tiles_x, int n_tiles);
+// K4-K6 without a host round trip: emission, stable tile sort of `cap`
+// entries (the tail padded with a sentinel key), tile ranges and the
+// tile-sorted splat ids / rectangles; a view with off_r[K] > cap is binned
+// empty
+void bin_tiles(cudaStream_t st, BinBuffers& b, int K, int tiles_x, int n_tiles, long long cap);
+// a view whose status is not read back on the host: its error, duplicate
+// total and overflow (total > cap) into the step's tail slots (errk/erri/
+// ndup may be null)
+void view_end(cudaStream_t st, const ViewStatus* vs, const long long* total, long long cap,
+              double* errk, double* erri, double* ndup, double* ovf);
 
-// ---------------------------------------------------------------- raster.cu
 struct TileLists {
     int tiles_x, tiles_y;
     const int* tile_start;
@@ -82,24 +93,20 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
-// K11: per splat, the sum of its flagged K10 partials (duplicate, block order)
-// and the chain through invert2x2 and the projection; mode 0 adds the
-// gradient into acc, mode 1 z (.) it (Hutchinson, probe dense or as bits); a
-// non-finite contribution stores 1.0 into *nonfinite_flag.
 // splat id -> offset of its duplicates (off_r scattered from depth-rank order)
 void launch_offsets_by_id(cudaStream_t st, const int* sorted_ids, int K, const long long* off_r,
                           long long* off_id);
-// K11: per splat (id order) the fixed-order sum of its K10 partials and the
-// chain rule to the 14 (+ SH) parameters, added into acc
+// K11: per splat (id order), the sum of its flagged K10 partials (duplicate,
+// block order) and the chain through invert2x2 and the projection; mode 0
+// adds the gradient into acc, mode 1 z (.) it (Hutchinson, probe dense or as
+// bits); a non-finite contribution stores 1.0 into *nonfinite_flag.  Splats
+// whose duplicates lie beyond the capacity `cap` are skipped (an overflowed
+// view, rerun by the step).
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                        const RenderP& ro, const long long* off_id, const int* tcount,
-                       const double* part, const unsigned char* mask, const double* zdense,
-                       const uint32_t* zbits, double* acc, double* nonfinite_flag);
-// per tile-sorted position j: tile ranges from the sorted keys (K6),
-// tile_ids[j] = dup_id[sorted_d[j]], trect[j] = rect[tile_ids[j]]
-void launch_tile_ids(cudaStream_t st, const unsigned int* tkeys, const int* sorted_d,
-                     const int* dup_id, long long n, const int4* rect, int* tile_ids, int4* trect,
-                     int* tile_start, int* tile_end);
+                       long long cap, const double* part, const unsigned char* mask,
+                       const double* zdense, const uint32_t* zbits, double* acc,
+                       double* nonfinite_flag);
 // K12 (raster half): tangent image along the tangent records
 void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro,

@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
         if (!finite) atomicMin(&status->nonfinite_splat, i);
         const Proj<double> pr = project_primal(p, cam, ro);
         if (!pr.culled && pr.degenerate) atomicMin(&status->degenerate_splat, i);
-        if (pr.culled || pr.degenerate) {
+        // a non-finite splat fails the view (its error is reported); it is not
+        // binned, so its NaN rectangle cannot inflate the duplicate count
+        if (pr.culled || pr.degenerate || !finite) {
             keys[i] = kCulledKey;
             tcount[i] = 0;
         } else {
@@ -236,7 +238,7 @@ template <bool kSH>
 __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
                                                const long long* __restrict__ off_id,
-                                               const int* __restrict__ tcount,
+                                               const int* __restrict__ tcount, long long cap,
                                                const double* __restrict__ part,
                                                const unsigned char* __restrict__ mask,
                                                const double* __restrict__ zdense,
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     const int cnt = tcount[id];
     if (cnt == 0) return;
     const long long off = off_id[id];
+    if (off + cnt > cap) return;  // an overflowed view (rerun)
     // the splat's parameters, fetched now: their latency overlaps the
     // partial sums
     const Splat p = load_splat(x, K, id);
@@ -395,18 +398,18 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const D
 
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb,
                        const DevCam& cam, const RenderP& ro, const long long* off_id,
-                       const int* tcount, const double* part, const unsigned char* mask,
-                       const double* zdense, const uint32_t* zbits, double* acc,
-                       double* nonfinite_flag) {
+                       const int* tcount, long long cap, const double* part,
+                       const unsigned char* mask, const double* zdense, const uint32_t* zbits,
+                       double* acc, double* nonfinite_flag) {
     if (K == 0) return;
     if (nb)
         k_chain_warp<true><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
-                                                             tcount, part, mask, zdense, zbits,
-                                                             acc, nonfinite_flag);
+                                                             tcount, cap, part, mask, zdense,
+                                                             zbits, acc, nonfinite_flag);
     else
         k_chain_warp<false><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
-                                                              tcount, part, mask, zdense, zbits,
-                                                              acc, nonfinite_flag);
+                                                              tcount, cap, part, mask, zdense,
+                                                              zbits, acc, nonfinite_flag);
     SGTR_CUDA(cudaGetLastError());
 }
 

@@ -298,6 +298,7 @@ class StepDiagnostics:  # optimizer.hpp:74-83
     applied_step: Optional[np.ndarray] = None
     refreshed: bool = False
     n_local_views: int = 0  # views of the batch this rank rendered (multi-rank split)
+    reruns: int = 0  # reruns after a view outgrew the tile-duplicate capacity
 
 
 # ------------------------------------------------------------------ context
@@ -506,11 +507,16 @@ class Context:
                                                    C.byref(d)))
         out = StepDiagnostics(d.batch_loss, d.gnorm, d.step_pre, d.step_post, d.clip_frac,
                               d.eps, d.max_step_over_radius, None, bool(d.refreshed),
-                              int(d.n_local_views))
+                              int(d.n_local_views), int(d.reruns))
         if opt.record_applied_step:
             out.applied_step = np.empty(self.dim)
             check(lib().sgtr_get_applied_step(self._h, _ptr(out.applied_step)))
         return out
+
+    def set_dup_capacity(self, capacity: int) -> None:
+        """Presize (or shrink) the per-view tile-duplicate arrays; a step
+        whose views outgrow them reruns with a grown capacity (0: default)."""
+        check(lib().sgtr_set_dup_capacity(self._h, capacity))
 
     def set_refresh_bands(self, bands_per_rank: int) -> None:
         """Split each refresh view into nranks * bands_per_rank row bands."""

@@ -1,5 +1,7 @@
 """Print a hash of the scene after a few training steps (A/B bit-identity
-checks between builds: SGTR_LIB=<other libsgtr.so> python tools/scene_hash.py)."""
+checks between builds: SGTR_LIB=<other libsgtr.so> python tools/scene_hash.py).
+
+  python tools/scene_hash.py [config] [steps] [duplicate capacity before the steps]"""
 import hashlib
 import sys
 
@@ -13,9 +15,11 @@ ctx = sp.Context(0)
 k, v, w, h, b, sh = bench.CONFIGS[cfg]
 bench.make_dataset(sp, ctx, cfg, 0)
 ctx.state_reset(0)
+if len(sys.argv) > 3:
+    ctx.set_dup_capacity(int(sys.argv[3]))
 opt = sp.OptimizerOptions(batch_size=b, schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 30000),
                           record_applied_step=False)
-for _ in range(steps):
-    ctx.step(opt)
+reruns = sum(ctx.step(opt).reruns for _ in range(steps))
 x = ctx.get_scene()
+print("reruns", reruns)
 print(cfg, steps, hashlib.sha256(x.tobytes()).hexdigest()[:16])
