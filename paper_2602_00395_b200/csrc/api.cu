@@ -368,12 +368,12 @@ typedef int (*CommInitRankFn)(void**, int, UniqueId, int);
 enum KClass {
     KC_PROJECT, KC_DEPTH_SORT, KC_TILE_BIN, KC_RASTER_FWD, KC_SSIM, KC_GATHER,
     KC_RASTER_VJP, KC_CHAIN, KC_PROJECT_JVP, KC_RASTER_JVP, KC_TR_UPDATE, KC_TR_BISECT,
-    KC_TR_APPLY, KC_COUNT
+    KC_TR_APPLY, KC_TR_ROT, KC_COUNT
 };
 const char* const kClassNames[KC_COUNT] = {
     "project", "depth_sort_scan", "tile_binning", "raster_fwd", "ssim_residual",
     "ssim_gather", "raster_vjp", "chain", "project_jvp", "raster_jvp", "tr_update",
-    "tr_bisect", "tr_apply"};
+    "tr_bisect", "tr_apply", "tr_rotation"};
 
 struct KTimer {
     bool on = false;
@@ -1199,6 +1199,10 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         {
             Timed t(c, KC_TR_UPDATE);
             launch_tr_update(c.st, a, 0);
+        }
+        {
+            Timed t(c, KC_TR_ROT);
+            launch_tr_update(c.st, a, 3);
         }
         {
             Timed t(c, KC_TR_BISECT);

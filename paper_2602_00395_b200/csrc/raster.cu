@@ -307,25 +307,22 @@ __global__ void __launch_bounds__(32 * WPB)
         cp_async_wait<1>();
         __syncwarp();
         const StagedRec* my_rec = s_rec[lw][buf];
-        unsigned wb = __reduce_or_sync(kFull, mine);
-        while (wb) {
-            const int j0 = __ffs(wb) - 1;
-            wb &= wb - 1u;
-            if (wb) {
-                const int j1 = __ffs(wb) - 1;
-                wb &= wb - 1u;
-                const bool h0 = (mine >> j0) & 1u, h1 = (mine >> j1) & 1u;
-                const StagedRec r0 = my_rec[j0], r1 = my_rec[j1];
-                const double ab0 = falloff(r0), ab1 = falloff(r1);
-                if (h0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, base + j0);
-                if (h1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, base + j1);
-            } else if ((mine >> j0) & 1u) {
-                const StagedRec r = my_rec[j0];
-                const double ab = falloff(r);
-                if (!(ab < ro.alpha_skip)) blend(r, ab, base + j0);
-            }
+        // every lane walks its own entries, two per round (two independent
+        // exp chains, then the blends in list order): the warp runs as many
+        // rounds as its busiest pixel needs, not one per entry any pixel
+        // needs, and no lane evaluates an entry that misses its pixel
+        while (__any_sync(kFull, mine != 0u)) {
+            const bool has0 = mine != 0u;
+            const int j0 = has0 ? __ffs(mine) - 1 : 0;
+            mine &= mine - 1u;
+            const bool has1 = mine != 0u;
+            const int j1 = has1 ? __ffs(mine) - 1 : j0;
+            mine &= mine - 1u;
+            const StagedRec r0 = my_rec[j0], r1 = my_rec[j1];
+            const double ab0 = falloff(r0), ab1 = falloff(r1);
+            if (has0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, base + j0);
+            if (has1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, base + j1);
             if (done) mine = 0u;
-            wb &= __reduce_or_sync(kFull, mine);
         }
         __syncwarp();
         slots_cur = slots_next;

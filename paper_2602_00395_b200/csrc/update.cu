@@ -561,12 +561,11 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
             k_tr_prepare<<<nbp, kThreads, 0, st>>>(a);
             SGTR_CUDA(cudaGetLastError());
         }
-        if (!a.ghat_only && a.kind != 1 && a.n > 0) {
-            k_tr_rot<<<ceil_div(4LL * a.n, kThreads), kThreads, 0, st>>>(a);
-            SGTR_CUDA(cudaGetLastError());
-        }
         if (a.ghat_only && a.elementwise)
             SGTR_CUDA(cudaMemsetAsync(a.partials + 5LL * nbK, 0, sizeof(double) * 5 * nbK, st));
+    } else if (phase == 3 && !a.ghat_only && a.kind != 1 && a.n > 0) {
+        k_tr_rot<<<ceil_div(4LL * a.n, kThreads), kThreads, 0, st>>>(a);
+        SGTR_CUDA(cudaGetLastError());
     } else if (phase == 1 && !a.ghat_only && a.kind != 1 && a.n > 0) {
         k_tr_bisect<<<ceil_div(4LL * a.n, kThreads), kThreads, 0, st>>>(a);
         SGTR_CUDA(cudaGetLastError());
