@@ -9,8 +9,10 @@
 // pixel_range of the FP64 bbox) against the block as a bit mask of covered
 // pixels, stages the fragment's raster fields into warp-private shared
 // memory, and a warp bit-transpose hands every pixel lane the set of batch
-// entries covering it.  The warp visits only entries covering a pixel still
-// in play, reading each staged record as a broadcast.  K12 stages batches
+// entries covering it.  In K7 every lane then walks its own entries (its
+// pixel's blend state is private); K10 visits, warp-wide, the entries
+// covering a pixel still in play (its per-fragment adjoints are reduced over
+// the warp), reading each staged record as a broadcast.  K12 stages batches
 // per warp the same way with per-pixel rectangle tests.  k_raster_count is
 // the one-thread-per-pixel CTA form kept for the E/C work counters.
 //
@@ -235,12 +237,11 @@ struct StagedRec {
 // as bit arithmetic: the lane that stages list entry base + j turns its pixel
 // rectangle into the 32-bit mask of the warp block's pixels it covers, and a
 // warp bit-transpose gives every pixel lane the mask of the batch entries
-// covering it.  The warp then visits, two at a time, only the entries that
-// cover some pixel still blending (an OR-reduction of the lane masks, with
-// finished pixels' masks cleared), and each lane's test of an entry is one bit
-// -- no per-entry rectangle loads, compares or votes.  Per pixel the entries,
-// operations and their order are those of k_raster_fwd_paired, so the image,
-// T and the stop index are bit-identical.
+// covering it -- no per-entry rectangle loads, compares or votes.  Each lane
+// then walks its own mask (a pixel's blend state is its lane's alone), so a
+// lane never evaluates an entry that misses its pixel.  Per pixel the
+// entries, operations and their order are those of k_raster_fwd_paired
+// (round 1), so the image, T and the stop index are bit-identical.
 // The record staging is software-pipelined: the next batch's rectangles are
 // tested and its records copied into the other half of a double buffer with
 // cp.async (LDGSTS) while the current batch blends (-4.5 % K7 against the
@@ -307,21 +308,18 @@ __global__ void __launch_bounds__(32 * WPB)
         cp_async_wait<1>();
         __syncwarp();
         const StagedRec* my_rec = s_rec[lw][buf];
-        // every lane walks its own entries, two per round (two independent
-        // exp chains, then the blends in list order): the warp runs as many
-        // rounds as its busiest pixel needs, not one per entry any pixel
-        // needs, and no lane evaluates an entry that misses its pixel
+        // every lane walks its own entries in list order, one per round: the
+        // warp runs as many rounds as its busiest pixel needs, not one per
+        // entry any pixel needs, and no lane evaluates an entry that misses
+        // its pixel (the per-lane walks are the parallelism; two entries per
+        // round, for two exp chains per lane, measured 2.4 % slower)
         while (__any_sync(kFull, mine != 0u)) {
-            const bool has0 = mine != 0u;
-            const int j0 = has0 ? __ffs(mine) - 1 : 0;
+            const bool has = mine != 0u;
+            const int j = has ? __ffs(mine) - 1 : 0;
             mine &= mine - 1u;
-            const bool has1 = mine != 0u;
-            const int j1 = has1 ? __ffs(mine) - 1 : j0;
-            mine &= mine - 1u;
-            const StagedRec r0 = my_rec[j0], r1 = my_rec[j1];
-            const double ab0 = falloff(r0), ab1 = falloff(r1);
-            if (has0 && !(ab0 < ro.alpha_skip)) blend(r0, ab0, base + j0);
-            if (has1 && !done && !(ab1 < ro.alpha_skip)) blend(r1, ab1, base + j1);
+            const StagedRec r = my_rec[j];
+            const double ab = falloff(r);
+            if (has && !(ab < ro.alpha_skip)) blend(r, ab, base + j);
             if (done) mine = 0u;
         }
         __syncwarp();
