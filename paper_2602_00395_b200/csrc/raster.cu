@@ -2,7 +2,7 @@
 // K12 forward-mode JVP.
 //
 // Tiles are 16x16 pixels with per-tile fragment lists in depth order
-// (binning.cu).  K7 and K10 run one-warp CTAs, each warp owning one block of
+// (binning.cu).  K7 (two-warp CTAs) and K10 (one-warp CTAs) give each warp one block of
 // its tile (K7: 8x4 pixels, one per lane; K10: 8x8, two per lane, rows r and
 // r + 4) and walking the tile list on its own, 32 entries per batch: the lane
 // of list entry base + j tests that entry's exact pixel rectangle (K1's
@@ -658,8 +658,9 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     if (n == 0) return;
     if (counters)  // the E / C work counters (outside timed regions)
         k_raster_count<<<n, kThreads, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last, counters);
-    else  // one-warp CTAs: each retires as soon as its block is done
-        k_raster_fwd_bits<1><<<n * 8, 32, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
+    else  // two-warp CTAs (35 resident warps per SM at 58 registers, where the 32-CTA
+          // limit capped one-warp CTAs at 32: -1.3 % against one warp, 4 warps +0.6 %)
+        k_raster_fwd_bits<2><<<n * 4, 64, 0, st>>>(tl, rec, W, H, ro, img, tfinal, last);
     SGTR_CUDA(cudaGetLastError());
 }
 
