@@ -2,9 +2,9 @@
 // K12 forward-mode JVP.
 //
 // Tiles are 16x16 pixels with per-tile fragment lists in depth order
-// (binning.cu).  K7 (two-warp CTAs) and K10 (one-warp CTAs) give each warp one block of
-// its tile (K7: 8x4 pixels, one per lane; K10: 8x8, two per lane, rows r and
-// r + 4) and walking the tile list on its own, 32 entries per batch: the lane
+// (binning.cu).  In K7 (two-warp CTAs) and K10 (one-warp CTAs) each warp owns
+// one block of its tile (K7: 8x4 pixels, one per lane; K10: 8x8, two per lane,
+// rows r and r + 4) and walks the tile list on its own, 32 entries per batch: the lane
 // of list entry base + j tests that entry's exact pixel rectangle (K1's
 // pixel_range of the FP64 bbox) against the block as a bit mask of covered
 // pixels, stages the fragment's raster fields into warp-private shared
