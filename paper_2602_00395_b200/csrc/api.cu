@@ -716,7 +716,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
 void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender& vr, int mode,
                    const double* zdense, const uint32_t* zbits, double* acc, double* flag) {
     const long long nd = std::max(vr.cap, 1LL);
-    double* part = c.part.as<double>((size_t)kVjpSlots * kAdj * nd);
+    double* part = c.part.as<double>((size_t)kVjpSlots * kPartStride * nd);
     unsigned char* mask = c.mask.as<unsigned char>((size_t)kVjpSlots * nd);
     {
         Timed t(c, KC_RASTER_VJP);

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
     // the <= 4 per-warp partials of each duplicate, in (duplicate, warp)
     // order; the partials are stored by splat-major duplicate slot, so a
-    // splat's are one contiguous run of 288-byte records; masks of 4
+    // splat's are one contiguous run of 320-byte records; masks of 4
     // duplicates (4 bytes each) are fetched together
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         long long jp[4];
@@ -276,12 +276,17 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (mk[u] == 0u) continue;
-            const double* pp = part + jp[u] * kVjpSlots * kAdj;
+            const double2* pp =
+                reinterpret_cast<const double2*>(part + jp[u] * kVjpSlots * kPartStride);
 #pragma unroll
             for (int w = 0; w < kVjpSlots; ++w) {
                 if ((mk[u] >> (8 * w)) & 0xffu) {
+                    // one 80-byte partial as five 16-byte loads (the pad unused)
+                    double2 q[kPartStride / 2];
 #pragma unroll
-                    for (int c = 0; c < kAdj; ++c) a[c] += pp[w * kAdj + c];
+                    for (int h = 0; h < kPartStride / 2; ++h) q[h] = pp[w * (kPartStride / 2) + h];
+#pragma unroll
+                    for (int c = 0; c < kAdj; ++c) a[c] += (c & 1) ? q[c >> 1].y : q[c >> 1].x;
                 }
             }
         }

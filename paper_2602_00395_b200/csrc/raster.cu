@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             if (c == 2 || c == 4) v *= -0.5;
             if (c == 3) v = -v;
             const long long slot = ring_out[fe] * kVjpSlots + warp;
-            part[slot * kAdj + c] = v;
+            part[slot * kPartStride + c] = v;
             if (c == 0) mask[slot] = 1;
         }
         __syncwarp();
