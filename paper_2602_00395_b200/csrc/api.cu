@@ -639,8 +639,8 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
         Timed t(c, KC_DEPTH_SORT);
         depth_sort_and_scan(c.st, b, K);
     }
-    // view begin, project, onesweep sort (histogram + 5 passes), tie fix, counts + scan
-    c.launches += 1 + 1 + 6 + 1 + 3;
+    // view begin, project, onesweep sort (histogram + 5 passes), tie fix, scan (init + scan)
+    c.launches += 1 + 1 + 6 + 1 + 2;
     if (defer) {
         view_end(c.st, &c.dstat->vs, b.off_r + K, c.dup_cap, defer->errk, defer->erri,
                  defer->ndup, defer->ovf);

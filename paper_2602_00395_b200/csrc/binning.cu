@@ -15,6 +15,8 @@
 #include <climits>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "common.cuh"
 #include "geometry.cuh"
@@ -53,12 +55,20 @@ __global__ void k_fix_depth_ties(unsigned long long* __restrict__ keys, int* __r
     }
 }
 
-__global__ void k_gather_counts(const int* __restrict__ sorted_ids,
-                                const int* __restrict__ tcount, int K,
-                                long long* __restrict__ cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < K) cnt[r] = tcount[sorted_ids[r]];
-    if (r == K) cnt[r] = 0;
+// K3's input: the tile count of the splat at depth rank r (0 at r = K), read
+// through the scan's input iterator
+struct CountAtRank {
+    const int* ids;
+    const int* tcount;
+    int K;
+    __host__ __device__ long long operator()(int r) const {
+        return r < K ? (long long)tcount[ids[r]] : 0LL;
+    }
+};
+using CountIter = thrust::transform_iterator<CountAtRank, thrust::counting_iterator<int>>;
+CountIter count_iter(const int* ids, const int* tcount, int K) {
+    return thrust::make_transform_iterator(thrust::make_counting_iterator(0),
+                                           CountAtRank{ids, tcount, K});
 }
 
 // K4a: one thread per depth rank (n_visible = K: the culled splats sort last
@@ -253,8 +263,8 @@ size_t depth_sort_temp_bytes(int K) {
 
 size_t scan_temp_bytes(int K) {
     size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (long long*)nullptr, (long long*)nullptr,
-                                  K + 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, count_iter(nullptr, nullptr, K),
+                                  (long long*)nullptr, K + 1);
     return bytes;
 }
 
@@ -281,12 +291,10 @@ void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
         k_fix_depth_ties<<<ceil_div(K, 256), 256, 0, st>>>(b.keys_alt, b.ids_alt, K);
         SGTR_CUDA(cudaGetLastError());
     }
-    // counts in depth-rank order (reuses keys as a long long scratch of K+1)
-    long long* cnt = reinterpret_cast<long long*>(b.keys);
-    k_gather_counts<<<ceil_div(K + 1, 256), 256, 0, st>>>(b.ids_alt, b.tcount, K, cnt);
-    SGTR_CUDA(cudaGetLastError());
+    // K3: exclusive scan of the tile counts gathered in depth-rank order
     size_t bytes = b.temp_bytes;
-    SGTR_CUDA(cub::DeviceScan::ExclusiveSum(b.temp, bytes, cnt, b.off_r, K + 1, st));
+    SGTR_CUDA(cub::DeviceScan::ExclusiveSum(b.temp, bytes, count_iter(b.ids_alt, b.tcount, K),
+                                            b.off_r, K + 1, st));
 }
 
 void bin_tiles(cudaStream_t st, BinBuffers& b, int K, int tiles_x, int n_tiles, long long cap) {
