@@ -112,3 +112,29 @@ def test_non_finite_update_names_the_group(sp, ds):
     assert np.max(np.abs(g[fin] - gr[fin])) <= 1e-3 * np.max(np.abs(gr[fin]))
     assert np.array_equal(r["x"][0], ds.init_x) and np.array_equal(r["x"][1], ds.init_x)
     assert np.array_equal(*r["rng"])
+
+
+def test_dup_capacity_rerun_is_transparent(sp, ds):
+    """A step whose views outgrow the tile-duplicate capacity is rerun with a
+    grown capacity (api.cu step_core); it reports the rerun and ends in the
+    state of a step that never overflowed.  Bad capacities are refused."""
+    views = [sp.Camera.from_c(c, g) for c, g in zip(ds.cams, ds.gts)]
+    opts = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 20), batch_size=3)
+    out = []
+    for cap in (0, 16):
+        ctx = sp.Context()
+        ctx.set_scene(ds.init_x)
+        ctx.set_views(views)
+        ctx.state_reset(5)
+        ctx.set_dup_capacity(cap)
+        d = [ctx.step(opts) for _ in range(3)]
+        out.append((ctx.get_scene(), ctx.state_get()[0], [x.reruns for x in d],
+                    [x.batch_loss for x in d]))
+        with pytest.raises(sp.InvalidArgument):
+            ctx.set_dup_capacity(-1)
+        with pytest.raises(sp.InvalidArgument):
+            ctx.set_dup_capacity(1 << 31)
+        ctx.close()
+    (x0, g0, r0, l0), (x1, g1, r1, l1) = out
+    assert r0 == [0, 0, 0] and r1[0] >= 1
+    assert np.array_equal(x0, x1) and np.array_equal(g0, g1) and l0 == l1
