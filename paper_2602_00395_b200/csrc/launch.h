@@ -183,9 +183,10 @@ struct TrArgs {
     int elementwise;      // K14a also runs the EMAs / direction over all K splats
 };
 int tr_num_blocks(int K);
-// phase 0: K14a (EMAs, direction, non-rotation radii), 3: K14a' (rotation
-// radii and their certification, failures queued), 1: K14b (queued
-// bisections), 2: K14c (clip, apply, clamp); in the order 0, 3, 1, 2
+// phase 0: K14a (EMAs, direction; radius, clip, apply and clamp of the ten
+// non-rotation coordinates), 3: K14a' (rotation radii and their
+// certification, failures queued), 1: K14b (queued bisections), 2: K14c
+// (clip and apply of the rotation coordinates); in the order 0, 3, 1, 2
 void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase);
 // 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
 // (partials hold 2 * tr_num_blocks(K) rows of 5)

@@ -1,7 +1,8 @@
-// update.cu — K14: the fused squared-Hellinger trust-region step.
+// update.cu — K14: the squared-Hellinger trust-region step.
 //
-// One thread per splat reads its 14 coordinates of x, g, g-hat, D-hat (and
-// z.w on refresh steps) once and writes g-hat, D-hat and the clamped x once:
+// K14a, one thread per splat, reads its 14 coordinates of x, g, g-hat, D-hat
+// (and z.w on refresh steps) once and writes g-hat, D-hat and, for the ten
+// non-rotation coordinates, the clamped x:
 //   g     = g_acc * M/(m|S1|)                     (optimizer.cpp:58-59)
 //   g_hat = theta1 g_hat + (1-theta1) g           (optimizer.hpp:119-122)
 //   D_hat = theta2 D_hat + (1-theta2) d  [refresh] (optimizer.cpp:212)
@@ -9,8 +10,10 @@
 //   eta   = shd_radii(x, eps)                     (trust_region.cpp:236-252)
 //   x'    = clamp(x + clip(dx, eta))              (optimizer.cpp:124-142,
 //                                                  scene.cpp:49-57)
-// with the step diagnostics as deterministic block partials.  Compiled with
-// --fmad=false so every expression rounds like the oracle.
+// The four rotation coordinates wait for their certified radii (K14a' per
+// (splat, axis), K14b's bisections of the failures) and are clipped and
+// applied by K14c.  The step diagnostics are deterministic block partials.
+// Compiled with --fmad=false so every expression rounds like the oracle.
 #include <math_constants.h>
 
 #include <cfloat>
@@ -330,33 +333,61 @@ __device__ void block_reduce5(double* v, int bad, double* out, int* bad_out) {
     }
 }
 
-// K14a: EMAs, Newton direction and all radii; rotation axes whose Taylor
-// radius fails certification are queued for K14b
-//
-// With `elementwise` the launch covers all K splats (EMAs, direction, the
-// block partials) and computes the radii of the splats in [i0, i0 + n);
-// without it, it covers [i0, i0 + n) and computes only their radii (the
-// other shards of a sharded update).
+// K14a, one thread per splat over all K: EMAs (or the ADAM moments), the
+// direction, and for every coordinate but the four rotation ones the radius,
+// clip, step statistics, apply and clamp (optimizer.cpp:124-142,
+// scene.cpp:49-57) -- those coordinates never touch a dx or eta buffer.  The
+// rotation coordinates' directions go to dx_buf for K14c, which clips them
+// against the certified rotation radii of K14a'/K14b.  (ADAM applies every
+// coordinate here, unclipped.)
+__device__ __forceinline__ double clamp_coord(int j, double v, const double* b) {
+    if (j >= 3 && j < 6) return v < b[0] ? b[0] : v;  // scales >= s_min
+    if (j == 10) {                                      // alpha in [alpha_min, alpha_max]
+        v = v < b[1] ? b[1] : v;
+        return b[2] < v ? b[2] : v;
+    }
+    if (j >= 11 && j < 14) {  // colours in [c_min, c_max]
+        v = v < b[3] ? b[3] : v;
+        return b[4] < v ? b[4] : v;
+    }
+    return v;  // means, rotation, SH coefficients
+}
+
 __global__ void __launch_bounds__(kThreads, 8) k_tr_prepare(TrArgs a) {
-    const bool ew = a.elementwise;
-    const int i = (ew ? 0 : a.i0) + blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const long long K = a.K;
-    double v[5] = {0, 0, 0, 0, 0};  // sum g^2, sum dx^2
-    if (i < (ew ? a.K : a.i0 + a.n)) {
+    // sum g^2, sum dx^2, sum clipped^2, n clipped, max ratio
+    double s_g2 = 0.0, s_dx2 = 0.0, s_c2 = 0.0, n_clip = 0.0, max_ratio = 0.0;
+    int bad = INT_MAX;
+    if (i < a.K) {
         const Prim p = load_prim(a.x, K, i);
         const bool degenerate =
             p.q[0] * p.q[0] + p.q[1] * p.q[1] + p.q[2] * p.q[2] + p.q[3] * p.q[3] < 1e-24;
+        const bool clipped = a.kind != 1;
         // shd_radii (and its degenerate-quaternion throw) runs for the
         // trust-region kinds only
-        if (ew && !a.ghat_only && a.kind != 1 && degenerate) atomicOr(a.degenerate_flag, 1);
-        const int npp = 14 + 3 * a.nb;
-        if (ew && a.kind != 0) {
-            // adam_direction (optimizer.cpp:153-185); SH coefficients at the
-            // colour rate / 20 (extension)
-            for (int j = 0; j < npp; ++j) {
-                const long long k = coord_index(K, a.nb, i, j);
-                const double g = a.g_acc[k] * a.gscale;
-                v[0] += g * g;
+        if (!a.ghat_only && clipped && degenerate) atomicOr(a.degenerate_flag, 1);
+        // the non-rotation radii (trust_region.cpp:236-252); a degenerate
+        // splat fails the step, its radii are never used
+        double eta[14] = {};
+        if (!a.ghat_only && clipped && !degenerate) {
+            radius_mean(p, a.eps, a.caps[0], eta);
+            for (int c = 0; c < 3; ++c) {
+                eta[3 + c] = cap_radius(sqrt(2.0 * p.s[c] * p.s[c] * a.eps / p.alpha), a.caps[1]);
+                eta[11 + c] = cap_radius(sqrt(4.0 * p.c[c] * a.eps / p.alpha), a.caps[4]);
+            }
+            eta[10] = cap_radius(sqrt(4.0 * p.alpha * a.eps), a.caps[3]);
+        }
+        // one coordinate: direction, then (but for rotation) clip, apply, clamp;
+        // e is its radius
+        auto coord = [&](int j, double e) {
+            const long long k = coord_index(K, a.nb, i, j);
+            const double g = a.g_acc[k] * a.gscale;
+            s_g2 += g * g;
+            double dx;
+            if (a.kind != 0) {
+                // adam_direction (optimizer.cpp:153-185); SH coefficients at
+                // the colour rate / 20 (extension)
                 const double m = a.beta1 * a.adam_m[k] + (1.0 - a.beta1) * g;
                 const double vv = a.beta2 * a.adam_v[k] + (1.0 - a.beta2) * (g * g);
                 a.adam_m[k] = m;
@@ -365,49 +396,49 @@ __global__ void __launch_bounds__(kThreads, 8) k_tr_prepare(TrArgs a) {
                 const double lr = j < 14 ? a.lr[grp] : a.lr[4] / 20.0;
                 const double mhat = m / a.bc1;
                 const double vhat = vv / a.bc2;
-                const double dx = -lr * mhat / (sqrt(vhat) + a.adam_eps);
-                v[1] += dx * dx;
+                dx = -lr * mhat / (sqrt(vhat) + a.adam_eps);
+            } else {
+                const double gh = a.theta1 * a.g_hat[k] + (1.0 - a.theta1) * g;
+                a.g_hat[k] = gh;
+                if (a.ghat_only) return;
+                double dh = a.d_hat[k];
+                if (a.refresh) {
+                    const double d = a.w_acc[k] * a.dscale;
+                    dh = a.theta2 * dh + (1.0 - a.theta2) * d;
+                    a.d_hat[k] = dh;
+                }
+                // std::max(d, gamma) returns d unless d < gamma (NaN d -> d)
+                dx = -gh / ((dh < a.gamma_d) ? a.gamma_d : dh);
+            }
+            s_dx2 += dx * dx;
+            if (clipped && j >= 6 && j < 10) {  // rotation: clipped by K14c
                 a.dx_buf[k] = dx;
+                return;
             }
-        }
-        for (int j = 0; j < npp && ew && a.kind == 0; ++j) {
-            const long long k = coord_index(K, a.nb, i, j);
-            const double g = a.g_acc[k] * a.gscale;
-            v[0] += g * g;
-            const double gh = a.theta1 * a.g_hat[k] + (1.0 - a.theta1) * g;
-            a.g_hat[k] = gh;
-            if (a.ghat_only) continue;
-            double dh = a.d_hat[k];
-            if (a.refresh) {
-                const double d = a.w_acc[k] * a.dscale;
-                dh = a.theta2 * dh + (1.0 - a.theta2) * d;
-                a.d_hat[k] = dh;
+            double c = dx;
+            if (clipped) {
+                // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
+                c = dx < -e ? -e : dx;
+                c = e < c ? e : c;
+                if (fabs(dx) > e) n_clip += 1.0;
+                const double ratio = fabs(c) / e;
+                max_ratio = max_ratio < ratio ? ratio : max_ratio;
             }
-            // std::max(d, gamma) returns d unless d < gamma (NaN d -> d)
-            const double dx = -gh / ((dh < a.gamma_d) ? a.gamma_d : dh);
-            v[1] += dx * dx;
-            a.dx_buf[k] = dx;
-        }
-        const bool in_shard = i >= a.i0 && i < a.i0 + a.n;
-        if (in_shard && !a.ghat_only && a.kind != 1 && !degenerate) {
-            double eta[14];
-            radius_mean(p, a.eps, a.caps[0], eta);
-            for (int c = 0; c < 3; ++c) {
-                eta[3 + c] = cap_radius(sqrt(2.0 * p.s[c] * p.s[c] * a.eps / p.alpha), a.caps[1]);
-                eta[11 + c] = cap_radius(sqrt(4.0 * p.c[c] * a.eps / p.alpha), a.caps[4]);
-            }
-            eta[10] = cap_radius(sqrt(4.0 * p.alpha * a.eps), a.caps[3]);
-            for (int j = 0; j < 3; ++j) a.eta_buf[3LL * i + j] = eta[j];
-            for (int j = 0; j < 3; ++j) a.eta_buf[3 * K + 3LL * i + j] = eta[3 + j];
-            a.eta_buf[10 * K + i] = eta[10];
-            for (int j = 0; j < 3; ++j) a.eta_buf[11 * K + 3LL * i + j] = eta[11 + j];
-            // SH extension: colour radius / max|Y_m|
-            for (int m = 0; m < a.nb; ++m)
-                for (int c = 0; c < 3; ++c)
-                    a.eta_buf[14 * K + 3LL * a.nb * i + 3 * m + c] = eta[11 + c] / sh_max(m);
+            if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
+            s_c2 += c * c;
+            if (a.applied) a.applied[k] = c;
+            a.x_out[k] = clamp_coord(j, a.x[k] + c, a.bounds);
+        };
+#pragma unroll
+        for (int j = 0; j < 14; ++j) coord(j, eta[j]);
+        // SH extension: colour radius / max|Y_m|
+        for (int j = 14; j < 14 + 3 * a.nb; ++j) {
+            const int ch = (j - 14) % 3;
+            coord(j, (ch == 0 ? eta[11] : ch == 1 ? eta[12] : eta[13]) / sh_max((j - 14) / 3));
         }
     }
-    if (ew) block_reduce5(v, INT_MAX, a.partials + 5LL * blockIdx.x, nullptr);
+    double v[5] = {s_g2, s_dx2, s_c2, n_clip, max_ratio};
+    block_reduce5(v, bad, a.partials + 5LL * blockIdx.x, a.bad_index);
 }
 
 // K14a': one thread per (splat, rotation axis) (trust_region.cpp:198-234):
@@ -452,47 +483,29 @@ __global__ void __launch_bounds__(kThreads) k_tr_bisect(TrArgs a) {
     a.eta_buf[k] = rot_bisect(ra, a.eta_buf[k], a.eps * (1.0 + 1e-9));
 }
 
-// K14c: clip, step statistics, apply and clamp (optimizer.cpp:124-142)
+// K14c: the rotation coordinates' clip against their certified radii, step
+// statistics and apply (optimizer.cpp:124-142; Scene::clamp leaves q alone)
 __global__ void __launch_bounds__(kThreads) k_tr_apply(TrArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;  // all K splats
     const long long K = a.K;
     double v[5] = {0, 0, 0, 0, 0};  // -, -, sum clipped^2, n clipped, max ratio
     int bad = INT_MAX;
-    if (i < a.K) {
-        double xo[14];
-        for (int j = 0; j < 14 + 3 * a.nb; ++j) {
-            const long long k = coord_index(K, a.nb, i, j);
+    if (i < a.K && a.kind != 1) {
+#pragma unroll
+        for (int cq = 0; cq < 4; ++cq) {
+            const long long k = 6 * K + 4LL * i + cq;
             const double dx = a.dx_buf[k];
-            double c = dx;
-            if (a.kind != 1) {
-                // cwiseMax(-eta).cwiseMin(eta) with std::max/std::min semantics
-                const double eta = a.eta_buf[k];
-                c = dx < -eta ? -eta : dx;
-                c = eta < c ? eta : c;
-                if (fabs(dx) > eta) v[3] += 1.0;
-                const double ratio = fabs(c) / eta;
-                v[4] = v[4] < ratio ? ratio : v[4];
-            }
+            const double eta = a.eta_buf[k];
+            double c = dx < -eta ? -eta : dx;
+            c = eta < c ? eta : c;
+            if (fabs(dx) > eta) v[3] += 1.0;
+            const double ratio = fabs(c) / eta;
+            v[4] = v[4] < ratio ? ratio : v[4];
             if (!isfinite(c)) bad = min(bad, (int)min(k, (long long)INT_MAX));
             v[2] += c * c;
             if (a.applied) a.applied[k] = c;
-            if (j < 14)
-                xo[j] = a.x[k] + c;
-            else
-                a.x_out[k] = a.x[k] + c;  // SH coefficients are not clamped
+            a.x_out[k] = a.x[k] + c;
         }
-        // Scene::clamp (scene.cpp:49-57)
-        for (int c = 0; c < 3; ++c) {
-            double& sc = xo[3 + c];
-            sc = sc < a.bounds[0] ? a.bounds[0] : sc;
-            double& col = xo[11 + c];
-            col = col < a.bounds[3] ? a.bounds[3] : col;
-            col = a.bounds[4] < col ? a.bounds[4] : col;
-        }
-        double& al = xo[10];
-        al = al < a.bounds[1] ? a.bounds[1] : al;
-        al = a.bounds[2] < al ? a.bounds[2] : al;
-        for (int j = 0; j < 14; ++j) a.x_out[flat_index(K, i, j)] = xo[j];
     }
     block_reduce5(v, bad, a.partials + 5LL * (gridDim.x + blockIdx.x), a.bad_index);
 }
@@ -556,9 +569,8 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
     const int nbK = tr_num_blocks(a.K);
     if (phase == 0) {
         SGTR_CUDA(cudaMemsetAsync(a.queue_count, 0, sizeof(int), st));
-        const int nbp = a.elementwise ? nbK : tr_num_blocks(a.n);
-        if (nbp > 0) {
-            k_tr_prepare<<<nbp, kThreads, 0, st>>>(a);
+        if (a.elementwise) {  // (further shards only add rotation radii)
+            k_tr_prepare<<<nbK, kThreads, 0, st>>>(a);
             SGTR_CUDA(cudaGetLastError());
         }
         if (a.ghat_only && a.elementwise)
