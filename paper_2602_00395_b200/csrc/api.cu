@@ -1211,20 +1211,25 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         c.launches += 3;
     }
     if (shards > 1) {
-        // shard-major staging of the radii, all-gather over ranks (a round
-        // trip on one rank)
-        const int npp = 14 + 3 * c.nb;
-        const long long B = (long long)npp * Kp;
+        // Only the rotation radii live in eta_buf (K14a clips the other
+        // coordinates itself), and a shard's are one contiguous block of the
+        // rotation group, at the same offset in a shard-major staging buffer
+        // of 4 Kp doubles per shard: copy in, all-gather over ranks (equal
+        // blocks; the last shard's tail is padding), copy back.
+        const long long B = 4 * Kp;
         double* S = c.stage.as<double>(std::max<long long>(B * shards, 1));
-        double* eta = a.eta_buf;
+        double* rot = a.eta_buf + 6LL * c.K;
         for (int r = r_first; r <= r_last; ++r) {
             int i0, n;
             shard_range(r, i0, n);
-            launch_stage(c.st, eta, S, c.K, c.nb, Kp, i0, n, true);
+            if (n > 0)
+                SGTR_CUDA(cudaMemcpyAsync(S + B * r, rot + 4LL * i0, sizeof(double) * 4 * n,
+                                          cudaMemcpyDeviceToDevice, c.st));
         }
         if (multi) allgather(c, S, B);
-        launch_stage(c.st, eta, S, c.K, c.nb, Kp, 0, c.K, false);
-        c.launches += (r_last - r_first + 1) + 1;
+        if (c.K > 0)
+            SGTR_CUDA(cudaMemcpyAsync(rot, S, sizeof(double) * 4 * c.K, cudaMemcpyDeviceToDevice,
+                                      c.st));
     }
     {
         Timed t(c, KC_TR_APPLY);

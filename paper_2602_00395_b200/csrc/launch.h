@@ -190,8 +190,6 @@ int tr_num_blocks(int K);
 void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase);
 // 5 reduced values: gnorm^2, step_pre^2, step_post^2, n_clipped, max ratio
 // (partials hold 2 * tr_num_blocks(K) rows of 5)
-void launch_stage(cudaStream_t st, double* vec, double* staged, long long K, int nb, long long Kp,
-                  long long i0, long long n, bool to_staged);
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5);
 void launch_shd_radii(cudaStream_t st, int K, int nb, const double* x, double eps,
                       const double caps[5], double* eta);

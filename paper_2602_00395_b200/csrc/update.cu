@@ -587,36 +587,9 @@ void launch_tr_update(cudaStream_t st, const TrArgs& a, int phase) {
     }
 }
 
-// shard-major staging of a scene-layout vector (sharded trust-region update):
-// shard r = splats [r Kp, (r+1) Kp) occupies block r of B = (14 + 3 nb) Kp
-// doubles, itself in the scene's group-major layout over Kp splats, so one
-// reduce-scatter / all-gather moves each shard as a contiguous block
-__global__ void k_stage(double* __restrict__ vec, double* __restrict__ staged, long long K, int nb,
-                        long long Kp, long long i0, long long n, int to_staged) {
-    const int npp = 14 + 3 * nb;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * npp) return;
-    const long long i = i0 + t / npp;
-    const int j = (int)(t % npp);
-    const long long r = i / Kp, il = i - r * Kp;
-    const long long si = r * npp * Kp + coord_index(Kp, nb, (int)il, j);
-    const long long vi = coord_index(K, nb, (int)i, j);
-    if (to_staged)
-        staged[si] = vec[vi];
-    else
-        vec[vi] = staged[si];
-}
-
-void launch_stage(cudaStream_t st, double* vec, double* staged, long long K, int nb, long long Kp,
-                  long long i0, long long n, bool to_staged) {
-    if (n <= 0) return;
-    k_stage<<<ceil_div(n * (14 + 3 * nb), 256), 256, 0, st>>>(vec, staged, K, nb, Kp, i0, n,
-                                                             to_staged ? 1 : 0);
-    SGTR_CUDA(cudaGetLastError());
-}
-
-// partials: [nblocks][5] from K14a (sum g^2, sum dx^2) then [nblocks][5] from
-// K14c (sum clipped^2, n clipped, max ratio)
+// partials: [nblocks][5] from K14a (sums of g^2, dx^2 and the non-rotation
+// coordinates' clipped^2, their clip count and max ratio) then [nblocks][5]
+// from K14c (the same three for the rotation coordinates)
 void launch_tr_finalize(cudaStream_t st, const double* partials, int nblocks, double* out5) {
     k_tr_finalize<<<1, 256, 0, st>>>(partials, 2 * nblocks, out5);
     SGTR_CUDA(cudaGetLastError());
