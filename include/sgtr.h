@@ -364,10 +364,10 @@ int sgtr_nccl_unique_id(uint8_t out[128]);
  * rank r renders bands r, r + nranks, ... (default bands_per_rank = 1; > 1
  * also splits on one rank, which tests use to check the band sums) */
 int sgtr_set_refresh_bands(sgtr_ctx* ctx, int32_t bands_per_rank);
-/* The trust-region radii (Hellinger radii, rotation certification and
- * bisection: the costly part of the update) are split by splat range over
- * the ranks and all-gathered (ncclAllGather) before the clip; the EMAs,
- * direction, clip and apply stay replicated, so the state needs no gather.
+/* The rotation radii (certification and bisection: the costly part of the
+ * update) are split by splat range over the ranks and all-gathered
+ * (ncclAllGather) before their clip; the other radii, the EMAs, direction,
+ * clip and apply stay replicated, so the state needs no gather.
  * On one rank, shards > 1 runs the same shard/stage/gather sequence back to
  * back (tests check it against the unsharded update, bit for bit). */
 int sgtr_set_tr_shards(sgtr_ctx* ctx, int32_t shards);
