@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "geometry.cuh"
 #include "launch.h"
@@ -582,6 +584,15 @@ struct Timed {
     }
 };
 
+// NVTX range over a scope (header-only NVTX 3: a no-op unless a profiler
+// injects itself), so nsys / ncu timelines show the step's phases
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void harvest_timing(Ctx& c) {
     if (c.timer.on) c.timer.harvest();
 }
@@ -950,6 +961,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     double* novf = ndup + (n1 + n2);
     const size_t fused_n = dim + tail_n + (refresh ? dim : 0);
     ensure_tail(c, tail_n);
+    NvtxRange step_range("sgtr step");
     int reruns = 0;
     for (;;) {
     SGTR_CUDA(cudaMemsetAsync(fused, 0, sizeof(double) * fused_n, c.st));
@@ -979,6 +991,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
     int li = 0;
     for (int p = c.rank; p < n1; p += c.nranks, ++li) {
         use_lane(c, li % lanes);
+        NvtxRange view_range("gradient view");
         const View& v = c.views[s1[p]];
         const ViewSlots vslots{errk + p, erri + p, ndup + p, novf};
         const ViewRender vr = render_view(c, v.dc, ro, false, 0, -1, &vslots);
@@ -1022,6 +1035,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
                     if (tr1 <= tr0) continue;
                     const int r0 = std::max(0, tr0 - 1), r1 = std::min(tiles_y, tr1 + 1);
                     const View& v = c.views[s2[q]];
+                    NvtxRange view_range("hutchinson view");
                     // the view's status is reported by its band 0 only (one
                     // writer per slot across ranks: the tail is summed)
                     ViewSlots vslots{nullptr, nullptr, nullptr, novf};
@@ -1114,6 +1128,7 @@ void step_core(Ctx& c, const sgtr_optimizer_options& o, const std::vector<int>& 
         }
     }
     // K14
+    NvtxRange update_range("trust-region update");
     double eps = -1.0;
     if (kind != 1) {
         if (!(o.eps_start >= o.eps_end) || !(o.eps_end > 0.0))
