@@ -240,8 +240,9 @@ struct StagedRec {
 // covering it -- no per-entry rectangle loads, compares or votes.  Each lane
 // then walks its own mask (a pixel's blend state is its lane's alone), so a
 // lane never evaluates an entry that misses its pixel.  Per pixel the
-// entries, operations and their order are those of k_raster_fwd_paired
-// (round 1), so the image, T and the stop index are bit-identical.
+// entries, operations and their order are those of the round-1 kernel
+// (k_raster_fwd_paired), so the image, T and the stop index are
+// bit-identical to it.
 // The record staging is software-pipelined: the next batch's rectangles are
 // tested and its records copied into the other half of a double buffer with
 // cp.async (LDGSTS) while the current batch blends (-4.5 % K7 against the
@@ -339,17 +340,20 @@ __global__ void __launch_bounds__(32 * WPB)
 constexpr int kRedStride = 33;
 
 // ------------------------------------------------------------------ K10, hit bitmasks
-// k_raster_vjp_staged3 with the per-(entry, pixel) tests done as bit
-// arithmetic (as k_raster_fwd_bits): the staging lane of list entry base + j
-// turns its pixel rectangle into the 64-bit mask of the 8x8 block's pixels it
-// covers; two warp bit-transposes give each lane the entries covering its two
-// pixels, cut to the entries below each pixel's stored last index (one
-// low-bits mask, render.cpp:238-257 walks [0, last)); an OR-reduction gives
-// the entries the warp visits, back to front.  Records are staged at their
-// list offset (no compaction), and the per-slot written-flag is set by the
-// ring flush; the record staging is double-buffered with cp.async as in K7.
-// Per pixel and per partial the operations and their order are those of
-// k_raster_vjp_staged3 (round 1): the partials are bit-identical.
+// One warp per 8x8 block of a tile, two pixels per lane (rows r and r + 4),
+// back to front from each pixel's stored last index (render.cpp:238-257
+// walks [0, last)), with the per-(entry, pixel) tests done as bit arithmetic
+// (as in K7): the staging lane of list entry base + j turns its pixel
+// rectangle into the 64-bit mask of the block's pixels it covers; two warp
+// bit-transposes give each lane the entries covering its two pixels, cut to
+// the entries below each pixel's last index (one low-bits mask); an
+// OR-reduction gives the entries the warp visits.  Each visited fragment's 9
+// adjoints are reduced over the warp (the ring below) into one partial per
+// (duplicate, block), flagged in mask.  Records are staged at their list
+// offset (no compaction); the staging is double-buffered with cp.async as in
+// K7.  Per pixel and per partial the operations and their order are those of
+// the round-1 kernel (k_raster_vjp_staged3): the partials are bit-identical
+// to it.
 template <int WPB, int kMinB = 10>
 __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     k_raster_vjp_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
