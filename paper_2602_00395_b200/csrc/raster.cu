@@ -12,8 +12,8 @@
 // entries covering it.  In K7 every lane then walks its own entries (its
 // pixel's blend state is private); K10 visits, warp-wide, the entries
 // covering a pixel still in play (its per-fragment adjoints are reduced over
-// the warp), reading each staged record as a broadcast.  K12 stages batches
-// per warp the same way with per-pixel rectangle tests.  k_raster_count is
+// the warp), reading each staged record as a broadcast.  K12 is K7's scheme
+// with the tangent fields staged beside the raster ones.  k_raster_count is
 // the one-thread-per-pixel CTA form kept for the E/C work counters.
 //
 // Branch parity: the three kernels evaluate the primal alpha with the same
@@ -46,17 +46,6 @@ struct PixelCtx {
     double wx0, wx1, wy0, wy1;  // the warp's span of pixel centres
     int ix0, iy0;               // the warp's first pixel column / row
 };
-
-// exact overlap of a splat's pixel rectangle (K1's pixel_range: the pixels
-// whose centre lies in the closed FP64 bbox, clipped to the image) with the
-// warp's 8x4 pixel block
-__device__ __forceinline__ bool rect_hits_warp(const PixelCtx& p, int4 r) {
-    return !(p.ix0 + 7 < r.x || p.ix0 > r.z || p.iy0 + 3 < r.y || p.iy0 > r.w);
-}
-// the reference's per-pixel bbox test (render.cpp:128-131) on that rectangle
-__device__ __forceinline__ bool rect_has_pixel(const PixelCtx& p, int4 r) {
-    return p.px >= r.x && p.px <= r.z && p.py >= r.y && p.py <= r.w;
-}
 
 // warp w covers columns (w & 1) * 8 .. +7 and rows (w >> 1) * 4 .. +3
 __device__ __forceinline__ PixelCtx pixel_ctx(int tile, int tiles_x, int W, int H,
@@ -551,24 +540,24 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
     if (nring) flush(nring);
 }
 
-// ------------------------------------------------------------------ K12, batch-staged
-// The tangent image with k_raster_fwd_staged's batches: the passing
-// fragments' 9 raster fields and 9 tangent fields are fetched lane-parallel
-// into warp-private shared slots, then blended in list order with the same
-// per-pixel operations as k_raster_jvp.
+// ------------------------------------------------------------------ K12, hit bitmasks
+// K12, the tangent image (render.cpp:175-192, blend_pixel<Dual>): K7's
+// per-batch bit masks (8x4 blocks, one pixel per lane) and per-lane walk in
+// list order, with each staged entry's 9 tangent fields beside its raster
+// fields.  Per pixel the operations and their order are those of the round-1
+// kernel (k_raster_jvp_staged), so the tangent image is bit-identical to it.
 struct StagedTan {
-    double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;
+    double mx, my, i00, i01, i11, alpha, c0, c1, c2, pad;  // tangent record fields 0..9
 };
 
 template <int WPB>
 __global__ void __launch_bounds__(32 * WPB)
-    k_raster_jvp_staged(TileLists tl, const double* __restrict__ rec,
-                        const double* __restrict__ trec, int W, int H, RenderP ro,
-                        double* __restrict__ tangent) {
+    k_raster_jvp_bits(TileLists tl, const double* __restrict__ rec,
+                      const double* __restrict__ trec, int W, int H, RenderP ro,
+                      double* __restrict__ tangent) {
     constexpr int SUB = kWarps / WPB;
     __shared__ __align__(16) StagedRec s_rec[WPB][32];
     __shared__ __align__(16) StagedTan s_tan[WPB][32];
-    __shared__ int4 s_rect[WPB][32];
     const int tile =
         tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
     const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
@@ -577,72 +566,64 @@ __global__ void __launch_bounds__(32 * WPB)
     const int start = tl.tile_start[tile], end = tl.tile_end[tile];
     double T = 1.0, dT = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
     bool done = !pc.inside;
-    StagedRec* my_rec = s_rec[lw];
-    StagedTan* my_tan = s_tan[lw];
-    int4* my_rect = s_rect[lw];
+    const StagedRec* my_rec = s_rec[lw];
+    const StagedTan* my_tan = s_tan[lw];
     for (int base = start; base < end; base += 32) {
         if (__all_sync(kFull, done)) break;
         const int jj = base + lane;
-        bool pass = false;
-        int4 rr;
+        unsigned slots = 0u;
         if (jj < end) {
-            rr = __ldg(tl.trect + jj);
-            pass = rect_hits_warp(pc, rr);
-        }
-        const unsigned m = __ballot_sync(kFull, pass);
-        if (pass) {
-            const int q = __popc(m & ((1u << lane) - 1u));
-            const int id = __ldg(tl.tile_ids + jj);
-            const double2* r2 = reinterpret_cast<const double2*>(rec + (long long)kRec * id);
-            double2* o = reinterpret_cast<double2*>(my_rec + q);
+            slots = (unsigned)block_slots(__ldg(tl.trect + jj), pc.ix0, pc.iy0, 4);
+            if (slots) {
+                const int id = __ldg(tl.tile_ids + jj);
+                const double* src = rec + (long long)kRec * id + 4;
+                double* dst = reinterpret_cast<double*>(&s_rec[lw][lane]);
+                const double* tsrc = trec + (long long)kTRec * id;
+                double* tdst = reinterpret_cast<double*>(&s_tan[lw][lane]);
 #pragma unroll
-            for (int k = 0; k < 5; ++k) o[k] = __ldg(r2 + 2 + k);
-            const double* t = trec + (long long)kTRec * id;
-            StagedTan& u = my_tan[q];
-            u.mx = __ldg(t + T_MX);
-            u.my = __ldg(t + T_MY);
-            u.i00 = __ldg(t + T_I00);
-            u.i01 = __ldg(t + T_I01);
-            u.i11 = __ldg(t + T_I11);
-            u.alpha = __ldg(t + T_ALPHA);
-            u.c0 = __ldg(t + T_C0);
-            u.c1 = __ldg(t + T_C0 + 1);
-            u.c2 = __ldg(t + T_C0 + 2);
-            my_rect[q] = rr;
-        }
-        __syncwarp();
-        const int n = __popc(m);
-        for (int e = 0; e < n; ++e) {
-            if (!done && rect_has_pixel(pc, my_rect[e])) {
-                const StagedRec r = my_rec[e];
-                const StagedTan t = my_tan[e];
-                const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
-                                      r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-                const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
-                const double ev = falloff_of(dx, dy, f);
-                double abar = __dmul_rn(f[R_ALPHA], ev);
-                // tangent of the same expression (dual.hpp semantics)
-                const Dual Dx(dx, -t.mx), Dy(dy, -t.my);
-                const Dual I00(f[R_I00], t.i00), I01(f[R_I01], t.i01), I11(f[R_I11], t.i11);
-                const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
-                double dabar = t.alpha * ev + f[R_ALPHA] * (ev * ex.d);
-                if (abar >= ro.alpha_clamp) {
-                    abar = ro.alpha_clamp;
-                    dabar = 0.0;
-                }
-                if (!(abar < ro.alpha_skip)) {
-                    const double w = abar * T;
-                    const double dw = dabar * T + abar * dT;
-                    d0 += t.c0 * w + f[R_C0] * dw;
-                    d1 += t.c1 * w + f[R_C1] * dw;
-                    d2 += t.c2 * w + f[R_C2] * dw;
-                    const double om = __dsub_rn(1.0, abar);
-                    dT = dT * om + T * (-dabar);
-                    T = __dmul_rn(T, om);
-                    if (T < ro.t_stop) done = true;
+                for (int q = 0; q < 5; ++q) {
+                    cp_async16(dst + 2 * q, src + 2 * q);
+                    cp_async16(tdst + 2 * q, tsrc + 2 * q);
                 }
             }
-            if (__all_sync(kFull, done)) break;
+        }
+        cp_async_commit();
+        unsigned mine = warp_transpose32(slots);  // bit j: entry base + j covers my pixel
+        if (done) mine = 0u;
+        cp_async_wait<0>();
+        __syncwarp();
+        while (__any_sync(kFull, mine != 0u)) {
+            const bool has = mine != 0u;
+            const int e = has ? __ffs(mine) - 1 : 0;
+            mine &= mine - 1u;
+            const StagedRec r = my_rec[e];
+            const StagedTan t = my_tan[e];
+            const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                  r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+            const double dx = pc.pxc - f[R_MX], dy = pc.pyc - f[R_MY];
+            const double ev = falloff_of(dx, dy, f);
+            double abar = __dmul_rn(f[R_ALPHA], ev);
+            // tangent of the same expression (dual.hpp semantics)
+            const Dual Dx(dx, -t.mx), Dy(dy, -t.my);
+            const Dual I00(f[R_I00], t.i00), I01(f[R_I01], t.i01), I11(f[R_I11], t.i11);
+            const Dual ex = -0.5 * (Dx * Dx * I00 + Dy * Dy * I11) - Dx * Dy * I01;
+            double dabar = t.alpha * ev + f[R_ALPHA] * (ev * ex.d);
+            if (abar >= ro.alpha_clamp) {
+                abar = ro.alpha_clamp;
+                dabar = 0.0;
+            }
+            if (has && !(abar < ro.alpha_skip)) {
+                const double w = abar * T;
+                const double dw = dabar * T + abar * dT;
+                d0 += t.c0 * w + f[R_C0] * dw;
+                d1 += t.c1 * w + f[R_C1] * dw;
+                d2 += t.c2 * w + f[R_C2] * dw;
+                const double om = __dsub_rn(1.0, abar);
+                dT = dT * om + T * (-dabar);
+                T = __dmul_rn(T, om);
+                if (T < ro.t_stop) done = true;
+            }
+            if (done) mine = 0u;
         }
         __syncwarp();
     }
@@ -681,7 +662,7 @@ void launch_raster_jvp(cudaStream_t st, const TileLists& tl, const double* rec,
                        const double* trec, int W, int H, const RenderP& ro, double* tangent) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    k_raster_jvp_staged<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
+    k_raster_jvp_bits<2><<<n * 4, 64, 0, st>>>(tl, rec, trec, W, H, ro, tangent);
     SGTR_CUDA(cudaGetLastError());
 }
 
