@@ -87,8 +87,8 @@ void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_e
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, double* img, double* tfinal, int* last,
                        unsigned long long* counters = nullptr);
-// K10: back-to-front adjoint sweep; each warp (one 8x8 block of a tile)
-// writes its reduced adjoints of duplicate d to part[(d * 4 + block) * 10 ...]
+// K10: back-to-front adjoint sweep; each warp (one 16x8 block of a tile)
+// writes its reduced adjoints of duplicate d to part[(d * 2 + block) * 10 ...]
 // and flags mask[d * 4 + block]; mask must be zeroed first
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,

@@ -261,10 +261,10 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
-    // the <= 4 per-warp partials of each duplicate, in (duplicate, warp)
+    // the <= 2 per-warp partials of each duplicate, in (duplicate, warp)
     // order; the partials are stored by splat-major duplicate slot, so a
-    // splat's are one contiguous run of 320-byte records; masks of 4
-    // duplicates (4 bytes each) are fetched together
+    // splat's are one contiguous run of 160-byte records; the masks of 4
+    // duplicates (2 bytes each) are fetched together
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         long long jp[4];
         unsigned mk[4];
@@ -272,7 +272,9 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
         for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? off + t0 + u : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            mk[u] = jp[u] >= 0 ? *reinterpret_cast<const unsigned*>(mask + kVjpSlots * jp[u]) : 0u;
+            mk[u] = jp[u] < 0
+                        ? 0u
+                        : *reinterpret_cast<const unsigned short*>(mask + kVjpSlots * jp[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (mk[u] == 0u) continue;

@@ -3,8 +3,8 @@
 //
 // Tiles are 16x16 pixels with per-tile fragment lists in depth order
 // (binning.cu).  In K7 (two-warp CTAs) and K10 (one-warp CTAs) each warp owns
-// one block of its tile (K7: 8x4 pixels, one per lane; K10: 8x8, two per lane,
-// rows r and r + 4) and walks the tile list on its own, 32 entries per batch: the lane
+// one block of its tile (K7: 8x4 pixels, one per lane; K10: 16x8, four per
+// lane) and walks the tile list on its own, 32 entries per batch: the lane
 // of list entry base + j tests that entry's exact pixel rectangle (K1's
 // pixel_range of the FP64 bbox) against the block as a bit mask of covered
 // pixels, stages the fragment's raster fields into warp-private shared
@@ -329,72 +329,71 @@ __global__ void __launch_bounds__(32 * WPB)
 constexpr int kRedStride = 33;
 
 // ------------------------------------------------------------------ K10, hit bitmasks
-// One warp per 8x8 block of a tile, two pixels per lane (rows r and r + 4),
-// back to front from each pixel's stored last index (render.cpp:238-257
-// walks [0, last)), with the per-(entry, pixel) tests done as bit arithmetic
-// (as in K7): the staging lane of list entry base + j turns its pixel
-// rectangle into the 64-bit mask of the block's pixels it covers; two warp
-// bit-transposes give each lane the entries covering its two pixels, cut to
-// the entries below each pixel's last index (one low-bits mask); an
-// OR-reduction gives the entries the warp visits.  Each visited fragment's 9
-// adjoints are reduced over the warp (the ring below) into one partial per
-// (duplicate, block), flagged in mask.  Records are staged at their list
-// offset (no compaction); the staging is double-buffered with cp.async as in
-// K7.  Per pixel and per partial the operations and their order are those of
-// the round-1 kernel (k_raster_vjp_staged3): the partials are bit-identical
-// to it.
-template <int WPB, int kMinB = 10>
-__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
-    k_raster_vjp_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+// One warp per 16x8 block, two per tile, four pixels per lane (columns c and
+// c + 8, rows r and r + 4), back to front from each pixel's stored last
+// index (render.cpp:238-257 walks [0, last)), with the per-(entry, pixel)
+// tests done as bit arithmetic (as in K7): the staging lane of list entry
+// base + j turns its pixel rectangle into the 64-bit masks of the block's two
+// 8x8 halves; four warp bit-transposes give each lane the entries covering
+// its four pixels, cut to the entries below each pixel's last index (one
+// low-bits mask); an OR-reduction gives the entries the warp visits.  Per
+// visited fragment each 8-column half runs a pixel-pair body (skipped,
+// warp-uniformly, when no lane's pixel in the half takes the fragment; both
+// pixels in one straight-line block when both rows do), and the fragment's
+// 9 adjoints, summed over a lane's pixels in (half, row) order, are reduced
+// over the warp (the ring) into one partial per (duplicate, block), flagged
+// in mask.  One list walk, record load, ring store and flush per fragment
+// serve 128 pixels, and a duplicate has two partials (K11 reads half of what
+// 8x8 blocks wrote: -27 % K11 for +2 % K10).  Records are staged at their
+// list offset; the staging is double-buffered with cp.async as in K7.
+template <int kMinB>
+__global__ void __launch_bounds__(32, kMinB)
+    k_raster_vjp_wide(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
                       const double* __restrict__ adj, const double* __restrict__ tfinal,
                       const int* __restrict__ last, double* __restrict__ part,
                       unsigned char* __restrict__ mask) {
-    constexpr int SUB = 4 / WPB;
     constexpr int kRing = 3;  // 27 columns: one per lane
-    __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
-    __shared__ long long s_ring_out[WPB][kRing];
-    __shared__ __align__(16) StagedRec s_rec[WPB][2][32];
-    __shared__ int s_slot[WPB][2][32];
-    const int tile =
-        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
-    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
-    const int warp = (blockIdx.x % SUB) * WPB + lw;
-    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
-    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
-    const int px = bx0 + (lane & 7);
+    __shared__ double s_ring[kRing * kAdj][kRedStride];
+    __shared__ long long s_ring_out[kRing];
+    __shared__ __align__(16) StagedRec s_rec[2][32];
+    __shared__ int s_slot[2][32];
+    const int tile = tl.order ? tl.order[blockIdx.x >> 1] : (blockIdx.x >> 1) + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31;
+    const int warp = blockIdx.x & 1;  // the tile's upper or lower 16x8 block
+    const int bx0 = (tile % tl.tiles_x) * kTile;
+    const int by0 = (tile / tl.tiles_x) * kTile + warp * 8;
+    const int px0 = bx0 + (lane & 7);
     const int py0 = by0 + (lane >> 3);
-    const double pxc = px + 0.5;
+    const double pxc[2] = {px0 + 0.5, px0 + 8.5};
     const double pyc[2] = {py0 + 0.5, py0 + 4.5};
     const int start = tl.tile_start[tile];
     const long long P = (long long)W * H;
-    double u0[2], u1[2], u2[2], T[2], ub[2];
-    int lastp[2];
+    // pixel q = 2 h + k: column half h, row k
+    double u0[4], u1[4], u2[4], T[4], ub[4];
+    int lastp[4];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int py = py0 + 4 * k;
-        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
-        lastp[k] = 0;
+    for (int q = 0; q < 4; ++q) {
+        const int px = px0 + 8 * (q >> 1), py = py0 + 4 * (q & 1);
+        u0[q] = u1[q] = u2[q] = T[q] = 0.0;
+        lastp[q] = 0;
         if (px < W && py < H) {
             const long long p = (long long)py * W + px;
-            u0[k] = adj[p];
-            u1[k] = adj[P + p];
-            u2[k] = adj[2 * P + p];
-            T[k] = tfinal[p];
-            lastp[k] = last[p];
-            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
+            u0[q] = adj[p];
+            u1[q] = adj[P + p];
+            u2[q] = adj[2 * P + p];
+            T[q] = tfinal[p];
+            lastp[q] = last[p];
+            if (u0[q] == 0.0 && u1[q] == 0.0 && u2[q] == 0.0) lastp[q] = 0;  // render.cpp:283
         }
-        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
+        ub[q] = T[q] * (u0[q] * ro.bg[0] + u1[q] * ro.bg[1] + u2[q] * ro.bg[2]);
     }
-    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
-    double(*ring)[kRedStride] = s_ring[lw];
-    long long* ring_out = s_ring_out[lw];
+    const int wlast =
+        __reduce_max_sync(kFull, max(max(lastp[0], lastp[1]), max(lastp[2], lastp[3])));
     int nring = 0;  // warp-uniform
-    // sum the parked columns (lane = fragment * 9 + adjoint), write them and
-    // flag the slots
     auto flush = [&](int n) {
         __syncwarp();
         if (lane < n * kAdj) {
-            const double* col = ring[lane];
+            const double* col = s_ring[lane];
             double t0 = col[0], t1 = col[11], t2 = col[22];
 #pragma unroll
             for (int k = 1; k < 11; ++k) {
@@ -406,75 +405,76 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
             double v = (t0 + t1) + t2;
             if (c == 2 || c == 4) v *= -0.5;
             if (c == 3) v = -v;
-            const long long slot = ring_out[fe] * kVjpSlots + warp;
+            const long long slot = s_ring_out[fe] * kVjpSlots + warp;
             part[slot * kPartStride + c] = v;
             if (c == 0) mask[slot] = 1;
         }
         __syncwarp();
     };
-    // stage the batch [base, top) into buffer `buf`: test the rectangles, start
-    // the record copies
-    auto stage = [&](int top, int buf) -> unsigned long long {
+    auto stage = [&](int top, int buf, unsigned long long& sl, unsigned long long& sr) {
         const int base = max(start, top - 32);
         const int jj = base + lane;
-        unsigned long long slots = 0ull;
+        sl = sr = 0ull;
         if (jj < top) {
-            slots = block_slots(__ldg(tl.trect + jj), bx0, by0, 8);
-            if (slots) {
+            const int4 rr = __ldg(tl.trect + jj);
+            sl = block_slots(rr, bx0, by0, 8);
+            sr = block_slots(rr, bx0 + 8, by0, 8);
+            if (sl | sr) {
                 const double* src = rec + (long long)kRec * __ldg(tl.tile_ids + jj) + 4;
-                double* dst = reinterpret_cast<double*>(&s_rec[lw][buf][lane]);
+                double* dst = reinterpret_cast<double*>(&s_rec[buf][lane]);
 #pragma unroll
                 for (int q = 0; q < 5; ++q) cp_async16(dst + 2 * q, src + 2 * q);
-                s_slot[lw][buf][lane] = __ldg(tl.sorted_d + jj);
+                s_slot[buf][lane] = __ldg(tl.sorted_d + jj);
             }
         }
         cp_async_commit();
-        return slots;
     };
     int buf = 0;
-    unsigned long long slots_cur = wlast > 0 ? stage(start + wlast, 0) : 0ull;
+    unsigned long long cl_cur = 0ull, cr_cur = 0ull;
+    if (wlast > 0) stage(start + wlast, 0, cl_cur, cr_cur);
     for (int top = start + wlast; top > start; top -= 32) {
         const int base = max(start, top - 32);
-        // the next (nearer) batch's copies overlap this batch's sweep
-        const unsigned long long slots = slots_cur;
-        slots_cur = base > start ? stage(base, buf ^ 1) : (cp_async_commit(), 0ull);
-        const StagedRec* my_rec = s_rec[lw][buf];
-        const int* my_slot = s_slot[lw][buf];
-        // bit j of m[k]: entry base + j covers pixel k and lies below its
+        const unsigned long long sl = cl_cur, sr = cr_cur;
+        if (base > start)
+            stage(base, buf ^ 1, cl_cur, cr_cur);
+        else
+            cp_async_commit();
+        const StagedRec* my_rec = s_rec[buf];
+        const int* my_slot = s_slot[buf];
+        // bit j of m[q]: entry base + j covers pixel q and lies below its
         // stored last index
-        unsigned m[2] = {warp_transpose32((unsigned)slots),
-                         warp_transpose32((unsigned)(slots >> 32))};
+        unsigned m[4] = {warp_transpose32((unsigned)sl), warp_transpose32((unsigned)(sl >> 32)),
+                         warp_transpose32((unsigned)sr), warp_transpose32((unsigned)(sr >> 32))};
+        unsigned w[4];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int lim = min(max(start + lastp[k] - base, 0), 32);
-            m[k] &= lim >= 32 ? ~0u : ((1u << lim) - 1u);
+        for (int q = 0; q < 4; ++q) {
+            const int lim = min(max(start + lastp[q] - base, 0), 32);
+            m[q] &= lim >= 32 ? ~0u : ((1u << lim) - 1u);
+            w[q] = __reduce_or_sync(kFull, m[q]);
         }
-        const unsigned w0 = __reduce_or_sync(kFull, m[0]), w1 = __reduce_or_sync(kFull, m[1]);
-        unsigned wb = w0 | w1;
+        unsigned wb = (w[0] | w[1]) | (w[2] | w[3]);
         cp_async_wait<1>();
         __syncwarp();
         while (wb) {
             const int e = 31 - __clz(wb);  // back to front
             wb &= ~(1u << e);
-            const bool any0 = (w0 >> e) & 1u, any1 = (w1 >> e) & 1u;
-            bool lv[2] = {(bool)((m[0] >> e) & 1u), (bool)((m[1] >> e) & 1u)};
             const StagedRec r = my_rec[e];
             double g[kAdj];
 #pragma unroll
             for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
             bool contrib = false;
             // one pixel's contribution given its falloff (render.cpp:238-283)
-            auto accumulate = [&](int k, double dx, double dxx, double dy, double ax, double ay,
+            auto accumulate = [&](int q, double dx, double dxx, double dy, double ax, double ay,
                                   double gauss, double abar, bool clamped, double rom) {
                 contrib = true;
-                const double t_in = T[k] * rom;
+                const double t_in = T[q] * rom;
                 const double at = abar * t_in;
-                g[6] += u0[k] * at;
-                g[7] += u1[k] * at;
-                g[8] += u2[k] * at;
-                const double uc = u0[k] * r.c0 + u1[k] * r.c1 + u2[k] * r.c2;
-                const double dab = uc * t_in - ub[k] * rom;
-                ub[k] += uc * at;
+                g[6] += u0[q] * at;
+                g[7] += u1[q] * at;
+                g[8] += u2[q] * at;
+                const double uc = u0[q] * r.c0 + u1[q] * r.c1 + u2[q] * r.c2;
+                const double dab = uc * t_in - ub[q] * rom;
+                ub[q] += uc * at;
                 if (!clamped) {
                     g[5] += gauss * dab;
                     const double de = abar * dab;
@@ -484,50 +484,56 @@ __global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
                     g[0] += de * ax;
                     g[1] += de * ay;
                 }
-                T[k] = t_in;
+                T[q] = t_in;
             };
             const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
                                   r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
-            const double dx = pxc - r.mx;
-            const double dxx = dx * dx;  // shared by the lane's two pixels (one column)
-            if (any0 && any1) {
-                double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
-                bool cl[2];
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    dy[k] = pyc[k] - r.my;
-                    gauss[k] = falloff_of(dx, dy[k], f, ax[k], ay[k]);
-                    abar[k] = __dmul_rn(r.alpha, gauss[k]);
-                    cl[k] = abar[k] >= ro.alpha_clamp;
-                    if (cl[k]) abar[k] = ro.alpha_clamp;
-                    lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
-                    rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
-                }
+            for (int h = 0; h < 2; ++h) {
+                const bool any0 = (w[2 * h] >> e) & 1u, any1 = (w[2 * h + 1] >> e) & 1u;
+                if (!any0 && !any1) continue;  // warp-uniform
+                bool lv[2] = {(bool)((m[2 * h] >> e) & 1u), (bool)((m[2 * h + 1] >> e) & 1u)};
+                const double dx = pxc[h] - r.mx;
+                const double dxx = dx * dx;  // shared by the half's two pixels (one column)
+                if (any0 && any1) {
+                    double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
+                    bool cl[2];
 #pragma unroll
-                for (int k = 0; k < 2; ++k)
-                    if (lv[k])
-                        accumulate(k, dx, dxx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k],
-                                   rom[k]);
-            } else {
+                    for (int k = 0; k < 2; ++k) {
+                        dy[k] = pyc[k] - r.my;
+                        gauss[k] = falloff_of(dx, dy[k], f, ax[k], ay[k]);
+                        abar[k] = __dmul_rn(r.alpha, gauss[k]);
+                        cl[k] = abar[k] >= ro.alpha_clamp;
+                        if (cl[k]) abar[k] = ro.alpha_clamp;
+                        lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
+                        rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
+                    }
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
-                    const double dy = pyc[k] - r.my;
-                    double ax, ay;
-                    const double gauss = falloff_of(dx, dy, f, ax, ay);
-                    double abar = __dmul_rn(r.alpha, gauss);
-                    const bool clamped = abar >= ro.alpha_clamp;
-                    if (clamped) abar = ro.alpha_clamp;
-                    if (abar < ro.alpha_skip) continue;
-                    accumulate(k, dx, dxx, dy, ax, ay, gauss, abar, clamped,
-                               rcp_unit(__dsub_rn(1.0, abar)));
+                    for (int k = 0; k < 2; ++k)
+                        if (lv[k])
+                            accumulate(2 * h + k, dx, dxx, dy[k], ax[k], ay[k], gauss[k], abar[k],
+                                       cl[k], rom[k]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
+                        const double dy = pyc[k] - r.my;
+                        double ax, ay;
+                        const double gauss = falloff_of(dx, dy, f, ax, ay);
+                        double abar = __dmul_rn(r.alpha, gauss);
+                        const bool clamped = abar >= ro.alpha_clamp;
+                        if (clamped) abar = ro.alpha_clamp;
+                        if (abar < ro.alpha_skip) continue;
+                        accumulate(2 * h + k, dx, dxx, dy, ax, ay, gauss, abar, clamped,
+                                   rcp_unit(__dsub_rn(1.0, abar)));
+                    }
                 }
             }
             const unsigned cm = __ballot_sync(kFull, contrib);
             if (cm == 0u) continue;
 #pragma unroll
-            for (int c = 0; c < kAdj; ++c) ring[nring * kAdj + c][lane] = g[c];
-            if (lane == 0) ring_out[nring] = my_slot[e];
+            for (int c = 0; c < kAdj; ++c) s_ring[nring * kAdj + c][lane] = g[c];
+            if (lane == 0) s_ring_out[nring] = my_slot[e];
             if (++nring == kRing) {
                 flush(kRing);
                 nring = 0;
@@ -654,7 +660,9 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    k_raster_vjp_bits<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
+    // 128 registers (16 one-warp CTAs per SM; the shared-memory limit is 17)
+    static_assert(kVjpSlots == 2, "K10 writes one partial per 16x8 block");
+    k_raster_vjp_wide<16><<<n * 2, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
     SGTR_CUDA(cudaGetLastError());
 }
 
