@@ -15,6 +15,6 @@ echo "launch list rc=$?"
 cmd1="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
 SGTR_LANES=1 $cmd1 > gpurun_out/pre1_$tag.log 2>&1 && \
   SGTR_LANES=1 ncu --set full --import-source on --clock-control none --kernel-name-base function \
-      -k regex:"^(k_raster_vjp_bits|k_raster_fwd_bits|k_chain_warp|k_ssim|k_gather|k_project|k_tile_ids|k_emit_small)$" \
+      -k regex:"^(k_raster_vjp_wide|k_raster_fwd_bits|k_chain_warp|k_ssim|k_gather|k_project|k_tile_ids|k_emit_small)$" \
       -s 700 -c 10 -o gpurun_out/prof_full_$tag $cmd1 > gpurun_out/ncu_full_$tag.log 2>&1
 echo "full capture rc=$?"
