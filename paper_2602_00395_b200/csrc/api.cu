@@ -632,6 +632,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.large = c.large.as<int>(K + 1);
     b.n_large = &c.dstat->n_large;
     b.off_r = c.off_r.as<long long>(K + 1);
+    b.off_id = c.off_id.as<long long>(std::max(K, 1));
     b.tile_start = c.tile_start.as<int>(std::max(n_tiles, 1));
     b.tile_end = c.tile_end.as<int>(std::max(n_tiles, 1));
     b.temp = c.temp.ensure(std::max(depth_sort_temp_bytes(K), scan_temp_bytes(K)));
@@ -737,11 +738,10 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
                                mask);
     }
     Timed t(c, KC_CHAIN);
-    long long* off_id = c.off_id.as<long long>(std::max(c.K, 1));
-    launch_offsets_by_id(c.st, c.ids_alt.get<int>(), c.K, c.off_r.get<long long>(), off_id);
+    const long long* off_id = c.off_id.get<long long>();  // written by K4 (bin_tiles)
     launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, off_id, c.tcount.get<int>(), vr.cap,
                       part, mask, zdense, zbits, acc, flag);
-    c.launches += 3;
+    c.launches += 2;
 }
 
 struct SsimOut {

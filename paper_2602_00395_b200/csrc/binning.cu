@@ -80,15 +80,17 @@ __global__ void __launch_bounds__(256) k_emit_small(const int* __restrict__ sort
                                                     const unsigned long long* __restrict__ tmask,
                                                     const long long* __restrict__ off_r,
                                                     int n_visible, int tiles_x, long long cap,
+                                                    long long* __restrict__ off_id,
                                                     unsigned int* __restrict__ tkeys,
                                                     int* __restrict__ dval,
                                                     int* __restrict__ dup_id,
                                                     int* __restrict__ large,
                                                     int* __restrict__ n_large) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_visible || off_r[n_visible] > cap) return;
+    if (r >= n_visible) return;
     const int id = sorted_ids[r];
-    if (tcount[id] == 0) return;
+    off_id[id] = off_r[r];  // K11 finds a splat's partials by id
+    if (off_r[n_visible] > cap || tcount[id] == 0) return;
     const int4 pr = rect[id];
     const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
     const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
@@ -304,8 +306,8 @@ void bin_tiles(cudaStream_t st, BinBuffers& b, int K, int tiles_x, int n_tiles, 
     const unsigned int sentinel = (unsigned int)n_tiles;
     SGTR_CUDA(cudaMemsetAsync(b.n_large, 0, sizeof(int), st));
     k_emit_small<<<ceil_div(K, 256), 256, 0, st>>>(b.ids_alt, b.tcount, b.rect, b.tmask, b.off_r, K,
-                                                   tiles_x, cap, b.tkeys, b.dval, b.dup_id, b.large,
-                                                   b.n_large);
+                                                   tiles_x, cap, b.off_id, b.tkeys, b.dval,
+                                                   b.dup_id, b.large, b.n_large);
     SGTR_CUDA(cudaGetLastError());
     k_emit_large<<<148 * 4, 256, 0, st>>>(b.ids_alt, b.rect, b.rec, b.off_r, tiles_x, b.large,
                                           b.n_large, b.tkeys, b.dval, b.dup_id);

@@ -37,6 +37,7 @@ struct BinBuffers {
     int* large;            // depth ranks of splats with > 64-tile rectangles
     int* n_large;
     long long* off_r;      // K+1 exclusive duplicate offsets in depth-rank order
+    long long* off_id;     // the same offsets by splat id (K4 scatters them, K11 reads them)
     // duplicate arrays, capacity `cap` entries
     unsigned int *tkeys, *tkeys_alt;
     int *dval, *dval_alt;  // duplicate index carried through the tile sort
@@ -93,9 +94,6 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
-// splat id -> offset of its duplicates (off_r scattered from depth-rank order)
-void launch_offsets_by_id(cudaStream_t st, const int* sorted_ids, int K, const long long* off_r,
-                          long long* off_id);
 // K11: per splat (id order), the sum of its flagged K10 partials (duplicate,
 // block order) and the chain through invert2x2 and the projection; mode 0
 // adds the gradient into acc, mode 1 z (.) it (Hutchinson, probe dense or as

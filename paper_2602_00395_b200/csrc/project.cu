@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     // threads in splat-id order, so the scene reads and the gradient
     // read-modify-writes below are coalesced (at C5's 10M splats they no
     // longer fit in L2); a splat's partials are found through its duplicate
-    // offset (off_id, k_offsets_by_id)
+    // offset (off_id, scattered by K4)
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= K) return;
     const int cnt = tcount[id];
@@ -357,23 +357,7 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     if (!finite) *nonfinite_flag = 1.0;  // idempotent store
 }
 
-// the offset of each splat id's duplicates (the K+1 entry scan of the
-// counts in depth-rank order, scattered to id order)
-__global__ void k_offsets_by_id(const int* __restrict__ sorted_ids, int K,
-                                const long long* __restrict__ off_r,
-                                long long* __restrict__ off_id) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < K) off_id[sorted_ids[r]] = off_r[r];
-}
-
 }  // namespace
-
-void launch_offsets_by_id(cudaStream_t st, const int* sorted_ids, int K, const long long* off_r,
-                          long long* off_id) {
-    if (K == 0) return;
-    k_offsets_by_id<<<ceil_div(K, 256), 256, 0, st>>>(sorted_ids, K, off_r, off_id);
-    SGTR_CUDA(cudaGetLastError());
-}
 
 void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
