@@ -453,7 +453,7 @@ struct Ctx {
     Rng rng{1};       // committed state: all draws of completed steps
     Prefetcher prefetch;
     // per-view workspace
-    Buf rec, trec, keys, keys_alt, ids, ids_alt, rect, tcount, off_r;
+    Buf rec, trec, keys, keys_alt, keys32, keys32_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
     Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, off_id, ovals;
@@ -468,7 +468,8 @@ struct Ctx {
         DevStatus* dstat = nullptr;
         DevStatus* hstat = nullptr;
 #define SGTR_LANE_BUFS(X)                                                                    \
-    X(rec) X(keys) X(keys_alt) X(ids) X(ids_alt) X(rect) X(tcount) X(off_r) X(tkeys)         \
+    X(rec) X(keys) X(keys_alt) X(keys32) X(keys32_alt) X(ids) X(ids_alt) X(rect) X(tcount)   \
+    X(off_r) X(tkeys)                                                                        \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp)             \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
     X(part) X(mask) X(tmask) X(large) X(trect) X(off_id) X(ovals)
@@ -624,6 +625,8 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     BinBuffers b;
     b.keys = c.keys.as<unsigned long long>(K + 1);
     b.keys_alt = c.keys_alt.as<unsigned long long>(K + 1);
+    b.keys32 = c.keys32.as<unsigned int>(K + 1);
+    b.keys32_alt = c.keys32_alt.as<unsigned int>(K + 1);
     b.ids = c.ids.as<int>(K + 1);
     b.ids_alt = c.ids_alt.as<int>(K + 1);
     b.rect = c.rect.as<int4>(K + 1);
@@ -644,8 +647,8 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     view_begin(c.st, &c.dstat->vs);
     {
         Timed t(c, KC_PROJECT);
-        launch_project(c.st, c.X(), K, c.nb, dc, ro, rec, b.keys, b.ids, b.rect, b.tcount, b.tmask,
-                       &c.dstat->vs);
+        launch_project(c.st, c.X(), K, c.nb, dc, ro, rec, b.keys, b.keys32, b.ids, b.rect,
+                       b.tcount, b.tmask, &c.dstat->vs);
     }
     {
         Timed t(c, KC_DEPTH_SORT);

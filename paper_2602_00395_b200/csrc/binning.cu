@@ -25,32 +25,31 @@
 namespace sgtr {
 namespace {
 
-// After a radix sort on key bits [kDepthLoBit, 64) only, keys that agree on
-// those bits keep their input (= splat index) order; each such run is put
-// into full-key order here (insertion sort, stable, so equal keys stay in
-// index order) -- the same (depth, index) order as a full 64-bit sort
-// (render.cpp:83-87).  Runs are rare and short: the ignored 24 low bits are
-// below 2^-28 relative depth.
-constexpr int kDepthLoBit = 24;
-
-__global__ void k_fix_depth_ties(unsigned long long* __restrict__ keys, int* __restrict__ ids,
-                                 int K) {
+// K2 sorts the FP32-rounded depths (a monotone map, so the order only
+// coarsens): 32-bit keys, 4 onesweep passes.  Splats whose FP32 depths
+// agree keep their input (= splat index) order; each such run is put into
+// (full 64-bit key, index) order here by a stable insertion sort on the full
+// keys -- the same (depth, index) order as a full 64-bit sort
+// (render.cpp:83-87).  Runs are rare and short: FP32 resolves 2^-24 relative
+// depth.  The culled splats (key 0xffffffff, no tiles) stay in index order.
+__global__ void k_fix_depth_ties(const unsigned int* __restrict__ k32,
+                                 const unsigned long long* __restrict__ k64,
+                                 int* __restrict__ ids, int K) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= K) return;
-    const unsigned long long hi = keys[i] >> kDepthLoBit;
-    if (i > 0 && (keys[i - 1] >> kDepthLoBit) == hi) return;  // not a run start
+    const unsigned int hi = k32[i];
+    if (hi == 0xffffffffu) return;
+    if (i > 0 && k32[i - 1] == hi) return;  // not a run start
     int e = i + 1;
-    while (e < K && (keys[e] >> kDepthLoBit) == hi) ++e;
+    while (e < K && k32[e] == hi) ++e;
     for (int a = i + 1; a < e; ++a) {
-        const unsigned long long k = keys[a];
         const int id = ids[a];
+        const unsigned long long k = k64[id];
         int b = a - 1;
-        while (b >= i && keys[b] > k) {
-            keys[b + 1] = keys[b];
+        while (b >= i && k64[ids[b]] > k) {
             ids[b + 1] = ids[b];
             --b;
         }
-        keys[b + 1] = k;
         ids[b + 1] = id;
     }
 }
@@ -257,9 +256,8 @@ void view_end(cudaStream_t st, const ViewStatus* vs, const long long* total, lon
 
 size_t depth_sort_temp_bytes(int K) {
     size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr,
-                                    K, kDepthLoBit, 64);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned int*)nullptr, (unsigned int*)nullptr,
+                                    (int*)nullptr, (int*)nullptr, K, 0, 32);
     return bytes;
 }
 
@@ -288,9 +286,9 @@ void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_e
 void depth_sort_and_scan(cudaStream_t st, BinBuffers& b, int K) {
     if (K > 0) {
         size_t bytes = b.temp_bytes;
-        SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.keys, b.keys_alt, b.ids,
-                                                  b.ids_alt, K, kDepthLoBit, 64, st));
-        k_fix_depth_ties<<<ceil_div(K, 256), 256, 0, st>>>(b.keys_alt, b.ids_alt, K);
+        SGTR_CUDA(cub::DeviceRadixSort::SortPairs(b.temp, bytes, b.keys32, b.keys32_alt, b.ids,
+                                                  b.ids_alt, K, 0, 32, st));
+        k_fix_depth_ties<<<ceil_div(K, 256), 256, 0, st>>>(b.keys32_alt, b.keys, b.ids_alt, K);
         SGTR_CUDA(cudaGetLastError());
     }
     // K3: exclusive scan of the tile counts gathered in depth-rank order

@@ -15,8 +15,9 @@ namespace sgtr {
 // tmask: per splat, the hit bits of its tile rectangle in row-major order
 // (rectangles of <= 64 tiles)
 void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
-                    const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
-                    int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status);
+                    const RenderP& ro, double* rec, unsigned long long* keys,
+                    unsigned int* keys32, int* ids, int4* rect, int* tcount,
+                    unsigned long long* tmask, ViewStatus* status);
 // parity dump: 12 doubles per splat (culled, depth, px, py, bx0..by1, i00..i11, 0)
 void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& cam,
                          const RenderP& ro, double* out);
@@ -29,6 +30,7 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const D
 // ---------------------------------------------------------------- binning.cu
 struct BinBuffers {
     unsigned long long *keys, *keys_alt;
+    unsigned int *keys32, *keys32_alt;  // K2's FP32-depth sort keys (K1 writes keys32)
     int *ids, *ids_alt;
     int4* rect;            // bbox pixel range (x0, y0, x1, y1) per splat
     const double* rec;     // fragment records (K1)

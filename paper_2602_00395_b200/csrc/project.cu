@@ -57,6 +57,7 @@ template <bool kSH>
 __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, int K, int nb,
                                                  DevCam cam, RenderP ro, double* __restrict__ rec,
                                                  unsigned long long* __restrict__ keys,
+                                                 unsigned int* __restrict__ keys32,
                                                  int* __restrict__ ids, int4* __restrict__ rect,
                                                  int* __restrict__ tcount,
                                                  unsigned long long* __restrict__ tmask,
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
         // binned, so its NaN rectangle cannot inflate the duplicate count
         if (pr.culled || pr.degenerate || !finite) {
             keys[i] = kCulledKey;
+            keys32[i] = 0xffffffffu;
             tcount[i] = 0;
         } else {
             visible = true;
@@ -95,6 +97,10 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
 #pragma unroll
             for (int j = 0; j < kRec / 2; ++j) dst[j] = make_double2(r[2 * j], r[2 * j + 1]);
             keys[i] = depth_key(pr.depth);
+            // K2's sort key: the depth rounded to FP32 (monotone; positive, so
+            // its bits order as unsigned); equal FP32 depths are ordered by
+            // the full key afterwards
+            keys32[i] = __float_as_uint(__double2float_rn(pr.depth));
             int x0, x1, y0, y1;
             pixel_range(r[R_BX0], r[R_BX1], cam.W, x0, x1);
             pixel_range(r[R_BY0], r[R_BY1], cam.H, y0, y1);
@@ -360,15 +366,16 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
 }  // namespace
 
 void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
-                    const RenderP& ro, double* rec, unsigned long long* keys, int* ids,
-                    int4* rect, int* tcount, unsigned long long* tmask, ViewStatus* status) {
+                    const RenderP& ro, double* rec, unsigned long long* keys,
+                    unsigned int* keys32, int* ids, int4* rect, int* tcount,
+                    unsigned long long* tmask, ViewStatus* status) {
     if (K == 0) return;
     if (nb)
-        k_project<true><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids, rect,
-                                                          tcount, tmask, status);
+        k_project<true><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, keys32,
+                                                          ids, rect, tcount, tmask, status);
     else
-        k_project<false><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, ids,
-                                                           rect, tcount, tmask, status);
+        k_project<false><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, keys32,
+                                                           ids, rect, tcount, tmask, status);
     SGTR_CUDA(cudaGetLastError());
 }
 
