@@ -742,8 +742,9 @@ void backward_view(Ctx& c, const DevCam& dc, const RenderP& ro, const ViewRender
     }
     Timed t(c, KC_CHAIN);
     const long long* off_id = c.off_id.get<long long>();  // written by K4 (bin_tiles)
+    const int slots = vjp_slots(vr.tl.tiles_x * (vr.tl.row1 - vr.tl.row0));
     launch_chain_warp(c.st, mode, c.X(), c.K, c.nb, dc, ro, off_id, c.tcount.get<int>(), vr.cap,
-                      part, mask, zdense, zbits, acc, flag);
+                      slots, part, mask, zdense, zbits, acc, flag);
     c.launches += 2;
 }
 

@@ -28,7 +28,8 @@ constexpr int kTilePixels = kTile * kTile;
 constexpr int kRec = 16;              // doubles per projected-fragment record
 constexpr int kTRec = 12;             // doubles per tangent record
 constexpr int kAdj = 9;               // adjoint slots per (tile, fragment)
-constexpr int kVjpSlots = 2;          // K10 partials per duplicate: one per 16x8 block of its tile
+constexpr int kVjpSlots = 4;          // K10 partials per duplicate, at most: one per block of its tile
+constexpr int kWideVjpTiles = 4096;   // from this many tiles on, K10 uses 16x8 blocks (2 per tile)
 constexpr int kPartStride = 10;       // doubles per K10 partial (9 adjoints + 1 pad: 16-B aligned)
 
 // fragment record fields (one 128-byte record per splat id)

@@ -90,9 +90,12 @@ void launch_tile_order(cudaStream_t st, const int* tile_start, const int* tile_e
 void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                        int H, const RenderP& ro, double* img, double* tfinal, int* last,
                        unsigned long long* counters = nullptr);
-// K10: back-to-front adjoint sweep; each warp (one 16x8 block of a tile)
-// writes its reduced adjoints of duplicate d to part[(d * 2 + block) * 10 ...]
-// and flags mask[d * 4 + block]; mask must be zeroed first
+// K10: back-to-front adjoint sweep; each warp (one block of a tile: 16x8,
+// s = 2 per tile, when the raster region has >= kWideVjpTiles tiles, else
+// 8x8, s = 4) writes its reduced adjoints of duplicate d to
+// part[(d * s + block) * 10 ...] and flags mask[d * s + block]; mask must be
+// zeroed first.  vjp_slots(tiles of the region) gives s.
+int vjp_slots(int n_tiles);
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask);
@@ -104,7 +107,7 @@ void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* 
 // view, rerun by the step).
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb, const DevCam& cam,
                        const RenderP& ro, const long long* off_id, const int* tcount,
-                       long long cap, const double* part, const unsigned char* mask,
+                       long long cap, int slots, const double* part, const unsigned char* mask,
                        const double* zdense, const uint32_t* zbits, double* acc,
                        double* nonfinite_flag);
 // K12 (raster half): tangent image along the tangent records

@@ -240,7 +240,7 @@ __device__ __forceinline__ void chain_sh(const double* x, int K, int nb, int id,
 // transpose of the 5x10 Jacobian of (mu2d, inverse covariance) w.r.t.
 // (mu, s, q), which the reference evaluates with 10 dual seeds, is applied in
 // one reverse sweep (geometry.cuh: chain_reverse).
-template <bool kSH>
+template <bool kSH, int kSlots>
 __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* __restrict__ x, int K,
                                                int nb, DevCam cam, RenderP ro,
                                                const long long* __restrict__ off_id,
@@ -267,10 +267,11 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
     double a[kAdj];
 #pragma unroll
     for (int j = 0; j < kAdj; ++j) a[j] = 0.0;
-    // the <= 2 per-warp partials of each duplicate, in (duplicate, warp)
-    // order; the partials are stored by splat-major duplicate slot, so a
-    // splat's are one contiguous run of 160-byte records; the masks of 4
-    // duplicates (2 bytes each) are fetched together
+    // the kSlots (2 or 4, K10's blocks per tile) per-warp partials of each
+    // duplicate, in (duplicate, warp) order; the partials are stored by
+    // splat-major duplicate slot, so a splat's are one contiguous run of
+    // kSlots * 80-byte records; the masks of 4 duplicates (kSlots bytes each)
+    // are fetched together
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         long long jp[4];
         unsigned mk[4];
@@ -278,16 +279,17 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
         for (int u = 0; u < 4; ++u) jp[u] = t0 + u < cnt ? off + t0 + u : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            mk[u] = jp[u] < 0
-                        ? 0u
-                        : *reinterpret_cast<const unsigned short*>(mask + kVjpSlots * jp[u]);
+            mk[u] = jp[u] < 0 ? 0u
+                    : kSlots == 4
+                        ? *reinterpret_cast<const unsigned*>(mask + kSlots * jp[u])
+                        : *reinterpret_cast<const unsigned short*>(mask + kSlots * jp[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (mk[u] == 0u) continue;
             const double2* pp =
-                reinterpret_cast<const double2*>(part + jp[u] * kVjpSlots * kPartStride);
+                reinterpret_cast<const double2*>(part + jp[u] * kSlots * kPartStride);
 #pragma unroll
-            for (int w = 0; w < kVjpSlots; ++w) {
+            for (int w = 0; w < kSlots; ++w) {
                 if ((mk[u] >> (8 * w)) & 0xffu) {
                     // one 80-byte partial as five 16-byte loads (the pad unused)
                     double2 q[kPartStride / 2];
@@ -396,18 +398,18 @@ void launch_project_jvp(cudaStream_t st, const double* x, int K, int nb, const D
 
 void launch_chain_warp(cudaStream_t st, int mode, const double* x, int K, int nb,
                        const DevCam& cam, const RenderP& ro, const long long* off_id,
-                       const int* tcount, long long cap, const double* part,
+                       const int* tcount, long long cap, int slots, const double* part,
                        const unsigned char* mask, const double* zdense, const uint32_t* zbits,
                        double* acc, double* nonfinite_flag) {
     if (K == 0) return;
+    auto go = [&](auto kernel) {
+        kernel<<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id, tcount, cap,
+                                                 part, mask, zdense, zbits, acc, nonfinite_flag);
+    };
     if (nb)
-        k_chain_warp<true><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
-                                                             tcount, cap, part, mask, zdense,
-                                                             zbits, acc, nonfinite_flag);
+        slots == 2 ? go(k_chain_warp<true, 2>) : go(k_chain_warp<true, 4>);
     else
-        k_chain_warp<false><<<ceil_div(K, 128), 128, 0, st>>>(mode, x, K, nb, cam, ro, off_id,
-                                                              tcount, cap, part, mask, zdense,
-                                                              zbits, acc, nonfinite_flag);
+        slots == 2 ? go(k_chain_warp<false, 2>) : go(k_chain_warp<false, 4>);
     SGTR_CUDA(cudaGetLastError());
 }
 

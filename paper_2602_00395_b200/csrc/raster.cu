@@ -328,6 +328,219 @@ __global__ void __launch_bounds__(32 * WPB)
 
 constexpr int kRedStride = 33;
 
+// ------------------------------------------------------------------ K10, 8x8 blocks
+// (Small images, whose 16x8 grid would leave SMs idle: see launch_raster_vjp_warp.)
+// One warp per 8x8 block of a tile, two pixels per lane (rows r and r + 4),
+// back to front from each pixel's stored last index (render.cpp:238-257
+// walks [0, last)), with the per-(entry, pixel) tests done as bit arithmetic
+// (as in K7): the staging lane of list entry base + j turns its pixel
+// rectangle into the 64-bit mask of the block's pixels it covers; two warp
+// bit-transposes give each lane the entries covering its two pixels, cut to
+// the entries below each pixel's last index (one low-bits mask); an
+// OR-reduction gives the entries the warp visits.  Each visited fragment's 9
+// adjoints are reduced over the warp (the ring below) into one partial per
+// (duplicate, block), flagged in mask.  Records are staged at their list
+// offset (no compaction); the staging is double-buffered with cp.async as in
+// K7.  Per pixel and per partial the operations and their order are those of
+// the round-1 kernel (k_raster_vjp_staged3): the partials are bit-identical
+// to it.
+template <int WPB, int kMinB = 10>
+__global__ void __launch_bounds__(32 * WPB, kMinB * 2 / WPB)
+    k_raster_vjp_bits(TileLists tl, const double* __restrict__ rec, int W, int H, RenderP ro,
+                      const double* __restrict__ adj, const double* __restrict__ tfinal,
+                      const int* __restrict__ last, double* __restrict__ part,
+                      unsigned char* __restrict__ mask) {
+    constexpr int SUB = 4 / WPB;
+    constexpr int kRing = 3;  // 27 columns: one per lane
+    __shared__ double s_ring[WPB][kRing * kAdj][kRedStride];
+    __shared__ long long s_ring_out[WPB][kRing];
+    __shared__ __align__(16) StagedRec s_rec[WPB][2][32];
+    __shared__ int s_slot[WPB][2][32];
+    const int tile =
+        tl.order ? tl.order[blockIdx.x / SUB] : blockIdx.x / SUB + tl.row0 * tl.tiles_x;
+    const int lane = threadIdx.x & 31, lw = threadIdx.x >> 5;
+    const int warp = (blockIdx.x % SUB) * WPB + lw;
+    const int bx0 = (tile % tl.tiles_x) * kTile + (warp & 1) * 8;
+    const int by0 = (tile / tl.tiles_x) * kTile + (warp >> 1) * 8;
+    const int px = bx0 + (lane & 7);
+    const int py0 = by0 + (lane >> 3);
+    const double pxc = px + 0.5;
+    const double pyc[2] = {py0 + 0.5, py0 + 4.5};
+    const int start = tl.tile_start[tile];
+    const long long P = (long long)W * H;
+    double u0[2], u1[2], u2[2], T[2], ub[2];
+    int lastp[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = py0 + 4 * k;
+        u0[k] = u1[k] = u2[k] = T[k] = 0.0;
+        lastp[k] = 0;
+        if (px < W && py < H) {
+            const long long p = (long long)py * W + px;
+            u0[k] = adj[p];
+            u1[k] = adj[P + p];
+            u2[k] = adj[2 * P + p];
+            T[k] = tfinal[p];
+            lastp[k] = last[p];
+            if (u0[k] == 0.0 && u1[k] == 0.0 && u2[k] == 0.0) lastp[k] = 0;  // render.cpp:283
+        }
+        ub[k] = T[k] * (u0[k] * ro.bg[0] + u1[k] * ro.bg[1] + u2[k] * ro.bg[2]);
+    }
+    const int wlast = __reduce_max_sync(kFull, max(lastp[0], lastp[1]));
+    double(*ring)[kRedStride] = s_ring[lw];
+    long long* ring_out = s_ring_out[lw];
+    int nring = 0;  // warp-uniform
+    // sum the parked columns (lane = fragment * 9 + adjoint), write them and
+    // flag the slots
+    auto flush = [&](int n) {
+        __syncwarp();
+        if (lane < n * kAdj) {
+            const double* col = ring[lane];
+            double t0 = col[0], t1 = col[11], t2 = col[22];
+#pragma unroll
+            for (int k = 1; k < 11; ++k) {
+                t0 += col[k];
+                t1 += col[11 + k];
+                if (k < 10) t2 += col[22 + k];
+            }
+            const int fe = lane / kAdj, c = lane - fe * kAdj;
+            double v = (t0 + t1) + t2;
+            if (c == 2 || c == 4) v *= -0.5;
+            if (c == 3) v = -v;
+            const long long slot = ring_out[fe] * 4 + warp;  // four 8x8 blocks per tile
+            part[slot * kPartStride + c] = v;
+            if (c == 0) mask[slot] = 1;
+        }
+        __syncwarp();
+    };
+    // stage the batch [base, top) into buffer `buf`: test the rectangles, start
+    // the record copies
+    auto stage = [&](int top, int buf) -> unsigned long long {
+        const int base = max(start, top - 32);
+        const int jj = base + lane;
+        unsigned long long slots = 0ull;
+        if (jj < top) {
+            slots = block_slots(__ldg(tl.trect + jj), bx0, by0, 8);
+            if (slots) {
+                const double* src = rec + (long long)kRec * __ldg(tl.tile_ids + jj) + 4;
+                double* dst = reinterpret_cast<double*>(&s_rec[lw][buf][lane]);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) cp_async16(dst + 2 * q, src + 2 * q);
+                s_slot[lw][buf][lane] = __ldg(tl.sorted_d + jj);
+            }
+        }
+        cp_async_commit();
+        return slots;
+    };
+    int buf = 0;
+    unsigned long long slots_cur = wlast > 0 ? stage(start + wlast, 0) : 0ull;
+    for (int top = start + wlast; top > start; top -= 32) {
+        const int base = max(start, top - 32);
+        // the next (nearer) batch's copies overlap this batch's sweep
+        const unsigned long long slots = slots_cur;
+        slots_cur = base > start ? stage(base, buf ^ 1) : (cp_async_commit(), 0ull);
+        const StagedRec* my_rec = s_rec[lw][buf];
+        const int* my_slot = s_slot[lw][buf];
+        // bit j of m[k]: entry base + j covers pixel k and lies below its
+        // stored last index
+        unsigned m[2] = {warp_transpose32((unsigned)slots),
+                         warp_transpose32((unsigned)(slots >> 32))};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int lim = min(max(start + lastp[k] - base, 0), 32);
+            m[k] &= lim >= 32 ? ~0u : ((1u << lim) - 1u);
+        }
+        const unsigned w0 = __reduce_or_sync(kFull, m[0]), w1 = __reduce_or_sync(kFull, m[1]);
+        unsigned wb = w0 | w1;
+        cp_async_wait<1>();
+        __syncwarp();
+        while (wb) {
+            const int e = 31 - __clz(wb);  // back to front
+            wb &= ~(1u << e);
+            const bool any0 = (w0 >> e) & 1u, any1 = (w1 >> e) & 1u;
+            bool lv[2] = {(bool)((m[0] >> e) & 1u), (bool)((m[1] >> e) & 1u)};
+            const StagedRec r = my_rec[e];
+            double g[kAdj];
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) g[c] = 0.0;
+            bool contrib = false;
+            // one pixel's contribution given its falloff (render.cpp:238-283)
+            auto accumulate = [&](int k, double dx, double dxx, double dy, double ax, double ay,
+                                  double gauss, double abar, bool clamped, double rom) {
+                contrib = true;
+                const double t_in = T[k] * rom;
+                const double at = abar * t_in;
+                g[6] += u0[k] * at;
+                g[7] += u1[k] * at;
+                g[8] += u2[k] * at;
+                const double uc = u0[k] * r.c0 + u1[k] * r.c1 + u2[k] * r.c2;
+                const double dab = uc * t_in - ub[k] * rom;
+                ub[k] += uc * at;
+                if (!clamped) {
+                    g[5] += gauss * dab;
+                    const double de = abar * dab;
+                    g[2] += de * dxx;  // (dx dx) x -1/2 at the write
+                    g[3] += de * (dx * dy);  // x -1
+                    g[4] += de * (dy * dy);  // x -1/2
+                    g[0] += de * ax;
+                    g[1] += de * ay;
+                }
+                T[k] = t_in;
+            };
+            const double f[13] = {0.0,   0.0,   0.0,     0.0,  r.mx, r.my, r.i00,
+                                  r.i01, r.i11, r.alpha, r.c0, r.c1, r.c2};
+            const double dx = pxc - r.mx;
+            const double dxx = dx * dx;  // shared by the lane's two pixels (one column)
+            if (any0 && any1) {
+                double dy[2], ax[2], ay[2], gauss[2], abar[2], rom[2];
+                bool cl[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    dy[k] = pyc[k] - r.my;
+                    gauss[k] = falloff_of(dx, dy[k], f, ax[k], ay[k]);
+                    abar[k] = __dmul_rn(r.alpha, gauss[k]);
+                    cl[k] = abar[k] >= ro.alpha_clamp;
+                    if (cl[k]) abar[k] = ro.alpha_clamp;
+                    lv[k] = lv[k] && !(abar[k] < ro.alpha_skip);
+                    rom[k] = rcp_unit(__dsub_rn(1.0, abar[k]));
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                    if (lv[k])
+                        accumulate(k, dx, dxx, dy[k], ax[k], ay[k], gauss[k], abar[k], cl[k],
+                                   rom[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!(k == 0 ? any0 : any1) || !lv[k]) continue;
+                    const double dy = pyc[k] - r.my;
+                    double ax, ay;
+                    const double gauss = falloff_of(dx, dy, f, ax, ay);
+                    double abar = __dmul_rn(r.alpha, gauss);
+                    const bool clamped = abar >= ro.alpha_clamp;
+                    if (clamped) abar = ro.alpha_clamp;
+                    if (abar < ro.alpha_skip) continue;
+                    accumulate(k, dx, dxx, dy, ax, ay, gauss, abar, clamped,
+                               rcp_unit(__dsub_rn(1.0, abar)));
+                }
+            }
+            const unsigned cm = __ballot_sync(kFull, contrib);
+            if (cm == 0u) continue;
+#pragma unroll
+            for (int c = 0; c < kAdj; ++c) ring[nring * kAdj + c][lane] = g[c];
+            if (lane == 0) ring_out[nring] = my_slot[e];
+            if (++nring == kRing) {
+                flush(kRing);
+                nring = 0;
+            }
+        }
+        __syncwarp();
+        buf ^= 1;
+    }
+    cp_async_wait<0>();
+    if (nring) flush(nring);
+}
+
 // ------------------------------------------------------------------ K10, hit bitmasks
 // One warp per 16x8 block, two per tile, four pixels per lane (columns c and
 // c + 8, rows r and r + 4), back to front from each pixel's stored last
@@ -405,7 +618,7 @@ __global__ void __launch_bounds__(32, kMinB)
             double v = (t0 + t1) + t2;
             if (c == 2 || c == 4) v *= -0.5;
             if (c == 3) v = -v;
-            const long long slot = s_ring_out[fe] * kVjpSlots + warp;
+            const long long slot = s_ring_out[fe] * 2 + warp;  // two 16x8 blocks per tile
             part[slot * kPartStride + c] = v;
             if (c == 0) mask[slot] = 1;
         }
@@ -655,14 +868,21 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     SGTR_CUDA(cudaGetLastError());
 }
 
+int vjp_slots(int n_tiles) { return n_tiles >= kWideVjpTiles ? 2 : 4; }
+
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
                             const int* last, double* part, unsigned char* mask) {
     const int n = tl.tiles_x * (tl.row1 - tl.row0);
     if (n == 0) return;
-    // 128 registers (16 one-warp CTAs per SM; the shared-memory limit is 17)
-    static_assert(kVjpSlots == 2, "K10 writes one partial per 16x8 block");
-    k_raster_vjp_wide<16><<<n * 2, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part, mask);
+    // 16x8 blocks (128 registers, 16 one-warp CTAs per SM) when the image has
+    // tiles enough to fill the GPU with them, else 8x8 blocks (twice the CTAs)
+    if (vjp_slots(n) == 2)
+        k_raster_vjp_wide<16><<<n * 2, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                     mask);
+    else
+        k_raster_vjp_bits<1><<<n * 4, 32, 0, st>>>(tl, rec, W, H, ro, adj, tfinal, last, part,
+                                                    mask);
     SGTR_CUDA(cudaGetLastError());
 }
 
