@@ -352,7 +352,7 @@ int sgtr_check_fast_exp(int64_t n, double lo, double hi, uint64_t seed,
  * without a host round trip and every view sorts `capacity` tile keys; a
  * training step in which some view outgrows it is rerun with the capacity
  * grown to fit (before any state changes), so this only presizes (or, for
- * tests, shrinks) it.  0 restores the default (4 K + 65536, grown on demand). */
+ * tests, shrinks) it.  0 restores the default (2 K + 4096, grown on demand). */
 int sgtr_set_dup_capacity(sgtr_ctx* ctx, int64_t capacity);
 
 /* ------------------------------------------------------------ multi-GPU */

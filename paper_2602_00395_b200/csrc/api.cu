@@ -642,7 +642,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.temp_bytes = c.temp.bytes;
     double* rec = c.rec.as<double>((size_t)kRec * (K + 1));
     b.rec = rec;
-    if (c.dup_cap == 0) c.dup_cap = 4LL * K + 65536;  // grown on demand
+    if (c.dup_cap == 0) c.dup_cap = 2LL * K + 4096;  // grown on demand (the tile sort runs on it)
 
     view_begin(c.st, &c.dstat->vs);
     {
