@@ -25,6 +25,7 @@
 // `alpha_bar < alpha_skip -> skip`, so a NaN alpha_bar is kept and
 // propagates as it does in the reference (render.cpp:136).
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "fastexp.cuh"
@@ -868,7 +869,18 @@ void launch_raster_fwd(cudaStream_t st, const TileLists& tl, const double* rec, 
     SGTR_CUDA(cudaGetLastError());
 }
 
-int vjp_slots(int n_tiles) { return n_tiles >= kWideVjpTiles ? 2 : 4; }
+// SGTR_VJP_BLOCK=16x8 / 8x8 forces the block shape (tests run the parity
+// suite on both; results agree to rounding, not bit for bit: the adjoints
+// are summed over different pixel groups)
+int vjp_slots(int n_tiles) {
+    static const int forced = [] {
+        const char* v = getenv("SGTR_VJP_BLOCK");
+        if (!v) return 0;
+        return std::string(v) == "16x8" ? 2 : std::string(v) == "8x8" ? 4 : 0;
+    }();
+    if (forced) return forced;
+    return n_tiles >= kWideVjpTiles ? 2 : 4;
+}
 
 void launch_raster_vjp_warp(cudaStream_t st, const TileLists& tl, const double* rec, int W,
                             int H, const RenderP& ro, const double* adj, const double* tfinal,
