@@ -86,9 +86,11 @@ def run_ranks(sp, ds, nranks, steps, batch, kind="3dgs2tr"):
     return out
 
 
-@pytest.mark.parametrize("nranks,batch", [(2, 4), (3, 4)])
+@pytest.mark.parametrize("nranks,batch", [(2, 4), (3, 4), (4, 4), (5, 4)])
 def test_n_ranks_match_one_rank(sp, ds, nranks, batch):
-    steps = 12  # refreshes at t = 1 and 11 (|S2| = 1 < ranks: row bands)
+    # refreshes at t = 1 and 11 (|S2| = 1 < ranks: row bands; at 4 and 5
+    # ranks some rank has no band, at 5 one also has no gradient view)
+    steps = 12
     one = run_ranks(sp, ds, 1, steps, batch)[0]
     many = run_ranks(sp, ds, nranks, steps, batch)
     for r, o in enumerate(many):
