@@ -43,7 +43,7 @@ def ds(orc):
                                               image_size=48, seed=5))
 
 
-def run_ranks(sp, ds, nranks, steps, batch, kind="3dgs2tr"):
+def run_ranks(sp, ds, nranks, steps, batch, kind="3dgs2tr", cap=None):
     views = [sp.Camera.from_c(c, g) for c, g in zip(ds.cams, ds.gts)]
     opt = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 40), batch_size=batch,
                               kind=kind, scene_extent=1.3, record_applied_step=False)
@@ -53,6 +53,8 @@ def run_ranks(sp, ds, nranks, steps, batch, kind="3dgs2tr"):
         c.set_scene(ds.init_x)
         c.set_views(views)
         c.state_reset(11)
+        if cap is not None:
+            c.set_dup_capacity(cap)
         ctxs.append(c)
     group = None
     if nranks > 1:
@@ -69,7 +71,8 @@ def run_ranks(sp, ds, nranks, steps, batch, kind="3dgs2tr"):
             out[r] = dict(g=g, d=d, t=t, x=ctxs[r].get_scene(),
                           loss=[dg.batch_loss for dg in diags],
                           refreshed=[dg.refreshed for dg in diags],
-                          local=[dg.n_local_views for dg in diags])
+                          local=[dg.n_local_views for dg in diags],
+                          reruns=[dg.reruns for dg in diags])
         except Exception as e:  # pragma: no cover - reported below
             errs.append(e)
 
@@ -104,6 +107,19 @@ def test_n_ranks_match_one_rank(sp, ds, nranks, batch):
     assert rel(m["d"], one["d"]) < 1e-11
     assert rel(m["x"], one["x"]) < 1e-8
     assert np.allclose(m["loss"], one["loss"], rtol=1e-12, atol=0)
+
+
+def test_capacity_reruns_are_collective(sp, ds):
+    """Every rank starts with a capacity its views outgrow: the overflow
+    count is part of the summed tail, so all ranks rerun the step together
+    and grow alike, and the result is the 1-rank run's."""
+    one = run_ranks(sp, ds, 1, 4, 4)[0]
+    many = run_ranks(sp, ds, 3, 4, 4, cap=16)
+    for o in many:
+        assert o["reruns"] == many[0]["reruns"] and o["reruns"][0] >= 1
+        assert np.array_equal(o["x"], many[0]["x"])
+    assert rel(many[0]["g"], one["g"]) < 1e-11
+    assert rel(many[0]["x"], one["x"]) < 1e-8
 
 
 def test_adam_tr_two_ranks(sp, ds):
