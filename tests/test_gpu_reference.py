@@ -155,3 +155,31 @@ def test_steps_match_reference(sp, ref, kind):
     gr, hr, _ = rst.get()
     if kind == "3dgs2tr":
         assert rel(g, gr) < GRAD_TOL and rel(d, hr) < IMG_TOL
+
+
+@pytest.mark.parametrize("opts", [
+    dict(background=(0.2, 0.3, 0.4)),
+    dict(background=(0.9, 0.1, 0.5), alpha_clamp=0.9, t_stop=1e-3, lowpass=0.5,
+         cutoff_sigma=2.5, alpha_skip=0.01),
+])
+def test_render_options_match_reference(sp, ref, c1, opts):
+    """Non-default RenderOptions (render.hpp:12-22): a background colour (the
+    VJP's behind-colour term and the JVP's bg * dT), a lower alpha clamp, an
+    earlier transmittance stop, a wider low-pass, a tighter cut-off and a
+    higher skip threshold -- forward, JVP and VJP against the reference."""
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal(c1.init_x.size)
+    adj = rng.standard_normal((128, 128, 3))
+    ro_sp = sp.RenderOptions(**opts)
+    ro_ref = ref.RenderOptions(**opts)
+    for which in (c1.init_x, c1.gt_x):
+        scene = sp.Scene(which)
+        for oc in c1.cams[:2]:
+            cam = sp.Camera.from_c(oc)
+            out = sp.rasterize(scene, cam, ro_sp)
+            color, t = ref.rasterize(which, oc, ro_ref)
+            assert rel(out.color, color) < 1e-12 and rel(out.t_final, t) < 1e-12
+            assert rel(sp.rasterize_jvp(scene, cam, v, ro_sp),
+                       ref.rasterize_jvp(which, oc, v, ro_ref)) < IMG_TOL
+            assert rel(sp.rasterize_vjp(scene, cam, adj, ro_sp),
+                       ref.rasterize_vjp(which, oc, adj, ro_ref)) < GRAD_TOL
