@@ -183,3 +183,22 @@ def test_render_options_match_reference(sp, ref, c1, opts):
                        ref.rasterize_jvp(which, oc, v, ro_ref)) < IMG_TOL
             assert rel(sp.rasterize_vjp(scene, cam, adj, ro_sp),
                        ref.rasterize_vjp(which, oc, adj, ro_ref)) < GRAD_TOL
+
+
+@pytest.mark.parametrize("lam,floor", [(0.0, 1e-12), (1.0, 1e-12), (0.5, 1e-6)])
+def test_residual_options_match_reference(sp, ref, c1, lam, floor):
+    """Non-default ResidualOptions (residuals.hpp:13-16): pure L1 (lambda 0),
+    pure D-SSIM (lambda 1) and a mixed weight with a large floor (more
+    residuals masked) -- the stochastic gradient and the Hutchinson diagonal
+    against the reference."""
+    views = [sp.Camera.from_c(c, g) for c, g in zip(c1.cams, c1.gts)]
+    scene = sp.Scene(c1.init_x)
+    ro = sp.ResidualOptions(lambda_=lam, floor=floor)
+    rr = ref.ResidualOptions(lambda_=lam, floor=floor)
+    g, loss = sp.stochastic_gradient(scene, views, [1, 3], ro)
+    gr, lr = ref.stochastic_gradient(c1.init_x, c1.cams, c1.gts, [1, 3], rr)
+    assert rel(g, gr) < GRAD_TOL and loss == pytest.approx(lr, rel=1e-10)
+    z = ref.Rng(7).rademacher(c1.init_x.size)
+    d = sp.hutchinson_diag(scene, views, [2], 1, lambda s: z, ro)
+    dr = ref.hutchinson_diag(c1.init_x, c1.cams, c1.gts, [2], z, rr)
+    assert rel(d, dr) < IMG_TOL
