@@ -202,3 +202,43 @@ def test_residual_options_match_reference(sp, ref, c1, lam, floor):
     d = sp.hutchinson_diag(scene, views, [2], 1, lambda s: z, ro)
     dr = ref.hutchinson_diag(c1.init_x, c1.cams, c1.gts, [2], z, rr)
     assert rel(d, dr) < IMG_TOL
+
+
+def test_step_options_match_reference(sp, ref):
+    """3DGS2-TR steps under non-default optimizer options (optimizer.hpp:37-53,
+    trust_region.hpp:66-72, scene.hpp:29-35): a refresh every 3rd step with
+    nu = 2 probes over |S2| = 2 views, |S1| = 3, different EMA weights and
+    damping, tight radius caps and parameter bounds, a non-default residual
+    weight and render options -- against the reference drawing from the same
+    seeded Rng."""
+    ds = ref.make_synthetic(ref.SynthConfig(gt_splats=300, init_splats=300, views=6,
+                                            image_size=48, seed=8))
+    views = [sp.Camera.from_c(c, g) for c, g in zip(ds.cams, ds.gts)]
+    caps = (0.05, 0.02, 0.3, 0.1, 0.2)
+    bounds = (1e-3, 0.02, 0.98, 0.01, 1.2)
+    lam, floor = 0.35, 1e-10
+    render = dict(background=(0.1, 0.2, 0.3), alpha_clamp=0.95, t_stop=1e-3)
+    opts = sp.OptimizerOptions(theta1=0.8, theta2=0.99, hess_interval=3, hutch_samples=2,
+                               batch_size=3, hutch_batch_size=2, gamma_d=1e-9,
+                               schedule=sp.TrustRegionSchedule(1e-5, 1e-7, 15),
+                               caps=sp.RadiusCaps(*caps), bounds=sp.ParamBounds(*bounds),
+                               residual=sp.ResidualOptions(lambda_=lam, floor=floor),
+                               render=sp.RenderOptions(**render))
+    ropts = ref.TrOptions(theta1=0.8, theta2=0.99, hess_interval=3, hutch_samples=2,
+                          batch_size=3, hutch_batch_size=2, gamma_d=1e-9, eps_start=1e-5,
+                          eps_end=1e-7, total_steps=15, caps=caps, bounds=bounds)
+    rr = ref.ResidualOptions(lambda_=lam, floor=floor)
+    ro = ref.RenderOptions(**render)
+    st = sp.OptimizerState(ds.init_x.size, 9)
+    scene = sp.Scene(ds.init_x)
+    rst = ref.State(ds.init_x.size, 9)
+    xr = ds.init_x.copy()
+    for t in range(1, 8):  # refreshes at t = 1, 4, 7
+        dg = sp.step_3dgs2tr(st, scene, views, opts)
+        dr = ref.step_3dgs2tr(rst, xr, ds.cams, ds.gts, ropts, rr, ro)
+        assert dg.batch_loss == pytest.approx(dr["batch_loss"], rel=1e-8)
+        assert dg.eps == dr["eps"] and bool(dg.refreshed) == (t % 3 == 1)
+        assert rel(scene.x, xr) < 1e-6
+    g, d, _ = st.ctx.state_get()
+    gr, hr, _ = rst.get()
+    assert rel(g, gr) < GRAD_TOL and rel(d, hr) < IMG_TOL
