@@ -242,3 +242,30 @@ def test_step_options_match_reference(sp, ref):
     g, d, _ = st.ctx.state_get()
     gr, hr, _ = rst.get()
     assert rel(g, gr) < GRAD_TOL and rel(d, hr) < IMG_TOL
+
+
+@pytest.mark.parametrize("kind", ["adam", "adam-tr"])
+def test_adam_options_match_reference(sp, ref, kind):
+    """ADAM / ADAM-TR (optimizer.cpp:153-253) under non-default AdamOptions:
+    other betas and epsilon, per-group rates, and a position rate that decays
+    to its final value within the run (lr_position_decay_steps 4)."""
+    ds = ref.make_synthetic(ref.SynthConfig(gt_splats=300, init_splats=300, views=6,
+                                            image_size=48, seed=3))
+    views = [sp.Camera.from_c(c, g) for c, g in zip(ds.cams, ds.gts)]
+    ad = dict(beta1=0.8, beta2=0.99, eps=1e-12, lr_position=1e-3, lr_position_final=1e-5,
+              lr_position_decay_steps=4, lr_scale=2e-3, lr_rotation=3e-3, lr_opacity=1e-2,
+              lr_color=4e-3)
+    opts = sp.OptimizerOptions(kind=kind, batch_size=2, scene_extent=2.5,
+                               schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 10),
+                               adam=sp.AdamOptions(**ad))
+    ropts = ref.TrOptions(batch_size=2, total_steps=10)
+    st = sp.OptimizerState(ds.init_x.size, 4)
+    scene = sp.Scene(ds.init_x)
+    rst = ref.State(ds.init_x.size, 4)
+    xr = ds.init_x.copy()
+    for t in range(1, 7):
+        dg = sp.optimizer_step(st, scene, views, opts)
+        dr = ref.step_adam(rst, xr, ds.cams, ds.gts, ropts,
+                           ref.AdamOptions(scene_extent=2.5, **ad), kind == "adam-tr")
+        assert dg.batch_loss == pytest.approx(dr["batch_loss"], rel=1e-8)
+        assert rel(scene.x, xr) < IMG_TOL
