@@ -604,6 +604,13 @@ def main():
                     "work": f"{flops_per[dom]:.4g} FP64 flops/launch = 32 E + k C with "
                             f"E={E:.4g} evaluated, C={Cc:.4g} contributing (pixel, fragment) "
                             f"pairs per view"}
+        # the same figure for each rasteriser (K7 forward, K10 VJP, K12 JVP on
+        # refresh views), so the forward pass's fraction is on the line too
+        roofline["rasterisers"] = {
+            n: {"ms_per_launch": ktimes[n][1] / ktimes[n][0],
+                "achieved": flops_per[n] / (ktimes[n][1] / ktimes[n][0] * 1e-3) / 1e12,
+                "frac": flops_per[n] / (ktimes[n][1] / ktimes[n][0] * 1e-3) / 1e12 / fp64_peak}
+            for n in flops_per if ktimes.get(n, [0])[0]}
     else:
         dim = npp_of(sh) * k
         bytes_per = {"tr_update": 56 * dim, "depth_sort_scan": 24 * k * 8}.get(dom, 0)
