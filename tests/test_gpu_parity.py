@@ -785,3 +785,25 @@ def test_binning_and_render_large_rectangles(sp, orc):
     assert rel(out.color, img) < IMG_TOL and rel(out.t_final, t) < IMG_TOL
     u = rng.normal(size=img.shape)
     assert rel(sp.rasterize_vjp(sp.Scene(x), cam, u), orc.rasterize_vjp(x, oc, u)) < GRAD_TOL
+
+
+def test_wide_vjp_odd_frame(sp, orc, c1):
+    """K10's 16x8-block path (frames of >= 4096 tiles) on a frame whose
+    sides are not tile multiples (1030 x 1027: a partial tile column and row,
+    the lower 16x8 block of the last tile row cut to 3 rows): VJP and the
+    stochastic gradient against the oracle restatement."""
+    W, H = 1030, 1027
+    oc = type(c1.cams[0]).from_buffer_copy(c1.cams[0])
+    s = W / oc.width
+    oc.width, oc.height = W, H
+    oc.fx, oc.fy = oc.fx * s, oc.fy * s
+    oc.cx, oc.cy = W / 2.0, H / 2.0
+    gt, _ = orc.rasterize(c1.gt_x, oc)
+    scene = sp.Scene(c1.init_x)
+    cam = sp.Camera.from_c(oc, gt)
+    adj = np.random.default_rng(8).standard_normal((H, W, 3))
+    assert rel(sp.rasterize_vjp(scene, cam, adj),
+               orc.rasterize_vjp(c1.init_x, oc, adj)) < GRAD_TOL
+    g, loss = sp.stochastic_gradient(scene, [cam], [0])
+    go, lo = orc.stochastic_gradient(c1.init_x, [oc], [gt], [0])
+    assert rel(g, go) < GRAD_TOL and loss == pytest.approx(lo, rel=1e-10)

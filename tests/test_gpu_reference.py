@@ -269,3 +269,33 @@ def test_adam_options_match_reference(sp, ref, kind):
                            ref.AdamOptions(scene_extent=2.5, **ad), kind == "adam-tr")
         assert dg.batch_loss == pytest.approx(dr["batch_loss"], rel=1e-8)
         assert rel(scene.x, xr) < IMG_TOL
+
+
+@pytest.mark.parametrize("W,H", [(53, 37), (17, 100), (200, 11)])
+def test_odd_sizes_match_reference(sp, ref, c1, W, H):
+    """Frames whose sides are not multiples of the 16-px tile, W != H, one
+    side under a tile (partial tiles in K7/K10/K12, SSIM reflection on both
+    borders of a short side): render, JVP, VJP, the stochastic gradient and
+    the Hutchinson diagonal against the reference."""
+    rng = np.random.default_rng(W * 1000 + H)
+    oc = type(c1.cams[0]).from_buffer_copy(c1.cams[0])
+    oc.width, oc.height = W, H
+    oc.cx, oc.cy = W / 2.0, H / 2.0
+    gt, _ = ref.rasterize(c1.gt_x, oc)
+    scene = sp.Scene(c1.init_x)
+    cam = sp.Camera.from_c(oc, gt)
+    out = sp.rasterize(scene, cam)
+    color, t = ref.rasterize(c1.init_x, oc)
+    assert rel(out.color, color) < 1e-12 and rel(out.t_final, t) < 1e-12
+    v = rng.standard_normal(c1.init_x.size)
+    adj = rng.standard_normal((H, W, 3))
+    assert rel(sp.rasterize_jvp(scene, cam, v), ref.rasterize_jvp(c1.init_x, oc, v)) < IMG_TOL
+    assert rel(sp.rasterize_vjp(scene, cam, adj),
+               ref.rasterize_vjp(c1.init_x, oc, adj)) < GRAD_TOL
+    g, loss = sp.stochastic_gradient(scene, [cam], [0])
+    gr, lr = ref.stochastic_gradient(c1.init_x, [oc], [gt], [0])
+    assert rel(g, gr) < GRAD_TOL and loss == pytest.approx(lr, rel=1e-10)
+    z = ref.Rng(W + H).rademacher(c1.init_x.size)
+    d = sp.hutchinson_diag(scene, [cam], [0], 1, lambda s: z)
+    dr = ref.hutchinson_diag(c1.init_x, [oc], [gt], [0], z)
+    assert rel(d, dr) < IMG_TOL
