@@ -299,3 +299,25 @@ def test_odd_sizes_match_reference(sp, ref, c1, W, H):
     d = sp.hutchinson_diag(scene, [cam], [0], 1, lambda s: z)
     dr = ref.hutchinson_diag(c1.init_x, [oc], [gt], [0], z)
     assert rel(d, dr) < IMG_TOL
+
+
+def test_view_that_sees_nothing_matches_reference(sp, ref, c1):
+    """A camera moved far off to the side (no splat in its frustum): the
+    background image, a zero gradient from that view and an unchanged loss
+    term on both sides; a batch mixing it with a normal view matches too."""
+    oc = type(c1.cams[0]).from_buffer_copy(c1.cams[0])
+    oc.t_wc[0] += 1e4
+    gt = np.full((oc.height, oc.width, 3), 0.3)
+    scene = sp.Scene(c1.init_x)
+    cam = sp.Camera.from_c(oc, gt)
+    out = sp.rasterize(scene, cam)
+    color, t = ref.rasterize(c1.init_x, oc)
+    assert np.array_equal(out.color, color) and np.array_equal(out.t_final, t)
+    assert np.all(t == 1.0)
+    g, loss = sp.stochastic_gradient(scene, [cam], [0])
+    gr, lr = ref.stochastic_gradient(c1.init_x, [oc], [gt], [0])
+    assert not np.any(g) and not np.any(gr) and loss == pytest.approx(lr, rel=1e-12)
+    views = [cam, sp.Camera.from_c(c1.cams[1], c1.gts[1])]
+    g2, l2 = sp.stochastic_gradient(scene, views, [1, 0])
+    gr2, lr2 = ref.stochastic_gradient(c1.init_x, [oc, c1.cams[1]], [gt, c1.gts[1]], [1, 0])
+    assert rel(g2, gr2) < GRAD_TOL and l2 == pytest.approx(lr2, rel=1e-10)
