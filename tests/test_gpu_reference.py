@@ -321,3 +321,56 @@ def test_view_that_sees_nothing_matches_reference(sp, ref, c1):
     g2, l2 = sp.stochastic_gradient(scene, views, [1, 0])
     gr2, lr2 = ref.stochastic_gradient(c1.init_x, [oc, c1.cams[1]], [gt, c1.gts[1]], [1, 0])
     assert rel(g2, gr2) < GRAD_TOL and l2 == pytest.approx(lr2, rel=1e-10)
+
+
+def _extreme_scene(c1, seed=21, W=200, H=200, K=1500):
+    """A sparse C1-derived scene with extreme splats (see the test)."""
+    oc = type(c1.cams[0]).from_buffer_copy(c1.cams[0])
+    sc = W / oc.width
+    oc.width, oc.height = W, H
+    oc.fx, oc.fy = oc.fx * sc, oc.fy * sc
+    oc.cx, oc.cy = W / 2.0, H / 2.0
+    X = c1.init_x
+    K0 = X.size // 14
+    rng = np.random.default_rng(seed)
+    sel = rng.choice(K0, K, replace=False)
+    mu = X[:3 * K0].reshape(K0, 3)[sel].copy()
+    s = 0.3 * X[3 * K0:6 * K0].reshape(K0, 3)[sel]
+    q = X[6 * K0:10 * K0].reshape(K0, 4)[sel].copy()
+    a = X[10 * K0:11 * K0][sel].copy()
+    col = X[11 * K0:].reshape(K0, 3)[sel].copy()
+    C = np.array(list(oc.t_wc))
+    idx = rng.permutation(K)
+    tiny, huge, op, behind, near = (idx[:100], idx[100:104], idx[104:204], idx[204:254],
+                                    idx[254:304])
+    s[tiny] = 1e-4
+    s[huge] = rng.uniform(0.3, 0.8, (len(huge), 3))
+    a[huge] = 0.05
+    a[op] = rng.choice([0.0, 1e-9, 0.999999, 1.0], len(op))
+    mu[behind] = C + (C - mu[behind])
+    mu[near] = C + (mu[near] - C) * rng.uniform(0.001, 0.02, (len(near), 1))
+    a[near] = 0.02
+    return np.concatenate([mu.ravel(), s.ravel(), q.ravel(), a, col.ravel()]), oc
+
+
+def test_extreme_scene_matches_reference(sp, ref, c1):
+    """A sparse C1-derived 200x200 scene with splats behind the camera and
+    straddling the near plane, sub-pixel splats (the low-pass dominates),
+    splats wider than 64 tiles (the queued emission path) and opacities 0,
+    1e-9, 1 - 1e-6 and 1: render, JVP, VJP and the gradient against the
+    reference."""
+    x, oc = _extreme_scene(c1)
+    gt, _ = ref.rasterize(c1.gt_x, oc)
+    rng = np.random.default_rng(22)
+    scene = sp.Scene(x)
+    cam = sp.Camera.from_c(oc, gt)
+    out = sp.rasterize(scene, cam)
+    color, t = ref.rasterize(x, oc)
+    assert rel(out.color, color) < 1e-12 and rel(out.t_final, t) < 1e-12
+    v = rng.standard_normal(x.size)
+    adj = rng.standard_normal(color.shape)
+    assert rel(sp.rasterize_jvp(scene, cam, v), ref.rasterize_jvp(x, oc, v)) < IMG_TOL
+    assert rel(sp.rasterize_vjp(scene, cam, adj), ref.rasterize_vjp(x, oc, adj)) < GRAD_TOL
+    g, loss = sp.stochastic_gradient(scene, [cam], [0])
+    gr, lr = ref.stochastic_gradient(x, [oc], [gt], [0])
+    assert rel(g, gr) < GRAD_TOL and loss == pytest.approx(lr, rel=1e-10)
