@@ -374,3 +374,33 @@ def test_extreme_scene_matches_reference(sp, ref, c1):
     g, loss = sp.stochastic_gradient(scene, [cam], [0])
     gr, lr = ref.stochastic_gradient(x, [oc], [gt], [0])
     assert rel(g, gr) < GRAD_TOL and loss == pytest.approx(lr, rel=1e-10)
+
+
+def test_extreme_scene_steps_match_reference(sp, ref, c1):
+    """Six 3DGS²-TR steps on the extreme scene (opacities at the clamp
+    bounds, sub-pixel scales, culled splats whose rows stay zero) with the
+    Hessian refresh at step 1, both sides drawing from the same seeded Rng."""
+    x, oc0 = _extreme_scene(c1)
+    cams = [oc0]
+    for c in c1.cams[1:3]:
+        oc = type(c).from_buffer_copy(c)
+        sc = oc0.width / oc.width
+        oc.width, oc.height = oc0.width, oc0.height
+        oc.fx, oc.fy = oc.fx * sc, oc.fy * sc
+        oc.cx, oc.cy = oc0.cx, oc0.cy
+        cams.append(oc)
+    gts = [ref.rasterize(c1.gt_x, c)[0] for c in cams]
+    views = [sp.Camera.from_c(c, g) for c, g in zip(cams, gts)]
+    st = sp.OptimizerState(x.size, 7)
+    scene = sp.Scene(x)
+    rst = ref.State(x.size, 7)
+    xr = x.copy()
+    opts = sp.OptimizerOptions(schedule=sp.TrustRegionSchedule(1e-6, 1e-8, 6), batch_size=2,
+                               scene_extent=1.3)
+    ropts = ref.TrOptions(total_steps=6, batch_size=2)
+    for t in range(1, 7):
+        dg = sp.optimizer_step(st, scene, views, opts)
+        dr = ref.step_3dgs2tr(rst, xr, cams, gts, ropts)
+        assert dg.batch_loss == pytest.approx(dr["batch_loss"], rel=1e-8)
+        assert dg.eps == dr["eps"]
+        assert rel(scene.x, xr) < 1e-6
