@@ -456,7 +456,7 @@ struct Ctx {
     Buf rec, trec, keys, keys_alt, keys32, keys32_alt, ids, ids_alt, rect, tcount, off_r;
     Buf tkeys, tkeys_alt, dval, dval_alt, dup_id, tile_start, tile_end, temp;
     Buf img, tfin, last, adj, tan, adjl1, Pf, Qf, Rf, partials, zbits, seam0, seam1, seam2;
-    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tmask, large, trect, off_id, ovals;
+    Buf dxbuf, etabuf, queue, tile_ids, inv, part, mask, tinfo, large, trect, off_id, ovals;
     DevStatus* dstat = nullptr;
     DevStatus* hstat = nullptr;  // pinned
     // further view lanes (stream + per-view workspace), swapped in by
@@ -472,7 +472,7 @@ struct Ctx {
     X(off_r) X(tkeys)                                                                        \
     X(tkeys_alt) X(dval) X(dval_alt) X(dup_id) X(tile_start) X(tile_end) X(temp)             \
     X(img) X(tfin) X(last) X(adj) X(adjl1) X(Pf) X(Qf) X(Rf) X(partials) X(tile_ids) X(inv) \
-    X(part) X(mask) X(tmask) X(large) X(trect) X(off_id) X(ovals)
+    X(part) X(mask) X(tinfo) X(large) X(trect) X(off_id) X(ovals)
 #define SGTR_DECL(n) Buf n;
         SGTR_LANE_BUFS(SGTR_DECL)
 #undef SGTR_DECL
@@ -631,7 +631,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     b.ids_alt = c.ids_alt.as<int>(K + 1);
     b.rect = c.rect.as<int4>(K + 1);
     b.tcount = c.tcount.as<int>(K + 1);
-    b.tmask = c.tmask.as<unsigned long long>(K + 1);
+    b.tinfo = c.tinfo.as<int4>(K + 1);
     b.large = c.large.as<int>(K + 1);
     b.n_large = &c.dstat->n_large;
     b.off_r = c.off_r.as<long long>(K + 1);
@@ -648,7 +648,7 @@ ViewRender render_view(Ctx& c, const DevCam& dc, const RenderP& ro, bool throw_e
     {
         Timed t(c, KC_PROJECT);
         launch_project(c.st, c.X(), K, c.nb, dc, ro, rec, b.keys, b.keys32, b.ids, b.rect,
-                       b.tcount, b.tmask, &c.dstat->vs);
+                       b.tcount, b.tinfo, &c.dstat->vs);
     }
     {
         Timed t(c, KC_DEPTH_SORT);

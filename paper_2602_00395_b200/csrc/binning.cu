@@ -74,9 +74,7 @@ CountIter count_iter(const int* ids, const int* tcount, int K) {
 // with no tiles).  Rectangles of <= 64 tiles are emitted from the hit bits K1
 // recorded, in row-major tile order; larger ones are queued for K4b.
 __global__ void __launch_bounds__(256) k_emit_small(const int* __restrict__ sorted_ids,
-                                                    const int* __restrict__ tcount,
-                                                    const int4* __restrict__ rect,
-                                                    const unsigned long long* __restrict__ tmask,
+                                                    const int4* __restrict__ tinfo,
                                                     const long long* __restrict__ off_r,
                                                     int n_visible, int tiles_x, long long cap,
                                                     long long* __restrict__ off_id,
@@ -88,17 +86,20 @@ __global__ void __launch_bounds__(256) k_emit_small(const int* __restrict__ sort
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_visible) return;
     const int id = sorted_ids[r];
-    off_id[id] = off_r[r];  // K11 finds a splat's partials by id
-    if (off_r[n_visible] > cap || tcount[id] == 0) return;
-    const int4 pr = rect[id];
-    const int tx0 = pr.x / kTile, ty0 = pr.y / kTile;
-    const int w = pr.z / kTile - tx0 + 1, h = pr.w / kTile - ty0 + 1;
+    long long d = off_r[r];
+    off_id[id] = d;  // K11 finds a splat's partials by id
+    // the splat's tile count is the scan's step (read in rank order); its
+    // rectangle and hit bits are one 16-byte gather by id (at C5 the
+    // per-splat arrays are DRAM-resident, so one sector instead of three)
+    if (off_r[n_visible] > cap || off_r[r + 1] == d) return;
+    const int4 ti = tinfo[id];
+    const int tx0 = ti.x & 0xffff, ty0 = (unsigned)ti.x >> 16;
+    const int w = ti.y & 0xffff, h = (unsigned)ti.y >> 16;
     if (w * h > 64) {
         large[atomicAdd(n_large, 1)] = r;
         return;
     }
-    unsigned long long bits = tmask[id];
-    long long d = off_r[r];
+    unsigned long long bits = ((unsigned long long)(unsigned)ti.w << 32) | (unsigned)ti.z;
     while (bits) {
         const int j = __ffsll((long long)bits) - 1;
         bits &= bits - 1ull;
@@ -303,7 +304,7 @@ void bin_tiles(cudaStream_t st, BinBuffers& b, int K, int tiles_x, int n_tiles, 
     if (K == 0 || n_tiles == 0) return;
     const unsigned int sentinel = (unsigned int)n_tiles;
     SGTR_CUDA(cudaMemsetAsync(b.n_large, 0, sizeof(int), st));
-    k_emit_small<<<ceil_div(K, 256), 256, 0, st>>>(b.ids_alt, b.tcount, b.rect, b.tmask, b.off_r, K,
+    k_emit_small<<<ceil_div(K, 256), 256, 0, st>>>(b.ids_alt, b.tinfo, b.off_r, K,
                                                    tiles_x, cap, b.off_id, b.tkeys, b.dval,
                                                    b.dup_id, b.large, b.n_large);
     SGTR_CUDA(cudaGetLastError());

@@ -12,12 +12,14 @@ namespace sgtr {
 // ---------------------------------------------------------------- project.cu
 // K1: per-splat projection -> 128-byte fragment record, order-preserving
 // 64-bit depth key (culled = ~0), tile rectangle and tile count.
-// tmask: per splat, the hit bits of its tile rectangle in row-major order
-// (rectangles of <= 64 tiles)
+// tinfo: per splat, what K4 needs in one 16-byte gather: the tile rectangle
+// (x: tx0 | ty0 << 16, y: width | height << 16, in tiles) and the hit bits of
+// its tiles in row-major order (z, w: low and high words; rectangles of <= 64
+// tiles)
 void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys,
                     unsigned int* keys32, int* ids, int4* rect, int* tcount,
-                    unsigned long long* tmask, ViewStatus* status);
+                    int4* tinfo, ViewStatus* status);
 // parity dump: 12 doubles per splat (culled, depth, px, py, bx0..by1, i00..i11, 0)
 void launch_project_dump(cudaStream_t st, const double* x, int K, const DevCam& cam,
                          const RenderP& ro, double* out);
@@ -35,7 +37,7 @@ struct BinBuffers {
     int4* rect;            // bbox pixel range (x0, y0, x1, y1) per splat
     const double* rec;     // fragment records (K1)
     int* tcount;
-    unsigned long long* tmask;  // tile-hit bits per splat (rects <= 64 tiles)
+    int4* tinfo;           // tile rectangle + hit bits per splat (K1 -> K4)
     int* large;            // depth ranks of splats with > 64-tile rectangles
     int* n_large;
     long long* off_r;      // K+1 exclusive duplicate offsets in depth-rank order

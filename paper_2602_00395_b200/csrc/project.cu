@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
                                                  unsigned int* __restrict__ keys32,
                                                  int* __restrict__ ids, int4* __restrict__ rect,
                                                  int* __restrict__ tcount,
-                                                 unsigned long long* __restrict__ tmask,
+                                                 int4* __restrict__ tinfo,
                                                  ViewStatus* status) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     bool visible = false;
@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(256) k_project(const double* __restrict__ x, i
                         if (hit && j < 64) bits |= 1ull << j;
                     }
                 tcount[i] = n;
-                tmask[i] = bits;
+                const int tx0 = x0 / kTile, ty0 = y0 / kTile;
+                tinfo[i] = make_int4(tx0 | (ty0 << 16),
+                                     (x1 / kTile - tx0 + 1) | ((y1 / kTile - ty0 + 1) << 16),
+                                     (int)(unsigned)bits, (int)(unsigned)(bits >> 32));
             }
         }
     }
@@ -370,14 +373,14 @@ __global__ void __launch_bounds__(128, 5) k_chain_warp(int mode, const double* _
 void launch_project(cudaStream_t st, const double* x, int K, int nb, const DevCam& cam,
                     const RenderP& ro, double* rec, unsigned long long* keys,
                     unsigned int* keys32, int* ids, int4* rect, int* tcount,
-                    unsigned long long* tmask, ViewStatus* status) {
+                    int4* tinfo, ViewStatus* status) {
     if (K == 0) return;
     if (nb)
         k_project<true><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, keys32,
-                                                          ids, rect, tcount, tmask, status);
+                                                          ids, rect, tcount, tinfo, status);
     else
         k_project<false><<<ceil_div(K, 256), 256, 0, st>>>(x, K, nb, cam, ro, rec, keys, keys32,
-                                                           ids, rect, tcount, tmask, status);
+                                                           ids, rect, tcount, tinfo, status);
     SGTR_CUDA(cudaGetLastError());
 }
 
